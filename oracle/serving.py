@@ -1,0 +1,202 @@
+"""Query splitting, fusion, virtual-clock serving replay and the SLA metric.
+
+TEST INFRASTRUCTURE (see oracle/__init__.py).
+
+PAPER.md:263-265 — "each large inference query is split into multiple
+sub-queries and the query dispatcher distributes sub-queries to the parallel
+inference threads.  On accelerators, the inference queries are fused into one
+large batch ... referred to as query fusion."  PAPER.md:258-261 — model
+co-location: m concurrent inference threads on one accelerator (here m CUDA
+streams).  PAPER.md:269 — "maximize the throughput while satisfying the strict
+SLA latency target" (latency-bounded throughput).
+
+  S1 split(n, d)       chunks of d, remainder last                       (reading R14)
+  S2 fuse              FIFO head while cumulative <= d, at least one; fire when a
+                       stream is idle (work-conserving), or with timeout tau>0 only
+                       when the batch is full or the oldest waited tau   (R15)
+  S3 dispatch          idle stream with the lowest id
+  S4 virtual clock     service = (alpha_ns + beta_ns*items)*1e-9 s; at equal times
+                       arrivals, then completions, then dispatch decisions
+  S5 metric            p95 nearest rank over post-warm-up queries; lambda* by
+                       geometric bracketing + bisection
+"""
+from __future__ import annotations
+
+import heapq
+from dataclasses import dataclass, field
+from typing import Callable, List, Tuple
+
+import numpy as np
+
+
+def split(n: int, d: int) -> List[Tuple[int, int]]:
+    """S1: [(start, len)...] with k = ceil(n/d) chunks; all of length d but the last."""
+    if n <= 0 or d <= 0:
+        raise ValueError("split needs n > 0 and d > 0")
+    k = -(-n // d)
+    return [(c * d, d if c < k - 1 else n - (k - 1) * d) for c in range(k)]
+
+
+def fuse_head(fifo_lens: List[int], d: int) -> int:
+    """S2: number of head sub-queries taken: cumulative length <= d, at least one."""
+    tot, k = 0, 0
+    for ln in fifo_lens:
+        if k > 0 and tot + ln > d:
+            break
+        tot += ln
+        k += 1
+    return k
+
+
+def p_nearest_rank(lat: np.ndarray, pct: int = 95) -> float:
+    """Nearest-rank percentile: sorted value at 1-based rank ceil(pct*n/100) (reading R11)."""
+    lat = np.sort(np.asarray(lat, dtype=np.float64))
+    n = lat.size
+    if n == 0:
+        return float("nan")
+    rank = (pct * n + 99) // 100
+    return float(lat[max(rank, 1) - 1])
+
+
+@dataclass
+class Replay:
+    batches: List[dict] = field(default_factory=list)     # dispatch order
+    latency_s: np.ndarray = None                           # per query (trace order)
+    completion_s: np.ndarray = None
+
+
+def replay_virtual(trace: np.ndarray, streams: int, max_batch: int, alpha_ns: float,
+                   beta_ns: float, fusion_timeout_ms: float = 0.0) -> Replay:
+    """S1-S4 on a virtual clock.  Returns the unique batch list and per-query latencies.
+
+    trace: structured array with fields arrival_s (sorted ascending), size, qid.
+    """
+    if streams < 1 or max_batch < 1:
+        raise ValueError("infeasible policy")
+    n = len(trace)
+    arr = trace["arrival_s"].astype(np.float64)
+    size = trace["size"].astype(np.int64)
+    qid = trace["qid"].astype(np.int64)
+    tau = fusion_timeout_ms * 1e-3
+    fifo: List[Tuple[int, int, int, float, int]] = []      # (qid, start, len, arrival, trace_pos)
+    head = 0
+    idle = list(range(streams))                            # sorted ids
+    busy: List[Tuple[float, int, int]] = []                # heap (completion, stream, batch_id)
+    remaining = np.array([len(split(int(s), max_batch)) for s in size], dtype=np.int64)
+    done_t = np.full(n, np.nan)
+    out = Replay()
+    batch_members: List[List[int]] = []
+    now = arr[0] if n else 0.0
+    a = 0
+    while True:
+        # 1. arrivals at or before now
+        while a < n and arr[a] <= now:
+            for (s, ln) in split(int(size[a]), max_batch):
+                fifo.append((int(qid[a]), s, ln, float(arr[a]), a))
+            a += 1
+        # 2. completions at or before now
+        while busy and busy[0][0] <= now:
+            t_c, st, bid = heapq.heappop(busy)
+            for pos in batch_members[bid]:
+                remaining[pos] -= 1
+                if remaining[pos] == 0:
+                    done_t[pos] = t_c
+            idle.append(st)
+            idle.sort()
+        # 3. dispatch decisions
+        while idle and head < len(fifo):
+            lens = [f[2] for f in fifo[head:head + max_batch + 1]]
+            k = fuse_head(lens, max_batch)
+            items = sum(lens[:k])
+            full = items == max_batch or (head + k < len(fifo))
+            if tau > 0 and not full and not (now >= fifo[head][3] + tau):
+                break
+            st = idle.pop(0)
+            segs = fifo[head:head + k]
+            head += k
+            bid = len(out.batches)
+            t_done = now + (alpha_ns + beta_ns * items) * 1e-9
+            out.batches.append(dict(stream=st, t_dispatch=now, t_done=t_done,
+                                    segs=[(s[0], s[1], s[2]) for s in segs]))
+            batch_members.append([s[4] for s in segs])
+            heapq.heappush(busy, (t_done, st, bid))
+        # 4. next event
+        cands = []
+        if a < n:
+            cands.append(arr[a])
+        if busy:
+            cands.append(busy[0][0])
+        if tau > 0 and head < len(fifo) and idle:
+            cands.append(fifo[head][3] + tau)
+        if not cands:
+            break
+        nxt = min(cands)
+        if not nxt > now:
+            raise RuntimeError("virtual clock made no progress")
+        now = nxt
+    out.completion_s = done_t
+    out.latency_s = done_t - arr
+    return out
+
+
+STABILITY_BAND = 0.98
+
+
+def summarize(trace: np.ndarray, latency_s: np.ndarray, completion_s: np.ndarray,
+              sla_ms: float, warmup_frac: float = 0.1) -> dict:
+    """S5 report: p50/p95/p99 (nearest rank) over queries arriving after warm-up."""
+    arr = trace["arrival_s"].astype(np.float64)
+    t0, t1 = arr[0], arr[-1]
+    w_end = t0 + warmup_frac * (t1 - t0)
+    sel = arr >= w_end
+    lat_ms = latency_s[sel] * 1e3
+    complete = bool(np.all(np.isfinite(latency_s)))
+    rep = dict(p50_ms=p_nearest_rank(lat_ms, 50), p95_ms=p_nearest_rank(lat_ms, 95),
+               p99_ms=p_nearest_rank(lat_ms, 99), mean_ms=float(np.mean(lat_ms)),
+               completed=int(np.isfinite(latency_s).sum()), measured=int(sel.sum()))
+    span = float(np.nanmax(completion_s) - t0) if complete else float("nan")
+    rep["offered_qps"] = len(arr) / (t1 - t0) if t1 > t0 else float("inf")
+    rep["achieved_qps"] = len(arr) / span if complete and span > 0 else 0.0
+    # "no drops": every query completes AND the server keeps up with
+    # the offered load within the 2% noise band of SPEC.md:419 (reading R23); this is
+    # what makes SLA = inf reduce to saturation throughput.
+    rep["stable"] = int(complete and rep["achieved_qps"] >= STABILITY_BAND * rep["offered_qps"])
+    rep["sla_met"] = int(rep["stable"] and rep["p95_ms"] <= sla_ms)
+    return rep
+
+
+def lambda_star(probe: Callable[[float], bool], lam0: float, max_iter: int = 12,
+                rel_tol: float = 0.01, lam_min: float = 1e-3, lam_max: float = 1e12) -> float:
+    """S5: largest passing rate by geometric bracketing then bisection.
+
+    probe(lam) -> True iff the SLA is met at offered rate lam.
+    Returns 0.0 when even lam_min fails.
+    """
+    lo, hi = None, None
+    lam = lam0
+    for _ in range(64):
+        if lam > lam_max:
+            return lo if lo is not None else 0.0
+        if probe(lam):
+            lo = lam
+            if hi is not None:
+                break
+            lam *= 2.0
+        else:
+            hi = lam
+            if lo is not None:
+                break
+            lam *= 0.5
+            if lam < lam_min:
+                return 0.0
+        if lo is not None and hi is not None:
+            break
+    for _ in range(max_iter):
+        if (hi - lo) <= rel_tol * lo:
+            break
+        mid = 0.5 * (lo + hi)
+        if probe(mid):
+            lo = mid
+        else:
+            hi = mid
+    return lo
