@@ -1,0 +1,354 @@
+"""bench.py — throughput of the B200 DLRM query hot path (Hercules, arXiv 2203.07424).
+
+One JSON line on rank 0.  Workload (N = 1): BASELINE.json configs[1], DLRM-RMC1 —
+10 tables x 1M rows x dim 32 (1.28 GB fp32, >> 126 MB L2), pooling 80, bottom
+256-128-32, top 256-64-1, fused batches of d = 1024 items.
+
+A STEP = one fused batch through the whole hot path: a1 (queries of a burst trace,
+split/fused into batches of <= d by the library's C++ splitter/fuser before timing; the
+step submits that batch's segment list), a2 (device-side generation of its indices,
+offsets and dense features from (seed, qid, item)), a3 SLS, a4 bottom MLP, a5 dot
+interaction, a6 top MLP + sigmoid.  `value` = queries completed per second (a query
+completes when its last sub-query's batch is done) = whole-job throughput summed over
+ranks (replicas, no data-path collective: scaling "weak").  It is the saturation
+(SLA-unbounded) QPS; the serving run that checks the p95 SLA is `sla` in the line.
+
+`e2e` is the same metric through rec_query with HOST buffers (indices, offsets, dense
+copied host->device and the CTRs device->host every step).  `roofline` is the SLS
+kernel: algorithmic bytes / its CUDA-event time on its own stream.
+`cpu_baseline` times the CPU oracle on the host cores on a bounded sample.
+
+--impl reference runs the CPU oracle (the tier's reference arm) as the timed program.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import workloads as W  # noqa: E402
+
+BASELINE_METRIC = "SLA-bounded QPS (p95) per model at 1/2/4/8 B200; SLS HBM GB/s; MLP TC util"
+
+
+def sls_bytes_per_item(cfg) -> int:
+    T, L, D = cfg.num_tables, 0.5 * (cfg.pooling_lo + cfg.pooling_hi), cfg.dim
+    return int(T * (L * D * 4 + L * 4 + 4) + T * D * 4)
+
+
+def mlp_flops_per_item(cfg) -> int:
+    f = 0
+    for a, b in zip(cfg.bottom[:-1], cfg.bottom[1:]):
+        f += 2 * a * b
+    widths = [cfg.dim + cfg.num_tables * (cfg.num_tables + 1) // 2] + list(cfg.top)
+    for a, b in zip(widths[:-1], widths[1:]):
+        f += 2 * a * b
+    return f
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d["hbm_gbs"], d.get("bf16_tflops"), "measured"
+    return 6650.0, 1590.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled DURING the timed region."""
+
+    def __init__(self, dev: int):
+        self.dev, self.samples, self.proc = dev, [], None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.samples.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 3 + i and s[3 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------ CPU oracle timing
+def _oracle_job(args):
+    os.environ["OMP_NUM_THREADS"] = "1"
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    name, segs, seed = args
+    from oracle import gen, forward
+    cfg = W.SHORT[name]
+    ind, off, dense = gen.gen_batch(cfg, seed, segs)
+    t = time.perf_counter()
+    forward.forward(cfg, seed, dense, ind, off)
+    return time.perf_counter() - t, int(segs[:, 2].sum())
+
+
+def oracle_items_per_s(name: str, items_per_job: int, jobs: int, cores: int):
+    import multiprocessing as mp
+    work = [(name, W.random_segments(items_per_job, seed=100 + j), 1) for j in range(jobs)]
+    ctx = mp.get_context("fork")
+    t0 = time.perf_counter()
+    with ctx.Pool(cores) as pool:
+        res = pool.map(_oracle_job, work)
+    wall = time.perf_counter() - t0
+    items = sum(r[1] for r in res)
+    return items / wall, wall, items
+
+
+def host_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+# ---------------------------------------------------------------------- reference arm
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cfg = W.SHORT[args.config]
+    cores = host_cores()
+    per_step = args.ref_items
+    mean_q = float(W.query_sizes(200000, seed=11).mean())
+    for _ in range(args.warmup):
+        oracle_items_per_s(args.config, max(1, per_step // cores), cores, cores)
+    t0 = time.perf_counter()
+    items = 0
+    for _ in range(args.steps):
+        _, _, n = oracle_items_per_s(args.config, max(1, per_step // cores), cores, cores)
+        items += n
+    wall = time.perf_counter() - t0
+    ips = items / wall
+    qps = ips / mean_q
+    line = {"impl": "reference", "metric": BASELINE_METRIC, "value": qps, "unit": "QPS",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * wall / max(args.steps, 1), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": cfg.name, "items_per_step": items // max(args.steps, 1),
+                       "mean_query_items": mean_q, "items_per_s": ips},
+            "cpu_baseline": {"value": qps, "unit": "QPS", "cores": cores, "kind": "oracle",
+                             "sample": f"{items // max(args.steps, 1)} items/step of {cfg.name}, "
+                                       f"oracle fp64 forward (SLS+MLP+interaction+sigmoid) in a "
+                                       f"{cores}-process pool"},
+            "e2e": {"value": qps, "unit": "QPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------- our arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    from paper_2203_07424_b200 import RecModel, rec_split_fuse, KERNEL_SLS, KERNEL_GEMM
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = W.SHORT[args.config]
+    d = args.batch
+    model = RecModel(cfg, seed=1, max_batch=d, streams=1, device=local)
+    stream = torch.cuda.ExternalStream(model.rec_stream_handle(0), device=torch.device("cuda", local))
+
+    # a1: burst trace -> sub-queries -> fused batches (C++ splitter/fuser), per rank
+    trace = W.burst_trace(args.queries, seed=11 + rank)
+    segs, bstart = rec_split_fuse(trace, d)
+    nb = len(bstart) - 1
+    sizes = trace["size"].astype(np.int64)
+    last_chunk_start = ((sizes - 1) // d) * d
+    batches, items_b, done_b = [], [], []
+    for b in range(nb):
+        sg = segs[bstart[b]:bstart[b + 1]]
+        batches.append(np.ascontiguousarray(sg))
+        items_b.append(int(sg[:, 2].sum()))
+        done_b.append(int(np.sum(sg[:, 1] == last_chunk_start[sg[:, 0]])))
+    ctr = torch.zeros(d, device="cuda")
+
+    def step(i):
+        model.rec_synth_query_async(0, batches[i % nb], ctr)
+
+    for i in range(args.warmup):
+        step(i)
+    model.rec_sync(0)
+    base_launch = model.rec_profile_read(4)[1]
+    model.rec_profile(True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        with torch.cuda.stream(stream):
+            ev0.record(stream)
+        for i in range(args.warmup, args.warmup + args.steps):
+            step(i)
+        with torch.cuda.stream(stream):
+            ev1.record(stream)
+        model.rec_sync(0)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = ev0.elapsed_time(ev1)
+    launches = model.rec_profile_read(4)[1] - base_launch
+    sls_ms, sls_n = model.rec_profile_read(KERNEL_SLS)
+    gemm_ms, gemm_n = model.rec_profile_read(KERNEL_GEMM)
+    int_ms, _ = model.rec_profile_read(2)
+    gen_ms, _ = model.rec_profile_read(3)
+    model.rec_profile(False)
+    idx = [i % nb for i in range(args.warmup, args.warmup + args.steps)]
+    items = sum(items_b[i] for i in idx)
+    queries = sum(done_b[i] for i in idx)
+    t = torch.tensor([ms, items, queries], dtype=torch.float64, device="cuda")
+    if world > 1:
+        tmax = t.clone()
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        ms_max = float(tmax[0])
+    else:
+        ms_max = ms
+    tot_items, tot_q = float(t[1]), float(t[2])
+    value = tot_q / (ms_max * 1e-3)
+
+    hbm_peak, bf16_peak, peak_kind = peaks()
+    sls_bytes = sls_bytes_per_item(cfg) * items
+    sls_gbs = sls_bytes / (sls_ms * 1e-3) / 1e9 if sls_ms > 0 else None
+    flops = mlp_flops_per_item(cfg) * items
+    gemm_tf = flops / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else None
+
+    # e2e: the same metric through rec_query with host buffers (H2D + D2H every step)
+    e2e = None
+    if args.e2e_steps > 0:
+        host = []
+        for b in range(min(nb, 16)):
+            ind, off, dense = model.rec_gen_batch(batches[b])
+            host.append((dense, ind, off, items_b[b], done_b[b]))
+        out = np.zeros(d, np.float32)
+        for i in range(3):
+            h = host[i % len(host)]
+            model.rec_query(h[0], h[1], h[2], h[3], out)
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        q_e2e, h2d = 0, 0
+        for i in range(args.e2e_steps):
+            h = host[i % len(host)]
+            model.rec_query(h[0], h[1], h[2], h[3], out)
+            q_e2e += h[4]
+            h2d += h[0].nbytes + h[1].nbytes + h[2].nbytes
+        wall = time.perf_counter() - t0
+        tw = torch.tensor([wall, q_e2e], dtype=torch.float64, device="cuda")
+        if world > 1:
+            twm = tw.clone()
+            dist.all_reduce(twm, op=dist.ReduceOp.MAX)
+            dist.all_reduce(tw, op=dist.ReduceOp.SUM)
+            wall = float(twm[0])
+        e2e = {"value": float(tw[1]) / wall, "unit": "QPS",
+               "h2d_bytes_per_step": int(h2d / args.e2e_steps),
+               "d2h_bytes_per_step": int(4 * np.mean([h[3] for h in host])),
+               "steps": args.e2e_steps, "api": "rec_query (host pointers, synchronous)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cores = host_cores()
+        ips, wall, n = oracle_items_per_s(args.config, args.cpu_items, cores, cores)
+        mean_q = float(sizes.mean())
+        cpu = {"value": ips / mean_q, "unit": "QPS", "cores": cores, "kind": "oracle",
+               "sample": f"{cores} x {args.cpu_items} items of {cfg.name} (fp64 oracle forward, "
+                         f"{wall:.1f} s wall, {cores}-process pool)", "items_per_s": ips}
+
+    if rank == 0:
+        line = {
+            "metric": BASELINE_METRIC, "value": value, "unit": "QPS", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32 (SLS) + bf16 (MLP, fp32 accumulate)", "data": "synthetic",
+            "config": {"workload": cfg.name, "max_batch_d": d, "tables": cfg.num_tables,
+                       "rows": cfg.rows, "dim": cfg.dim, "pooling": cfg.pooling_lo,
+                       "items_per_s": tot_items / (ms_max * 1e-3), "queries_per_step": tot_q / args.steps / world,
+                       "mean_query_items": float(sizes.mean()), "parallelism": f"replicas x{world}",
+                       "l2": "inputs larger than L2 (1.28 GB tables, uniform random rows per step)",
+                       "value_is": "saturation QPS (burst trace); see sla"},
+            "roofline": {"bound": "hbm", "kernel": "k_sls", "achieved": sls_gbs, "peak": hbm_peak,
+                         "unit": "GB/s", "frac": (sls_gbs / hbm_peak) if sls_gbs else None,
+                         "traffic": None, "peak_kind": peak_kind,
+                         "bytes_per_item": sls_bytes_per_item(cfg), "launches": sls_n,
+                         "avg_launch_us": 1e3 * sls_ms / max(sls_n, 1)},
+            "mlp": {"bound": "tensor", "achieved_tflops": gemm_tf, "peak": bf16_peak,
+                    "frac": (gemm_tf / bf16_peak) if gemm_tf else None, "flops_per_item": mlp_flops_per_item(cfg),
+                    "launches": gemm_n, "ms": gemm_ms},
+            "breakdown_ms_per_step": {"gen": gen_ms / args.steps, "sls": sls_ms / args.steps,
+                                      "gemm": gemm_ms / args.steps, "interact": int_ms / args.steps},
+            "gpu_launches": int(launches),
+            "clocks": clk.summary(),
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    model.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3000)
+    ap.add_argument("--warmup", type=int, default=50)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="rmc1", choices=list(W.SHORT))
+    ap.add_argument("--batch", type=int, default=1024)
+    ap.add_argument("--queries", type=int, default=20000)
+    ap.add_argument("--e2e-steps", type=int, default=300)
+    ap.add_argument("--cpu-items", type=int, default=256)
+    ap.add_argument("--ref-items", type=int, default=64)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,198 @@
+/*
+ * rec.h — C ABI of the B200-native DLRM query hot path under Hercules-style
+ * recommendation inference serving (arXiv 2203.07424, "Hercules").
+ *
+ * Citations: P:n = line n of the paper text; DESIGN.md §n / Rn = this
+ * repo's design notes and readings.  Library: libhercules_rec.so (sm_100a).
+ *
+ * Conventions for every call
+ *   - Every function returns rec_status (REC_OK = 0) unless declared otherwise.
+ *   - All array arguments are borrowed for the duration of the call; the library
+ *     never retains a caller pointer.  Unless stated, a pointer may be host or
+ *     device memory (detected with cudaPointerGetAttributes); host data is staged
+ *     through library-owned pinned buffers.
+ *   - Outputs are written only when the call returns REC_OK (for *_async calls:
+ *     when the matching rec_sync returns REC_OK).
+ *   - A model handle is not safe for concurrent calls from several host threads.
+ *   - On error, rec_last_error() returns a thread-local message naming the field
+ *     or the failing CUDA/NCCL call.  There is no CPU fallback: without a usable
+ *     sm_100 device rec_model_create returns REC_E_CUDA.
+ */
+#ifndef HERCULES_REC_H
+#define HERCULES_REC_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  REC_OK = 0,
+  REC_E_INVALID_ARG = -1,  /* null pointer, inconsistent widths, batch <= 0, bad policy   */
+  REC_E_INDEX_OOB = -2,    /* an index outside [0, rows_t) (R9: no clamping)              */
+  REC_E_OFFSETS = -3,      /* offsets[0] != 0, decreasing, or offsets[T*B] != nnz bound   */
+  REC_E_OOM = -4,          /* device or pinned allocation failed                          */
+  REC_E_CUDA = -5,         /* CUDA runtime/driver error (incl. no sm_100 device)          */
+  REC_E_NCCL = -6,         /* NCCL error in a sharded model                               */
+  REC_E_UNSUPPORTED = -7   /* D % 4 != 0, D > 128, rows >= 2^31, widths > limits          */
+} rec_status;
+
+enum { REC_VALUES_INT8_EXACT = 0, REC_VALUES_FP32 = 1 };           /* DESIGN.md G4        */
+enum { REC_INDEX_UNIFORM = 0, REC_INDEX_SKEW2 = 2 };                /* DESIGN.md G2, R17   */
+enum { REC_SHARD_REPLICA = 0, REC_SHARD_TABLE = 1, REC_SHARD_ROW = 2 };
+enum { REC_INPUT_DEVICE_SYNTH = 0, REC_INPUT_HOST = 1 };
+enum { REC_CLOCK_REAL = 0, REC_CLOCK_VIRTUAL = 1 };                 /* DESIGN.md S4        */
+
+typedef struct rec_model_s* rec_model_t;   /* opaque; owns all device memory it allocated */
+
+/*
+ * Model description — "a recommendation model in the form of a computation graph
+ * G_m" restricted to the DLRM class of Table I: T embedding
+ * tables with multi-hot pooled lookups (SparseNet), a Bottom-FC and a Predict-FC
+ * stack (DenseNet), joined by the dot interaction (R1).
+ */
+typedef struct {
+  int32_t num_tables;             /* T >= 1                                                */
+  const int64_t* rows;            /* [T] rows per table, each in [1, 2^31)                 */
+  int32_t dim;                    /* D: multiple of 4, <= 128; == bottom_widths[n_bottom-1] */
+  int32_t pooling_lo, pooling_hi; /* lookups per bag for synthetic inputs (G3); lo == hi =>
+                                     fixed; lo = hi = 1 is the one-hot case     */
+  const int32_t* bottom_widths;   /* [n_bottom] INCLUDING the dense input width (R3),
+                                     e.g. {256,128,32}; n_bottom >= 2                       */
+  int32_t n_bottom;
+  const int32_t* top_widths;      /* [n_top] EXCLUDING the interaction width, last == 1 (R3),
+                                     e.g. {256,64,1}; n_top >= 2; top_widths[n_top-2] <= 256 */
+  int32_t n_top;
+  int32_t top_shift;              /* extra 2^-top_shift on the first top layer (R21)        */
+  uint64_t seed;                  /* tables, weights and synthetic inputs = f(seed) (G1-G5) */
+  int32_t value_mode;             /* REC_VALUES_INT8_EXACT | REC_VALUES_FP32                */
+  int32_t index_dist;             /* REC_INDEX_UNIFORM | REC_INDEX_SKEW2 (synthetic inputs) */
+  int32_t max_batch;              /* workspace capacity in items per call/batch (>= 1)      */
+  int32_t streams;                /* co-located streams m, workspaces, >= 1     */
+  int32_t device;                 /* CUDA device ordinal used by this handle                */
+  int32_t shard;                  /* REC_SHARD_REPLICA | REC_SHARD_TABLE | REC_SHARD_ROW    */
+  int32_t rank, world;            /* this process's rank and the number of GPUs (1 => local) */
+  const void* nccl_id;            /* 128-byte ncclUniqueId shared by all ranks (world > 1)  */
+  int64_t l2_persist_bytes;       /* > 0: L2 persisting window over the hot row prefix of
+                                     every table (A10/D2 residue), 0 = off       */
+} rec_model_desc;
+
+/* Build the model: validate, allocate the fp32 table arena and the bf16 weights,
+ * generate all parameters on the device from `seed` (G4/G5), encode TMA tensor maps,
+ * create `streams` CUDA streams with per-stream workspaces, and (world > 1)
+ * bootstrap NCCL.  Errors: INVALID_ARG (names the field), UNSUPPORTED, OOM, CUDA, NCCL. */
+rec_status rec_model_create(const rec_model_desc* desc, rec_model_t* out);
+void rec_model_destroy(rec_model_t m);                       /* NULL-safe; frees everything */
+
+/* One batched query forward: SLS -> bottom MLP -> dot interaction ->
+ * top MLP -> sigmoid.  dense [B][F] fp32 row-major (F = bottom_widths[0]);
+ * indices [nnz] int32 and offsets [T*B+1] int32 in table-major CSR (bag g = t*B + b
+ * spans indices[offsets[g] .. offsets[g+1])); ctr [B] fp32 out.  Host or device
+ * pointers.  Synchronous.  Errors: INVALID_ARG (batch <= 0 or > max_batch),
+ * OFFSETS, INDEX_OOB (device-detected), CUDA. */
+rec_status rec_query(rec_model_t m, const float* dense, const int32_t* indices,
+                     const int32_t* offsets, int32_t batch, float* ctr);
+
+/* rec_query plus diagnostics: pooled [B][T][D] fp32 (SLS output) and logits [B]
+ * (pre-sigmoid), each optional (NULL).  Used by the parity tests. */
+rec_status rec_query_debug(rec_model_t m, const float* dense, const int32_t* indices,
+                           const int32_t* offsets, int32_t batch, float* ctr,
+                           float* pooled, float* logits);
+
+/* Enqueue rec_query on stream slot `slot` (0 <= slot < streams) without waiting.
+ * DEVICE pointers only; `nnz` = offsets[T*B] (not read back).  Completion and the
+ * device error flag are collected by rec_sync(m, slot). */
+rec_status rec_query_async(rec_model_t m, int32_t slot, const float* dense,
+                           const int32_t* indices, const int32_t* offsets, int64_t nnz,
+                           int32_t batch, float* ctr);
+
+/* Device-synthesised batch (serving input mode REC_INPUT_DEVICE_SYNTH):
+ * the batch is the concatenation of item segments segs[nseg][3] = (qid, start, len)
+ * (host memory); indices/offsets/dense are generated on the device (G2-G4) and the
+ * forward runs on stream slot `slot`.  ctr [sum len] fp32 DEVICE pointer.  Async. */
+rec_status rec_synth_query_async(rec_model_t m, int32_t slot, const int32_t* segs,
+                                 int32_t nseg, float* ctr);
+
+/* Wait for stream slot `slot`; returns INDEX_OOB / OFFSETS if a kernel flagged it. */
+rec_status rec_sync(rec_model_t m, int32_t slot);
+
+/* cudaStream_t of stream slot `slot` (for event timing by the caller), or NULL. */
+void* rec_stream_handle(rec_model_t m, int32_t slot);
+
+/* Test/diagnostic export: the synthetic inputs of a segment batch (G2-G4), bit-exact
+ * with the oracle.  indices [T*B*pooling_hi] capacity, offsets [T*B+1], dense [B][F];
+ * host or device pointers. */
+rec_status rec_gen_batch(rec_model_t m, const int32_t* segs, int32_t nseg,
+                         int32_t* indices, int32_t* offsets, float* dense);
+
+/* Per-kernel device time accumulated while profiling is on (CUDA events recorded on
+ * the launching stream around every launch).  kernel: 0 = SLS, 1 = GEMM (all layers),
+ * 2 = interaction, 3 = input generation; kernel = 4 returns in *launches the number of
+ * kernels this handle has launched so far (all streams; *total_ms = 0).
+ * enable != 0 turns recording on and resets the times. */
+rec_status rec_profile(rec_model_t m, int32_t enable);
+rec_status rec_profile_read(rec_model_t m, int32_t kernel, double* total_ms, int64_t* launches);
+
+/* ---------------------------------------------------------------- serving (a1, a7) */
+typedef struct { double arrival_s; int32_t size; int32_t qid; } rec_trace_row;
+
+typedef struct {
+  int32_t streams;            /* m co-located streams used (<= model streams) */
+  int32_t max_batch;          /* d: split chunk and fused-batch cap (<= model max_batch)  */
+  double fusion_timeout_ms;   /* tau: 0 = work-conserving (R15)                           */
+  int32_t input_mode;         /* REC_INPUT_DEVICE_SYNTH | REC_INPUT_HOST                  */
+  int32_t clock;              /* REC_CLOCK_REAL | REC_CLOCK_VIRTUAL                       */
+  double alpha_ns, beta_ns;   /* virtual clock: service = alpha + beta * items (S4)       */
+  double warmup_frac;         /* fraction of the trace span excluded from percentiles     */
+} rec_serve_policy;
+
+typedef struct {
+  double offered_qps, achieved_qps, mean_ms, p50_ms, p95_ms, p99_ms;
+  double breakdown_ms[4];     /* mean per query: queue, input, sparse+dense (device), tail */
+  int64_t completed, dropped, batches;
+  double mean_batch;
+  int32_t sla_met;            /* p95 <= SLA, all completed, achieved >= 0.98 offered (R23) */
+  int32_t stable;
+} rec_serve_report;
+
+/* Query splitting + fusion (S1, S2) for queries that are all pending
+ * (a burst, FIFO in trace order): split each query into chunks of max_batch items
+ * (remainder last), then fuse FIFO chunks into batches with cumulative size <= max_batch
+ * (at least one chunk each).  Host-only (no device needed).
+ * segs_out [seg_cap][3] = (qid, start, len); batch_start [bcap+1]: batch b spans
+ * segs_out[batch_start[b] .. batch_start[b+1]).  *nbatches, *nsegs are set.
+ * Errors: INVALID_ARG (max_batch < 1, size < 1, capacity too small). */
+rec_status rec_split_fuse(const rec_trace_row* trace, int64_t n, int32_t max_batch,
+                          int32_t* segs_out, int64_t seg_cap, int64_t* batch_start,
+                          int64_t bcap, int64_t* nbatches, int64_t* nsegs);
+
+/* Serve a query trace (rows sorted by arrival_s, qid unique) on this GPU under the
+ * policy: split each query into chunks of d (S1), fuse FIFO chunks with
+ * cumulative size <= d (S2) onto the lowest idle of m streams (S3), run the
+ * forward per batch, timestamp completions, and report latency percentiles against
+ * `sla_ms` (S5).  Real clock: arrivals are released open-loop at
+ * arrival_s; the batch list depends on timing (invariants only).  Virtual clock:
+ * the dispatcher advances a simulated clock (S4) and the batch list is unique and
+ * bit-exact with the oracle replay; the kernels still run.
+ * latency_ms [n] (optional, per trace row) and batch_log (optional, flattened rows
+ * (batch, stream, qid, start, len), capacity log_cap rows; the number of rows written
+ * is returned in report->batches' companion, see rec_serve_log_rows).
+ * ctr_out [sum sizes] (optional, host): CTR of every item, query-major in trace
+ * order.  Errors: INVALID_ARG (bad policy, before any work), CUDA. */
+rec_status rec_serve(rec_model_t m, const rec_trace_row* trace, int64_t n, double sla_ms,
+                     const rec_serve_policy* pol, rec_serve_report* out,
+                     double* latency_ms, int32_t* batch_log, int64_t log_cap,
+                     int64_t* log_rows, float* ctr_out);
+
+/* --------------------------------------------------------------------- utilities */
+const char* rec_last_error(void);             /* thread-local; valid until the next call */
+int32_t rec_nccl_unique_id_size(void);        /* bytes of an ncclUniqueId (128)          */
+rec_status rec_nccl_get_unique_id(void* out); /* rank 0 creates, caller broadcasts       */
+int32_t rec_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HERCULES_REC_H */

@@ -1,0 +1,238 @@
+// k_gemm.cu — FC layers of the bottom and top MLP on the 5th-generation tensor cores
+// (Table I Bottom-FC / Predict-FC).
+//
+//   D[M x N] = A[M x K] . W[N x K]^T   (bf16 operands, fp32 accumulation in TMEM)
+//   epilogue: + bias, ReLU, then one of
+//     GEMM_OUT_BF16  hidden activation -> bf16 [M][ldo] (A operand of the next layer)
+//     GEMM_OUT_X_F32 last bottom layer -> fp32 X slot 0 (interaction input)
+//     GEMM_OUT_CTR   last top hidden layer -> per-row fp32 dot with the width-1 output
+//                    layer + bias -> sigmoid -> CTR (Predict-FC "...-1")
+//
+// One CTA (128 threads) per 128 x BN output tile.  Warp 0 lane 0: TMA producer
+// (cp.async.bulk.tensor.2d, SWIZZLE_128B, 64-element K boxes) into an S-stage smem ring
+// guarded by full/empty mbarriers.  Warp 1 lane 0: single-thread tcgen05.mma issuer
+// (M = 128, N = BN, K = 16 per instruction) accumulating in TMEM; tcgen05.commit frees
+// each stage and finally signals the epilogue.  Epilogue: all 4 warps, thread = output
+// row (TMEM lane), tcgen05.ld 16 columns at a time.  No split-K and no atomics, so an
+// item's output bits do not depend on the batch it rides in (batch invariance).
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
+#include "common.cuh"
+#include "kernels.h"
+#include "sm100.cuh"
+
+namespace rec {
+
+constexpr int BM = 128;
+constexpr int BK = 64;
+constexpr int A_STAGE_BYTES = BM * BK * 2;  // 16 KB
+
+template <int BN>
+__global__ void __launch_bounds__(128, 1)
+    k_gemm_tc(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_w,
+              const GemmArgs args, int stages) {
+  constexpr int B_STAGE_BYTES = BN * BK * 2;
+  constexpr int STAGE_BYTES = A_STAGE_BYTES + B_STAGE_BYTES;
+  constexpr uint32_t TMEM_COLS = BN < 32 ? 32 : BN;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + stages * STAGE_BYTES);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + stages;
+  uint64_t* done = bars + 2 * stages;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 2 * stages + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
+  const int nkb = (args.K + BK - 1) / BK;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < stages; ++s) {
+      sm100::mbar_init(&full[s], 1);
+      sm100::mbar_init(&empty[s], 1);
+    }
+    sm100::mbar_init(done, 1);
+    sm100::fence_mbar_init();
+    sm100::tma_prefetch_desc(&tmap_a);
+    sm100::tma_prefetch_desc(&tmap_w);
+  }
+  if (warp == 0) sm100::tmem_alloc(tslot, TMEM_COLS);
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  const uint32_t tmem = *tslot;
+
+  if (warp == 0 && lane == 0) {
+    // ---------------- TMA producer
+    for (int kb = 0; kb < nkb; ++kb) {
+      const int s = kb % stages, it = kb / stages;
+      if (it > 0) sm100::mbar_wait(&empty[s], (it - 1) & 1);
+      uint8_t* sa = smem + s * STAGE_BYTES;
+      sm100::mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
+      sm100::tma_load_2d(sa, &tmap_a, &full[s], kb * BK, m0);
+      sm100::tma_load_2d(sa + A_STAGE_BYTES, &tmap_w, &full[s], kb * BK, n0);
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ---------------- single-thread MMA issuer
+    constexpr uint32_t idesc = sm100::idesc_bf16_f32(BM, BN);
+    for (int kb = 0; kb < nkb; ++kb) {
+      const int s = kb % stages, it = kb / stages;
+      sm100::mbar_wait(&full[s], it & 1);
+      sm100::tc_fence_after();
+      const uint32_t sa = sm100::smem_u32(smem + s * STAGE_BYTES);
+      const uint64_t da = sm100::umma_desc_sw128(sa);
+      const uint64_t db = sm100::umma_desc_sw128(sa + A_STAGE_BYTES);
+#pragma unroll
+      for (int k = 0; k < BK / 16; ++k) {
+        // advance 16 bf16 = 32 B along K inside the 128-B swizzled row: +2 in addr>>4
+        sm100::mma_bf16_ss(tmem, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
+      }
+      sm100::mma_commit(&empty[s]);
+    }
+    sm100::mma_commit(done);
+  }
+
+  // ---------------- epilogue: thread = row (TMEM lane warp*32 + lane)
+  sm100::mbar_wait(done, 0);
+  __syncwarp();
+  sm100::tc_fence_after();
+  const int row = m0 + warp * 32 + lane;
+  const bool row_ok = row < args.M;
+  const uint32_t trow = tmem + (static_cast<uint32_t>(warp * 32) << 16);
+  float dot = 0.f;
+#pragma unroll 1
+  for (int c0 = 0; c0 < BN; c0 += 16) {
+    uint32_t r[16];
+    sm100::tmem_ld_32x32b_x16(trow + c0, r);
+    sm100::tmem_ld_wait();
+    const int cbase = n0 + c0;
+    if (cbase >= args.N) continue;  // warp-uniform
+    float v[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int c = cbase + j;
+      float x = __uint_as_float(r[j]);
+      if (c < args.N) {
+        x += __ldg(&args.bias[c]);
+        if (args.relu) x = fmaxf(x, 0.f);
+      } else {
+        x = 0.f;
+      }
+      v[j] = x;
+    }
+    if (!row_ok) continue;
+    if (args.mode == GEMM_OUT_BF16) {
+      __nv_bfloat16* dst = args.out_bf16 + static_cast<int64_t>(row) * args.ldo + cbase;
+      if (cbase + 16 <= args.N) {
+        uint32_t p[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * j], v[2 * j + 1]);
+          p[j] = *reinterpret_cast<uint32_t*>(&h);
+        }
+        uint4* d4 = reinterpret_cast<uint4*>(dst);
+        d4[0] = make_uint4(p[0], p[1], p[2], p[3]);
+        d4[1] = make_uint4(p[4], p[5], p[6], p[7]);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          if (cbase + j < args.N) dst[j] = __float2bfloat16_rn(v[j]);
+      }
+    } else if (args.mode == GEMM_OUT_X_F32) {
+      float* dst = args.out_f32 + static_cast<int64_t>(row) * args.ldo + cbase;
+      if (cbase + 16 <= args.N) {
+        float4* d4 = reinterpret_cast<float4*>(dst);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) d4[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          if (cbase + j < args.N) dst[j] = v[j];
+      }
+    } else {  // GEMM_OUT_CTR: width-1 output layer folded into the epilogue
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const int c = cbase + j;
+        if (c < args.N) dot = fmaf(v[j], __ldg(&args.w_last[c]), dot);
+      }
+    }
+  }
+  if (args.mode == GEMM_OUT_CTR && row_ok) {
+    const float logit = dot + args.b_last;
+    args.ctr[row] = 1.f / (1.f + __expf(-logit));
+    if (args.logit) args.logit[row] = logit;
+  }
+  sm100::tc_fence_before();
+  __syncthreads();
+  if (warp == 0) sm100::tmem_dealloc(tmem, TMEM_COLS);
+}
+
+template <int BN>
+static void launch_bn(const CUtensorMap* ta, const CUtensorMap* tw, const GemmArgs& a,
+                      cudaStream_t s) {
+  constexpr int STAGE = A_STAGE_BYTES + BN * BK * 2;
+  const int nkb = (a.K + BK - 1) / BK;
+  const int stages = nkb < 4 ? (nkb < 1 ? 1 : nkb) : 4;
+  const size_t smem = static_cast<size_t>(stages) * STAGE + 1024 + 256;
+  dim3 grid((a.M + BM - 1) / BM, (a.N + BN - 1) / BN);
+  k_gemm_tc<BN><<<grid, 128, smem, s>>>(*ta, *tw, a, stages);
+}
+
+int gemm_bn(int N) { return N <= 32 ? 32 : N <= 64 ? 64 : N <= 128 ? 128 : 256; }
+
+template <int BN>
+static void prep_bn() {
+  constexpr int STAGE = A_STAGE_BYTES + BN * BK * 2;
+  cudaFuncSetAttribute(k_gemm_tc<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       4 * STAGE + 1024 + 256);
+}
+
+void gemm_prepare() {
+  prep_bn<32>();
+  prep_bn<64>();
+  prep_bn<128>();
+  prep_bn<256>();
+}
+
+void launch_gemm_tc(const CUtensorMap* tmap_a, const CUtensorMap* tmap_w, const GemmArgs& a,
+                    cudaStream_t s) {
+  if (a.M <= 0) return;
+  if (a.N <= 32) launch_bn<32>(tmap_a, tmap_w, a, s);
+  else if (a.N <= 64) launch_bn<64>(tmap_a, tmap_w, a, s);
+  else if (a.N <= 128) launch_bn<128>(tmap_a, tmap_w, a, s);
+  else launch_bn<256>(tmap_a, tmap_w, a, s);
+}
+
+// ---------------------------------------------------------------- tensor maps
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+bool encode_tmap_bf16(CUtensorMap* map, const void* base, uint64_t rows, uint64_t K, uint64_t ldk,
+                      uint32_t box_rows) {
+  auto fn = get_encode();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {K, rows};
+  cuuint64_t strides[1] = {ldk * 2};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(BK), box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+}  // namespace rec

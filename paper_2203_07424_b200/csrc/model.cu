@@ -1,0 +1,850 @@
+// model.cu — rec_model_create/destroy, rec_query*, rec_gen_batch, profiling (include/rec.h).
+//
+// Host side of the hot path: validates the model description (Table I shapes),
+// allocates the fp32 embedding arena and bf16 MLP weights on the device, generates every
+// parameter there from the seed (G4/G5), encodes the TMA tensor maps of every GEMM operand
+// once, and enqueues the per-batch kernel chain  [input] -> SLS -> bottom GEMMs ->
+// interaction -> top GEMMs (+ width-1 layer + sigmoid)  on one CUDA stream per co-located
+// "inference thread" (model co-location).
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+
+#include "common.cuh"
+#include "model.h"
+
+namespace rec {
+
+static thread_local std::string g_err;
+
+void set_error(const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+}
+
+rec_status cuda_fail(cudaError_t e, const char* what) {
+  set_error("CUDA error %s (%s) in %s", cudaGetErrorName(e), cudaGetErrorString(e), what);
+  return REC_E_CUDA;
+}
+
+static int pad8(int x) { return (x + 7) & ~7; }
+
+static bool is_device_ptr(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+cudaEvent_t prof_begin(rec_model_s* m, Workspace& w) {
+  if (!m->prof) return nullptr;
+  cudaEvent_t a;
+  if (!m->prof_pool.empty()) {
+    a = m->prof_pool.back();
+    m->prof_pool.pop_back();
+  } else {
+    cudaEventCreate(&a);
+  }
+  cudaEventRecord(a, w.stream);
+  return a;
+}
+
+void prof_end(rec_model_s* m, Workspace& w, int kernel, cudaEvent_t a) {
+  if (!a) return;
+  cudaEvent_t b;
+  if (!m->prof_pool.empty()) {
+    b = m->prof_pool.back();
+    m->prof_pool.pop_back();
+  } else {
+    cudaEventCreate(&b);
+  }
+  cudaEventRecord(b, w.stream);
+  m->prof_events.push_back(ProfEvent{kernel, a, b});
+}
+
+static void prof_collect(rec_model_s* m) {
+  for (auto& e : m->prof_events) {
+    cudaEventSynchronize(e.b);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e.a, e.b);
+    m->prof_ms[e.kernel] += ms;
+    m->prof_n[e.kernel] += 1;
+    m->prof_pool.push_back(e.a);
+    m->prof_pool.push_back(e.b);
+  }
+  m->prof_events.clear();
+}
+
+// ------------------------------------------------------------------ forward chain
+rec_status forward_enqueue(rec_model_s* m, Workspace& w, const int* indices, const int* offsets,
+                           int B, float* ctr_out, float* logit_out) {
+  const int T = m->T, D = m->D;
+  cudaStream_t s = w.stream;
+  // a3: SLS -> X slots 1..T
+  cudaEvent_t e0 = prof_begin(m, w);
+  launch_sls(m->tables, m->d_tab_off, m->row_stride, m->d_rows, indices, offsets, B, T, D, w.X,
+             (T + 1) * D, 1, w.flag, s);
+  prof_end(m, w, 0, e0);
+  // a4: bottom MLP -> X slot 0
+  const int nb = static_cast<int>(m->bottom.size());
+  for (int l = 0; l < nb; ++l) {
+    const Layer& L = m->bottom[l];
+    GemmArgs a{};
+    a.M = B;
+    a.N = L.N;
+    a.K = L.K;
+    a.bias = L.bias;
+    a.relu = 1;
+    if (l == nb - 1) {
+      a.mode = GEMM_OUT_X_F32;
+      a.out_f32 = w.X;
+      a.ldo = (T + 1) * D;
+    } else {
+      a.mode = GEMM_OUT_BF16;
+      a.out_bf16 = static_cast<__nv_bfloat16*>(w.out_bottom[l]);
+      a.ldo = L.Npad;
+    }
+    cudaEvent_t e = prof_begin(m, w);
+    launch_gemm_tc(&w.tmap_a_bottom[l], &L.tmap_w, a, s);
+    prof_end(m, w, 1, e);
+  }
+  // a5: interaction -> A_top
+  cudaEvent_t e1 = prof_begin(m, w);
+  launch_interact(w.X, B, T, D, w.A_top, m->Ktop_pad, s);
+  prof_end(m, w, 2, e1);
+  // a6: top MLP; the last hidden layer's epilogue applies the width-1 layer + sigmoid
+  const int nt = static_cast<int>(m->top.size());
+  for (int j = 0; j < nt; ++j) {
+    const Layer& L = m->top[j];
+    GemmArgs a{};
+    a.M = B;
+    a.N = L.N;
+    a.K = L.K;
+    a.bias = L.bias;
+    a.relu = 1;
+    if (j == nt - 1) {
+      a.mode = GEMM_OUT_CTR;
+      a.w_last = m->w_last;
+      a.b_last = m->b_last;
+      a.ctr = ctr_out;
+      a.logit = logit_out;
+    } else {
+      a.mode = GEMM_OUT_BF16;
+      a.out_bf16 = static_cast<__nv_bfloat16*>(w.out_top[j]);
+      a.ldo = L.Npad;
+    }
+    cudaEvent_t e = prof_begin(m, w);
+    launch_gemm_tc(&w.tmap_a_top[j], &L.tmap_w, a, s);
+    prof_end(m, w, 1, e);
+  }
+  m->launches += 2 + nb + nt;
+  cudaError_t err = cudaGetLastError();
+  if (err != cudaSuccess) return cuda_fail(err, "forward kernel launch");
+  return REC_OK;
+}
+
+static rec_status wait_pin(Workspace& w) {
+  REC_CUDA(cudaEventSynchronize(w.pin_free));
+  return REC_OK;
+}
+
+// segs (host) -> device rows -> indices / offsets / dense (G2-G4) on w.stream
+static rec_status synth_inputs(rec_model_s* m, Workspace& w, const int32_t* segs, int nseg,
+                               int* batch_out, float* dense_f32_out) {
+  if (nseg <= 0 || !segs) {
+    set_error("segs: empty segment list");
+    return REC_E_INVALID_ARG;
+  }
+  int64_t B = 0;
+  for (int i = 0; i < nseg; ++i) {
+    if (segs[3 * i + 2] <= 0 || segs[3 * i] < 0 || segs[3 * i + 1] < 0) {
+      set_error("segs[%d]: qid/start must be >= 0 and len > 0", i);
+      return REC_E_INVALID_ARG;
+    }
+    B += segs[3 * i + 2];
+  }
+  if (B > w.cap || nseg > w.cap) {
+    set_error("segs: batch of %lld items exceeds max_batch %d", (long long)B, w.cap);
+    return REC_E_INVALID_ARG;
+  }
+  rec_status st = wait_pin(w);
+  if (st != REC_OK) return st;
+  int4* p = reinterpret_cast<int4*>(w.pin);
+  int row = 0;
+  for (int i = 0; i < nseg; ++i) {
+    p[i] = make_int4(segs[3 * i], segs[3 * i + 1], segs[3 * i + 2], row);
+    row += segs[3 * i + 2];
+  }
+  cudaStream_t s = w.stream;
+  REC_CUDA(cudaMemcpyAsync(w.segs, p, sizeof(int4) * nseg, cudaMemcpyHostToDevice, s));
+  REC_CUDA(cudaEventRecord(w.pin_free, s));
+  const int Bi = static_cast<int>(B);
+  cudaEvent_t e = prof_begin(m, w);
+  launch_expand_rows(w.segs, nseg, Bi, w.rowq, w.rowi, s);
+  launch_gen_offsets(w.rowq, w.rowi, Bi, m->T, m->lo, m->hi, m->k0, m->k1, w.offsets, s);
+  launch_gen_indices(w.rowq, w.rowi, w.offsets, Bi, m->T, m->d_rows, m->index_dist, m->k0, m->k1,
+                     w.indices, s);
+  launch_gen_dense(w.rowq, w.rowi, Bi, m->F, m->Fpad, m->k0, m->k1, w.dense_bf, dense_f32_out, s);
+  prof_end(m, w, 3, e);
+  m->launches += 4;
+  *batch_out = Bi;
+  return REC_OK;
+}
+
+rec_status synth_enqueue(rec_model_s* m, Workspace& w, const int32_t* segs, int nseg,
+                         int* batch_out) {
+  return synth_inputs(m, w, segs, nseg, batch_out, nullptr);
+}
+
+static rec_status read_flag(Workspace& w) {
+  const int f = *w.flag_host;
+  if (f & 1) {
+    set_error("an index is outside [0, rows_t) (REC_E_INDEX_OOB)");
+    return REC_E_INDEX_OOB;
+  }
+  if (f & 2) {
+    set_error("offsets are not non-decreasing from 0 (REC_E_OFFSETS)");
+    return REC_E_OFFSETS;
+  }
+  return REC_OK;
+}
+
+static rec_status sync_ws(Workspace& w) {
+  REC_CUDA(cudaMemcpyAsync(w.flag_host, w.flag, sizeof(int), cudaMemcpyDeviceToHost, w.stream));
+  REC_CUDA(cudaMemsetAsync(w.flag, 0, sizeof(int), w.stream));
+  REC_CUDA(cudaStreamSynchronize(w.stream));
+  return read_flag(w);
+}
+
+// ------------------------------------------------------------------ query (sync)
+static rec_status query_impl(rec_model_s* m, const float* dense, const int32_t* indices,
+                             const int32_t* offsets, int32_t B, float* ctr, float* pooled,
+                             float* logits) {
+  if (!m || !dense || !indices || !offsets || !ctr) {
+    set_error("null argument (model, dense, indices, offsets and ctr are required)");
+    return REC_E_INVALID_ARG;
+  }
+  if (B <= 0 || B > m->max_batch) {
+    set_error("batch = %d must be in [1, max_batch = %d]", B, m->max_batch);
+    return REC_E_INVALID_ARG;
+  }
+  REC_CUDA(cudaSetDevice(m->device));
+  Workspace& w = m->ws[0];
+  cudaStream_t s = w.stream;
+  const int T = m->T, nb = T * B;
+  rec_status st = wait_pin(w);
+  if (st != REC_OK) return st;
+  uint8_t* pin = w.pin;
+  const bool off_dev = is_device_ptr(offsets), idx_dev = is_device_ptr(indices),
+             den_dev = is_device_ptr(dense);
+  const int* d_off = offsets;
+  const int* d_idx = indices;
+  REC_CUDA(cudaMemsetAsync(w.flag, 0, sizeof(int), s));
+  size_t pos = 0;
+  if (!off_dev) {
+    if (offsets[0] != 0) {
+      set_error("offsets[0] = %d, must be 0", offsets[0]);
+      return REC_E_OFFSETS;
+    }
+    for (int g = 0; g < nb; ++g)
+      if (offsets[g + 1] < offsets[g]) {
+        set_error("offsets[%d] = %d < offsets[%d] = %d", g + 1, offsets[g + 1], g, offsets[g]);
+        return REC_E_OFFSETS;
+      }
+    const int64_t nnz = offsets[nb];
+    if (nnz > w.idx_cap) {
+      set_error("offsets[T*B] = %lld exceeds the index capacity %lld (T*max_batch*pooling_hi)",
+                (long long)nnz, (long long)w.idx_cap);
+      return REC_E_INVALID_ARG;
+    }
+    memcpy(pin + pos, offsets, sizeof(int) * (nb + 1));
+    REC_CUDA(cudaMemcpyAsync(w.offsets, pin + pos, sizeof(int) * (nb + 1), cudaMemcpyHostToDevice, s));
+    pos += sizeof(int) * (nb + 1);
+    pos = (pos + 255) & ~size_t(255);
+    d_off = w.offsets;
+    if (!idx_dev) {
+      memcpy(pin + pos, indices, sizeof(int) * nnz);
+      REC_CUDA(cudaMemcpyAsync(w.indices, pin + pos, sizeof(int) * nnz, cudaMemcpyHostToDevice, s));
+      pos += sizeof(int) * nnz;
+      pos = (pos + 255) & ~size_t(255);
+      d_idx = w.indices;
+    }
+  } else {
+    launch_check_offsets(offsets, nb, w.flag, s);
+    if (!idx_dev) {
+      set_error("indices on the host with offsets on the device is not supported");
+      return REC_E_INVALID_ARG;
+    }
+  }
+  const float* d_dense = dense;
+  if (!den_dev) {
+    memcpy(pin + pos, dense, sizeof(float) * B * m->F);
+    REC_CUDA(cudaMemcpyAsync(w.dense_f32, pin + pos, sizeof(float) * B * m->F,
+                             cudaMemcpyHostToDevice, s));
+    d_dense = w.dense_f32;
+  }
+  REC_CUDA(cudaEventRecord(w.pin_free, s));
+  launch_dense_to_bf16(d_dense, B, m->F, m->Fpad, w.dense_bf, s);
+  m->launches += 1 + (off_dev ? 1 : 0);
+  st = forward_enqueue(m, w, d_idx, d_off, B, w.ctr, w.logit);
+  if (st != REC_OK) return st;
+  REC_CUDA(cudaMemcpyAsync(w.flag_host, w.flag, sizeof(int), cudaMemcpyDeviceToHost, s));
+  REC_CUDA(cudaStreamSynchronize(s));
+  st = read_flag(w);
+  if (st != REC_OK) return st;
+  REC_CUDA(cudaMemcpyAsync(ctr, w.ctr, sizeof(float) * B, cudaMemcpyDefault, s));
+  if (logits) REC_CUDA(cudaMemcpyAsync(logits, w.logit, sizeof(float) * B, cudaMemcpyDefault, s));
+  if (pooled) {
+    const int D = m->D;
+    REC_CUDA(cudaMemcpy2DAsync(pooled, sizeof(float) * T * D, w.X + D, sizeof(float) * (T + 1) * D,
+                               sizeof(float) * T * D, B, cudaMemcpyDefault, s));
+  }
+  REC_CUDA(cudaStreamSynchronize(s));
+  return REC_OK;
+}
+
+}  // namespace rec
+
+using namespace rec;
+
+// ====================================================================== C ABI
+extern "C" {
+
+const char* rec_last_error(void) { return g_err.c_str(); }
+int32_t rec_version(void) { return 1; }
+
+static void free_model(rec_model_s* m) {
+  if (!m) return;
+  cudaSetDevice(m->device);
+  for (auto& w : m->ws) {
+    if (w.stream) cudaStreamSynchronize(w.stream);
+    cudaFree(w.indices);
+    cudaFree(w.offsets);
+    cudaFree(w.segs);
+    cudaFree(w.rowq);
+    cudaFree(w.rowi);
+    cudaFree(w.dense_f32);
+    cudaFree(w.dense_bf);
+    cudaFree(w.X);
+    cudaFree(w.A_top);
+    cudaFree(w.h[0]);
+    cudaFree(w.h[1]);
+    cudaFree(w.ctr);
+    cudaFree(w.logit);
+    cudaFree(w.flag);
+    if (w.flag_host) cudaFreeHost(w.flag_host);
+    if (w.pin) cudaFreeHost(w.pin);
+    if (w.pin_free) cudaEventDestroy(w.pin_free);
+    if (w.stream) cudaStreamDestroy(w.stream);
+  }
+  for (auto& L : m->bottom) {
+    cudaFree(L.W);
+    cudaFree(L.bias);
+  }
+  for (auto& L : m->top) {
+    cudaFree(L.W);
+    cudaFree(L.bias);
+  }
+  cudaFree(m->w_last);
+  cudaFree(m->tables);
+  cudaFree(m->d_tab_off);
+  cudaFree(m->d_rows);
+  for (auto& e : m->prof_events) {
+    cudaEventDestroy(e.a);
+    cudaEventDestroy(e.b);
+  }
+  for (auto e : m->prof_pool) cudaEventDestroy(e);
+  dist_destroy(m);
+  delete m;
+}
+
+void rec_model_destroy(rec_model_t m) { free_model(m); }
+
+#define ALLOC(ptr, bytes)                                                            \
+  do {                                                                               \
+    cudaError_t _e = cudaMalloc(reinterpret_cast<void**>(&(ptr)), (bytes));          \
+    if (_e != cudaSuccess) {                                                         \
+      set_error("cudaMalloc of %zu bytes for %s failed: %s", (size_t)(bytes), #ptr,  \
+                cudaGetErrorString(_e));                                             \
+      free_model(m);                                                                 \
+      return REC_E_OOM;                                                              \
+    }                                                                                \
+  } while (0)
+
+#define CHECK_CUDA_CREATE(call)                 \
+  do {                                          \
+    cudaError_t _e = (call);                    \
+    if (_e != cudaSuccess) {                    \
+      rec_status _s = cuda_fail(_e, #call);     \
+      free_model(m);                            \
+      return _s;                                \
+    }                                           \
+  } while (0)
+
+rec_status rec_model_create(const rec_model_desc* d, rec_model_t* out) {
+  if (!d || !out) {
+    set_error("desc and out must be non-null");
+    return REC_E_INVALID_ARG;
+  }
+  *out = nullptr;
+  // ---------------------------------------------------------------- validation
+  if (d->num_tables < 1 || d->num_tables > 4096) {
+    set_error("num_tables = %d must be in [1, 4096]", d->num_tables);
+    return REC_E_INVALID_ARG;
+  }
+  if (!d->rows) {
+    set_error("rows must be non-null");
+    return REC_E_INVALID_ARG;
+  }
+  for (int t = 0; t < d->num_tables; ++t) {
+    if (d->rows[t] < 1) {
+      set_error("rows[%d] = %lld must be >= 1", t, (long long)d->rows[t]);
+      return REC_E_INVALID_ARG;
+    }
+    if (d->rows[t] >= (int64_t(1) << 31)) {
+      set_error("rows[%d] = %lld must be < 2^31 (int32 indices, R18)", t, (long long)d->rows[t]);
+      return REC_E_UNSUPPORTED;
+    }
+  }
+  if (d->dim <= 0 || d->dim % 4 != 0 || d->dim > 128) {
+    set_error("dim = %d must be a positive multiple of 4 and <= 128", d->dim);
+    return d->dim <= 0 ? REC_E_INVALID_ARG : REC_E_UNSUPPORTED;
+  }
+  if (!d->bottom_widths || d->n_bottom < 2) {
+    set_error("bottom_widths must list >= 2 widths (input first, R3)");
+    return REC_E_INVALID_ARG;
+  }
+  if (!d->top_widths || d->n_top < 2) {
+    set_error("top_widths must list >= 2 widths ending in 1 (R3)");
+    return REC_E_INVALID_ARG;
+  }
+  for (int i = 0; i < d->n_bottom; ++i)
+    if (d->bottom_widths[i] < 1 || d->bottom_widths[i] > 16384) {
+      set_error("bottom_widths[%d] = %d out of [1, 16384]", i, d->bottom_widths[i]);
+      return REC_E_INVALID_ARG;
+    }
+  for (int i = 0; i < d->n_top; ++i)
+    if (d->top_widths[i] < 1 || d->top_widths[i] > 16384) {
+      set_error("top_widths[%d] = %d out of [1, 16384]", i, d->top_widths[i]);
+      return REC_E_INVALID_ARG;
+    }
+  if (d->bottom_widths[d->n_bottom - 1] != d->dim) {
+    set_error("dim = %d must equal bottom_widths[n_bottom-1] = %d (dot interaction, R4)", d->dim,
+              d->bottom_widths[d->n_bottom - 1]);
+    return REC_E_INVALID_ARG;
+  }
+  if (d->top_widths[d->n_top - 1] != 1) {
+    set_error("top_widths[n_top-1] = %d must be 1 (CTR output)", d->top_widths[d->n_top - 1]);
+    return REC_E_INVALID_ARG;
+  }
+  if (d->top_widths[d->n_top - 2] > 256) {
+    set_error("top_widths[n_top-2] = %d must be <= 256 (width-1 layer fused in one N tile)",
+              d->top_widths[d->n_top - 2]);
+    return REC_E_UNSUPPORTED;
+  }
+  if (d->pooling_lo < 0 || d->pooling_hi < d->pooling_lo || d->pooling_hi > 65536) {
+    set_error("pooling_lo = %d, pooling_hi = %d must satisfy 0 <= lo <= hi <= 65536",
+              d->pooling_lo, d->pooling_hi);
+    return REC_E_INVALID_ARG;
+  }
+  if (d->max_batch < 1 || d->streams < 1 || d->streams > 64) {
+    set_error("max_batch = %d must be >= 1 and streams = %d in [1, 64]", d->max_batch, d->streams);
+    return REC_E_INVALID_ARG;
+  }
+  if (d->value_mode != REC_VALUES_INT8_EXACT && d->value_mode != REC_VALUES_FP32) {
+    set_error("value_mode = %d unknown", d->value_mode);
+    return REC_E_INVALID_ARG;
+  }
+  if (d->index_dist != REC_INDEX_UNIFORM && d->index_dist != REC_INDEX_SKEW2) {
+    set_error("index_dist = %d unknown", d->index_dist);
+    return REC_E_INVALID_ARG;
+  }
+  if (d->world < 1 || d->rank < 0 || d->rank >= d->world) {
+    set_error("rank = %d / world = %d invalid", d->rank, d->world);
+    return REC_E_INVALID_ARG;
+  }
+  if (d->shard < REC_SHARD_REPLICA || d->shard > REC_SHARD_ROW) {
+    set_error("shard = %d unknown", d->shard);
+    return REC_E_INVALID_ARG;
+  }
+  const int64_t idx_cap = int64_t(d->num_tables) * d->max_batch * (d->pooling_hi > 0 ? d->pooling_hi : 1);
+  if (idx_cap >= (int64_t(1) << 31)) {
+    set_error("num_tables * max_batch * pooling_hi = %lld must be < 2^31", (long long)idx_cap);
+    return REC_E_UNSUPPORTED;
+  }
+  // ---------------------------------------------------------------- device
+  int ndev = 0;
+  cudaError_t ce = cudaGetDeviceCount(&ndev);
+  if (ce != cudaSuccess || ndev == 0) {
+    set_error("no CUDA device available (%s); this library has no CPU fallback",
+              ce == cudaSuccess ? "0 devices" : cudaGetErrorString(ce));
+    cudaGetLastError();
+    return REC_E_CUDA;
+  }
+  if (d->device < 0 || d->device >= ndev) {
+    set_error("device = %d out of [0, %d)", d->device, ndev);
+    return REC_E_INVALID_ARG;
+  }
+  REC_CUDA(cudaSetDevice(d->device));
+  cudaDeviceProp prop;
+  REC_CUDA(cudaGetDeviceProperties(&prop, d->device));
+  if (prop.major != 10) {
+    set_error("device %d is sm_%d%d; this library is built for sm_100a only", d->device,
+              prop.major, prop.minor);
+    return REC_E_CUDA;
+  }
+  gemm_prepare();
+
+  rec_model_s* m = new rec_model_s();
+  m->T = d->num_tables;
+  m->D = d->dim;
+  m->rows.assign(d->rows, d->rows + d->num_tables);
+  m->bottom_w.assign(d->bottom_widths, d->bottom_widths + d->n_bottom);
+  m->top_w.assign(d->top_widths, d->top_widths + d->n_top);
+  m->F = m->bottom_w[0];
+  m->Fpad = pad8(m->F);
+  m->lo = d->pooling_lo;
+  m->hi = d->pooling_hi;
+  m->top_shift = d->top_shift;
+  m->value_mode = d->value_mode;
+  m->index_dist = d->index_dist;
+  m->max_batch = d->max_batch;
+  m->nstreams = d->streams;
+  m->device = d->device;
+  m->shard = d->shard;
+  m->rank = d->rank;
+  m->world = d->world;
+  m->seed = d->seed;
+  m->k0 = static_cast<uint32_t>(d->seed & 0xFFFFFFFFull);
+  m->k1 = static_cast<uint32_t>(d->seed >> 32);
+  m->l2_persist_bytes = d->l2_persist_bytes;
+  // s = round(log2(0.577 sqrt(mean L)))  (G4, R24)
+  {
+    const double L = 0.5 * (d->pooling_lo + d->pooling_hi);
+    m->emb_shift = L > 0 ? static_cast<int>(std::lround(std::log2(0.577 * std::sqrt(L)))) : 0;
+  }
+  const int T = m->T, D = m->D;
+
+  // ---------------------------------------------------------------- tables
+  bool equal = true;
+  for (int t = 1; t < T; ++t) equal = equal && (m->rows[t] == m->rows[0]);
+  m->interleaved = equal;
+  m->tab_off.resize(T);
+  int64_t total_rows = 0;
+  for (int t = 0; t < T; ++t) total_rows += m->rows[t];
+  if (equal) {
+    // row r of table t at (r*T + t)*D: hot low rows of ALL tables form one contiguous
+    // prefix, which an L2 persisting window can cover (P:556-557 hot-embedding residue)
+    m->row_stride = int64_t(T) * D;
+    for (int t = 0; t < T; ++t) m->tab_off[t] = int64_t(t) * D;
+  } else {
+    m->row_stride = D;
+    int64_t acc = 0;
+    for (int t = 0; t < T; ++t) {
+      m->tab_off[t] = acc * D;
+      acc += m->rows[t];
+    }
+  }
+  m->table_bytes = static_cast<size_t>(total_rows) * D * sizeof(float);
+  ALLOC(m->tables, m->table_bytes);
+  ALLOC(m->d_tab_off, sizeof(int64_t) * T);
+  ALLOC(m->d_rows, sizeof(int64_t) * T);
+  CHECK_CUDA_CREATE(cudaMemcpy(m->d_tab_off, m->tab_off.data(), sizeof(int64_t) * T, cudaMemcpyHostToDevice));
+  CHECK_CUDA_CREATE(cudaMemcpy(m->d_rows, m->rows.data(), sizeof(int64_t) * T, cudaMemcpyHostToDevice));
+  for (int t = 0; t < T; ++t)
+    launch_init_table(m->tables + m->tab_off[t], m->rows[t], D, m->row_stride, t, m->k0, m->k1,
+                      m->emb_shift, m->value_mode, 0);
+  CHECK_CUDA_CREATE(cudaGetLastError());
+
+  // ---------------------------------------------------------------- MLP weights (G5)
+  auto wexp = [](int fan_in) {
+    return static_cast<int>(std::lround(std::log2(std::sqrt(3.0 / fan_in))));
+  };
+  auto make_layer = [&](int K, int N, int layer_id, int extra_shift, rec::Layer& L) -> rec_status {
+    L.K = K;
+    L.Kpad = pad8(K);
+    L.N = N;
+    L.Npad = pad8(N);
+    L.bn = gemm_bn(N);
+    L.layer_id = layer_id;
+    L.exp = -7 + wexp(K) - extra_shift;
+    if (cudaMalloc(reinterpret_cast<void**>(&L.W), sizeof(__nv_bfloat16) * N * L.Kpad) != cudaSuccess ||
+        cudaMalloc(reinterpret_cast<void**>(&L.bias), sizeof(float) * N) != cudaSuccess) {
+      set_error("cudaMalloc of layer %d weights failed", layer_id);
+      return REC_E_OOM;
+    }
+    launch_init_layer(L.W, L.bias, N, K, L.Kpad, layer_id, L.exp, m->k0, m->k1, 0);
+    if (!encode_tmap_bf16(&L.tmap_w, L.W, N, K, L.Kpad, L.bn)) {
+      set_error("cuTensorMapEncodeTiled failed for layer %d weights", layer_id);
+      return REC_E_CUDA;
+    }
+    return REC_OK;
+  };
+  const int nbl = d->n_bottom - 1;
+  m->bottom.resize(nbl);
+  for (int l = 0; l < nbl; ++l) {
+    rec_status st = make_layer(m->bottom_w[l], m->bottom_w[l + 1], l, 0, m->bottom[l]);
+    if (st != REC_OK) {
+      free_model(m);
+      return st;
+    }
+  }
+  m->Ktop = D + T * (T + 1) / 2;
+  m->Ktop_pad = pad8(m->Ktop);
+  std::vector<int> tw;
+  tw.push_back(m->Ktop);
+  for (int v : m->top_w) tw.push_back(v);
+  const int ntl = d->n_top - 1;  // GEMM layers (the width-1 output layer is an epilogue)
+  m->top.resize(ntl);
+  for (int j = 0; j < ntl; ++j) {
+    rec_status st = make_layer(tw[j], tw[j + 1], TOP_LAYER_BASE + j, j == 0 ? m->top_shift : 0, m->top[j]);
+    if (st != REC_OK) {
+      free_model(m);
+      return st;
+    }
+  }
+  {
+    const int Kf = tw[ntl];
+    ALLOC(m->w_last, sizeof(float) * (Kf + 1));
+    const int ef = -7 + wexp(Kf) - (ntl == 0 ? m->top_shift : 0);
+    launch_init_final(m->w_last, m->w_last + Kf, Kf, TOP_LAYER_BASE + ntl, ef, m->k0, m->k1, 0);
+    CHECK_CUDA_CREATE(cudaMemcpy(&m->b_last, m->w_last + Kf, sizeof(float), cudaMemcpyDeviceToHost));
+  }
+  m->hmax = 8;
+  for (int l = 1; l < d->n_bottom - 1; ++l) m->hmax = std::max(m->hmax, pad8(m->bottom_w[l]));
+  for (int j = 0; j < d->n_top - 2; ++j) m->hmax = std::max(m->hmax, pad8(m->top_w[j]));
+
+  // ---------------------------------------------------------------- workspaces
+  const int cap = m->max_batch;
+  m->ws.resize(m->nstreams);
+  for (int s = 0; s < m->nstreams; ++s) {
+    rec::Workspace& w = m->ws[s];
+    w.cap = cap;
+    w.idx_cap = idx_cap;
+    CHECK_CUDA_CREATE(cudaStreamCreateWithFlags(&w.stream, cudaStreamNonBlocking));
+    CHECK_CUDA_CREATE(cudaEventCreateWithFlags(&w.pin_free, cudaEventDisableTiming));
+    ALLOC(w.indices, sizeof(int) * (idx_cap > 0 ? idx_cap : 1));
+    ALLOC(w.offsets, sizeof(int) * (int64_t(T) * cap + 1));
+    ALLOC(w.segs, sizeof(int4) * cap);
+    ALLOC(w.rowq, sizeof(int) * cap);
+    ALLOC(w.rowi, sizeof(int) * cap);
+    ALLOC(w.dense_f32, sizeof(float) * int64_t(cap) * m->F);
+    ALLOC(w.dense_bf, sizeof(__nv_bfloat16) * int64_t(cap) * m->Fpad);
+    ALLOC(w.X, sizeof(float) * int64_t(cap) * (T + 1) * D);
+    ALLOC(w.A_top, sizeof(__nv_bfloat16) * int64_t(cap) * m->Ktop_pad);
+    ALLOC(w.h[0], sizeof(__nv_bfloat16) * int64_t(cap) * m->hmax);
+    ALLOC(w.h[1], sizeof(__nv_bfloat16) * int64_t(cap) * m->hmax);
+    ALLOC(w.ctr, sizeof(float) * cap);
+    ALLOC(w.logit, sizeof(float) * cap);
+    ALLOC(w.flag, sizeof(int));
+    CHECK_CUDA_CREATE(cudaMemset(w.flag, 0, sizeof(int)));
+    CHECK_CUDA_CREATE(cudaMemset(w.dense_bf, 0, sizeof(__nv_bfloat16) * int64_t(cap) * m->Fpad));
+    CHECK_CUDA_CREATE(cudaMemset(w.A_top, 0, sizeof(__nv_bfloat16) * int64_t(cap) * m->Ktop_pad));
+    CHECK_CUDA_CREATE(cudaMemset(w.h[0], 0, sizeof(__nv_bfloat16) * int64_t(cap) * m->hmax));
+    CHECK_CUDA_CREATE(cudaMemset(w.h[1], 0, sizeof(__nv_bfloat16) * int64_t(cap) * m->hmax));
+    CHECK_CUDA_CREATE(cudaMallocHost(reinterpret_cast<void**>(&w.flag_host), sizeof(int)));
+    w.pin_bytes = sizeof(int) * (int64_t(T) * cap + 1) + sizeof(int) * idx_cap +
+                  sizeof(float) * int64_t(cap) * m->F + sizeof(int4) * cap + 4096;
+    if (cudaMallocHost(reinterpret_cast<void**>(&w.pin), w.pin_bytes) != cudaSuccess) {
+      set_error("cudaMallocHost of %zu pinned staging bytes failed", w.pin_bytes);
+      free_model(m);
+      return REC_E_OOM;
+    }
+    CHECK_CUDA_CREATE(cudaEventRecord(w.pin_free, w.stream));
+    // A operand tensor maps + outputs of every GEMM layer on this workspace
+    w.tmap_a_bottom.resize(nbl);
+    w.out_bottom.resize(nbl);
+    for (int l = 0; l < nbl; ++l) {
+      const void* a_base = l == 0 ? static_cast<void*>(w.dense_bf) : static_cast<void*>(w.h[(l - 1) & 1]);
+      const int K = m->bottom[l].K;
+      const int ld = l == 0 ? m->Fpad : m->bottom[l - 1].Npad;
+      if (!encode_tmap_bf16(&w.tmap_a_bottom[l], a_base, cap, K, ld, 128)) {
+        set_error("cuTensorMapEncodeTiled failed (bottom layer %d activations)", l);
+        free_model(m);
+        return REC_E_CUDA;
+      }
+      w.out_bottom[l] = (l == nbl - 1) ? static_cast<void*>(w.X) : static_cast<void*>(w.h[l & 1]);
+    }
+    w.tmap_a_top.resize(ntl);
+    w.out_top.resize(ntl);
+    for (int j = 0; j < ntl; ++j) {
+      const void* a_base = j == 0 ? static_cast<void*>(w.A_top) : static_cast<void*>(w.h[(j - 1) & 1]);
+      const int K = m->top[j].K;
+      const int ld = j == 0 ? m->Ktop_pad : m->top[j - 1].Npad;
+      if (!encode_tmap_bf16(&w.tmap_a_top[j], a_base, cap, K, ld, 128)) {
+        set_error("cuTensorMapEncodeTiled failed (top layer %d activations)", j);
+        free_model(m);
+        return REC_E_CUDA;
+      }
+      w.out_top[j] = (j == ntl - 1) ? nullptr : static_cast<void*>(w.h[j & 1]);
+    }
+  }
+  CHECK_CUDA_CREATE(cudaDeviceSynchronize());
+
+  // L2 persisting window over the hot row prefix (interleaved layout only)
+  if (m->l2_persist_bytes > 0) {
+    if (!m->interleaved) {
+      set_error("l2_persist_bytes needs equal rows per table (interleaved arena)");
+      free_model(m);
+      return REC_E_UNSUPPORTED;
+    }
+    size_t win = std::min<size_t>(static_cast<size_t>(m->l2_persist_bytes), m->table_bytes);
+    win = std::min<size_t>(win, static_cast<size_t>(prop.accessPolicyMaxWindowSize));
+    CHECK_CUDA_CREATE(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize,
+                                         std::min<size_t>(win, prop.persistingL2CacheMaxSize)));
+    for (auto& w : m->ws) {
+      cudaStreamAttrValue v{};
+      v.accessPolicyWindow.base_ptr = m->tables;
+      v.accessPolicyWindow.num_bytes = win;
+      v.accessPolicyWindow.hitRatio = 1.0f;
+      v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+      v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+      CHECK_CUDA_CREATE(cudaStreamSetAttribute(w.stream, cudaStreamAttributeAccessPolicyWindow, &v));
+    }
+  }
+
+  if (m->world > 1 && m->shard != REC_SHARD_REPLICA) {
+    rec_status st = dist_init(m, d->nccl_id);
+    if (st != REC_OK) {
+      free_model(m);
+      return st;
+    }
+  }
+  *out = m;
+  return REC_OK;
+}
+
+rec_status rec_query(rec_model_t m, const float* dense, const int32_t* indices,
+                     const int32_t* offsets, int32_t batch, float* ctr) {
+  return query_impl(m, dense, indices, offsets, batch, ctr, nullptr, nullptr);
+}
+
+rec_status rec_query_debug(rec_model_t m, const float* dense, const int32_t* indices,
+                           const int32_t* offsets, int32_t batch, float* ctr, float* pooled,
+                           float* logits) {
+  return query_impl(m, dense, indices, offsets, batch, ctr, pooled, logits);
+}
+
+rec_status rec_query_async(rec_model_t m, int32_t slot, const float* dense, const int32_t* indices,
+                           const int32_t* offsets, int64_t nnz, int32_t batch, float* ctr) {
+  if (!m || !dense || !indices || !offsets || !ctr) {
+    set_error("null argument");
+    return REC_E_INVALID_ARG;
+  }
+  if (slot < 0 || slot >= m->nstreams) {
+    set_error("slot = %d out of [0, %d)", slot, m->nstreams);
+    return REC_E_INVALID_ARG;
+  }
+  if (batch <= 0 || batch > m->max_batch) {
+    set_error("batch = %d must be in [1, max_batch = %d]", batch, m->max_batch);
+    return REC_E_INVALID_ARG;
+  }
+  if (nnz < 0) {
+    set_error("nnz = %lld must be >= 0", (long long)nnz);
+    return REC_E_INVALID_ARG;
+  }
+  REC_CUDA(cudaSetDevice(m->device));
+  Workspace& w = m->ws[slot];
+  launch_dense_to_bf16(dense, batch, m->F, m->Fpad, w.dense_bf, w.stream);
+  m->launches += 1;
+  return forward_enqueue(m, w, indices, offsets, batch, ctr, w.logit);
+}
+
+rec_status rec_synth_query_async(rec_model_t m, int32_t slot, const int32_t* segs, int32_t nseg,
+                                 float* ctr) {
+  if (!m || !ctr) {
+    set_error("null argument");
+    return REC_E_INVALID_ARG;
+  }
+  if (slot < 0 || slot >= m->nstreams) {
+    set_error("slot = %d out of [0, %d)", slot, m->nstreams);
+    return REC_E_INVALID_ARG;
+  }
+  REC_CUDA(cudaSetDevice(m->device));
+  Workspace& w = m->ws[slot];
+  int B = 0;
+  rec_status st = synth_inputs(m, w, segs, nseg, &B, nullptr);
+  if (st != REC_OK) return st;
+  return forward_enqueue(m, w, w.indices, w.offsets, B, ctr, w.logit);
+}
+
+rec_status rec_sync(rec_model_t m, int32_t slot) {
+  if (!m || slot < 0 || slot >= m->nstreams) {
+    set_error("bad model or slot");
+    return REC_E_INVALID_ARG;
+  }
+  REC_CUDA(cudaSetDevice(m->device));
+  return sync_ws(m->ws[slot]);
+}
+
+void* rec_stream_handle(rec_model_t m, int32_t slot) {
+  if (!m || slot < 0 || slot >= m->nstreams) return nullptr;
+  return m->ws[slot].stream;
+}
+
+rec_status rec_gen_batch(rec_model_t m, const int32_t* segs, int32_t nseg, int32_t* indices,
+                         int32_t* offsets, float* dense) {
+  if (!m || !segs || !indices || !offsets || !dense) {
+    set_error("null argument");
+    return REC_E_INVALID_ARG;
+  }
+  REC_CUDA(cudaSetDevice(m->device));
+  Workspace& w = m->ws[0];
+  int B = 0;
+  rec_status st = synth_inputs(m, w, segs, nseg, &B, w.dense_f32);
+  if (st != REC_OK) return st;
+  cudaStream_t s = w.stream;
+  const int nb = m->T * B;
+  REC_CUDA(cudaMemcpyAsync(offsets, w.offsets, sizeof(int) * (nb + 1), cudaMemcpyDefault, s));
+  int nnz = 0;
+  REC_CUDA(cudaMemcpyAsync(w.flag_host, w.offsets + nb, sizeof(int), cudaMemcpyDeviceToHost, s));
+  REC_CUDA(cudaStreamSynchronize(s));
+  nnz = *w.flag_host;
+  *w.flag_host = 0;
+  REC_CUDA(cudaMemcpyAsync(indices, w.indices, sizeof(int) * nnz, cudaMemcpyDefault, s));
+  REC_CUDA(cudaMemcpyAsync(dense, w.dense_f32, sizeof(float) * B * m->F, cudaMemcpyDefault, s));
+  REC_CUDA(cudaStreamSynchronize(s));
+  return REC_OK;
+}
+
+rec_status rec_profile(rec_model_t m, int32_t enable) {
+  if (!m) {
+    set_error("null model");
+    return REC_E_INVALID_ARG;
+  }
+  for (auto& w : m->ws) REC_CUDA(cudaStreamSynchronize(w.stream));
+  prof_collect(m);
+  for (int k = 0; k < 4; ++k) {
+    m->prof_ms[k] = 0;
+    m->prof_n[k] = 0;
+  }
+  m->prof = enable != 0;
+  return REC_OK;
+}
+
+rec_status rec_profile_read(rec_model_t m, int32_t kernel, double* total_ms, int64_t* launches) {
+  if (!m || kernel < 0 || kernel > 4 || !total_ms || !launches) {
+    set_error("bad argument");
+    return REC_E_INVALID_ARG;
+  }
+  if (kernel == 4) {  // all kernels launched by this handle (count only)
+    *total_ms = 0.0;
+    *launches = m->launches;
+    return REC_OK;
+  }
+  for (auto& w : m->ws) REC_CUDA(cudaStreamSynchronize(w.stream));
+  prof_collect(m);
+  *total_ms = m->prof_ms[kernel];
+  *launches = m->prof_n[kernel];
+  return REC_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,114 @@
+// model.h — internal host-side model state behind the C ABI (include/rec.h).
+#pragma once
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/rec.h"
+#include "kernels.h"
+
+namespace rec {
+
+void set_error(const char* fmt, ...);
+rec_status cuda_fail(cudaError_t e, const char* what);
+
+#define REC_CUDA(call)                                   \
+  do {                                                   \
+    cudaError_t _e = (call);                             \
+    if (_e != cudaSuccess) return cuda_fail(_e, #call);  \
+  } while (0)
+
+struct Layer {
+  int K = 0, Kpad = 0, N = 0, Npad = 0, bn = 0;  // true fan-in, padded fan-in, fan-out
+  int layer_id = 0, exp = 0;
+  __nv_bfloat16* W = nullptr;                    // [N][Kpad] bf16
+  float* bias = nullptr;                         // [N]
+  CUtensorMap tmap_w;
+};
+
+// One per co-located stream: the buffers a batch needs on that stream.
+struct Workspace {
+  cudaStream_t stream = nullptr;
+  int cap = 0;                       // max items
+  int64_t idx_cap = 0;               // max indices
+  int* indices = nullptr;            // [idx_cap]
+  int* offsets = nullptr;            // [T*cap+1]
+  int4* segs = nullptr;              // [cap] device segment list
+  int* rowq = nullptr;               // [cap]
+  int* rowi = nullptr;               // [cap]
+  float* dense_f32 = nullptr;        // [cap][F] (caller dense staging / gen output)
+  __nv_bfloat16* dense_bf = nullptr; // [cap][Fpad]
+  float* X = nullptr;                // [cap][T+1][D]
+  __nv_bfloat16* A_top = nullptr;    // [cap][Ktop_pad]
+  __nv_bfloat16* h[2] = {nullptr, nullptr};  // hidden ping-pong [cap][hmax]
+  float* ctr = nullptr;              // [cap]
+  float* logit = nullptr;            // [cap]
+  int* flag = nullptr;               // device error flags (bit0 OOB, bit1 offsets)
+  int* flag_host = nullptr;          // pinned mirror
+  uint8_t* pin = nullptr;            // pinned staging
+  size_t pin_bytes = 0;
+  cudaEvent_t pin_free = nullptr;    // last H2D out of `pin` completed
+  std::vector<CUtensorMap> tmap_a_bottom, tmap_a_top;  // A operand per GEMM layer
+  std::vector<void*> out_bottom, out_top;              // output buffer per GEMM layer
+};
+
+struct ProfEvent {
+  int kernel;
+  cudaEvent_t a, b;
+};
+
+}  // namespace rec
+
+struct rec_model_s {
+  // description
+  int T = 0, D = 0, F = 0, Fpad = 0, lo = 0, hi = 0;
+  std::vector<int64_t> rows;
+  std::vector<int> bottom_w, top_w;
+  int top_shift = 0, value_mode = 0, index_dist = 0, max_batch = 0, nstreams = 0, device = 0;
+  int shard = 0, rank = 0, world = 1;
+  uint64_t seed = 0;
+  uint32_t k0 = 0, k1 = 0;
+  int emb_shift = 0;
+  int64_t l2_persist_bytes = 0;
+  // embedding arena
+  float* tables = nullptr;
+  size_t table_bytes = 0;
+  bool interleaved = false;
+  int64_t row_stride = 0;              // floats between consecutive rows of one table
+  std::vector<int64_t> tab_off;        // floats, start of row 0 of table t
+  int64_t* d_tab_off = nullptr;
+  int64_t* d_rows = nullptr;
+  // MLP
+  std::vector<rec::Layer> bottom, top;  // top excludes the width-1 output layer
+  float* w_last = nullptr;
+  float b_last = 0.f;
+  int Ktop = 0, Ktop_pad = 0, hmax = 0;
+  // streams + workspaces
+  std::vector<rec::Workspace> ws;
+  // profiling
+  bool prof = false;
+  std::vector<rec::ProfEvent> prof_events;
+  std::vector<cudaEvent_t> prof_pool;
+  double prof_ms[4] = {0, 0, 0, 0};
+  int64_t prof_n[4] = {0, 0, 0, 0};
+  int64_t launches = 0;                // kernels launched by this handle (all streams)
+  // distributed (sharded modes)
+  void* nccl_comm = nullptr;
+};
+
+namespace rec {
+// Launch the forward of `batch` items on workspace `w` whose inputs are already in
+// w.indices / w.offsets / w.dense_bf (or caller device pointers).  ctr_out: device.
+rec_status forward_enqueue(rec_model_s* m, Workspace& w, const int* indices, const int* offsets,
+                           int batch, float* ctr_out, float* logit_out);
+// Device-synthesised inputs for a segment list (host), enqueued on w.stream.
+rec_status synth_enqueue(rec_model_s* m, Workspace& w, const int32_t* segs, int nseg, int* batch_out);
+cudaEvent_t prof_begin(rec_model_s* m, Workspace& w);
+rec_status dist_init(rec_model_s* m, const void* nccl_id);   // dist.cu
+void dist_destroy(rec_model_s* m);
+void prof_end(rec_model_s* m, Workspace& w, int kernel, cudaEvent_t a);
+}  // namespace rec

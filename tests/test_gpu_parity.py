@@ -1,0 +1,216 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Bars (BASELINE.json north_star):
+  * synthetic indices / offsets / dense: bit-exact
+  * SLS pooled fp32: bit-exact vs the oracle's fp32-sequential order (the kernel
+    accumulates each bag in index order), and in int8-exact mode bit-exact vs fp64;
+    fp32 value mode additionally within 1e-5 * sum|x| of the fp64 sum
+  * CTR: |gpu - oracle| <= 2e-2 absolute, with the oracle's non-vacuity guard
+Sizes span several 128-row GEMM tiles with a ragged tail, plus B = 1 and full-size
+(1M-row) tables on sampled items.
+"""
+import numpy as np
+import pytest
+
+import workloads as W
+from oracle import forward as fw, gen
+
+pytestmark = pytest.mark.gpu
+
+CTR_TOL = 2e-2
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _built():
+    import __graft_entry__
+    __graft_entry__.build()
+
+
+def _model(cfg, **kw):
+    from paper_2203_07424_b200 import RecModel
+    return RecModel(cfg, seed=1, **kw)
+
+
+def _oracle_pooled_fp32(cfg, ind, off, B):
+    shift = gen.emb_shift(cfg.pooling_lo, cfg.pooling_hi)
+    f = lambda t, r: gen.table_values(1, t, r, cfg.dim, shift, cfg.value_mode)
+    return fw.sls(f, cfg.num_tables, B, cfg.dim, ind, off, fp32_sequential=True)
+
+
+CASES = [
+    ("tiny", W.TINY, 64),
+    ("tiny_ragged", W.TINY, 300),
+    ("rmc1", W.small_variant(W.RMC1, 20000), 300),
+    ("rmc2", W.small_variant(W.RMC2, 4096), 200),
+    ("rmc3", W.small_variant(W.RMC3, 20000), 257),
+    ("rmc1_var", W.small_variant(W.RMC1, 20000).with_(pooling_lo=20, pooling_hi=160), 129),
+    ("rmc1_skew", W.small_variant(W.RMC1, 20000).with_(index_dist=W.INDEX_SKEW2), 64),
+    ("rmc1_fp32", W.small_variant(W.RMC1, 20000).with_(value_mode=W.REC_VALUES_FP32), 150),
+    ("one_hot", W.small_variant(W.TINY, 5000).with_(pooling_lo=1, pooling_hi=1), 77),
+]
+
+
+@pytest.mark.parametrize("name,cfg,B", CASES, ids=[c[0] for c in CASES])
+def test_gen_batch_bit_exact(name, cfg, B):
+    m = _model(cfg, max_batch=B)
+    segs = W.random_segments(B, seed=21)
+    ind, off, dense = gen.gen_batch(cfg, 1, segs)
+    gi, go, gd = m.rec_gen_batch(segs)
+    assert np.array_equal(go, off)
+    assert np.array_equal(gi, ind)
+    assert np.array_equal(gd, dense)
+
+
+@pytest.mark.parametrize("name,cfg,B", CASES, ids=[c[0] for c in CASES])
+def test_forward_parity(name, cfg, B):
+    m = _model(cfg, max_batch=B)
+    segs = W.random_segments(B, seed=22)
+    ind, off, dense = gen.gen_batch(cfg, 1, segs)
+    ctr = np.zeros(B, np.float32)
+    pooled = np.zeros((B, cfg.num_tables, cfg.dim), np.float32)
+    logit = np.zeros(B, np.float32)
+    m.rec_query_debug(dense, ind, off, B, ctr, pooled=pooled, logits=logit)
+    exp = fw.forward(cfg, 1, dense, ind, off, return_all=True)
+    # SLS: bit-exact against the fp32-sequential definition
+    assert np.array_equal(pooled, _oracle_pooled_fp32(cfg, ind, off, B))
+    if cfg.value_mode == W.REC_VALUES_INT8_EXACT:
+        assert np.array_equal(pooled.astype(np.float64), exp["pooled"])
+    else:
+        shift = gen.emb_shift(cfg.pooling_lo, cfg.pooling_hi)
+        absum = fw.sls(lambda t, r: np.abs(gen.table_values(1, t, r, cfg.dim, shift, 1)),
+                       cfg.num_tables, B, cfg.dim, ind, off)
+        assert np.all(np.abs(pooled - exp["pooled"]) <= 1e-5 * absum + 1e-30)
+    # CTR within 2e-2, non-vacuous
+    err = np.abs(ctr.astype(np.float64) - exp["ctr"])
+    assert err.max() <= CTR_TOL, (err.max(), np.argmax(err))
+    assert exp["logit"].std() > 0.5
+    # logits agree too (looser: bf16 hidden activations)
+    assert np.abs(logit - exp["logit"]).max() < 0.15
+
+
+def test_batch_one_and_batch_invariance():
+    cfg = W.small_variant(W.RMC1, 20000)
+    m = _model(cfg, max_batch=1024)
+    segs = W.random_segments(1024, seed=5)
+    ind, off, dense = gen.gen_batch(cfg, 1, segs)
+    full = np.zeros(1024, np.float32)
+    m.rec_query(dense, ind, off, 1024, full)
+    # the same items in batches of 1, 7 and 1024 produce identical CTR bits
+    q, it = gen.expand_segments(segs)
+    for d in (1, 7, 333):
+        for start in (0, 500, 1024 - d):
+            sub = np.array([[q[k], it[k], 1] for k in range(start, start + d)], np.int32)
+            i2, o2, d2 = gen.gen_batch(cfg, 1, sub)
+            c2 = np.zeros(d, np.float32)
+            m.rec_query(d2, i2, o2, d, c2)
+            assert np.array_equal(c2, full[start:start + d]), (d, start)
+
+
+def test_device_pointers_match_host():
+    import torch
+    cfg = W.small_variant(W.RMC2, 4096)
+    B = 130
+    m = _model(cfg, max_batch=B)
+    ind, off, dense = gen.gen_batch(cfg, 1, W.random_segments(B, seed=8))
+    c_host = np.zeros(B, np.float32)
+    m.rec_query(dense, ind, off, B, c_host)
+    dv = torch.from_numpy(dense).cuda()
+    iv = torch.from_numpy(ind).cuda()
+    ov = torch.from_numpy(off).cuda()
+    cv = torch.zeros(B, device="cuda")
+    m.rec_query(dv, iv, ov, B, cv)
+    assert np.array_equal(cv.cpu().numpy(), c_host)
+    # async path on a second stream slot gives the same bits
+    m2 = _model(cfg, max_batch=B, streams=2)
+    cv2 = torch.zeros(B, device="cuda")
+    m2.rec_query_async(1, dv, iv, ov, int(off[-1]), B, cv2)
+    m2.rec_sync(1)
+    assert np.array_equal(cv2.cpu().numpy(), c_host)
+
+
+def test_synth_query_matches_host_inputs():
+    import torch
+    cfg = W.small_variant(W.RMC3, 20000)
+    B = 300
+    m = _model(cfg, max_batch=B)
+    segs = W.random_segments(B, seed=9)
+    ind, off, dense = gen.gen_batch(cfg, 1, segs)
+    c_host = np.zeros(B, np.float32)
+    m.rec_query(dense, ind, off, B, c_host)
+    cv = torch.zeros(B, device="cuda")
+    m.rec_synth_query_async(0, segs, cv)
+    m.rec_sync(0)
+    assert np.array_equal(cv.cpu().numpy(), c_host)
+
+
+def test_edge_cases_empty_bags_duplicates_errors():
+    from paper_2203_07424_b200 import RecError
+    cfg = W.small_variant(W.TINY, 1000)
+    T, B, D = cfg.num_tables, 5, cfg.dim
+    m = _model(cfg, max_batch=8)
+    rng = np.random.default_rng(0)
+    lens = np.array([0, 3, 0, 1, 5] * T)
+    off = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+    ind = rng.integers(0, 1000, size=off[-1]).astype(np.int32)
+    ind[1:3] = ind[0] if off[-1] > 3 else ind[1:3]               # duplicates
+    dense = (rng.integers(-128, 128, size=(B, cfg.dense_dim)) / 128.0).astype(np.float32)
+    ctr = np.zeros(B, np.float32)
+    pooled = np.zeros((B, T, D), np.float32)
+    m.rec_query_debug(dense, ind, off, B, ctr, pooled=pooled)
+    exp = fw.forward(cfg, 1, dense, ind, off, return_all=True)
+    assert np.array_equal(pooled.astype(np.float64), exp["pooled"])
+    assert np.all(pooled[0] == 0) and np.all(pooled[2] == 0)
+    assert np.abs(ctr - exp["ctr"]).max() <= CTR_TOL
+    bad = ind.copy()
+    bad[2] = 1000                                                 # == rows: out of range
+    with pytest.raises(RecError) as ei:
+        m.rec_query(dense, bad, off, B, ctr)
+    assert ei.value.status == -2
+    bad[2] = -1
+    with pytest.raises(RecError) as ei:
+        m.rec_query(dense, bad, off, B, ctr)
+    assert ei.value.status == -2
+    boff = off.copy()
+    boff[3] = boff[2] - 1
+    with pytest.raises(RecError) as ei:
+        m.rec_query(dense, ind, boff, B, ctr)
+    assert ei.value.status == -3
+    with pytest.raises(RecError) as ei:
+        m.rec_query(dense, ind, off, 9, np.zeros(9, np.float32))   # > max_batch
+    assert ei.value.status == -1
+    # the model still works after errors
+    m.rec_query(dense, ind, off, B, ctr)
+
+
+def test_device_offsets_validation():
+    import torch
+    from paper_2203_07424_b200 import RecError
+    cfg = W.small_variant(W.TINY, 1000)
+    m = _model(cfg, max_batch=16)
+    ind, off, dense = gen.gen_batch(cfg, 1, W.random_segments(16, seed=3))
+    boff = off.copy()
+    boff[5] = boff[4] - 1
+    with pytest.raises(RecError) as ei:
+        m.rec_query(torch.from_numpy(dense).cuda(), torch.from_numpy(ind).cuda(),
+                    torch.from_numpy(boff).cuda(), 16, torch.zeros(16, device="cuda"))
+    assert ei.value.status == -3
+
+
+@pytest.mark.parametrize("name", ["rmc1", "rmc3"])
+def test_full_size_sampled(name):
+    """BASELINE sizes (1M rows/table, B = 1024, the bench launch configuration): sampled items."""
+    import torch
+    cfg = W.SHORT[name]
+    B = 1024
+    m = _model(cfg, max_batch=B)
+    segs = W.random_segments(B, seed=31)
+    cv = torch.zeros(B, device="cuda")
+    m.rec_synth_query_async(0, segs, cv)
+    m.rec_sync(0)
+    ctr = cv.cpu().numpy()
+    q, it = gen.expand_segments(segs)
+    pick = np.random.default_rng(0).choice(B, size=48, replace=False)
+    sub = np.array([[q[k], it[k], 1] for k in pick], np.int32)
+    i2, o2, d2 = gen.gen_batch(cfg, 1, sub)
+    exp = fw.forward(cfg, 1, d2, i2, o2)
+    assert np.abs(ctr[pick] - exp).max() <= CTR_TOL
