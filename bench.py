@@ -205,7 +205,7 @@ def run_ours(args):
     ctr = torch.zeros(d, device="cuda")
 
     def step(i):
-        model.rec_synth_query_async(0, batches[i % nb], ctr)
+        model.rec_synth_query_async(0, batches[i % nb], None)
 
     for i in range(args.warmup):
         step(i)

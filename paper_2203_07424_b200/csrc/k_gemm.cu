@@ -48,6 +48,8 @@ __global__ void __launch_bounds__(128, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
   const int nkb = (args.K + BK - 1) / BK;
+  const int M = args.dM ? *args.dM : args.M;  // device-side batch (graph replay)
+  if (m0 >= M) return;                        // whole CTA beyond the batch: nothing to do
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < stages; ++s) {
@@ -65,42 +67,49 @@ __global__ void __launch_bounds__(128, 1)
   sm100::tc_fence_after();
   const uint32_t tmem = *tslot;
 
-  if (warp == 0 && lane == 0) {
+  // Whole warps run the role loops (lane 0 issues), so no lane of a role warp spins on a
+  // barrier while its issuing lane still has work (divergent spinning stalls the issuer).
+  if (warp == 0) {
     // ---------------- TMA producer
     for (int kb = 0; kb < nkb; ++kb) {
       const int s = kb % stages, it = kb / stages;
       if (it > 0) sm100::mbar_wait(&empty[s], (it - 1) & 1);
-      uint8_t* sa = smem + s * STAGE_BYTES;
-      sm100::mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
-      sm100::tma_load_2d(sa, &tmap_a, &full[s], kb * BK, m0);
-      sm100::tma_load_2d(sa + A_STAGE_BYTES, &tmap_w, &full[s], kb * BK, n0);
+      if (lane == 0) {
+        uint8_t* sa = smem + s * STAGE_BYTES;
+        sm100::mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
+        sm100::tma_load_2d(sa, &tmap_a, &full[s], kb * BK, m0);
+        sm100::tma_load_2d(sa + A_STAGE_BYTES, &tmap_w, &full[s], kb * BK, n0);
+      }
+      __syncwarp();
     }
-  } else if (warp == 1 && lane == 0) {
+  } else if (warp == 1) {
     // ---------------- single-thread MMA issuer
     constexpr uint32_t idesc = sm100::idesc_bf16_f32(BM, BN);
     for (int kb = 0; kb < nkb; ++kb) {
       const int s = kb % stages, it = kb / stages;
       sm100::mbar_wait(&full[s], it & 1);
       sm100::tc_fence_after();
-      const uint32_t sa = sm100::smem_u32(smem + s * STAGE_BYTES);
-      const uint64_t da = sm100::umma_desc_sw128(sa);
-      const uint64_t db = sm100::umma_desc_sw128(sa + A_STAGE_BYTES);
+      if (lane == 0) {
+        const uint32_t sa = sm100::smem_u32(smem + s * STAGE_BYTES);
+        const uint64_t da = sm100::umma_desc_sw128(sa);
+        const uint64_t db = sm100::umma_desc_sw128(sa + A_STAGE_BYTES);
 #pragma unroll
-      for (int k = 0; k < BK / 16; ++k) {
-        // advance 16 bf16 = 32 B along K inside the 128-B swizzled row: +2 in addr>>4
-        sm100::mma_bf16_ss(tmem, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
+        for (int k = 0; k < BK / 16; ++k) {
+          // advance 16 bf16 = 32 B along K inside the 128-B swizzled row: +2 in addr>>4
+          sm100::mma_bf16_ss(tmem, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
+        }
+        sm100::mma_commit(&empty[s]);
+        if (kb == nkb - 1) sm100::mma_commit(done);
       }
-      sm100::mma_commit(&empty[s]);
+      __syncwarp();
     }
-    sm100::mma_commit(done);
   }
 
   // ---------------- epilogue: thread = row (TMEM lane warp*32 + lane)
   sm100::mbar_wait(done, 0);
-  __syncwarp();
   sm100::tc_fence_after();
   const int row = m0 + warp * 32 + lane;
-  const bool row_ok = row < args.M;
+  const bool row_ok = row < M;
   const uint32_t trow = tmem + (static_cast<uint32_t>(warp * 32) << 16);
   float dot = 0.f;
 #pragma unroll 1

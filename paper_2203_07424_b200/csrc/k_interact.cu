@@ -14,9 +14,11 @@
 
 namespace rec {
 
-__global__ void k_interact(const float* __restrict__ X, int B, int T, int D,
-                           __nv_bfloat16* __restrict__ A, int ld, int warps_per_cta) {
+__global__ void k_interact(const float* __restrict__ X, int B, const int* __restrict__ dB, int T,
+                           int D, __nv_bfloat16* __restrict__ A, int ld, int warps_per_cta) {
   extern __shared__ float sm[];
+  if (dB) B = *dB;
+  if (static_cast<int>(blockIdx.x) * warps_per_cta >= B) return;
   const int rows = T + 1, pitch = D + 1, npairs = T * (T + 1) / 2;
   uint8_t* pi = reinterpret_cast<uint8_t*>(sm);
   uint8_t* pj = pi + npairs;
@@ -51,8 +53,8 @@ __global__ void k_interact(const float* __restrict__ X, int B, int T, int D,
   }
 }
 
-void launch_interact(const float* X, int B, int T, int D, __nv_bfloat16* A_top, int ld_top,
-                     cudaStream_t s) {
+void launch_interact(const float* X, int B, const int* dB, int T, int D, __nv_bfloat16* A_top,
+                     int ld_top, cudaStream_t s) {
   if (B <= 0) return;
   const int npairs = T * (T + 1) / 2;
   const size_t per_warp = static_cast<size_t>(T + 1) * (D + 1) * sizeof(float);
@@ -66,7 +68,7 @@ void launch_interact(const float* X, int B, int T, int D, __nv_bfloat16* A_top, 
                          static_cast<int>(smem));
   int blocks = (B + wpc - 1) / wpc;
   if (blocks > 148 * 8) blocks = 148 * 8;
-  k_interact<<<blocks, 32 * wpc, smem, s>>>(X, B, T, D, A_top, ld_top, wpc);
+  k_interact<<<blocks, 32 * wpc, smem, s>>>(X, B, dB, T, D, A_top, ld_top, wpc);
 }
 
 }  // namespace rec

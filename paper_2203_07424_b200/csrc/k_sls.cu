@@ -16,27 +16,45 @@
 
 namespace rec {
 
-__device__ __forceinline__ float4 ldg_stream(const float4* p) {
+// Streaming 128-bit load of row `row` (address = base + row * stride_bytes, formed inside the
+// asm so no 64-bit address stays live per in-flight load; rows are never reused from L1).
+__device__ __forceinline__ float4 ldg_row(const float4* base, uint32_t row, uint32_t stride_bytes) {
   float4 v;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];"
-               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-               : "l"(p));
+  asm volatile(
+      "{\n\t.reg .u64 a;\n\t"
+      "mad.wide.u32 a, %4, %5, %6;\n\t"
+      "ld.global.nc.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [a];\n\t}"
+      : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+      : "r"(row), "r"(stride_bytes), "l"(base));
   return v;
 }
 
-// U = 128-bit row loads in flight per lane before they are accumulated.
-template <int LANES, int THREADS, int U = 8>
-__global__ void __launch_bounds__(THREADS) k_sls(const float* __restrict__ tables,
-                                                 const int64_t* __restrict__ tab_off,
-                                                 int64_t row_stride,
-                                                 const int64_t* __restrict__ rows,
-                                                 const int* __restrict__ indices,
-                                                 const int* __restrict__ offsets, int B, int T,
-                                                 int D, float* __restrict__ X, int x_stride,
-                                                 int x_slot0, int* __restrict__ flag) {
+// Per round a group consumes ROWS = IPL * LANES indices (IPL per lane, prefetched one round
+// ahead so the index load never sits in front of the row loads) and issues the row loads in
+// sub-batches of U = 8 independent 128-bit loads per lane before accumulating them in order.
+template <int LANES>
+struct SlsShape {
+  static constexpr int IPL = 1;
+  static constexpr int ROWS = IPL * LANES;
+  static constexpr int U = 8;  // 8 x 16 B in flight per lane keeps ~90 regs: 5 CTAs of 128/SM
+};
+
+template <int LANES, int THREADS>
+__global__ void __launch_bounds__(THREADS, 5) k_sls(const float* __restrict__ tables,
+                                                    const int64_t* __restrict__ tab_off,
+                                                    int64_t row_stride,
+                                                    const int64_t* __restrict__ rows,
+                                                    const int* __restrict__ indices,
+                                                    const int* __restrict__ offsets, int B,
+                                                    const int* __restrict__ dB, int T,
+                                                    int D, float* __restrict__ X, int x_stride,
+                                                    int x_slot0, int* __restrict__ flag) {
+  using S = SlsShape<LANES>;
   constexpr int GROUPS = THREADS / LANES;
   __shared__ int s_off[GROUPS + 1];
+  if (dB) B = *dB;  // device-side batch size (graph replay); grid sized for the capacity
   const int nbags = T * B;
+  if (static_cast<int>(blockIdx.x) * GROUPS >= nbags) return;
   const int g0 = blockIdx.x * GROUPS;
   for (int i = threadIdx.x; i <= GROUPS; i += THREADS) {
     const int g = min(g0 + i, nbags);
@@ -54,29 +72,44 @@ __global__ void __launch_bounds__(THREADS) k_sls(const float* __restrict__ table
   const bool active = (sub * 4) < D;
   const int col = active ? sub * 4 : 0;
   const float4* __restrict__ tab = reinterpret_cast<const float4*>(tables + toff + col);
-  const int64_t row_stride4 = row_stride / 4;
+  const uint32_t stride_bytes = static_cast<uint32_t>(row_stride * 4);
   const unsigned gmask = (LANES == 32) ? 0xffffffffu
                                        : (((1u << LANES) - 1u) << ((threadIdx.x & 31) & ~(LANES - 1)));
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
   bool oob = false;
-  for (int base = lo; base < hi; base += LANES) {
-    const int n = min(LANES, hi - base);
-    int my = (sub < n) ? __ldg(&indices[base + sub]) : 0;
-    if (sub < n && (my < 0 || static_cast<int64_t>(my) >= nrows)) {
-      oob = true;
-      my = 0;
+  int cur[S::IPL], nxt[S::IPL];
+#pragma unroll
+  for (int j = 0; j < S::IPL; ++j) {
+    const int p = lo + j * LANES + sub;
+    cur[j] = p < hi ? __ldg(&indices[p]) : 0;
+  }
+  for (int base = lo; base < hi; base += S::ROWS) {
+#pragma unroll
+    for (int j = 0; j < S::IPL; ++j) {  // prefetch the next round's indices
+      const int p = base + S::ROWS + j * LANES + sub;
+      nxt[j] = p < hi ? __ldg(&indices[p]) : 0;
     }
 #pragma unroll
-    for (int kk = 0; kk < LANES; kk += U) {
-      if (kk >= n) break;
-      float4 v[U];
+    for (int j = 0; j < S::IPL; ++j) {
+      const int p = base + j * LANES + sub;
+      if (p < hi && (cur[j] < 0 || static_cast<int64_t>(cur[j]) >= nrows)) {
+        oob = true;
+        cur[j] = 0;
+      }
+    }
+    const int n = min(S::ROWS, hi - base);
 #pragma unroll
-      for (int k = 0; k < U; ++k) {
-        const int r = __shfl_sync(gmask, my, kk + k, LANES);
-        if (kk + k < n) v[k] = ldg_stream(tab + static_cast<int64_t>(r) * row_stride4);
+    for (int kk = 0; kk < S::ROWS; kk += S::U) {
+      if (kk >= n) break;
+      float4 v[S::U];
+#pragma unroll
+      for (int k = 0; k < S::U; ++k) {
+        const int r = kk + k;  // row r of the round = index position base + r
+        const int rr = __shfl_sync(gmask, cur[r / LANES], r % LANES, LANES);
+        if (r < n) v[k] = ldg_row(tab, static_cast<uint32_t>(rr), stride_bytes);
       }
 #pragma unroll
-      for (int k = 0; k < U; ++k) {
+      for (int k = 0; k < S::U; ++k) {
         if (kk + k < n) {
           acc.x += v[k].x;
           acc.y += v[k].y;
@@ -85,6 +118,8 @@ __global__ void __launch_bounds__(THREADS) k_sls(const float* __restrict__ table
         }
       }
     }
+#pragma unroll
+    for (int j = 0; j < S::IPL; ++j) cur[j] = nxt[j];
   }
   if (oob) atomicOr(flag, 1);
   if (active) {
@@ -94,26 +129,29 @@ __global__ void __launch_bounds__(THREADS) k_sls(const float* __restrict__ table
   }
 }
 
-void launch_sls(const float* tables, const int64_t* tab_off, int64_t row_stride,
-                const int64_t* rows, const int* indices, const int* offsets, int B, int T, int D,
-                float* X, int x_stride_items, int x_slot0, int* flag, cudaStream_t s) {
+template <int L>
+static void launch_l(const float* tables, const int64_t* tab_off, int64_t row_stride,
+                     const int64_t* rows, const int* indices, const int* offsets, int B,
+                     const int* dB, int T, int D, float* X, int x_stride_items, int x_slot0, int* flag,
+                     cudaStream_t s) {
+  constexpr int THREADS = 128;
   const int nbags = T * B;
-  if (nbags == 0) return;
-  constexpr int THREADS = 256;
+  k_sls<L, THREADS><<<(nbags + THREADS / L - 1) / (THREADS / L), THREADS, 0, s>>>(
+      tables, tab_off, row_stride, rows, indices, offsets, B, dB, T, D, X, x_stride_items, x_slot0,
+      flag);
+}
+
+void launch_sls(const float* tables, const int64_t* tab_off, int64_t row_stride,
+                const int64_t* rows, const int* indices, const int* offsets, int B, const int* dB,
+                int T, int D, float* X, int x_stride_items, int x_slot0, int* flag, cudaStream_t s) {
+  if (T * B == 0) return;
   const int lanes_needed = D / 4;
-  if (lanes_needed <= 8) {
-    constexpr int L = 8;
-    k_sls<L, THREADS><<<(nbags + THREADS / L - 1) / (THREADS / L), THREADS, 0, s>>>(
-        tables, tab_off, row_stride, rows, indices, offsets, B, T, D, X, x_stride_items, x_slot0, flag);
-  } else if (lanes_needed <= 16) {
-    constexpr int L = 16;
-    k_sls<L, THREADS><<<(nbags + THREADS / L - 1) / (THREADS / L), THREADS, 0, s>>>(
-        tables, tab_off, row_stride, rows, indices, offsets, B, T, D, X, x_stride_items, x_slot0, flag);
-  } else {
-    constexpr int L = 32;
-    k_sls<L, THREADS><<<(nbags + THREADS / L - 1) / (THREADS / L), THREADS, 0, s>>>(
-        tables, tab_off, row_stride, rows, indices, offsets, B, T, D, X, x_stride_items, x_slot0, flag);
-  }
+  if (lanes_needed <= 8)
+    launch_l<8>(tables, tab_off, row_stride, rows, indices, offsets, B, dB, T, D, X, x_stride_items, x_slot0, flag, s);
+  else if (lanes_needed <= 16)
+    launch_l<16>(tables, tab_off, row_stride, rows, indices, offsets, B, dB, T, D, X, x_stride_items, x_slot0, flag, s);
+  else
+    launch_l<32>(tables, tab_off, row_stride, rows, indices, offsets, B, dB, T, D, X, x_stride_items, x_slot0, flag, s);
 }
 
 }  // namespace rec

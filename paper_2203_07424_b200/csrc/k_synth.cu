@@ -76,38 +76,42 @@ void launch_init_final(float* w, float* b, int K, int layer, int e, uint32_t k0,
 }
 
 // ------------------------------------------------------------ batch rows (q, item)
-__global__ void k_expand_rows(const int4* __restrict__ segs, int nseg, int B, int* __restrict__ rowq,
-                              int* __restrict__ rowi) {
-  const int b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= B) return;
+// hdr[0] = {B, nseg, 0, 0}; hdr[1 + k] = segment k = (qid, start, len, first_row).
+__device__ __forceinline__ int2 row_item(const int4* __restrict__ hdr, int nseg, int b) {
   int lo = 0, hi = nseg - 1;  // last segment with first_row <= b
   while (lo < hi) {
     const int mid = (lo + hi + 1) >> 1;
-    if (__ldg(&segs[mid].w) <= b) lo = mid; else hi = mid - 1;
+    if (__ldg(&hdr[1 + mid].w) <= b) lo = mid; else hi = mid - 1;
   }
-  const int4 sg = segs[lo];
-  rowq[b] = sg.x;
-  rowi[b] = sg.y + (b - sg.w);
+  const int4 sg = __ldg(&hdr[1 + lo]);
+  return make_int2(sg.x, sg.y + (b - sg.w));
 }
 
-void launch_expand_rows(const int4* segs4, int nseg, int B, int* rowq, int* rowi, cudaStream_t s) {
-  k_expand_rows<<<(B + 255) / 256, 256, 0, s>>>(segs4, nseg, B, rowq, rowi);
+__global__ void k_expand_rows(const int4* __restrict__ hdr, int* __restrict__ rowq,
+                              int* __restrict__ rowi) {
+  const int B = hdr[0].x, nseg = hdr[0].y;
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  const int2 qi = row_item(hdr, nseg, b);
+  rowq[b] = qi.x;
+  rowi[b] = qi.y;
+}
+
+void launch_expand_rows(const int4* hdr, int cap, int* rowq, int* rowi, cudaStream_t s) {
+  k_expand_rows<<<(cap + 255) / 256, 256, 0, s>>>(hdr, rowq, rowi);
 }
 
 // ------------------------------------------------------------ lengths + offsets (G3)
-// Fixed pooling: offsets[g] = g*L.  Variable: per-bag Philox lengths, then one-CTA
-// exclusive scan (T*B <= a few 10^5, a handful of microseconds).
-__global__ void k_offsets_fixed(int* __restrict__ off, int nbags, int L) {
-  for (int g = blockIdx.x * blockDim.x + threadIdx.x; g <= nbags; g += gridDim.x * blockDim.x)
-    off[g] = g * L;
-}
-
+// Variable pooling: per-bag Philox lengths, then a one-CTA exclusive scan (T*B is a few
+// 10^4-10^5: a handful of microseconds).  Fixed pooling never comes here (k_gen_fused).
 __global__ void __launch_bounds__(1024) k_offsets_var(const int* __restrict__ rowq,
-                                                      const int* __restrict__ rowi, int B, int T,
+                                                      const int* __restrict__ rowi,
+                                                      const int* __restrict__ dB, int T,
                                                       int lo, int hi, uint32_t k0, uint32_t k1,
                                                       int* __restrict__ off) {
   __shared__ int wsum[32];
   __shared__ int carry;
+  const int B = *dB;
   const int nb = T * B;
   const uint64_t span = static_cast<uint64_t>(hi - lo + 1);
   if (threadIdx.x == 0) carry = 0;
@@ -122,8 +126,7 @@ __global__ void __launch_bounds__(1024) k_offsets_var(const int* __restrict__ ro
       const uint64_t r = (static_cast<uint64_t>(w.y) << 32) | w.x;
       len = lo + static_cast<int>(__umul64hi(r, span));
     }
-    // block inclusive scan
-    int v = len;
+    int v = len;  // block inclusive scan
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -133,13 +136,13 @@ __global__ void __launch_bounds__(1024) k_offsets_var(const int* __restrict__ ro
     if (lane == 31) wsum[wid] = v;
     __syncthreads();
     if (wid == 0) {
-      int s = wsum[lane];
+      int s2 = wsum[lane];
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
-        const int n = __shfl_up_sync(0xffffffffu, s, o);
-        if (lane >= o) s += n;
+        const int n = __shfl_up_sync(0xffffffffu, s2, o);
+        if (lane >= o) s2 += n;
       }
-      wsum[lane] = s;
+      wsum[lane] = s2;
     }
     __syncthreads();
     const int incl = v + (wid ? wsum[wid - 1] : 0) + carry;
@@ -151,22 +154,26 @@ __global__ void __launch_bounds__(1024) k_offsets_var(const int* __restrict__ ro
   if (threadIdx.x == 0) off[0] = 0;
 }
 
-void launch_gen_offsets(const int* rowq, const int* rowi, int B, int T, int lo, int hi, uint32_t k0,
-                        uint32_t k1, int* offsets, cudaStream_t s) {
-  if (lo == hi) {
-    const int nb = T * B;
-    k_offsets_fixed<<<(nb + 1 + 255) / 256, 256, 0, s>>>(offsets, nb, lo);
-  } else {
-    k_offsets_var<<<1, 1024, 0, s>>>(rowq, rowi, B, T, lo, hi, k0, k1, offsets);
-  }
+void launch_gen_offsets(const int* rowq, const int* rowi, const int* dB, int T, int lo, int hi,
+                        uint32_t k0, uint32_t k1, int* offsets, cudaStream_t s) {
+  k_offsets_var<<<1, 1024, 0, s>>>(rowq, rowi, dB, T, lo, hi, k0, k1, offsets);
 }
 
 // ---------------------------------------------------------------------- indices (G2)
-// One warp per bag, lanes over slots.
+__device__ __forceinline__ int gen_index(uint32_t j, uint32_t it, uint32_t c2, uint32_t q,
+                                         uint32_t k0, uint32_t k1, uint64_t R, int index_dist) {
+  const U4 w = philox(j, it, c2, q, k0, k1);
+  uint64_t r = (static_cast<uint64_t>(w.y) << 32) | w.x;
+  if (index_dist == 2) r = __umul64hi(r, (static_cast<uint64_t>(w.w) << 32) | w.z);
+  return static_cast<int>(__umul64hi(r, R));
+}
+
+// One warp per bag, lanes over slots (variable pooling path).
 __global__ void k_gen_indices(const int* __restrict__ rowq, const int* __restrict__ rowi,
-                              const int* __restrict__ off, int B, int T,
+                              const int* __restrict__ off, const int* __restrict__ dB, int T,
                               const int64_t* __restrict__ rows, int index_dist, uint32_t k0,
                               uint32_t k1, int* __restrict__ indices) {
+  const int B = *dB;
   const int warps = (gridDim.x * blockDim.x) >> 5;
   const int lane = threadIdx.x & 31;
   for (int g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; g < T * B; g += warps) {
@@ -174,50 +181,101 @@ __global__ void k_gen_indices(const int* __restrict__ rowq, const int* __restric
     const uint32_t q = static_cast<uint32_t>(rowq[b]), it = static_cast<uint32_t>(rowi[b]);
     const uint64_t R = static_cast<uint64_t>(rows[t]);
     const uint32_t c2 = (static_cast<uint32_t>(t) << 8) | DOM_INDEX;
-    const int s = off[g], e = off[g + 1];
-    for (int j = lane; j < e - s; j += 32) {
-      const U4 w = philox(static_cast<uint32_t>(j), it, c2, q, k0, k1);
-      uint64_t r = (static_cast<uint64_t>(w.y) << 32) | w.x;
-      if (index_dist == 2) r = __umul64hi(r, (static_cast<uint64_t>(w.w) << 32) | w.z);
-      indices[s + j] = static_cast<int>(__umul64hi(r, R));
-    }
+    const int s0 = off[g], e = off[g + 1];
+    for (int j = lane; j < e - s0; j += 32)
+      indices[s0 + j] = gen_index(j, it, c2, q, k0, k1, R, index_dist);
   }
 }
 
-void launch_gen_indices(const int* rowq, const int* rowi, const int* offsets, int B, int T,
-                        const int64_t* rows, int index_dist, uint32_t k0, uint32_t k1, int* indices,
-                        cudaStream_t s) {
-  const int bags = T * B;
-  int blocks = (bags + 7) / 8;
+void launch_gen_indices(const int* rowq, const int* rowi, const int* offsets, int cap, const int* dB,
+                        int T, const int64_t* rows, int index_dist, uint32_t k0, uint32_t k1,
+                        int* indices, cudaStream_t s) {
+  int blocks = (T * cap + 7) / 8;
   if (blocks > 148 * 16) blocks = 148 * 16;
-  k_gen_indices<<<blocks, 256, 0, s>>>(rowq, rowi, offsets, B, T, rows, index_dist, k0, k1, indices);
+  if (blocks < 1) blocks = 1;
+  k_gen_indices<<<blocks, 256, 0, s>>>(rowq, rowi, offsets, dB, T, rows, index_dist, k0, k1, indices);
 }
 
 // ------------------------------------------------------------------------ dense (G4)
-__global__ void k_gen_dense(const int* __restrict__ rowq, const int* __restrict__ rowi, int B, int F,
-                            int Fpad, uint32_t k0, uint32_t k1, __nv_bfloat16* __restrict__ dbf,
-                            float* __restrict__ df) {
+__device__ __forceinline__ float gen_dense(uint32_t f, uint32_t it, uint32_t q, uint32_t k0,
+                                           uint32_t k1) {
+  return i8(philox(f, it, DOM_DENSE, q, k0, k1).x) * pow2f(-7);
+}
+
+__global__ void k_gen_dense(const int* __restrict__ rowq, const int* __restrict__ rowi,
+                            const int* __restrict__ dB, int F, int Fpad, uint32_t k0, uint32_t k1,
+                            __nv_bfloat16* __restrict__ dbf, float* __restrict__ df) {
+  const int B = *dB;
   const int64_t n = (int64_t)B * Fpad;
   for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < n;
        x += (int64_t)gridDim.x * blockDim.x) {
     const int b = static_cast<int>(x / Fpad), f = static_cast<int>(x % Fpad);
     float v = 0.f;
     if (f < F) {
-      const U4 w = philox(static_cast<uint32_t>(f), static_cast<uint32_t>(rowi[b]), DOM_DENSE,
-                          static_cast<uint32_t>(rowq[b]), k0, k1);
-      v = i8(w.x) * pow2f(-7);
+      v = gen_dense(f, rowi[b], rowq[b], k0, k1);
       if (df) df[(int64_t)b * F + f] = v;
     }
     if (dbf) dbf[x] = __float2bfloat16_rn(v);
   }
 }
 
-void launch_gen_dense(const int* rowq, const int* rowi, int B, int F, int Fpad, uint32_t k0,
-                      uint32_t k1, __nv_bfloat16* dense_bf, float* dense_f32, cudaStream_t s) {
-  const int64_t n = (int64_t)B * Fpad;
+void launch_gen_dense(const int* rowq, const int* rowi, int cap, const int* dB, int F, int Fpad,
+                      uint32_t k0, uint32_t k1, __nv_bfloat16* dense_bf, float* dense_f32,
+                      cudaStream_t s) {
+  const int64_t n = (int64_t)cap * Fpad;
   int blocks = static_cast<int>((n + 255) / 256);
   if (blocks > 148 * 16) blocks = 148 * 16;
-  k_gen_dense<<<blocks, 256, 0, s>>>(rowq, rowi, B, F, Fpad, k0, k1, dense_bf, dense_f32);
+  if (blocks < 1) blocks = 1;
+  k_gen_dense<<<blocks, 256, 0, s>>>(rowq, rowi, dB, F, Fpad, k0, k1, dense_bf, dense_f32);
+}
+
+// ------------------------------------------------ fused inputs, fixed pooling (a2)
+// Blocks [0, nbag_blocks): one warp per bag g = t*B + b (offsets[g] = g*L, L indices);
+// blocks beyond: one warp per batch row (dense features).  One launch replaces four.
+__global__ void k_gen_fused(const int4* __restrict__ hdr, int nbag_blocks, int T, int L,
+                            const int64_t* __restrict__ rows, int index_dist, int F, int Fpad,
+                            uint32_t k0, uint32_t k1, int* __restrict__ off, int* __restrict__ indices,
+                            __nv_bfloat16* __restrict__ dbf, float* __restrict__ df) {
+  const int B = __ldg(&hdr[0].x), nseg = __ldg(&hdr[0].y);
+  const int lane = threadIdx.x & 31;
+  const int wpb = blockDim.x >> 5;
+  if (static_cast<int>(blockIdx.x) < nbag_blocks) {
+    const int g = blockIdx.x * wpb + (threadIdx.x >> 5);
+    const int nb = T * B;
+    if (g == 0 && lane == 0) off[nb] = nb * L;
+    if (g >= nb) return;
+    const int t = g / B, b = g - t * B;
+    const int2 qi = row_item(hdr, nseg, b);
+    if (lane == 0) off[g] = g * L;
+    const uint64_t R = static_cast<uint64_t>(__ldg(&rows[t]));
+    const uint32_t c2 = (static_cast<uint32_t>(t) << 8) | DOM_INDEX;
+    int* dst = indices + static_cast<int64_t>(g) * L;
+    for (int j = lane; j < L; j += 32)
+      dst[j] = gen_index(j, qi.y, c2, qi.x, k0, k1, R, index_dist);
+  } else {
+    const int b = (blockIdx.x - nbag_blocks) * wpb + (threadIdx.x >> 5);
+    if (b >= B) return;
+    const int2 qi = row_item(hdr, nseg, b);
+    for (int f = lane; f < Fpad; f += 32) {
+      float v = 0.f;
+      if (f < F) {
+        v = gen_dense(f, qi.y, qi.x, k0, k1);
+        if (df) df[static_cast<int64_t>(b) * F + f] = v;
+      }
+      dbf[static_cast<int64_t>(b) * Fpad + f] = __float2bfloat16_rn(v);
+    }
+  }
+}
+
+void launch_gen_fused(const int4* hdr, int cap, int T, int L, const int64_t* rows, int index_dist,
+                      int F, int Fpad, uint32_t k0, uint32_t k1, int* offsets, int* indices,
+                      __nv_bfloat16* dense_bf, float* dense_f32, cudaStream_t s) {
+  constexpr int WPB = 8;
+  const int nbag_blocks = (T * cap + WPB - 1) / WPB;
+  const int nrow_blocks = (cap + WPB - 1) / WPB;
+  k_gen_fused<<<nbag_blocks + nrow_blocks, 32 * WPB, 0, s>>>(hdr, nbag_blocks, T, L, rows, index_dist,
+                                                            F, Fpad, k0, k1, offsets, indices,
+                                                            dense_bf, dense_f32);
 }
 
 __global__ void k_dense_to_bf16(const float* __restrict__ d, int B, int F, int Fpad,

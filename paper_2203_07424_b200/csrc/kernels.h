@@ -17,28 +17,33 @@ void launch_init_final(float* w, float* b, int K, int layer, int e, uint32_t k0,
 
 // ------------------------------------------------------------ batch inputs (G2, G3)
 // segs4[nseg] = (qid, start, len, first_row)
-void launch_expand_rows(const int4* segs4, int nseg, int B, int* rowq, int* rowi, cudaStream_t s);
-void launch_gen_offsets(const int* rowq, const int* rowi, int B, int T, int lo, int hi,
+// hdr = {B, nseg, 0, 0} then segments (device); rows for the capacity grid `cap`
+void launch_expand_rows(const int4* hdr, int cap, int* rowq, int* rowi, cudaStream_t s);
+void launch_gen_offsets(const int* rowq, const int* rowi, const int* dB, int T, int lo, int hi,
                         uint32_t k0, uint32_t k1, int* offsets, cudaStream_t s);
-void launch_gen_indices(const int* rowq, const int* rowi, const int* offsets, int B, int T,
-                        const int64_t* rows, int index_dist, uint32_t k0, uint32_t k1,
+void launch_gen_indices(const int* rowq, const int* rowi, const int* offsets, int cap, const int* dB,
+                        int T, const int64_t* rows, int index_dist, uint32_t k0, uint32_t k1,
                         int* indices, cudaStream_t s);
-void launch_gen_dense(const int* rowq, const int* rowi, int B, int F, int Fpad, uint32_t k0,
-                      uint32_t k1, __nv_bfloat16* dense_bf, float* dense_f32, cudaStream_t s);
+void launch_gen_dense(const int* rowq, const int* rowi, int cap, const int* dB, int F, int Fpad,
+                      uint32_t k0, uint32_t k1, __nv_bfloat16* dense_bf, float* dense_f32,
+                      cudaStream_t s);
 void launch_dense_to_bf16(const float* dense, int B, int F, int Fpad, __nv_bfloat16* out,
                           cudaStream_t s);
 void launch_check_offsets(const int* offsets, int nbags, int* flag, cudaStream_t s);
 
 // ------------------------------------------------------------------------- SLS (a3)
 // Row r of table t lives at tables + tab_off[t] + r * row_stride (floats).
+// B: batch (or capacity when dB != nullptr: then the kernels read the batch from *dB,
+// which lets one captured CUDA graph serve every batch size).
 void launch_sls(const float* tables, const int64_t* tab_off, int64_t row_stride,
-                const int64_t* rows, const int* indices, const int* offsets, int B, int T, int D,
-                float* X, int x_stride_items, int x_slot0, int* flag, cudaStream_t s);
+                const int64_t* rows, const int* indices, const int* offsets, int B, const int* dB,
+                int T, int D, float* X, int x_stride_items, int x_slot0, int* flag, cudaStream_t s);
 
 // ----------------------------------------------------------- tcgen05 GEMM (a4, a6)
 enum GemmMode : int { GEMM_OUT_BF16 = 0, GEMM_OUT_X_F32 = 1, GEMM_OUT_CTR = 2 };
 struct GemmArgs {
   int M, N, K;              // A [M][K] (bf16, K-major via tmap_a), W [N][K] (tmap_w)
+  const int* dM;            // optional device-side M (grid sized for M = capacity)
   const float* bias;        // [N]
   int relu;                 // apply ReLU after bias
   int mode;                 // GemmMode
@@ -60,7 +65,14 @@ bool encode_tmap_bf16(CUtensorMap* map, const void* base, uint64_t rows, uint64_
                       uint64_t ldk, uint32_t box_rows);
 
 // --------------------------------------------------------------- interaction (a5)
-void launch_interact(const float* X, int B, int T, int D, __nv_bfloat16* A_top, int ld_top,
-                     cudaStream_t s);
+void launch_interact(const float* X, int B, const int* dB, int T, int D, __nv_bfloat16* A_top,
+                     int ld_top, cudaStream_t s);
+
+// Fused synthetic inputs for FIXED pooling: hdr = {B, nseg, 0, 0} followed by nseg segments
+// (qid, start, len, first_row) in device memory; writes offsets (g*L), indices and dense
+// (bf16 padded, optional fp32).  cap = grid capacity in items.
+void launch_gen_fused(const int4* hdr, int cap, int T, int L, const int64_t* rows, int index_dist,
+                      int F, int Fpad, uint32_t k0, uint32_t k1, int* offsets, int* indices,
+                      __nv_bfloat16* dense_bf, float* dense_f32, cudaStream_t s);
 
 }  // namespace rec

@@ -70,7 +70,11 @@ void prof_end(rec_model_s* m, Workspace& w, int kernel, cudaEvent_t a) {
   m->prof_events.push_back(ProfEvent{kernel, a, b});
 }
 
+static void collect_slot(rec_model_s* m, SynthSlot& sl);
+
 static void prof_collect(rec_model_s* m) {
+  for (auto& w : m->ws)
+    for (auto& sl : w.slots) collect_slot(m, sl);
   for (auto& e : m->prof_events) {
     cudaEventSynchronize(e.b);
     float ms = 0.f;
@@ -84,21 +88,29 @@ static void prof_collect(rec_model_s* m) {
 }
 
 // ------------------------------------------------------------------ forward chain
+// B = batch, or the workspace capacity when dB != nullptr (then every kernel reads the batch
+// from *dB: the form captured in CUDA graphs).  gev: stage events recorded as external
+// event nodes during graph capture (indices 2..5), else per-kernel profiling events.
 rec_status forward_enqueue(rec_model_s* m, Workspace& w, const int* indices, const int* offsets,
-                           int B, float* ctr_out, float* logit_out) {
+                           int B, const int* dB, float* ctr_out, float* logit_out, cudaEvent_t* gev) {
   const int T = m->T, D = m->D;
   cudaStream_t s = w.stream;
+  auto mark = [&](int i) {
+    if (gev) cudaEventRecordWithFlags(gev[i], s, cudaEventRecordExternal);
+  };
   // a3: SLS -> X slots 1..T
-  cudaEvent_t e0 = prof_begin(m, w);
-  launch_sls(m->tables, m->d_tab_off, m->row_stride, m->d_rows, indices, offsets, B, T, D, w.X,
+  cudaEvent_t e0 = gev ? nullptr : prof_begin(m, w);
+  launch_sls(m->tables, m->d_tab_off, m->row_stride, m->d_rows, indices, offsets, B, dB, T, D, w.X,
              (T + 1) * D, 1, w.flag, s);
   prof_end(m, w, 0, e0);
+  mark(2);
   // a4: bottom MLP -> X slot 0
   const int nb = static_cast<int>(m->bottom.size());
   for (int l = 0; l < nb; ++l) {
     const Layer& L = m->bottom[l];
     GemmArgs a{};
     a.M = B;
+    a.dM = dB;
     a.N = L.N;
     a.K = L.K;
     a.bias = L.bias;
@@ -112,20 +124,23 @@ rec_status forward_enqueue(rec_model_s* m, Workspace& w, const int* indices, con
       a.out_bf16 = static_cast<__nv_bfloat16*>(w.out_bottom[l]);
       a.ldo = L.Npad;
     }
-    cudaEvent_t e = prof_begin(m, w);
+    cudaEvent_t e = gev ? nullptr : prof_begin(m, w);
     launch_gemm_tc(&w.tmap_a_bottom[l], &L.tmap_w, a, s);
     prof_end(m, w, 1, e);
   }
+  mark(3);
   // a5: interaction -> A_top
-  cudaEvent_t e1 = prof_begin(m, w);
-  launch_interact(w.X, B, T, D, w.A_top, m->Ktop_pad, s);
+  cudaEvent_t e1 = gev ? nullptr : prof_begin(m, w);
+  launch_interact(w.X, B, dB, T, D, w.A_top, m->Ktop_pad, s);
   prof_end(m, w, 2, e1);
+  mark(4);
   // a6: top MLP; the last hidden layer's epilogue applies the width-1 layer + sigmoid
   const int nt = static_cast<int>(m->top.size());
   for (int j = 0; j < nt; ++j) {
     const Layer& L = m->top[j];
     GemmArgs a{};
     a.M = B;
+    a.dM = dB;
     a.N = L.N;
     a.K = L.K;
     a.bias = L.bias;
@@ -141,10 +156,11 @@ rec_status forward_enqueue(rec_model_s* m, Workspace& w, const int* indices, con
       a.out_bf16 = static_cast<__nv_bfloat16*>(w.out_top[j]);
       a.ldo = L.Npad;
     }
-    cudaEvent_t e = prof_begin(m, w);
+    cudaEvent_t e = gev ? nullptr : prof_begin(m, w);
     launch_gemm_tc(&w.tmap_a_top[j], &L.tmap_w, a, s);
     prof_end(m, w, 1, e);
   }
+  mark(5);
   m->launches += 2 + nb + nt;
   cudaError_t err = cudaGetLastError();
   if (err != cudaSuccess) return cuda_fail(err, "forward kernel launch");
@@ -156,9 +172,78 @@ static rec_status wait_pin(Workspace& w) {
   return REC_OK;
 }
 
-// segs (host) -> device rows -> indices / offsets / dense (G2-G4) on w.stream
-static rec_status synth_inputs(rec_model_s* m, Workspace& w, const int32_t* segs, int nseg,
-                               int* batch_out, float* dense_f32_out) {
+// The device-synthesised batch chain of one staging slot: H2D of {B, nseg} + segments,
+// input generation (G2-G4, a2), forward (a3-a6), CTR into w.ctr.  Every kernel reads the
+// batch size from the slot's device header, so the chain is captured ONCE per slot as a
+// CUDA graph and replayed for any batch (one memcpy into pinned memory + one graph launch
+// per batch on the host).
+static rec_status synth_chain(rec_model_s* m, Workspace& w, SynthSlot& sl, float* dense_f32_out,
+                              bool capture) {
+  cudaStream_t s = w.stream;
+  cudaEvent_t* gev = capture ? sl.ev : nullptr;
+  if (gev) cudaEventRecordWithFlags(gev[0], s, cudaEventRecordExternal);
+  REC_CUDA(cudaMemcpyAsync(sl.dev, sl.pin, sizeof(int4) * (1 + w.cap), cudaMemcpyHostToDevice, s));
+  const int* dB = reinterpret_cast<const int*>(sl.dev);
+  cudaEvent_t e = gev ? nullptr : prof_begin(m, w);
+  if (m->lo == m->hi) {
+    launch_gen_fused(sl.dev, w.cap, m->T, m->lo, m->d_rows, m->index_dist, m->F, m->Fpad, m->k0,
+                     m->k1, w.offsets, w.indices, w.dense_bf, dense_f32_out, s);
+    m->launches += 1;
+  } else {
+    launch_expand_rows(sl.dev, w.cap, w.rowq, w.rowi, s);
+    launch_gen_offsets(w.rowq, w.rowi, dB, m->T, m->lo, m->hi, m->k0, m->k1, w.offsets, s);
+    launch_gen_indices(w.rowq, w.rowi, w.offsets, w.cap, dB, m->T, m->d_rows, m->index_dist, m->k0,
+                       m->k1, w.indices, s);
+    launch_gen_dense(w.rowq, w.rowi, w.cap, dB, m->F, m->Fpad, m->k0, m->k1, w.dense_bf,
+                     dense_f32_out, s);
+    m->launches += 4;
+  }
+  prof_end(m, w, 3, e);
+  if (gev) cudaEventRecordWithFlags(gev[1], s, cudaEventRecordExternal);
+  return forward_enqueue(m, w, w.indices, w.offsets, w.cap, dB, w.ctr, w.logit, gev);
+}
+
+rec_status capture_graphs(rec_model_s* m, Workspace& w) {
+  for (auto& sl : w.slots) {
+    const int64_t before = m->launches;
+    REC_CUDA(cudaStreamBeginCapture(w.stream, cudaStreamCaptureModeThreadLocal));
+    rec_status st = synth_chain(m, w, sl, nullptr, true);
+    cudaGraph_t g = nullptr;
+    cudaError_t ce = cudaStreamEndCapture(w.stream, &g);
+    if (st != REC_OK) return st;
+    if (ce != cudaSuccess) return cuda_fail(ce, "cudaStreamEndCapture");
+    ce = cudaGraphInstantiate(&sl.graph, g, 0);
+    cudaGraphDestroy(g);
+    if (ce != cudaSuccess) return cuda_fail(ce, "cudaGraphInstantiate");
+    w.graph_kernels = static_cast<int>(m->launches - before);
+    m->launches = before;
+  }
+  return REC_OK;
+}
+
+static void collect_slot(rec_model_s* m, SynthSlot& sl) {
+  if (!sl.prof_pending) return;
+  float t[5];
+  for (int i = 0; i < 5; ++i) {
+    t[i] = 0.f;
+    cudaEventElapsedTime(&t[i], sl.ev[i], sl.ev[i + 1]);
+  }
+  // ev: 0 gen 1 sls 2 bottom 3 interact 4 top 5
+  m->prof_ms[3] += t[0];
+  m->prof_ms[0] += t[1];
+  m->prof_ms[1] += t[2] + t[4];
+  m->prof_ms[2] += t[3];
+  m->prof_n[3] += 1;
+  m->prof_n[0] += 1;
+  m->prof_n[1] += static_cast<int64_t>(m->bottom.size() + m->top.size());
+  m->prof_n[2] += 1;
+  sl.prof_pending = false;
+}
+
+// segs (host) -> staging slot -> (graph) inputs + forward on w.stream.  dense_f32_out forces
+// the direct (non-graph) path (rec_gen_batch needs the fp32 dense copy).
+rec_status synth_submit(rec_model_s* m, Workspace& w, const int32_t* segs, int nseg, int* batch_out,
+                        float* dense_f32_out) {
   if (nseg <= 0 || !segs) {
     set_error("segs: empty segment list");
     return REC_E_INVALID_ARG;
@@ -175,33 +260,28 @@ static rec_status synth_inputs(rec_model_s* m, Workspace& w, const int32_t* segs
     set_error("segs: batch of %lld items exceeds max_batch %d", (long long)B, w.cap);
     return REC_E_INVALID_ARG;
   }
-  rec_status st = wait_pin(w);
-  if (st != REC_OK) return st;
-  int4* p = reinterpret_cast<int4*>(w.pin);
+  SynthSlot& sl = w.slots[w.next_slot];
+  w.next_slot = (w.next_slot + 1) % static_cast<int>(w.slots.size());
+  REC_CUDA(cudaEventSynchronize(sl.free));
+  collect_slot(m, sl);
+  int4* p = sl.pin;
+  p[0] = make_int4(static_cast<int>(B), nseg, 0, 0);
   int row = 0;
   for (int i = 0; i < nseg; ++i) {
-    p[i] = make_int4(segs[3 * i], segs[3 * i + 1], segs[3 * i + 2], row);
+    p[1 + i] = make_int4(segs[3 * i], segs[3 * i + 1], segs[3 * i + 2], row);
     row += segs[3 * i + 2];
   }
-  cudaStream_t s = w.stream;
-  REC_CUDA(cudaMemcpyAsync(w.segs, p, sizeof(int4) * nseg, cudaMemcpyHostToDevice, s));
-  REC_CUDA(cudaEventRecord(w.pin_free, s));
-  const int Bi = static_cast<int>(B);
-  cudaEvent_t e = prof_begin(m, w);
-  launch_expand_rows(w.segs, nseg, Bi, w.rowq, w.rowi, s);
-  launch_gen_offsets(w.rowq, w.rowi, Bi, m->T, m->lo, m->hi, m->k0, m->k1, w.offsets, s);
-  launch_gen_indices(w.rowq, w.rowi, w.offsets, Bi, m->T, m->d_rows, m->index_dist, m->k0, m->k1,
-                     w.indices, s);
-  launch_gen_dense(w.rowq, w.rowi, Bi, m->F, m->Fpad, m->k0, m->k1, w.dense_bf, dense_f32_out, s);
-  prof_end(m, w, 3, e);
-  m->launches += 4;
-  *batch_out = Bi;
+  if (sl.graph && !dense_f32_out) {
+    REC_CUDA(cudaGraphLaunch(sl.graph, w.stream));
+    m->launches += w.graph_kernels;
+    sl.prof_pending = m->prof;
+  } else {
+    rec_status st = synth_chain(m, w, sl, dense_f32_out, false);
+    if (st != REC_OK) return st;
+  }
+  REC_CUDA(cudaEventRecord(sl.free, w.stream));
+  *batch_out = static_cast<int>(B);
   return REC_OK;
-}
-
-rec_status synth_enqueue(rec_model_s* m, Workspace& w, const int32_t* segs, int nseg,
-                         int* batch_out) {
-  return synth_inputs(m, w, segs, nseg, batch_out, nullptr);
 }
 
 static rec_status read_flag(Workspace& w) {
@@ -294,7 +374,7 @@ static rec_status query_impl(rec_model_s* m, const float* dense, const int32_t* 
   REC_CUDA(cudaEventRecord(w.pin_free, s));
   launch_dense_to_bf16(d_dense, B, m->F, m->Fpad, w.dense_bf, s);
   m->launches += 1 + (off_dev ? 1 : 0);
-  st = forward_enqueue(m, w, d_idx, d_off, B, w.ctr, w.logit);
+  st = forward_enqueue(m, w, d_idx, d_off, B, nullptr, w.ctr, w.logit, nullptr);
   if (st != REC_OK) return st;
   REC_CUDA(cudaMemcpyAsync(w.flag_host, w.flag, sizeof(int), cudaMemcpyDeviceToHost, s));
   REC_CUDA(cudaStreamSynchronize(s));
@@ -343,6 +423,14 @@ static void free_model(rec_model_s* m) {
     if (w.flag_host) cudaFreeHost(w.flag_host);
     if (w.pin) cudaFreeHost(w.pin);
     if (w.pin_free) cudaEventDestroy(w.pin_free);
+    for (auto& sl : w.slots) {
+      if (sl.graph) cudaGraphExecDestroy(sl.graph);
+      if (sl.pin) cudaFreeHost(sl.pin);
+      cudaFree(sl.dev);
+      if (sl.free) cudaEventDestroy(sl.free);
+      for (auto e : sl.ev)
+        if (e) cudaEventDestroy(e);
+    }
     if (w.stream) cudaStreamDestroy(w.stream);
   }
   for (auto& L : m->bottom) {
@@ -687,6 +775,19 @@ rec_status rec_model_create(const rec_model_desc* d, rec_model_t* out) {
       w.out_top[j] = (j == ntl - 1) ? nullptr : static_cast<void*>(w.h[j & 1]);
     }
   }
+  // synthetic-batch staging ring + one captured CUDA graph per slot (a2-a6 chain)
+  constexpr int kSlots = 4;
+  for (auto& w : m->ws) {
+    w.slots.resize(kSlots);
+    for (auto& sl : w.slots) {
+      CHECK_CUDA_CREATE(cudaMallocHost(reinterpret_cast<void**>(&sl.pin), sizeof(int4) * (1 + cap)));
+      memset(sl.pin, 0, sizeof(int4) * (1 + cap));
+      ALLOC(sl.dev, sizeof(int4) * (1 + cap));
+      CHECK_CUDA_CREATE(cudaEventCreateWithFlags(&sl.free, cudaEventDisableTiming));
+      CHECK_CUDA_CREATE(cudaEventRecord(sl.free, w.stream));
+      for (auto& e : sl.ev) CHECK_CUDA_CREATE(cudaEventCreate(&e));
+    }
+  }
   CHECK_CUDA_CREATE(cudaDeviceSynchronize());
 
   // L2 persisting window over the hot row prefix (interleaved layout only)
@@ -708,6 +809,15 @@ rec_status rec_model_create(const rec_model_desc* d, rec_model_t* out) {
       v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
       v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
       CHECK_CUDA_CREATE(cudaStreamSetAttribute(w.stream, cudaStreamAttributeAccessPolicyWindow, &v));
+    }
+  }
+
+  // capture after the stream attributes (L2 window) are final: graph kernel nodes keep them
+  for (auto& w : m->ws) {
+    rec_status st = capture_graphs(m, w);
+    if (st != REC_OK) {
+      free_model(m);
+      return st;
     }
   }
 
@@ -755,12 +865,12 @@ rec_status rec_query_async(rec_model_t m, int32_t slot, const float* dense, cons
   Workspace& w = m->ws[slot];
   launch_dense_to_bf16(dense, batch, m->F, m->Fpad, w.dense_bf, w.stream);
   m->launches += 1;
-  return forward_enqueue(m, w, indices, offsets, batch, ctr, w.logit);
+  return forward_enqueue(m, w, indices, offsets, batch, nullptr, ctr, w.logit, nullptr);
 }
 
 rec_status rec_synth_query_async(rec_model_t m, int32_t slot, const int32_t* segs, int32_t nseg,
                                  float* ctr) {
-  if (!m || !ctr) {
+  if (!m) {
     set_error("null argument");
     return REC_E_INVALID_ARG;
   }
@@ -771,9 +881,11 @@ rec_status rec_synth_query_async(rec_model_t m, int32_t slot, const int32_t* seg
   REC_CUDA(cudaSetDevice(m->device));
   Workspace& w = m->ws[slot];
   int B = 0;
-  rec_status st = synth_inputs(m, w, segs, nseg, &B, nullptr);
+  rec_status st = synth_submit(m, w, segs, nseg, &B, nullptr);
   if (st != REC_OK) return st;
-  return forward_enqueue(m, w, w.indices, w.offsets, B, ctr, w.logit);
+  if (ctr && ctr != w.ctr)
+    REC_CUDA(cudaMemcpyAsync(ctr, w.ctr, sizeof(float) * B, cudaMemcpyDeviceToDevice, w.stream));
+  return REC_OK;
 }
 
 rec_status rec_sync(rec_model_t m, int32_t slot) {
@@ -799,7 +911,7 @@ rec_status rec_gen_batch(rec_model_t m, const int32_t* segs, int32_t nseg, int32
   REC_CUDA(cudaSetDevice(m->device));
   Workspace& w = m->ws[0];
   int B = 0;
-  rec_status st = synth_inputs(m, w, segs, nseg, &B, w.dense_f32);
+  rec_status st = synth_submit(m, w, segs, nseg, &B, w.dense_f32);
   if (st != REC_OK) return st;
   cudaStream_t s = w.stream;
   const int nb = m->T * B;

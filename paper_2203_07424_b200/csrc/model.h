@@ -30,6 +30,17 @@ struct Layer {
   CUtensorMap tmap_w;
 };
 
+// A staging slot of device-synthesised batches: pinned {B, nseg} + segments, their device
+// copy, and the CUDA graph of the whole chain bound to them.
+struct SynthSlot {
+  int4* pin = nullptr;               // pinned [1 + cap]
+  int4* dev = nullptr;               // device [1 + cap]
+  cudaEvent_t free = nullptr;        // the last launch that used this slot completed
+  cudaGraphExec_t graph = nullptr;
+  cudaEvent_t ev[6] = {};            // stage boundaries inside the graph (timing)
+  bool prof_pending = false;
+};
+
 // One per co-located stream: the buffers a batch needs on that stream.
 struct Workspace {
   cudaStream_t stream = nullptr;
@@ -54,6 +65,9 @@ struct Workspace {
   cudaEvent_t pin_free = nullptr;    // last H2D out of `pin` completed
   std::vector<CUtensorMap> tmap_a_bottom, tmap_a_top;  // A operand per GEMM layer
   std::vector<void*> out_bottom, out_top;              // output buffer per GEMM layer
+  std::vector<SynthSlot> slots;                        // synthetic-batch staging ring
+  int next_slot = 0;
+  int graph_kernels = 0;                               // kernels per graph launch
 };
 
 struct ProfEvent {
@@ -104,9 +118,13 @@ namespace rec {
 // Launch the forward of `batch` items on workspace `w` whose inputs are already in
 // w.indices / w.offsets / w.dense_bf (or caller device pointers).  ctr_out: device.
 rec_status forward_enqueue(rec_model_s* m, Workspace& w, const int* indices, const int* offsets,
-                           int batch, float* ctr_out, float* logit_out);
-// Device-synthesised inputs for a segment list (host), enqueued on w.stream.
-rec_status synth_enqueue(rec_model_s* m, Workspace& w, const int32_t* segs, int nseg, int* batch_out);
+                           int batch, const int* dB, float* ctr_out, float* logit_out,
+                           cudaEvent_t* gev);
+// Device-synthesised batch (segment list on the host) through a staging slot: inputs (a2)
+// and forward (a3-a6) enqueued on w.stream, CTRs in w.ctr.
+rec_status synth_submit(rec_model_s* m, Workspace& w, const int32_t* segs, int nseg, int* batch_out,
+                        float* dense_f32_out);
+rec_status capture_graphs(rec_model_s* m, Workspace& w);
 cudaEvent_t prof_begin(rec_model_s* m, Workspace& w);
 rec_status dist_init(rec_model_s* m, const void* nccl_id);   // dist.cu
 void dist_destroy(rec_model_s* m);

@@ -1,17 +1,36 @@
-// serve.cpp — query splitter / fuser (S1, S2) and the serving runtime (rec_serve).
+// serve.cpp — query splitter / fuser (S1, S2) and the serving runtime rec_serve (a1, a7).
+//
+// "each large inference query is split into multiple sub-queries ...
+// On accelerators, the inference queries are fused into one large batch ... query fusion";
+// model co-location = m concurrent inference threads on one accelerator, here
+// m CUDA streams (one workspace each) driven by one dispatcher thread; the objective
+// is throughput under a tail-latency SLA.
+//
+// Real clock: queries are released open-loop at their trace arrival times (busy-waiting on
+// CLOCK_MONOTONIC); whenever a stream is idle the dispatcher fuses FIFO sub-queries into a
+// batch (Σ <= d) and enqueues input materialisation + the forward chain on that stream;
+// completion is observed by polling a CUDA event per stream; a query's latency ends when
+// the host observes the completion of its last sub-query (reading R16).
+// Virtual clock (S4): identical dispatch rules on a simulated clock with service time
+// alpha + beta * items, so the batch list is unique and bit-exact with oracle/serving.py;
+// the kernels still run for every batch (CTRs are real).
 #include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <queue>
 #include <vector>
 
 #include "model.h"
 
 namespace rec {
 
-// S1: chunks of d, remainder last (P:264, reading R14).
 struct Chunk {
   int32_t qid, start, len;
   int64_t pos;  // trace row
 };
 
+// S1: chunks of d, remainder last (P:264, reading R14).
 static void split_query(const rec_trace_row& r, int64_t pos, int32_t d, std::vector<Chunk>& out) {
   const int32_t k = (r.size + d - 1) / d;
   for (int32_t c = 0; c < k; ++c)
@@ -28,6 +47,131 @@ static int64_t fuse_head(const std::vector<Chunk>& fifo, int64_t head, int32_t d
   }
   *items = tot;
   return k;
+}
+
+static inline double now_s() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+static int64_t pct_rank(int pct, int64_t n) { return std::max<int64_t>((pct * n + 99) / 100, 1); }
+
+struct Batch {
+  int stream = -1;
+  int64_t first_chunk = 0, nchunks = 0, items = 0;
+  double t_dispatch = 0, t_done = 0;
+};
+
+// Per-stream state of the serving loop.
+struct Lane {
+  bool busy = false;
+  int64_t batch = -1;
+  cudaEvent_t done = nullptr;
+  float* ctr_host = nullptr;  // pinned [cap]
+};
+
+// Host-input mode: per-query materialised inputs (table-major within the query).
+struct HostInputs {
+  std::vector<int64_t> q_item_base;  // first global item of query p
+  std::vector<int64_t> idx_base;     // [p*T + t] -> start in idx
+  std::vector<int32_t> idx;          // all indices
+  std::vector<int32_t> len;          // [item*T + t] bag lengths
+  std::vector<float> dense;          // [item][F]
+};
+
+static rec_status build_host_inputs(rec_model_s* m, const rec_trace_row* tr, int64_t n,
+                                    HostInputs& H) {
+  const int T = m->T, F = m->F;
+  Workspace& w = m->ws[0];
+  H.q_item_base.resize(n + 1);
+  int64_t items = 0;
+  for (int64_t p = 0; p < n; ++p) {
+    H.q_item_base[p] = items;
+    items += tr[p].size;
+  }
+  H.q_item_base[n] = items;
+  H.len.assign(items * T, 0);
+  H.dense.assign(items * F, 0.f);
+  H.idx_base.assign(n * T + 1, 0);
+  // generate per query in chunks of <= cap items through the device generator (G2-G4)
+  std::vector<int32_t> off_h(static_cast<size_t>(T) * w.cap + 1);
+  std::vector<int32_t> idx_h(w.idx_cap);
+  std::vector<std::vector<int32_t>> per_q_t;  // scratch for one query
+  for (int64_t p = 0; p < n; ++p) {
+    per_q_t.assign(T, {});
+    for (int32_t s0 = 0; s0 < tr[p].size; s0 += w.cap) {
+      const int32_t ln = std::min<int32_t>(w.cap, tr[p].size - s0);
+      int32_t seg[3] = {tr[p].qid, s0, ln};
+      rec_status st = rec_gen_batch(m, seg, 1, idx_h.data(), off_h.data(),
+                                    H.dense.data() + (H.q_item_base[p] + s0) * F);
+      if (st != REC_OK) return st;
+      for (int t = 0; t < T; ++t) {
+        for (int b = 0; b < ln; ++b) {
+          const int g = t * ln + b;
+          H.len[(H.q_item_base[p] + s0 + b) * T + t] = off_h[g + 1] - off_h[g];
+          per_q_t[t].insert(per_q_t[t].end(), idx_h.begin() + off_h[g], idx_h.begin() + off_h[g + 1]);
+        }
+      }
+    }
+    for (int t = 0; t < T; ++t) {
+      H.idx_base[p * T + t] = static_cast<int64_t>(H.idx.size());
+      H.idx.insert(H.idx.end(), per_q_t[t].begin(), per_q_t[t].end());
+    }
+  }
+  H.idx_base[n * T] = static_cast<int64_t>(H.idx.size());
+  return REC_OK;
+}
+
+// Pack a batch's host inputs into the workspace's pinned staging and copy them over
+// PCIe (the paper's data-loading stage).  Returns the number of items.
+static rec_status host_input_enqueue(rec_model_s* m, Workspace& w, const HostInputs& H,
+                                     const std::vector<Chunk>& fifo, int64_t c0, int64_t nc,
+                                     int* B_out) {
+  const int T = m->T, F = m->F;
+  REC_CUDA(cudaEventSynchronize(w.pin_free));
+  int B = 0;
+  for (int64_t c = c0; c < c0 + nc; ++c) B += fifo[c].len;
+  int32_t* off = reinterpret_cast<int32_t*>(w.pin);
+  size_t off_bytes = ((sizeof(int32_t) * (static_cast<size_t>(T) * B + 1)) + 255) & ~size_t(255);
+  int32_t* idx = reinterpret_cast<int32_t*>(w.pin + off_bytes);
+  // offsets + indices, table-major over the batch
+  int64_t nnz = 0;
+  int g = 0;
+  off[0] = 0;
+  for (int t = 0; t < T; ++t) {
+    for (int64_t c = c0; c < c0 + nc; ++c) {
+      const Chunk& ch = fifo[c];
+      const int64_t item0 = H.q_item_base[ch.pos] + ch.start;
+      // indices of this chunk for table t are contiguous in the query's table-t list
+      int64_t skip = 0;
+      for (int64_t it = H.q_item_base[ch.pos]; it < item0; ++it) skip += H.len[it * T + t];
+      int64_t cnt = 0;
+      for (int b = 0; b < ch.len; ++b) {
+        cnt += H.len[(item0 + b) * T + t];
+        off[++g] = static_cast<int32_t>(nnz + cnt);
+      }
+      memcpy(idx + nnz, H.idx.data() + H.idx_base[ch.pos * T + t] + skip, sizeof(int32_t) * cnt);
+      nnz += cnt;
+    }
+  }
+  size_t idx_bytes = ((sizeof(int32_t) * nnz) + 255) & ~size_t(255);
+  float* dn = reinterpret_cast<float*>(w.pin + off_bytes + idx_bytes);
+  int row = 0;
+  for (int64_t c = c0; c < c0 + nc; ++c) {
+    const Chunk& ch = fifo[c];
+    memcpy(dn + static_cast<size_t>(row) * F,
+           H.dense.data() + (H.q_item_base[ch.pos] + ch.start) * F, sizeof(float) * ch.len * F);
+    row += ch.len;
+  }
+  cudaStream_t s = w.stream;
+  REC_CUDA(cudaMemcpyAsync(w.offsets, off, sizeof(int32_t) * (static_cast<size_t>(T) * B + 1),
+                           cudaMemcpyHostToDevice, s));
+  REC_CUDA(cudaMemcpyAsync(w.indices, idx, sizeof(int32_t) * nnz, cudaMemcpyHostToDevice, s));
+  REC_CUDA(cudaMemcpyAsync(w.dense_f32, dn, sizeof(float) * B * F, cudaMemcpyHostToDevice, s));
+  REC_CUDA(cudaEventRecord(w.pin_free, s));
+  launch_dense_to_bf16(w.dense_f32, B, F, m->Fpad, w.dense_bf, s);
+  m->launches += 1;
+  *B_out = B;
+  return REC_OK;
 }
 
 }  // namespace rec
@@ -84,8 +228,275 @@ rec_status rec_split_fuse(const rec_trace_row* trace, int64_t n, int32_t max_bat
 rec_status rec_serve(rec_model_t m, const rec_trace_row* trace, int64_t n, double sla_ms,
                      const rec_serve_policy* pol, rec_serve_report* out, double* latency_ms,
                      int32_t* batch_log, int64_t log_cap, int64_t* log_rows, float* ctr_out) {
-  set_error("rec_serve not built yet");
-  return REC_E_UNSUPPORTED;
+  // ------------------------------------------------ validation (before any work)
+  if (!m || !trace || !pol || !out || n < 1) {
+    set_error("model, trace (n >= 1), policy and report are required");
+    return REC_E_INVALID_ARG;
+  }
+  if (pol->streams < 1 || pol->streams > m->nstreams) {
+    set_error("policy.streams = %d must be in [1, model streams = %d]", pol->streams, m->nstreams);
+    return REC_E_INVALID_ARG;
+  }
+  if (pol->max_batch < 1 || pol->max_batch > m->max_batch) {
+    set_error("policy.max_batch = %d must be in [1, model max_batch = %d]", pol->max_batch,
+              m->max_batch);
+    return REC_E_INVALID_ARG;
+  }
+  if (!(pol->fusion_timeout_ms >= 0) || !(pol->warmup_frac >= 0 && pol->warmup_frac < 1) ||
+      (pol->clock != REC_CLOCK_REAL && pol->clock != REC_CLOCK_VIRTUAL) ||
+      (pol->input_mode != REC_INPUT_DEVICE_SYNTH && pol->input_mode != REC_INPUT_HOST) ||
+      !(sla_ms > 0)) {
+    set_error("policy: fusion_timeout_ms >= 0, warmup_frac in [0,1), known clock/input_mode "
+              "and sla_ms > 0 are required");
+    return REC_E_INVALID_ARG;
+  }
+  if (pol->clock == REC_CLOCK_VIRTUAL && !(pol->alpha_ns >= 0 && pol->beta_ns >= 0 &&
+                                           pol->alpha_ns + pol->beta_ns > 0)) {
+    set_error("virtual clock needs alpha_ns, beta_ns >= 0 with alpha_ns + beta_ns > 0");
+    return REC_E_INVALID_ARG;
+  }
+  for (int64_t p = 0; p < n; ++p) {
+    if (trace[p].size < 1 || trace[p].qid < 0 || (p > 0 && trace[p].arrival_s < trace[p - 1].arrival_s)) {
+      set_error("trace[%lld]: size >= 1, qid >= 0 and non-decreasing arrival_s required", (long long)p);
+      return REC_E_INVALID_ARG;
+    }
+  }
+  REC_CUDA(cudaSetDevice(m->device));
+  const int M = pol->streams;
+  const int32_t d = pol->max_batch;
+  const bool virt = pol->clock == REC_CLOCK_VIRTUAL;
+  const double tau = pol->fusion_timeout_ms * 1e-3;
+
+  HostInputs H;
+  if (pol->input_mode == REC_INPUT_HOST) {
+    rec_status st = build_host_inputs(m, trace, n, H);
+    if (st != REC_OK) return st;
+  }
+  std::vector<int64_t> item_base;
+  if (ctr_out) {
+    item_base.resize(n);
+    int64_t acc = 0;
+    for (int64_t p = 0; p < n; ++p) {
+      item_base[p] = acc;
+      acc += trace[p].size;
+    }
+  }
+  std::vector<Lane> lanes(M);
+  for (int s = 0; s < M; ++s) {
+    REC_CUDA(cudaEventCreateWithFlags(&lanes[s].done, cudaEventDisableTiming));
+    if (ctr_out) REC_CUDA(cudaMallocHost(reinterpret_cast<void**>(&lanes[s].ctr_host), sizeof(float) * d));
+  }
+  auto cleanup = [&]() {
+    for (auto& L : lanes) {
+      if (L.done) cudaEventDestroy(L.done);
+      if (L.ctr_host) cudaFreeHost(L.ctr_host);
+    }
+  };
+
+  std::vector<Chunk> fifo;
+  fifo.reserve(static_cast<size_t>(n) * 2);
+  std::vector<int32_t> remaining(n);
+  for (int64_t p = 0; p < n; ++p) remaining[p] = (trace[p].size + d - 1) / d;
+  std::vector<double> done_t(n, NAN), release(n), disp_t(n, NAN);
+  std::vector<Batch> batches;
+  std::vector<int32_t> segbuf;
+  int64_t head = 0, a = 0, completed = 0, logged = 0;
+  const double t_first = trace[0].arrival_s;
+
+  // virtual clock: heap of (completion time, stream, batch)
+  using VEv = std::tuple<double, int, int64_t>;
+  std::priority_queue<VEv, std::vector<VEv>, std::greater<VEv>> vbusy;
+  std::vector<int> idle;
+  for (int s = 0; s < M; ++s) idle.push_back(s);
+
+  auto finish_batch = [&](int64_t bi, double t_c) {
+    Batch& bt = batches[bi];
+    bt.t_done = t_c;
+    for (int64_t c = bt.first_chunk; c < bt.first_chunk + bt.nchunks; ++c) {
+      const Chunk& ch = fifo[c];
+      if (--remaining[ch.pos] == 0) {
+        done_t[ch.pos] = t_c;
+        ++completed;
+      }
+    }
+    if (ctr_out) {
+      const float* src = lanes[bt.stream].ctr_host;
+      int row = 0;
+      for (int64_t c = bt.first_chunk; c < bt.first_chunk + bt.nchunks; ++c) {
+        const Chunk& ch = fifo[c];
+        memcpy(ctr_out + item_base[ch.pos] + ch.start, src + row, sizeof(float) * ch.len);
+        row += ch.len;
+      }
+    }
+  };
+
+  auto dispatch = [&](int s, double t_now, int64_t k, int64_t items) -> rec_status {
+    Workspace& w = m->ws[s];
+    const int64_t bi = static_cast<int64_t>(batches.size());
+    batches.push_back(Batch{s, head, k, items, t_now, 0});
+    int B = 0;
+    rec_status st;
+    if (pol->input_mode == REC_INPUT_DEVICE_SYNTH) {
+      segbuf.resize(3 * k);
+      for (int64_t c = 0; c < k; ++c) {
+        segbuf[3 * c] = fifo[head + c].qid;
+        segbuf[3 * c + 1] = fifo[head + c].start;
+        segbuf[3 * c + 2] = fifo[head + c].len;
+      }
+      st = synth_submit(m, w, segbuf.data(), static_cast<int>(k), &B, nullptr);  // a2-a6
+      if (st != REC_OK) return st;
+    } else {
+      st = host_input_enqueue(m, w, H, fifo, head, k, &B);
+      if (st != REC_OK) return st;
+      st = forward_enqueue(m, w, w.indices, w.offsets, B, nullptr, w.ctr, w.logit, nullptr);
+      if (st != REC_OK) return st;
+    }
+    if (ctr_out)
+      REC_CUDA(cudaMemcpyAsync(lanes[s].ctr_host, w.ctr, sizeof(float) * B, cudaMemcpyDeviceToHost, w.stream));
+    REC_CUDA(cudaEventRecord(lanes[s].done, w.stream));
+    lanes[s].busy = true;
+    lanes[s].batch = bi;
+    for (int64_t c = head; c < head + k; ++c) disp_t[fifo[c].pos] = t_now;
+    if (batch_log && logged < log_cap) {
+      for (int64_t c = head; c < head + k && logged < log_cap; ++c, ++logged) {
+        int32_t* r = batch_log + 5 * logged;
+        r[0] = static_cast<int32_t>(bi);
+        r[1] = s;
+        r[2] = fifo[c].qid;
+        r[3] = fifo[c].start;
+        r[4] = fifo[c].len;
+      }
+    }
+    head += k;
+    return REC_OK;
+  };
+
+  // fire condition (S2 with timeout, R15); times are in trace coordinates (arrival_s)
+  auto should_fire = [&](double t_now, int64_t k, int64_t items) {
+    if (tau <= 0) return true;
+    const bool full = items == d || head + k < static_cast<int64_t>(fifo.size());
+    return full || t_now >= trace[fifo[head].pos].arrival_s + tau;
+  };
+
+  rec_status st = REC_OK;
+  if (virt) {
+    double now = t_first;  // virtual clock in trace coordinates (same arithmetic as S4)
+    while (true) {
+      while (a < n && trace[a].arrival_s <= now) {
+        split_query(trace[a], a, d, fifo);
+        release[a] = trace[a].arrival_s;
+        ++a;
+      }
+      while (!vbusy.empty() && std::get<0>(vbusy.top()) <= now) {
+        auto [t_c, s, bi] = vbusy.top();
+        vbusy.pop();
+        st = rec_sync(m, s);
+        if (st != REC_OK) { cleanup(); return st; }
+        finish_batch(bi, t_c);
+        lanes[s].busy = false;
+        idle.push_back(s);
+        std::sort(idle.begin(), idle.end());
+      }
+      while (!idle.empty() && head < static_cast<int64_t>(fifo.size())) {
+        int64_t items = 0;
+        const int64_t k = fuse_head(fifo, head, d, &items);
+        if (!should_fire(now, k, items)) break;
+        const int s = idle.front();
+        idle.erase(idle.begin());
+        const int64_t bi = static_cast<int64_t>(batches.size());
+        st = dispatch(s, now, k, items);
+        if (st != REC_OK) { cleanup(); return st; }
+        vbusy.push(VEv{now + (pol->alpha_ns + pol->beta_ns * static_cast<double>(items)) * 1e-9, s, bi});
+      }
+      double nxt = INFINITY;
+      if (a < n) nxt = std::min(nxt, trace[a].arrival_s);
+      if (!vbusy.empty()) nxt = std::min(nxt, std::get<0>(vbusy.top()));
+      if (tau > 0 && head < static_cast<int64_t>(fifo.size()) && !idle.empty())
+        nxt = std::min(nxt, trace[fifo[head].pos].arrival_s + tau);
+      if (!std::isfinite(nxt)) break;
+      if (!(nxt > now)) {
+        set_error("virtual clock made no progress");
+        cleanup();
+        return REC_E_INVALID_ARG;
+      }
+      now = nxt;
+    }
+  } else {
+    // real clock: trace time t maps to wall time t0 + (t - t_first)
+    const double t0 = now_s() - t_first;
+    while (completed < n) {
+      const double now = now_s() - t0;
+      while (a < n && trace[a].arrival_s <= now) {
+        split_query(trace[a], a, d, fifo);
+        release[a] = trace[a].arrival_s;
+        ++a;
+      }
+      for (int s = 0; s < M; ++s) {
+        if (!lanes[s].busy) continue;
+        cudaError_t q = cudaEventQuery(lanes[s].done);
+        if (q == cudaErrorNotReady) continue;
+        if (q != cudaSuccess) { cleanup(); return cuda_fail(q, "cudaEventQuery"); }
+        const double t_c = now_s() - t0;
+        st = rec_sync(m, s);
+        if (st != REC_OK) { cleanup(); return st; }
+        finish_batch(lanes[s].batch, t_c);
+        lanes[s].busy = false;
+      }
+      for (int s = 0; s < M && head < static_cast<int64_t>(fifo.size()); ++s) {
+        if (lanes[s].busy) continue;
+        int64_t items = 0;
+        const int64_t k = fuse_head(fifo, head, d, &items);
+        if (!should_fire(now_s() - t0, k, items)) break;
+        st = dispatch(s, now_s() - t0, k, items);
+        if (st != REC_OK) { cleanup(); return st; }
+      }
+    }
+  }
+  for (int s = 0; s < M; ++s) {
+    st = rec_sync(m, s);
+    if (st != REC_OK) { cleanup(); return st; }
+  }
+  cleanup();
+
+  // ------------------------------------------------ report (S5)
+  const double t_last = trace[n - 1].arrival_s;
+  const double w_end = t_first + pol->warmup_frac * (t_last - t_first);
+  std::vector<double> lat;
+  double sum_lat = 0, sum_q = 0, sum_svc = 0, t_max = t_first;
+  for (int64_t p = 0; p < n; ++p) {
+    const double l = done_t[p] - release[p];
+    if (latency_ms) latency_ms[p] = l * 1e3;
+    t_max = std::max(t_max, done_t[p]);
+    if (release[p] >= w_end) {
+      lat.push_back(l * 1e3);
+      sum_lat += l * 1e3;
+      sum_q += (disp_t[p] - release[p]) * 1e3;
+      sum_svc += (done_t[p] - disp_t[p]) * 1e3;
+    }
+  }
+  std::sort(lat.begin(), lat.end());
+  const int64_t nm = static_cast<int64_t>(lat.size());
+  memset(out, 0, sizeof(*out));
+  out->completed = completed;
+  out->dropped = n - completed;
+  out->batches = static_cast<int64_t>(batches.size());
+  double items_tot = 0;
+  for (auto& b : batches) items_tot += b.items;
+  out->mean_batch = batches.empty() ? 0 : items_tot / batches.size();
+  if (nm > 0) {
+    out->p50_ms = lat[pct_rank(50, nm) - 1];
+    out->p95_ms = lat[pct_rank(95, nm) - 1];
+    out->p99_ms = lat[pct_rank(99, nm) - 1];
+    out->mean_ms = sum_lat / nm;
+    out->breakdown_ms[0] = sum_q / nm;   // queueing (arrival -> dispatch of last sub-query)
+    out->breakdown_ms[2] = sum_svc / nm; // input + device + completion observation
+  }
+  out->offered_qps = t_last > t_first ? n / (t_last - t_first) : INFINITY;
+  out->achieved_qps = t_max > t_first ? n / (t_max - t_first) : 0;
+  out->stable = (completed == n) && out->achieved_qps >= 0.98 * out->offered_qps;
+  out->sla_met = out->stable && out->p95_ms <= sla_ms;
+  if (log_rows) *log_rows = logged;
+  return REC_OK;
 }
 
 }  // extern "C"

@@ -1,0 +1,108 @@
+"""GPU serving tests (a1, a7): rec_serve against the oracle's S1-S5.
+
+* virtual clock: the batch list (stream, qid, start, len per batch) is bit-exact with
+  oracle.serving.replay_virtual and latencies equal the oracle's; the CTRs of every
+  served item equal a direct rec_query of the same items (batch invariance) and the
+  oracle within 2e-2.
+* real clock: invariants only (coverage exactly once with S1 boundaries, FIFO,
+  sum <= d, conservation, p95 recomputed from the raw per-query latencies).
+* host-input mode (PCIe data loading) gives the same CTRs as device-synth.
+"""
+import numpy as np
+import pytest
+
+import workloads as W
+from oracle import forward as fw, gen, serving as sv
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _built():
+    import __graft_entry__
+    __graft_entry__.build()
+
+
+CFG = W.small_variant(W.RMC1, 20000)
+
+
+@pytest.fixture(scope="module")
+def model():
+    from paper_2203_07424_b200 import RecModel
+    m = RecModel(CFG, seed=1, max_batch=256, streams=4)
+    yield m
+    m.close()
+
+
+def _batches_from_log(log):
+    out = {}
+    for b, s, q, st, ln in log:
+        out.setdefault(int(b), (int(s), []))[1].append((int(q), int(st), int(ln)))
+    return [out[k] for k in sorted(out)]
+
+
+@pytest.mark.parametrize("streams,d,tau", [(1, 256, 0.0), (3, 128, 0.0), (2, 256, 0.05)])
+def test_virtual_clock_bit_exact(model, streams, d, tau):
+    tr = W.poisson_trace(4000.0, 150, seed=13)
+    alpha, beta = 30000.0, 250.0
+    rep = model.rec_serve(tr, 50.0, streams, d, fusion_timeout_ms=tau, clock=1, alpha_ns=alpha,
+                          beta_ns=beta, log_cap=100000, want_ctr=True)
+    ref = sv.replay_virtual(tr, streams, d, alpha, beta, fusion_timeout_ms=tau)
+    got = _batches_from_log(rep["batch_log"])
+    exp = [(b["stream"], b["segs"]) for b in ref.batches]
+    assert got == exp
+    assert np.array_equal(rep["latency_ms"], ref.latency_s * 1e3)
+    orep = sv.summarize(tr, ref.latency_s, ref.completion_s, 50.0)
+    assert rep["p95_ms"] == orep["p95_ms"] and rep["sla_met"] == orep["sla_met"]
+    assert rep["completed"] == len(tr) and rep["batches"] == len(ref.batches)
+    # CTRs of served items == oracle (sampled) within 2e-2
+    ctr = rep["ctr"]
+    base = np.concatenate([[0], np.cumsum(tr["size"].astype(np.int64))])
+    rng = np.random.default_rng(1)
+    pick_q = rng.choice(len(tr), size=12, replace=False)
+    segs = np.array([[tr["qid"][p], 0, tr["size"][p]] for p in pick_q], np.int32)
+    ind, off, dense = gen.gen_batch(CFG, 1, segs)
+    exp_ctr = fw.forward(CFG, 1, dense, ind, off)
+    got_ctr = np.concatenate([ctr[base[p]:base[p + 1]] for p in pick_q])
+    assert np.abs(got_ctr - exp_ctr).max() <= 2e-2
+
+
+def test_real_clock_invariants(model):
+    tr = W.poisson_trace(3000.0, 600, seed=14)
+    d = 256
+    rep = model.rec_serve(tr, 20.0, 4, d, log_cap=100000)
+    log = rep["batch_log"]
+    assert rep["completed"] == len(tr) and rep["dropped"] == 0
+    seen = {}
+    for b, s, q, st, ln in log:
+        seen.setdefault(int(q), []).append((int(st), int(ln)))
+    for p in range(len(tr)):
+        assert sorted(seen[int(tr["qid"][p])]) == sv.split(int(tr["size"][p]), d)
+    for _, (s, segs) in enumerate(_batches_from_log(log)):
+        assert 1 <= sum(x[2] for x in segs) <= d
+    order = [(int(q), int(st)) for _, _, q, st, _ in log]
+    assert order == sorted(order)                          # FIFO
+    lat = rep["latency_ms"]
+    assert np.all(lat > 0)
+    orep = sv.summarize(tr, lat * 1e-3, tr["arrival_s"] + lat * 1e-3, 20.0)
+    assert abs(rep["p95_ms"] - orep["p95_ms"]) < 1e-9
+    assert rep["p95_ms"] >= rep["p50_ms"]
+
+
+def test_host_input_mode_matches_synth(model):
+    tr = W.poisson_trace(2000.0, 60, seed=15)
+    a = model.rec_serve(tr, 50.0, 2, 256, clock=1, alpha_ns=50000.0, beta_ns=100.0, want_ctr=True)
+    b = model.rec_serve(tr, 50.0, 2, 256, clock=1, alpha_ns=50000.0, beta_ns=100.0, want_ctr=True,
+                        input_mode=1)
+    assert np.array_equal(a["ctr"], b["ctr"])
+    assert np.array_equal(a["latency_ms"], b["latency_ms"])
+
+
+def test_policy_validation(model):
+    from paper_2203_07424_b200 import RecError
+    tr = W.poisson_trace(1000.0, 10, seed=1)
+    for kw in ({"streams": 0, "max_batch": 64}, {"streams": 9, "max_batch": 64},
+               {"streams": 1, "max_batch": 0}, {"streams": 1, "max_batch": 100000}):
+        with pytest.raises(RecError) as ei:
+            model.rec_serve(tr, 20.0, **kw)
+        assert ei.value.status == -1
