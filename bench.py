@@ -187,8 +187,11 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     cfg = W.SHORT[args.config]
     d = args.batch
-    model = RecModel(cfg, seed=1, max_batch=d, streams=1, device=local)
-    stream = torch.cuda.ExternalStream(model.rec_stream_handle(0), device=torch.device("cuda", local))
+    m_streams = args.streams
+    model = RecModel(cfg, seed=1, max_batch=d, streams=m_streams, device=local)
+    dev = torch.device("cuda", local)
+    streams = [torch.cuda.ExternalStream(model.rec_stream_handle(k), device=dev) for k in range(m_streams)]
+    stream = streams[0]
 
     # a1: burst trace -> sub-queries -> fused batches (C++ splitter/fuser), per rank
     trace = W.burst_trace(args.queries, seed=11 + rank)
@@ -204,37 +207,54 @@ def run_ours(args):
         done_b.append(int(np.sum(sg[:, 1] == last_chunk_start[sg[:, 0]])))
     ctr = torch.zeros(d, device="cuda")
 
-    def step(i):
-        model.rec_synth_query_async(0, batches[i % nb], None)
+    # model co-location: consecutive batches go round-robin to m streams
+    def step(i, slot=None):
+        model.rec_synth_query_async(i % m_streams if slot is None else slot, batches[i % nb], None)
+
+    def sync_all():
+        for k in range(m_streams):
+            model.rec_sync(k)
 
     for i in range(args.warmup):
         step(i)
-    model.rec_sync(0)
+    sync_all()
     base_launch = model.rec_profile_read(4)[1]
-    model.rec_profile(True)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
-        with torch.cuda.stream(stream):
-            ev0.record(stream)
+        ev0.record(stream)
+        for s in streams[1:]:
+            s.wait_event(ev0)                    # fork: every stream starts after ev0
         for i in range(args.warmup, args.warmup + args.steps):
             step(i)
-        with torch.cuda.stream(stream):
-            ev1.record(stream)
-        model.rec_sync(0)
+        for s in streams[1:]:
+            e = torch.cuda.Event()
+            e.record(s)
+            stream.wait_event(e)                 # join: ev1 after every stream's last batch
+        ev1.record(stream)
+        sync_all()
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     ms = ev0.elapsed_time(ev1)
     launches = model.rec_profile_read(4)[1] - base_launch
+
+    # roofline pass: the same batches on ONE stream with per-stage CUDA events recorded on
+    # that stream around every kernel class (SLS alone on the GPU -> per-launch duration)
+    rsteps = min(args.steps, args.roofline_steps)
+    model.rec_profile(True)
+    for i in range(args.warmup, args.warmup + rsteps):
+        step(i, slot=0)
     sls_ms, sls_n = model.rec_profile_read(KERNEL_SLS)
     gemm_ms, gemm_n = model.rec_profile_read(KERNEL_GEMM)
     int_ms, _ = model.rec_profile_read(2)
     gen_ms, _ = model.rec_profile_read(3)
     model.rec_profile(False)
+    ridx = [i % nb for i in range(args.warmup, args.warmup + rsteps)]
+    ritems = sum(items_b[i] for i in ridx)
     idx = [i % nb for i in range(args.warmup, args.warmup + args.steps)]
     items = sum(items_b[i] for i in idx)
     queries = sum(done_b[i] for i in idx)
@@ -250,9 +270,9 @@ def run_ours(args):
     value = tot_q / (ms_max * 1e-3)
 
     hbm_peak, bf16_peak, peak_kind = peaks()
-    sls_bytes = sls_bytes_per_item(cfg) * items
+    sls_bytes = sls_bytes_per_item(cfg) * ritems
     sls_gbs = sls_bytes / (sls_ms * 1e-3) / 1e9 if sls_ms > 0 else None
-    flops = mlp_flops_per_item(cfg) * items
+    flops = mlp_flops_per_item(cfg) * ritems
     gemm_tf = flops / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else None
 
     # e2e: the same metric through rec_query with host buffers (H2D + D2H every step)
@@ -306,18 +326,22 @@ def run_ours(args):
                        "rows": cfg.rows, "dim": cfg.dim, "pooling": cfg.pooling_lo,
                        "items_per_s": tot_items / (ms_max * 1e-3), "queries_per_step": tot_q / args.steps / world,
                        "mean_query_items": float(sizes.mean()), "parallelism": f"replicas x{world}",
+                       "streams_per_gpu": m_streams,
                        "l2": "inputs larger than L2 (1.28 GB tables, uniform random rows per step)",
                        "value_is": "saturation QPS (burst trace); see sla"},
             "roofline": {"bound": "hbm", "kernel": "k_sls", "achieved": sls_gbs, "peak": hbm_peak,
                          "unit": "GB/s", "frac": (sls_gbs / hbm_peak) if sls_gbs else None,
                          "traffic": None, "peak_kind": peak_kind,
                          "bytes_per_item": sls_bytes_per_item(cfg), "launches": sls_n,
-                         "avg_launch_us": 1e3 * sls_ms / max(sls_n, 1)},
+                         "avg_launch_us": 1e3 * sls_ms / max(sls_n, 1),
+                         "measured": f"CUDA events around every SLS launch on its stream, "
+                                     f"{rsteps} single-stream steps of the same batches"},
             "mlp": {"bound": "tensor", "achieved_tflops": gemm_tf, "peak": bf16_peak,
                     "frac": (gemm_tf / bf16_peak) if gemm_tf else None, "flops_per_item": mlp_flops_per_item(cfg),
                     "launches": gemm_n, "ms": gemm_ms},
-            "breakdown_ms_per_step": {"gen": gen_ms / args.steps, "sls": sls_ms / args.steps,
-                                      "gemm": gemm_ms / args.steps, "interact": int_ms / args.steps},
+            "breakdown_us_per_batch_single_stream": {
+                "gen": 1e3 * gen_ms / rsteps, "sls": 1e3 * sls_ms / rsteps,
+                "gemm": 1e3 * gemm_ms / rsteps, "interact": 1e3 * int_ms / rsteps},
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
             "e2e": e2e,
@@ -337,6 +361,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="rmc1", choices=list(W.SHORT))
     ap.add_argument("--batch", type=int, default=1024)
+    ap.add_argument("--streams", type=int, default=4)
+    ap.add_argument("--roofline-steps", type=int, default=1000)
     ap.add_argument("--queries", type=int, default=20000)
     ap.add_argument("--e2e-steps", type=int, default=300)
     ap.add_argument("--cpu-items", type=int, default=256)

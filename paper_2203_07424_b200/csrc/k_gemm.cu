@@ -50,6 +50,8 @@ __global__ void __launch_bounds__(128, 1)
   const int nkb = (args.K + BK - 1) / BK;
   const int M = args.dM ? *args.dM : args.M;  // device-side batch (graph replay)
   if (m0 >= M) return;                        // whole CTA beyond the batch: nothing to do
+  __shared__ float s_bias[BN];                // epilogue operands, staged by warps 2-3
+  __shared__ float s_wl[BN];
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < stages; ++s) {
@@ -103,10 +105,18 @@ __global__ void __launch_bounds__(128, 1)
       }
       __syncwarp();
     }
+  } else {
+    // ---------------- warps 2-3: stage bias (and the width-1 layer) while the MMA runs
+    for (int c = threadIdx.x - 64; c < BN; c += 64) {
+      const int n = n0 + c;
+      s_bias[c] = n < args.N ? __ldg(&args.bias[n]) : 0.f;
+      if (args.mode == GEMM_OUT_CTR) s_wl[c] = n < args.N ? __ldg(&args.w_last[n]) : 0.f;
+    }
   }
 
   // ---------------- epilogue: thread = row (TMEM lane warp*32 + lane)
   sm100::mbar_wait(done, 0);
+  __syncthreads();  // s_bias / s_wl visible to every epilogue thread
   sm100::tc_fence_after();
   const int row = m0 + warp * 32 + lane;
   const bool row_ok = row < M;
@@ -114,22 +124,16 @@ __global__ void __launch_bounds__(128, 1)
   float dot = 0.f;
 #pragma unroll 1
   for (int c0 = 0; c0 < BN; c0 += 16) {
+    const int cbase = n0 + c0;
+    if (cbase >= args.N) break;  // warp-uniform
     uint32_t r[16];
     sm100::tmem_ld_32x32b_x16(trow + c0, r);
     sm100::tmem_ld_wait();
-    const int cbase = n0 + c0;
-    if (cbase >= args.N) continue;  // warp-uniform
     float v[16];
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
-      const int c = cbase + j;
-      float x = __uint_as_float(r[j]);
-      if (c < args.N) {
-        x += __ldg(&args.bias[c]);
-        if (args.relu) x = fmaxf(x, 0.f);
-      } else {
-        x = 0.f;
-      }
+      float x = __uint_as_float(r[j]) + s_bias[c0 + j];
+      if (args.relu) x = fmaxf(x, 0.f);
       v[j] = x;
     }
     if (!row_ok) continue;
@@ -163,10 +167,7 @@ __global__ void __launch_bounds__(128, 1)
       }
     } else {  // GEMM_OUT_CTR: width-1 output layer folded into the epilogue
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const int c = cbase + j;
-        if (c < args.N) dot = fmaf(v[j], __ldg(&args.w_last[c]), dot);
-      }
+      for (int j = 0; j < 16; ++j) dot = fmaf(v[j], s_wl[c0 + j], dot);
     }
   }
   if (args.mode == GEMM_OUT_CTR && row_ok) {
