@@ -76,34 +76,102 @@ void launch_init_final(float* w, float* b, int K, int layer, int e, uint32_t k0,
 }
 
 // ------------------------------------------------------------ batch rows (q, item)
-// hdr[0] = {B, nseg, 0, 0}; hdr[1 + k] = segment k = (qid, start, len, first_row).
-__device__ __forceinline__ int2 row_item(const int4* __restrict__ hdr, int nseg, int b) {
-  int lo = 0, hi = nseg - 1;  // last segment with first_row <= b
+__device__ __forceinline__ int2 row_item(const SegBatch& sb, int b) {
+  const int4* segs = sb.nseg > kParamSegs ? sb.gsegs : sb.seg;
+  int lo = 0, hi = sb.nseg - 1;  // last segment with first_row <= b
   while (lo < hi) {
     const int mid = (lo + hi + 1) >> 1;
-    if (__ldg(&hdr[1 + mid].w) <= b) lo = mid; else hi = mid - 1;
+    if (segs[mid].w <= b) lo = mid; else hi = mid - 1;
   }
-  const int4 sg = __ldg(&hdr[1 + lo]);
+  const int4 sg = segs[lo];
   return make_int2(sg.x, sg.y + (b - sg.w));
 }
 
-__global__ void k_expand_rows(const int4* __restrict__ hdr, int* __restrict__ rowq,
-                              int* __restrict__ rowi) {
-  const int B = hdr[0].x, nseg = hdr[0].y;
-  const int b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= B) return;
-  const int2 qi = row_item(hdr, nseg, b);
-  rowq[b] = qi.x;
-  rowi[b] = qi.y;
+// ---------------------------------------------------------------------- indices (G2)
+__device__ __forceinline__ int gen_index(uint32_t j, uint32_t it, uint32_t c2, uint32_t q,
+                                         uint32_t k0, uint32_t k1, uint64_t R, int index_dist) {
+  const U4 w = philox(j, it, c2, q, k0, k1);
+  uint64_t r = (static_cast<uint64_t>(w.y) << 32) | w.x;
+  if (index_dist == 2) r = __umul64hi(r, (static_cast<uint64_t>(w.w) << 32) | w.z);
+  return static_cast<int>(__umul64hi(r, R));
 }
 
-void launch_expand_rows(const int4* hdr, int cap, int* rowq, int* rowi, cudaStream_t s) {
-  k_expand_rows<<<(cap + 255) / 256, 256, 0, s>>>(hdr, rowq, rowi);
+__device__ __forceinline__ float gen_dense(uint32_t f, uint32_t it, uint32_t q, uint32_t k0,
+                                           uint32_t k1) {
+  return i8(philox(f, it, DOM_DENSE, q, k0, k1).x) * pow2f(-7);
+}
+
+// ------------------------------------------------ fused inputs, fixed pooling (a2)
+// Blocks [0, nbag_blocks): one warp per bag g = t*B + b (offsets[g] = g*L, L indices);
+// blocks beyond: one warp per batch row (dense features).  One launch for all of a2.
+constexpr int kGenWPB = 8;
+
+__global__ void __launch_bounds__(32 * kGenWPB) k_gen_fused(const __grid_constant__ SegBatch sb,
+                                                            const GenArgs ga) {
+  const int B = sb.B;
+  const int lane = threadIdx.x & 31;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *ga.dB = B;
+  const int L = ga.lo;
+  if (static_cast<int>(blockIdx.x) < ga.nbag_blocks) {
+    const int g = blockIdx.x * kGenWPB + (threadIdx.x >> 5);
+    const int nb = ga.T * B;
+    if (g == 0 && lane == 0) ga.offsets[nb] = nb * L;
+    if (g >= nb) return;
+    const int t = g / B, b = g - t * B;
+    const int2 qi = row_item(sb, b);
+    if (lane == 0) ga.offsets[g] = g * L;
+    const uint64_t R = static_cast<uint64_t>(__ldg(&ga.rows[t]));
+    const uint32_t c2 = (static_cast<uint32_t>(t) << 8) | DOM_INDEX;
+    int* dst = ga.indices + static_cast<int64_t>(g) * L;
+    for (int j = lane; j < L; j += 32)
+      dst[j] = gen_index(j, qi.y, c2, qi.x, ga.k0, ga.k1, R, ga.index_dist);
+  } else {
+    const int b = (blockIdx.x - ga.nbag_blocks) * kGenWPB + (threadIdx.x >> 5);
+    if (b >= B) return;
+    const int2 qi = row_item(sb, b);
+    for (int f = lane; f < ga.Fpad; f += 32) {
+      float v = 0.f;
+      if (f < ga.F) {
+        v = gen_dense(f, qi.y, qi.x, ga.k0, ga.k1);
+        if (ga.dense_f32) ga.dense_f32[static_cast<int64_t>(b) * ga.F + f] = v;
+      }
+      ga.dense_bf[static_cast<int64_t>(b) * ga.Fpad + f] = __float2bfloat16_rn(v);
+    }
+  }
+}
+
+// Variable pooling, step 1: rows (q, item) of the batch + the device batch size.
+__global__ void k_expand_rows(const __grid_constant__ SegBatch sb, const GenArgs ga) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b == 0) *ga.dB = sb.B;
+  if (b >= sb.B) return;
+  const int2 qi = row_item(sb, b);
+  ga.rowq[b] = qi.x;
+  ga.rowi[b] = qi.y;
+}
+
+void* gen_first_kernel(const GenArgs& ga, dim3* grid, dim3* block) {
+  if (ga.lo == ga.hi) {
+    const int nrow_blocks = (ga.cap + kGenWPB - 1) / kGenWPB;
+    *grid = dim3(ga.nbag_blocks + nrow_blocks);
+    *block = dim3(32 * kGenWPB);
+    return reinterpret_cast<void*>(k_gen_fused);
+  }
+  *grid = dim3((ga.cap + 255) / 256);
+  *block = dim3(256);
+  return reinterpret_cast<void*>(k_expand_rows);
+}
+
+void launch_gen_first(const SegBatch& sb, const GenArgs& ga, cudaStream_t s) {
+  dim3 grid, block;
+  void* fn = gen_first_kernel(ga, &grid, &block);
+  void* args[2] = {const_cast<SegBatch*>(&sb), const_cast<GenArgs*>(&ga)};
+  cudaLaunchKernel(fn, grid, block, args, 0, s);
 }
 
 // ------------------------------------------------------------ lengths + offsets (G3)
 // Variable pooling: per-bag Philox lengths, then a one-CTA exclusive scan (T*B is a few
-// 10^4-10^5: a handful of microseconds).  Fixed pooling never comes here (k_gen_fused).
+// 10^4-10^5: a handful of microseconds).
 __global__ void __launch_bounds__(1024) k_offsets_var(const int* __restrict__ rowq,
                                                       const int* __restrict__ rowi,
                                                       const int* __restrict__ dB, int T,
@@ -154,20 +222,6 @@ __global__ void __launch_bounds__(1024) k_offsets_var(const int* __restrict__ ro
   if (threadIdx.x == 0) off[0] = 0;
 }
 
-void launch_gen_offsets(const int* rowq, const int* rowi, const int* dB, int T, int lo, int hi,
-                        uint32_t k0, uint32_t k1, int* offsets, cudaStream_t s) {
-  k_offsets_var<<<1, 1024, 0, s>>>(rowq, rowi, dB, T, lo, hi, k0, k1, offsets);
-}
-
-// ---------------------------------------------------------------------- indices (G2)
-__device__ __forceinline__ int gen_index(uint32_t j, uint32_t it, uint32_t c2, uint32_t q,
-                                         uint32_t k0, uint32_t k1, uint64_t R, int index_dist) {
-  const U4 w = philox(j, it, c2, q, k0, k1);
-  uint64_t r = (static_cast<uint64_t>(w.y) << 32) | w.x;
-  if (index_dist == 2) r = __umul64hi(r, (static_cast<uint64_t>(w.w) << 32) | w.z);
-  return static_cast<int>(__umul64hi(r, R));
-}
-
 // One warp per bag, lanes over slots (variable pooling path).
 __global__ void k_gen_indices(const int* __restrict__ rowq, const int* __restrict__ rowi,
                               const int* __restrict__ off, const int* __restrict__ dB, int T,
@@ -187,21 +241,6 @@ __global__ void k_gen_indices(const int* __restrict__ rowq, const int* __restric
   }
 }
 
-void launch_gen_indices(const int* rowq, const int* rowi, const int* offsets, int cap, const int* dB,
-                        int T, const int64_t* rows, int index_dist, uint32_t k0, uint32_t k1,
-                        int* indices, cudaStream_t s) {
-  int blocks = (T * cap + 7) / 8;
-  if (blocks > 148 * 16) blocks = 148 * 16;
-  if (blocks < 1) blocks = 1;
-  k_gen_indices<<<blocks, 256, 0, s>>>(rowq, rowi, offsets, dB, T, rows, index_dist, k0, k1, indices);
-}
-
-// ------------------------------------------------------------------------ dense (G4)
-__device__ __forceinline__ float gen_dense(uint32_t f, uint32_t it, uint32_t q, uint32_t k0,
-                                           uint32_t k1) {
-  return i8(philox(f, it, DOM_DENSE, q, k0, k1).x) * pow2f(-7);
-}
-
 __global__ void k_gen_dense(const int* __restrict__ rowq, const int* __restrict__ rowi,
                             const int* __restrict__ dB, int F, int Fpad, uint32_t k0, uint32_t k1,
                             __nv_bfloat16* __restrict__ dbf, float* __restrict__ df) {
@@ -219,63 +258,20 @@ __global__ void k_gen_dense(const int* __restrict__ rowq, const int* __restrict_
   }
 }
 
-void launch_gen_dense(const int* rowq, const int* rowi, int cap, const int* dB, int F, int Fpad,
-                      uint32_t k0, uint32_t k1, __nv_bfloat16* dense_bf, float* dense_f32,
-                      cudaStream_t s) {
-  const int64_t n = (int64_t)cap * Fpad;
-  int blocks = static_cast<int>((n + 255) / 256);
+void launch_gen_variable_rest(const GenArgs& ga, cudaStream_t s) {
+  k_offsets_var<<<1, 1024, 0, s>>>(ga.rowq, ga.rowi, ga.dB, ga.T, ga.lo, ga.hi, ga.k0, ga.k1,
+                                   ga.offsets);
+  int blocks = (ga.T * ga.cap + 7) / 8;
   if (blocks > 148 * 16) blocks = 148 * 16;
   if (blocks < 1) blocks = 1;
-  k_gen_dense<<<blocks, 256, 0, s>>>(rowq, rowi, dB, F, Fpad, k0, k1, dense_bf, dense_f32);
-}
-
-// ------------------------------------------------ fused inputs, fixed pooling (a2)
-// Blocks [0, nbag_blocks): one warp per bag g = t*B + b (offsets[g] = g*L, L indices);
-// blocks beyond: one warp per batch row (dense features).  One launch replaces four.
-__global__ void k_gen_fused(const int4* __restrict__ hdr, int nbag_blocks, int T, int L,
-                            const int64_t* __restrict__ rows, int index_dist, int F, int Fpad,
-                            uint32_t k0, uint32_t k1, int* __restrict__ off, int* __restrict__ indices,
-                            __nv_bfloat16* __restrict__ dbf, float* __restrict__ df) {
-  const int B = __ldg(&hdr[0].x), nseg = __ldg(&hdr[0].y);
-  const int lane = threadIdx.x & 31;
-  const int wpb = blockDim.x >> 5;
-  if (static_cast<int>(blockIdx.x) < nbag_blocks) {
-    const int g = blockIdx.x * wpb + (threadIdx.x >> 5);
-    const int nb = T * B;
-    if (g == 0 && lane == 0) off[nb] = nb * L;
-    if (g >= nb) return;
-    const int t = g / B, b = g - t * B;
-    const int2 qi = row_item(hdr, nseg, b);
-    if (lane == 0) off[g] = g * L;
-    const uint64_t R = static_cast<uint64_t>(__ldg(&rows[t]));
-    const uint32_t c2 = (static_cast<uint32_t>(t) << 8) | DOM_INDEX;
-    int* dst = indices + static_cast<int64_t>(g) * L;
-    for (int j = lane; j < L; j += 32)
-      dst[j] = gen_index(j, qi.y, c2, qi.x, k0, k1, R, index_dist);
-  } else {
-    const int b = (blockIdx.x - nbag_blocks) * wpb + (threadIdx.x >> 5);
-    if (b >= B) return;
-    const int2 qi = row_item(hdr, nseg, b);
-    for (int f = lane; f < Fpad; f += 32) {
-      float v = 0.f;
-      if (f < F) {
-        v = gen_dense(f, qi.y, qi.x, k0, k1);
-        if (df) df[static_cast<int64_t>(b) * F + f] = v;
-      }
-      dbf[static_cast<int64_t>(b) * Fpad + f] = __float2bfloat16_rn(v);
-    }
-  }
-}
-
-void launch_gen_fused(const int4* hdr, int cap, int T, int L, const int64_t* rows, int index_dist,
-                      int F, int Fpad, uint32_t k0, uint32_t k1, int* offsets, int* indices,
-                      __nv_bfloat16* dense_bf, float* dense_f32, cudaStream_t s) {
-  constexpr int WPB = 8;
-  const int nbag_blocks = (T * cap + WPB - 1) / WPB;
-  const int nrow_blocks = (cap + WPB - 1) / WPB;
-  k_gen_fused<<<nbag_blocks + nrow_blocks, 32 * WPB, 0, s>>>(hdr, nbag_blocks, T, L, rows, index_dist,
-                                                            F, Fpad, k0, k1, offsets, indices,
-                                                            dense_bf, dense_f32);
+  k_gen_indices<<<blocks, 256, 0, s>>>(ga.rowq, ga.rowi, ga.offsets, ga.dB, ga.T, ga.rows,
+                                       ga.index_dist, ga.k0, ga.k1, ga.indices);
+  const int64_t n = (int64_t)ga.cap * ga.Fpad;
+  int dblocks = static_cast<int>((n + 255) / 256);
+  if (dblocks > 148 * 16) dblocks = 148 * 16;
+  if (dblocks < 1) dblocks = 1;
+  k_gen_dense<<<dblocks, 256, 0, s>>>(ga.rowq, ga.rowi, ga.dB, ga.F, ga.Fpad, ga.k0, ga.k1,
+                                      ga.dense_bf, ga.dense_f32);
 }
 
 __global__ void k_dense_to_bf16(const float* __restrict__ d, int B, int F, int Fpad,

@@ -16,17 +16,34 @@ void launch_init_final(float* w, float* b, int K, int layer, int e, uint32_t k0,
                        cudaStream_t s);
 
 // ------------------------------------------------------------ batch inputs (G2, G3)
-// segs4[nseg] = (qid, start, len, first_row)
-// hdr = {B, nseg, 0, 0} then segments (device); rows for the capacity grid `cap`
-void launch_expand_rows(const int4* hdr, int cap, int* rowq, int* rowi, cudaStream_t s);
-void launch_gen_offsets(const int* rowq, const int* rowi, const int* dB, int T, int lo, int hi,
-                        uint32_t k0, uint32_t k1, int* offsets, cudaStream_t s);
-void launch_gen_indices(const int* rowq, const int* rowi, const int* offsets, int cap, const int* dB,
-                        int T, const int64_t* rows, int index_dist, uint32_t k0, uint32_t k1,
-                        int* indices, cudaStream_t s);
-void launch_gen_dense(const int* rowq, const int* rowi, int cap, const int* dB, int F, int Fpad,
-                      uint32_t k0, uint32_t k1, __nv_bfloat16* dense_bf, float* dense_f32,
-                      cudaStream_t s);
+// A fused batch as segments (qid, start, len, first_row).  Passed BY VALUE as a
+// __grid_constant__ kernel parameter, so a captured CUDA graph is re-pointed at a new batch
+// with one kernel-node parameter update (no host->device copy per batch).  Batches with more
+// than kParamSegs segments read them from `gsegs` (device memory) instead.
+constexpr int kParamSegs = 120;
+struct SegBatch {
+  int B, nseg;
+  const int4* gsegs;
+  int4 seg[kParamSegs];
+};
+struct GenArgs {
+  int cap, T, lo, hi, index_dist, F, Fpad, nbag_blocks;
+  uint32_t k0, k1;
+  const int64_t* rows;
+  int* offsets;
+  int* indices;
+  __nv_bfloat16* dense_bf;
+  float* dense_f32;  // optional fp32 copy (rec_gen_batch)
+  int* rowq;         // variable pooling path
+  int* rowi;
+  int* dB;           // device batch size, written by the first input kernel
+};
+// The first kernel of the input chain (fused fixed-pooling generator, or row expansion for
+// variable pooling).  Both take (SegBatch, GenArgs) so graph updates are uniform.
+void* gen_first_kernel(const GenArgs& ga, dim3* grid, dim3* block);
+void launch_gen_first(const SegBatch& sb, const GenArgs& ga, cudaStream_t s);
+// Variable pooling only (after launch_gen_first): lengths + scan, indices, dense.
+void launch_gen_variable_rest(const GenArgs& ga, cudaStream_t s);
 void launch_dense_to_bf16(const float* dense, int B, int F, int Fpad, __nv_bfloat16* out,
                           cudaStream_t s);
 void launch_check_offsets(const int* offsets, int nbags, int* flag, cudaStream_t s);
@@ -68,11 +85,5 @@ bool encode_tmap_bf16(CUtensorMap* map, const void* base, uint64_t rows, uint64_
 void launch_interact(const float* X, int B, const int* dB, int T, int D, __nv_bfloat16* A_top,
                      int ld_top, cudaStream_t s);
 
-// Fused synthetic inputs for FIXED pooling: hdr = {B, nseg, 0, 0} followed by nseg segments
-// (qid, start, len, first_row) in device memory; writes offsets (g*L), indices and dense
-// (bf16 padded, optional fp32).  cap = grid capacity in items.
-void launch_gen_fused(const int4* hdr, int cap, int T, int L, const int64_t* rows, int index_dist,
-                      int F, int Fpad, uint32_t k0, uint32_t k1, int* offsets, int* indices,
-                      __nv_bfloat16* dense_bf, float* dense_f32, cudaStream_t s);
 
 }  // namespace rec

@@ -44,7 +44,7 @@ static bool is_device_ptr(const void* p) {
   return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
 }
 
-cudaEvent_t prof_begin(rec_model_s* m, Workspace& w) {
+cudaEvent_t prof_begin(rec_model_s* m, cudaStream_t s) {
   if (!m->prof) return nullptr;
   cudaEvent_t a;
   if (!m->prof_pool.empty()) {
@@ -53,11 +53,11 @@ cudaEvent_t prof_begin(rec_model_s* m, Workspace& w) {
   } else {
     cudaEventCreate(&a);
   }
-  cudaEventRecord(a, w.stream);
+  cudaEventRecord(a, s);
   return a;
 }
 
-void prof_end(rec_model_s* m, Workspace& w, int kernel, cudaEvent_t a) {
+void prof_end(rec_model_s* m, cudaStream_t s, int kernel, cudaEvent_t a) {
   if (!a) return;
   cudaEvent_t b;
   if (!m->prof_pool.empty()) {
@@ -66,7 +66,7 @@ void prof_end(rec_model_s* m, Workspace& w, int kernel, cudaEvent_t a) {
   } else {
     cudaEventCreate(&b);
   }
-  cudaEventRecord(b, w.stream);
+  cudaEventRecord(b, s);
   m->prof_events.push_back(ProfEvent{kernel, a, b});
 }
 
@@ -89,22 +89,22 @@ static void prof_collect(rec_model_s* m) {
 
 // ------------------------------------------------------------------ forward chain
 // B = batch, or the workspace capacity when dB != nullptr (then every kernel reads the batch
-// from *dB: the form captured in CUDA graphs).  gev: stage events recorded as external
-// event nodes during graph capture (indices 2..5), else per-kernel profiling events.
+// from *dB: the form captured in CUDA graphs).  The bottom MLP (a4) depends only on the
+// dense features, the SLS (a3) only on the sparse ones: they run on two streams (a fork in
+// the captured graph) and join before the interaction (a5), which needs both.
+// gev (graph capture): stage events 2 = SLS done, 3 = join, 4 = interaction done, 5 = top
+// done, 6/7 = bottom start/end on the branch stream.
 rec_status forward_enqueue(rec_model_s* m, Workspace& w, const int* indices, const int* offsets,
                            int B, const int* dB, float* ctr_out, float* logit_out, cudaEvent_t* gev) {
   const int T = m->T, D = m->D;
-  cudaStream_t s = w.stream;
-  auto mark = [&](int i) {
-    if (gev) cudaEventRecordWithFlags(gev[i], s, cudaEventRecordExternal);
+  cudaStream_t s = w.stream, sb = w.stream_b;
+  auto mark = [&](int i, cudaStream_t st) {
+    if (gev) cudaEventRecordWithFlags(gev[i], st, cudaEventRecordExternal);
   };
-  // a3: SLS -> X slots 1..T
-  cudaEvent_t e0 = gev ? nullptr : prof_begin(m, w);
-  launch_sls(m->tables, m->d_tab_off, m->row_stride, m->d_rows, indices, offsets, B, dB, T, D, w.X,
-             (T + 1) * D, 1, w.flag, s);
-  prof_end(m, w, 0, e0);
-  mark(2);
-  // a4: bottom MLP -> X slot 0
+  // fork: bottom MLP on the branch stream
+  REC_CUDA(cudaEventRecord(w.ev_fork, s));
+  REC_CUDA(cudaStreamWaitEvent(sb, w.ev_fork, 0));
+  mark(6, sb);
   const int nb = static_cast<int>(m->bottom.size());
   for (int l = 0; l < nb; ++l) {
     const Layer& L = m->bottom[l];
@@ -124,16 +124,25 @@ rec_status forward_enqueue(rec_model_s* m, Workspace& w, const int* indices, con
       a.out_bf16 = static_cast<__nv_bfloat16*>(w.out_bottom[l]);
       a.ldo = L.Npad;
     }
-    cudaEvent_t e = gev ? nullptr : prof_begin(m, w);
-    launch_gemm_tc(&w.tmap_a_bottom[l], &L.tmap_w, a, s);
-    prof_end(m, w, 1, e);
+    cudaEvent_t e = gev ? nullptr : prof_begin(m, sb);
+    launch_gemm_tc(&w.tmap_a_bottom[l], &L.tmap_w, a, sb);
+    prof_end(m, sb, 1, e);
   }
-  mark(3);
+  mark(7, sb);
+  REC_CUDA(cudaEventRecord(w.ev_join, sb));
+  // a3: SLS -> X slots 1..T on the main stream
+  cudaEvent_t e0 = gev ? nullptr : prof_begin(m, s);
+  launch_sls(m->tables, m->d_tab_off, m->row_stride, m->d_rows, indices, offsets, B, dB, T, D, w.X,
+             (T + 1) * D, 1, w.flag, s);
+  prof_end(m, s, 0, e0);
+  mark(2, s);
+  REC_CUDA(cudaStreamWaitEvent(s, w.ev_join, 0));  // join
+  mark(3, s);
   // a5: interaction -> A_top
-  cudaEvent_t e1 = gev ? nullptr : prof_begin(m, w);
+  cudaEvent_t e1 = gev ? nullptr : prof_begin(m, s);
   launch_interact(w.X, B, dB, T, D, w.A_top, m->Ktop_pad, s);
-  prof_end(m, w, 2, e1);
-  mark(4);
+  prof_end(m, s, 2, e1);
+  mark(4, s);
   // a6: top MLP; the last hidden layer's epilogue applies the width-1 layer + sigmoid
   const int nt = static_cast<int>(m->top.size());
   for (int j = 0; j < nt; ++j) {
@@ -156,11 +165,11 @@ rec_status forward_enqueue(rec_model_s* m, Workspace& w, const int* indices, con
       a.out_bf16 = static_cast<__nv_bfloat16*>(w.out_top[j]);
       a.ldo = L.Npad;
     }
-    cudaEvent_t e = gev ? nullptr : prof_begin(m, w);
+    cudaEvent_t e = gev ? nullptr : prof_begin(m, s);
     launch_gemm_tc(&w.tmap_a_top[j], &L.tmap_w, a, s);
-    prof_end(m, w, 1, e);
+    prof_end(m, s, 1, e);
   }
-  mark(5);
+  mark(5, s);
   m->launches += 2 + nb + nt;
   cudaError_t err = cudaGetLastError();
   if (err != cudaSuccess) return cuda_fail(err, "forward kernel launch");
@@ -172,48 +181,71 @@ static rec_status wait_pin(Workspace& w) {
   return REC_OK;
 }
 
-// The device-synthesised batch chain of one staging slot: H2D of {B, nseg} + segments,
-// input generation (G2-G4, a2), forward (a3-a6), CTR into w.ctr.  Every kernel reads the
-// batch size from the slot's device header, so the chain is captured ONCE per slot as a
-// CUDA graph and replayed for any batch (one memcpy into pinned memory + one graph launch
-// per batch on the host).
-static rec_status synth_chain(rec_model_s* m, Workspace& w, SynthSlot& sl, float* dense_f32_out,
-                              bool capture) {
+static void fill_genargs(rec_model_s* m, Workspace& w, GenArgs& ga, float* dense_f32_out) {
+  ga = GenArgs{};
+  ga.cap = w.cap;
+  ga.T = m->T;
+  ga.lo = m->lo;
+  ga.hi = m->hi;
+  ga.index_dist = m->index_dist;
+  ga.F = m->F;
+  ga.Fpad = m->Fpad;
+  ga.nbag_blocks = (m->T * w.cap + 7) / 8;
+  ga.k0 = m->k0;
+  ga.k1 = m->k1;
+  ga.rows = m->d_rows;
+  ga.offsets = w.offsets;
+  ga.indices = w.indices;
+  ga.dense_bf = w.dense_bf;
+  ga.dense_f32 = dense_f32_out;
+  ga.rowq = w.rowq;
+  ga.rowi = w.rowi;
+  ga.dB = w.dB;
+}
+
+// The device-synthesised batch chain: input generation (G2-G4, a2) from the slot's batch
+// descriptor, then the forward (a3-a6) with CTRs in w.ctr.  Every kernel after the first
+// reads the batch size from w.dB, so the chain is captured ONCE per slot as a CUDA graph
+// and re-targeted per batch by updating the first kernel's by-value parameters.
+static rec_status synth_chain(rec_model_s* m, Workspace& w, SynthSlot& sl, bool capture) {
   cudaStream_t s = w.stream;
   cudaEvent_t* gev = capture ? sl.ev : nullptr;
   if (gev) cudaEventRecordWithFlags(gev[0], s, cudaEventRecordExternal);
-  REC_CUDA(cudaMemcpyAsync(sl.dev, sl.pin, sizeof(int4) * (1 + w.cap), cudaMemcpyHostToDevice, s));
-  const int* dB = reinterpret_cast<const int*>(sl.dev);
-  cudaEvent_t e = gev ? nullptr : prof_begin(m, w);
-  if (m->lo == m->hi) {
-    launch_gen_fused(sl.dev, w.cap, m->T, m->lo, m->d_rows, m->index_dist, m->F, m->Fpad, m->k0,
-                     m->k1, w.offsets, w.indices, w.dense_bf, dense_f32_out, s);
-    m->launches += 1;
-  } else {
-    launch_expand_rows(sl.dev, w.cap, w.rowq, w.rowi, s);
-    launch_gen_offsets(w.rowq, w.rowi, dB, m->T, m->lo, m->hi, m->k0, m->k1, w.offsets, s);
-    launch_gen_indices(w.rowq, w.rowi, w.offsets, w.cap, dB, m->T, m->d_rows, m->index_dist, m->k0,
-                       m->k1, w.indices, s);
-    launch_gen_dense(w.rowq, w.rowi, w.cap, dB, m->F, m->Fpad, m->k0, m->k1, w.dense_bf,
-                     dense_f32_out, s);
-    m->launches += 4;
+  cudaEvent_t e = gev ? nullptr : prof_begin(m, s);
+  launch_gen_first(*sl.sb, sl.ga, s);
+  if (capture) {
+    cudaStreamCaptureStatus cs;
+    const cudaGraphNode_t* deps = nullptr;
+    size_t ndeps = 0;
+    REC_CUDA(cudaStreamGetCaptureInfo(s, &cs, nullptr, nullptr, &deps, &ndeps));
+    if (ndeps != 1) {
+      set_error("graph capture: expected one dependency after the input kernel, got %zu", ndeps);
+      return REC_E_CUDA;
+    }
+    sl.gen_node = deps[0];
   }
-  prof_end(m, w, 3, e);
+  if (m->lo != m->hi) {
+    launch_gen_variable_rest(sl.ga, s);
+    m->launches += 4;
+  } else {
+    m->launches += 1;
+  }
+  prof_end(m, s, 3, e);
   if (gev) cudaEventRecordWithFlags(gev[1], s, cudaEventRecordExternal);
-  return forward_enqueue(m, w, w.indices, w.offsets, w.cap, dB, w.ctr, w.logit, gev);
+  return forward_enqueue(m, w, w.indices, w.offsets, w.cap, w.dB, w.ctr, w.logit, gev);
 }
 
 rec_status capture_graphs(rec_model_s* m, Workspace& w) {
   for (auto& sl : w.slots) {
     const int64_t before = m->launches;
     REC_CUDA(cudaStreamBeginCapture(w.stream, cudaStreamCaptureModeThreadLocal));
-    rec_status st = synth_chain(m, w, sl, nullptr, true);
+    rec_status st = synth_chain(m, w, sl, true);
     cudaGraph_t g = nullptr;
     cudaError_t ce = cudaStreamEndCapture(w.stream, &g);
     if (st != REC_OK) return st;
     if (ce != cudaSuccess) return cuda_fail(ce, "cudaStreamEndCapture");
-    ce = cudaGraphInstantiate(&sl.graph, g, 0);
-    cudaGraphDestroy(g);
+    sl.graph = g;
+    ce = cudaGraphInstantiate(&sl.exec, g, 0);
     if (ce != cudaSuccess) return cuda_fail(ce, "cudaGraphInstantiate");
     w.graph_kernels = static_cast<int>(m->launches - before);
     m->launches = before;
@@ -223,15 +255,20 @@ rec_status capture_graphs(rec_model_s* m, Workspace& w) {
 
 static void collect_slot(rec_model_s* m, SynthSlot& sl) {
   if (!sl.prof_pending) return;
-  float t[5];
-  for (int i = 0; i < 5; ++i) {
-    t[i] = 0.f;
-    cudaEventElapsedTime(&t[i], sl.ev[i], sl.ev[i + 1]);
-  }
-  // ev: 0 gen 1 sls 2 bottom 3 interact 4 top 5
+  float t[8] = {};
+  auto el = [&](int a, int b) {
+    float x = 0.f;
+    cudaEventElapsedTime(&x, sl.ev[a], sl.ev[b]);
+    return x;
+  };
+  // 0 gen 1 (fork) ... SLS ... 2 ; 6 bottom 7 ; join 3 ; interact 4 ; top 5
+  t[0] = el(0, 1);
+  t[1] = el(1, 2);
+  t[2] = el(6, 7) + el(4, 5);
+  t[3] = el(3, 4);
   m->prof_ms[3] += t[0];
   m->prof_ms[0] += t[1];
-  m->prof_ms[1] += t[2] + t[4];
+  m->prof_ms[1] += t[2];
   m->prof_ms[2] += t[3];
   m->prof_n[3] += 1;
   m->prof_n[0] += 1;
@@ -240,8 +277,8 @@ static void collect_slot(rec_model_s* m, SynthSlot& sl) {
   sl.prof_pending = false;
 }
 
-// segs (host) -> staging slot -> (graph) inputs + forward on w.stream.  dense_f32_out forces
-// the direct (non-graph) path (rec_gen_batch needs the fp32 dense copy).
+// segs (host) -> a slot's batch descriptor -> graph launch (inputs + forward) on w.stream.
+// dense_f32_out forces the direct (non-graph) path (rec_gen_batch needs the fp32 dense).
 rec_status synth_submit(rec_model_s* m, Workspace& w, const int32_t* segs, int nseg, int* batch_out,
                         float* dense_f32_out) {
   if (nseg <= 0 || !segs) {
@@ -264,19 +301,44 @@ rec_status synth_submit(rec_model_s* m, Workspace& w, const int32_t* segs, int n
   w.next_slot = (w.next_slot + 1) % static_cast<int>(w.slots.size());
   REC_CUDA(cudaEventSynchronize(sl.free));
   collect_slot(m, sl);
-  int4* p = sl.pin;
-  p[0] = make_int4(static_cast<int>(B), nseg, 0, 0);
+  SegBatch& sb = *sl.sb;
+  sb.B = static_cast<int>(B);
+  sb.nseg = nseg;
+  sb.gsegs = w.gsegs;
+  int4* dst = sb.seg;
+  if (nseg > kParamSegs) {  // long segment lists go through pinned staging + H2D
+    rec_status st = wait_pin(w);
+    if (st != REC_OK) return st;
+    dst = reinterpret_cast<int4*>(w.pin);
+  }
   int row = 0;
   for (int i = 0; i < nseg; ++i) {
-    p[1 + i] = make_int4(segs[3 * i], segs[3 * i + 1], segs[3 * i + 2], row);
+    dst[i] = make_int4(segs[3 * i], segs[3 * i + 1], segs[3 * i + 2], row);
     row += segs[3 * i + 2];
   }
-  if (sl.graph && !dense_f32_out) {
-    REC_CUDA(cudaGraphLaunch(sl.graph, w.stream));
+  if (nseg > kParamSegs) {
+    REC_CUDA(cudaMemcpyAsync(w.gsegs, w.pin, sizeof(int4) * nseg, cudaMemcpyHostToDevice, w.stream));
+    REC_CUDA(cudaEventRecord(w.pin_free, w.stream));
+  }
+  const bool direct = dense_f32_out != nullptr || !sl.exec;
+  if (!direct) {
+    dim3 grid, block;
+    cudaKernelNodeParams kp{};
+    kp.func = gen_first_kernel(sl.ga, &grid, &block);
+    kp.gridDim = grid;
+    kp.blockDim = block;
+    kp.sharedMemBytes = 0;
+    void* args[2] = {sl.sb, &sl.ga};
+    kp.kernelParams = args;
+    REC_CUDA(cudaGraphExecKernelNodeSetParams(sl.exec, sl.gen_node, &kp));
+    REC_CUDA(cudaGraphLaunch(sl.exec, w.stream));
     m->launches += w.graph_kernels;
     sl.prof_pending = m->prof;
   } else {
-    rec_status st = synth_chain(m, w, sl, dense_f32_out, false);
+    GenArgs saved = sl.ga;
+    sl.ga.dense_f32 = dense_f32_out;
+    rec_status st = synth_chain(m, w, sl, false);
+    sl.ga = saved;
     if (st != REC_OK) return st;
   }
   REC_CUDA(cudaEventRecord(sl.free, w.stream));
@@ -424,12 +486,20 @@ static void free_model(rec_model_s* m) {
     if (w.pin) cudaFreeHost(w.pin);
     if (w.pin_free) cudaEventDestroy(w.pin_free);
     for (auto& sl : w.slots) {
-      if (sl.graph) cudaGraphExecDestroy(sl.graph);
-      if (sl.pin) cudaFreeHost(sl.pin);
-      cudaFree(sl.dev);
+      if (sl.exec) cudaGraphExecDestroy(sl.exec);
+      if (sl.graph) cudaGraphDestroy(sl.graph);
+      delete sl.sb;
       if (sl.free) cudaEventDestroy(sl.free);
       for (auto e : sl.ev)
         if (e) cudaEventDestroy(e);
+    }
+    cudaFree(w.dB);
+    cudaFree(w.gsegs);
+    if (w.ev_fork) cudaEventDestroy(w.ev_fork);
+    if (w.ev_join) cudaEventDestroy(w.ev_join);
+    if (w.stream_b) {
+      cudaStreamSynchronize(w.stream_b);
+      cudaStreamDestroy(w.stream_b);
     }
     if (w.stream) cudaStreamDestroy(w.stream);
   }
@@ -718,6 +788,11 @@ rec_status rec_model_create(const rec_model_desc* d, rec_model_t* out) {
     w.cap = cap;
     w.idx_cap = idx_cap;
     CHECK_CUDA_CREATE(cudaStreamCreateWithFlags(&w.stream, cudaStreamNonBlocking));
+    CHECK_CUDA_CREATE(cudaStreamCreateWithFlags(&w.stream_b, cudaStreamNonBlocking));
+    CHECK_CUDA_CREATE(cudaEventCreateWithFlags(&w.ev_fork, cudaEventDisableTiming));
+    CHECK_CUDA_CREATE(cudaEventCreateWithFlags(&w.ev_join, cudaEventDisableTiming));
+    ALLOC(w.dB, sizeof(int) * 4);
+    ALLOC(w.gsegs, sizeof(int4) * (cap + 1));
     CHECK_CUDA_CREATE(cudaEventCreateWithFlags(&w.pin_free, cudaEventDisableTiming));
     ALLOC(w.indices, sizeof(int) * (idx_cap > 0 ? idx_cap : 1));
     ALLOC(w.offsets, sizeof(int) * (int64_t(T) * cap + 1));
@@ -780,9 +855,12 @@ rec_status rec_model_create(const rec_model_desc* d, rec_model_t* out) {
   for (auto& w : m->ws) {
     w.slots.resize(kSlots);
     for (auto& sl : w.slots) {
-      CHECK_CUDA_CREATE(cudaMallocHost(reinterpret_cast<void**>(&sl.pin), sizeof(int4) * (1 + cap)));
-      memset(sl.pin, 0, sizeof(int4) * (1 + cap));
-      ALLOC(sl.dev, sizeof(int4) * (1 + cap));
+      sl.sb = new SegBatch();
+      memset(sl.sb, 0, sizeof(SegBatch));
+      sl.sb->B = 1;
+      sl.sb->nseg = 1;
+      sl.sb->seg[0] = make_int4(0, 0, 1, 0);
+      fill_genargs(m, w, sl.ga, nullptr);
       CHECK_CUDA_CREATE(cudaEventCreateWithFlags(&sl.free, cudaEventDisableTiming));
       CHECK_CUDA_CREATE(cudaEventRecord(sl.free, w.stream));
       for (auto& e : sl.ev) CHECK_CUDA_CREATE(cudaEventCreate(&e));

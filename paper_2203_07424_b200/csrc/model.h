@@ -30,20 +30,27 @@ struct Layer {
   CUtensorMap tmap_w;
 };
 
-// A staging slot of device-synthesised batches: pinned {B, nseg} + segments, their device
-// copy, and the CUDA graph of the whole chain bound to them.
+// A staging slot of device-synthesised batches: the batch descriptor (kernel parameters of
+// the chain's first kernel) and the CUDA graph of the whole a2-a6 chain.  Several slots per
+// stream let the host run ahead of the GPU while profiling events stay per launch.
 struct SynthSlot {
-  int4* pin = nullptr;               // pinned [1 + cap]
-  int4* dev = nullptr;               // device [1 + cap]
+  SegBatch* sb = nullptr;            // host copy of the first kernel's by-value parameter
+  GenArgs ga{};
   cudaEvent_t free = nullptr;        // the last launch that used this slot completed
-  cudaGraphExec_t graph = nullptr;
-  cudaEvent_t ev[6] = {};            // stage boundaries inside the graph (timing)
+  cudaGraph_t graph = nullptr;       // kept alive: gen_node belongs to it
+  cudaGraphExec_t exec = nullptr;
+  cudaGraphNode_t gen_node = nullptr;
+  cudaEvent_t ev[8] = {};            // stage boundaries inside the graph (timing)
   bool prof_pending = false;
 };
 
 // One per co-located stream: the buffers a batch needs on that stream.
 struct Workspace {
   cudaStream_t stream = nullptr;
+  cudaStream_t stream_b = nullptr;   // parallel branch: bottom MLP runs concurrently with SLS
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  int* dB = nullptr;                 // device batch size of the in-flight synthetic batch
+  int4* gsegs = nullptr;             // device segments for batches with > kParamSegs segments
   int cap = 0;                       // max items
   int64_t idx_cap = 0;               // max indices
   int* indices = nullptr;            // [idx_cap]
@@ -119,14 +126,14 @@ namespace rec {
 // w.indices / w.offsets / w.dense_bf (or caller device pointers).  ctr_out: device.
 rec_status forward_enqueue(rec_model_s* m, Workspace& w, const int* indices, const int* offsets,
                            int batch, const int* dB, float* ctr_out, float* logit_out,
-                           cudaEvent_t* gev);
+                           cudaEvent_t* gev);   // gev: 8 stage events (graph capture) or null
 // Device-synthesised batch (segment list on the host) through a staging slot: inputs (a2)
 // and forward (a3-a6) enqueued on w.stream, CTRs in w.ctr.
 rec_status synth_submit(rec_model_s* m, Workspace& w, const int32_t* segs, int nseg, int* batch_out,
                         float* dense_f32_out);
 rec_status capture_graphs(rec_model_s* m, Workspace& w);
-cudaEvent_t prof_begin(rec_model_s* m, Workspace& w);
+cudaEvent_t prof_begin(rec_model_s* m, cudaStream_t s);
 rec_status dist_init(rec_model_s* m, const void* nccl_id);   // dist.cu
 void dist_destroy(rec_model_s* m);
-void prof_end(rec_model_s* m, Workspace& w, int kernel, cudaEvent_t a);
+void prof_end(rec_model_s* m, cudaStream_t s, int kernel, cudaEvent_t a);
 }  // namespace rec
