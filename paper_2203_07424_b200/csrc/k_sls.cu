@@ -60,7 +60,7 @@ __global__ void __launch_bounds__(128) k_sls_async(const float* __restrict__ tab
                                                    const int* __restrict__ dB, int T, int D,
                                                    float* __restrict__ X, int x_stride, int x_slot0,
                                                    int* __restrict__ flag) {
-  extern __shared__ float4 ring[];  // [blockDim.x][P][LANES]
+  extern __shared__ float4 ring[];  // [P][LANES][128 threads]: lanes interleaved (no bank conflicts)
   if (dB) B = *dB;
   const int nbags = T * B;
   constexpr int GPB = 128 / LANES;  // groups per block
@@ -75,7 +75,7 @@ __global__ void __launch_bounds__(128) k_sls_async(const float* __restrict__ tab
                                        : (((1u << LANES) - 1u) << ((threadIdx.x & 31) & ~(LANES - 1)));
   const bool active = (sub * 4) < D;
   const int col = active ? sub * 4 : 0;
-  const float4* slot = ring + threadIdx.x * (P * LANES);
+  const float4* slot = ring + threadIdx.x;  // element (round slot q, row j) at [(q*LANES + j)*128]
   const uint32_t saddr = static_cast<uint32_t>(__cvta_generic_to_shared(slot));
 
   const int p_begin = __ldg(&offsets[gb0]), p_end = __ldg(&offsets[gb1]);
@@ -124,7 +124,7 @@ __global__ void __launch_bounds__(128) k_sls_async(const float* __restrict__ tab
           ri = 0;
         }
         if (active)
-          cp_async16(saddr + static_cast<uint32_t>(((r % P) * LANES + j) * 16),
+          cp_async16(saddr + static_cast<uint32_t>(((r % P) * LANES + j) * 128 * 16),
                      itab + static_cast<int64_t>(ri) * row_stride);
       }
     }
@@ -142,7 +142,7 @@ __global__ void __launch_bounds__(128) k_sls_async(const float* __restrict__ tab
   for (int r = 0; r < nrounds; ++r) {
     cp_async_wait<P - 1>();  // round r has landed (this lane's own copies)
     const int pr = p_begin + r * LANES;
-    const float4* s = slot + (r % P) * LANES;
+    const float4* s = slot + (r % P) * LANES * 128;
 #pragma unroll
     for (int j = 0; j < LANES; ++j) {
       const int p = pr + j;
@@ -152,7 +152,7 @@ __global__ void __launch_bounds__(128) k_sls_async(const float* __restrict__ tab
         ++cb;
         cb_end = __ldg(&offsets[cb + 1]);
       }
-      const float4 v = s[j];
+      const float4 v = s[j * 128];
       acc.x += v.x;
       acc.y += v.y;
       acc.z += v.z;
