@@ -11,6 +11,8 @@
 // the bag's indices LANES at a time (one per lane), broadcasts them with shuffles, and keeps
 // LANES independent 128-bit row loads in flight per lane (ld.global.nc.L1::no_allocate —
 // rows are streamed, never reused from L1) before accumulating them in order.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -291,7 +293,12 @@ void launch_sls(const float* tables, const int64_t* tab_off, int64_t row_stride,
                 int T, int D, float* X, int x_stride_items, int x_slot0, int* flag, cudaStream_t s) {
   if (T * B == 0) return;
   const int lanes_needed = D / 4;
-  if (lanes_needed <= 16) {
+  // REC_SLS_IMPL=reg selects the register-pipelined kernel (diagnostics / A-B profiling)
+  static const int impl = [] {
+    const char* e = getenv("REC_SLS_IMPL");
+    return (e && e[0] == 'r') ? 1 : 0;
+  }();
+  if (lanes_needed <= 16 && impl == 0) {
     // persistent grid of k_sls_async: every CTA resident (smem-limited), groups stream bags
     static int grid8 = 0, grid16 = 0;
     constexpr size_t SMEM = 128 * 512;  // 512 B of ring per lane
@@ -315,8 +322,13 @@ void launch_sls(const float* tables, const int64_t* tab_off, int64_t row_stride,
     else
       k_sls_async<16, 2><<<grid, 128, SMEM, s>>>(tables, tab_off, row_stride, rows, indices, offsets,
                                                   B, dB, T, D, X, x_stride_items, x_slot0, flag);
-  } else
+  } else if (lanes_needed <= 8) {
+    launch_l<8>(tables, tab_off, row_stride, rows, indices, offsets, B, dB, T, D, X, x_stride_items, x_slot0, flag, s);
+  } else if (lanes_needed <= 16) {
+    launch_l<16>(tables, tab_off, row_stride, rows, indices, offsets, B, dB, T, D, X, x_stride_items, x_slot0, flag, s);
+  } else {
     launch_l<32>(tables, tab_off, row_stride, rows, indices, offsets, B, dB, T, D, X, x_stride_items, x_slot0, flag, s);
+  }
 }
 
 }  // namespace rec
