@@ -41,8 +41,13 @@ import workloads as W  # noqa: E402
 BASELINE_METRIC = "SLA-bounded QPS (p95) per model at 1/2/4/8 B200; SLS HBM GB/s; MLP TC util"
 
 
-def sls_bytes_per_item(cfg) -> int:
+def sls_bytes_per_item(cfg, synth: bool = False) -> int:
+    """Algorithmic bytes of the SLS per item: T*L fp32 rows of D + int32 indices
+    + int32 offsets + the fp32 pooled write.  synth=True: the serving/bench kernel generates
+    its indices in-kernel (fixed pooling), so no index / offset array is read."""
     T, L, D = cfg.num_tables, 0.5 * (cfg.pooling_lo + cfg.pooling_hi), cfg.dim
+    if synth and cfg.pooling_lo == cfg.pooling_hi:
+        return int(T * L * D * 4 + T * D * 4)
     return int(T * (L * D * 4 + L * 4 + 4) + T * D * 4)
 
 
@@ -270,7 +275,7 @@ def run_ours(args):
     value = tot_q / (ms_max * 1e-3)
 
     hbm_peak, bf16_peak, peak_kind = peaks()
-    sls_bytes = sls_bytes_per_item(cfg) * ritems
+    sls_bytes = sls_bytes_per_item(cfg, synth=True) * ritems
     sls_gbs = sls_bytes / (sls_ms * 1e-3) / 1e9 if sls_ms > 0 else None
     flops = mlp_flops_per_item(cfg) * ritems
     gemm_tf = flops / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else None
@@ -332,7 +337,7 @@ def run_ours(args):
             "roofline": {"bound": "hbm", "kernel": "k_sls", "achieved": sls_gbs, "peak": hbm_peak,
                          "unit": "GB/s", "frac": (sls_gbs / hbm_peak) if sls_gbs else None,
                          "traffic": None, "peak_kind": peak_kind,
-                         "bytes_per_item": sls_bytes_per_item(cfg), "launches": sls_n,
+                         "bytes_per_item": sls_bytes_per_item(cfg, synth=True), "launches": sls_n,
                          "avg_launch_us": 1e3 * sls_ms / max(sls_n, 1),
                          "measured": f"CUDA events around every SLS launch on its stream, "
                                      f"{rsteps} single-stream steps of the same batches"},

@@ -19,7 +19,7 @@ BUILD = os.path.join(ROOT, "build", "obj")
 
 SOURCES = ["k_synth.cu", "k_sls.cu", "k_gemm.cu", "k_interact.cu", "model.cu", "dist.cu",
            "serve.cpp"]
-HEADERS = ["common.cuh", "sm100.cuh", "kernels.h", "model.h"]
+HEADERS = ["common.cuh", "sm100.cuh", "kernels.h", "model.h", "synth.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -11,10 +11,9 @@
 // the bag's indices LANES at a time (one per lane), broadcasts them with shuffles, and keeps
 // LANES independent 128-bit row loads in flight per lane (ld.global.nc.L1::no_allocate —
 // rows are streamed, never reused from L1) before accumulating them in order.
-#include <cstdlib>
-
 #include "common.cuh"
 #include "kernels.h"
+#include "synth.cuh"
 
 namespace rec {
 
@@ -29,151 +28,6 @@ __device__ __forceinline__ float4 ldg_row(const float4* base, uint32_t row, uint
       : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
       : "r"(row), "r"(stride_bytes), "l"(base));
   return v;
-}
-
-// ------------------------------------------------------------------------------------
-// k_sls_async — the production SLS for D <= 64.  Memory-level parallelism is what bounds a
-// random 128-B-row gather on B200 (ncu of the register version: 24 % warps active, 44 % of
-// DRAM peak), so rows land in SHARED memory through cp.async (LDGSTS, L1-bypassing .cg):
-// an in-flight row costs 16 B of smem per lane instead of 4 registers.  Each lane owns a
-// private ring of P rounds x LANES rows; a round is LANES consecutive index positions (one
-// index loaded per lane, broadcast by shuffles), so P*LANES rows per group are in flight
-// and no CTA barrier is ever needed (each lane reads back exactly the bytes it copied).
-// The grid is persistent (all CTAs resident); group i streams the contiguous bag range
-// [i*k, (i+1)*k), k = ceil(T*B / groups), whose indices are contiguous in the CSR array,
-// flushing a bag's sum when the stream crosses offsets[g+1].  Rows are accumulated in
-// index order, exactly like the register kernel below.
-__device__ __forceinline__ void cp_async16(uint32_t saddr, const void* gptr) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(saddr), "l"(gptr) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-
-template <int LANES, int P>
-__global__ void __launch_bounds__(128) k_sls_async(const float* __restrict__ tables,
-                                                   const int64_t* __restrict__ tab_off,
-                                                   int64_t row_stride,
-                                                   const int64_t* __restrict__ rows,
-                                                   const int* __restrict__ indices,
-                                                   const int* __restrict__ offsets, int B,
-                                                   const int* __restrict__ dB, int T, int D,
-                                                   float* __restrict__ X, int x_stride, int x_slot0,
-                                                   int* __restrict__ flag) {
-  extern __shared__ float4 ring[];  // [P][LANES][128 threads]: lanes interleaved (no bank conflicts)
-  if (dB) B = *dB;
-  const int nbags = T * B;
-  constexpr int GPB = 128 / LANES;  // groups per block
-  const int total_groups = gridDim.x * GPB;
-  const int gid = blockIdx.x * GPB + threadIdx.x / LANES;
-  const int k = (nbags + total_groups - 1) / total_groups;
-  const int gb0 = gid * k;
-  if (gb0 >= nbags) return;
-  const int gb1 = min(gb0 + k, nbags);
-  const int sub = threadIdx.x % LANES;
-  const unsigned gmask = (LANES == 32) ? 0xffffffffu
-                                       : (((1u << LANES) - 1u) << ((threadIdx.x & 31) & ~(LANES - 1)));
-  const bool active = (sub * 4) < D;
-  const int col = active ? sub * 4 : 0;
-  const float4* slot = ring + threadIdx.x;  // element (round slot q, row j) at [(q*LANES + j)*128]
-  const uint32_t saddr = static_cast<uint32_t>(__cvta_generic_to_shared(slot));
-
-  const int p_begin = __ldg(&offsets[gb0]), p_end = __ldg(&offsets[gb1]);
-  const int nrounds = (p_end - p_begin + LANES - 1) / LANES;
-
-  // issue cursor (bag / table of the next row to fetch)
-  int ib = gb0, ib_end = __ldg(&offsets[gb0 + 1]);
-  int it = gb0 / B;
-  const float* itab = tables + __ldg(&tab_off[it]) + col;
-  int64_t inrows = __ldg(&rows[it]);
-  // consume cursor (bag being summed)
-  int cb = gb0, cb_end = ib_end;
-  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-  bool oob = false;
-
-  auto flush = [&](int bag) {
-    if (active) {
-      const int t = bag / B, b = bag - t * B;
-      *reinterpret_cast<float4*>(X + (static_cast<int64_t>(b) * x_stride +
-                                      static_cast<int64_t>(x_slot0 + t) * D + col)) = acc;
-    }
-    acc = make_float4(0.f, 0.f, 0.f, 0.f);
-  };
-  auto load_idx = [&](int r) {
-    const int p = p_begin + r * LANES + sub;
-    return (r < nrounds && p < p_end) ? __ldg(&indices[p]) : 0;
-  };
-  auto issue = [&](int r, int mine) {
-    const int pr = p_begin + r * LANES;
-#pragma unroll
-    for (int j = 0; j < LANES; ++j) {
-      const int p = pr + j;
-      int ri = __shfl_sync(gmask, mine, j, LANES);
-      if (p < p_end) {
-        while (p >= ib_end) {
-          ++ib;
-          ib_end = __ldg(&offsets[ib + 1]);
-        }
-        if (ib / B != it) {
-          it = ib / B;
-          itab = tables + __ldg(&tab_off[it]) + col;
-          inrows = __ldg(&rows[it]);
-        }
-        if (ri < 0 || static_cast<int64_t>(ri) >= inrows) {
-          oob = true;
-          ri = 0;
-        }
-        if (active)
-          cp_async16(saddr + static_cast<uint32_t>(((r % P) * LANES + j) * 128 * 16),
-                     itab + static_cast<int64_t>(ri) * row_stride);
-      }
-    }
-    cp_async_commit();
-  };
-
-  // prologue: P rounds in flight
-#pragma unroll
-  for (int r = 0; r < P; ++r) {
-    const int mine = load_idx(r);
-    if (r < nrounds) issue(r, mine);
-    else cp_async_commit();
-  }
-  int nxt = load_idx(P);
-  for (int r = 0; r < nrounds; ++r) {
-    cp_async_wait<P - 1>();  // round r has landed (this lane's own copies)
-    const int pr = p_begin + r * LANES;
-    const float4* s = slot + (r % P) * LANES * 128;
-#pragma unroll
-    for (int j = 0; j < LANES; ++j) {
-      const int p = pr + j;
-      if (p >= p_end) break;
-      while (p >= cb_end) {  // crossing into the next bag(s), empty ones included
-        flush(cb);
-        ++cb;
-        cb_end = __ldg(&offsets[cb + 1]);
-      }
-      const float4 v = s[j * 128];
-      acc.x += v.x;
-      acc.y += v.y;
-      acc.z += v.z;
-      acc.w += v.w;
-    }
-    if (r + P < nrounds) {
-      const int cur = nxt;
-      nxt = load_idx(r + P + 1);
-      issue(r + P, cur);
-    } else {
-      cp_async_commit();
-    }
-  }
-  cp_async_wait<0>();
-  while (cb < gb1) {  // last bag and any trailing empty bags
-    flush(cb);
-    ++cb;
-  }
-  if (oob) atomicOr(flag, 1);
 }
 
 // Per round a group consumes ROWS = IPL * LANES indices (IPL per lane, prefetched one round
@@ -276,6 +130,84 @@ __global__ void __launch_bounds__(THREADS, 5) k_sls(const float* __restrict__ ta
   }
 }
 
+// Synthetic-index variant (device-synth serving mode, fixed pooling): identical gather /
+// accumulate structure, but lane `sub` computes the index of slot base + sub with Philox
+// (G2) instead of loading it, so the kernel has no predecessor in the chain and
+// no dependent index load in front of its first row loads.
+template <int LANES, int THREADS>
+__global__ void __launch_bounds__(THREADS, 5) k_sls_synth(const __grid_constant__ SegBatch sb,
+                                                          const SlsSynthArgs a) {
+  using S = SlsShape<LANES>;
+  constexpr int GROUPS = THREADS / LANES;
+  const int B = sb.B;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *a.dB = B;
+  const int nbags = a.T * B;
+  const int g = blockIdx.x * GROUPS + threadIdx.x / LANES;
+  if (g >= nbags) return;
+  const int sub = threadIdx.x % LANES;
+  const int t = g / B, b = g - t * B;
+  const int2 qi = row_item(sb, b);
+  const uint64_t R = static_cast<uint64_t>(__ldg(&a.rows[t]));
+  const uint32_t c2 = (static_cast<uint32_t>(t) << 8) | DOM_INDEX;
+  const bool active = (sub * 4) < a.D;
+  const int col = active ? sub * 4 : 0;
+  const float4* __restrict__ tab = reinterpret_cast<const float4*>(a.tables + __ldg(&a.tab_off[t]) + col);
+  const uint32_t stride_bytes = static_cast<uint32_t>(a.row_stride * 4);
+  const unsigned gmask = (LANES == 32) ? 0xffffffffu
+                                       : (((1u << LANES) - 1u) << ((threadIdx.x & 31) & ~(LANES - 1)));
+  const int L = a.L;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  int cur = sub < L ? gen_index(sub, qi.y, c2, qi.x, a.k0, a.k1, R, a.index_dist) : 0;
+  for (int base = 0; base < L; base += S::ROWS) {
+    const int n = min(S::ROWS, L - base);
+#pragma unroll
+    for (int kk = 0; kk < S::ROWS; kk += S::U) {
+      if (kk >= n) break;
+      float4 v[S::U];
+#pragma unroll
+      for (int k = 0; k < S::U; ++k) {
+        const int r = kk + k;
+        const int rr = __shfl_sync(gmask, cur, r % LANES, LANES);
+        if (r < n) v[k] = ldg_row(tab, static_cast<uint32_t>(rr), stride_bytes);
+      }
+      if (kk + S::U >= S::ROWS) {  // next round's index, computed while the rows are in flight
+        const int j = base + S::ROWS + sub;
+        cur = j < L ? gen_index(j, qi.y, c2, qi.x, a.k0, a.k1, R, a.index_dist) : 0;
+      }
+#pragma unroll
+      for (int k = 0; k < S::U; ++k) {
+        if (kk + k < n) {
+          acc.x += v[k].x;
+          acc.y += v[k].y;
+          acc.z += v[k].z;
+          acc.w += v[k].w;
+        }
+      }
+    }
+  }
+  if (active)
+    *reinterpret_cast<float4*>(a.X + static_cast<int64_t>(b) * a.x_stride +
+                               static_cast<int64_t>(1 + t) * a.D + col) = acc;
+}
+
+void* sls_synth_kernel(const SlsSynthArgs& a, dim3* grid, dim3* block) {
+  constexpr int THREADS = 128;
+  const int L = a.D / 4 <= 8 ? 8 : a.D / 4 <= 16 ? 16 : 32;
+  const int nb = a.T * a.cap;
+  *grid = dim3((nb + THREADS / L - 1) / (THREADS / L));
+  *block = dim3(THREADS);
+  if (L == 8) return reinterpret_cast<void*>(k_sls_synth<8, THREADS>);
+  if (L == 16) return reinterpret_cast<void*>(k_sls_synth<16, THREADS>);
+  return reinterpret_cast<void*>(k_sls_synth<32, THREADS>);
+}
+
+void launch_sls_synth(const SegBatch& sb, const SlsSynthArgs& a, cudaStream_t s) {
+  dim3 grid, block;
+  void* fn = sls_synth_kernel(a, &grid, &block);
+  void* args[2] = {const_cast<SegBatch*>(&sb), const_cast<SlsSynthArgs*>(&a)};
+  cudaLaunchKernel(fn, grid, block, args, 0, s);
+}
+
 template <int L>
 static void launch_l(const float* tables, const int64_t* tab_off, int64_t row_stride,
                      const int64_t* rows, const int* indices, const int* offsets, int B,
@@ -293,36 +225,7 @@ void launch_sls(const float* tables, const int64_t* tab_off, int64_t row_stride,
                 int T, int D, float* X, int x_stride_items, int x_slot0, int* flag, cudaStream_t s) {
   if (T * B == 0) return;
   const int lanes_needed = D / 4;
-  // REC_SLS_IMPL=reg selects the register-pipelined kernel (diagnostics / A-B profiling)
-  static const int impl = [] {
-    const char* e = getenv("REC_SLS_IMPL");
-    return (e && e[0] == 'r') ? 1 : 0;
-  }();
-  if (lanes_needed <= 16 && impl == 0) {
-    // persistent grid of k_sls_async: every CTA resident (smem-limited), groups stream bags
-    static int grid8 = 0, grid16 = 0;
-    constexpr size_t SMEM = 128 * 512;  // 512 B of ring per lane
-    int& grid = lanes_needed <= 8 ? grid8 : grid16;
-    if (grid == 0) {
-      int dev = 0, sms = 0, per_sm = 0;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      if (lanes_needed <= 8) {
-        cudaFuncSetAttribute(k_sls_async<8, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sls_async<8, 4>, 128, SMEM);
-      } else {
-        cudaFuncSetAttribute(k_sls_async<16, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sls_async<16, 2>, 128, SMEM);
-      }
-      grid = sms * (per_sm > 0 ? per_sm : 1);
-    }
-    if (lanes_needed <= 8)
-      k_sls_async<8, 4><<<grid, 128, SMEM, s>>>(tables, tab_off, row_stride, rows, indices, offsets,
-                                                 B, dB, T, D, X, x_stride_items, x_slot0, flag);
-    else
-      k_sls_async<16, 2><<<grid, 128, SMEM, s>>>(tables, tab_off, row_stride, rows, indices, offsets,
-                                                  B, dB, T, D, X, x_stride_items, x_slot0, flag);
-  } else if (lanes_needed <= 8) {
+  if (lanes_needed <= 8) {
     launch_l<8>(tables, tab_off, row_stride, rows, indices, offsets, B, dB, T, D, X, x_stride_items, x_slot0, flag, s);
   } else if (lanes_needed <= 16) {
     launch_l<16>(tables, tab_off, row_stride, rows, indices, offsets, B, dB, T, D, X, x_stride_items, x_slot0, flag, s);

@@ -2,15 +2,9 @@
 // (G2-G5).  Every value is bit-identical to oracle/gen.py.
 #include "common.cuh"
 #include "kernels.h"
+#include "synth.cuh"
 
 namespace rec {
-
-__device__ __forceinline__ float pow2f(int e) {  // exact 2^e for e in [-126, 127]
-  return __int_as_float((127 + e) << 23);
-}
-__device__ __forceinline__ float i8(uint32_t w) {
-  return static_cast<float>(static_cast<int>(static_cast<int8_t>(w & 0xFFu)));
-}
 
 // ------------------------------------------------------------------ tables (G4)
 // Element (r, k) of table t is stored at base[r * stride + k] (base = start of row 0 of t).
@@ -75,32 +69,6 @@ void launch_init_final(float* w, float* b, int K, int layer, int e, uint32_t k0,
   k_init_final<<<4, 256, 0, s>>>(w, b, K, layer, e, k0, k1);
 }
 
-// ------------------------------------------------------------ batch rows (q, item)
-__device__ __forceinline__ int2 row_item(const SegBatch& sb, int b) {
-  const int4* segs = sb.nseg > kParamSegs ? sb.gsegs : sb.seg;
-  int lo = 0, hi = sb.nseg - 1;  // last segment with first_row <= b
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (segs[mid].w <= b) lo = mid; else hi = mid - 1;
-  }
-  const int4 sg = segs[lo];
-  return make_int2(sg.x, sg.y + (b - sg.w));
-}
-
-// ---------------------------------------------------------------------- indices (G2)
-__device__ __forceinline__ int gen_index(uint32_t j, uint32_t it, uint32_t c2, uint32_t q,
-                                         uint32_t k0, uint32_t k1, uint64_t R, int index_dist) {
-  const U4 w = philox(j, it, c2, q, k0, k1);
-  uint64_t r = (static_cast<uint64_t>(w.y) << 32) | w.x;
-  if (index_dist == 2) r = __umul64hi(r, (static_cast<uint64_t>(w.w) << 32) | w.z);
-  return static_cast<int>(__umul64hi(r, R));
-}
-
-__device__ __forceinline__ float gen_dense(uint32_t f, uint32_t it, uint32_t q, uint32_t k0,
-                                           uint32_t k1) {
-  return i8(philox(f, it, DOM_DENSE, q, k0, k1).x) * pow2f(-7);
-}
-
 // ------------------------------------------------ fused inputs, fixed pooling (a2)
 // Blocks [0, nbag_blocks): one warp per bag g = t*B + b (offsets[g] = g*L, L indices);
 // blocks beyond: one warp per batch row (dense features).  One launch for all of a2.
@@ -138,6 +106,35 @@ __global__ void __launch_bounds__(32 * kGenWPB) k_gen_fused(const __grid_constan
       ga.dense_bf[static_cast<int64_t>(b) * ga.Fpad + f] = __float2bfloat16_rn(v);
     }
   }
+}
+
+// Dense features only (fixed-pooling synthetic path, where the SLS kernel generates its own
+// indices): one warp per batch row, bf16 padded row for the bottom MLP.
+__global__ void __launch_bounds__(32 * kGenWPB) k_gen_dense_seg(const __grid_constant__ SegBatch sb,
+                                                                const GenArgs ga) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) *ga.dB = sb.B;
+  const int b = blockIdx.x * kGenWPB + (threadIdx.x >> 5);
+  if (b >= sb.B) return;
+  const int lane = threadIdx.x & 31;
+  const int2 qi = row_item(sb, b);
+  for (int f = lane; f < ga.Fpad; f += 32) {
+    float v = 0.f;
+    if (f < ga.F) v = gen_dense(f, qi.y, qi.x, ga.k0, ga.k1);
+    ga.dense_bf[static_cast<int64_t>(b) * ga.Fpad + f] = __float2bfloat16_rn(v);
+  }
+}
+
+void* gen_dense_seg_kernel(const GenArgs& ga, dim3* grid, dim3* block) {
+  *grid = dim3((ga.cap + kGenWPB - 1) / kGenWPB);
+  *block = dim3(32 * kGenWPB);
+  return reinterpret_cast<void*>(k_gen_dense_seg);
+}
+
+void launch_gen_dense_seg(const SegBatch& sb, const GenArgs& ga, cudaStream_t s) {
+  dim3 grid, block;
+  void* fn = gen_dense_seg_kernel(ga, &grid, &block);
+  void* args[2] = {const_cast<SegBatch*>(&sb), const_cast<GenArgs*>(&ga)};
+  cudaLaunchKernel(fn, grid, block, args, 0, s);
 }
 
 // Variable pooling, step 1: rows (q, item) of the batch + the device batch size.

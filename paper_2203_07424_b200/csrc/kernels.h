@@ -42,6 +42,9 @@ struct GenArgs {
 // variable pooling).  Both take (SegBatch, GenArgs) so graph updates are uniform.
 void* gen_first_kernel(const GenArgs& ga, dim3* grid, dim3* block);
 void launch_gen_first(const SegBatch& sb, const GenArgs& ga, cudaStream_t s);
+// Fixed pooling, fused path: dense features only (indices are generated inside the SLS).
+void* gen_dense_seg_kernel(const GenArgs& ga, dim3* grid, dim3* block);
+void launch_gen_dense_seg(const SegBatch& sb, const GenArgs& ga, cudaStream_t s);
 // Variable pooling only (after launch_gen_first): lengths + scan, indices, dense.
 void launch_gen_variable_rest(const GenArgs& ga, cudaStream_t s);
 void launch_dense_to_bf16(const float* dense, int B, int F, int Fpad, __nv_bfloat16* out,
@@ -55,6 +58,23 @@ void launch_check_offsets(const int* offsets, int nbags, int* flag, cudaStream_t
 void launch_sls(const float* tables, const int64_t* tab_off, int64_t row_stride,
                 const int64_t* rows, const int* indices, const int* offsets, int B, const int* dB,
                 int T, int D, float* X, int x_stride_items, int x_slot0, int* flag, cudaStream_t s);
+
+// SLS over device-synthesised indices (fixed pooling L): each index is the Philox value of
+// (slot, item, table, qid) computed where it is consumed (a2 fused into a3): no index array,
+// no dependency on an input kernel.  Writes X slots 1..T and *dB = batch.
+struct SlsSynthArgs {
+  const float* tables;
+  const int64_t* tab_off;
+  int64_t row_stride;
+  const int64_t* rows;
+  int cap, T, D, L, index_dist;
+  uint32_t k0, k1;
+  float* X;
+  int x_stride;
+  int* dB;
+};
+void* sls_synth_kernel(const SlsSynthArgs& a, dim3* grid, dim3* block);
+void launch_sls_synth(const SegBatch& sb, const SlsSynthArgs& a, cudaStream_t s);
 
 // ----------------------------------------------------------- tcgen05 GEMM (a4, a6)
 enum GemmMode : int { GEMM_OUT_BF16 = 0, GEMM_OUT_X_F32 = 1, GEMM_OUT_CTR = 2 };

@@ -88,23 +88,18 @@ static void prof_collect(rec_model_s* m) {
 }
 
 // ------------------------------------------------------------------ forward chain
-// B = batch, or the workspace capacity when dB != nullptr (then every kernel reads the batch
-// from *dB: the form captured in CUDA graphs).  The bottom MLP (a4) depends only on the
-// dense features, the SLS (a3) only on the sparse ones: they run on two streams (a fork in
-// the captured graph) and join before the interaction (a5), which needs both.
-// gev (graph capture): stage events 2 = SLS done, 3 = join, 4 = interaction done, 5 = top
-// done, 6/7 = bottom start/end on the branch stream.
-rec_status forward_enqueue(rec_model_s* m, Workspace& w, const int* indices, const int* offsets,
-                           int B, const int* dB, float* ctr_out, float* logit_out, cudaEvent_t* gev) {
+// Stage helpers.  B = batch, or the workspace capacity when dB != nullptr (then every kernel
+// reads the batch from *dB: the form captured in CUDA graphs).  gev != nullptr: graph capture
+// with stage events recorded as external event nodes; else per-kernel profiling events.
+//   gev: 0 chain start, 1 inputs done, 2 SLS done, 3 join, 4 interaction done, 5 top done,
+//        6/7 bottom-branch start/end (the branch stream)
+static inline void mark(cudaEvent_t* gev, int i, cudaStream_t st) {
+  if (gev) cudaEventRecordWithFlags(gev[i], st, cudaEventRecordExternal);
+}
+
+static void enqueue_bottom(rec_model_s* m, Workspace& w, cudaStream_t st, int B, const int* dB,
+                           cudaEvent_t* gev) {
   const int T = m->T, D = m->D;
-  cudaStream_t s = w.stream, sb = w.stream_b;
-  auto mark = [&](int i, cudaStream_t st) {
-    if (gev) cudaEventRecordWithFlags(gev[i], st, cudaEventRecordExternal);
-  };
-  // fork: bottom MLP on the branch stream
-  REC_CUDA(cudaEventRecord(w.ev_fork, s));
-  REC_CUDA(cudaStreamWaitEvent(sb, w.ev_fork, 0));
-  mark(6, sb);
   const int nb = static_cast<int>(m->bottom.size());
   for (int l = 0; l < nb; ++l) {
     const Layer& L = m->bottom[l];
@@ -124,25 +119,21 @@ rec_status forward_enqueue(rec_model_s* m, Workspace& w, const int* indices, con
       a.out_bf16 = static_cast<__nv_bfloat16*>(w.out_bottom[l]);
       a.ldo = L.Npad;
     }
-    cudaEvent_t e = gev ? nullptr : prof_begin(m, sb);
-    launch_gemm_tc(&w.tmap_a_bottom[l], &L.tmap_w, a, sb);
-    prof_end(m, sb, 1, e);
+    cudaEvent_t e = gev ? nullptr : prof_begin(m, st);
+    launch_gemm_tc(&w.tmap_a_bottom[l], &L.tmap_w, a, st);
+    prof_end(m, st, 1, e);
   }
-  mark(7, sb);
-  REC_CUDA(cudaEventRecord(w.ev_join, sb));
-  // a3: SLS -> X slots 1..T on the main stream
-  cudaEvent_t e0 = gev ? nullptr : prof_begin(m, s);
-  launch_sls(m->tables, m->d_tab_off, m->row_stride, m->d_rows, indices, offsets, B, dB, T, D, w.X,
-             (T + 1) * D, 1, w.flag, s);
-  prof_end(m, s, 0, e0);
-  mark(2, s);
-  REC_CUDA(cudaStreamWaitEvent(s, w.ev_join, 0));  // join
-  mark(3, s);
+  m->launches += nb;
+}
+
+static void enqueue_interact_top(rec_model_s* m, Workspace& w, cudaStream_t st, int B, const int* dB,
+                                 float* ctr_out, float* logit_out, cudaEvent_t* gev) {
+  const int T = m->T, D = m->D;
   // a5: interaction -> A_top
-  cudaEvent_t e1 = gev ? nullptr : prof_begin(m, s);
-  launch_interact(w.X, B, dB, T, D, w.A_top, m->Ktop_pad, s);
-  prof_end(m, s, 2, e1);
-  mark(4, s);
+  cudaEvent_t e1 = gev ? nullptr : prof_begin(m, st);
+  launch_interact(w.X, B, dB, T, D, w.A_top, m->Ktop_pad, st);
+  prof_end(m, st, 2, e1);
+  mark(gev, 4, st);
   // a6: top MLP; the last hidden layer's epilogue applies the width-1 layer + sigmoid
   const int nt = static_cast<int>(m->top.size());
   for (int j = 0; j < nt; ++j) {
@@ -165,12 +156,35 @@ rec_status forward_enqueue(rec_model_s* m, Workspace& w, const int* indices, con
       a.out_bf16 = static_cast<__nv_bfloat16*>(w.out_top[j]);
       a.ldo = L.Npad;
     }
-    cudaEvent_t e = gev ? nullptr : prof_begin(m, s);
-    launch_gemm_tc(&w.tmap_a_top[j], &L.tmap_w, a, s);
-    prof_end(m, s, 1, e);
+    cudaEvent_t e = gev ? nullptr : prof_begin(m, st);
+    launch_gemm_tc(&w.tmap_a_top[j], &L.tmap_w, a, st);
+    prof_end(m, st, 1, e);
   }
-  mark(5, s);
-  m->launches += 2 + nb + nt;
+  mark(gev, 5, st);
+  m->launches += 1 + nt;
+}
+
+// Forward over materialised inputs (w.indices / caller arrays).  The bottom MLP (a4)
+// depends only on the dense features and the SLS (a3) only on the sparse ones: they run on
+// two streams (a fork in a captured graph) and join before the interaction (a5).
+rec_status forward_enqueue(rec_model_s* m, Workspace& w, const int* indices, const int* offsets,
+                           int B, const int* dB, float* ctr_out, float* logit_out, cudaEvent_t* gev) {
+  cudaStream_t s = w.stream, sb = w.stream_b;
+  REC_CUDA(cudaEventRecord(w.ev_fork, s));
+  REC_CUDA(cudaStreamWaitEvent(sb, w.ev_fork, 0));
+  mark(gev, 6, sb);
+  enqueue_bottom(m, w, sb, B, dB, gev);
+  mark(gev, 7, sb);
+  REC_CUDA(cudaEventRecord(w.ev_join, sb));
+  cudaEvent_t e0 = gev ? nullptr : prof_begin(m, s);
+  launch_sls(m->tables, m->d_tab_off, m->row_stride, m->d_rows, indices, offsets, B, dB, m->T, m->D,
+             w.X, (m->T + 1) * m->D, 1, w.flag, s);
+  prof_end(m, s, 0, e0);
+  m->launches += 1;
+  mark(gev, 2, s);
+  REC_CUDA(cudaStreamWaitEvent(s, w.ev_join, 0));  // join
+  mark(gev, 3, s);
+  enqueue_interact_top(m, w, s, B, dB, ctr_out, logit_out, gev);
   cudaError_t err = cudaGetLastError();
   if (err != cudaSuccess) return cuda_fail(err, "forward kernel launch");
   return REC_OK;
@@ -181,7 +195,8 @@ static rec_status wait_pin(Workspace& w) {
   return REC_OK;
 }
 
-static void fill_genargs(rec_model_s* m, Workspace& w, GenArgs& ga, float* dense_f32_out) {
+static void fill_genargs(rec_model_s* m, Workspace& w, GenArgs& ga, SlsSynthArgs& sa,
+                         float* dense_f32_out) {
   ga = GenArgs{};
   ga.cap = w.cap;
   ga.T = m->T;
@@ -201,28 +216,93 @@ static void fill_genargs(rec_model_s* m, Workspace& w, GenArgs& ga, float* dense
   ga.rowq = w.rowq;
   ga.rowi = w.rowi;
   ga.dB = w.dB;
+  sa = SlsSynthArgs{};
+  sa.tables = m->tables;
+  sa.tab_off = m->d_tab_off;
+  sa.row_stride = m->row_stride;
+  sa.rows = m->d_rows;
+  sa.cap = w.cap;
+  sa.T = m->T;
+  sa.D = m->D;
+  sa.L = m->lo;
+  sa.index_dist = m->index_dist;
+  sa.k0 = m->k0;
+  sa.k1 = m->k1;
+  sa.X = w.X;
+  sa.x_stride = (m->T + 1) * m->D;
+  sa.dB = w.dB;
 }
 
-// The device-synthesised batch chain: input generation (G2-G4, a2) from the slot's batch
-// descriptor, then the forward (a3-a6) with CTRs in w.ctr.  Every kernel after the first
-// reads the batch size from w.dB, so the chain is captured ONCE per slot as a CUDA graph
-// and re-targeted per batch by updating the first kernel's by-value parameters.
-static rec_status synth_chain(rec_model_s* m, Workspace& w, SynthSlot& sl, bool capture) {
-  cudaStream_t s = w.stream;
+static const cudaGraphNode_t* last_node(cudaStream_t s, size_t* n) {
+  cudaStreamCaptureStatus cs;
+  const cudaGraphNode_t* deps = nullptr;
+  if (cudaStreamGetCaptureInfo(s, &cs, nullptr, nullptr, &deps, n) != cudaSuccess) *n = 0;
+  return deps;
+}
+
+// A device-synthesised batch described by the slot's SegBatch (a2-a6, CTRs into w.ctr).
+//  * fused (fixed pooling, serving/bench path): branch stream = dense features -> bottom MLP;
+//    main stream = SLS over Philox indices generated in-kernel; join -> interaction -> top.
+//    Both first kernels take the batch by value, so a captured graph is re-targeted per batch
+//    by two kernel-node parameter updates (no host->device copy).
+//  * materialised (variable pooling, rec_gen_batch): input kernels write indices / offsets /
+//    dense, then the generic forward.
+static rec_status synth_chain(rec_model_s* m, Workspace& w, SynthSlot& sl, bool capture,
+                              bool materialize) {
+  cudaStream_t s = w.stream, sb = w.stream_b;
   cudaEvent_t* gev = capture ? sl.ev : nullptr;
-  if (gev) cudaEventRecordWithFlags(gev[0], s, cudaEventRecordExternal);
+  mark(gev, 0, s);
+  if (!materialize && m->lo == m->hi) {
+    REC_CUDA(cudaEventRecord(w.ev_fork, s));
+    REC_CUDA(cudaStreamWaitEvent(sb, w.ev_fork, 0));
+    mark(gev, 6, sb);
+    cudaEvent_t ed = gev ? nullptr : prof_begin(m, sb);
+    launch_gen_dense_seg(*sl.sb, sl.ga, sb);
+    prof_end(m, sb, 3, ed);
+    if (capture) {
+      size_t n = 0;
+      const cudaGraphNode_t* d = last_node(sb, &n);
+      if (n != 1) {
+        set_error("graph capture: dense node not found");
+        return REC_E_CUDA;
+      }
+      sl.dense_node = d[0];
+    }
+    enqueue_bottom(m, w, sb, w.cap, w.dB, gev);
+    mark(gev, 7, sb);
+    REC_CUDA(cudaEventRecord(w.ev_join, sb));
+    mark(gev, 1, s);
+    cudaEvent_t e0 = gev ? nullptr : prof_begin(m, s);
+    launch_sls_synth(*sl.sb, sl.sa, s);
+    prof_end(m, s, 0, e0);
+    if (capture) {
+      size_t n = 0;
+      const cudaGraphNode_t* d = last_node(s, &n);
+      if (n != 1) {
+        set_error("graph capture: SLS node not found");
+        return REC_E_CUDA;
+      }
+      sl.gen_node = d[0];
+    }
+    m->launches += 2;
+    mark(gev, 2, s);
+    REC_CUDA(cudaStreamWaitEvent(s, w.ev_join, 0));
+    mark(gev, 3, s);
+    enqueue_interact_top(m, w, s, w.cap, w.dB, w.ctr, w.logit, gev);
+    cudaError_t err = cudaGetLastError();
+    if (err != cudaSuccess) return cuda_fail(err, "synthetic chain launch");
+    return REC_OK;
+  }
   cudaEvent_t e = gev ? nullptr : prof_begin(m, s);
   launch_gen_first(*sl.sb, sl.ga, s);
   if (capture) {
-    cudaStreamCaptureStatus cs;
-    const cudaGraphNode_t* deps = nullptr;
-    size_t ndeps = 0;
-    REC_CUDA(cudaStreamGetCaptureInfo(s, &cs, nullptr, nullptr, &deps, &ndeps));
-    if (ndeps != 1) {
-      set_error("graph capture: expected one dependency after the input kernel, got %zu", ndeps);
+    size_t n = 0;
+    const cudaGraphNode_t* d = last_node(s, &n);
+    if (n != 1) {
+      set_error("graph capture: input node not found");
       return REC_E_CUDA;
     }
-    sl.gen_node = deps[0];
+    sl.gen_node = d[0];
   }
   if (m->lo != m->hi) {
     launch_gen_variable_rest(sl.ga, s);
@@ -231,7 +311,7 @@ static rec_status synth_chain(rec_model_s* m, Workspace& w, SynthSlot& sl, bool 
     m->launches += 1;
   }
   prof_end(m, s, 3, e);
-  if (gev) cudaEventRecordWithFlags(gev[1], s, cudaEventRecordExternal);
+  mark(gev, 1, s);
   return forward_enqueue(m, w, w.indices, w.offsets, w.cap, w.dB, w.ctr, w.logit, gev);
 }
 
@@ -239,7 +319,7 @@ rec_status capture_graphs(rec_model_s* m, Workspace& w) {
   for (auto& sl : w.slots) {
     const int64_t before = m->launches;
     REC_CUDA(cudaStreamBeginCapture(w.stream, cudaStreamCaptureModeThreadLocal));
-    rec_status st = synth_chain(m, w, sl, true);
+    rec_status st = synth_chain(m, w, sl, true, false);
     cudaGraph_t g = nullptr;
     cudaError_t ce = cudaStreamEndCapture(w.stream, &g);
     if (st != REC_OK) return st;
@@ -261,7 +341,7 @@ static void collect_slot(rec_model_s* m, SynthSlot& sl) {
     cudaEventElapsedTime(&x, sl.ev[a], sl.ev[b]);
     return x;
   };
-  // 0 gen 1 (fork) ... SLS ... 2 ; 6 bottom 7 ; join 3 ; interact 4 ; top 5
+  // 0 inputs 1 | SLS 2 | branch 6 [dense gen] bottom 7 | join 3 | interact 4 | top 5
   t[0] = el(0, 1);
   t[1] = el(1, 2);
   t[2] = el(6, 7) + el(4, 5);
@@ -322,22 +402,31 @@ rec_status synth_submit(rec_model_s* m, Workspace& w, const int32_t* segs, int n
   }
   const bool direct = dense_f32_out != nullptr || !sl.exec;
   if (!direct) {
+    const bool fused = m->lo == m->hi;
     dim3 grid, block;
     cudaKernelNodeParams kp{};
-    kp.func = gen_first_kernel(sl.ga, &grid, &block);
+    void* args_a[2] = {sl.sb, fused ? static_cast<void*>(&sl.sa) : static_cast<void*>(&sl.ga)};
+    kp.func = fused ? sls_synth_kernel(sl.sa, &grid, &block) : gen_first_kernel(sl.ga, &grid, &block);
     kp.gridDim = grid;
     kp.blockDim = block;
-    kp.sharedMemBytes = 0;
-    void* args[2] = {sl.sb, &sl.ga};
-    kp.kernelParams = args;
+    kp.kernelParams = args_a;
     REC_CUDA(cudaGraphExecKernelNodeSetParams(sl.exec, sl.gen_node, &kp));
+    if (fused) {
+      cudaKernelNodeParams kd{};
+      void* args_d[2] = {sl.sb, &sl.ga};
+      kd.func = gen_dense_seg_kernel(sl.ga, &grid, &block);
+      kd.gridDim = grid;
+      kd.blockDim = block;
+      kd.kernelParams = args_d;
+      REC_CUDA(cudaGraphExecKernelNodeSetParams(sl.exec, sl.dense_node, &kd));
+    }
     REC_CUDA(cudaGraphLaunch(sl.exec, w.stream));
     m->launches += w.graph_kernels;
     sl.prof_pending = m->prof;
   } else {
     GenArgs saved = sl.ga;
     sl.ga.dense_f32 = dense_f32_out;
-    rec_status st = synth_chain(m, w, sl, false);
+    rec_status st = synth_chain(m, w, sl, false, dense_f32_out != nullptr);
     sl.ga = saved;
     if (st != REC_OK) return st;
   }
@@ -860,7 +949,7 @@ rec_status rec_model_create(const rec_model_desc* d, rec_model_t* out) {
       sl.sb->B = 1;
       sl.sb->nseg = 1;
       sl.sb->seg[0] = make_int4(0, 0, 1, 0);
-      fill_genargs(m, w, sl.ga, nullptr);
+      fill_genargs(m, w, sl.ga, sl.sa, nullptr);
       CHECK_CUDA_CREATE(cudaEventCreateWithFlags(&sl.free, cudaEventDisableTiming));
       CHECK_CUDA_CREATE(cudaEventRecord(sl.free, w.stream));
       for (auto& e : sl.ev) CHECK_CUDA_CREATE(cudaEventCreate(&e));

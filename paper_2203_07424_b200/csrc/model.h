@@ -36,10 +36,12 @@ struct Layer {
 struct SynthSlot {
   SegBatch* sb = nullptr;            // host copy of the first kernel's by-value parameter
   GenArgs ga{};
+  SlsSynthArgs sa{};
   cudaEvent_t free = nullptr;        // the last launch that used this slot completed
   cudaGraph_t graph = nullptr;       // kept alive: gen_node belongs to it
   cudaGraphExec_t exec = nullptr;
-  cudaGraphNode_t gen_node = nullptr;
+  cudaGraphNode_t gen_node = nullptr;   // first kernel of the main stream (SLS or inputs)
+  cudaGraphNode_t dense_node = nullptr; // fused path: dense-feature kernel on the branch
   cudaEvent_t ev[8] = {};            // stage boundaries inside the graph (timing)
   bool prof_pending = false;
 };
