@@ -233,8 +233,10 @@ def run_ours(args):
         ev0.record(stream)
         for s in streams[1:]:
             s.wait_event(ev0)                    # fork: every stream starts after ev0
+        t_host0 = time.perf_counter()
         for i in range(args.warmup, args.warmup + args.steps):
             step(i)
+        host_submit_s = time.perf_counter() - t_host0
         for s in streams[1:]:
             e = torch.cuda.Event()
             e.record(s)
@@ -348,6 +350,7 @@ def run_ours(args):
                 "gen": 1e3 * gen_ms / rsteps, "sls": 1e3 * sls_ms / rsteps,
                 "gemm": 1e3 * gemm_ms / rsteps, "interact": 1e3 * int_ms / rsteps},
             "gpu_launches": int(launches),
+            "host_submit_us_per_step": 1e6 * host_submit_s / args.steps,
             "clocks": clk.summary(),
             "e2e": e2e,
             "cpu_baseline": cpu,

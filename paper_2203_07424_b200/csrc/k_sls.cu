@@ -11,6 +11,8 @@
 // the bag's indices LANES at a time (one per lane), broadcasts them with shuffles, and keeps
 // LANES independent 128-bit row loads in flight per lane (ld.global.nc.L1::no_allocate —
 // rows are streamed, never reused from L1) before accumulating them in order.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.h"
 #include "synth.cuh"
@@ -33,11 +35,11 @@ __device__ __forceinline__ float4 ldg_row(const float4* base, uint32_t row, uint
 // Per round a group consumes ROWS = IPL * LANES indices (IPL per lane, prefetched one round
 // ahead so the index load never sits in front of the row loads) and issues the row loads in
 // sub-batches of U = 8 independent 128-bit loads per lane before accumulating them in order.
-template <int LANES>
+template <int LANES, int RIF = 8>
 struct SlsShape {
-  static constexpr int IPL = 1;
+  static constexpr int IPL = RIF > LANES ? RIF / LANES : 1;
   static constexpr int ROWS = IPL * LANES;
-  static constexpr int U = 8;  // 8 x 16 B in flight per lane keeps ~90 regs: 5 CTAs of 128/SM
+  static constexpr int U = RIF;  // RIF x 16 B in flight per lane (8: ~90 regs, 5 CTAs of 128/SM)
 };
 
 template <int LANES, int THREADS>
@@ -134,10 +136,10 @@ __global__ void __launch_bounds__(THREADS, 5) k_sls(const float* __restrict__ ta
 // accumulate structure, but lane `sub` computes the index of slot base + sub with Philox
 // (G2) instead of loading it, so the kernel has no predecessor in the chain and
 // no dependent index load in front of its first row loads.
-template <int LANES, int THREADS>
-__global__ void __launch_bounds__(THREADS, 5) k_sls_synth(const __grid_constant__ SegBatch sb,
-                                                          const SlsSynthArgs a) {
-  using S = SlsShape<LANES>;
+template <int LANES, int THREADS, int RIF>
+__global__ void __launch_bounds__(THREADS, RIF > 8 ? 4 : 5) k_sls_synth(const __grid_constant__ SegBatch sb,
+                                                                        const SlsSynthArgs a) {
+  using S = SlsShape<LANES, RIF>;
   constexpr int GROUPS = THREADS / LANES;
   const int B = sb.B;
   if (blockIdx.x == 0 && threadIdx.x == 0) *a.dB = B;
@@ -157,7 +159,12 @@ __global__ void __launch_bounds__(THREADS, 5) k_sls_synth(const __grid_constant_
                                        : (((1u << LANES) - 1u) << ((threadIdx.x & 31) & ~(LANES - 1)));
   const int L = a.L;
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-  int cur = sub < L ? gen_index(sub, qi.y, c2, qi.x, a.k0, a.k1, R, a.index_dist) : 0;
+  int cur[S::IPL];
+#pragma unroll
+  for (int q = 0; q < S::IPL; ++q) {
+    const int j = q * LANES + sub;
+    cur[q] = j < L ? gen_index(j, qi.y, c2, qi.x, a.k0, a.k1, R, a.index_dist) : 0;
+  }
   for (int base = 0; base < L; base += S::ROWS) {
     const int n = min(S::ROWS, L - base);
 #pragma unroll
@@ -167,12 +174,15 @@ __global__ void __launch_bounds__(THREADS, 5) k_sls_synth(const __grid_constant_
 #pragma unroll
       for (int k = 0; k < S::U; ++k) {
         const int r = kk + k;
-        const int rr = __shfl_sync(gmask, cur, r % LANES, LANES);
+        const int rr = __shfl_sync(gmask, cur[r / LANES], r % LANES, LANES);
         if (r < n) v[k] = ldg_row(tab, static_cast<uint32_t>(rr), stride_bytes);
       }
-      if (kk + S::U >= S::ROWS) {  // next round's index, computed while the rows are in flight
-        const int j = base + S::ROWS + sub;
-        cur = j < L ? gen_index(j, qi.y, c2, qi.x, a.k0, a.k1, R, a.index_dist) : 0;
+      if (kk + S::U >= S::ROWS) {  // next round's indices, computed while the rows are in flight
+#pragma unroll
+        for (int q = 0; q < S::IPL; ++q) {
+          const int j = base + S::ROWS + q * LANES + sub;
+          cur[q] = j < L ? gen_index(j, qi.y, c2, qi.x, a.k0, a.k1, R, a.index_dist) : 0;
+        }
       }
 #pragma unroll
       for (int k = 0; k < S::U; ++k) {
@@ -192,13 +202,19 @@ __global__ void __launch_bounds__(THREADS, 5) k_sls_synth(const __grid_constant_
 
 void* sls_synth_kernel(const SlsSynthArgs& a, dim3* grid, dim3* block) {
   constexpr int THREADS = 128;
+  static const int rif16 = [] {  // REC_SLS_RIF=16: 16 rows in flight per lane (experiment)
+    const char* e = getenv("REC_SLS_RIF");
+    return (e && atoi(e) == 16) ? 1 : 0;
+  }();
   const int L = a.D / 4 <= 8 ? 8 : a.D / 4 <= 16 ? 16 : 32;
   const int nb = a.T * a.cap;
   *grid = dim3((nb + THREADS / L - 1) / (THREADS / L));
   *block = dim3(THREADS);
-  if (L == 8) return reinterpret_cast<void*>(k_sls_synth<8, THREADS>);
-  if (L == 16) return reinterpret_cast<void*>(k_sls_synth<16, THREADS>);
-  return reinterpret_cast<void*>(k_sls_synth<32, THREADS>);
+  if (L == 8) return rif16 ? reinterpret_cast<void*>(k_sls_synth<8, THREADS, 16>)
+                           : reinterpret_cast<void*>(k_sls_synth<8, THREADS, 8>);
+  if (L == 16) return rif16 ? reinterpret_cast<void*>(k_sls_synth<16, THREADS, 16>)
+                            : reinterpret_cast<void*>(k_sls_synth<16, THREADS, 8>);
+  return reinterpret_cast<void*>(k_sls_synth<32, THREADS, 8>);
 }
 
 void launch_sls_synth(const SegBatch& sb, const SlsSynthArgs& a, cudaStream_t s) {
