@@ -109,10 +109,18 @@ rec_status rec_query_async(rec_model_t m, int32_t slot, const float* dense,
 
 /* Device-synthesised batch (serving input mode REC_INPUT_DEVICE_SYNTH):
  * the batch is the concatenation of item segments segs[nseg][3] = (qid, start, len)
- * (host memory); indices/offsets/dense are generated on the device (G2-G4) and the
- * forward runs on stream slot `slot`.  ctr [sum len] fp32 DEVICE pointer.  Async. */
+ * (host memory); its inputs are generated on the device (G2-G4) and the forward runs on
+ * stream slot `slot`.  ctr [sum len] fp32 DEVICE pointer, or NULL (the CTRs stay in the
+ * stream's workspace).  Async. */
 rec_status rec_synth_query_async(rec_model_t m, int32_t slot, const int32_t* segs,
                                  int32_t nseg, float* ctr);
+
+/* Submit nbatches device-synthesised batches (as rec_synth_query_async with ctr = NULL:
+ * CTRs stay in each stream's workspace), batch b = segments segs[batch_start[b] ..
+ * batch_start[b+1]) on stream slot (first_slot + b) % streams — model co-location
+ * round-robin without a host round trip per batch.  Async. */
+rec_status rec_synth_query_batches(rec_model_t m, const int32_t* segs, const int64_t* batch_start,
+                                   int64_t nbatches, int32_t first_slot);
 
 /* Wait for stream slot `slot`; returns INDEX_OOB / OFFSETS if a kernel flagged it. */
 rec_status rec_sync(rec_model_t m, int32_t slot);
@@ -129,7 +137,9 @@ rec_status rec_gen_batch(rec_model_t m, const int32_t* segs, int32_t nseg,
 /* Per-kernel device time accumulated while profiling is on (CUDA events recorded on
  * the launching stream around every launch).  kernel: 0 = SLS, 1 = GEMM (all layers),
  * 2 = interaction, 3 = input generation; kernel = 4 returns in *launches the number of
- * kernels this handle has launched so far (all streams; *total_ms = 0).
+ * kernels this handle has launched so far (all streams; *total_ms = 0); kernels 5..8 return
+ * host time of the synthetic submit path (5 graph-parameter updates, 6 graph launches,
+ * 7 slot waits, 8 total).
  * enable != 0 turns recording on and resets the times. */
 rec_status rec_profile(rec_model_t m, int32_t enable);
 rec_status rec_profile_read(rec_model_t m, int32_t kernel, double* total_ms, int64_t* launches);

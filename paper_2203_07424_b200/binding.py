@@ -31,7 +31,8 @@ KERNEL_SLS, KERNEL_GEMM, KERNEL_INTERACT, KERNEL_GEN = 0, 1, 2, 3
 EXPORTS = ["rec_model_create", "rec_model_destroy", "rec_query", "rec_query_debug",
            "rec_query_async", "rec_synth_query_async", "rec_sync", "rec_stream_handle",
            "rec_gen_batch", "rec_profile", "rec_profile_read", "rec_serve", "rec_last_error",
-           "rec_nccl_unique_id_size", "rec_nccl_get_unique_id", "rec_version", "rec_split_fuse"]
+           "rec_nccl_unique_id_size", "rec_nccl_get_unique_id", "rec_version", "rec_split_fuse",
+           "rec_synth_query_batches"]
 
 
 class rec_model_desc(C.Structure):
@@ -97,6 +98,8 @@ def lib() -> C.CDLL:
         L.rec_version.restype = i32
         L.rec_split_fuse.argtypes = [vp, i64, i32, vp, i64, vp, i64, C.POINTER(i64), C.POINTER(i64)]
         L.rec_split_fuse.restype = i32
+        L.rec_synth_query_batches.argtypes = [vp, vp, vp, i64, i32]
+        L.rec_synth_query_batches.restype = i32
         for f in ("rec_model_create", "rec_query", "rec_query_debug", "rec_query_async",
                   "rec_synth_query_async", "rec_sync", "rec_gen_batch", "rec_profile",
                   "rec_profile_read", "rec_serve", "rec_nccl_get_unique_id"):
@@ -195,6 +198,11 @@ class RecModel:
     def rec_synth_query_async(self, slot: int, segs: np.ndarray, ctr):
         segs = np.ascontiguousarray(segs, dtype=np.int32).reshape(-1, 3)
         _check(lib().rec_synth_query_async(self.h, slot, _ptr(segs), segs.shape[0], _ptr(ctr)))
+
+    def rec_synth_query_batches(self, segs: np.ndarray, batch_start: np.ndarray, first_slot: int = 0):
+        segs = np.ascontiguousarray(segs, dtype=np.int32).reshape(-1, 3)
+        bs = np.ascontiguousarray(batch_start, dtype=np.int64)
+        _check(lib().rec_synth_query_batches(self.h, _ptr(segs), _ptr(bs), len(bs) - 1, first_slot))
 
     def rec_sync(self, slot: int = 0):
         _check(lib().rec_sync(self.h, slot))

@@ -6,6 +6,7 @@
 // once, and enqueues the per-batch kernel chain  [input] -> SLS -> bottom GEMMs ->
 // interaction -> top GEMMs (+ width-1 layer + sigmoid)  on one CUDA stream per co-located
 // "inference thread" (model co-location).
+#include <chrono>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -357,6 +358,11 @@ static void collect_slot(rec_model_s* m, SynthSlot& sl) {
   sl.prof_pending = false;
 }
 
+static inline double host_now_ns() {
+  return std::chrono::duration<double, std::nano>(std::chrono::steady_clock::now().time_since_epoch())
+      .count();
+}
+
 // segs (host) -> a slot's batch descriptor -> graph launch (inputs + forward) on w.stream.
 // dense_f32_out forces the direct (non-graph) path (rec_gen_batch needs the fp32 dense).
 rec_status synth_submit(rec_model_s* m, Workspace& w, const int32_t* segs, int nseg, int* batch_out,
@@ -377,10 +383,12 @@ rec_status synth_submit(rec_model_s* m, Workspace& w, const int32_t* segs, int n
     set_error("segs: batch of %lld items exceeds max_batch %d", (long long)B, w.cap);
     return REC_E_INVALID_ARG;
   }
+  const double t0 = m->prof ? host_now_ns() : 0.0;
   SynthSlot& sl = w.slots[w.next_slot];
   w.next_slot = (w.next_slot + 1) % static_cast<int>(w.slots.size());
   REC_CUDA(cudaEventSynchronize(sl.free));
   collect_slot(m, sl);
+  const double t1 = m->prof ? host_now_ns() : 0.0;
   SegBatch& sb = *sl.sb;
   sb.B = static_cast<int>(B);
   sb.nseg = nseg;
@@ -420,7 +428,14 @@ rec_status synth_submit(rec_model_s* m, Workspace& w, const int32_t* segs, int n
       kd.kernelParams = args_d;
       REC_CUDA(cudaGraphExecKernelNodeSetParams(sl.exec, sl.dense_node, &kd));
     }
+    const double t2 = m->prof ? host_now_ns() : 0.0;
     REC_CUDA(cudaGraphLaunch(sl.exec, w.stream));
+    if (m->prof) {
+      const double t3 = host_now_ns();
+      m->host_ns[0] += t2 - t1;
+      m->host_ns[1] += t3 - t2;
+      m->host_ns[2] += t1 - t0;
+    }
     m->launches += w.graph_kernels;
     sl.prof_pending = m->prof;
   } else {
@@ -431,6 +446,7 @@ rec_status synth_submit(rec_model_s* m, Workspace& w, const int32_t* segs, int n
     if (st != REC_OK) return st;
   }
   REC_CUDA(cudaEventRecord(sl.free, w.stream));
+  if (m->prof) m->host_ns[3] += host_now_ns() - t0;
   *batch_out = static_cast<int>(B);
   return REC_OK;
 }
@@ -1055,6 +1071,23 @@ rec_status rec_synth_query_async(rec_model_t m, int32_t slot, const int32_t* seg
   return REC_OK;
 }
 
+rec_status rec_synth_query_batches(rec_model_t m, const int32_t* segs, const int64_t* batch_start,
+                                   int64_t nbatches, int32_t first_slot) {
+  if (!m || !segs || !batch_start || nbatches < 0 || first_slot < 0) {
+    set_error("null argument or negative count");
+    return REC_E_INVALID_ARG;
+  }
+  REC_CUDA(cudaSetDevice(m->device));
+  for (int64_t b = 0; b < nbatches; ++b) {
+    Workspace& w = m->ws[(first_slot + b) % m->nstreams];
+    const int64_t s0 = batch_start[b], s1 = batch_start[b + 1];
+    int B = 0;
+    rec_status st = synth_submit(m, w, segs + 3 * s0, static_cast<int>(s1 - s0), &B, nullptr);
+    if (st != REC_OK) return st;
+  }
+  return REC_OK;
+}
+
 rec_status rec_sync(rec_model_t m, int32_t slot) {
   if (!m || slot < 0 || slot >= m->nstreams) {
     set_error("bad model or slot");
@@ -1104,19 +1137,25 @@ rec_status rec_profile(rec_model_t m, int32_t enable) {
   for (int k = 0; k < 4; ++k) {
     m->prof_ms[k] = 0;
     m->prof_n[k] = 0;
+    m->host_ns[k] = 0;
   }
   m->prof = enable != 0;
   return REC_OK;
 }
 
 rec_status rec_profile_read(rec_model_t m, int32_t kernel, double* total_ms, int64_t* launches) {
-  if (!m || kernel < 0 || kernel > 4 || !total_ms || !launches) {
+  if (!m || kernel < 0 || kernel > 8 || !total_ms || !launches) {
     set_error("bad argument");
     return REC_E_INVALID_ARG;
   }
   if (kernel == 4) {  // all kernels launched by this handle (count only)
     *total_ms = 0.0;
     *launches = m->launches;
+    return REC_OK;
+  }
+  if (kernel >= 5 && kernel <= 8) {  // host time of the synthetic submit path
+    *total_ms = m->host_ns[kernel - 5] * 1e-6;
+    *launches = 0;
     return REC_OK;
   }
   for (auto& w : m->ws) REC_CUDA(cudaStreamSynchronize(w.stream));

@@ -119,6 +119,8 @@ struct rec_model_s {
   double prof_ms[4] = {0, 0, 0, 0};
   int64_t prof_n[4] = {0, 0, 0, 0};
   int64_t launches = 0;                // kernels launched by this handle (all streams)
+  double host_ns[4] = {0, 0, 0, 0};    // profiling: host time in synth_submit (params, launch,
+                                       // slot wait+events, total)
   // distributed (sharded modes)
   void* nccl_comm = nullptr;
 };
