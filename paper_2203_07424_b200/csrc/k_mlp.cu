@@ -1,0 +1,239 @@
+// k_mlp.cu — a whole FC stack (bottom MLP, or top MLP + width-1 output) in ONE kernel per
+// 128-row tile (Table I Bottom-FC / Predict-FC).
+//
+// Per-layer GEMM launches are latency chains at serving batch sizes (launch, TMA descriptor
+// and weight fetch, commit, epilogue: 7-10 us each for ~1 us of work, see profiles/).  Here
+// the layers of a tile run back to back inside one CTA:
+//   layer 0:  A = activations from global (TMA, 64-wide K boxes, SWIZZLE_128B)
+//   layer l:  A = the previous layer's output, written by the epilogue warps straight into
+//             shared memory in the same 128-byte-swizzled K-major layout TMA produces, so
+//             tcgen05.mma reads it with the same descriptors
+//   all l:    W = weight tiles streamed by TMA through an S-stage ring (<= 256 rows per
+//             N-chunk), accumulators in TMEM (N <= 512 columns)
+//   epilogue: + bias, ReLU -> bf16 -> smem (hidden layers); the last layer writes fp32 X
+//             slot 0 (bottom) or folds the width-1 output layer + sigmoid (top -> CTR).
+// Warp roles (192 threads): warp 0 TMA producer, warp 1 single-thread MMA issuer, warps 2-5
+// epilogue (warp w owns TMEM lanes 32*(w%4) .. +31, i.e. tile rows).  No split-K, no atomics:
+// an item's result is independent of its batch (batch invariance).
+#include "common.cuh"
+#include "kernels.h"
+#include "sm100.cuh"
+
+namespace rec {
+
+constexpr int CBM = 128;
+constexpr int CBK = 64;
+constexpr int C_A_BYTES = CBM * CBK * 2;     // 16 KB: one A k-block (128 rows x 128 B)
+constexpr int C_W_BYTES = 256 * CBK * 2;     // 32 KB: one W k-block of a <= 256-row N-chunk
+constexpr int C_STAGE = C_A_BYTES + C_W_BYTES;
+
+__device__ __forceinline__ void fence_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ const CUtensorMap* wmap(const ChainMaps& mp, int l) {
+  return l == 0 ? &mp.w0 : l == 1 ? &mp.w1 : l == 2 ? &mp.w2 : &mp.w3;
+}
+
+__global__ void __launch_bounds__(192, 1)
+    k_mlp_chain(const __grid_constant__ ChainMaps maps, const ChainArgs args) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  const int S = args.stages;
+  uint8_t* ring = smem;                                   // S x C_STAGE
+  uint8_t* act = smem + S * C_STAGE;                      // act_kblocks x 16 KB
+  float* s_bias = reinterpret_cast<float*>(act + args.act_kblocks * C_A_BYTES);  // bias_total
+  float* s_wl = s_bias + args.bias_total;                 // [N_last]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(s_wl + args.wl_n + 2);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + S;
+  uint64_t* acc_full = bars + 2 * S;   // MMA -> epilogue, one phase per layer
+  uint64_t* act_ready = bars + 2 * S + 1;  // epilogue -> MMA, one phase per hidden layer
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 2 * S + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m0 = blockIdx.x * CBM;
+  const int M = args.dM ? *args.dM : args.M;
+  if (m0 >= M) return;
+  const int nl = args.nlayers;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      sm100::mbar_init(&full[s], 1);
+      sm100::mbar_init(&empty[s], 1);
+    }
+    sm100::mbar_init(acc_full, 1);
+    sm100::mbar_init(act_ready, 128);
+    sm100::fence_mbar_init();
+    sm100::tma_prefetch_desc(&maps.a0);
+    for (int l = 0; l < nl; ++l) sm100::tma_prefetch_desc(wmap(maps, l));
+  }
+  if (warp == 0) sm100::tmem_alloc(tslot, args.tmem_cols);
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  const uint32_t tmem = *tslot;
+
+  if (warp == 0) {
+    // ------------------------------------------------ TMA producer: (layer, n-chunk, k-block)
+    int it = 0;
+    for (int l = 0; l < nl; ++l) {
+      const int K = args.K[l], N = args.N[l];
+      const int nkb = (K + CBK - 1) / CBK;
+      for (int n0 = 0; n0 < N; n0 += 256) {
+        const int box_rows = args.wbox[l];
+        const uint32_t bytes = (l == 0 ? C_A_BYTES : 0) + box_rows * CBK * 2;
+        for (int kb = 0; kb < nkb; ++kb, ++it) {
+          const int s = it % S, use = it / S;
+          if (use > 0) sm100::mbar_wait(&empty[s], (use - 1) & 1);
+          if (lane == 0) {
+            uint8_t* st = ring + s * C_STAGE;
+            sm100::mbar_arrive_expect_tx(&full[s], bytes);
+            if (l == 0) sm100::tma_load_2d(st, &maps.a0, &full[s], kb * CBK, m0);
+            sm100::tma_load_2d(st + C_A_BYTES, wmap(maps, l), &full[s], kb * CBK, n0);
+          }
+          __syncwarp();
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------ single-thread MMA issuer
+    int it = 0;
+    for (int l = 0; l < nl; ++l) {
+      const int K = args.K[l], N = args.N[l];
+      const int nkb = (K + CBK - 1) / CBK;
+      if (l > 0) {  // the previous layer's activations are in smem; its TMEM has been drained
+        sm100::mbar_wait(act_ready, (l - 1) & 1);
+        sm100::tc_fence_after();
+      }
+      for (int n0 = 0; n0 < N; n0 += 256) {
+        const int nc = min(256, args.wbox[l]);
+        const uint32_t idesc = sm100::idesc_bf16_f32(CBM, nc);
+        for (int kb = 0; kb < nkb; ++kb, ++it) {
+          const int s = it % S, use = it / S;
+          sm100::mbar_wait(&full[s], use & 1);
+          sm100::tc_fence_after();
+          if (lane == 0) {
+            const uint32_t st = sm100::smem_u32(ring + s * C_STAGE);
+            const uint64_t da = sm100::umma_desc_sw128(l == 0 ? st : sm100::smem_u32(act + kb * C_A_BYTES));
+            const uint64_t db = sm100::umma_desc_sw128(st + C_A_BYTES);
+#pragma unroll
+            for (int k = 0; k < CBK / 16; ++k)
+              sm100::mma_bf16_ss(tmem + n0, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
+            sm100::mma_commit(&empty[s]);
+            if (kb == nkb - 1 && n0 + 256 >= N) sm100::mma_commit(acc_full);
+          }
+          __syncwarp();
+        }
+      }
+    }
+  } else {
+    // ------------------------------------------------ epilogue warps 2..5
+    const int et = threadIdx.x - 64;                 // 0..127
+    for (int i = et; i < args.bias_total; i += 128) s_bias[i] = __ldg(&args.bias_all[i]);
+    if (args.mode_last == GEMM_OUT_CTR)
+      for (int i = et; i < args.wl_n; i += 128) s_wl[i] = __ldg(&args.w_last[i]);
+    asm volatile("bar.sync 1, 128;" ::: "memory");   // epilogue warps only
+    const int qw = warp & 3;                         // TMEM lane quarter of this warp
+    const int r = qw * 32 + lane;                    // tile row
+    const int row = m0 + r;
+    const bool row_ok = row < M;
+    const uint32_t trow = tmem + (static_cast<uint32_t>(qw * 32) << 16);
+    int boff = 0;
+    for (int l = 0; l < nl; ++l) {
+      const int N = args.N[l];
+      const bool last = l == nl - 1;
+      sm100::mbar_wait(acc_full, l & 1);
+      sm100::tc_fence_after();
+      float dot = 0.f;
+      const int cols = last ? N : ((N + CBK - 1) / CBK) * CBK;  // hidden: zero the K padding
+#pragma unroll 1
+      for (int c0 = 0; c0 < cols; c0 += 16) {
+        uint32_t rr[16];
+        if (c0 < N) {
+          sm100::tmem_ld_32x32b_x16(trow + c0, rr);
+          sm100::tmem_ld_wait();
+        }
+        float v[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const int c = c0 + j;
+          float x = 0.f;
+          if (c < N) x = fmaxf(__uint_as_float(rr[j]) + s_bias[boff + c], 0.f);
+          v[j] = x;
+        }
+        if (!last) {
+          // bf16 into the swizzled K-major A operand of layer l+1: column c0 lies in k-block
+          // c0/64, 16-byte unit (c0%64)/8 (and the next one), XOR-swizzled by row % 8.
+          uint32_t p[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * j], v[2 * j + 1]);
+            p[j] = *reinterpret_cast<uint32_t*>(&h);
+          }
+          uint8_t* blk = act + (c0 / CBK) * C_A_BYTES + r * 128;
+          const int u = (c0 % CBK) / 8;
+          *reinterpret_cast<uint4*>(blk + ((u ^ (r & 7)) << 4)) = make_uint4(p[0], p[1], p[2], p[3]);
+          *reinterpret_cast<uint4*>(blk + (((u + 1) ^ (r & 7)) << 4)) = make_uint4(p[4], p[5], p[6], p[7]);
+        } else if (args.mode_last == GEMM_OUT_X_F32) {
+          if (row_ok) {
+            float* dst = args.out_f32 + static_cast<int64_t>(row) * args.ldo + c0;
+            if (c0 + 16 <= N) {
+              float4* d4 = reinterpret_cast<float4*>(dst);
+#pragma unroll
+              for (int j = 0; j < 4; ++j) d4[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+            } else {
+#pragma unroll
+              for (int j = 0; j < 16; ++j)
+                if (c0 + j < N) dst[j] = v[j];
+            }
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            if (c0 + j < N) dot = fmaf(v[j], s_wl[c0 + j], dot);
+        }
+      }
+      boff += N;
+      if (!last) {
+        fence_async_smem();          // generic-proxy smem writes -> visible to tcgen05.mma
+        sm100::tc_fence_before();    // our tcgen05.ld of this layer are complete
+        sm100::mbar_arrive(act_ready);
+      } else if (args.mode_last == GEMM_OUT_CTR && row_ok) {
+        const float logit = dot + args.b_last;
+        args.ctr[row] = 1.f / (1.f + __expf(-logit));
+        if (args.logit) args.logit[row] = logit;
+      }
+    }
+  }
+  sm100::tc_fence_before();
+  __syncthreads();
+  if (warp == 0) sm100::tmem_dealloc(tmem, args.tmem_cols);
+}
+
+size_t chain_smem_bytes(const ChainArgs& a) {
+  return 1024 + static_cast<size_t>(a.stages) * C_STAGE + static_cast<size_t>(a.act_kblocks) * C_A_BYTES +
+         sizeof(float) * (a.bias_total + a.wl_n + 2) + 8 * (2 * a.stages + 4);
+}
+
+bool chain_configure(ChainArgs& a) {
+  // stages: as many as fit next to the activation buffer (>= 2)
+  for (int s = 4; s >= 2; --s) {
+    a.stages = s;
+    if (chain_smem_bytes(a) <= 227 * 1024) return true;
+  }
+  return false;
+}
+
+void chain_prepare() {
+  cudaFuncSetAttribute(k_mlp_chain, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+}
+
+void launch_mlp_chain(const ChainMaps& maps, const ChainArgs& a, cudaStream_t s) {
+  if (a.M <= 0) return;
+  const size_t smem = chain_smem_bytes(a);
+  k_mlp_chain<<<(a.M + CBM - 1) / CBM, 192, smem, s>>>(maps, a);
+}
+
+}  // namespace rec

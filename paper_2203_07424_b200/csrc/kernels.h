@@ -101,6 +101,35 @@ void launch_gemm_tc(const CUtensorMap* tmap_a, const CUtensorMap* tmap_w, const 
 bool encode_tmap_bf16(CUtensorMap* map, const void* base, uint64_t rows, uint64_t K,
                       uint64_t ldk, uint32_t box_rows);
 
+// ------------------------------------------- fused FC stack, one CTA per 128 rows (k_mlp.cu)
+struct ChainMaps {
+  CUtensorMap a0;  // layer-0 activations [M][K0] (box 64 x 128)
+  CUtensorMap w0, w1, w2, w3;  // weights of layer l [N_l][K_l] (box 64 x wbox[l])
+};
+struct ChainArgs {
+  int M;
+  const int* dM;          // optional device-side M (grid sized for M = capacity)
+  int nlayers;            // <= 4 GEMM layers, ReLU after every one
+  int K[4], N[4], wbox[4];
+  const float* bias_all;  // concatenated biases of all layers
+  int bias_total;
+  int mode_last;          // GEMM_OUT_X_F32 (bottom) | GEMM_OUT_CTR (top)
+  float* out_f32;         // X slot 0, row stride ldo
+  int ldo;
+  const float* w_last;    // width-1 output layer [N_last] + b_last (top)
+  int wl_n;
+  float b_last;
+  float* ctr;
+  float* logit;
+  int act_kblocks;        // 64-column blocks of the widest hidden activation
+  int tmem_cols;          // power of two >= 32 and >= max N
+  int stages;             // set by chain_configure
+};
+size_t chain_smem_bytes(const ChainArgs& a);
+bool chain_configure(ChainArgs& a);   // false: does not fit in shared memory
+void chain_prepare();                 // per-device kernel attribute
+void launch_mlp_chain(const ChainMaps& maps, const ChainArgs& a, cudaStream_t s);
+
 // --------------------------------------------------------------- interaction (a5)
 void launch_interact(const float* X, int B, const int* dB, int T, int D, __nv_bfloat16* A_top,
                      int ld_top, cudaStream_t s);

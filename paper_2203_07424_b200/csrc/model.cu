@@ -6,8 +6,10 @@
 // once, and enqueues the per-batch kernel chain  [input] -> SLS -> bottom GEMMs ->
 // interaction -> top GEMMs (+ width-1 layer + sigmoid)  on one CUDA stream per co-located
 // "inference thread" (model co-location).
+#include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -102,6 +104,18 @@ static void enqueue_bottom(rec_model_s* m, Workspace& w, cudaStream_t st, int B,
                            cudaEvent_t* gev) {
   const int T = m->T, D = m->D;
   const int nb = static_cast<int>(m->bottom.size());
+  if (m->chain_bottom) {  // whole bottom MLP in one kernel (k_mlp.cu)
+    ChainArgs a = m->chain_bottom_args;
+    a.M = B;
+    a.dM = dB;
+    a.out_f32 = w.X;
+    a.ldo = (T + 1) * D;
+    cudaEvent_t e = gev ? nullptr : prof_begin(m, st);
+    launch_mlp_chain(w.chain_bottom, a, st);
+    prof_end(m, st, 1, e);
+    m->launches += 1;
+    return;
+  }
   for (int l = 0; l < nb; ++l) {
     const Layer& L = m->bottom[l];
     GemmArgs a{};
@@ -137,6 +151,19 @@ static void enqueue_interact_top(rec_model_s* m, Workspace& w, cudaStream_t st, 
   mark(gev, 4, st);
   // a6: top MLP; the last hidden layer's epilogue applies the width-1 layer + sigmoid
   const int nt = static_cast<int>(m->top.size());
+  if (m->chain_top) {  // whole top MLP in one kernel (k_mlp.cu)
+    ChainArgs a = m->chain_top_args;
+    a.M = B;
+    a.dM = dB;
+    a.ctr = ctr_out;
+    a.logit = logit_out;
+    cudaEvent_t e = gev ? nullptr : prof_begin(m, st);
+    launch_mlp_chain(w.chain_top, a, st);
+    prof_end(m, st, 1, e);
+    mark(gev, 5, st);
+    m->launches += 2;
+    return;
+  }
   for (int j = 0; j < nt; ++j) {
     const Layer& L = m->top[j];
     GemmArgs a{};
@@ -617,6 +644,8 @@ static void free_model(rec_model_s* m) {
     cudaFree(L.bias);
   }
   cudaFree(m->w_last);
+  cudaFree(m->bias_bottom_all);
+  cudaFree(m->bias_top_all);
   cudaFree(m->tables);
   cudaFree(m->d_tab_off);
   cudaFree(m->d_rows);
@@ -765,6 +794,7 @@ rec_status rec_model_create(const rec_model_desc* d, rec_model_t* out) {
     return REC_E_CUDA;
   }
   gemm_prepare();
+  chain_prepare();
 
   rec_model_s* m = new rec_model_s();
   m->T = d->num_tables;
@@ -885,6 +915,51 @@ rec_status rec_model_create(const rec_model_desc* d, rec_model_t* out) {
   for (int l = 1; l < d->n_bottom - 1; ++l) m->hmax = std::max(m->hmax, pad8(m->bottom_w[l]));
   for (int j = 0; j < d->n_top - 2; ++j) m->hmax = std::max(m->hmax, pad8(m->top_w[j]));
 
+  // ---------------------------------------------------------------- fused FC stacks
+  {
+    const char* e = getenv("REC_MLP");
+    const bool allow = !(e && e[0] == 'l');  // REC_MLP=layers: per-layer GEMMs (A/B profiling)
+    auto build = [&](std::vector<rec::Layer>& Ls, ChainArgs& ca, float** bias_all, int mode) -> bool {
+      const int nl = static_cast<int>(Ls.size());
+      if (!allow || nl < 1 || nl > 4) return false;
+      ca = ChainArgs{};
+      ca.nlayers = nl;
+      int total = 0, maxn = 0, act = 0;
+      for (int l = 0; l < nl; ++l) {
+        ca.K[l] = Ls[l].K;
+        ca.N[l] = Ls[l].N;
+        ca.wbox[l] = Ls[l].bn;
+        total += Ls[l].N;
+        maxn = std::max(maxn, Ls[l].N);
+        if (l < nl - 1) act = std::max(act, (Ls[l].N + 63) / 64);
+      }
+      ca.bias_total = total;
+      ca.act_kblocks = act;
+      int tc = 32;
+      while (tc < maxn) tc *= 2;
+      if (tc > 512) return false;
+      ca.tmem_cols = tc;
+      ca.mode_last = mode;
+      ca.wl_n = mode == GEMM_OUT_CTR ? Ls[nl - 1].N : 0;
+      if (!chain_configure(ca)) return false;
+      if (cudaMalloc(reinterpret_cast<void**>(bias_all), sizeof(float) * total) != cudaSuccess) return false;
+      int off = 0;
+      for (int l = 0; l < nl; ++l) {
+        cudaMemcpy(*bias_all + off, Ls[l].bias, sizeof(float) * Ls[l].N, cudaMemcpyDeviceToDevice);
+        off += Ls[l].N;
+      }
+      ca.bias_all = *bias_all;
+      if (mode == GEMM_OUT_CTR) {
+        ca.w_last = m->w_last;
+        ca.b_last = m->b_last;
+      }
+      return true;
+    };
+    CHECK_CUDA_CREATE(cudaDeviceSynchronize());  // biases initialised
+    m->chain_bottom = build(m->bottom, m->chain_bottom_args, &m->bias_bottom_all, GEMM_OUT_X_F32);
+    m->chain_top = build(m->top, m->chain_top_args, &m->bias_top_all, GEMM_OUT_CTR);
+  }
+
   // ---------------------------------------------------------------- workspaces
   const int cap = m->max_batch;
   m->ws.resize(m->nstreams);
@@ -954,6 +1029,13 @@ rec_status rec_model_create(const rec_model_desc* d, rec_model_t* out) {
       }
       w.out_top[j] = (j == ntl - 1) ? nullptr : static_cast<void*>(w.h[j & 1]);
     }
+    auto fill_maps = [&](ChainMaps& mp, const CUtensorMap& a0, std::vector<rec::Layer>& Ls) {
+      mp.a0 = a0;
+      CUtensorMap* ws_[4] = {&mp.w0, &mp.w1, &mp.w2, &mp.w3};
+      for (int l = 0; l < 4; ++l) *ws_[l] = Ls[std::min<int>(l, static_cast<int>(Ls.size()) - 1)].tmap_w;
+    };
+    fill_maps(w.chain_bottom, w.tmap_a_bottom[0], m->bottom);
+    fill_maps(w.chain_top, w.tmap_a_top[0], m->top);
   }
   // synthetic-batch staging ring + one captured CUDA graph per slot (a2-a6 chain)
   constexpr int kSlots = 4;

@@ -74,6 +74,7 @@ struct Workspace {
   cudaEvent_t pin_free = nullptr;    // last H2D out of `pin` completed
   std::vector<CUtensorMap> tmap_a_bottom, tmap_a_top;  // A operand per GEMM layer
   std::vector<void*> out_bottom, out_top;              // output buffer per GEMM layer
+  ChainMaps chain_bottom{}, chain_top{};                // fused-MLP tensor maps (k_mlp.cu)
   std::vector<SynthSlot> slots;                        // synthetic-batch staging ring
   int next_slot = 0;
   int graph_kernels = 0;                               // kernels per graph launch
@@ -109,6 +110,11 @@ struct rec_model_s {
   std::vector<rec::Layer> bottom, top;  // top excludes the width-1 output layer
   float* w_last = nullptr;
   float b_last = 0.f;
+  // fused FC stacks (one kernel per MLP per 128-row tile) when they fit
+  bool chain_bottom = false, chain_top = false;
+  rec::ChainArgs chain_bottom_args{}, chain_top_args{};
+  float* bias_bottom_all = nullptr;
+  float* bias_top_all = nullptr;
   int Ktop = 0, Ktop_pad = 0, hmax = 0;
   // streams + workspaces
   std::vector<rec::Workspace> ws;
