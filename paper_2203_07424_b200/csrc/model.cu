@@ -276,9 +276,9 @@ static const cudaGraphNode_t* last_node(cudaStream_t s, size_t* n) {
 //  * materialised (variable pooling, rec_gen_batch): input kernels write indices / offsets /
 //    dense, then the generic forward.
 static rec_status synth_chain(rec_model_s* m, Workspace& w, SynthSlot& sl, bool capture,
-                              bool materialize) {
+                              bool materialize, bool with_events = false) {
   cudaStream_t s = w.stream, sb = w.stream_b;
-  cudaEvent_t* gev = capture ? sl.ev : nullptr;
+  cudaEvent_t* gev = capture && with_events ? sl.ev : nullptr;
   mark(gev, 0, s);
   if (!materialize && m->lo == m->hi) {
     REC_CUDA(cudaEventRecord(w.ev_fork, s));
@@ -294,7 +294,7 @@ static rec_status synth_chain(rec_model_s* m, Workspace& w, SynthSlot& sl, bool 
         set_error("graph capture: dense node not found");
         return REC_E_CUDA;
       }
-      sl.dense_node = d[0];
+      *sl.cap_dense = d[0];
     }
     enqueue_bottom(m, w, sb, w.cap, w.dB, gev);
     mark(gev, 7, sb);
@@ -310,7 +310,7 @@ static rec_status synth_chain(rec_model_s* m, Workspace& w, SynthSlot& sl, bool 
         set_error("graph capture: SLS node not found");
         return REC_E_CUDA;
       }
-      sl.gen_node = d[0];
+      *sl.cap_gen = d[0];
     }
     m->launches += 2;
     mark(gev, 2, s);
@@ -330,7 +330,7 @@ static rec_status synth_chain(rec_model_s* m, Workspace& w, SynthSlot& sl, bool 
       set_error("graph capture: input node not found");
       return REC_E_CUDA;
     }
-    sl.gen_node = d[0];
+    *sl.cap_gen = d[0];
   }
   if (m->lo != m->hi) {
     launch_gen_variable_rest(sl.ga, s);
@@ -345,18 +345,23 @@ static rec_status synth_chain(rec_model_s* m, Workspace& w, SynthSlot& sl, bool 
 
 rec_status capture_graphs(rec_model_s* m, Workspace& w) {
   for (auto& sl : w.slots) {
-    const int64_t before = m->launches;
-    REC_CUDA(cudaStreamBeginCapture(w.stream, cudaStreamCaptureModeThreadLocal));
-    rec_status st = synth_chain(m, w, sl, true, false);
-    cudaGraph_t g = nullptr;
-    cudaError_t ce = cudaStreamEndCapture(w.stream, &g);
-    if (st != REC_OK) return st;
-    if (ce != cudaSuccess) return cuda_fail(ce, "cudaStreamEndCapture");
-    sl.graph = g;
-    ce = cudaGraphInstantiate(&sl.exec, g, 0);
-    if (ce != cudaSuccess) return cuda_fail(ce, "cudaGraphInstantiate");
-    w.graph_kernels = static_cast<int>(m->launches - before);
-    m->launches = before;
+    for (int v = 0; v < 2; ++v) {  // 0: kernels only (production), 1: with stage events
+      SynthSlot::Variant& V = sl.var[v];
+      sl.cap_gen = &V.gen_node;
+      sl.cap_dense = &V.dense_node;
+      const int64_t before = m->launches;
+      REC_CUDA(cudaStreamBeginCapture(w.stream, cudaStreamCaptureModeThreadLocal));
+      rec_status st = synth_chain(m, w, sl, true, false, v == 1);
+      cudaGraph_t g = nullptr;
+      cudaError_t ce = cudaStreamEndCapture(w.stream, &g);
+      if (st != REC_OK) return st;
+      if (ce != cudaSuccess) return cuda_fail(ce, "cudaStreamEndCapture");
+      V.graph = g;
+      ce = cudaGraphInstantiate(&V.exec, g, 0);
+      if (ce != cudaSuccess) return cuda_fail(ce, "cudaGraphInstantiate");
+      w.graph_kernels = static_cast<int>(m->launches - before);
+      m->launches = before;
+    }
   }
   return REC_OK;
 }
@@ -435,7 +440,8 @@ rec_status synth_submit(rec_model_s* m, Workspace& w, const int32_t* segs, int n
     REC_CUDA(cudaMemcpyAsync(w.gsegs, w.pin, sizeof(int4) * nseg, cudaMemcpyHostToDevice, w.stream));
     REC_CUDA(cudaEventRecord(w.pin_free, w.stream));
   }
-  const bool direct = dense_f32_out != nullptr || !sl.exec;
+  SynthSlot::Variant& V = sl.var[m->prof ? 1 : 0];
+  const bool direct = dense_f32_out != nullptr || !V.exec;
   if (!direct) {
     const bool fused = m->lo == m->hi;
     dim3 grid, block;
@@ -445,7 +451,7 @@ rec_status synth_submit(rec_model_s* m, Workspace& w, const int32_t* segs, int n
     kp.gridDim = grid;
     kp.blockDim = block;
     kp.kernelParams = args_a;
-    REC_CUDA(cudaGraphExecKernelNodeSetParams(sl.exec, sl.gen_node, &kp));
+    REC_CUDA(cudaGraphExecKernelNodeSetParams(V.exec, V.gen_node, &kp));
     if (fused) {
       cudaKernelNodeParams kd{};
       void* args_d[2] = {sl.sb, &sl.ga};
@@ -453,10 +459,10 @@ rec_status synth_submit(rec_model_s* m, Workspace& w, const int32_t* segs, int n
       kd.gridDim = grid;
       kd.blockDim = block;
       kd.kernelParams = args_d;
-      REC_CUDA(cudaGraphExecKernelNodeSetParams(sl.exec, sl.dense_node, &kd));
+      REC_CUDA(cudaGraphExecKernelNodeSetParams(V.exec, V.dense_node, &kd));
     }
     const double t2 = m->prof ? host_now_ns() : 0.0;
-    REC_CUDA(cudaGraphLaunch(sl.exec, w.stream));
+    REC_CUDA(cudaGraphLaunch(V.exec, w.stream));
     if (m->prof) {
       const double t3 = host_now_ns();
       m->host_ns[0] += t2 - t1;
@@ -618,8 +624,10 @@ static void free_model(rec_model_s* m) {
     if (w.pin) cudaFreeHost(w.pin);
     if (w.pin_free) cudaEventDestroy(w.pin_free);
     for (auto& sl : w.slots) {
-      if (sl.exec) cudaGraphExecDestroy(sl.exec);
-      if (sl.graph) cudaGraphDestroy(sl.graph);
+      for (auto& V : sl.var) {
+        if (V.exec) cudaGraphExecDestroy(V.exec);
+        if (V.graph) cudaGraphDestroy(V.graph);
+      }
       delete sl.sb;
       if (sl.free) cudaEventDestroy(sl.free);
       for (auto e : sl.ev)

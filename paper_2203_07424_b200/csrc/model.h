@@ -38,10 +38,14 @@ struct SynthSlot {
   GenArgs ga{};
   SlsSynthArgs sa{};
   cudaEvent_t free = nullptr;        // the last launch that used this slot completed
-  cudaGraph_t graph = nullptr;       // kept alive: gen_node belongs to it
-  cudaGraphExec_t exec = nullptr;
-  cudaGraphNode_t gen_node = nullptr;   // first kernel of the main stream (SLS or inputs)
-  cudaGraphNode_t dense_node = nullptr; // fused path: dense-feature kernel on the branch
+  struct Variant {                   // [0] kernels only (production), [1] + stage events
+    cudaGraph_t graph = nullptr;     // kept alive: the node handles belong to it
+    cudaGraphExec_t exec = nullptr;
+    cudaGraphNode_t gen_node = nullptr;    // first kernel of the main stream (SLS or inputs)
+    cudaGraphNode_t dense_node = nullptr;  // fused path: dense-feature kernel on the branch
+  } var[2];
+  cudaGraphNode_t* cap_gen = nullptr;  // capture target for the node handles
+  cudaGraphNode_t* cap_dense = nullptr;
   cudaEvent_t ev[8] = {};            // stage boundaries inside the graph (timing)
   bool prof_pending = false;
 };
