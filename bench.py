@@ -268,8 +268,8 @@ def run_ours(args):
     gemm_ms, gemm_n = model.rec_profile_read(KERNEL_GEMM)
     int_ms, _ = model.rec_profile_read(2)
     gen_ms, _ = model.rec_profile_read(3)
-    # host cost of the submit path (all streams, C++ loop)
-    model.rec_profile(True)
+    # host cost of the submit path (all streams, C++ loop, production graphs)
+    model.rec_profile(False)
     hsteps = min(args.steps, 1000)
     hb = tbstart[:hsteps + 1]
     model.rec_synth_query_batches(tsegs[:hb[-1]], hb, first_slot=0)

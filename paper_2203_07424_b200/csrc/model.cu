@@ -415,12 +415,12 @@ rec_status synth_submit(rec_model_s* m, Workspace& w, const int32_t* segs, int n
     set_error("segs: batch of %lld items exceeds max_batch %d", (long long)B, w.cap);
     return REC_E_INVALID_ARG;
   }
-  const double t0 = m->prof ? host_now_ns() : 0.0;
+  const double t0 = host_now_ns();
   SynthSlot& sl = w.slots[w.next_slot];
   w.next_slot = (w.next_slot + 1) % static_cast<int>(w.slots.size());
   REC_CUDA(cudaEventSynchronize(sl.free));
   collect_slot(m, sl);
-  const double t1 = m->prof ? host_now_ns() : 0.0;
+  const double t1 = host_now_ns();
   SegBatch& sb = *sl.sb;
   sb.B = static_cast<int>(B);
   sb.nseg = nseg;
@@ -461,14 +461,12 @@ rec_status synth_submit(rec_model_s* m, Workspace& w, const int32_t* segs, int n
       kd.kernelParams = args_d;
       REC_CUDA(cudaGraphExecKernelNodeSetParams(V.exec, V.dense_node, &kd));
     }
-    const double t2 = m->prof ? host_now_ns() : 0.0;
+    const double t2 = host_now_ns();
     REC_CUDA(cudaGraphLaunch(V.exec, w.stream));
-    if (m->prof) {
-      const double t3 = host_now_ns();
-      m->host_ns[0] += t2 - t1;
-      m->host_ns[1] += t3 - t2;
-      m->host_ns[2] += t1 - t0;
-    }
+    const double t3 = host_now_ns();
+    m->host_ns[0] += t2 - t1;
+    m->host_ns[1] += t3 - t2;
+    m->host_ns[2] += t1 - t0;
     m->launches += w.graph_kernels;
     sl.prof_pending = m->prof;
   } else {
@@ -479,7 +477,7 @@ rec_status synth_submit(rec_model_s* m, Workspace& w, const int32_t* segs, int n
     if (st != REC_OK) return st;
   }
   REC_CUDA(cudaEventRecord(sl.free, w.stream));
-  if (m->prof) m->host_ns[3] += host_now_ns() - t0;
+  m->host_ns[3] += host_now_ns() - t0;
   *batch_out = static_cast<int>(B);
   return REC_OK;
 }
