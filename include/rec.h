@@ -195,6 +195,14 @@ rec_status rec_serve(rec_model_t m, const rec_trace_row* trace, int64_t n, doubl
                      double* latency_ms, int32_t* batch_log, int64_t log_cap,
                      int64_t* log_rows, float* ctr_out);
 
+/* Shard plan of a rank (host-only): out[6] = {first local table, local table
+ * count, first local row, end local row (row-wise; else 0 / INT32_MAX), first item of this
+ * rank's block, items in the block} for a global batch of `batch` items (contiguous blocks
+ * of ceil(batch / world), reading R22).  Errors: INVALID_ARG, UNSUPPORTED (table-wise needs
+ * num_tables % world == 0, row-wise needs equal rows). */
+rec_status rec_shard_plan(int32_t num_tables, const int64_t* rows, int32_t world, int32_t rank,
+                          int32_t shard, int32_t batch, int64_t* out);
+
 /* --------------------------------------------------------------------- utilities */
 const char* rec_last_error(void);             /* thread-local; valid until the next call */
 int32_t rec_nccl_unique_id_size(void);        /* bytes of an ncclUniqueId (128)          */

@@ -32,7 +32,7 @@ EXPORTS = ["rec_model_create", "rec_model_destroy", "rec_query", "rec_query_debu
            "rec_query_async", "rec_synth_query_async", "rec_sync", "rec_stream_handle",
            "rec_gen_batch", "rec_profile", "rec_profile_read", "rec_serve", "rec_last_error",
            "rec_nccl_unique_id_size", "rec_nccl_get_unique_id", "rec_version", "rec_split_fuse",
-           "rec_synth_query_batches"]
+           "rec_synth_query_batches", "rec_shard_plan"]
 
 
 class rec_model_desc(C.Structure):
@@ -100,6 +100,8 @@ def lib() -> C.CDLL:
         L.rec_split_fuse.restype = i32
         L.rec_synth_query_batches.argtypes = [vp, vp, vp, i64, i32]
         L.rec_synth_query_batches.restype = i32
+        L.rec_shard_plan.argtypes = [i32, vp, i32, i32, i32, i32, vp]
+        L.rec_shard_plan.restype = i32
         for f in ("rec_model_create", "rec_query", "rec_query_debug", "rec_query_async",
                   "rec_synth_query_async", "rec_sync", "rec_gen_batch", "rec_profile",
                   "rec_profile_read", "rec_serve", "rec_nccl_get_unique_id"):
@@ -263,6 +265,15 @@ def rec_split_fuse(trace: np.ndarray, max_batch: int):
     _check(lib().rec_split_fuse(_ptr(trace), n, max_batch, _ptr(segs), cap, _ptr(bstart), cap + 1,
                                 C.byref(nb), C.byref(ns)))
     return segs[:ns.value], bstart[:nb.value + 1]
+
+
+def rec_shard_plan(rows, world: int, rank: int, shard: int, batch: int) -> dict:
+    """Host-only shard plan of `rank` (first/count of local tables, local row range, item block)."""
+    r = np.ascontiguousarray(rows, dtype=np.int64)
+    out = np.zeros(6, dtype=np.int64)
+    _check(lib().rec_shard_plan(len(r), _ptr(r), world, rank, shard, batch, _ptr(out)))
+    return dict(t0=int(out[0]), t_local=int(out[1]), row_lo=int(out[2]), row_hi=int(out[3]),
+                item0=int(out[4]), items=int(out[5]))
 
 
 def nccl_unique_id() -> bytes:

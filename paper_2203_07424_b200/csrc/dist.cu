@@ -1,11 +1,38 @@
-// dist.cu — NCCL bootstrap for the sharded modes.  One process per GPU;
-// the ncclUniqueId is created by rank 0 (rec_nccl_get_unique_id) and broadcast by the
-// caller (torch.distributed is only the bootstrap plumbing).
+// dist.cu — multi-GPU embedding sharding.
+//
+// One process per GPU; the ncclUniqueId is created by rank 0 (rec_nccl_get_unique_id) and
+// broadcast by the caller (torch.distributed is bootstrap plumbing only).
+//
+// Table-wise (REC_SHARD_TABLE, e.g. RMC2: 40 tables = 8 x 5): rank r holds tables
+// [r*T/G, (r+1)*T/G) and pools them for ALL B items straight into an all-to-all send buffer
+// laid out [B_pad][T/G][D] — item b's block of rows belongs to the rank that owns item b
+// (contiguous item blocks of Bq = ceil(B/G), reading R22), so no repacking is needed.  One
+// ncclAlltoAll (C1) delivers to every rank the pooled vectors of its items for every table;
+// the rank runs the bottom MLP, interaction and top MLP for its Bq items, and an
+// ncclAllGather (C3) returns every CTR to every rank.  Each bag is pooled by the same kernel
+// in the same order and the GEMMs are batch-invariant, so results are bit-identical to
+// replicas.
+// Row-wise (REC_SHARD_ROW, 10-table configs where 10 % 8 != 0): rank r holds rows
+// [r*R/G, (r+1)*R/G) of every table; every rank pools its rows of every bag (partial sums,
+// [B_pad][T][D]); one ncclReduceScatter (C2, sum) leaves each rank the full pooled vectors
+// of its Bq items.  The cross-rank sum changes the fp32 association: bit-exact in int8-exact
+// value mode (G4), within the SLS tolerance otherwise.
 #include <nccl.h>
+
+#include <cstring>
 
 #include "model.h"
 
 namespace rec {
+
+#define REC_NCCL(call)                                                          \
+  do {                                                                          \
+    ncclResult_t _r = (call);                                                   \
+    if (_r != ncclSuccess) {                                                    \
+      set_error("NCCL error %s in %s", ncclGetErrorString(_r), #call);          \
+      return REC_E_NCCL;                                                        \
+    }                                                                           \
+  } while (0)
 
 rec_status dist_init(rec_model_s* m, const void* nccl_id) {
   if (!nccl_id) {
@@ -15,20 +42,93 @@ rec_status dist_init(rec_model_s* m, const void* nccl_id) {
   ncclUniqueId id;
   memcpy(&id, nccl_id, sizeof(id));
   ncclComm_t comm = nullptr;
-  ncclResult_t r = ncclCommInitRank(&comm, m->world, id, m->rank);
-  if (r != ncclSuccess) {
-    set_error("ncclCommInitRank failed: %s", ncclGetErrorString(r));
-    return REC_E_NCCL;
-  }
+  REC_NCCL(ncclCommInitRank(&comm, m->world, id, m->rank));
   m->nccl_comm = comm;
+  return sharded_alloc(m);
+}
+
+rec_status sharded_alloc(rec_model_s* m) {
+  const int G = m->world, cap = m->max_batch, D = m->D;
+  const int64_t Bq = (cap + G - 1) / G;
+  const int64_t per_item = (m->shard == REC_SHARD_TABLE ? m->T_loc : m->T) * static_cast<int64_t>(D);
+  const size_t send = sizeof(float) * Bq * G * per_item;
+  const size_t recv = m->shard == REC_SHARD_TABLE ? send : sizeof(float) * Bq * per_item;
+  REC_CUDA(cudaMalloc(reinterpret_cast<void**>(&m->sh_send), send));
+  REC_CUDA(cudaMalloc(reinterpret_cast<void**>(&m->sh_recv), recv));
+  REC_CUDA(cudaMalloc(reinterpret_cast<void**>(&m->sh_ctr), sizeof(float) * Bq * G));
+  REC_CUDA(cudaMemset(m->sh_send, 0, send));
   return REC_OK;
 }
 
 void dist_destroy(rec_model_s* m) {
-  if (m && m->nccl_comm) {
+  if (!m) return;
+  if (m->nccl_comm) {
     ncclCommDestroy(static_cast<ncclComm_t>(m->nccl_comm));
     m->nccl_comm = nullptr;
   }
+  cudaFree(m->sh_send);
+  cudaFree(m->sh_recv);
+  cudaFree(m->sh_ctr);
+  m->sh_send = m->sh_recv = m->sh_ctr = nullptr;
+}
+
+rec_status sharded_forward(rec_model_s* m, Workspace& w, const float* d_dense, const int* d_idx,
+                           const int* d_off, int B, float* ctr, float* logits) {
+  const int G = m->world, r = m->rank, T = m->T, TL = m->T_loc, D = m->D;
+  const int Bq = (B + G - 1) / G;
+  const int item0 = r * Bq;
+  const int Bl = B - item0 < 0 ? 0 : (B - item0 < Bq ? B - item0 : Bq);
+  cudaStream_t s = w.stream;
+  ncclComm_t comm = static_cast<ncclComm_t>(m->nccl_comm);
+  const size_t xs = sizeof(float) * (T + 1) * D;
+  // a3 on this GPU's shard, written in all-to-all / reduce-scatter order
+  if (m->shard == REC_SHARD_TABLE) {
+    launch_sls(m->tables, m->d_tab_off, m->row_stride, m->d_rows, d_idx, d_off + m->t0 * B, B,
+               nullptr, TL, D, m->sh_send, TL * D, 0, w.flag, s);
+    REC_NCCL(ncclAlltoAll(m->sh_send, m->sh_recv, static_cast<size_t>(Bq) * TL * D, ncclFloat, comm, s));
+    if (Bl > 0)
+      for (int p = 0; p < G; ++p)  // peer p's tables [p*TL, (p+1)*TL) of my items -> X slots
+        REC_CUDA(cudaMemcpy2DAsync(w.X + (1 + p * TL) * D, xs,
+                                   m->sh_recv + static_cast<size_t>(p) * Bq * TL * D,
+                                   sizeof(float) * TL * D, sizeof(float) * TL * D, Bl,
+                                   cudaMemcpyDeviceToDevice, s));
+  } else {
+    launch_sls(m->tables, m->d_tab_off, m->row_stride, m->d_rows, d_idx, d_off, B, nullptr, T, D,
+               m->sh_send, T * D, 0, w.flag, s, static_cast<int>(m->row_lo), static_cast<int>(m->row_hi));
+    REC_NCCL(ncclReduceScatter(m->sh_send, m->sh_recv, static_cast<size_t>(Bq) * T * D, ncclFloat,
+                               ncclSum, comm, s));
+    if (Bl > 0)
+      REC_CUDA(cudaMemcpy2DAsync(w.X + D, xs, m->sh_recv, sizeof(float) * T * D, sizeof(float) * T * D,
+                                 Bl, cudaMemcpyDeviceToDevice, s));
+  }
+  m->launches += 1;
+  // a4-a6 for this rank's item block
+  if (Bl > 0) {
+    launch_dense_to_bf16(d_dense + static_cast<size_t>(item0) * m->F, Bl, m->F, m->Fpad, w.dense_bf, s);
+    m->launches += 1;
+    enqueue_bottom(m, w, s, Bl, nullptr, nullptr);
+    enqueue_interact_top(m, w, s, Bl, nullptr, w.ctr, w.logit, nullptr);
+  }
+  // C3: every rank gets every CTR (positions >= B of the padded gather are ignored)
+  REC_NCCL(ncclAllGather(w.ctr, m->sh_ctr, Bq, ncclFloat, comm, s));
+  REC_CUDA(cudaMemcpyAsync(w.flag_host, w.flag, sizeof(int), cudaMemcpyDeviceToHost, s));
+  REC_CUDA(cudaStreamSynchronize(s));
+  const int f = *w.flag_host;
+  if (f & 1) {
+    set_error("an index is outside [0, rows_t) (REC_E_INDEX_OOB)");
+    return REC_E_INDEX_OOB;
+  }
+  if (f & 2) {
+    set_error("offsets are not non-decreasing from 0 (REC_E_OFFSETS)");
+    return REC_E_OFFSETS;
+  }
+  REC_CUDA(cudaMemcpyAsync(ctr, m->sh_ctr, sizeof(float) * B, cudaMemcpyDefault, s));
+  if (logits) {  // logits of this rank's own items only (diagnostic)
+    if (Bl > 0)
+      REC_CUDA(cudaMemcpyAsync(logits + item0, w.logit, sizeof(float) * Bl, cudaMemcpyDefault, s));
+  }
+  REC_CUDA(cudaStreamSynchronize(s));
+  return REC_OK;
 }
 
 }  // namespace rec
@@ -49,6 +149,28 @@ rec_status rec_nccl_get_unique_id(void* out) {
     return REC_E_NCCL;
   }
   memcpy(out, &id, sizeof(id));
+  return REC_OK;
+}
+
+rec_status rec_shard_plan(int32_t num_tables, const int64_t* rows, int32_t world, int32_t rank,
+                          int32_t shard, int32_t batch, int64_t* out) {
+  if (!rows || !out || num_tables < 1 || world < 1 || rank < 0 || rank >= world || batch < 0) {
+    rec::set_error("bad argument");
+    return REC_E_INVALID_ARG;
+  }
+  rec::ShardPlan p{};
+  rec_status st = rec::shard_plan(num_tables, rows, world, rank, shard, &p);
+  if (st != REC_OK) return st;
+  const int64_t Bq = world > 1 && shard != REC_SHARD_REPLICA ? (batch + world - 1) / world : batch;
+  const int64_t item0 = world > 1 && shard != REC_SHARD_REPLICA ? rank * Bq : 0;
+  int64_t cnt = batch - item0;
+  cnt = cnt < 0 ? 0 : (cnt < Bq ? cnt : Bq);
+  out[0] = p.t0;
+  out[1] = p.t_local;
+  out[2] = p.row_lo;
+  out[3] = p.row_hi;
+  out[4] = item0;
+  out[5] = cnt;
   return REC_OK;
 }
 

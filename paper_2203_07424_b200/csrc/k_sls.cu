@@ -51,7 +51,8 @@ __global__ void __launch_bounds__(THREADS, 5) k_sls(const float* __restrict__ ta
                                                     const int* __restrict__ offsets, int B,
                                                     const int* __restrict__ dB, int T,
                                                     int D, float* __restrict__ X, int x_stride,
-                                                    int x_slot0, int* __restrict__ flag) {
+                                                    int x_slot0, int* __restrict__ flag, int row_lo,
+                                                    int row_hi) {
   using S = SlsShape<LANES>;
   constexpr int GROUPS = THREADS / LANES;
   __shared__ int s_off[GROUPS + 1];
@@ -109,7 +110,10 @@ __global__ void __launch_bounds__(THREADS, 5) k_sls(const float* __restrict__ ta
       for (int k = 0; k < S::U; ++k) {
         const int r = kk + k;  // row r of the round = index position base + r
         const int rr = __shfl_sync(gmask, cur[r / LANES], r % LANES, LANES);
-        if (r < n) v[k] = ldg_row(tab, static_cast<uint32_t>(rr), stride_bytes);
+        // row-wise sharding: only rows in [row_lo, row_hi) live on this GPU (others add 0)
+        const bool take = r < n && rr >= row_lo && rr < row_hi;
+        v[k] = take ? ldg_row(tab, static_cast<uint32_t>(rr - row_lo), stride_bytes)
+                    : make_float4(0.f, 0.f, 0.f, 0.f);
       }
 #pragma unroll
       for (int k = 0; k < S::U; ++k) {
@@ -228,25 +232,26 @@ template <int L>
 static void launch_l(const float* tables, const int64_t* tab_off, int64_t row_stride,
                      const int64_t* rows, const int* indices, const int* offsets, int B,
                      const int* dB, int T, int D, float* X, int x_stride_items, int x_slot0, int* flag,
-                     cudaStream_t s) {
+                     cudaStream_t s, int row_lo, int row_hi) {
   constexpr int THREADS = 128;
   const int nbags = T * B;
   k_sls<L, THREADS><<<(nbags + THREADS / L - 1) / (THREADS / L), THREADS, 0, s>>>(
       tables, tab_off, row_stride, rows, indices, offsets, B, dB, T, D, X, x_stride_items, x_slot0,
-      flag);
+      flag, row_lo, row_hi);
 }
 
 void launch_sls(const float* tables, const int64_t* tab_off, int64_t row_stride,
                 const int64_t* rows, const int* indices, const int* offsets, int B, const int* dB,
-                int T, int D, float* X, int x_stride_items, int x_slot0, int* flag, cudaStream_t s) {
+                int T, int D, float* X, int x_stride_items, int x_slot0, int* flag, cudaStream_t s,
+                int row_lo, int row_hi) {
   if (T * B == 0) return;
   const int lanes_needed = D / 4;
   if (lanes_needed <= 8) {
-    launch_l<8>(tables, tab_off, row_stride, rows, indices, offsets, B, dB, T, D, X, x_stride_items, x_slot0, flag, s);
+    launch_l<8>(tables, tab_off, row_stride, rows, indices, offsets, B, dB, T, D, X, x_stride_items, x_slot0, flag, s, row_lo, row_hi);
   } else if (lanes_needed <= 16) {
-    launch_l<16>(tables, tab_off, row_stride, rows, indices, offsets, B, dB, T, D, X, x_stride_items, x_slot0, flag, s);
+    launch_l<16>(tables, tab_off, row_stride, rows, indices, offsets, B, dB, T, D, X, x_stride_items, x_slot0, flag, s, row_lo, row_hi);
   } else {
-    launch_l<32>(tables, tab_off, row_stride, rows, indices, offsets, B, dB, T, D, X, x_stride_items, x_slot0, flag, s);
+    launch_l<32>(tables, tab_off, row_stride, rows, indices, offsets, B, dB, T, D, X, x_stride_items, x_slot0, flag, s, row_lo, row_hi);
   }
 }
 

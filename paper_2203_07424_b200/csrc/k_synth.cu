@@ -9,13 +9,13 @@ namespace rec {
 // ------------------------------------------------------------------ tables (G4)
 // Element (r, k) of table t is stored at base[r * stride + k] (base = start of row 0 of t).
 __global__ void k_init_table(float* __restrict__ base, int64_t rows, int D, int64_t stride, int t,
-                             uint32_t k0, uint32_t k1, int shift, int value_mode) {
+                             uint32_t k0, uint32_t k1, int shift, int value_mode, int64_t r0) {
   const int64_t n = rows * D;
   const uint32_t c2 = (static_cast<uint32_t>(t) << 8) | DOM_TABLE;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
        e += (int64_t)gridDim.x * blockDim.x) {
     const uint32_t r = static_cast<uint32_t>(e / D), k = static_cast<uint32_t>(e % D);
-    const U4 w = philox(k, r, c2, 0u, k0, k1);
+    const U4 w = philox(k, static_cast<uint32_t>(r0 + r), c2, 0u, k0, k1);
     float v;
     if (value_mode == 0) {
       v = i8(w.x) * pow2f(-(7 + shift));
@@ -27,8 +27,8 @@ __global__ void k_init_table(float* __restrict__ base, int64_t rows, int D, int6
 }
 
 void launch_init_table(float* base, int64_t rows, int D, int64_t stride, int t, uint32_t k0,
-                       uint32_t k1, int shift, int value_mode, cudaStream_t s) {
-  k_init_table<<<148 * 8, 256, 0, s>>>(base, rows, D, stride, t, k0, k1, shift, value_mode);
+                       uint32_t k1, int shift, int value_mode, cudaStream_t s, int64_t r0) {
+  k_init_table<<<148 * 8, 256, 0, s>>>(base, rows, D, stride, t, k0, k1, shift, value_mode, r0);
 }
 
 // ------------------------------------------------------------------ weights (G5)

@@ -8,8 +8,9 @@
 namespace rec {
 
 // ---------------------------------------------------------------- parameters (G4, G5)
+// rows [r0, r0 + rows) of table t (global Philox counters) into base[(r - r0) * stride + k]
 void launch_init_table(float* base, int64_t rows, int D, int64_t stride, int t, uint32_t k0,
-                       uint32_t k1, int shift, int value_mode, cudaStream_t s);
+                       uint32_t k1, int shift, int value_mode, cudaStream_t s, int64_t r0 = 0);
 void launch_init_layer(__nv_bfloat16* W, float* bias, int N, int K, int Kpad, int layer,
                        int e, uint32_t k0, uint32_t k1, cudaStream_t s);
 void launch_init_final(float* w, float* b, int K, int layer, int e, uint32_t k0, uint32_t k1,
@@ -55,9 +56,12 @@ void launch_check_offsets(const int* offsets, int nbags, int* flag, cudaStream_t
 // Row r of table t lives at tables + tab_off[t] + r * row_stride (floats).
 // B: batch (or capacity when dB != nullptr: then the kernels read the batch from *dB,
 // which lets one captured CUDA graph serve every batch size).
+// row_lo/row_hi: row-wise sharding keeps rows [row_lo, row_hi) of every table on this GPU
+// (arena row r - row_lo); other rows add nothing.  Replicated / table-wise: 0, INT32_MAX.
 void launch_sls(const float* tables, const int64_t* tab_off, int64_t row_stride,
                 const int64_t* rows, const int* indices, const int* offsets, int B, const int* dB,
-                int T, int D, float* X, int x_stride_items, int x_slot0, int* flag, cudaStream_t s);
+                int T, int D, float* X, int x_stride_items, int x_slot0, int* flag, cudaStream_t s,
+                int row_lo = 0, int row_hi = 0x7fffffff);
 
 // SLS over device-synthesised indices (fixed pooling L): each index is the Philox value of
 // (slot, item, table, qid) computed where it is consumed (a2 fused into a3): no index array,

@@ -100,8 +100,8 @@ static inline void mark(cudaEvent_t* gev, int i, cudaStream_t st) {
   if (gev) cudaEventRecordWithFlags(gev[i], st, cudaEventRecordExternal);
 }
 
-static void enqueue_bottom(rec_model_s* m, Workspace& w, cudaStream_t st, int B, const int* dB,
-                           cudaEvent_t* gev) {
+void enqueue_bottom(rec_model_s* m, Workspace& w, cudaStream_t st, int B, const int* dB,
+                    cudaEvent_t* gev) {
   const int T = m->T, D = m->D;
   const int nb = static_cast<int>(m->bottom.size());
   if (m->chain_bottom) {  // whole bottom MLP in one kernel (k_mlp.cu)
@@ -141,8 +141,8 @@ static void enqueue_bottom(rec_model_s* m, Workspace& w, cudaStream_t st, int B,
   m->launches += nb;
 }
 
-static void enqueue_interact_top(rec_model_s* m, Workspace& w, cudaStream_t st, int B, const int* dB,
-                                 float* ctr_out, float* logit_out, cudaEvent_t* gev) {
+void enqueue_interact_top(rec_model_s* m, Workspace& w, cudaStream_t st, int B, const int* dB,
+                          float* ctr_out, float* logit_out, cudaEvent_t* gev) {
   const int T = m->T, D = m->D;
   // a5: interaction -> A_top
   cudaEvent_t e1 = gev ? nullptr : prof_begin(m, st);
@@ -340,6 +340,7 @@ static rec_status synth_chain(rec_model_s* m, Workspace& w, SynthSlot& sl, bool 
   }
   prof_end(m, s, 3, e);
   mark(gev, 1, s);
+  if (m->world > 1 && m->shard != REC_SHARD_REPLICA) return REC_OK;  // inputs only (gen_batch)
   return forward_enqueue(m, w, w.indices, w.offsets, w.cap, w.dB, w.ctr, w.logit, gev);
 }
 
@@ -570,6 +571,8 @@ static rec_status query_impl(rec_model_s* m, const float* dense, const int32_t* 
     d_dense = w.dense_f32;
   }
   REC_CUDA(cudaEventRecord(w.pin_free, s));
+  if (m->world > 1 && m->shard != REC_SHARD_REPLICA)  // model-parallel embeddings (dist.cu)
+    return sharded_forward(m, w, d_dense, d_idx, d_off, B, ctr, logits);
   launch_dense_to_bf16(d_dense, B, m->F, m->Fpad, w.dense_bf, s);
   m->launches += 1 + (off_dev ? 1 : 0);
   st = forward_enqueue(m, w, d_idx, d_off, B, nullptr, w.ctr, w.logit, nullptr);
@@ -586,6 +589,31 @@ static rec_status query_impl(rec_model_s* m, const float* dense, const int32_t* 
                                sizeof(float) * T * D, B, cudaMemcpyDefault, s));
   }
   REC_CUDA(cudaStreamSynchronize(s));
+  return REC_OK;
+}
+
+rec_status shard_plan(int T, const int64_t* rows, int world, int rank, int shard, ShardPlan* p) {
+  p->t0 = 0;
+  p->t_local = T;
+  p->row_lo = 0;
+  p->row_hi = 0x7fffffff;
+  if (world <= 1 || shard == REC_SHARD_REPLICA) return REC_OK;
+  if (shard == REC_SHARD_TABLE) {
+    if (T % world != 0) {
+      set_error("table-wise sharding needs num_tables (%d) divisible by world (%d)", T, world);
+      return REC_E_UNSUPPORTED;
+    }
+    p->t_local = T / world;
+    p->t0 = rank * p->t_local;
+    return REC_OK;
+  }
+  for (int t = 1; t < T; ++t)
+    if (rows[t] != rows[0]) {
+      set_error("row-wise sharding needs equal rows per table");
+      return REC_E_UNSUPPORTED;
+    }
+  p->row_lo = rows[0] * rank / world;
+  p->row_hi = rows[0] * (rank + 1) / world;
   return REC_OK;
 }
 
@@ -833,34 +861,57 @@ rec_status rec_model_create(const rec_model_desc* d, rec_model_t* out) {
   const int T = m->T, D = m->D;
 
   // ---------------------------------------------------------------- tables
+  // shard plan: which tables / rows of them live on this GPU
+  {
+    ShardPlan sp{};
+    rec_status st = shard_plan(T, m->rows.data(), m->world, m->rank, m->shard, &sp);
+    if (st != REC_OK) {
+      delete m;
+      return st;
+    }
+    m->t0 = sp.t0;
+    m->T_loc = sp.t_local;
+    m->row_lo = sp.row_lo;
+    m->row_hi = sp.row_hi;
+  }
+  const int TL = m->T_loc;
+  auto local_rows = [&](int tl) -> int64_t {
+    const int64_t R = m->rows[m->t0 + tl];
+    return m->shard == REC_SHARD_ROW && m->world > 1 ? m->row_hi - m->row_lo : R;
+  };
   bool equal = true;
-  for (int t = 1; t < T; ++t) equal = equal && (m->rows[t] == m->rows[0]);
+  for (int tl = 1; tl < TL; ++tl) equal = equal && (local_rows(tl) == local_rows(0));
   m->interleaved = equal;
-  m->tab_off.resize(T);
+  m->tab_off.resize(TL);
+  std::vector<int64_t> grows(TL);
   int64_t total_rows = 0;
-  for (int t = 0; t < T; ++t) total_rows += m->rows[t];
+  for (int tl = 0; tl < TL; ++tl) {
+    total_rows += local_rows(tl);
+    grows[tl] = m->rows[m->t0 + tl];
+  }
   if (equal) {
     // row r of table t at (r*T + t)*D: hot low rows of ALL tables form one contiguous
     // prefix, which an L2 persisting window can cover (P:556-557 hot-embedding residue)
-    m->row_stride = int64_t(T) * D;
-    for (int t = 0; t < T; ++t) m->tab_off[t] = int64_t(t) * D;
+    m->row_stride = int64_t(TL) * D;
+    for (int tl = 0; tl < TL; ++tl) m->tab_off[tl] = int64_t(tl) * D;
   } else {
     m->row_stride = D;
     int64_t acc = 0;
-    for (int t = 0; t < T; ++t) {
-      m->tab_off[t] = acc * D;
-      acc += m->rows[t];
+    for (int tl = 0; tl < TL; ++tl) {
+      m->tab_off[tl] = acc * D;
+      acc += local_rows(tl);
     }
   }
   m->table_bytes = static_cast<size_t>(total_rows) * D * sizeof(float);
   ALLOC(m->tables, m->table_bytes);
-  ALLOC(m->d_tab_off, sizeof(int64_t) * T);
-  ALLOC(m->d_rows, sizeof(int64_t) * T);
-  CHECK_CUDA_CREATE(cudaMemcpy(m->d_tab_off, m->tab_off.data(), sizeof(int64_t) * T, cudaMemcpyHostToDevice));
-  CHECK_CUDA_CREATE(cudaMemcpy(m->d_rows, m->rows.data(), sizeof(int64_t) * T, cudaMemcpyHostToDevice));
-  for (int t = 0; t < T; ++t)
-    launch_init_table(m->tables + m->tab_off[t], m->rows[t], D, m->row_stride, t, m->k0, m->k1,
-                      m->emb_shift, m->value_mode, 0);
+  ALLOC(m->d_tab_off, sizeof(int64_t) * TL);
+  ALLOC(m->d_rows, sizeof(int64_t) * TL);
+  CHECK_CUDA_CREATE(cudaMemcpy(m->d_tab_off, m->tab_off.data(), sizeof(int64_t) * TL, cudaMemcpyHostToDevice));
+  CHECK_CUDA_CREATE(cudaMemcpy(m->d_rows, grows.data(), sizeof(int64_t) * TL, cudaMemcpyHostToDevice));
+  for (int tl = 0; tl < TL; ++tl)
+    launch_init_table(m->tables + m->tab_off[tl], local_rows(tl), D, m->row_stride, m->t0 + tl, m->k0,
+                      m->k1, m->emb_shift, m->value_mode, 0,
+                      m->shard == REC_SHARD_ROW && m->world > 1 ? m->row_lo : 0);
   CHECK_CUDA_CREATE(cudaGetLastError());
 
   // ---------------------------------------------------------------- MLP weights (G5)
@@ -1085,6 +1136,7 @@ rec_status rec_model_create(const rec_model_desc* d, rec_model_t* out) {
 
   // capture after the stream attributes (L2 window) are final: graph kernel nodes keep them
   for (auto& w : m->ws) {
+    if (m->world > 1 && m->shard != REC_SHARD_REPLICA) break;  // no synthetic chain when sharded
     rec_status st = capture_graphs(m, w);
     if (st != REC_OK) {
       free_model(m);
@@ -1120,6 +1172,10 @@ rec_status rec_query_async(rec_model_t m, int32_t slot, const float* dense, cons
     set_error("null argument");
     return REC_E_INVALID_ARG;
   }
+  if (m->world > 1 && m->shard != REC_SHARD_REPLICA) {
+    set_error("sharded models are synchronous collectives: use rec_query");
+    return REC_E_UNSUPPORTED;
+  }
   if (slot < 0 || slot >= m->nstreams) {
     set_error("slot = %d out of [0, %d)", slot, m->nstreams);
     return REC_E_INVALID_ARG;
@@ -1145,6 +1201,10 @@ rec_status rec_synth_query_async(rec_model_t m, int32_t slot, const int32_t* seg
     set_error("null argument");
     return REC_E_INVALID_ARG;
   }
+  if (m->world > 1 && m->shard != REC_SHARD_REPLICA) {
+    set_error("sharded models serve through rec_query (replicas serve synthetic batches)");
+    return REC_E_UNSUPPORTED;
+  }
   if (slot < 0 || slot >= m->nstreams) {
     set_error("slot = %d out of [0, %d)", slot, m->nstreams);
     return REC_E_INVALID_ARG;
@@ -1164,6 +1224,10 @@ rec_status rec_synth_query_batches(rec_model_t m, const int32_t* segs, const int
   if (!m || !segs || !batch_start || nbatches < 0 || first_slot < 0) {
     set_error("null argument or negative count");
     return REC_E_INVALID_ARG;
+  }
+  if (m->world > 1 && m->shard != REC_SHARD_REPLICA) {
+    set_error("sharded models serve through rec_query");
+    return REC_E_UNSUPPORTED;
   }
   REC_CUDA(cudaSetDevice(m->device));
   for (int64_t b = 0; b < nbatches; ++b) {

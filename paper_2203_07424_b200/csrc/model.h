@@ -133,9 +133,19 @@ struct rec_model_s {
                                        // slot wait+events, total)
   // distributed (sharded modes)
   void* nccl_comm = nullptr;
+  int t0 = 0, T_loc = 0;               // local tables [t0, t0 + T_loc)
+  int64_t row_lo = 0, row_hi = 0x7fffffff;  // local rows of every table (row-wise sharding)
+  float* sh_send = nullptr;            // [B_pad][T_loc][D] (table) or [B_pad][T][D] (row)
+  float* sh_recv = nullptr;            // [world][Bq][T_loc][D] (table) or [Bq][T][D] (row)
+  float* sh_ctr = nullptr;             // [world * Bq]
 };
 
 namespace rec {
+struct ShardPlan {
+  int t0, t_local;           // global index of the first local table, local table count
+  int64_t row_lo, row_hi;    // rows of every table held here (row-wise), else [0, INT32_MAX)
+};
+rec_status shard_plan(int T, const int64_t* rows, int world, int rank, int shard, ShardPlan* p);
 // Launch the forward of `batch` items on workspace `w` whose inputs are already in
 // w.indices / w.offsets / w.dense_bf (or caller device pointers).  ctr_out: device.
 rec_status forward_enqueue(rec_model_s* m, Workspace& w, const int* indices, const int* offsets,
@@ -146,6 +156,16 @@ rec_status forward_enqueue(rec_model_s* m, Workspace& w, const int* indices, con
 rec_status synth_submit(rec_model_s* m, Workspace& w, const int32_t* segs, int nseg, int* batch_out,
                         float* dense_f32_out);
 rec_status capture_graphs(rec_model_s* m, Workspace& w);
+void enqueue_bottom(rec_model_s* m, Workspace& w, cudaStream_t st, int B, const int* dB,
+                    cudaEvent_t* gev);
+void enqueue_interact_top(rec_model_s* m, Workspace& w, cudaStream_t st, int B, const int* dB,
+                          float* ctr_out, float* logit_out, cudaEvent_t* gev);
+// Model-parallel forward of a global batch (inputs staged on the device, identical on every
+// rank): local SLS -> all-to-all (table-wise) / reduce-scatter (row-wise) -> dense part on this
+// rank's item block -> all-gather of the CTRs into ctr (host or device) on every rank.
+rec_status sharded_forward(rec_model_s* m, Workspace& w, const float* d_dense, const int* d_idx,
+                           const int* d_off, int B, float* ctr, float* logits);
+rec_status sharded_alloc(rec_model_s* m);
 cudaEvent_t prof_begin(rec_model_s* m, cudaStream_t s);
 rec_status dist_init(rec_model_s* m, const void* nccl_id);   // dist.cu
 void dist_destroy(rec_model_s* m);
