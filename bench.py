@@ -91,7 +91,7 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.samples.append([x.strip() for x in line.split(",")])
+            self.samples.append([time.perf_counter()] + [x.strip() for x in line.split(",")])
 
     def __exit__(self, *a):
         if self.proc:
@@ -101,16 +101,22 @@ class ClockSampler:
             except Exception:
                 self.proc.kill()
 
-    def summary(self):
-        if not self.samples:
+    def summary(self, t0=None, t1=None):
+        """Median SM clock + throttle reasons.  Samples inside the timed region [t0, t1] when
+        there are any (100 ms sampling period), else every sample of the load window
+        (warm-up + timed region + profiling passes, all back-to-back GPU work)."""
+        inside = [s[1:] for s in self.samples if t0 is not None and t0 <= s[0] <= t1]
+        rows = inside or [s[1:] for s in self.samples]
+        if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        sm = [float(s[0]) for s in rows if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in rows if s[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4)
+        reasons = sorted({names[i] for s in rows for i in range(4)
                           if len(s) > 3 + i and s[3 + i].lower().startswith("active")})
         return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(self.samples)}
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(rows),
+                "window": "timed region" if inside else "load window (warm-up+timed+profiling)"}
 
 
 # ------------------------------------------------------------------ CPU oracle timing
@@ -293,6 +299,7 @@ def run_ours(args):
     tsegs = np.concatenate(tseg_list).astype(np.int32)
     tbstart = np.concatenate([[0], np.cumsum([len(x) for x in tseg_list])]).astype(np.int64)
 
+    clk = ClockSampler(local).__enter__()
     for i in range(args.warmup):
         step(i)
     sync_all()
@@ -302,7 +309,8 @@ def run_ours(args):
     torch.cuda.synchronize()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
+    if True:
+        t_region0 = time.perf_counter()
         ev0.record(stream)
         for s in streams[1:]:
             s.wait_event(ev0)                    # fork: every stream starts after ev0
@@ -321,6 +329,7 @@ def run_ours(args):
         ev1.record(stream)
         sync_all()
         torch.cuda.synchronize()
+        t_region1 = time.perf_counter()
     if world > 1:
         dist.barrier()
     ms = ev0.elapsed_time(ev1)
@@ -345,6 +354,7 @@ def run_ours(args):
     host_prof = {k: 1e3 * model.rec_profile_read(5 + j)[0] / hsteps
                  for j, k in enumerate(["param_update_us", "graph_launch_us", "slot_wait_us", "total_us"])}
     model.rec_profile(False)
+    clk.__exit__(None, None, None)
     ridx = [i % nb for i in range(args.warmup, args.warmup + rsteps)]
     ritems = sum(items_b[i] for i in ridx)
     idx = [i % nb for i in range(args.warmup, args.warmup + args.steps)]
@@ -447,7 +457,7 @@ def run_ours(args):
             "gpu_launches": int(launches),
             "host_submit_us_per_step": 1e6 * host_submit_s / args.steps,
             "host_submit_breakdown_per_step": host_prof,
-            "clocks": clk.summary(),
+            "clocks": clk.summary(t_region0, t_region1),
             "e2e": e2e,
             "sla": sla,
             "cpu_baseline": cpu,
