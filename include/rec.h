@@ -142,6 +142,11 @@ rec_status rec_gen_batch(rec_model_t m, const int32_t* segs, int32_t nseg,
  * 7 slot waits, 8 total).
  * enable != 0 turns recording on and resets the times. */
 rec_status rec_profile(rec_model_t m, int32_t enable);
+/* Diagnostic: time `iters` back-to-back launches of one dense stage on stream slot 0 at
+ * `batch` rows (which: 0 = bottom MLP, 1 = interaction + top MLP, 2 = interaction only)
+ * over whatever the workspace holds; *ms_per_iter = CUDA-event time per iteration.  Used to
+ * report tensor-pipe utilisation at large batches (north_star "MLP TC util"). */
+rec_status rec_bench_mlp(rec_model_t m, int32_t which, int32_t batch, int32_t iters, double* ms_per_iter);
 rec_status rec_profile_read(rec_model_t m, int32_t kernel, double* total_ms, int64_t* launches);
 
 /* ---------------------------------------------------------------- serving (a1, a7) */

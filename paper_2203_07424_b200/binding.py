@@ -32,7 +32,7 @@ EXPORTS = ["rec_model_create", "rec_model_destroy", "rec_query", "rec_query_debu
            "rec_query_async", "rec_synth_query_async", "rec_sync", "rec_stream_handle",
            "rec_gen_batch", "rec_profile", "rec_profile_read", "rec_serve", "rec_last_error",
            "rec_nccl_unique_id_size", "rec_nccl_get_unique_id", "rec_version", "rec_split_fuse",
-           "rec_synth_query_batches", "rec_shard_plan"]
+           "rec_synth_query_batches", "rec_shard_plan", "rec_bench_mlp"]
 
 
 class rec_model_desc(C.Structure):
@@ -102,6 +102,8 @@ def lib() -> C.CDLL:
         L.rec_synth_query_batches.restype = i32
         L.rec_shard_plan.argtypes = [i32, vp, i32, i32, i32, i32, vp]
         L.rec_shard_plan.restype = i32
+        L.rec_bench_mlp.argtypes = [vp, i32, i32, i32, C.POINTER(C.c_double)]
+        L.rec_bench_mlp.restype = i32
         for f in ("rec_model_create", "rec_query", "rec_query_debug", "rec_query_async",
                   "rec_synth_query_async", "rec_sync", "rec_gen_batch", "rec_profile",
                   "rec_profile_read", "rec_serve", "rec_nccl_get_unique_id"):
@@ -221,6 +223,11 @@ class RecModel:
         dense = np.zeros((B, cfg.dense_dim), dtype=np.float32)
         _check(lib().rec_gen_batch(self.h, _ptr(segs), segs.shape[0], _ptr(ind), _ptr(off), _ptr(dense)))
         return ind[:off[-1]].copy(), off, dense
+
+    def rec_bench_mlp(self, which: int, batch: int, iters: int = 50) -> float:
+        ms = C.c_double()
+        _check(lib().rec_bench_mlp(self.h, which, batch, iters, C.byref(ms)))
+        return ms.value
 
     def rec_profile(self, enable: bool):
         _check(lib().rec_profile(self.h, 1 if enable else 0))

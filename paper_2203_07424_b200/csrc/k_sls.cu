@@ -240,6 +240,16 @@ static void launch_l(const float* tables, const int64_t* tab_off, int64_t row_st
       flag, row_lo, row_hi);
 }
 
+void set_max_smem_carveout() {
+  const int c = cudaSharedmemCarveoutMaxShared;
+  cudaFuncSetAttribute(k_sls<8, 128>, cudaFuncAttributePreferredSharedMemoryCarveout, c);
+  cudaFuncSetAttribute(k_sls<16, 128>, cudaFuncAttributePreferredSharedMemoryCarveout, c);
+  cudaFuncSetAttribute(k_sls<32, 128>, cudaFuncAttributePreferredSharedMemoryCarveout, c);
+  cudaFuncSetAttribute(k_sls_synth<8, 128, 8>, cudaFuncAttributePreferredSharedMemoryCarveout, c);
+  cudaFuncSetAttribute(k_sls_synth<16, 128, 8>, cudaFuncAttributePreferredSharedMemoryCarveout, c);
+  cudaFuncSetAttribute(k_sls_synth<32, 128, 8>, cudaFuncAttributePreferredSharedMemoryCarveout, c);
+}
+
 void launch_sls(const float* tables, const int64_t* tab_off, int64_t row_stride,
                 const int64_t* rows, const int* indices, const int* offsets, int B, const int* dB,
                 int T, int D, float* X, int x_stride_items, int x_slot0, int* flag, cudaStream_t s,

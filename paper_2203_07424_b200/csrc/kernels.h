@@ -51,6 +51,7 @@ void launch_gen_variable_rest(const GenArgs& ga, cudaStream_t s);
 void launch_dense_to_bf16(const float* dense, int B, int F, int Fpad, __nv_bfloat16* out,
                           cudaStream_t s);
 void launch_check_offsets(const int* offsets, int nbags, int* flag, cudaStream_t s);
+void set_max_smem_carveout();  // prefer the max shared-memory carveout for every kernel
 
 // ------------------------------------------------------------------------- SLS (a3)
 // Row r of table t lives at tables + tab_off[t] + r * row_stride (floats).

@@ -829,6 +829,10 @@ rec_status rec_model_create(const rec_model_desc* d, rec_model_t* out) {
   }
   gemm_prepare();
   chain_prepare();
+  {
+    const char* e = getenv("REC_CARVEOUT");
+    if (e && e[0] == 'm') set_max_smem_carveout();  // experiment: never reconfigure smem/L1
+  }
 
   rec_model_s* m = new rec_model_s();
   m->T = d->num_tables;
@@ -1276,6 +1280,40 @@ rec_status rec_gen_batch(rec_model_t m, const int32_t* segs, int32_t nseg, int32
   REC_CUDA(cudaMemcpyAsync(indices, w.indices, sizeof(int) * nnz, cudaMemcpyDefault, s));
   REC_CUDA(cudaMemcpyAsync(dense, w.dense_f32, sizeof(float) * B * m->F, cudaMemcpyDefault, s));
   REC_CUDA(cudaStreamSynchronize(s));
+  return REC_OK;
+}
+
+rec_status rec_bench_mlp(rec_model_t m, int32_t which, int32_t batch, int32_t iters, double* ms_per_iter) {
+  if (!m || !ms_per_iter || batch < 1 || batch > m->max_batch || iters < 1 || which < 0 || which > 2) {
+    set_error("bad argument");
+    return REC_E_INVALID_ARG;
+  }
+  REC_CUDA(cudaSetDevice(m->device));
+  Workspace& w = m->ws[0];
+  cudaStream_t s = w.stream;
+  cudaEvent_t a, b;
+  REC_CUDA(cudaEventCreate(&a));
+  REC_CUDA(cudaEventCreate(&b));
+  const bool prof = m->prof;
+  m->prof = false;
+  auto once = [&]() {
+    if (which == 0) enqueue_bottom(m, w, s, batch, nullptr, nullptr);
+    else if (which == 1) enqueue_interact_top(m, w, s, batch, nullptr, w.ctr, w.logit, nullptr);
+    else launch_interact(w.X, batch, nullptr, m->T, m->D, w.A_top, m->Ktop_pad, s);
+  };
+  for (int i = 0; i < 3; ++i) once();
+  REC_CUDA(cudaEventRecord(a, s));
+  for (int i = 0; i < iters; ++i) once();
+  REC_CUDA(cudaEventRecord(b, s));
+  REC_CUDA(cudaEventSynchronize(b));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, a, b);
+  *ms_per_iter = ms / iters;
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  m->prof = prof;
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "rec_bench_mlp");
   return REC_OK;
 }
 
