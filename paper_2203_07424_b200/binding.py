@@ -16,7 +16,7 @@ from typing import Optional
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libhercules_rec.so")
+LIB_PATH = os.environ.get("REC_LIB_PATH") or os.path.join(HERE, "libhercules_rec.so")
 
 REC_OK = 0
 STATUS = {0: "REC_OK", -1: "REC_E_INVALID_ARG", -2: "REC_E_INDEX_OOB", -3: "REC_E_OFFSETS",

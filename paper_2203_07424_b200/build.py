@@ -38,8 +38,13 @@ def _nvcc() -> str:
     return "nvcc"
 
 
-def build(verbose: bool = False, force: bool = False) -> str:
-    os.makedirs(BUILD, exist_ok=True)
+def build(verbose: bool = False, force: bool = False, defines=(), out: str = OUT,
+          objdir: str = BUILD) -> str:
+    """Compile every source for sm_100a and link `out`.  `defines` (e.g. REC_MBAR_SPIN) go to
+    every translation unit; use a separate `objdir` for variant builds."""
+    BUILD_ = objdir
+    os.makedirs(BUILD_, exist_ok=True)
+    dflags = [f"-D{d}" for d in defines]
     nccl = _nccl_dir()
     inc = ["-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", os.path.join(nccl, "include")]
     hdr_mtime = max(os.path.getmtime(os.path.join(CSRC, h)) for h in HEADERS)
@@ -47,28 +52,28 @@ def build(verbose: bool = False, force: bool = False) -> str:
     objs = []
     for src in SOURCES:
         sp = os.path.join(CSRC, src)
-        op = os.path.join(BUILD, src + ".o")
+        op = os.path.join(BUILD_, src + ".o")
         objs.append(op)
         if not force and os.path.exists(op) and os.path.getmtime(op) > max(os.path.getmtime(sp), hdr_mtime):
             continue
         if src.endswith(".cu"):
             cmd = [_nvcc(), *ARCH, "-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC",
-                   "-Xcompiler", "-ffp-contract=off", "--expt-relaxed-constexpr", *inc,
+                   "-Xcompiler", "-ffp-contract=off", "--expt-relaxed-constexpr", *dflags, *inc,
                    "-c", sp, "-o", op]
         else:
-            cmd = ["g++", "-O2", "-std=c++17", "-fPIC", "-ffp-contract=off", "-pthread",
+            cmd = ["g++", "-O2", "-std=c++17", "-fPIC", "-ffp-contract=off", "-pthread", *dflags,
                    "-I", "/usr/local/cuda/include", *inc, "-c", sp, "-o", op]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
         subprocess.run(cmd, check=True)
-    link = [_nvcc(), *ARCH, "-shared", "-Xcompiler", "-fPIC", "-o", OUT, *objs,
+    link = [_nvcc(), *ARCH, "-shared", "-Xcompiler", "-fPIC", "-o", out, *objs,
             "-L", os.path.join(nccl, "lib"), "-l:libnccl.so.2",
             "-Xlinker", "-rpath=" + os.path.join(nccl, "lib"), "-lpthread"]
-    if force or not os.path.exists(OUT) or os.path.getmtime(OUT) < max(os.path.getmtime(o) for o in objs):
+    if force or not os.path.exists(out) or os.path.getmtime(out) < max(os.path.getmtime(o) for o in objs):
         if verbose:
             print(" ".join(link), file=sys.stderr)
         subprocess.run(link, check=True)
-    return OUT
+    return out
 
 
 if __name__ == "__main__":

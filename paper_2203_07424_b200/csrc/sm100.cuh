@@ -39,13 +39,30 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
+__device__ __forceinline__ bool mbar_test_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, P1;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
 // Blocking wait with a watchdog: a pipeline bug traps (a reported fault) instead of
-// hanging the GPU.  2^26 suspended try_waits is many seconds, far beyond any real wait.
+// hanging the GPU.  REC_MBAR_SPIN selects a non-suspending test_wait spin (A/B experiment).
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   uint32_t n = 0;
+#ifdef REC_MBAR_SPIN
+  while (!mbar_test_wait(bar, parity)) {
+    if (++n == (1u << 30)) __trap();
+  }
+#else
   while (!mbar_try_wait(bar, parity)) {
     if (++n == (1u << 26)) __trap();
   }
+#endif
 }
 
 // ------------------------------------------------------------------------------ TMA
