@@ -147,6 +147,11 @@ rec_status rec_profile(rec_model_t m, int32_t enable);
  * over whatever the workspace holds; *ms_per_iter = CUDA-event time per iteration.  Used to
  * report tensor-pipe utilisation at large batches (north_star "MLP TC util"). */
 rec_status rec_bench_mlp(rec_model_t m, int32_t which, int32_t batch, int32_t iters, double* ms_per_iter);
+/* Diagnostic: %globaltimer stamps (ns) of CTA 0 of one fused-MLP launch (which: 0 bottom,
+ * 1 top): [0] entry [1] TMEM+barriers ready [2] first TMA issued [3] first stage landed
+ * [4+l] layer l MMAs committed [8+2l]/[9+2l] epilogue l start/end [15] exit; [14] = CUDA-event
+ * time of the launch in ns.  Zero = stage not reached. */
+rec_status rec_debug_chain_timeline(rec_model_t m, int32_t which, int32_t batch, int64_t* out16);
 rec_status rec_profile_read(rec_model_t m, int32_t kernel, double* total_ms, int64_t* launches);
 
 /* ---------------------------------------------------------------- serving (a1, a7) */

@@ -32,7 +32,8 @@ EXPORTS = ["rec_model_create", "rec_model_destroy", "rec_query", "rec_query_debu
            "rec_query_async", "rec_synth_query_async", "rec_sync", "rec_stream_handle",
            "rec_gen_batch", "rec_profile", "rec_profile_read", "rec_serve", "rec_last_error",
            "rec_nccl_unique_id_size", "rec_nccl_get_unique_id", "rec_version", "rec_split_fuse",
-           "rec_synth_query_batches", "rec_shard_plan", "rec_bench_mlp"]
+           "rec_synth_query_batches", "rec_shard_plan", "rec_bench_mlp",
+           "rec_debug_chain_timeline"]
 
 
 class rec_model_desc(C.Structure):
@@ -104,6 +105,8 @@ def lib() -> C.CDLL:
         L.rec_shard_plan.restype = i32
         L.rec_bench_mlp.argtypes = [vp, i32, i32, i32, C.POINTER(C.c_double)]
         L.rec_bench_mlp.restype = i32
+        L.rec_debug_chain_timeline.argtypes = [vp, i32, i32, vp]
+        L.rec_debug_chain_timeline.restype = i32
         for f in ("rec_model_create", "rec_query", "rec_query_debug", "rec_query_async",
                   "rec_synth_query_async", "rec_sync", "rec_gen_batch", "rec_profile",
                   "rec_profile_read", "rec_serve", "rec_nccl_get_unique_id"):
@@ -228,6 +231,11 @@ class RecModel:
         ms = C.c_double()
         _check(lib().rec_bench_mlp(self.h, which, batch, iters, C.byref(ms)))
         return ms.value
+
+    def rec_debug_chain_timeline(self, which: int, batch: int):
+        out = np.zeros(16, dtype=np.int64)
+        _check(lib().rec_debug_chain_timeline(self.h, which, batch, _ptr(out)))
+        return out
 
     def rec_profile(self, enable: bool):
         _check(lib().rec_profile(self.h, 1 if enable else 0))

@@ -31,6 +31,16 @@ __device__ __forceinline__ void fence_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define STAMP(i)                                            \
+  do {                                                      \
+    if (args.dbg && blockIdx.x == 0) args.dbg[i] = gtimer(); \
+  } while (0)
+
 __device__ __forceinline__ const CUtensorMap* wmap(const ChainMaps& mp, int l) {
   return l == 0 ? &mp.w0 : l == 1 ? &mp.w1 : l == 2 ? &mp.w2 : &mp.w3;
 }
@@ -57,6 +67,7 @@ __global__ void __launch_bounds__(192, 1)
   const int M = args.dM ? *args.dM : args.M;
   if (m0 >= M) return;
   const int nl = args.nlayers;
+  if (threadIdx.x == 0) STAMP(0);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
@@ -74,6 +85,7 @@ __global__ void __launch_bounds__(192, 1)
   __syncthreads();
   sm100::tc_fence_after();
   const uint32_t tmem = *tslot;
+  if (threadIdx.x == 0) STAMP(1);
 
   if (warp == 0) {
     // ------------------------------------------------ TMA producer: (layer, n-chunk, k-block)
@@ -92,6 +104,7 @@ __global__ void __launch_bounds__(192, 1)
             sm100::mbar_arrive_expect_tx(&full[s], bytes);
             if (l == 0) sm100::tma_load_2d(st, &maps.a0, &full[s], kb * CBK, m0);
             sm100::tma_load_2d(st + C_A_BYTES, wmap(maps, l), &full[s], kb * CBK, n0);
+            if (it == 0) STAMP(2);
           }
           __syncwarp();
         }
@@ -115,6 +128,7 @@ __global__ void __launch_bounds__(192, 1)
           sm100::mbar_wait(&full[s], use & 1);
           sm100::tc_fence_after();
           if (lane == 0) {
+            if (it == 0) STAMP(3);
             const uint32_t st = sm100::smem_u32(ring + s * C_STAGE);
             const uint64_t da = sm100::umma_desc_sw128(l == 0 ? st : sm100::smem_u32(act + kb * C_A_BYTES));
             const uint64_t db = sm100::umma_desc_sw128(st + C_A_BYTES);
@@ -122,7 +136,10 @@ __global__ void __launch_bounds__(192, 1)
             for (int k = 0; k < CBK / 16; ++k)
               sm100::mma_bf16_ss(tmem + n0, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
             sm100::mma_commit(&empty[s]);
-            if (kb == nkb - 1 && n0 + 256 >= N) sm100::mma_commit(acc_full);
+            if (kb == nkb - 1 && n0 + 256 >= N) {
+              sm100::mma_commit(acc_full);
+              STAMP(4 + l);
+            }
           }
           __syncwarp();
         }
@@ -146,6 +163,7 @@ __global__ void __launch_bounds__(192, 1)
       const bool last = l == nl - 1;
       sm100::mbar_wait(acc_full, l & 1);
       sm100::tc_fence_after();
+      if (et == 0) STAMP(8 + 2 * l);
       float dot = 0.f;
       const int cols = last ? N : ((N + CBK - 1) / CBK) * CBK;  // hidden: zero the K padding
 #pragma unroll 1
@@ -196,6 +214,7 @@ __global__ void __launch_bounds__(192, 1)
         }
       }
       boff += N;
+      if (et == 0) STAMP(9 + 2 * l);
       if (!last) {
         fence_async_smem();          // generic-proxy smem writes -> visible to tcgen05.mma
         sm100::tc_fence_before();    // our tcgen05.ld of this layer are complete
@@ -210,6 +229,7 @@ __global__ void __launch_bounds__(192, 1)
   sm100::tc_fence_before();
   __syncthreads();
   if (warp == 0) sm100::tmem_dealloc(tmem, args.tmem_cols);
+  if (threadIdx.x == 0) STAMP(15);
 }
 
 size_t chain_smem_bytes(const ChainArgs& a) {

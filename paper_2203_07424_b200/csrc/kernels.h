@@ -129,6 +129,7 @@ struct ChainArgs {
   int act_kblocks;        // 64-column blocks of the widest hidden activation
   int tmem_cols;          // power of two >= 32 and >= max N
   int stages;             // set by chain_configure
+  unsigned long long* dbg;  // diagnostic: %globaltimer stamps of CTA 0 (nullptr = off)
 };
 size_t chain_smem_bytes(const ChainArgs& a);
 bool chain_configure(ChainArgs& a);   // false: does not fit in shared memory

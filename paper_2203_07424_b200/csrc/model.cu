@@ -1317,6 +1317,49 @@ rec_status rec_bench_mlp(rec_model_t m, int32_t which, int32_t batch, int32_t it
   return REC_OK;
 }
 
+rec_status rec_debug_chain_timeline(rec_model_t m, int32_t which, int32_t batch, int64_t* out16) {
+  if (!m || !out16 || batch < 1 || batch > m->max_batch || which < 0 || which > 1) {
+    set_error("bad argument");
+    return REC_E_INVALID_ARG;
+  }
+  if (!(which == 0 ? m->chain_bottom : m->chain_top)) {
+    set_error("no fused chain for this MLP");
+    return REC_E_UNSUPPORTED;
+  }
+  REC_CUDA(cudaSetDevice(m->device));
+  Workspace& w = m->ws[0];
+  unsigned long long* d = nullptr;
+  REC_CUDA(cudaMalloc(reinterpret_cast<void**>(&d), 16 * sizeof(unsigned long long)));
+  REC_CUDA(cudaMemset(d, 0, 16 * sizeof(unsigned long long)));
+  ChainArgs a = which == 0 ? m->chain_bottom_args : m->chain_top_args;
+  a.M = batch;
+  a.dM = nullptr;
+  a.out_f32 = w.X;
+  a.ldo = (m->T + 1) * m->D;
+  a.ctr = w.ctr;
+  a.logit = w.logit;
+  a.dbg = d;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  for (int rep = 0; rep < 3; ++rep) {
+    cudaEventRecord(e0, w.stream);
+    launch_mlp_chain(which == 0 ? w.chain_bottom : w.chain_top, a, w.stream);
+    cudaEventRecord(e1, w.stream);
+  }
+  REC_CUDA(cudaStreamSynchronize(w.stream));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  unsigned long long h[16];
+  REC_CUDA(cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost));
+  cudaFree(d);
+  for (int i = 0; i < 16; ++i) out16[i] = static_cast<int64_t>(h[i]);
+  out16[14] = static_cast<int64_t>(ms * 1e6);  // event time of the last launch (ns)
+  return REC_OK;
+}
+
 rec_status rec_profile(rec_model_t m, int32_t enable) {
   if (!m) {
     set_error("null model");
