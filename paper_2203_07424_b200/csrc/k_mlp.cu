@@ -166,51 +166,58 @@ __global__ void __launch_bounds__(192, 1)
       if (et == 0) STAMP(8 + 2 * l);
       float dot = 0.f;
       const int cols = last ? N : ((N + CBK - 1) / CBK) * CBK;  // hidden: zero the K padding
+      // 64 columns per round: four tcgen05.ld (16 columns each) in flight, ONE wait, then the
+      // math / stores of all four (a wait per 16 columns serialised the epilogue).
 #pragma unroll 1
-      for (int c0 = 0; c0 < cols; c0 += 16) {
-        uint32_t rr[16];
-        if (c0 < N) {
-          sm100::tmem_ld_32x32b_x16(trow + c0, rr);
-          sm100::tmem_ld_wait();
-        }
-        float v[16];
+      for (int g0 = 0; g0 < cols; g0 += 64) {
+        uint32_t rr[4][16];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const int c = c0 + j;
-          float x = 0.f;
-          if (c < N) x = fmaxf(__uint_as_float(rr[j]) + s_bias[boff + c], 0.f);
-          v[j] = x;
-        }
-        if (!last) {
-          // bf16 into the swizzled K-major A operand of layer l+1: column c0 lies in k-block
-          // c0/64, 16-byte unit (c0%64)/8 (and the next one), XOR-swizzled by row % 8.
-          uint32_t p[8];
+        for (int q = 0; q < 4; ++q)
+          if (g0 + 16 * q < N) sm100::tmem_ld_32x32b_x16(trow + g0 + 16 * q, rr[q]);
+        sm100::tmem_ld_wait();
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * j], v[2 * j + 1]);
-            p[j] = *reinterpret_cast<uint32_t*>(&h);
+        for (int q = 0; q < 4; ++q) {
+          const int c0 = g0 + 16 * q;
+          if (c0 >= cols) break;
+          float v[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const int c = c0 + j;
+            float x = 0.f;
+            if (c < N) x = fmaxf(__uint_as_float(rr[q][j]) + s_bias[boff + c], 0.f);
+            v[j] = x;
           }
-          uint8_t* blk = act + (c0 / CBK) * C_A_BYTES + r * 128;
-          const int u = (c0 % CBK) / 8;
-          *reinterpret_cast<uint4*>(blk + ((u ^ (r & 7)) << 4)) = make_uint4(p[0], p[1], p[2], p[3]);
-          *reinterpret_cast<uint4*>(blk + (((u + 1) ^ (r & 7)) << 4)) = make_uint4(p[4], p[5], p[6], p[7]);
-        } else if (args.mode_last == GEMM_OUT_X_F32) {
-          if (row_ok) {
-            float* dst = args.out_f32 + static_cast<int64_t>(row) * args.ldo + c0;
-            if (c0 + 16 <= N) {
-              float4* d4 = reinterpret_cast<float4*>(dst);
+          if (!last) {
+            // bf16 into the swizzled K-major A operand of layer l+1: column c0 lies in k-block
+            // c0/64, 16-byte unit (c0%64)/8 (and the next one), XOR-swizzled by row % 8.
+            uint32_t p[8];
 #pragma unroll
-              for (int j = 0; j < 4; ++j) d4[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-            } else {
-#pragma unroll
-              for (int j = 0; j < 16; ++j)
-                if (c0 + j < N) dst[j] = v[j];
+            for (int j = 0; j < 8; ++j) {
+              __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * j], v[2 * j + 1]);
+              p[j] = *reinterpret_cast<uint32_t*>(&h);
             }
-          }
-        } else {
+            uint8_t* blk = act + (c0 / CBK) * C_A_BYTES + r * 128;
+            const int u = (c0 % CBK) / 8;
+            *reinterpret_cast<uint4*>(blk + ((u ^ (r & 7)) << 4)) = make_uint4(p[0], p[1], p[2], p[3]);
+            *reinterpret_cast<uint4*>(blk + (((u + 1) ^ (r & 7)) << 4)) = make_uint4(p[4], p[5], p[6], p[7]);
+          } else if (args.mode_last == GEMM_OUT_X_F32) {
+            if (row_ok) {
+              float* dst = args.out_f32 + static_cast<int64_t>(row) * args.ldo + c0;
+              if (c0 + 16 <= N) {
+                float4* d4 = reinterpret_cast<float4*>(dst);
 #pragma unroll
-          for (int j = 0; j < 16; ++j)
-            if (c0 + j < N) dot = fmaf(v[j], s_wl[c0 + j], dot);
+                for (int j = 0; j < 4; ++j) d4[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+              } else {
+#pragma unroll
+                for (int j = 0; j < 16; ++j)
+                  if (c0 + j < N) dst[j] = v[j];
+              }
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+              if (c0 + j < N) dot = fmaf(v[j], s_wl[c0 + j], dot);
+          }
         }
       }
       boff += N;
