@@ -172,9 +172,17 @@ __global__ void __launch_bounds__(192, 1)
       for (int g0 = 0; g0 < cols; g0 += 64) {
         uint32_t rr[4][16];
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
-          if (g0 + 16 * q < N) sm100::tmem_ld_32x32b_x16(trow + g0 + 16 * q, rr[q]);
-        sm100::tmem_ld_wait();
+        if (args.dbg_mode & 1) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+#pragma unroll
+            for (int j = 0; j < 16; ++j) rr[q][j] = 0u;
+        } else {
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (g0 + 16 * q < N) sm100::tmem_ld_32x32b_x16(trow + g0 + 16 * q, rr[q]);
+          sm100::tmem_ld_wait();
+        }
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           const int c0 = g0 + 16 * q;
@@ -187,7 +195,9 @@ __global__ void __launch_bounds__(192, 1)
             if (c < N) x = fmaxf(__uint_as_float(rr[q][j]) + s_bias[boff + c], 0.f);
             v[j] = x;
           }
-          if (!last) {
+          if (!last && (args.dbg_mode & 2)) {
+            dot += v[0];  // keep the math alive, skip the stores
+          } else if (!last) {
             // bf16 into the swizzled K-major A operand of layer l+1: column c0 lies in k-block
             // c0/64, 16-byte unit (c0%64)/8 (and the next one), XOR-swizzled by row % 8.
             uint32_t p[8];

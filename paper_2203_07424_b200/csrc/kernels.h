@@ -130,6 +130,7 @@ struct ChainArgs {
   int tmem_cols;          // power of two >= 32 and >= max N
   int stages;             // set by chain_configure
   unsigned long long* dbg;  // diagnostic: %globaltimer stamps of CTA 0 (nullptr = off)
+  int dbg_mode;             // diagnostic: bit0 skip TMEM loads, bit1 skip hidden smem stores
 };
 size_t chain_smem_bytes(const ChainArgs& a);
 bool chain_configure(ChainArgs& a);   // false: does not fit in shared memory

@@ -1339,6 +1339,7 @@ rec_status rec_debug_chain_timeline(rec_model_t m, int32_t which, int32_t batch,
   a.ctr = w.ctr;
   a.logit = w.logit;
   a.dbg = d;
+  if (const char* e = getenv("REC_DBG_EPI")) a.dbg_mode = atoi(e);
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
