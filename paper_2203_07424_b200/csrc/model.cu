@@ -391,66 +391,6 @@ static void collect_slot(rec_model_s* m, SynthSlot& sl) {
   sl.prof_pending = false;
 }
 
-// ------------------------------------------------------------ VMM table arena (experiment)
-#include <cudaTypedefs.h>
-template <typename F>
-static F drv(const char* name) {
-  void* p = nullptr;
-  cudaDriverEntryPointQueryResult q;
-  cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q);
-  return reinterpret_cast<F>(p);
-}
-
-rec_status vmm_alloc(int device, size_t bytes, void** out, size_t* mapped) {
-  auto create = drv<PFN_cuMemCreate_v10020>("cuMemCreate");
-  auto reserve = drv<PFN_cuMemAddressReserve_v10020>("cuMemAddressReserve");
-  auto map = drv<PFN_cuMemMap_v10020>("cuMemMap");
-  auto access = drv<PFN_cuMemSetAccess_v10020>("cuMemSetAccess");
-  auto gran = drv<PFN_cuMemGetAllocationGranularity_v10020>("cuMemGetAllocationGranularity");
-  auto release = drv<PFN_cuMemRelease_v10020>("cuMemRelease");
-  if (!create || !reserve || !map || !access || !gran || !release) {
-    set_error("VMM driver entry points unavailable");
-    return REC_E_CUDA;
-  }
-  CUmemAllocationProp prop{};
-  prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
-  prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
-  prop.location.id = device;
-  size_t g = 0;
-  gran(&g, &prop, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED);
-  if (g == 0) g = size_t(2) << 20;
-  const size_t sz = (bytes + g - 1) / g * g;
-  CUmemGenericAllocationHandle h;
-  if (create(&h, sz, &prop, 0) != CUDA_SUCCESS) {
-    set_error("cuMemCreate of %zu bytes failed", sz);
-    return REC_E_OOM;
-  }
-  CUdeviceptr va = 0;
-  if (reserve(&va, sz, size_t(1) << 30, 0, 0) != CUDA_SUCCESS || map(va, sz, 0, h, 0) != CUDA_SUCCESS) {
-    release(h);
-    set_error("cuMemAddressReserve/cuMemMap failed");
-    return REC_E_OOM;
-  }
-  release(h);  // the mapping keeps the memory alive
-  CUmemAccessDesc ad{};
-  ad.location = prop.location;
-  ad.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
-  if (access(va, sz, &ad, 1) != CUDA_SUCCESS) {
-    set_error("cuMemSetAccess failed");
-    return REC_E_CUDA;
-  }
-  *out = reinterpret_cast<void*>(va);
-  *mapped = sz;
-  return REC_OK;
-}
-
-void vmm_free(void* p, size_t bytes) {
-  auto unmap = drv<PFN_cuMemUnmap_v10020>("cuMemUnmap");
-  auto freeva = drv<PFN_cuMemAddressFree_v10020>("cuMemAddressFree");
-  if (unmap) unmap(reinterpret_cast<CUdeviceptr>(p), bytes);
-  if (freeva) freeva(reinterpret_cast<CUdeviceptr>(p), bytes);
-}
-
 static inline double host_now_ns() {
   return std::chrono::duration<double, std::nano>(std::chrono::steady_clock::now().time_since_epoch())
       .count();
@@ -740,8 +680,7 @@ static void free_model(rec_model_s* m) {
   cudaFree(m->w_last);
   cudaFree(m->bias_bottom_all);
   cudaFree(m->bias_top_all);
-  if (m->vmm_bytes) vmm_free(m->tables, m->vmm_bytes);
-  else cudaFree(m->tables);
+  cudaFree(m->tables);
   cudaFree(m->d_tab_off);
   cudaFree(m->d_rows);
   for (auto& e : m->prof_events) {
@@ -968,19 +907,7 @@ rec_status rec_model_create(const rec_model_desc* d, rec_model_t* out) {
     }
   }
   m->table_bytes = static_cast<size_t>(total_rows) * D * sizeof(float);
-  {
-    const char* e = getenv("REC_VMM_TABLES");  // experiment: one physical allocation, 1 GB-aligned VA
-    if (e && e[0] == '1') {
-      rec_status st = vmm_alloc(m->device, m->table_bytes, reinterpret_cast<void**>(&m->tables),
-                                &m->vmm_bytes);
-      if (st != REC_OK) {
-        free_model(m);
-        return st;
-      }
-    } else {
-      ALLOC(m->tables, m->table_bytes);
-    }
-  }
+  ALLOC(m->tables, m->table_bytes);
   ALLOC(m->d_tab_off, sizeof(int64_t) * TL);
   ALLOC(m->d_rows, sizeof(int64_t) * TL);
   CHECK_CUDA_CREATE(cudaMemcpy(m->d_tab_off, m->tab_off.data(), sizeof(int64_t) * TL, cudaMemcpyHostToDevice));

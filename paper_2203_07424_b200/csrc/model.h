@@ -105,7 +105,6 @@ struct rec_model_s {
   // embedding arena
   float* tables = nullptr;
   size_t table_bytes = 0;
-  size_t vmm_bytes = 0;                // > 0: arena mapped through the VMM API
   bool interleaved = false;
   int64_t row_stride = 0;              // floats between consecutive rows of one table
   std::vector<int64_t> tab_off;        // floats, start of row 0 of table t
@@ -147,8 +146,6 @@ struct ShardPlan {
   int64_t row_lo, row_hi;    // rows of every table held here (row-wise), else [0, INT32_MAX)
 };
 rec_status shard_plan(int T, const int64_t* rows, int world, int rank, int shard, ShardPlan* p);
-rec_status vmm_alloc(int device, size_t bytes, void** out, size_t* mapped);
-void vmm_free(void* p, size_t bytes);
 // Launch the forward of `batch` items on workspace `w` whose inputs are already in
 // w.indices / w.offsets / w.dense_bf (or caller device pointers).  ctr_out: device.
 rec_status forward_enqueue(rec_model_s* m, Workspace& w, const int* indices, const int* offsets,
