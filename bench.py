@@ -372,6 +372,10 @@ def run_ours(args):
     value = tot_q / (ms_max * 1e-3)
 
     hbm_peak, bf16_peak, peak_kind = peaks()
+    traffic = None  # ncu dram__bytes_read.sum + dram__bytes_write.sum per SLS launch (committed capture)
+    tp = os.path.join(ROOT, "profiles", "sls_traffic.json")
+    if os.path.exists(tp):
+        traffic = json.load(open(tp)).get("dram_bytes_per_launch")
     sls_bytes = sls_bytes_per_item(cfg, synth=True) * ritems
     sls_gbs = sls_bytes / (sls_ms * 1e-3) / 1e9 if sls_ms > 0 else None
     flops = mlp_flops_per_item(cfg) * ritems
@@ -443,7 +447,8 @@ def run_ours(args):
                        "value_is": "saturation QPS (burst trace); see sla"},
             "roofline": {"bound": "hbm", "kernel": "k_sls", "achieved": sls_gbs, "peak": hbm_peak,
                          "unit": "GB/s", "frac": (sls_gbs / hbm_peak) if sls_gbs else None,
-                         "traffic": None, "peak_kind": peak_kind,
+                         "traffic": traffic, "traffic_source": "profiles/sls_traffic.json (ncu --set full)",
+                         "algorithmic_bytes_per_launch": sls_bytes / max(sls_n, 1), "peak_kind": peak_kind,
                          "bytes_per_item": sls_bytes_per_item(cfg, synth=True), "launches": sls_n,
                          "avg_launch_us": 1e3 * sls_ms / max(sls_n, 1),
                          "measured": f"CUDA events around every SLS launch on its stream, "
@@ -471,7 +476,7 @@ def run_ours(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=3000)
+    ap.add_argument("--steps", type=int, default=20000)
     ap.add_argument("--warmup", type=int, default=50)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="rmc1", choices=list(W.SHORT))
