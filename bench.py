@@ -151,72 +151,8 @@ def host_cores() -> int:
         return os.cpu_count() or 1
 
 
-# ------------------------------------------------------------- replica serving helpers
-def rank_share(trace: np.ndarray, world: int, rank: int) -> np.ndarray:
-    """Replica dispatch: query q is served by GPU q mod G; arrival times kept."""
-    return trace[trace["qid"] % world == rank]
-
-
-def gather_latencies(lat_ms: np.ndarray, world: int, rank: int, dist):
-    """All ranks' per-query latencies on rank 0 (C4; None elsewhere)."""
-    if world == 1:
-        return np.asarray(lat_ms)
-    parts = [None] * world
-    dist.all_gather_object(parts, np.asarray(lat_ms))
-    return np.concatenate(parts) if rank == 0 else None
-
-
-def p95_nearest_rank(lat_ms: np.ndarray) -> float:
-    s = np.sort(np.asarray(lat_ms, dtype=np.float64))
-    return float(s[max((95 * s.size + 99) // 100, 1) - 1]) if s.size else float("nan")
-
-
-def sla_search(model, cfg, world, rank, dist, streams, d, lam0, n, sla_ms, max_iter=10):
-    """lambda*: largest offered Poisson rate (all GPUs) with p95 <= SLA and every GPU keeping up
-    (S5; geometric bracketing then bisection).  Real clock, device-synth inputs."""
-    import torch
-    probes = []
-    count = [0]
-
-    def probe(lam):
-        count[0] += 1
-        tr = W.poisson_trace(lam, n, seed=12)
-        mine = rank_share(tr, world, rank)
-        rep = model.rec_serve(mine, sla_ms, streams, d, warmup_frac=0.1)
-        arr = mine["arrival_s"]
-        w_end = tr["arrival_s"][0] + 0.1 * (tr["arrival_s"][-1] - tr["arrival_s"][0])
-        lat = gather_latencies(rep["latency_ms"][arr >= w_end], world, rank, dist)
-        stable = torch.tensor([rep["stable"]], device="cuda")
-        if world > 1:
-            dist.all_reduce(stable, op=dist.ReduceOp.MIN)
-        ok = torch.tensor([0], device="cuda")
-        if rank == 0:
-            p95 = p95_nearest_rank(lat)
-            ok[0] = int(stable.item() == 1 and p95 <= sla_ms)
-            probes.append({"offered_qps": round(lam), "p95_ms": round(p95, 3), "ok": int(ok.item())})
-        if world > 1:
-            dist.broadcast(ok, 0)
-        return bool(ok.item())
-
-    lo, hi, lam = None, None, lam0
-    for _ in range(max_iter):
-        if probe(lam):
-            lo = lam
-            if hi is not None:
-                break
-            lam *= 2.0
-        else:
-            hi = lam
-            if lo is not None:
-                break
-            lam *= 0.5
-    while lo is not None and hi is not None and (hi - lo) > 0.01 * lo and count[0] < 2 * max_iter:
-        mid = 0.5 * (lo + hi)
-        if probe(mid):
-            lo = mid
-        else:
-            hi = mid
-    return (lo or 0.0), probes
+from harness.sla import rank_share, gather_latencies, p95_nearest_rank, sla_search  # noqa: E402
+from harness.schedsearch import gradient_search  # noqa: E402
 
 
 # ---------------------------------------------------------------------- reference arm
@@ -415,13 +351,30 @@ def run_ours(args):
 
     sla = None
     if args.sla_queries > 0:
-        lam_star, probes = sla_search(model, cfg, world, rank, dist, m_streams, d, 0.5 * value,
-                                      args.sla_queries, cfg.sla_ms)
-        sla = {"sla_ms": cfg.sla_ms, "percentile": "p95 (nearest rank)", "lambda_star_qps": lam_star,
-               "queries_per_probe": args.sla_queries, "probes": probes,
-               "mode": "rec_serve real clock, Poisson arrivals, lognormal sizes (R13), "
-                       f"split/fuse d={d}, {m_streams} co-located streams per GPU, device-synth inputs, "
-                       "replica dispatch q mod G"}
+        # Alg. 1 over the serving policy (m streams x d max batch); each point is
+        # evaluated by its SLA-bounded QPS lambda* (real-clock rec_serve, p95 <= SLA)
+        probes_all = {}
+        lam_hint = [0.5 * value]
+
+        def evaluate(m, dd):
+            lam, pr = sla_search(model, cfg, world, rank, dist, m, dd, lam_hint[0],
+                                 args.sla_queries, cfg.sla_ms)
+            probes_all[f"m{m}_d{dd}"] = pr
+            if lam > 0:
+                lam_hint[0] = lam
+            return lam
+
+        ms = [x for x in (1, 2, 4, 8) if x <= m_streams]
+        ds = [x for x in (256, 512, 1024) if x <= d]
+        res = gradient_search(evaluate, ms, ds, noise=0.02)
+        sla = {"sla_ms": cfg.sla_ms, "percentile": "p95 (nearest rank)",
+               "lambda_star_qps": res["qps"], "policy": {"streams": res["m"], "max_batch": res["d"]},
+               "alg1_path": res["path"], "alg1_evaluated": res["evaluated"],
+               "queries_per_probe": args.sla_queries,
+               "probes_at_best": probes_all.get(f"m{res['m']}_d{res['d']}"),
+               "mode": "rec_serve real clock, Poisson arrivals, lognormal sizes (R13), split/fuse, "
+                       "device-synth inputs, replica dispatch q mod G; Alg. 1 gradient search over "
+                       "(streams, max_batch)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

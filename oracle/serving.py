@@ -200,3 +200,64 @@ def lambda_star(probe: Callable[[float], bool], lam0: float, max_iter: int = 12,
         else:
             hi = mid
     return lo
+
+
+# ------------------------------------------------------------------------------------
+# Algorithm 1: gradient-based search over P_sp(M+D) on an accelerator
+# (no op-parallelism loop on a GPU).  Start at the origin (minimal co-location m and
+# batch d); the three candidates are "(1) increasing the batch size only, (2)
+# increasing the number of threads only, and (3) increasing both"; move to the
+# candidate with the largest throughput gain while it is positive, where the
+# throughput of a configuration is its latency-bounded QPS (lambda*, which embeds the SLA
+# constraint of Alg. 1).  Ties: lower m, then lower d.
+# ------------------------------------------------------------------------------------
+def candidate_moves(im: int, id_: int, nm: int, nd: int):
+    """Grid neighbours of (m index, d index): d+1, m+1, both (SPEC.md candidate_moves)."""
+    out = []
+    if id_ + 1 < nd:
+        out.append((im, id_ + 1))
+    if im + 1 < nm:
+        out.append((im + 1, id_))
+    if im + 1 < nm and id_ + 1 < nd:
+        out.append((im + 1, id_ + 1))
+    return out
+
+
+def gradient_search(evaluate, ms, ds, noise: float = 0.0):
+    """Alg. 1 on the grid ms x ds; evaluate(m, d) -> latency-bounded QPS (>= 0).
+
+    Returns dict(m, d, qps, evals, path).  A move needs gain > noise * current (SPEC.md:419
+    noise band for measured surfaces; 0 for exact ones)."""
+    cache = {}
+
+    def f(i, j):
+        if (i, j) not in cache:
+            cache[(i, j)] = float(evaluate(ms[i], ds[j]))
+        return cache[(i, j)]
+
+    cur = (0, 0)
+    path = [cur]
+    while True:
+        cands = candidate_moves(cur[0], cur[1], len(ms), len(ds))
+        if not cands:
+            break
+        best = max(cands, key=lambda c: (f(*c), -c[0], -c[1]))
+        if f(*best) - f(*cur) > noise * f(*cur) and f(*best) > f(*cur):
+            cur = best
+            path.append(cur)
+        else:
+            break
+    return dict(m=ms[cur[0]], d=ds[cur[1]], qps=f(*cur), evals=len(cache),
+                path=[(ms[i], ds[j]) for i, j in path])
+
+
+def brute_force_search(evaluate, ms, ds):
+    """Exhaustive argmax over the grid; ties: lower m, then lower d."""
+    best = None
+    for i, m in enumerate(ms):
+        for j, d in enumerate(ds):
+            v = float(evaluate(m, d))
+            key = (v, -i, -j)
+            if best is None or key > best[0]:
+                best = (key, m, d, v)
+    return dict(m=best[1], d=best[2], qps=best[3])

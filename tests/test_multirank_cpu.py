@@ -79,22 +79,22 @@ def test_shard_plans_partition_gloo():
 def _replica_p95(rank, world):
     import sys
     sys.path.insert(0, ROOT)
-    import bench
+    from harness import sla
     from oracle import serving as sv
     tr = W.poisson_trace(20000.0, 400, seed=5)
-    mine = bench.rank_share(tr, world, rank)
+    mine = sla.rank_share(tr, world, rank)
     r = sv.replay_virtual(mine, 2, 256, 20000.0, 30.0)
-    lat = bench.gather_latencies(r.latency_s * 1e3, world, rank, dist)
+    lat = sla.gather_latencies(r.latency_s * 1e3, world, rank, dist)
     return None if lat is None else sorted(lat.tolist())
 
 
 def test_replica_dispatch_and_latency_gather_gloo():
     out = _spawn(_replica_p95, port=29611)
     assert not isinstance(out[0], str), out
-    import bench
+    from harness import sla
     from oracle import serving as sv
     tr = W.poisson_trace(20000.0, 400, seed=5)
-    parts = [bench.rank_share(tr, 2, r) for r in range(2)]
+    parts = [sla.rank_share(tr, 2, r) for r in range(2)]
     assert sorted(np.concatenate([p["qid"] for p in parts]).tolist()) == list(range(400))
     exp = np.concatenate([sv.replay_virtual(p, 2, 256, 20000.0, 30.0).latency_s * 1e3 for p in parts])
     assert out[0] == sorted(exp.tolist())
