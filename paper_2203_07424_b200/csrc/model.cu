@@ -465,9 +465,9 @@ rec_status synth_submit(rec_model_s* m, Workspace& w, const int32_t* segs, int n
     const double t2 = host_now_ns();
     REC_CUDA(cudaGraphLaunch(V.exec, w.stream));
     const double t3 = host_now_ns();
-    m->host_ns[0] += t2 - t1;
-    m->host_ns[1] += t3 - t2;
-    m->host_ns[2] += t1 - t0;
+    w.host_ns[0] += t2 - t1;
+    w.host_ns[1] += t3 - t2;
+    w.host_ns[2] += t1 - t0;
     m->launches += w.graph_kernels;
     sl.prof_pending = m->prof;
   } else {
@@ -478,7 +478,7 @@ rec_status synth_submit(rec_model_s* m, Workspace& w, const int32_t* segs, int n
     if (st != REC_OK) return st;
   }
   REC_CUDA(cudaEventRecord(sl.free, w.stream));
-  m->host_ns[3] += host_now_ns() - t0;
+  w.host_ns[3] += host_now_ns() - t0;
   *batch_out = static_cast<int>(B);
   return REC_OK;
 }
@@ -1371,7 +1371,7 @@ rec_status rec_profile(rec_model_t m, int32_t enable) {
   for (int k = 0; k < 4; ++k) {
     m->prof_ms[k] = 0;
     m->prof_n[k] = 0;
-    m->host_ns[k] = 0;
+    for (auto& w : m->ws) w.host_ns[k] = 0;
   }
   m->prof = enable != 0;
   return REC_OK;
@@ -1388,7 +1388,9 @@ rec_status rec_profile_read(rec_model_t m, int32_t kernel, double* total_ms, int
     return REC_OK;
   }
   if (kernel >= 5 && kernel <= 8) {  // host time of the synthetic submit path
-    *total_ms = m->host_ns[kernel - 5] * 1e-6;
+    double ns = 0;
+    for (auto& w : m->ws) ns += w.host_ns[kernel - 5];
+    *total_ms = ns * 1e-6;
     *launches = 0;
     return REC_OK;
   }

@@ -4,6 +4,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 #include <string>
 #include <vector>
@@ -82,6 +83,8 @@ struct Workspace {
   std::vector<SynthSlot> slots;                        // synthetic-batch staging ring
   int next_slot = 0;
   int graph_kernels = 0;                               // kernels per graph launch
+  double host_ns[4] = {0, 0, 0, 0};  // host time in synth_submit (param update, graph launch,
+                                     // slot wait, total) — per stream: dispatch threads
 };
 
 struct ProfEvent {
@@ -128,9 +131,7 @@ struct rec_model_s {
   std::vector<cudaEvent_t> prof_pool;
   double prof_ms[4] = {0, 0, 0, 0};
   int64_t prof_n[4] = {0, 0, 0, 0};
-  int64_t launches = 0;                // kernels launched by this handle (all streams)
-  double host_ns[4] = {0, 0, 0, 0};    // profiling: host time in synth_submit (params, launch,
-                                       // slot wait+events, total)
+  std::atomic<int64_t> launches{0};    // kernels launched by this handle (all streams)
   // distributed (sharded modes)
   void* nccl_comm = nullptr;
   int t0 = 0, T_loc = 0;               // local tables [t0, t0 + T_loc)

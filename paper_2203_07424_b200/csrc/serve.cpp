@@ -3,19 +3,23 @@
 // "each large inference query is split into multiple sub-queries ...
 // On accelerators, the inference queries are fused into one large batch ... query fusion";
 // model co-location = m concurrent inference threads on one accelerator, here
-// m CUDA streams (one workspace each) driven by one dispatcher thread; the objective
+// m CUDA streams (one workspace each) with one dispatcher thread each; the objective
 // is throughput under a tail-latency SLA.
 //
 // Real clock: queries are released open-loop at their trace arrival times (busy-waiting on
-// CLOCK_MONOTONIC); whenever a stream is idle the dispatcher fuses FIFO sub-queries into a
-// batch (Σ <= d) and enqueues input materialisation + the forward chain on that stream;
-// completion is observed by polling a CUDA event per stream; a query's latency ends when
-// the host observes the completion of its last sub-query (reading R16).
+// CLOCK_MONOTONIC); whenever a stream is idle its dispatcher fuses FIFO sub-queries into a
+// batch (Σ <= d) and submits input materialisation + the forward chain (one captured graph)
+// on that stream; completion is observed by polling a host-mapped word the stream writes
+// after the batch; a query's latency ends when the host observes the completion of its last
+// sub-query (reading R16).
 // Virtual clock (S4): identical dispatch rules on a simulated clock with service time
 // alpha + beta * items, so the batch list is unique and bit-exact with oracle/serving.py;
 // the kernels still run for every batch (CTRs are real).
 #include <algorithm>
+#include <atomic>
 #include <chrono>
+#include <mutex>
+#include <thread>
 #include <cmath>
 #include <cstring>
 #include <queue>
@@ -66,8 +70,23 @@ struct Lane {
   bool busy = false;
   int64_t batch = -1;
   cudaEvent_t done = nullptr;
-  float* ctr_host = nullptr;  // pinned [cap]
+  float* ctr_host = nullptr;       // pinned [cap]
+  uint32_t* flag_host = nullptr;   // pinned + mapped: batch sequence number written by the GPU
+  CUdeviceptr flag_dev = 0;
 };
+
+// cuStreamWriteValue32 through the runtime's driver entry point (no libcuda link).
+static rec_status stream_write_u32(cudaStream_t s, CUdeviceptr addr, uint32_t v) {
+  using Fn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+  static Fn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q);
+    return reinterpret_cast<Fn>(p);
+  }();
+  if (!fn) return REC_E_UNSUPPORTED;
+  return fn(reinterpret_cast<CUstream>(s), addr, v, 0) == CUDA_SUCCESS ? REC_OK : REC_E_CUDA;
+}
 
 // Host-input mode: per-query materialised inputs (table-major within the query).
 struct HostInputs {
@@ -285,11 +304,26 @@ rec_status rec_serve(rec_model_t m, const rec_trace_row* trace, int64_t n, doubl
   for (int s = 0; s < M; ++s) {
     REC_CUDA(cudaEventCreateWithFlags(&lanes[s].done, cudaEventDisableTiming));
     if (ctr_out) REC_CUDA(cudaMallocHost(reinterpret_cast<void**>(&lanes[s].ctr_host), sizeof(float) * d));
+    if (!virt) {  // host-mapped completion word (falls back to event polling if unavailable)
+      void* hp = nullptr;
+      void* dp = nullptr;
+      if (cudaHostAlloc(&hp, 64, cudaHostAllocMapped) == cudaSuccess &&
+          cudaHostGetDevicePointer(&dp, hp, 0) == cudaSuccess &&
+          stream_write_u32(m->ws[s].stream, reinterpret_cast<CUdeviceptr>(dp), 0) == REC_OK &&
+          cudaStreamSynchronize(m->ws[s].stream) == cudaSuccess) {
+        lanes[s].flag_host = static_cast<uint32_t*>(hp);
+        lanes[s].flag_dev = reinterpret_cast<CUdeviceptr>(dp);
+      } else {
+        cudaGetLastError();
+        if (hp) cudaFreeHost(hp);
+      }
+    }
   }
   auto cleanup = [&]() {
     for (auto& L : lanes) {
       if (L.done) cudaEventDestroy(L.done);
       if (L.ctr_host) cudaFreeHost(L.ctr_host);
+      if (L.flag_host) cudaFreeHost(L.flag_host);
     }
   };
 
@@ -422,34 +456,119 @@ rec_status rec_serve(rec_model_t m, const rec_trace_row* trace, int64_t n, doubl
       now = nxt;
     }
   } else {
-    // real clock: trace time t maps to wall time t0 + (t - t_first)
+    // Real clock: trace time t maps to wall time t0 + (t - t_first).  This thread releases
+    // arrivals open-loop into the FIFO; one dispatcher thread per co-located stream takes a
+    // fused batch whenever its stream is idle (work-conserving, S2/S3), submits it, and
+    // detects completion by polling a host-mapped sequence word the stream writes after
+    // the batch (no CUDA API call on the polling path).  The FIFO, the batch list and the
+    // per-query counters are shared under one mutex.
+    std::mutex mu;
+    std::atomic<int64_t> avail{0}, head_a{0};  // lock-free "is there work" hint
+    std::atomic<int64_t> done_q{0};
+    std::atomic<bool> failed{false};
+    std::atomic<int> fail_status{REC_OK};
     const double t0 = now_s() - t_first;
-    while (completed < n) {
+    auto worker = [&](int s) {
+      cudaSetDevice(m->device);
+      Workspace& w = m->ws[s];
+      Lane& L = lanes[s];
+      std::vector<int32_t> segs_local;
+      uint32_t seq = 0;
+      int64_t my_batch = -1;
+      double my_disp = 0;
+      while (done_q.load(std::memory_order_relaxed) < n && !failed.load(std::memory_order_relaxed)) {
+        if (L.busy) {
+          const bool done = L.flag_host ? (*reinterpret_cast<volatile uint32_t*>(L.flag_host) == seq)
+                                        : (cudaEventQuery(L.done) == cudaSuccess);
+          if (!done) continue;
+          const double t_c = now_s() - t0;
+          std::lock_guard<std::mutex> g(mu);
+          finish_batch(my_batch, t_c);
+          done_q.store(completed, std::memory_order_relaxed);
+          L.busy = false;
+          continue;
+        }
+        int64_t k = 0, items = 0, c0 = 0;
+        if (avail.load(std::memory_order_acquire) <= head_a.load(std::memory_order_acquire)) continue;
+        {
+          std::lock_guard<std::mutex> g(mu);
+          if (head >= static_cast<int64_t>(fifo.size())) continue;
+          k = fuse_head(fifo, head, d, &items);
+          const double tn = now_s() - t0;
+          if (!should_fire(tn, k, items)) continue;
+          c0 = head;
+          my_batch = static_cast<int64_t>(batches.size());
+          batches.push_back(Batch{s, head, k, items, tn, 0});
+          segs_local.resize(3 * k);
+          for (int64_t c = 0; c < k; ++c) {
+            const Chunk& ch = fifo[head + c];
+            segs_local[3 * c] = ch.qid;
+            segs_local[3 * c + 1] = ch.start;
+            segs_local[3 * c + 2] = ch.len;
+            disp_t[ch.pos] = tn;
+            if (batch_log && logged < log_cap) {
+              int32_t* r = batch_log + 5 * logged++;
+              r[0] = static_cast<int32_t>(my_batch);
+              r[1] = s;
+              r[2] = ch.qid;
+              r[3] = ch.start;
+              r[4] = ch.len;
+            }
+          }
+          head += k;
+          head_a.store(head, std::memory_order_release);
+          my_disp = tn;
+        }
+        (void)my_disp;
+        int B = 0;
+        rec_status rs;
+        if (pol->input_mode == REC_INPUT_DEVICE_SYNTH) {
+          rs = synth_submit(m, w, segs_local.data(), static_cast<int>(k), &B, nullptr);
+        } else {
+          std::vector<Chunk> local(k);
+          {
+            std::lock_guard<std::mutex> g(mu);
+            for (int64_t c = 0; c < k; ++c) local[c] = fifo[c0 + c];
+          }
+          rs = host_input_enqueue(m, w, H, local, 0, k, &B);
+          if (rs == REC_OK) rs = forward_enqueue(m, w, w.indices, w.offsets, B, nullptr, w.ctr, w.logit, nullptr);
+        }
+        if (rs == REC_OK && ctr_out)
+          if (cudaMemcpyAsync(L.ctr_host, w.ctr, sizeof(float) * B, cudaMemcpyDeviceToHost, w.stream) != cudaSuccess)
+            rs = REC_E_CUDA;
+        if (rs == REC_OK) {
+          ++seq;
+          if (L.flag_host) {
+            if (stream_write_u32(w.stream, L.flag_dev, seq) != REC_OK) rs = REC_E_CUDA;
+          } else if (cudaEventRecord(L.done, w.stream) != cudaSuccess) {
+            rs = REC_E_CUDA;
+          }
+        }
+        if (rs != REC_OK) {
+          fail_status.store(rs);
+          failed.store(true);
+          return;
+        }
+        L.busy = true;
+      }
+    };
+    std::vector<std::thread> th;
+    for (int s = 0; s < M; ++s) th.emplace_back(worker, s);
+    while (a < n && !failed.load()) {
       const double now = now_s() - t0;
+      if (trace[a].arrival_s > now) continue;  // open-loop release: spin until the next arrival
+      std::lock_guard<std::mutex> g(mu);
       while (a < n && trace[a].arrival_s <= now) {
         split_query(trace[a], a, d, fifo);
         release[a] = trace[a].arrival_s;
         ++a;
       }
-      for (int s = 0; s < M; ++s) {
-        if (!lanes[s].busy) continue;
-        cudaError_t q = cudaEventQuery(lanes[s].done);
-        if (q == cudaErrorNotReady) continue;
-        if (q != cudaSuccess) { cleanup(); return cuda_fail(q, "cudaEventQuery"); }
-        const double t_c = now_s() - t0;
-        st = rec_sync(m, s);
-        if (st != REC_OK) { cleanup(); return st; }
-        finish_batch(lanes[s].batch, t_c);
-        lanes[s].busy = false;
-      }
-      for (int s = 0; s < M && head < static_cast<int64_t>(fifo.size()); ++s) {
-        if (lanes[s].busy) continue;
-        int64_t items = 0;
-        const int64_t k = fuse_head(fifo, head, d, &items);
-        if (!should_fire(now_s() - t0, k, items)) break;
-        st = dispatch(s, now_s() - t0, k, items);
-        if (st != REC_OK) { cleanup(); return st; }
-      }
+      avail.store(static_cast<int64_t>(fifo.size()), std::memory_order_release);
+    }
+    for (auto& t : th) t.join();
+    if (failed.load()) {
+      cleanup();
+      return static_cast<rec_status>(fail_status.load());
     }
   }
   for (int s = 0; s < M; ++s) {
