@@ -17,6 +17,10 @@
 #include "kernels.h"
 #include "synth.cuh"
 
+#ifndef REC_SLS_MINB
+#define REC_SLS_MINB 5  // CTAs of 128 per SM the register budget must allow (5: ~85 regs)
+#endif
+
 namespace rec {
 
 // Streaming 128-bit load of row `row` (address = base + row * stride_bytes, formed inside the
@@ -43,7 +47,7 @@ struct SlsShape {
 };
 
 template <int LANES, int THREADS>
-__global__ void __launch_bounds__(THREADS, 5) k_sls(const float* __restrict__ tables,
+__global__ void __launch_bounds__(THREADS, REC_SLS_MINB) k_sls(const float* __restrict__ tables,
                                                     const int64_t* __restrict__ tab_off,
                                                     int64_t row_stride,
                                                     const int64_t* __restrict__ rows,
@@ -141,7 +145,7 @@ __global__ void __launch_bounds__(THREADS, 5) k_sls(const float* __restrict__ ta
 // (G2) instead of loading it, so the kernel has no predecessor in the chain and
 // no dependent index load in front of its first row loads.
 template <int LANES, int THREADS, int RIF>
-__global__ void __launch_bounds__(THREADS, RIF > 8 ? 4 : 5) k_sls_synth(const __grid_constant__ SegBatch sb,
+__global__ void __launch_bounds__(THREADS, REC_SLS_MINB) k_sls_synth(const __grid_constant__ SegBatch sb,
                                                                         const SlsSynthArgs a) {
   using S = SlsShape<LANES, RIF>;
   constexpr int GROUPS = THREADS / LANES;
