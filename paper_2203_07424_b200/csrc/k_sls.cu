@@ -11,8 +11,6 @@
 // the bag's indices LANES at a time (one per lane), broadcasts them with shuffles, and keeps
 // LANES independent 128-bit row loads in flight per lane (ld.global.nc.L1::no_allocate —
 // rows are streamed, never reused from L1) before accumulating them in order.
-#include <cstdlib>
-
 #include "common.cuh"
 #include "kernels.h"
 #include "synth.cuh"
@@ -208,94 +206,13 @@ __global__ void __launch_bounds__(THREADS, REC_SLS_MINB) k_sls_synth(const __gri
                                static_cast<int64_t>(1 + t) * a.D + col) = acc;
 }
 
-// Synthetic-index SLS with the in-flight rows held in SHARED memory (cp.async.cg, L1-bypass):
-// same one-bag-per-8-lane-group structure and index-order accumulation as k_sls_synth, but a
-// lane keeps P rounds x 8 rows of 16 B in a lane-interleaved smem ring (conflict-free) instead
-// of registers, so occupancy and bytes in flight are bounded by shared memory, not registers.
-__device__ __forceinline__ void cpa16(uint32_t saddr, const void* g) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(saddr), "l"(g) : "memory");
-}
-__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cpa_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-
-template <int P>
-__global__ void __launch_bounds__(128) k_sls_synth_cpa(const __grid_constant__ SegBatch sb,
-                                                       const SlsSynthArgs a) {
-  constexpr int LANES = 8, GROUPS = 128 / LANES;
-  __shared__ float4 ring[P * LANES * 128];  // [round slot][row][thread]
-  const int B = sb.B;
-  if (blockIdx.x == 0 && threadIdx.x == 0) *a.dB = B;
-  const int nbags = a.T * B;
-  const int g = blockIdx.x * GROUPS + threadIdx.x / LANES;
-  if (g >= nbags) return;
-  const int sub = threadIdx.x % LANES;
-  const int t = g / B, b = g - t * B;
-  const int2 qi = row_item(sb, b);
-  const uint64_t R = static_cast<uint64_t>(__ldg(&a.rows[t]));
-  const uint32_t c2 = (static_cast<uint32_t>(t) << 8) | DOM_INDEX;
-  const bool active = (sub * 4) < a.D;
-  const int col = active ? sub * 4 : 0;
-  const float* tab = a.tables + __ldg(&a.tab_off[t]) + col;
-  const unsigned gmask = ((1u << LANES) - 1u) << ((threadIdx.x & 31) & ~(LANES - 1));
-  const int L = a.L;
-  const int nr = (L + LANES - 1) / LANES;
-  float4* mine = ring + threadIdx.x;
-  const uint32_t sbase = static_cast<uint32_t>(__cvta_generic_to_shared(mine));
-  auto idx_of = [&](int r) {
-    const int j = r * LANES + sub;
-    return (r < nr && j < L) ? gen_index(j, qi.y, c2, qi.x, a.k0, a.k1, R, a.index_dist) : 0;
-  };
-  auto issue = [&](int r, int cur) {
-#pragma unroll
-    for (int k = 0; k < LANES; ++k) {
-      const int rr = __shfl_sync(gmask, cur, k, LANES);
-      if (r < nr && r * LANES + k < L && active)
-        cpa16(sbase + static_cast<uint32_t>(((r % P) * LANES + k) * 128 * 16),
-              tab + static_cast<int64_t>(rr) * a.row_stride);
-    }
-    cpa_commit();
-  };
-#pragma unroll
-  for (int r = 0; r < P; ++r) issue(r, idx_of(r));
-  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-  for (int r = 0; r < nr; ++r) {
-    const int nxt = idx_of(r + P);  // Philox of a future round while this one lands
-    cpa_wait<P - 1>();
-    const float4* s = mine + (r % P) * LANES * 128;
-    const int n = min(LANES, L - r * LANES);
-#pragma unroll
-    for (int k = 0; k < LANES; ++k) {
-      if (k < n) {
-        const float4 v = s[k * 128];
-        acc.x += v.x;
-        acc.y += v.y;
-        acc.z += v.z;
-        acc.w += v.w;
-      }
-    }
-    issue(r + P, nxt);  // same slot as round r: reads above are complete (same thread)
-  }
-  cpa_wait<0>();
-  if (active)
-    *reinterpret_cast<float4*>(a.X + static_cast<int64_t>(b) * a.x_stride +
-                               static_cast<int64_t>(1 + t) * a.D + col) = acc;
-}
-
 void* sls_synth_kernel(const SlsSynthArgs& a, dim3* grid, dim3* block) {
   constexpr int THREADS = 128;
-  static const int cpa = [] {  // REC_SLS_CPA=1: shared-memory (cp.async) in-flight variant
-    const char* e = getenv("REC_SLS_CPA");
-    return (e && e[0] == '1') ? 1 : 0;
-  }();
   const int L = a.D / 4 <= 8 ? 8 : a.D / 4 <= 16 ? 16 : 32;
   const int nb = a.T * a.cap;
   *grid = dim3((nb + THREADS / L - 1) / (THREADS / L));
   *block = dim3(THREADS);
-  if (L == 8) return cpa ? reinterpret_cast<void*>(k_sls_synth_cpa<2>)
-                         : reinterpret_cast<void*>(k_sls_synth<8, THREADS, 8>);
+  if (L == 8) return reinterpret_cast<void*>(k_sls_synth<8, THREADS, 8>);
   if (L == 16) return reinterpret_cast<void*>(k_sls_synth<16, THREADS, 8>);
   return reinterpret_cast<void*>(k_sls_synth<32, THREADS, 8>);
 }
