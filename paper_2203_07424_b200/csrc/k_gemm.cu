@@ -29,13 +29,15 @@ constexpr int BM = 128;
 constexpr int BK = 64;
 constexpr int A_STAGE_BYTES = BM * BK * 2;  // 16 KB
 
-template <int BN>
+// MT = 128-row M tiles per CTA sharing every weight stage (MT = 2 halves the weight bytes
+// each MMA needs from L2, which is what bounds large-batch GEMMs such as RMC3's 2560x512).
+template <int BN, int MT>
 __global__ void __launch_bounds__(128, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_w,
               const GemmArgs args, int stages) {
   constexpr int B_STAGE_BYTES = BN * BK * 2;
-  constexpr int STAGE_BYTES = A_STAGE_BYTES + B_STAGE_BYTES;
-  constexpr uint32_t TMEM_COLS = BN < 32 ? 32 : BN;
+  constexpr int STAGE_BYTES = MT * A_STAGE_BYTES + B_STAGE_BYTES;
+  constexpr uint32_t TMEM_COLS = (BN < 32 ? 32 : BN) * MT;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
@@ -46,7 +48,7 @@ __global__ void __launch_bounds__(128, 1)
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 2 * stages + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
+  const int m0 = blockIdx.x * BM * MT, n0 = blockIdx.y * BN;
   const int nkb = (args.K + BK - 1) / BK;
   const int M = args.dM ? *args.dM : args.M;  // device-side batch (graph replay)
   if (m0 >= M) return;                        // whole CTA beyond the batch: nothing to do
@@ -79,8 +81,10 @@ __global__ void __launch_bounds__(128, 1)
       if (lane == 0) {
         uint8_t* sa = smem + s * STAGE_BYTES;
         sm100::mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
-        sm100::tma_load_2d(sa, &tmap_a, &full[s], kb * BK, m0);
-        sm100::tma_load_2d(sa + A_STAGE_BYTES, &tmap_w, &full[s], kb * BK, n0);
+#pragma unroll
+        for (int h = 0; h < MT; ++h)
+          sm100::tma_load_2d(sa + h * A_STAGE_BYTES, &tmap_a, &full[s], kb * BK, m0 + h * BM);
+        sm100::tma_load_2d(sa + MT * A_STAGE_BYTES, &tmap_w, &full[s], kb * BK, n0);
       }
       __syncwarp();
     }
@@ -93,12 +97,15 @@ __global__ void __launch_bounds__(128, 1)
       sm100::tc_fence_after();
       if (lane == 0) {
         const uint32_t sa = sm100::smem_u32(smem + s * STAGE_BYTES);
-        const uint64_t da = sm100::umma_desc_sw128(sa);
-        const uint64_t db = sm100::umma_desc_sw128(sa + A_STAGE_BYTES);
+        const uint64_t db = sm100::umma_desc_sw128(sa + MT * A_STAGE_BYTES);
 #pragma unroll
-        for (int k = 0; k < BK / 16; ++k) {
-          // advance 16 bf16 = 32 B along K inside the 128-B swizzled row: +2 in addr>>4
-          sm100::mma_bf16_ss(tmem, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
+        for (int h = 0; h < MT; ++h) {
+          const uint64_t da = sm100::umma_desc_sw128(sa + h * A_STAGE_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            // advance 16 bf16 = 32 B along K inside the 128-B swizzled row: +2 in addr>>4
+            sm100::mma_bf16_ss(tmem + h * BN, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
+          }
         }
         sm100::mma_commit(&empty[s]);
         if (kb == nkb - 1) sm100::mma_commit(done);
@@ -118,9 +125,11 @@ __global__ void __launch_bounds__(128, 1)
   sm100::mbar_wait(done, 0);
   __syncthreads();  // s_bias / s_wl visible to every epilogue thread
   sm100::tc_fence_after();
-  const int row = m0 + warp * 32 + lane;
+#pragma unroll 1
+  for (int h = 0; h < MT; ++h) {
+  const int row = m0 + h * BM + warp * 32 + lane;
   const bool row_ok = row < M;
-  const uint32_t trow = tmem + (static_cast<uint32_t>(warp * 32) << 16);
+  const uint32_t trow = tmem + (static_cast<uint32_t>(warp * 32) << 16) + h * BN;
   float dot = 0.f;
 #pragma unroll 1
   for (int c0 = 0; c0 < BN; c0 += 16) {
@@ -175,45 +184,51 @@ __global__ void __launch_bounds__(128, 1)
     args.ctr[row] = 1.f / (1.f + __expf(-logit));
     if (args.logit) args.logit[row] = logit;
   }
+  }
   sm100::tc_fence_before();
   __syncthreads();
   if (warp == 0) sm100::tmem_dealloc(tmem, TMEM_COLS);
 }
 
-template <int BN>
+template <int BN, int MT>
 static void launch_bn(const CUtensorMap* ta, const CUtensorMap* tw, const GemmArgs& a,
                       cudaStream_t s) {
-  constexpr int STAGE = A_STAGE_BYTES + BN * BK * 2;
+  constexpr int STAGE = MT * A_STAGE_BYTES + BN * BK * 2;
+  constexpr int SMAX = (MT == 1 ? 4 : 3);
   const int nkb = (a.K + BK - 1) / BK;
-  const int stages = nkb < 4 ? (nkb < 1 ? 1 : nkb) : 4;
+  const int stages = nkb < SMAX ? (nkb < 1 ? 1 : nkb) : SMAX;
   const size_t smem = static_cast<size_t>(stages) * STAGE + 1024 + 256;
-  dim3 grid((a.M + BM - 1) / BM, (a.N + BN - 1) / BN);
-  k_gemm_tc<BN><<<grid, 128, smem, s>>>(*ta, *tw, a, stages);
+  dim3 grid((a.M + BM * MT - 1) / (BM * MT), (a.N + BN - 1) / BN);
+  k_gemm_tc<BN, MT><<<grid, 128, smem, s>>>(*ta, *tw, a, stages);
 }
 
 int gemm_bn(int N) { return N <= 32 ? 32 : N <= 64 ? 64 : N <= 128 ? 128 : 256; }
 
-template <int BN>
+template <int BN, int MT>
 static void prep_bn() {
-  constexpr int STAGE = A_STAGE_BYTES + BN * BK * 2;
-  cudaFuncSetAttribute(k_gemm_tc<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       4 * STAGE + 1024 + 256);
+  constexpr int STAGE = MT * A_STAGE_BYTES + BN * BK * 2;
+  constexpr int SMAX = (MT == 1 ? 4 : 3);
+  cudaFuncSetAttribute(k_gemm_tc<BN, MT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       SMAX * STAGE + 1024 + 256);
 }
 
 void gemm_prepare() {
-  prep_bn<32>();
-  prep_bn<64>();
-  prep_bn<128>();
-  prep_bn<256>();
+  prep_bn<32, 1>();
+  prep_bn<64, 1>();
+  prep_bn<128, 1>();
+  prep_bn<256, 1>();
+  prep_bn<256, 2>();
 }
 
 void launch_gemm_tc(const CUtensorMap* tmap_a, const CUtensorMap* tmap_w, const GemmArgs& a,
                     cudaStream_t s) {
   if (a.M <= 0) return;
-  if (a.N <= 32) launch_bn<32>(tmap_a, tmap_w, a, s);
-  else if (a.N <= 64) launch_bn<64>(tmap_a, tmap_w, a, s);
-  else if (a.N <= 128) launch_bn<128>(tmap_a, tmap_w, a, s);
-  else launch_bn<256>(tmap_a, tmap_w, a, s);
+  if (a.N <= 32) launch_bn<32, 1>(tmap_a, tmap_w, a, s);
+  else if (a.N <= 64) launch_bn<64, 1>(tmap_a, tmap_w, a, s);
+  else if (a.N <= 128) launch_bn<128, 1>(tmap_a, tmap_w, a, s);
+  else if (((a.M + 255) / 256) * ((a.N + 255) / 256) >= 148 && a.K >= 512)
+    launch_bn<256, 2>(tmap_a, tmap_w, a, s);  // enough 256-row tiles to fill the GPU: share W
+  else launch_bn<256, 1>(tmap_a, tmap_w, a, s);
 }
 
 // ---------------------------------------------------------------- tensor maps

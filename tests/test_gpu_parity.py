@@ -214,3 +214,29 @@ def test_full_size_sampled(name):
     i2, o2, d2 = gen.gen_batch(cfg, 1, sub)
     exp = fw.forward(cfg, 1, d2, i2, o2)
     assert np.abs(ctr[pick] - exp).max() <= CTR_TOL
+
+
+def test_large_batch_weight_sharing_gemm_invariance():
+    """B = 20480 on RMC3 shapes routes the 2560x512 bottom layer through the 2-M-tile
+    (weight-sharing) tcgen05 GEMM; every item's CTR must equal the small-batch result bit for
+    bit (batch invariance) and the oracle within 2e-2 on sampled items."""
+    import torch
+    cfg = W.small_variant(W.RMC3, 20000)
+    B = 20480
+    m = _model(cfg, max_batch=B)
+    segs = W.random_segments(B, seed=41, max_seg=1000)
+    cv = torch.zeros(B, device="cuda")
+    m.rec_synth_query_async(0, segs, cv)
+    m.rec_sync(0)
+    big = cv.cpu().numpy()
+    q, it = gen.expand_segments(segs)
+    pick = np.random.default_rng(3).choice(B, size=40, replace=False)
+    sub = np.array([[q[k], it[k], 1] for k in pick], np.int32)
+    small = _model(cfg, max_batch=64)
+    cs = torch.zeros(40, device="cuda")
+    small.rec_synth_query_async(0, sub, cs)
+    small.rec_sync(0)
+    assert np.array_equal(cs.cpu().numpy(), big[pick])
+    i2, o2, d2 = gen.gen_batch(cfg, 1, sub)
+    exp = fw.forward(cfg, 1, d2, i2, o2)
+    assert np.abs(big[pick] - exp).max() <= CTR_TOL
