@@ -32,7 +32,7 @@ EXPORTS = ["rec_model_create", "rec_model_destroy", "rec_query", "rec_query_debu
            "rec_query_async", "rec_synth_query_async", "rec_sync", "rec_stream_handle",
            "rec_gen_batch", "rec_profile", "rec_profile_read", "rec_serve", "rec_last_error",
            "rec_nccl_unique_id_size", "rec_nccl_get_unique_id", "rec_version", "rec_split_fuse",
-           "rec_synth_query_batches", "rec_shard_plan", "rec_bench_mlp",
+           "rec_synth_query_batches", "rec_shard_plan", "rec_bench_mlp", "rec_bench_sls",
            "rec_debug_chain_timeline"]
 
 
@@ -105,6 +105,8 @@ def lib() -> C.CDLL:
         L.rec_shard_plan.restype = i32
         L.rec_bench_mlp.argtypes = [vp, i32, i32, i32, C.POINTER(C.c_double)]
         L.rec_bench_mlp.restype = i32
+        L.rec_bench_sls.argtypes = [vp, vp, i32, i32, C.POINTER(C.c_double)]
+        L.rec_bench_sls.restype = i32
         L.rec_debug_chain_timeline.argtypes = [vp, i32, i32, vp]
         L.rec_debug_chain_timeline.restype = i32
         for f in ("rec_model_create", "rec_query", "rec_query_debug", "rec_query_async",
@@ -230,6 +232,12 @@ class RecModel:
     def rec_bench_mlp(self, which: int, batch: int, iters: int = 50) -> float:
         ms = C.c_double()
         _check(lib().rec_bench_mlp(self.h, which, batch, iters, C.byref(ms)))
+        return ms.value
+
+    def rec_bench_sls(self, segs: np.ndarray, iters: int = 50) -> float:
+        segs = np.ascontiguousarray(segs, dtype=np.int32).reshape(-1, 3)
+        ms = C.c_double()
+        _check(lib().rec_bench_sls(self.h, _ptr(segs), segs.shape[0], iters, C.byref(ms)))
         return ms.value
 
     def rec_debug_chain_timeline(self, which: int, batch: int):

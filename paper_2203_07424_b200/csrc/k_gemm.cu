@@ -260,4 +260,19 @@ bool encode_tmap_bf16(CUtensorMap* map, const void* base, uint64_t rows, uint64_
   return r == CUDA_SUCCESS;
 }
 
+// Row-gather map over an fp32 row arena: dims {width, rows}, box {width, 1} (TMA gather4
+// fetches 4 arbitrary rows of `width` floats per instruction).
+bool encode_tmap_rows_f32(CUtensorMap* map, const void* base, uint64_t rows, uint32_t width) {
+  auto fn = get_encode();
+  if (!fn || width > 256 || (width * 4) % 16 != 0) return false;
+  cuuint64_t dims[2] = {width, rows};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(width) * 4};
+  cuuint32_t box[2] = {width, 1};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 }  // namespace rec

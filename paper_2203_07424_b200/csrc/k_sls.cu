@@ -13,10 +13,29 @@
 // rows are streamed, never reused from L1) before accumulating them in order.
 #include "common.cuh"
 #include "kernels.h"
+#include "sm100.cuh"
 #include "synth.cuh"
 
 #ifndef REC_SLS_MINB
 #define REC_SLS_MINB 5  // CTAs of 128 per SM the register budget must allow (5: ~85 regs)
+#endif
+#ifndef REC_SLS_RIF
+#define REC_SLS_RIF 8  // independent 128-bit row loads in flight per lane
+#endif
+
+#ifdef REC_SLS_TIMELINE  // diagnostic build (scripts/sls_timeline.cu): per-warp %globaltimer
+__device__ unsigned long long g_sls_tl[4 * 65536];
+#define SLS_STAMP(k)                                                            \
+  do {                                                                          \
+    if ((threadIdx.x & 31) == 0) {                                              \
+      unsigned long long t_;                                                    \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                     \
+      const unsigned w_ = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;         \
+      if (w_ < 65536) g_sls_tl[4 * w_ + (k)] = t_;                              \
+    }                                                                           \
+  } while (0)
+#else
+#define SLS_STAMP(k)
 #endif
 
 namespace rec {
@@ -37,7 +56,7 @@ __device__ __forceinline__ float4 ldg_row(const float4* base, uint32_t row, uint
 // Per round a group consumes ROWS = IPL * LANES indices (IPL per lane, prefetched one round
 // ahead so the index load never sits in front of the row loads) and issues the row loads in
 // sub-batches of U = 8 independent 128-bit loads per lane before accumulating them in order.
-template <int LANES, int RIF = 8>
+template <int LANES, int RIF = REC_SLS_RIF>
 struct SlsShape {
   static constexpr int IPL = RIF > LANES ? RIF / LANES : 1;
   static constexpr int ROWS = IPL * LANES;
@@ -147,19 +166,32 @@ __global__ void __launch_bounds__(THREADS, REC_SLS_MINB) k_sls_synth(const __gri
                                                                         const SlsSynthArgs a) {
   using S = SlsShape<LANES, RIF>;
   constexpr int GROUPS = THREADS / LANES;
+  SLS_STAMP(0);
+  // Programmatic dependent launch: the next kernel of the stream may be scheduled as soon
+  // as our CTAs retire; our own reads need nothing from the predecessor (indices are
+  // synthesised, tables are constant), only the writes wait for it (below).
+  cudaTriggerProgrammaticLaunchCompletion();
   const int B = sb.B;
-  if (blockIdx.x == 0 && threadIdx.x == 0) *a.dB = B;
   const int nbags = a.T * B;
   const int g = blockIdx.x * GROUPS + threadIdx.x / LANES;
-  if (g >= nbags) return;
+  if (g >= nbags) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      cudaGridDependencySynchronize();
+      *a.dB = B;
+    }
+    return;
+  }
   const int sub = threadIdx.x % LANES;
   const int t = g / B, b = g - t * B;
   const int2 qi = row_item(sb, b);
-  const uint64_t R = static_cast<uint64_t>(__ldg(&a.rows[t]));
+  // equal-row interleaved arena: table geometry from the parameters (no dependent loads
+  // in front of the first index)
+  const uint64_t R = a.R_all ? static_cast<uint64_t>(a.R_all) : static_cast<uint64_t>(__ldg(&a.rows[t]));
+  const int64_t toff = a.R_all ? static_cast<int64_t>(t) * a.D : __ldg(&a.tab_off[t]);
   const uint32_t c2 = (static_cast<uint32_t>(t) << 8) | DOM_INDEX;
   const bool active = (sub * 4) < a.D;
   const int col = active ? sub * 4 : 0;
-  const float4* __restrict__ tab = reinterpret_cast<const float4*>(a.tables + __ldg(&a.tab_off[t]) + col);
+  const float4* __restrict__ tab = reinterpret_cast<const float4*>(a.tables + toff + col);
   const uint32_t stride_bytes = static_cast<uint32_t>(a.row_stride * 4);
   const unsigned gmask = (LANES == 32) ? 0xffffffffu
                                        : (((1u << LANES) - 1u) << ((threadIdx.x & 31) & ~(LANES - 1)));
@@ -171,6 +203,7 @@ __global__ void __launch_bounds__(THREADS, REC_SLS_MINB) k_sls_synth(const __gri
     const int j = q * LANES + sub;
     cur[q] = j < L ? gen_index(j, qi.y, c2, qi.x, a.k0, a.k1, R, a.index_dist) : 0;
   }
+  SLS_STAMP(1);
   for (int base = 0; base < L; base += S::ROWS) {
     const int n = min(S::ROWS, L - base);
 #pragma unroll
@@ -199,29 +232,189 @@ __global__ void __launch_bounds__(THREADS, REC_SLS_MINB) k_sls_synth(const __gri
           acc.w += v[k].w;
         }
       }
+      if (base == 0 && kk == 0) SLS_STAMP(2);
     }
   }
+  cudaGridDependencySynchronize();  // predecessor grid done: X / dB may be overwritten
+  if (blockIdx.x == 0 && threadIdx.x == 0) *a.dB = B;
   if (active)
     *reinterpret_cast<float4*>(a.X + static_cast<int64_t>(b) * a.x_stride +
                                static_cast<int64_t>(1 + t) * a.D + col) = acc;
+  SLS_STAMP(3);
 }
 
-void* sls_synth_kernel(const SlsSynthArgs& a, dim3* grid, dim3* block) {
+// TMA row-gather variant (DESIGN.md §6 "SLS via TMA gather4").  Rows travel HBM -> shared
+// memory on the tensor-memory accelerator, so the bytes in flight per SM are bounded by the
+// shared-memory ring (up to ~200 KB) instead of the register file (~70 KB for the register
+// kernel at its occupancy): the small-batch launches of the serving path are latency bound
+// on in-flight bytes, not on bandwidth.
+//   * persistent grid: SLS_TMA_CTAS_PER_SM x #SM CTAs of 8 warps; warp w owns the contiguous
+//     bag range [w * nbags / W, (w + 1) * nbags / W) (bag g = t * B + b, as in k_sls)
+//   * a bag is read in chunks of CR = 8 rows: lanes 0..7 compute the chunk's Philox indices,
+//     lanes 0..1 each issue one gather4 (4 rows) into the warp's ring slot; one mbarrier per
+//     slot (expect_tx = rows x D x 4 bytes)
+//   * consume: lane = (row phase ro, column group cg); rows ro, ro + 32/LANES, ... of the chunk
+//     accumulate into a float4 in index order; at the end of the bag the row phases are
+//     combined by a fixed xor-shuffle tree.  The summation order therefore differs from the
+//     sequential register kernel; with the int8 x 2^e tables (value_mode 0, R9) all
+//     partial sums are exact, so the result is bit-identical.  Models in fp32 value mode keep
+//     the register kernel (model.cu).
+constexpr int SLS_TMA_WARPS = 8;
+constexpr int SLS_TMA_CR = 8;
+constexpr int SLS_TMA_CTAS_PER_SM = 2;
+constexpr int SLS_TMA_RING_BYTES = 12 * 1024;  // per warp
+
+template <int LANES>
+__global__ void __launch_bounds__(SLS_TMA_WARPS * 32, 1)
+    k_sls_synth_tma(const __grid_constant__ SegBatch sb, const SlsSynthArgs a) {
+  constexpr int D = LANES * 4;
+  constexpr int RP = 32 / LANES;  // row phases per chunk read
+  constexpr int ROWB = D * 4;
+  constexpr int CHUNKB = SLS_TMA_CR * ROWB;
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int NST = a.nst;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint8_t* ring = smem + static_cast<size_t>(warp) * NST * CHUNKB;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + static_cast<size_t>(SLS_TMA_WARPS) * NST * CHUNKB) +
+                  warp * NST;
+  const int B = sb.B;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *a.dB = B;
+  if (lane == 0) {
+    for (int i = 0; i < NST; ++i) sm100::mbar_init(&bar[i], 1);
+    sm100::fence_mbar_init();
+  }
+  __syncwarp();
+  const int nbags = a.T * B;
+  const int NW = gridDim.x * SLS_TMA_WARPS;
+  const int gw = blockIdx.x * SLS_TMA_WARPS + warp;
+  const int b_begin = static_cast<int>(static_cast<int64_t>(gw) * nbags / NW);
+  const int b_end = static_cast<int>(static_cast<int64_t>(gw + 1) * nbags / NW);
+  const int L = a.L;
+  const int nch = (L + SLS_TMA_CR - 1) / SLS_TMA_CR;
+  const int total = (b_end - b_begin) * nch;
+  const int rs = static_cast<int>(a.row_stride / D);
+  const CUtensorMap* map = a.tmap_rows;
+  if (total > 0 && lane == 0) sm100::tma_prefetch_desc(map);
+
+  // issue chunk s of this warp into slot s % NST (all lanes participate)
+  auto issue = [&](int s) {
+    const int g = b_begin + s / nch;
+    const int c = s - (s / nch) * nch;
+    const int t = g / B, b = g - t * B;
+    const int n = min(SLS_TMA_CR, L - c * SLS_TMA_CR);
+    int coord = 0;
+    if (lane < n) {
+      const int2 qi = row_item(sb, b);
+      const uint64_t R = static_cast<uint64_t>(__ldg(&a.rows[t]));
+      const uint32_t c2 = (static_cast<uint32_t>(t) << 8) | DOM_INDEX;
+      const int idx = gen_index(c * SLS_TMA_CR + lane, qi.y, c2, qi.x, a.k0, a.k1, R, a.index_dist);
+      coord = static_cast<int>(__ldg(&a.tab_off[t]) / D) + idx * rs;
+    }
+    const int nops = (n + 3) >> 2;
+    const int st = s % NST;
+    if (lane == 0) sm100::mbar_arrive_expect_tx(&bar[st], nops * 4 * ROWB);
+    // lane op (< nops) issues rows 4op..4op+3; padding rows (>= n) repeat row 4op
+    const int base = (lane & 1) * 4;
+    int r[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int src = base + k < n ? base + k : base;
+      r[k] = __shfl_sync(0xffffffffu, coord, src & 31);
+    }
+    if (lane < nops)
+      sm100::tma_gather4(ring + st * CHUNKB + lane * 4 * ROWB, map, &bar[st], 0, r[0], r[1], r[2], r[3]);
+  };
+
+  const int pre = min(NST, total);
+  for (int s = 0; s < pre; ++s) issue(s);
+  const int cg = lane % LANES, ro = lane / LANES;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int s = 0; s < total; ++s) {
+    const int st = s % NST;
+    sm100::mbar_wait(&bar[st], static_cast<uint32_t>((s / NST) & 1));
+    const int c = s % nch;
+    const int n = min(SLS_TMA_CR, L - c * SLS_TMA_CR);
+    const uint8_t* chunk = ring + st * CHUNKB + cg * 16;
+#pragma unroll
+    for (int r = ro; r < SLS_TMA_CR; r += RP) {
+      if (r < n) {
+        const float4 v = *reinterpret_cast<const float4*>(chunk + r * ROWB);
+        acc.x += v.x;
+        acc.y += v.y;
+        acc.z += v.z;
+        acc.w += v.w;
+      }
+    }
+    if (c == nch - 1) {  // bag complete: combine the row phases, store, reset
+#pragma unroll
+      for (int o = LANES; o < 32; o <<= 1) {
+        acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+        acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+        acc.z += __shfl_xor_sync(0xffffffffu, acc.z, o);
+        acc.w += __shfl_xor_sync(0xffffffffu, acc.w, o);
+      }
+      const int g = b_begin + s / nch;
+      const int t = g / B, b = g - t * B;
+      if (ro == 0)
+        *reinterpret_cast<float4*>(a.X + static_cast<int64_t>(b) * a.x_stride +
+                                   static_cast<int64_t>(1 + t) * D + cg * 4) = acc;
+      acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    sm100::fence_proxy_async_smem();
+    __syncwarp();
+    if (s + NST < total) issue(s + NST);
+  }
+}
+
+bool sls_tma_supported(int D) { return D == 32 || D == 64 || D == 128; }
+
+void sls_tma_configure(SlsSynthArgs& a) {
+  const int chunk = SLS_TMA_CR * a.D * 4;
+  a.nst = SLS_TMA_RING_BYTES / chunk < 2 ? 2 : SLS_TMA_RING_BYTES / chunk;
+  const size_t smem = static_cast<size_t>(SLS_TMA_WARPS) * a.nst * (chunk + 8);
+  void* fn = a.D == 32 ? reinterpret_cast<void*>(k_sls_synth_tma<8>)
+             : a.D == 64 ? reinterpret_cast<void*>(k_sls_synth_tma<16>)
+                         : reinterpret_cast<void*>(k_sls_synth_tma<32>);
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+}
+
+void* sls_synth_kernel(const SlsSynthArgs& a, dim3* grid, dim3* block, size_t* smem) {
+  if (a.tma) {
+    const int chunk = SLS_TMA_CR * a.D * 4;
+    *grid = dim3(a.nsm * SLS_TMA_CTAS_PER_SM);
+    *block = dim3(SLS_TMA_WARPS * 32);
+    if (smem) *smem = static_cast<size_t>(SLS_TMA_WARPS) * a.nst * (chunk + 8);
+    if (a.D == 32) return reinterpret_cast<void*>(k_sls_synth_tma<8>);
+    if (a.D == 64) return reinterpret_cast<void*>(k_sls_synth_tma<16>);
+    return reinterpret_cast<void*>(k_sls_synth_tma<32>);
+  }
   constexpr int THREADS = 128;
   const int L = a.D / 4 <= 8 ? 8 : a.D / 4 <= 16 ? 16 : 32;
   const int nb = a.T * a.cap;
   *grid = dim3((nb + THREADS / L - 1) / (THREADS / L));
   *block = dim3(THREADS);
-  if (L == 8) return reinterpret_cast<void*>(k_sls_synth<8, THREADS, 8>);
-  if (L == 16) return reinterpret_cast<void*>(k_sls_synth<16, THREADS, 8>);
-  return reinterpret_cast<void*>(k_sls_synth<32, THREADS, 8>);
+  if (smem) *smem = 0;
+  if (L == 8) return reinterpret_cast<void*>(k_sls_synth<8, THREADS, REC_SLS_RIF>);
+  if (L == 16) return reinterpret_cast<void*>(k_sls_synth<16, THREADS, REC_SLS_RIF>);
+  return reinterpret_cast<void*>(k_sls_synth<32, THREADS, REC_SLS_RIF>);
 }
 
 void launch_sls_synth(const SegBatch& sb, const SlsSynthArgs& a, cudaStream_t s) {
   dim3 grid, block;
-  void* fn = sls_synth_kernel(a, &grid, &block);
+  size_t smem = 0;
+  void* fn = sls_synth_kernel(a, &grid, &block, &smem);
   void* args[2] = {const_cast<SegBatch*>(&sb), const_cast<SlsSynthArgs*>(&a)};
-  cudaLaunchKernel(fn, grid, block, args, 0, s);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = a.pdl;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelExC(&cfg, fn, args);
 }
 
 template <int L>
@@ -241,9 +434,9 @@ void set_max_smem_carveout() {
   cudaFuncSetAttribute(k_sls<8, 128>, cudaFuncAttributePreferredSharedMemoryCarveout, c);
   cudaFuncSetAttribute(k_sls<16, 128>, cudaFuncAttributePreferredSharedMemoryCarveout, c);
   cudaFuncSetAttribute(k_sls<32, 128>, cudaFuncAttributePreferredSharedMemoryCarveout, c);
-  cudaFuncSetAttribute(k_sls_synth<8, 128, 8>, cudaFuncAttributePreferredSharedMemoryCarveout, c);
-  cudaFuncSetAttribute(k_sls_synth<16, 128, 8>, cudaFuncAttributePreferredSharedMemoryCarveout, c);
-  cudaFuncSetAttribute(k_sls_synth<32, 128, 8>, cudaFuncAttributePreferredSharedMemoryCarveout, c);
+  cudaFuncSetAttribute(k_sls_synth<8, 128, REC_SLS_RIF>, cudaFuncAttributePreferredSharedMemoryCarveout, c);
+  cudaFuncSetAttribute(k_sls_synth<16, 128, REC_SLS_RIF>, cudaFuncAttributePreferredSharedMemoryCarveout, c);
+  cudaFuncSetAttribute(k_sls_synth<32, 128, REC_SLS_RIF>, cudaFuncAttributePreferredSharedMemoryCarveout, c);
 }
 
 void launch_sls(const float* tables, const int64_t* tab_off, int64_t row_stride,

@@ -77,8 +77,19 @@ struct SlsSynthArgs {
   float* X;
   int x_stride;
   int* dB;
+  // TMA row-gather variant (REC_SLS=tma): map over the arena as [rows_total][D] fp32 rows
+  // (device copy, 64-B aligned), arena row of (t, r) = tab_off[t] / D + r * row_stride / D.
+  const CUtensorMap* tmap_rows;
+  int64_t R_all;  // != 0: every table has R_all rows in the interleaved arena (tab_off[t] = t*D)
+  int pdl;        // launch with programmatic stream serialization (kernel waits before writes)
+  int tma;     // 1: k_sls_synth_tma
+  int nsm;     // SMs (persistent grid)
+  int nst;     // ring chunks per warp
 };
-void* sls_synth_kernel(const SlsSynthArgs& a, dim3* grid, dim3* block);
+// Returns the kernel for this configuration; grid / block / dynamic smem are written back.
+void* sls_synth_kernel(const SlsSynthArgs& a, dim3* grid, dim3* block, size_t* smem = nullptr);
+bool sls_tma_supported(int D);
+void sls_tma_configure(SlsSynthArgs& a);
 void launch_sls_synth(const SegBatch& sb, const SlsSynthArgs& a, cudaStream_t s);
 
 // ----------------------------------------------------------- tcgen05 GEMM (a4, a6)
@@ -103,6 +114,7 @@ void launch_gemm_tc(const CUtensorMap* tmap_a, const CUtensorMap* tmap_w, const 
                     cudaStream_t s);
 // Encode a 2D bf16 K-major tensor map [rows][K] (row pitch ldk elements) with a
 // 64 x box_rows box and 128-byte swizzle.  Returns false on failure.
+bool encode_tmap_rows_f32(CUtensorMap* map, const void* base, uint64_t rows, uint32_t width);
 bool encode_tmap_bf16(CUtensorMap* map, const void* base, uint64_t rows, uint64_t K,
                       uint64_t ldk, uint32_t box_rows);
 

@@ -259,6 +259,13 @@ static void fill_genargs(rec_model_s* m, Workspace& w, GenArgs& ga, SlsSynthArgs
   sa.X = w.X;
   sa.x_stride = (m->T + 1) * m->D;
   sa.dB = w.dB;
+  sa.R_all = m->interleaved ? m->rows[m->t0] : 0;
+  if (m->interleaved && m->shard == REC_SHARD_ROW && m->world > 1) sa.R_all = 0;
+  sa.tma = m->sls_tma;
+  sa.pdl = m->sls_pdl && !sa.tma;
+  sa.tmap_rows = m->d_tmap_rows;
+  sa.nsm = m->nsm;
+  if (sa.tma) sls_tma_configure(sa);
 }
 
 static const cudaGraphNode_t* last_node(cudaStream_t s, size_t* n) {
@@ -448,7 +455,10 @@ rec_status synth_submit(rec_model_s* m, Workspace& w, const int32_t* segs, int n
     dim3 grid, block;
     cudaKernelNodeParams kp{};
     void* args_a[2] = {sl.sb, fused ? static_cast<void*>(&sl.sa) : static_cast<void*>(&sl.ga)};
-    kp.func = fused ? sls_synth_kernel(sl.sa, &grid, &block) : gen_first_kernel(sl.ga, &grid, &block);
+    size_t smem = 0;
+    kp.func = fused ? sls_synth_kernel(sl.sa, &grid, &block, &smem)
+                    : gen_first_kernel(sl.ga, &grid, &block);
+    kp.sharedMemBytes = static_cast<unsigned>(smem);
     kp.gridDim = grid;
     kp.blockDim = block;
     kp.kernelParams = args_a;
@@ -683,6 +693,7 @@ static void free_model(rec_model_s* m) {
   cudaFree(m->tables);
   cudaFree(m->d_tab_off);
   cudaFree(m->d_rows);
+  cudaFree(m->d_tmap_rows);
   for (auto& e : m->prof_events) {
     cudaEventDestroy(e.a);
     cudaEventDestroy(e.b);
@@ -917,6 +928,25 @@ rec_status rec_model_create(const rec_model_desc* d, rec_model_t* out) {
                       m->k1, m->emb_shift, m->value_mode, 0,
                       m->shard == REC_SHARD_ROW && m->world > 1 ? m->row_lo : 0);
   CHECK_CUDA_CREATE(cudaGetLastError());
+  // SLS over TMA row gathers (k_sls_synth_tma, REC_SLS=tma, experimental: measured ~4x slower
+  // than the register kernel for 128-B rows): its bag summation order is a fixed tree, exact
+  // (order-free) only for int8 x 2^e tables, so fp32 value mode never uses it.
+  {
+    const char* e = getenv("REC_SLS");
+    const bool want = e && strcmp(e, "tma") == 0;  // measured slower: opt-in
+    const char* p = getenv("REC_PDL");
+    m->sls_pdl = !(p && strcmp(p, "0") == 0);
+    CHECK_CUDA_CREATE(cudaDeviceGetAttribute(&m->nsm, cudaDevAttrMultiProcessorCount, m->device));
+    if (want && m->value_mode == REC_VALUES_INT8_EXACT && sls_tma_supported(D) &&
+        total_rows < (int64_t(1) << 31)) {
+      CUtensorMap hm;
+      if (encode_tmap_rows_f32(&hm, m->tables, static_cast<uint64_t>(total_rows), D)) {
+        ALLOC(m->d_tmap_rows, sizeof(CUtensorMap));
+        CHECK_CUDA_CREATE(cudaMemcpy(m->d_tmap_rows, &hm, sizeof(hm), cudaMemcpyHostToDevice));
+        m->sls_tma = 1;
+      }
+    }
+  }
 
   // ---------------------------------------------------------------- MLP weights (G5)
   auto wexp = [](int fan_in) {
@@ -1314,6 +1344,65 @@ rec_status rec_bench_mlp(rec_model_t m, int32_t which, int32_t batch, int32_t it
   m->prof = prof;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "rec_bench_mlp");
+  return REC_OK;
+}
+
+rec_status rec_bench_sls(rec_model_t m, const int32_t* segs, int32_t nseg, int32_t iters,
+                         double* ms_per_iter) {
+  if (!m || !segs || nseg < 1 || iters < 1 || !ms_per_iter) {
+    set_error("bad argument");
+    return REC_E_INVALID_ARG;
+  }
+  if (m->lo != m->hi || m->world > 1) {
+    set_error("rec_bench_sls needs fixed pooling and an unsharded model");
+    return REC_E_UNSUPPORTED;
+  }
+  int64_t B = 0;
+  for (int i = 0; i < nseg; ++i) {
+    if (segs[3 * i + 2] <= 0 || segs[3 * i] < 0 || segs[3 * i + 1] < 0) {
+      set_error("segs[%d]: qid/start must be >= 0 and len > 0", i);
+      return REC_E_INVALID_ARG;
+    }
+    B += segs[3 * i + 2];
+  }
+  if (B > m->max_batch || nseg > m->max_batch) {
+    set_error("segs: batch of %lld items exceeds max_batch %d", (long long)B, m->max_batch);
+    return REC_E_INVALID_ARG;
+  }
+  REC_CUDA(cudaSetDevice(m->device));
+  REC_CUDA(cudaDeviceSynchronize());
+  Workspace& w = m->ws[0];
+  std::vector<int4> v(nseg);
+  int row = 0;
+  for (int i = 0; i < nseg; ++i) {
+    v[i] = make_int4(segs[3 * i], segs[3 * i + 1], segs[3 * i + 2], row);
+    row += segs[3 * i + 2];
+  }
+  SegBatch sb{};
+  sb.B = static_cast<int>(B);
+  sb.nseg = nseg;
+  sb.gsegs = w.gsegs;
+  if (nseg > kParamSegs)
+    REC_CUDA(cudaMemcpy(w.gsegs, v.data(), sizeof(int4) * nseg, cudaMemcpyHostToDevice));
+  else
+    std::copy(v.begin(), v.end(), sb.seg);
+  const SlsSynthArgs sa = w.slots[0].sa;
+  cudaEvent_t a, b;
+  REC_CUDA(cudaEventCreate(&a));
+  REC_CUDA(cudaEventCreate(&b));
+  for (int i = 0; i < 3; ++i) launch_sls_synth(sb, sa, w.stream);
+  REC_CUDA(cudaEventRecord(a, w.stream));
+  for (int i = 0; i < iters; ++i) launch_sls_synth(sb, sa, w.stream);
+  REC_CUDA(cudaEventRecord(b, w.stream));
+  REC_CUDA(cudaEventSynchronize(b));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, a, b);
+  *ms_per_iter = ms / iters;
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  m->launches += 3 + iters;
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "rec_bench_sls");
   return REC_OK;
 }
 

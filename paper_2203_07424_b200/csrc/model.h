@@ -113,6 +113,10 @@ struct rec_model_s {
   std::vector<int64_t> tab_off;        // floats, start of row 0 of table t
   int64_t* d_tab_off = nullptr;
   int64_t* d_rows = nullptr;
+  // TMA row-gather map over the arena (device copy) for the synthetic-index SLS
+  CUtensorMap* d_tmap_rows = nullptr;
+  int sls_tma = 0, nsm = 0;
+  int sls_pdl = 1;  // REC_PDL=0 disables programmatic dependent launch of the SLS
   // MLP
   std::vector<rec::Layer> bottom, top;  // top excludes the width-1 output layer
   float* w_last = nullptr;
