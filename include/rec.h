@@ -150,11 +150,13 @@ rec_status rec_bench_mlp(rec_model_t m, int32_t which, int32_t batch, int32_t it
 /* Time `iters` back-to-back launches of the synthetic-index SLS kernel (a2+a3 fused) on
  * stream slot 0 for the batch described by segs[nseg][3] (qid, first item, items; the
  * rec_synth_query_async format); *ms_per_iter = CUDA-event time on the launching stream
- * divided by iters (launch gaps included, no graph/event nodes between launches).  Needs
- * fixed pooling and an unsharded model (REC_E_UNSUPPORTED otherwise); writes the
- * workspace's X only.  bench.py uses it for the SLS roofline line. */
+ * divided by iters.  pdl = 0: plain launches (each starts after the previous one retired;
+ * launch gap included); pdl = 1: programmatic dependent launch (a launch's gathers overlap
+ * the previous launch's tail, its writes wait for it).  Needs fixed pooling and an
+ * unsharded model (REC_E_UNSUPPORTED otherwise); writes the workspace's X only.  bench.py
+ * uses it for the SLS roofline line. */
 rec_status rec_bench_sls(rec_model_t m, const int32_t* segs, int32_t nseg, int32_t iters,
-                         double* ms_per_iter);
+                         int32_t pdl, double* ms_per_iter);
 /* Diagnostic: %globaltimer stamps (ns) of CTA 0 of one fused-MLP launch (which: 0 bottom,
  * 1 top): [0] entry [1] TMEM+barriers ready [2] first TMA issued [3] first stage landed
  * [4+l] layer l MMAs committed [8+2l]/[9+2l] epilogue l start/end [15] exit; [14] = CUDA-event

@@ -19,6 +19,13 @@
 #ifndef REC_SLS_MINB
 #define REC_SLS_MINB 5  // CTAs of 128 per SM the register budget must allow (5: ~85 regs)
 #endif
+#ifdef REC_SLS_NO_GDC  // A/B: build without the griddepcontrol instructions
+#define SLS_GDC_TRIGGER()
+#define SLS_GDC_WAIT()
+#else
+#define SLS_GDC_TRIGGER() cudaTriggerProgrammaticLaunchCompletion()
+#define SLS_GDC_WAIT() cudaGridDependencySynchronize()
+#endif
 #ifndef REC_SLS_RIF
 #define REC_SLS_RIF 8  // independent 128-bit row loads in flight per lane
 #endif
@@ -168,26 +175,18 @@ __global__ void __launch_bounds__(THREADS, REC_SLS_MINB) k_sls_synth(const __gri
   constexpr int GROUPS = THREADS / LANES;
   SLS_STAMP(0);
   // Programmatic dependent launch: the next kernel of the stream may be scheduled as soon
-  // as our CTAs retire; our own reads need nothing from the predecessor (indices are
-  // synthesised, tables are constant), only the writes wait for it (below).
-  cudaTriggerProgrammaticLaunchCompletion();
+  // as our CTAs retire; our reads need nothing from the predecessor grid (indices are
+  // synthesised, tables constant), only the writes (X, dB) wait for it (below).
+  SLS_GDC_TRIGGER();
   const int B = sb.B;
-  const int nbags = a.T * B;
+  const int nbags = a.T * B;  // >= T: a synthetic batch is never empty (block 0 writes dB)
   const int g = blockIdx.x * GROUPS + threadIdx.x / LANES;
-  if (g >= nbags) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-      cudaGridDependencySynchronize();
-      *a.dB = B;
-    }
-    return;
-  }
+  if (g >= nbags) return;
   const int sub = threadIdx.x % LANES;
   const int t = g / B, b = g - t * B;
   const int2 qi = row_item(sb, b);
-  // equal-row interleaved arena: table geometry from the parameters (no dependent loads
-  // in front of the first index)
-  const uint64_t R = a.R_all ? static_cast<uint64_t>(a.R_all) : static_cast<uint64_t>(__ldg(&a.rows[t]));
-  const int64_t toff = a.R_all ? static_cast<int64_t>(t) * a.D : __ldg(&a.tab_off[t]);
+  const uint64_t R = static_cast<uint64_t>(__ldg(&a.rows[t]));
+  const int64_t toff = __ldg(&a.tab_off[t]);
   const uint32_t c2 = (static_cast<uint32_t>(t) << 8) | DOM_INDEX;
   const bool active = (sub * 4) < a.D;
   const int col = active ? sub * 4 : 0;
@@ -235,7 +234,7 @@ __global__ void __launch_bounds__(THREADS, REC_SLS_MINB) k_sls_synth(const __gri
       if (base == 0 && kk == 0) SLS_STAMP(2);
     }
   }
-  cudaGridDependencySynchronize();  // predecessor grid done: X / dB may be overwritten
+  SLS_GDC_WAIT();  // predecessor grid done: X / dB may be overwritten
   if (blockIdx.x == 0 && threadIdx.x == 0) *a.dB = B;
   if (active)
     *reinterpret_cast<float4*>(a.X + static_cast<int64_t>(b) * a.x_stride +
@@ -414,7 +413,8 @@ void launch_sls_synth(const SegBatch& sb, const SlsSynthArgs& a, cudaStream_t s)
   at[0].val.programmaticStreamSerializationAllowed = a.pdl;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  cudaLaunchKernelExC(&cfg, fn, args);
+  if (a.pdl) cudaLaunchKernelExC(&cfg, fn, args);
+  else cudaLaunchKernel(fn, grid, block, args, smem, s);
 }
 
 template <int L>

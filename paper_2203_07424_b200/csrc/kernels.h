@@ -80,7 +80,6 @@ struct SlsSynthArgs {
   // TMA row-gather variant (REC_SLS=tma): map over the arena as [rows_total][D] fp32 rows
   // (device copy, 64-B aligned), arena row of (t, r) = tab_off[t] / D + r * row_stride / D.
   const CUtensorMap* tmap_rows;
-  int64_t R_all;  // != 0: every table has R_all rows in the interleaved arena (tab_off[t] = t*D)
   int pdl;        // launch with programmatic stream serialization (kernel waits before writes)
   int tma;     // 1: k_sls_synth_tma
   int nsm;     // SMs (persistent grid)

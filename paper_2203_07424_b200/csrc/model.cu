@@ -259,8 +259,6 @@ static void fill_genargs(rec_model_s* m, Workspace& w, GenArgs& ga, SlsSynthArgs
   sa.X = w.X;
   sa.x_stride = (m->T + 1) * m->D;
   sa.dB = w.dB;
-  sa.R_all = m->interleaved ? m->rows[m->t0] : 0;
-  if (m->interleaved && m->shard == REC_SHARD_ROW && m->world > 1) sa.R_all = 0;
   sa.tma = m->sls_tma;
   sa.pdl = m->sls_pdl && !sa.tma;
   sa.tmap_rows = m->d_tmap_rows;
@@ -1348,8 +1346,8 @@ rec_status rec_bench_mlp(rec_model_t m, int32_t which, int32_t batch, int32_t it
 }
 
 rec_status rec_bench_sls(rec_model_t m, const int32_t* segs, int32_t nseg, int32_t iters,
-                         double* ms_per_iter) {
-  if (!m || !segs || nseg < 1 || iters < 1 || !ms_per_iter) {
+                         int32_t pdl, double* ms_per_iter) {
+  if (!m || !segs || nseg < 1 || iters < 1 || !ms_per_iter || (pdl != 0 && pdl != 1)) {
     set_error("bad argument");
     return REC_E_INVALID_ARG;
   }
@@ -1386,7 +1384,8 @@ rec_status rec_bench_sls(rec_model_t m, const int32_t* segs, int32_t nseg, int32
     REC_CUDA(cudaMemcpy(w.gsegs, v.data(), sizeof(int4) * nseg, cudaMemcpyHostToDevice));
   else
     std::copy(v.begin(), v.end(), sb.seg);
-  const SlsSynthArgs sa = w.slots[0].sa;
+  SlsSynthArgs sa = w.slots[0].sa;
+  sa.pdl = pdl && !sa.tma;
   cudaEvent_t a, b;
   REC_CUDA(cudaEventCreate(&a));
   REC_CUDA(cudaEventCreate(&b));

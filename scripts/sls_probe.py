@@ -86,11 +86,14 @@ def synth(a):
         ms, n = m.rec_profile_read(KERNEL_SLS)
         m.rec_profile(False)
         us = 1e3 * ms / n
-        us_b2b = 1e3 * m.rec_bench_sls(segs, a.iters)
+        us_b2b = 1e3 * m.rec_bench_sls(segs, a.iters, pdl=False)
+        us_pdl = 1e3 * m.rec_bench_sls(segs, a.iters, pdl=True)
         res[f"B{B}_L{cfg.pooling_lo}"] = {"us": round(us, 2),
                                           "GBps": round(per_item * B / (us * 1e-6) / 1e9, 1),
                                           "b2b_us": round(us_b2b, 2),
-                                          "b2b_GBps": round(per_item * B / (us_b2b * 1e-6) / 1e9, 1)}
+                                          "b2b_GBps": round(per_item * B / (us_b2b * 1e-6) / 1e9, 1),
+                                          "pdl_us": round(us_pdl, 2),
+                                          "pdl_GBps": round(per_item * B / (us_pdl * 1e-6) / 1e9, 1)}
         del m
     print(json.dumps({"mode": "synth", "lib": os.environ.get("REC_LIB_PATH", "default"),
                       "config": a.config, "results": res}))
