@@ -281,15 +281,14 @@ def run_ours(args):
     gemm_ms, gemm_n = model.rec_profile_read(KERNEL_GEMM)
     int_ms, _ = model.rec_profile_read(2)
     gen_ms, _ = model.rec_profile_read(3)
-    # back-to-back launch pass: the SLS kernel alone, `sls_iters` launches in a row per
-    # batch of the timed sequence (CUDA events on its stream, PDL between launches)
+    # back-to-back launch pass: the SLS kernel alone, one launch per batch of the timed
+    # sequence (CUDA events on its stream; with and without PDL between launches)
     model.rec_profile(False)
-    b2b_bytes, b2b_ms, ser_ms, b2b_n = 0.0, 0.0, 0.0, 0
-    for i in range(args.warmup, args.warmup + min(args.steps, args.sls_batches)):
-        b2b_ms += model.rec_bench_sls(batches[i % nb], args.sls_iters, pdl=True)
-        ser_ms += model.rec_bench_sls(batches[i % nb], args.sls_iters, pdl=False)
-        b2b_bytes += sls_bytes_per_item(cfg, synth=True) * items_b[i % nb]
-        b2b_n += 1
+    b2b_n = min(args.steps, args.sls_batches)
+    bseg = tsegs[:tbstart[b2b_n]]
+    b2b_ms = model.rec_bench_sls(bseg, tbstart[:b2b_n + 1], pdl=True)
+    ser_ms = model.rec_bench_sls(bseg, tbstart[:b2b_n + 1], pdl=False)
+    b2b_bytes = float(sls_bytes_per_item(cfg, synth=True) * int(bseg[:, 2].sum()))
     # host cost of the submit path (all streams, C++ loop, production graphs)
     hsteps = min(args.steps, 1000)
     hb = tbstart[:hsteps + 1]
@@ -319,7 +318,9 @@ def run_ours(args):
     traffic = None  # ncu dram__bytes_read.sum + dram__bytes_write.sum per SLS launch (committed capture)
     tp = os.path.join(ROOT, "profiles", "sls_traffic.json")
     if os.path.exists(tp):
-        traffic = json.load(open(tp)).get("dram_bytes_per_launch")
+        per_item = json.load(open(tp)).get("dram_bytes_per_item")
+        if per_item:  # scaled to the mean batch of the measured launches
+            traffic = per_item * (b2b_bytes / sls_bytes_per_item(cfg, synth=True)) / max(b2b_n, 1)
     sls_bytes = sls_bytes_per_item(cfg, synth=True) * ritems
     sls_gbs_isolated = sls_bytes / (sls_ms * 1e-3) / 1e9 if sls_ms > 0 else None
     sls_gbs = b2b_bytes / (b2b_ms * 1e-3) / 1e9 if b2b_ms > 0 else None
@@ -414,8 +415,9 @@ def run_ours(args):
                          "algorithmic_bytes_per_launch": b2b_bytes / max(b2b_n, 1), "peak_kind": peak_kind,
                          "bytes_per_item": sls_bytes_per_item(cfg, synth=True),
                          "avg_launch_us": 1e3 * b2b_ms / max(b2b_n, 1),
-                         "measured": f"rec_bench_sls: {b2b_n} batches of the timed sequence, each "
-                                     f"launched {args.sls_iters}x back to back on one stream "
+                         "measured": f"rec_bench_sls: the first {b2b_n} batches of the timed sequence, "
+                                     f"one launch each, back to back on one stream (distinct rows per "
+                                     f"launch: no L2 reuse between launches) "
                                      f"(programmatic dependent launch: a launch's gathers overlap the "
                                      f"previous launch's drain, its stores wait for it; CUDA events on "
                                      f"that stream, time / launches)",
@@ -467,8 +469,7 @@ def main():
     ap.add_argument("--streams", type=int, default=8)
     ap.add_argument("--submit", default="batch", choices=["batch", "python"])
     ap.add_argument("--roofline-steps", type=int, default=1000)
-    ap.add_argument("--sls-batches", type=int, default=64, help="batches in the back-to-back SLS pass")
-    ap.add_argument("--sls-iters", type=int, default=20, help="launches per batch in that pass")
+    ap.add_argument("--sls-batches", type=int, default=1000, help="batches in the back-to-back SLS pass")
     ap.add_argument("--queries", type=int, default=20000)
     ap.add_argument("--e2e-steps", type=int, default=300)
     ap.add_argument("--sla-queries", type=int, default=20000)

@@ -147,16 +147,18 @@ rec_status rec_profile(rec_model_t m, int32_t enable);
  * over whatever the workspace holds; *ms_per_iter = CUDA-event time per iteration.  Used to
  * report tensor-pipe utilisation at large batches (north_star "MLP TC util"). */
 rec_status rec_bench_mlp(rec_model_t m, int32_t which, int32_t batch, int32_t iters, double* ms_per_iter);
-/* Time `iters` back-to-back launches of the synthetic-index SLS kernel (a2+a3 fused) on
- * stream slot 0 for the batch described by segs[nseg][3] (qid, first item, items; the
- * rec_synth_query_async format); *ms_per_iter = CUDA-event time on the launching stream
- * divided by iters.  pdl = 0: plain launches (each starts after the previous one retired;
- * launch gap included); pdl = 1: programmatic dependent launch (a launch's gathers overlap
- * the previous launch's tail, its writes wait for it).  Needs fixed pooling and an
- * unsharded model (REC_E_UNSUPPORTED otherwise); writes the workspace's X only.  bench.py
- * uses it for the SLS roofline line. */
-rec_status rec_bench_sls(rec_model_t m, const int32_t* segs, int32_t nseg, int32_t iters,
-                         int32_t pdl, double* ms_per_iter);
+/* Time back-to-back launches of the synthetic-index SLS kernel (a2+a3 fused) on stream
+ * slot 0, one launch per batch of a batch sequence in the rec_synth_query_batches format
+ * (segs[][3] = (qid, first item, items); batch k = segs[batch_start[k] .. batch_start[k+1])),
+ * each batch once, so no launch re-reads rows a previous one left in L2 (distinct query ids
+ * draw distinct rows).  *ms_total = CUDA-event time on the launching stream over all
+ * nbatches launches.  pdl = 0: plain launches (each starts after the previous one retired;
+ * launch gap, ramp and drain included); pdl = 1: programmatic dependent launch (a launch's
+ * gathers overlap the previous launch's drain, its writes wait for it).  Needs fixed pooling
+ * and an unsharded model (REC_E_UNSUPPORTED otherwise); writes the workspace's X only.
+ * bench.py uses it for the SLS roofline line. */
+rec_status rec_bench_sls(rec_model_t m, const int32_t* segs, const int64_t* batch_start,
+                         int32_t nbatches, int32_t pdl, double* ms_total);
 /* Diagnostic: %globaltimer stamps (ns) of CTA 0 of one fused-MLP launch (which: 0 bottom,
  * 1 top): [0] entry [1] TMEM+barriers ready [2] first TMA issued [3] first stage landed
  * [4+l] layer l MMAs committed [8+2l]/[9+2l] epilogue l start/end [15] exit; [14] = CUDA-event

@@ -105,7 +105,7 @@ def lib() -> C.CDLL:
         L.rec_shard_plan.restype = i32
         L.rec_bench_mlp.argtypes = [vp, i32, i32, i32, C.POINTER(C.c_double)]
         L.rec_bench_mlp.restype = i32
-        L.rec_bench_sls.argtypes = [vp, vp, i32, i32, i32, C.POINTER(C.c_double)]
+        L.rec_bench_sls.argtypes = [vp, vp, vp, i32, i32, C.POINTER(C.c_double)]
         L.rec_bench_sls.restype = i32
         L.rec_debug_chain_timeline.argtypes = [vp, i32, i32, vp]
         L.rec_debug_chain_timeline.restype = i32
@@ -234,10 +234,12 @@ class RecModel:
         _check(lib().rec_bench_mlp(self.h, which, batch, iters, C.byref(ms)))
         return ms.value
 
-    def rec_bench_sls(self, segs: np.ndarray, iters: int = 50, pdl: bool = True) -> float:
+    def rec_bench_sls(self, segs: np.ndarray, batch_start: np.ndarray, pdl: bool = True) -> float:
+        """Total CUDA-event ms of one SLS launch per batch, back to back (see rec.h)."""
         segs = np.ascontiguousarray(segs, dtype=np.int32).reshape(-1, 3)
+        bs = np.ascontiguousarray(batch_start, dtype=np.int64)
         ms = C.c_double()
-        _check(lib().rec_bench_sls(self.h, _ptr(segs), segs.shape[0], iters, int(pdl), C.byref(ms)))
+        _check(lib().rec_bench_sls(self.h, _ptr(segs), _ptr(bs), len(bs) - 1, int(pdl), C.byref(ms)))
         return ms.value
 
     def rec_debug_chain_timeline(self, which: int, batch: int):

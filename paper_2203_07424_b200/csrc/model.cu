@@ -1345,9 +1345,9 @@ rec_status rec_bench_mlp(rec_model_t m, int32_t which, int32_t batch, int32_t it
   return REC_OK;
 }
 
-rec_status rec_bench_sls(rec_model_t m, const int32_t* segs, int32_t nseg, int32_t iters,
-                         int32_t pdl, double* ms_per_iter) {
-  if (!m || !segs || nseg < 1 || iters < 1 || !ms_per_iter || (pdl != 0 && pdl != 1)) {
+rec_status rec_bench_sls(rec_model_t m, const int32_t* segs, const int64_t* batch_start,
+                         int32_t nbatches, int32_t pdl, double* ms_total) {
+  if (!m || !segs || !batch_start || nbatches < 1 || !ms_total || (pdl != 0 && pdl != 1)) {
     set_error("bad argument");
     return REC_E_INVALID_ARG;
   }
@@ -1355,51 +1355,71 @@ rec_status rec_bench_sls(rec_model_t m, const int32_t* segs, int32_t nseg, int32
     set_error("rec_bench_sls needs fixed pooling and an unsharded model");
     return REC_E_UNSUPPORTED;
   }
-  int64_t B = 0;
-  for (int i = 0; i < nseg; ++i) {
-    if (segs[3 * i + 2] <= 0 || segs[3 * i] < 0 || segs[3 * i + 1] < 0) {
-      set_error("segs[%d]: qid/start must be >= 0 and len > 0", i);
+  // host: one batch descriptor per launch (long segment lists go to one device buffer)
+  std::vector<SegBatch> sbs(nbatches + 1);
+  std::vector<int4> longsegs;
+  std::vector<int64_t> long_at(nbatches + 1, -1);
+  for (int k = 0; k <= nbatches; ++k) {
+    // k == nbatches: warm-up copy of batch 0 with disjoint query ids (rows not reused)
+    const int kb = k == nbatches ? 0 : k;
+    const int64_t s0 = batch_start[kb], s1 = batch_start[kb + 1];
+    const int nseg = static_cast<int>(s1 - s0);
+    if (nseg < 1 || nseg > m->max_batch) {
+      set_error("batch %d: %d segments", kb, nseg);
       return REC_E_INVALID_ARG;
     }
-    B += segs[3 * i + 2];
-  }
-  if (B > m->max_batch || nseg > m->max_batch) {
-    set_error("segs: batch of %lld items exceeds max_batch %d", (long long)B, m->max_batch);
-    return REC_E_INVALID_ARG;
+    int64_t B = 0;
+    std::vector<int4> v(nseg);
+    for (int i = 0; i < nseg; ++i) {
+      const int32_t* sg = segs + 3 * (s0 + i);
+      if (sg[2] <= 0 || sg[0] < 0 || sg[1] < 0) {
+        set_error("batch %d segment %d: qid/start must be >= 0 and len > 0", kb, i);
+        return REC_E_INVALID_ARG;
+      }
+      v[i] = make_int4(k == nbatches ? (sg[0] ^ 0x40000000) : sg[0], sg[1], sg[2], static_cast<int>(B));
+      B += sg[2];
+    }
+    if (B > m->max_batch) {
+      set_error("batch %d: %lld items exceed max_batch %d", kb, (long long)B, m->max_batch);
+      return REC_E_INVALID_ARG;
+    }
+    SegBatch& sb = sbs[k];
+    sb = SegBatch{};
+    sb.B = static_cast<int>(B);
+    sb.nseg = nseg;
+    if (nseg > kParamSegs) {
+      long_at[k] = static_cast<int64_t>(longsegs.size());
+      longsegs.insert(longsegs.end(), v.begin(), v.end());
+    } else {
+      std::copy(v.begin(), v.end(), sb.seg);
+    }
   }
   REC_CUDA(cudaSetDevice(m->device));
   REC_CUDA(cudaDeviceSynchronize());
-  Workspace& w = m->ws[0];
-  std::vector<int4> v(nseg);
-  int row = 0;
-  for (int i = 0; i < nseg; ++i) {
-    v[i] = make_int4(segs[3 * i], segs[3 * i + 1], segs[3 * i + 2], row);
-    row += segs[3 * i + 2];
+  int4* dlong = nullptr;
+  if (!longsegs.empty()) {
+    REC_CUDA(cudaMalloc(reinterpret_cast<void**>(&dlong), sizeof(int4) * longsegs.size()));
+    REC_CUDA(cudaMemcpy(dlong, longsegs.data(), sizeof(int4) * longsegs.size(), cudaMemcpyHostToDevice));
   }
-  SegBatch sb{};
-  sb.B = static_cast<int>(B);
-  sb.nseg = nseg;
-  sb.gsegs = w.gsegs;
-  if (nseg > kParamSegs)
-    REC_CUDA(cudaMemcpy(w.gsegs, v.data(), sizeof(int4) * nseg, cudaMemcpyHostToDevice));
-  else
-    std::copy(v.begin(), v.end(), sb.seg);
+  for (int k = 0; k <= nbatches; ++k) sbs[k].gsegs = long_at[k] >= 0 ? dlong + long_at[k] : nullptr;
+  Workspace& w = m->ws[0];
   SlsSynthArgs sa = w.slots[0].sa;
   sa.pdl = pdl && !sa.tma;
   cudaEvent_t a, b;
   REC_CUDA(cudaEventCreate(&a));
   REC_CUDA(cudaEventCreate(&b));
-  for (int i = 0; i < 3; ++i) launch_sls_synth(sb, sa, w.stream);
+  for (int i = 0; i < 3; ++i) launch_sls_synth(sbs[nbatches], sa, w.stream);
   REC_CUDA(cudaEventRecord(a, w.stream));
-  for (int i = 0; i < iters; ++i) launch_sls_synth(sb, sa, w.stream);
+  for (int k = 0; k < nbatches; ++k) launch_sls_synth(sbs[k], sa, w.stream);
   REC_CUDA(cudaEventRecord(b, w.stream));
   REC_CUDA(cudaEventSynchronize(b));
   float ms = 0.f;
   cudaEventElapsedTime(&ms, a, b);
-  *ms_per_iter = ms / iters;
+  *ms_total = ms;
   cudaEventDestroy(a);
   cudaEventDestroy(b);
-  m->launches += 3 + iters;
+  if (dlong) cudaFree(dlong);
+  m->launches += 3 + nbatches;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "rec_bench_sls");
   return REC_OK;

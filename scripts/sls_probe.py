@@ -86,8 +86,10 @@ def synth(a):
         ms, n = m.rec_profile_read(KERNEL_SLS)
         m.rec_profile(False)
         us = 1e3 * ms / n
-        us_b2b = 1e3 * m.rec_bench_sls(segs, a.iters, pdl=False)
-        us_pdl = 1e3 * m.rec_bench_sls(segs, a.iters, pdl=True)
+        bsegs = np.array([[1000 + k, 0, B] for k in range(a.iters)], np.int32)  # distinct rows
+        bst = np.arange(a.iters + 1, dtype=np.int64)
+        us_b2b = 1e3 * m.rec_bench_sls(bsegs, bst, pdl=False) / a.iters
+        us_pdl = 1e3 * m.rec_bench_sls(bsegs, bst, pdl=True) / a.iters
         res[f"B{B}_L{cfg.pooling_lo}"] = {"us": round(us, 2),
                                           "GBps": round(per_item * B / (us * 1e-6) / 1e9, 1),
                                           "b2b_us": round(us_b2b, 2),
