@@ -239,6 +239,11 @@ def run_ours(args):
     for i in range(args.warmup):
         step(i)
     sync_all()
+    if args.pipe > 0:
+        model.rec_set_pipeline(args.pipe)
+        wb = tbstart[:args.warmup + 1] if args.warmup < len(tbstart) else tbstart
+        model.rec_synth_query_batches(tsegs[:wb[-1]], wb)  # warm the lane graphs
+        sync_all()
     base_launch = model.rec_profile_read(4)[1]
     if world > 1:
         dist.barrier()
@@ -375,7 +380,7 @@ def run_ours(args):
                 lam_hint[0] = lam
             return lam
 
-        ms = [x for x in (1, 2, 4, 8) if x <= m_streams]
+        ms = [x for x in (1, 2, 4, 8, 16) if x <= m_streams]
         ds = [x for x in (256, 512, 1024) if x <= d]
         res = gradient_search(evaluate, ms, ds, noise=0.02)
         sla = {"sla_ms": cfg.sla_ms, "percentile": "p95 (nearest rank)",
@@ -406,7 +411,7 @@ def run_ours(args):
                        "rows": cfg.rows, "dim": cfg.dim, "pooling": cfg.pooling_lo,
                        "items_per_s": tot_items / (ms_max * 1e-3), "queries_per_step": tot_q / args.steps / world,
                        "mean_query_items": float(sizes.mean()), "parallelism": f"replicas x{world}",
-                       "streams_per_gpu": m_streams,
+                       "streams_per_gpu": m_streams, "pipeline_lanes": args.pipe,
                        "l2": "inputs larger than L2 (1.28 GB tables, uniform random rows per step)",
                        "value_is": "saturation QPS (burst trace); see sla"},
             "roofline": {"bound": "hbm", "kernel": "k_sls", "achieved": sls_gbs, "peak": hbm_peak,
@@ -466,8 +471,10 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="rmc1", choices=list(W.SHORT))
     ap.add_argument("--batch", type=int, default=1024)
-    ap.add_argument("--streams", type=int, default=8)
+    ap.add_argument("--streams", type=int, default=16)
     ap.add_argument("--submit", default="batch", choices=["batch", "python"])
+    ap.add_argument("--pipe", type=int, default=0,
+                    help="S-D pipeline lanes (rec_set_pipeline) for the timed region; 0 = slot graphs")
     ap.add_argument("--roofline-steps", type=int, default=1000)
     ap.add_argument("--sls-batches", type=int, default=1000, help="batches in the back-to-back SLS pass")
     ap.add_argument("--queries", type=int, default=20000)

@@ -122,6 +122,23 @@ rec_status rec_synth_query_async(rec_model_t m, int32_t slot, const int32_t* seg
 rec_status rec_synth_query_batches(rec_model_t m, const int32_t* segs, const int64_t* batch_start,
                                    int64_t nbatches, int32_t first_slot);
 
+/* S-D pipeline (SparseNet and DenseNet stages of consecutive
+ * batches overlap).  lanes > 0 splits the model's `streams` workspaces into `lanes` groups
+ * of N = streams / lanes (2 <= N <= 64); each lane is one captured graph that runs N batches:
+ * their SLS kernels back to back on the lane stream with programmatic dependent launch,
+ * each batch's dense features + bottom MLP and its interaction + top MLP on that batch's
+ * own streams.  While lanes exist, rec_synth_query_batches submits groups of N batches per
+ * lane launch (lanes alternate; a remainder < N uses the slot graphs).  lanes = 0 removes
+ * the lanes.  Needs fixed pooling and an unsharded model (REC_E_UNSUPPORTED); streams not
+ * divisible into groups of 2..64 -> REC_E_INVALID_ARG.  Synchronises the device. */
+rec_status rec_set_pipeline(rec_model_t m, int32_t lanes);
+/* rec_synth_query_batches through the lanes, also returning the CTRs: ctr_out (DEVICE,
+ * fp32, or NULL) receives every batch's CTRs concatenated in batch order (sum of items).
+ * Bit-identical to submitting the same batches with rec_synth_query_async.  Async; needs
+ * rec_set_pipeline(m, > 0) first (REC_E_INVALID_ARG otherwise). */
+rec_status rec_synth_query_pipeline(rec_model_t m, const int32_t* segs, const int64_t* batch_start,
+                                    int64_t nbatches, float* ctr_out);
+
 /* Wait for stream slot `slot`; returns INDEX_OOB / OFFSETS if a kernel flagged it. */
 rec_status rec_sync(rec_model_t m, int32_t slot);
 

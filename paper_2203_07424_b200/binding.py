@@ -32,7 +32,7 @@ EXPORTS = ["rec_model_create", "rec_model_destroy", "rec_query", "rec_query_debu
            "rec_query_async", "rec_synth_query_async", "rec_sync", "rec_stream_handle",
            "rec_gen_batch", "rec_profile", "rec_profile_read", "rec_serve", "rec_last_error",
            "rec_nccl_unique_id_size", "rec_nccl_get_unique_id", "rec_version", "rec_split_fuse",
-           "rec_synth_query_batches", "rec_shard_plan", "rec_bench_mlp", "rec_bench_sls",
+           "rec_synth_query_batches", "rec_shard_plan", "rec_bench_mlp", "rec_bench_sls", "rec_set_pipeline", "rec_synth_query_pipeline",
            "rec_debug_chain_timeline"]
 
 
@@ -107,6 +107,10 @@ def lib() -> C.CDLL:
         L.rec_bench_mlp.restype = i32
         L.rec_bench_sls.argtypes = [vp, vp, vp, i32, i32, C.POINTER(C.c_double)]
         L.rec_bench_sls.restype = i32
+        L.rec_set_pipeline.argtypes = [vp, i32]
+        L.rec_set_pipeline.restype = i32
+        L.rec_synth_query_pipeline.argtypes = [vp, vp, vp, C.c_int64, vp]
+        L.rec_synth_query_pipeline.restype = i32
         L.rec_debug_chain_timeline.argtypes = [vp, i32, i32, vp]
         L.rec_debug_chain_timeline.restype = i32
         for f in ("rec_model_create", "rec_query", "rec_query_debug", "rec_query_async",
@@ -212,6 +216,15 @@ class RecModel:
         segs = np.ascontiguousarray(segs, dtype=np.int32).reshape(-1, 3)
         bs = np.ascontiguousarray(batch_start, dtype=np.int64)
         _check(lib().rec_synth_query_batches(self.h, _ptr(segs), _ptr(bs), len(bs) - 1, first_slot))
+
+    def rec_set_pipeline(self, lanes: int):
+        _check(lib().rec_set_pipeline(self.h, lanes))
+
+    def rec_synth_query_pipeline(self, segs: np.ndarray, batch_start: np.ndarray, ctr=None):
+        segs = np.ascontiguousarray(segs, dtype=np.int32).reshape(-1, 3)
+        bs = np.ascontiguousarray(batch_start, dtype=np.int64)
+        _check(lib().rec_synth_query_pipeline(self.h, _ptr(segs), _ptr(bs), len(bs) - 1,
+                                              _ptr(ctr) if ctr is not None else None))
 
     def rec_sync(self, slot: int = 0):
         _check(lib().rec_sync(self.h, slot))

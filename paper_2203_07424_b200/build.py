@@ -17,7 +17,7 @@ CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libhercules_rec.so")
 BUILD = os.path.join(ROOT, "build", "obj")
 
-SOURCES = ["k_synth.cu", "k_sls.cu", "k_gemm.cu", "k_mlp.cu", "k_interact.cu", "model.cu", "dist.cu",
+SOURCES = ["k_synth.cu", "k_sls.cu", "k_gemm.cu", "k_mlp.cu", "k_interact.cu", "model.cu", "pipe.cu", "dist.cu",
            "serve.cpp"]
 HEADERS = ["common.cuh", "sm100.cuh", "kernels.h", "model.h", "synth.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -6,49 +6,66 @@
 //   A_top[b] = bf16([x_b, Z(1,0), Z(2,0), Z(2,1), ..., Z(T,T-1), 0-pad])
 // which is the A operand (K-major bf16 row) of the first top-MLP GEMM.
 //
-// One warp per item: X_b (<= 41 x 64 fp32 for RMC2) is staged in shared memory with a
-// padded row pitch (D+1 floats, conflict-free column reads); lanes own pairs; each dot is a
-// sequential fp32 FMA chain.  (T+1)^2/2 * D FMAs per item is < 1 % of the item's SLS time.
+// One warp per item (see k_interact below).  (T+1)^2/2 * D FMAs per item is < 1 % of the
+// item's SLS time; the kernel is latency bound, so loads and stores are vectorised.
 #include "common.cuh"
 #include "kernels.h"
 
 namespace rec {
 
+// Pair p of the strict lower triangle in row-major order: (i, j), 1 <= i <= T, 0 <= j < i,
+// p = i(i-1)/2 + j.
+__device__ __forceinline__ int2 pair_of(int p) {
+  int i = static_cast<int>((1.0f + sqrtf(1.0f + 8.0f * static_cast<float>(p))) * 0.5f);
+  while (i * (i - 1) / 2 > p) --i;
+  while ((i + 1) * i / 2 <= p) ++i;
+  return make_int2(i, p - i * (i - 1) / 2);
+}
+
+// One warp per item.  X_b arrives as 16-B vector loads issued back to back (one L2 round
+// trip), rows land in shared memory with a D+4 pitch (float4-aligned, rows 4 banks apart);
+// each lane forms whole pairs as sequential fp32 FMA chains over k; the bf16 output row is
+// staged in shared memory and written with 16-B vector stores (ld is a multiple of 8).
 __global__ void k_interact(const float* __restrict__ X, int B, const int* __restrict__ dB, int T,
                            int D, __nv_bfloat16* __restrict__ A, int ld, int warps_per_cta) {
-  extern __shared__ float sm[];
+  extern __shared__ float4 sm4[];
   if (dB) B = *dB;
   if (static_cast<int>(blockIdx.x) * warps_per_cta >= B) return;
-  const int rows = T + 1, pitch = D + 1, npairs = T * (T + 1) / 2;
-  uint8_t* pi = reinterpret_cast<uint8_t*>(sm);
-  uint8_t* pj = pi + npairs;
-  float* xs_all = sm + (2 * npairs + 15) / 4 + 4;
-  for (int p = threadIdx.x; p < npairs; p += blockDim.x) {
-    int i = 1, base = 0;
-    while (base + i <= p) {  // row i holds pairs [i(i-1)/2, i(i+1)/2)
-      base += i;
-      ++i;
-    }
-    pi[p] = static_cast<uint8_t>(i);
-    pj[p] = static_cast<uint8_t>(p - base);
-  }
-  __syncthreads();
+  const int rows = T + 1, pitch = D + 4, npairs = T * (T + 1) / 2, d4 = D / 4;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  float* xs = xs_all + warp * rows * pitch;
+  const int per_warp_f = rows * pitch + ld / 2;  // floats: X rows + bf16 output row
+  float* xs = reinterpret_cast<float*>(sm4) + warp * per_warp_f;
+  __nv_bfloat16* outs = reinterpret_cast<__nv_bfloat16*>(xs + rows * pitch);
+  const int nvec = rows * d4;
   for (int b = blockIdx.x * warps_per_cta + warp; b < B; b += gridDim.x * warps_per_cta) {
-    const float* xb = X + static_cast<int64_t>(b) * rows * D;
-    for (int e = lane; e < rows * D; e += 32) xs[(e / D) * pitch + (e % D)] = xb[e];
-    __syncwarp();
-    __nv_bfloat16* ab = A + static_cast<int64_t>(b) * ld;
-    for (int k = lane; k < D; k += 32) ab[k] = __float2bfloat16_rn(xs[k]);
-    for (int p = lane; p < npairs; p += 32) {
-      const float* xi = xs + pi[p] * pitch;
-      const float* xj = xs + pj[p] * pitch;
-      float acc = 0.f;
-      for (int k = 0; k < D; ++k) acc = fmaf(xi[k], xj[k], acc);
-      ab[D + p] = __float2bfloat16_rn(acc);
+    const float4* xb = reinterpret_cast<const float4*>(X + static_cast<int64_t>(b) * rows * D);
+#pragma unroll 4
+    for (int e = lane; e < nvec; e += 32) {
+      const float4 v = __ldg(xb + e);
+      const int r = e / d4, c = e - r * d4;
+      *reinterpret_cast<float4*>(xs + r * pitch + 4 * c) = v;
     }
-    for (int k = D + npairs + lane; k < ld; k += 32) ab[k] = __float2bfloat16_rn(0.f);
+    __syncwarp();
+    for (int k = lane; k < D; k += 32) outs[k] = __float2bfloat16_rn(xs[k]);
+    for (int p = lane; p < npairs; p += 32) {
+      const int2 ij = pair_of(p);
+      const float4* xi = reinterpret_cast<const float4*>(xs + ij.x * pitch);
+      const float4* xj = reinterpret_cast<const float4*>(xs + ij.y * pitch);
+      float acc = 0.f;
+      for (int k = 0; k < d4; ++k) {
+        const float4 a = xi[k], c = xj[k];
+        acc = fmaf(a.x, c.x, acc);
+        acc = fmaf(a.y, c.y, acc);
+        acc = fmaf(a.z, c.z, acc);
+        acc = fmaf(a.w, c.w, acc);
+      }
+      outs[D + p] = __float2bfloat16_rn(acc);
+    }
+    for (int k = D + npairs + lane; k < ld; k += 32) outs[k] = __float2bfloat16_rn(0.f);
+    __syncwarp();
+    int4* ab = reinterpret_cast<int4*>(A + static_cast<int64_t>(b) * ld);
+    const int4* os = reinterpret_cast<const int4*>(outs);
+    for (int v = lane; v < ld / 8; v += 32) ab[v] = os[v];
     __syncwarp();
   }
 }
@@ -56,13 +73,11 @@ __global__ void k_interact(const float* __restrict__ X, int B, const int* __rest
 void launch_interact(const float* X, int B, const int* dB, int T, int D, __nv_bfloat16* A_top,
                      int ld_top, cudaStream_t s) {
   if (B <= 0) return;
-  const int npairs = T * (T + 1) / 2;
-  const size_t per_warp = static_cast<size_t>(T + 1) * (D + 1) * sizeof(float);
-  const size_t head = ((2 * npairs + 15) / 4 + 4) * sizeof(float);
-  int wpc = static_cast<int>((44 * 1024 - head) / per_warp);
+  const size_t per_warp = (static_cast<size_t>(T + 1) * (D + 4) + ld_top / 2) * sizeof(float);
+  int wpc = static_cast<int>((96 * 1024) / per_warp);
   if (wpc > 8) wpc = 8;
   if (wpc < 1) wpc = 1;
-  const size_t smem = head + wpc * per_warp;
+  const size_t smem = wpc * per_warp;
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(k_interact, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(smem));

@@ -223,8 +223,8 @@ static rec_status wait_pin(Workspace& w) {
   return REC_OK;
 }
 
-static void fill_genargs(rec_model_s* m, Workspace& w, GenArgs& ga, SlsSynthArgs& sa,
-                         float* dense_f32_out) {
+void fill_genargs(rec_model_s* m, Workspace& w, GenArgs& ga, SlsSynthArgs& sa,
+                  float* dense_f32_out) {
   ga = GenArgs{};
   ga.cap = w.cap;
   ga.T = m->T;
@@ -266,7 +266,7 @@ static void fill_genargs(rec_model_s* m, Workspace& w, GenArgs& ga, SlsSynthArgs
   if (sa.tma) sls_tma_configure(sa);
 }
 
-static const cudaGraphNode_t* last_node(cudaStream_t s, size_t* n) {
+const cudaGraphNode_t* last_node(cudaStream_t s, size_t* n) {
   cudaStreamCaptureStatus cs;
   const cudaGraphNode_t* deps = nullptr;
   if (cudaStreamGetCaptureInfo(s, &cs, nullptr, nullptr, &deps, n) != cudaSuccess) *n = 0;
@@ -301,7 +301,7 @@ static rec_status synth_chain(rec_model_s* m, Workspace& w, SynthSlot& sl, bool 
       }
       *sl.cap_dense = d[0];
     }
-    enqueue_bottom(m, w, sb, w.cap, w.dB, gev);
+    if (!(m->diag_skip & 1)) enqueue_bottom(m, w, sb, w.cap, w.dB, gev);
     mark(gev, 7, sb);
     REC_CUDA(cudaEventRecord(w.ev_join, sb));
     mark(gev, 1, s);
@@ -321,7 +321,7 @@ static rec_status synth_chain(rec_model_s* m, Workspace& w, SynthSlot& sl, bool 
     mark(gev, 2, s);
     REC_CUDA(cudaStreamWaitEvent(s, w.ev_join, 0));
     mark(gev, 3, s);
-    enqueue_interact_top(m, w, s, w.cap, w.dB, w.ctr, w.logit, gev);
+    if (!(m->diag_skip & 2)) enqueue_interact_top(m, w, s, w.cap, w.dB, w.ctr, w.logit, gev);
     cudaError_t err = cudaGetLastError();
     if (err != cudaSuccess) return cuda_fail(err, "synthetic chain launch");
     return REC_OK;
@@ -420,6 +420,10 @@ rec_status synth_submit(rec_model_s* m, Workspace& w, const int32_t* segs, int n
   if (B > w.cap || nseg > w.cap) {
     set_error("segs: batch of %lld items exceeds max_batch %d", (long long)B, w.cap);
     return REC_E_INVALID_ARG;
+  }
+  if (m->pipe_active.load(std::memory_order_acquire)) {
+    rec_status st = pipe_leave(m);
+    if (st != REC_OK) return st;
   }
   const double t0 = host_now_ns();
   SynthSlot& sl = w.slots[w.next_slot];
@@ -524,6 +528,10 @@ static rec_status query_impl(rec_model_s* m, const float* dense, const int32_t* 
     return REC_E_INVALID_ARG;
   }
   REC_CUDA(cudaSetDevice(m->device));
+  if (m->pipe_active.load()) {
+    rec_status st = pipe_leave(m);
+    if (st != REC_OK) return st;
+  }
   Workspace& w = m->ws[0];
   cudaStream_t s = w.stream;
   const int T = m->T, nb = T * B;
@@ -638,6 +646,7 @@ int32_t rec_version(void) { return 1; }
 static void free_model(rec_model_s* m) {
   if (!m) return;
   cudaSetDevice(m->device);
+  pipe_destroy(m);
   for (auto& w : m->ws) {
     if (w.stream) cudaStreamSynchronize(w.stream);
     cudaFree(w.indices);
@@ -671,6 +680,12 @@ static void free_model(rec_model_s* m) {
     cudaFree(w.gsegs);
     if (w.ev_fork) cudaEventDestroy(w.ev_fork);
     if (w.ev_join) cudaEventDestroy(w.ev_join);
+    if (w.ev_sls) cudaEventDestroy(w.ev_sls);
+    if (w.ev_done) cudaEventDestroy(w.ev_done);
+    if (w.stream_c) {
+      cudaStreamSynchronize(w.stream_c);
+      cudaStreamDestroy(w.stream_c);
+    }
     if (w.stream_b) {
       cudaStreamSynchronize(w.stream_b);
       cudaStreamDestroy(w.stream_b);
@@ -932,6 +947,9 @@ rec_status rec_model_create(const rec_model_desc* d, rec_model_t* out) {
   {
     const char* e = getenv("REC_SLS");
     const bool want = e && strcmp(e, "tma") == 0;  // measured slower: opt-in
+    // diagnostic only (REC_STEP_DIAG, never set by tests or bench): bit 0 drops the bottom
+    // MLP, bit 1 the interaction + top MLP from the synthetic step graphs (CTRs invalid)
+    if (const char* d = getenv("REC_STEP_DIAG")) m->diag_skip = atoi(d);
     const char* p = getenv("REC_PDL");
     m->sls_pdl = !(p && strcmp(p, "0") == 0);
     CHECK_CUDA_CREATE(cudaDeviceGetAttribute(&m->nsm, cudaDevAttrMultiProcessorCount, m->device));
@@ -1060,6 +1078,9 @@ rec_status rec_model_create(const rec_model_desc* d, rec_model_t* out) {
     CHECK_CUDA_CREATE(cudaStreamCreateWithFlags(&w.stream_b, cudaStreamNonBlocking));
     CHECK_CUDA_CREATE(cudaEventCreateWithFlags(&w.ev_fork, cudaEventDisableTiming));
     CHECK_CUDA_CREATE(cudaEventCreateWithFlags(&w.ev_join, cudaEventDisableTiming));
+    CHECK_CUDA_CREATE(cudaStreamCreateWithFlags(&w.stream_c, cudaStreamNonBlocking));
+    CHECK_CUDA_CREATE(cudaEventCreateWithFlags(&w.ev_sls, cudaEventDisableTiming));
+    CHECK_CUDA_CREATE(cudaEventCreateWithFlags(&w.ev_done, cudaEventDisableTiming));
     ALLOC(w.dB, sizeof(int) * 4);
     ALLOC(w.gsegs, sizeof(int4) * (cap + 1));
     CHECK_CUDA_CREATE(cudaEventCreateWithFlags(&w.pin_free, cudaEventDisableTiming));
@@ -1221,6 +1242,10 @@ rec_status rec_query_async(rec_model_t m, int32_t slot, const float* dense, cons
     return REC_E_INVALID_ARG;
   }
   REC_CUDA(cudaSetDevice(m->device));
+  if (m->pipe_active.load()) {
+    rec_status st = pipe_leave(m);
+    if (st != REC_OK) return st;
+  }
   Workspace& w = m->ws[slot];
   launch_dense_to_bf16(dense, batch, m->F, m->Fpad, w.dense_bf, w.stream);
   m->launches += 1;
@@ -1262,6 +1287,7 @@ rec_status rec_synth_query_batches(rec_model_t m, const int32_t* segs, const int
     return REC_E_UNSUPPORTED;
   }
   REC_CUDA(cudaSetDevice(m->device));
+  if (!m->pipe.empty()) return pipe_submit(m, segs, batch_start, nbatches, nullptr);
   for (int64_t b = 0; b < nbatches; ++b) {
     Workspace& w = m->ws[(first_slot + b) % m->nstreams];
     const int64_t s0 = batch_start[b], s1 = batch_start[b + 1];
@@ -1278,6 +1304,11 @@ rec_status rec_sync(rec_model_t m, int32_t slot) {
     return REC_E_INVALID_ARG;
   }
   REC_CUDA(cudaSetDevice(m->device));
+  if (m->pipe_active.load()) {  // the slot's batches may run inside a lane graph
+    for (auto& L : m->pipe)
+      for (int k : L.ws)
+        if (k == slot) REC_CUDA(cudaEventSynchronize(L.free));
+  }
   return sync_ws(m->ws[slot]);
 }
 

@@ -56,6 +56,8 @@ struct Workspace {
   cudaStream_t stream = nullptr;
   cudaStream_t stream_b = nullptr;   // parallel branch: bottom MLP runs concurrently with SLS
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaStream_t stream_c = nullptr;   // pipeline lanes: interaction + top of this workspace's batch
+  cudaEvent_t ev_sls = nullptr, ev_done = nullptr;  // pipeline capture edges
   int* dB = nullptr;                 // device batch size of the in-flight synthetic batch
   int4* gsegs = nullptr;             // device segments for batches with > kParamSegs segments
   int cap = 0;                       // max items
@@ -87,6 +89,23 @@ struct Workspace {
                                      // slot wait, total) — per stream: dispatch threads
 };
 
+// S-D pipeline lane: one captured graph over N workspaces that
+// runs N batches with the SparseNet and DenseNet stages decoupled — all N SLS kernels on one
+// stream as a programmatic-dependent-launch chain (each launch's gathers overlap the previous
+// one's drain), every batch's dense features + bottom MLP on its workspace's branch stream,
+// and its interaction + top MLP on a third stream once both halves are done.
+struct PipeLane {
+  std::vector<int> ws;               // workspace of batch i (ws[0]'s stream launches the graph)
+  std::vector<SegBatch*> sb;         // host copies of the by-value batch descriptors
+  std::vector<GenArgs> ga;
+  std::vector<SlsSynthArgs> sa;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  std::vector<cudaGraphNode_t> sls_node, dense_node;
+  cudaEvent_t free = nullptr;        // the lane's last graph launch completed
+  int kernels = 0;                   // kernels per launch
+};
+
 struct ProfEvent {
   int kernel;
   cudaEvent_t a, b;
@@ -116,7 +135,8 @@ struct rec_model_s {
   // TMA row-gather map over the arena (device copy) for the synthetic-index SLS
   CUtensorMap* d_tmap_rows = nullptr;
   int sls_tma = 0, nsm = 0;
-  int sls_pdl = 1;  // REC_PDL=0 disables programmatic dependent launch of the SLS
+  int sls_pdl = 1;    // REC_PDL=0 disables programmatic dependent launch of the SLS
+  int diag_skip = 0;  // REC_STEP_DIAG (diagnostic): stages dropped from the synthetic step
   // MLP
   std::vector<rec::Layer> bottom, top;  // top excludes the width-1 output layer
   float* w_last = nullptr;
@@ -129,6 +149,11 @@ struct rec_model_s {
   int Ktop = 0, Ktop_pad = 0, hmax = 0;
   // streams + workspaces
   std::vector<rec::Workspace> ws;
+  // S-D pipeline lanes (rec_set_pipeline); pipe_active: the last synthetic submission used
+  // the lanes (switching modes synchronises, workspaces are shared)
+  std::vector<rec::PipeLane> pipe;
+  std::atomic<int> pipe_active{0};
+  int pipe_next = 0;
   // profiling
   bool prof = false;
   std::vector<rec::ProfEvent> prof_events;
@@ -161,6 +186,16 @@ rec_status forward_enqueue(rec_model_s* m, Workspace& w, const int* indices, con
 rec_status synth_submit(rec_model_s* m, Workspace& w, const int32_t* segs, int nseg, int* batch_out,
                         float* dense_f32_out);
 rec_status capture_graphs(rec_model_s* m, Workspace& w);
+void fill_genargs(rec_model_s* m, Workspace& w, GenArgs& ga, SlsSynthArgs& sa, float* dense_f32_out);
+const cudaGraphNode_t* last_node(cudaStream_t s, size_t* n);
+// Leave pipeline mode (wait for every lane) before a non-pipeline submission.
+rec_status pipe_leave(rec_model_s* m);
+void pipe_destroy(rec_model_s* m);
+// Submit nbatches synthetic batches through the lanes (groups of N = batches per lane); a
+// remainder < N goes through the per-stream slot graphs.  ctr_out (device, optional): the
+// CTRs of all batches, concatenated in batch order.
+rec_status pipe_submit(rec_model_s* m, const int32_t* segs, const int64_t* batch_start,
+                       int64_t nbatches, float* ctr_out);
 void enqueue_bottom(rec_model_s* m, Workspace& w, cudaStream_t st, int B, const int* dB,
                     cudaEvent_t* gev);
 void enqueue_interact_top(rec_model_s* m, Workspace& w, cudaStream_t st, int B, const int* dB,

@@ -21,11 +21,18 @@
 #include <mutex>
 #include <thread>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <queue>
 #include <vector>
 
 #include "model.h"
+
+static inline void cpu_relax() {
+#if defined(__x86_64__) || defined(__i386__)
+  __builtin_ia32_pause();
+#endif
+}
 
 namespace rec {
 
@@ -468,95 +475,118 @@ rec_status rec_serve(rec_model_t m, const rec_trace_row* trace, int64_t n, doubl
     std::atomic<bool> failed{false};
     std::atomic<int> fail_status{REC_OK};
     const double t0 = now_s() - t_first;
-    auto worker = [&](int s) {
-      cudaSetDevice(m->device);
-      Workspace& w = m->ws[s];
-      Lane& L = lanes[s];
-      std::vector<int32_t> segs_local;
+    // one dispatcher thread per stream up to half the host's hardware threads; beyond that a
+    // thread owns several streams (streams s = t, t + nthreads, ...) so the spinning
+    // dispatchers never oversubscribe the cores
+    int hw = static_cast<int>(std::max(2u, std::thread::hardware_concurrency()));
+    if (const char* lw = getenv("LOCAL_WORLD_SIZE"))  // torchrun: ranks of this box share its cores
+      hw = std::max(2, hw / std::max(1, atoi(lw)));
+    const int nthreads = std::max(1, std::min(M, hw / 2));
+    struct Own {
       uint32_t seq = 0;
       int64_t my_batch = -1;
-      double my_disp = 0;
+    };
+    std::vector<Own> own(M);
+    auto worker = [&](int tid) {
+      cudaSetDevice(m->device);
+      std::vector<int32_t> segs_local;
+      int idle_polls = 0;
       while (done_q.load(std::memory_order_relaxed) < n && !failed.load(std::memory_order_relaxed)) {
-        if (L.busy) {
-          const bool done = L.flag_host ? (*reinterpret_cast<volatile uint32_t*>(L.flag_host) == seq)
-                                        : (cudaEventQuery(L.done) == cudaSuccess);
-          if (!done) continue;
-          const double t_c = now_s() - t0;
-          std::lock_guard<std::mutex> g(mu);
-          finish_batch(my_batch, t_c);
-          done_q.store(completed, std::memory_order_relaxed);
-          L.busy = false;
-          continue;
-        }
-        int64_t k = 0, items = 0, c0 = 0;
-        if (avail.load(std::memory_order_acquire) <= head_a.load(std::memory_order_acquire)) continue;
-        {
-          std::lock_guard<std::mutex> g(mu);
-          if (head >= static_cast<int64_t>(fifo.size())) continue;
-          k = fuse_head(fifo, head, d, &items);
-          const double tn = now_s() - t0;
-          if (!should_fire(tn, k, items)) continue;
-          c0 = head;
-          my_batch = static_cast<int64_t>(batches.size());
-          batches.push_back(Batch{s, head, k, items, tn, 0});
-          segs_local.resize(3 * k);
-          for (int64_t c = 0; c < k; ++c) {
-            const Chunk& ch = fifo[head + c];
-            segs_local[3 * c] = ch.qid;
-            segs_local[3 * c + 1] = ch.start;
-            segs_local[3 * c + 2] = ch.len;
-            disp_t[ch.pos] = tn;
-            if (batch_log && logged < log_cap) {
-              int32_t* r = batch_log + 5 * logged++;
-              r[0] = static_cast<int32_t>(my_batch);
-              r[1] = s;
-              r[2] = ch.qid;
-              r[3] = ch.start;
-              r[4] = ch.len;
-            }
+        bool progressed = false;
+        for (int s = tid; s < M; s += nthreads) {
+          Workspace& w = m->ws[s];
+          Lane& L = lanes[s];
+          Own& O = own[s];
+          if (L.busy) {
+            const bool done = L.flag_host ? (*reinterpret_cast<volatile uint32_t*>(L.flag_host) == O.seq)
+                                          : (cudaEventQuery(L.done) == cudaSuccess);
+            if (!done) continue;
+            const double t_c = now_s() - t0;
+            std::lock_guard<std::mutex> g(mu);
+            finish_batch(O.my_batch, t_c);
+            done_q.store(completed, std::memory_order_relaxed);
+            L.busy = false;
+            progressed = true;
           }
-          head += k;
-          head_a.store(head, std::memory_order_release);
-          my_disp = tn;
-        }
-        (void)my_disp;
-        int B = 0;
-        rec_status rs;
-        if (pol->input_mode == REC_INPUT_DEVICE_SYNTH) {
-          rs = synth_submit(m, w, segs_local.data(), static_cast<int>(k), &B, nullptr);
-        } else {
-          std::vector<Chunk> local(k);
+          int64_t k = 0, items = 0, c0 = 0;
+          if (avail.load(std::memory_order_acquire) <= head_a.load(std::memory_order_acquire)) continue;
           {
             std::lock_guard<std::mutex> g(mu);
-            for (int64_t c = 0; c < k; ++c) local[c] = fifo[c0 + c];
+            if (head >= static_cast<int64_t>(fifo.size())) continue;
+            k = fuse_head(fifo, head, d, &items);
+            const double tn = now_s() - t0;
+            if (!should_fire(tn, k, items)) continue;
+            c0 = head;
+            O.my_batch = static_cast<int64_t>(batches.size());
+            batches.push_back(Batch{s, head, k, items, tn, 0});
+            segs_local.resize(3 * k);
+            for (int64_t c = 0; c < k; ++c) {
+              const Chunk& ch = fifo[head + c];
+              segs_local[3 * c] = ch.qid;
+              segs_local[3 * c + 1] = ch.start;
+              segs_local[3 * c + 2] = ch.len;
+              disp_t[ch.pos] = tn;
+              if (batch_log && logged < log_cap) {
+                int32_t* r = batch_log + 5 * logged++;
+                r[0] = static_cast<int32_t>(O.my_batch);
+                r[1] = s;
+                r[2] = ch.qid;
+                r[3] = ch.start;
+                r[4] = ch.len;
+              }
+            }
+            head += k;
+            head_a.store(head, std::memory_order_release);
           }
-          rs = host_input_enqueue(m, w, H, local, 0, k, &B);
-          if (rs == REC_OK) rs = forward_enqueue(m, w, w.indices, w.offsets, B, nullptr, w.ctr, w.logit, nullptr);
-        }
-        if (rs == REC_OK && ctr_out)
-          if (cudaMemcpyAsync(L.ctr_host, w.ctr, sizeof(float) * B, cudaMemcpyDeviceToHost, w.stream) != cudaSuccess)
-            rs = REC_E_CUDA;
-        if (rs == REC_OK) {
-          ++seq;
-          if (L.flag_host) {
-            if (stream_write_u32(w.stream, L.flag_dev, seq) != REC_OK) rs = REC_E_CUDA;
-          } else if (cudaEventRecord(L.done, w.stream) != cudaSuccess) {
-            rs = REC_E_CUDA;
+          int B = 0;
+          rec_status rs;
+          if (pol->input_mode == REC_INPUT_DEVICE_SYNTH) {
+            rs = synth_submit(m, w, segs_local.data(), static_cast<int>(k), &B, nullptr);
+          } else {
+            std::vector<Chunk> local(k);
+            {
+              std::lock_guard<std::mutex> g(mu);
+              for (int64_t c = 0; c < k; ++c) local[c] = fifo[c0 + c];
+            }
+            rs = host_input_enqueue(m, w, H, local, 0, k, &B);
+            if (rs == REC_OK) rs = forward_enqueue(m, w, w.indices, w.offsets, B, nullptr, w.ctr, w.logit, nullptr);
           }
+          if (rs == REC_OK && ctr_out)
+            if (cudaMemcpyAsync(L.ctr_host, w.ctr, sizeof(float) * B, cudaMemcpyDeviceToHost, w.stream) != cudaSuccess)
+              rs = REC_E_CUDA;
+          if (rs == REC_OK) {
+            ++O.seq;
+            if (L.flag_host) {
+              if (stream_write_u32(w.stream, L.flag_dev, O.seq) != REC_OK) rs = REC_E_CUDA;
+            } else if (cudaEventRecord(L.done, w.stream) != cudaSuccess) {
+              rs = REC_E_CUDA;
+            }
+          }
+          if (rs != REC_OK) {
+            fail_status.store(rs);
+            failed.store(true);
+            return;
+          }
+          L.busy = true;
+          progressed = true;
         }
-        if (rs != REC_OK) {
-          fail_status.store(rs);
-          failed.store(true);
-          return;
+        if (progressed) {
+          idle_polls = 0;
+        } else if (++idle_polls > 64) {
+          std::this_thread::yield();  // batches in flight, nothing queued: let others run
+        } else {
+          cpu_relax();
         }
-        L.busy = true;
       }
     };
     std::vector<std::thread> th;
-    for (int s = 0; s < M; ++s) th.emplace_back(worker, s);
+    for (int t = 0; t < nthreads; ++t) th.emplace_back(worker, t);
     while (a < n && !failed.load()) {
       const double now = now_s() - t0;
-      if (trace[a].arrival_s > now) continue;  // open-loop release: spin until the next arrival
+      if (trace[a].arrival_s > now) {  // open-loop release: spin until the next arrival
+        cpu_relax();
+        continue;
+      }
       std::lock_guard<std::mutex> g(mu);
       while (a < n && trace[a].arrival_s <= now) {
         split_query(trace[a], a, d, fifo);

@@ -106,3 +106,57 @@ def test_policy_validation(model):
         with pytest.raises(RecError) as ei:
             model.rec_serve(tr, 20.0, **kw)
         assert ei.value.status == -1
+
+
+@pytest.mark.parametrize("lanes,nb", [(2, 13), (1, 8)])
+def test_pipeline_matches_slots(lanes, nb):
+    """S-D pipeline lanes (rec_set_pipeline): the CTRs of every batch are bit-identical to the
+    per-stream slot graphs (same kernels, same per-batch buffers), including a remainder
+    group that falls back to the slot graphs, and match the oracle on sampled items."""
+    import torch
+    from paper_2203_07424_b200 import RecModel, rec_split_fuse
+    m = RecModel(CFG, seed=1, max_batch=256, streams=4)
+    tr = W.burst_trace(60, seed=23)
+    segs, bstart = rec_split_fuse(tr, 256)
+    bstart = bstart[:nb + 1]
+    items = int(segs[:bstart[-1], 2].sum())
+    ref = torch.zeros(items, device="cuda")
+    off = 0
+    for b in range(nb):
+        sg = segs[bstart[b]:bstart[b + 1]]
+        n = int(sg[:, 2].sum())
+        m.rec_synth_query_async(b % 4, sg, ref[off:off + n])
+        m.rec_sync(b % 4)
+        off += n
+    m.rec_set_pipeline(lanes)
+    got = torch.full((items,), -1.0, device="cuda")
+    for _ in range(2):  # second pass reuses the lane graphs
+        m.rec_synth_query_pipeline(segs[:bstart[-1]], bstart, got)
+        for k in range(4):
+            m.rec_sync(k)
+        assert np.array_equal(got.cpu().numpy(), ref.cpu().numpy())
+    # back to slot graphs after pipeline mode: same bits
+    sg = segs[bstart[0]:bstart[1]]
+    n0 = int(sg[:, 2].sum())
+    again = torch.zeros(n0, device="cuda")
+    m.rec_synth_query_async(1, sg, again)
+    m.rec_sync(1)
+    assert np.array_equal(again.cpu().numpy(), ref[:n0].cpu().numpy())
+    q, it = gen.expand_segments(segs[:bstart[-1]])
+    pick = np.random.default_rng(5).choice(items, size=24, replace=False)
+    sub = np.array([[q[k], it[k], 1] for k in pick], np.int32)
+    i2, o2, d2 = gen.gen_batch(CFG, 1, sub)
+    exp = fw.forward(CFG, 1, d2, i2, o2)
+    assert np.abs(got.cpu().numpy()[pick] - exp).max() <= 2e-2
+    m.close()
+
+
+def test_pipeline_argument_errors():
+    from paper_2203_07424_b200 import RecModel, RecError
+    m = RecModel(CFG, seed=1, max_batch=64, streams=3)
+    with pytest.raises(RecError):
+        m.rec_set_pipeline(2)          # 3 streams do not split into lanes of >= 2
+    with pytest.raises(RecError):
+        m.rec_synth_query_pipeline(np.array([[0, 0, 4]], np.int32), np.array([0, 1], np.int64))
+    m.rec_set_pipeline(0)
+    m.close()
