@@ -392,6 +392,27 @@ def run_ours(args):
                        "device-synth inputs, replica dispatch q mod G; Alg. 1 gradient search over "
                        "(streams, max_batch)"}
 
+    # MLP tensor-pipe utilisation at a large batch (north_star "MLP TC util"): the same MLP
+    # stacks in a second handle with max_batch = --mlp-batch (tiny tables: SLS not involved)
+    mlp_large = None
+    if args.mlp_batch > 0 and rank == 0:
+        mb = args.mlp_batch
+        mm = RecModel(cfg.with_(rows=1000), seed=1, max_batch=mb, streams=1, device=local)
+        fb = sum(2 * x * y for x, y in zip(cfg.bottom[:-1], cfg.bottom[1:]))
+        wt = [cfg.dim + cfg.num_tables * (cfg.num_tables + 1) // 2] + list(cfg.top)
+        ft = sum(2 * x * y for x, y in zip(wt[:-1], wt[1:]))
+        tb = mm.rec_bench_mlp(0, mb, 20)
+        ti = mm.rec_bench_mlp(2, mb, 20)
+        tt = mm.rec_bench_mlp(1, mb, 20)
+        mm.close()
+        mlp_large = {"batch": mb,
+                     "bottom": {"us": 1e3 * tb, "tflops": fb * mb / (tb * 1e-3) / 1e12,
+                                "frac": fb * mb / (tb * 1e-3) / 1e12 / bf16_peak},
+                     "top": {"us": 1e3 * (tt - ti), "tflops": ft * mb / ((tt - ti) * 1e-3) / 1e12,
+                             "frac": ft * mb / ((tt - ti) * 1e-3) / 1e12 / bf16_peak},
+                     "measured": "rec_bench_mlp: 20 back-to-back launches of each stage on one stream "
+                                 "(CUDA events); top = (interaction + top) - interaction"}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cores = host_cores()
@@ -445,7 +466,9 @@ def run_ours(args):
                                          "(all kernels of the step running on co-located streams)"}},
             "mlp": {"bound": "tensor", "achieved_tflops": gemm_tf, "peak": bf16_peak,
                     "frac": (gemm_tf / bf16_peak) if gemm_tf else None, "flops_per_item": mlp_flops_per_item(cfg),
-                    "launches": gemm_n, "ms": gemm_ms},
+                    "launches": gemm_n, "ms": gemm_ms,
+                    "measured": "per-launch CUDA events in the single-stream pass (batches <= d: "
+                                "latency-bound)", "large_batch": mlp_large},
             "breakdown_us_per_batch_single_stream": {
                 "gen": 1e3 * gen_ms / rsteps, "sls": 1e3 * sls_ms / rsteps,
                 "gemm": 1e3 * gemm_ms / rsteps, "interact": 1e3 * int_ms / rsteps},
@@ -481,6 +504,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=300)
     ap.add_argument("--sla-queries", type=int, default=20000)
     ap.add_argument("--cpu-items", type=int, default=256)
+    ap.add_argument("--mlp-batch", type=int, default=65536, help="large-batch MLP TC probe (0 = off)")
     ap.add_argument("--ref-items", type=int, default=64)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
