@@ -83,7 +83,21 @@ void launch_interact(const float* X, int B, const int* dB, int T, int D, __nv_bf
                          static_cast<int>(smem));
   int blocks = (B + wpc - 1) / wpc;
   if (blocks > 148 * 8) blocks = 148 * 8;
-  k_interact<<<blocks, 32 * wpc, smem, s>>>(X, B, dB, T, D, A_top, ld_top, wpc);
+  if (g_dense_prio == 0) {
+    k_interact<<<blocks, 32 * wpc, smem, s>>>(X, B, dB, T, D, A_top, ld_top, wpc);
+    return;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(blocks);
+  cfg.blockDim = dim3(32 * wpc);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributePriority;
+  at[0].val.priority = g_dense_prio;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k_interact, X, B, dB, T, D, A_top, ld_top, wpc);
 }
 
 }  // namespace rec

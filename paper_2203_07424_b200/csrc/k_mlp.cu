@@ -12,20 +12,27 @@
 //             N-chunk), accumulators in TMEM (N <= 512 columns)
 //   epilogue: + bias, ReLU -> bf16 -> smem (hidden layers); the last layer writes fp32 X
 //             slot 0 (bottom) or folds the width-1 output layer + sigmoid (top -> CTR).
-// Warp roles (192 threads): warp 0 TMA producer, warp 1 single-thread MMA issuer, warps 2-5
-// epilogue (warp w owns TMEM lanes 32*(w%4) .. +31, i.e. tile rows).  No split-K, no atomics:
-// an item's result is independent of its batch (batch invariance).
+// Warp roles (320 threads): warp 0 TMA producer, warp 1 single-thread MMA issuer, warps 2-9
+// epilogue: warp w owns TMEM lanes 32*(w%4) .. +31 (tile rows) and half (w-2)/4 of every
+// layer's 64-column groups, so two warps per SM sub-partition hide each other's TMEM-load,
+// math and shared-store latency.  No split-K, no atomics: an item's result is independent of
+// its batch (batch invariance).
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.h"
 #include "sm100.cuh"
 
 namespace rec {
 
+int g_dense_prio = 0;
+
 constexpr int CBM = 128;
 constexpr int CBK = 64;
 constexpr int C_A_BYTES = CBM * CBK * 2;     // 16 KB: one A k-block (128 rows x 128 B)
-constexpr int C_W_BYTES = 256 * CBK * 2;     // 32 KB: one W k-block of a <= 256-row N-chunk
-constexpr int C_STAGE = C_A_BYTES + C_W_BYTES;
+// ring stage = one A k-block + one W k-block of an N-chunk (nchunk = 128 or 256 rows:
+// 32 KB or 48 KB per stage; chain_configure picks the smallest ring that keeps the CTA's
+// shared memory under the co-location budget, see chain_configure)
 
 __device__ __forceinline__ void fence_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -45,17 +52,23 @@ __device__ __forceinline__ const CUtensorMap* wmap(const ChainMaps& mp, int l) {
   return l == 0 ? &mp.w0 : l == 1 ? &mp.w1 : l == 2 ? &mp.w2 : &mp.w3;
 }
 
-__global__ void __launch_bounds__(192, 1)
+constexpr int C_EPI_THREADS = 256;  // 8 epilogue warps
+constexpr int C_THREADS = 64 + C_EPI_THREADS;
+
+__global__ void __launch_bounds__(C_THREADS, 1)
     k_mlp_chain(const __grid_constant__ ChainMaps maps, const ChainArgs args) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
   const int S = args.stages;
+  const int NCH = args.nchunk;
+  const int C_STAGE = C_A_BYTES + NCH * CBK * 2;
   uint8_t* ring = smem;                                   // S x C_STAGE
   uint8_t* act = smem + S * C_STAGE;                      // act_kblocks x 16 KB
   float* s_bias = reinterpret_cast<float*>(act + args.act_kblocks * C_A_BYTES);  // bias_total
   float* s_wl = s_bias + args.bias_total;                 // [N_last]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(s_wl + args.wl_n + 2);
+  float* s_dot = s_wl + args.wl_n + 2;                    // [128] CTR partial of half 1
+  uint64_t* bars = reinterpret_cast<uint64_t*>(s_dot + CBM);
   uint64_t* full = bars;
   uint64_t* empty = bars + S;
   uint64_t* acc_full = bars + 2 * S;   // MMA -> epilogue, one phase per layer
@@ -75,7 +88,7 @@ __global__ void __launch_bounds__(192, 1)
       sm100::mbar_init(&empty[s], 1);
     }
     sm100::mbar_init(acc_full, 1);
-    sm100::mbar_init(act_ready, 128);
+    sm100::mbar_init(act_ready, C_EPI_THREADS);
     sm100::fence_mbar_init();
     sm100::tma_prefetch_desc(&maps.a0);
     for (int l = 0; l < nl; ++l) sm100::tma_prefetch_desc(wmap(maps, l));
@@ -93,7 +106,7 @@ __global__ void __launch_bounds__(192, 1)
     for (int l = 0; l < nl; ++l) {
       const int K = args.K[l], N = args.N[l];
       const int nkb = (K + CBK - 1) / CBK;
-      for (int n0 = 0; n0 < N; n0 += 256) {
+      for (int n0 = 0; n0 < N; n0 += NCH) {
         const int box_rows = args.wbox[l];
         const uint32_t bytes = (l == 0 ? C_A_BYTES : 0) + box_rows * CBK * 2;
         for (int kb = 0; kb < nkb; ++kb, ++it) {
@@ -120,8 +133,8 @@ __global__ void __launch_bounds__(192, 1)
         sm100::mbar_wait(act_ready, (l - 1) & 1);
         sm100::tc_fence_after();
       }
-      for (int n0 = 0; n0 < N; n0 += 256) {
-        const int nc = min(256, args.wbox[l]);
+      for (int n0 = 0; n0 < N; n0 += NCH) {
+        const int nc = min(NCH, args.wbox[l]);
         const uint32_t idesc = sm100::idesc_bf16_f32(CBM, nc);
         for (int kb = 0; kb < nkb; ++kb, ++it) {
           const int s = it % S, use = it / S;
@@ -136,7 +149,7 @@ __global__ void __launch_bounds__(192, 1)
             for (int k = 0; k < CBK / 16; ++k)
               sm100::mma_bf16_ss(tmem + n0, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
             sm100::mma_commit(&empty[s]);
-            if (kb == nkb - 1 && n0 + 256 >= N) {
+            if (kb == nkb - 1 && n0 + NCH >= N) {
               sm100::mma_commit(acc_full);
               STAMP(4 + l);
             }
@@ -146,12 +159,13 @@ __global__ void __launch_bounds__(192, 1)
       }
     }
   } else {
-    // ------------------------------------------------ epilogue warps 2..5
-    const int et = threadIdx.x - 64;                 // 0..127
-    for (int i = et; i < args.bias_total; i += 128) s_bias[i] = __ldg(&args.bias_all[i]);
+    // ------------------------------------------------ epilogue warps 2..9
+    const int et = threadIdx.x - 64;                 // 0..255
+    const int half = et >> 7;                        // column-group half of this warp
+    for (int i = et; i < args.bias_total; i += C_EPI_THREADS) s_bias[i] = __ldg(&args.bias_all[i]);
     if (args.mode_last == GEMM_OUT_CTR)
-      for (int i = et; i < args.wl_n; i += 128) s_wl[i] = __ldg(&args.w_last[i]);
-    asm volatile("bar.sync 1, 128;" ::: "memory");   // epilogue warps only
+      for (int i = et; i < args.wl_n; i += C_EPI_THREADS) s_wl[i] = __ldg(&args.w_last[i]);
+    asm volatile("bar.sync 1, 256;" ::: "memory");   // epilogue warps only
     const int qw = warp & 3;                         // TMEM lane quarter of this warp
     const int r = qw * 32 + lane;                    // tile row
     const int row = m0 + r;
@@ -169,9 +183,8 @@ __global__ void __launch_bounds__(192, 1)
       // 64 columns per round: four tcgen05.ld (16 columns each) in flight, ONE wait, then the
       // math / stores of all four (a wait per 16 columns serialised the epilogue).
 #pragma unroll 1
-      for (int g0 = 0; g0 < cols; g0 += 64) {
+      for (int g0 = 64 * half; g0 < cols; g0 += 128) {
         uint32_t rr[4][16];
-#pragma unroll
         if (args.dbg_mode & 1) {
 #pragma unroll
           for (int q = 0; q < 4; ++q)
@@ -236,10 +249,15 @@ __global__ void __launch_bounds__(192, 1)
         fence_async_smem();          // generic-proxy smem writes -> visible to tcgen05.mma
         sm100::tc_fence_before();    // our tcgen05.ld of this layer are complete
         sm100::mbar_arrive(act_ready);
-      } else if (args.mode_last == GEMM_OUT_CTR && row_ok) {
-        const float logit = dot + args.b_last;
-        args.ctr[row] = 1.f / (1.f + __expf(-logit));
-        if (args.logit) args.logit[row] = logit;
+      } else if (args.mode_last == GEMM_OUT_CTR) {
+        // the two halves' partial dots meet in smem: CTR = sigmoid(d_half0 + d_half1 + b)
+        if (half == 1) s_dot[r] = dot;
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+        if (half == 0 && row_ok) {
+          const float logit = (dot + s_dot[r]) + args.b_last;
+          args.ctr[row] = 1.f / (1.f + __expf(-logit));
+          if (args.logit) args.logit[row] = logit;
+        }
       }
     }
   }
@@ -250,15 +268,34 @@ __global__ void __launch_bounds__(192, 1)
 }
 
 size_t chain_smem_bytes(const ChainArgs& a) {
-  return 1024 + static_cast<size_t>(a.stages) * C_STAGE + static_cast<size_t>(a.act_kblocks) * C_A_BYTES +
-         sizeof(float) * (a.bias_total + a.wl_n + 2) + 8 * (2 * a.stages + 4);
+  return 1024 + static_cast<size_t>(a.stages) * (C_A_BYTES + a.nchunk * CBK * 2) +
+         static_cast<size_t>(a.act_kblocks) * C_A_BYTES +
+         sizeof(float) * (a.bias_total + a.wl_n + 2 + CBM) + 8 * (2 * a.stages + 4);
 }
 
 bool chain_configure(ChainArgs& a) {
-  // stages: as many as fit next to the activation buffer (>= 2)
-  for (int s = 4; s >= 2; --s) {
-    a.stages = s;
-    if (chain_smem_bytes(a) <= 227 * 1024) return true;
+  // Shared-memory budget: a chain CTA co-resides with SLS CTAs of other co-located streams;
+  // every KB of shared memory it takes is carved out of those SMs' L1, which the SLS gathers
+  // need for their in-flight rows (measured: 208 KB chains cost 7 % RMC1 throughput vs
+  // <= 160 KB).  Prefer the fastest ring within REC_CHAIN_SMEM KB (default 132), else the
+  // smallest ring that fits at all.
+  int budget = 132;
+  if (const char* e = getenv("REC_CHAIN_SMEM")) budget = atoi(e);
+  int smax = 4;
+  if (const char* e = getenv("REC_CHAIN_STAGES")) smax = atoi(e) < 2 ? 2 : atoi(e) > 4 ? 4 : atoi(e);
+  for (int nch : {256, 128}) {
+    for (int s = smax; s >= 2; --s) {
+      a.stages = s;
+      a.nchunk = nch;
+      if (chain_smem_bytes(a) <= static_cast<size_t>(budget) * 1024) return true;
+    }
+  }
+  for (int nch : {256, 128}) {
+    for (int s = smax; s >= 2; --s) {
+      a.stages = s;
+      a.nchunk = nch;
+      if (chain_smem_bytes(a) <= 227 * 1024) return true;
+    }
   }
   return false;
 }
@@ -270,7 +307,21 @@ void chain_prepare() {
 void launch_mlp_chain(const ChainMaps& maps, const ChainArgs& a, cudaStream_t s) {
   if (a.M <= 0) return;
   const size_t smem = chain_smem_bytes(a);
-  k_mlp_chain<<<(a.M + CBM - 1) / CBM, 192, smem, s>>>(maps, a);
+  if (g_dense_prio == 0) {
+    k_mlp_chain<<<(a.M + CBM - 1) / CBM, C_THREADS, smem, s>>>(maps, a);
+    return;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((a.M + CBM - 1) / CBM);
+  cfg.blockDim = dim3(C_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributePriority;
+  at[0].val.priority = g_dense_prio;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k_mlp_chain, maps, a);
 }
 
 }  // namespace rec

@@ -47,6 +47,8 @@ __device__ unsigned long long g_sls_tl[4 * 65536];
 
 namespace rec {
 
+int g_sls_prio = 0;
+
 // Streaming 128-bit load of row `row` (address = base + row * stride_bytes, formed inside the
 // asm so no 64-bit address stays live per in-flight load; rows are never reused from L1).
 __device__ __forceinline__ float4 ldg_row(const float4* base, uint32_t row, uint32_t stride_bytes) {
@@ -408,12 +410,14 @@ void launch_sls_synth(const SegBatch& sb, const SlsSynthArgs& a, cudaStream_t s)
   cfg.blockDim = block;
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = a.pdl;
+  at[1].id = cudaLaunchAttributePriority;
+  at[1].val.priority = g_sls_prio;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
-  if (a.pdl) cudaLaunchKernelExC(&cfg, fn, args);
+  cfg.numAttrs = g_sls_prio ? 2 : 1;
+  if (a.pdl || g_sls_prio) cudaLaunchKernelExC(&cfg, fn, args);
   else cudaLaunchKernel(fn, grid, block, args, smem, s);
 }
 
@@ -429,8 +433,7 @@ static void launch_l(const float* tables, const int64_t* tab_off, int64_t row_st
       flag, row_lo, row_hi);
 }
 
-void set_max_smem_carveout() {
-  const int c = cudaSharedmemCarveoutMaxShared;
+void set_max_smem_carveout(int c) {
   cudaFuncSetAttribute(k_sls<8, 128>, cudaFuncAttributePreferredSharedMemoryCarveout, c);
   cudaFuncSetAttribute(k_sls<16, 128>, cudaFuncAttributePreferredSharedMemoryCarveout, c);
   cudaFuncSetAttribute(k_sls<32, 128>, cudaFuncAttributePreferredSharedMemoryCarveout, c);

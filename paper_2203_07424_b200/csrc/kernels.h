@@ -51,7 +51,7 @@ void launch_gen_variable_rest(const GenArgs& ga, cudaStream_t s);
 void launch_dense_to_bf16(const float* dense, int B, int F, int Fpad, __nv_bfloat16* out,
                           cudaStream_t s);
 void launch_check_offsets(const int* offsets, int nbags, int* flag, cudaStream_t s);
-void set_max_smem_carveout();  // prefer the max shared-memory carveout for every kernel
+void set_max_smem_carveout(int percent);  // SLS kernels' preferred shared-memory carveout (0..100)
 
 // ------------------------------------------------------------------------- SLS (a3)
 // Row r of table t lives at tables + tab_off[t] + r * row_stride (floats).
@@ -140,6 +140,7 @@ struct ChainArgs {
   int act_kblocks;        // 64-column blocks of the widest hidden activation
   int tmem_cols;          // power of two >= 32 and >= max N
   int stages;             // set by chain_configure
+  int nchunk;             // N-chunk rows per MMA / weight box (128 or 256), set by chain_configure
   unsigned long long* dbg;  // diagnostic: %globaltimer stamps of CTA 0 (nullptr = off)
   int dbg_mode;             // diagnostic: bit0 skip TMEM loads, bit1 skip hidden smem stores
 };
@@ -147,6 +148,10 @@ size_t chain_smem_bytes(const ChainArgs& a);
 bool chain_configure(ChainArgs& a);   // false: does not fit in shared memory
 void chain_prepare();                 // per-device kernel attribute
 void launch_mlp_chain(const ChainMaps& maps, const ChainArgs& a, cudaStream_t s);
+// Scheduling priority given to the dense-stage kernels (fused MLPs, interaction) through the
+// launch attribute (0 = stream default).  Experiment knob (REC_PRIO).
+extern int g_dense_prio;
+extern int g_sls_prio;  // same for the synthetic-index SLS
 
 // --------------------------------------------------------------- interaction (a5)
 void launch_interact(const float* X, int B, const int* dB, int T, int D, __nv_bfloat16* A_top,

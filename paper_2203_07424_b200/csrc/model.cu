@@ -321,7 +321,12 @@ static rec_status synth_chain(rec_model_s* m, Workspace& w, SynthSlot& sl, bool 
     mark(gev, 2, s);
     REC_CUDA(cudaStreamWaitEvent(s, w.ev_join, 0));
     mark(gev, 3, s);
-    if (!(m->diag_skip & 2)) enqueue_interact_top(m, w, s, w.cap, w.dB, w.ctr, w.logit, gev);
+    if (!(m->diag_skip & 2)) {
+      enqueue_interact_top(m, w, s, w.cap, w.dB, w.ctr, w.logit, gev);
+    } else {
+      mark(gev, 4, s);
+      mark(gev, 5, s);
+    }
     cudaError_t err = cudaGetLastError();
     if (err != cudaSuccess) return cuda_fail(err, "synthetic chain launch");
     return REC_OK;
@@ -363,7 +368,7 @@ rec_status capture_graphs(rec_model_s* m, Workspace& w) {
       if (st != REC_OK) return st;
       if (ce != cudaSuccess) return cuda_fail(ce, "cudaStreamEndCapture");
       V.graph = g;
-      ce = cudaGraphInstantiate(&V.exec, g, 0);
+      ce = cudaGraphInstantiate(&V.exec, g, cudaGraphInstantiateFlagUseNodePriority);
       if (ce != cudaSuccess) return cuda_fail(ce, "cudaGraphInstantiate");
       w.graph_kernels = static_cast<int>(m->launches - before);
       m->launches = before;
@@ -855,7 +860,7 @@ rec_status rec_model_create(const rec_model_desc* d, rec_model_t* out) {
   chain_prepare();
   {
     const char* e = getenv("REC_CARVEOUT");
-    if (e && e[0] == 'm') set_max_smem_carveout();  // experiment: never reconfigure smem/L1
+    if (e) set_max_smem_carveout(e[0] == 'm' ? 100 : atoi(e));  // experiment: SLS carveout %
   }
 
   rec_model_s* m = new rec_model_s();
@@ -950,6 +955,12 @@ rec_status rec_model_create(const rec_model_desc* d, rec_model_t* out) {
     // diagnostic only (REC_STEP_DIAG, never set by tests or bench): bit 0 drops the bottom
     // MLP, bit 1 the interaction + top MLP from the synthetic step graphs (CTRs invalid)
     if (const char* d = getenv("REC_STEP_DIAG")) m->diag_skip = atoi(d);
+    if (const char* pr = getenv("REC_PRIO")) {
+      int lo = 0, hi = 0;
+      cudaDeviceGetStreamPriorityRange(&lo, &hi);
+      g_dense_prio = atoi(pr) > 0 ? hi : 0;
+      g_sls_prio = atoi(pr) < 0 ? hi : 0;
+    }
     const char* p = getenv("REC_PDL");
     m->sls_pdl = !(p && strcmp(p, "0") == 0);
     CHECK_CUDA_CREATE(cudaDeviceGetAttribute(&m->nsm, cudaDevAttrMultiProcessorCount, m->device));
@@ -982,6 +993,10 @@ rec_status rec_model_create(const rec_model_desc* d, rec_model_t* out) {
       return REC_E_OOM;
     }
     launch_init_layer(L.W, L.bias, N, K, L.Kpad, layer_id, L.exp, m->k0, m->k1, 0);
+    if (!encode_tmap_bf16(&L.tmap_w128, L.W, N, K, L.Kpad, std::min(L.bn, 128))) {
+      set_error("cuTensorMapEncodeTiled failed for layer %d weights", layer_id);
+      return REC_E_CUDA;
+    }
     if (!encode_tmap_bf16(&L.tmap_w, L.W, N, K, L.Kpad, L.bn)) {
       set_error("cuTensorMapEncodeTiled failed for layer %d weights", layer_id);
       return REC_E_CUDA;
@@ -1049,6 +1064,7 @@ rec_status rec_model_create(const rec_model_desc* d, rec_model_t* out) {
       ca.mode_last = mode;
       ca.wl_n = mode == GEMM_OUT_CTR ? Ls[nl - 1].N : 0;
       if (!chain_configure(ca)) return false;
+      for (int l = 0; l < nl; ++l) ca.wbox[l] = std::min(Ls[l].bn, ca.nchunk);
       if (cudaMalloc(reinterpret_cast<void**>(bias_all), sizeof(float) * total) != cudaSuccess) return false;
       int off = 0;
       for (int l = 0; l < nl; ++l) {
@@ -1139,13 +1155,16 @@ rec_status rec_model_create(const rec_model_desc* d, rec_model_t* out) {
       }
       w.out_top[j] = (j == ntl - 1) ? nullptr : static_cast<void*>(w.h[j & 1]);
     }
-    auto fill_maps = [&](ChainMaps& mp, const CUtensorMap& a0, std::vector<rec::Layer>& Ls) {
+    auto fill_maps = [&](ChainMaps& mp, const CUtensorMap& a0, std::vector<rec::Layer>& Ls, int nch) {
       mp.a0 = a0;
       CUtensorMap* ws_[4] = {&mp.w0, &mp.w1, &mp.w2, &mp.w3};
-      for (int l = 0; l < 4; ++l) *ws_[l] = Ls[std::min<int>(l, static_cast<int>(Ls.size()) - 1)].tmap_w;
+      for (int l = 0; l < 4; ++l) {
+        const rec::Layer& L = Ls[std::min<int>(l, static_cast<int>(Ls.size()) - 1)];
+        *ws_[l] = nch == 128 ? L.tmap_w128 : L.tmap_w;
+      }
     };
-    fill_maps(w.chain_bottom, w.tmap_a_bottom[0], m->bottom);
-    fill_maps(w.chain_top, w.tmap_a_top[0], m->top);
+    fill_maps(w.chain_bottom, w.tmap_a_bottom[0], m->bottom, m->chain_bottom_args.nchunk);
+    fill_maps(w.chain_top, w.tmap_a_top[0], m->top, m->chain_top_args.nchunk);
   }
   // synthetic-batch staging ring + one captured CUDA graph per slot (a2-a6 chain)
   constexpr int kSlots = 4;

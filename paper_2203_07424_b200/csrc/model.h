@@ -29,6 +29,7 @@ struct Layer {
   __nv_bfloat16* W = nullptr;                    // [N][Kpad] bf16
   float* bias = nullptr;                         // [N]
   CUtensorMap tmap_w;
+  CUtensorMap tmap_w128;                         // box rows min(bn, 128) (fused MLP, 128-row chunks)
 };
 
 // A staging slot of device-synthesised batches: the batch descriptor (kernel parameters of

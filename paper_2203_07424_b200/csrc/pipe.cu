@@ -119,7 +119,7 @@ static rec_status pipe_capture(rec_model_s* m, PipeLane& L) {
   }
   if (ce != cudaSuccess) return cuda_fail(ce, "cudaStreamEndCapture (pipeline)");
   L.graph = g;
-  ce = cudaGraphInstantiate(&L.exec, g, 0);
+  ce = cudaGraphInstantiate(&L.exec, g, cudaGraphInstantiateFlagUseNodePriority);
   if (ce != cudaSuccess) return cuda_fail(ce, "cudaGraphInstantiate (pipeline)");
   return REC_OK;
 }
