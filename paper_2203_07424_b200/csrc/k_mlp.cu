@@ -52,10 +52,21 @@ __device__ __forceinline__ const CUtensorMap* wmap(const ChainMaps& mp, int l) {
   return l == 0 ? &mp.w0 : l == 1 ? &mp.w1 : l == 2 ? &mp.w2 : &mp.w3;
 }
 
-constexpr int C_EPI_THREADS = 256;  // 8 epilogue warps
+#ifndef REC_CHAIN_EPI_WARPS
+#define REC_CHAIN_EPI_WARPS 8  // 4 or 8 (A/B: register footprint vs epilogue latency)
+#endif
+constexpr int C_EPI_THREADS = 32 * REC_CHAIN_EPI_WARPS;
+constexpr int C_HALVES = C_EPI_THREADS / 128;  // warps per TMEM lane quarter
+#ifndef REC_CHAIN_Q
+#define REC_CHAIN_Q 2  // tcgen05.ld x16 in flight per wait (2: 32 columns; 4: 64 columns, +50 regs)
+#endif
+constexpr int C_Q = REC_CHAIN_Q;
+#ifndef REC_CHAIN_MINB
+#define REC_CHAIN_MINB 1
+#endif
 constexpr int C_THREADS = 64 + C_EPI_THREADS;
 
-__global__ void __launch_bounds__(C_THREADS, 1)
+__global__ void __launch_bounds__(C_THREADS, REC_CHAIN_MINB)
     k_mlp_chain(const __grid_constant__ ChainMaps maps, const ChainArgs args) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -165,7 +176,7 @@ __global__ void __launch_bounds__(C_THREADS, 1)
     for (int i = et; i < args.bias_total; i += C_EPI_THREADS) s_bias[i] = __ldg(&args.bias_all[i]);
     if (args.mode_last == GEMM_OUT_CTR)
       for (int i = et; i < args.wl_n; i += C_EPI_THREADS) s_wl[i] = __ldg(&args.w_last[i]);
-    asm volatile("bar.sync 1, 256;" ::: "memory");   // epilogue warps only
+    asm volatile("bar.sync 1, %0;" ::"n"(C_EPI_THREADS) : "memory");   // epilogue warps only
     const int qw = warp & 3;                         // TMEM lane quarter of this warp
     const int r = qw * 32 + lane;                    // tile row
     const int row = m0 + r;
@@ -183,21 +194,23 @@ __global__ void __launch_bounds__(C_THREADS, 1)
       // 64 columns per round: four tcgen05.ld (16 columns each) in flight, ONE wait, then the
       // math / stores of all four (a wait per 16 columns serialised the epilogue).
 #pragma unroll 1
-      for (int g0 = 64 * half; g0 < cols; g0 += 128) {
-        uint32_t rr[4][16];
+      for (int gg = 64 * half; gg < cols; gg += 64 * C_HALVES) {
+#pragma unroll 1
+      for (int g0 = gg; g0 < gg + 64 && g0 < cols; g0 += 16 * C_Q) {
+        uint32_t rr[C_Q][16];
         if (args.dbg_mode & 1) {
 #pragma unroll
-          for (int q = 0; q < 4; ++q)
+          for (int q = 0; q < C_Q; ++q)
 #pragma unroll
             for (int j = 0; j < 16; ++j) rr[q][j] = 0u;
         } else {
 #pragma unroll
-          for (int q = 0; q < 4; ++q)
+          for (int q = 0; q < C_Q; ++q)
             if (g0 + 16 * q < N) sm100::tmem_ld_32x32b_x16(trow + g0 + 16 * q, rr[q]);
           sm100::tmem_ld_wait();
         }
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
+        for (int q = 0; q < C_Q; ++q) {
           const int c0 = g0 + 16 * q;
           if (c0 >= cols) break;
           float v[16];
@@ -243,6 +256,7 @@ __global__ void __launch_bounds__(C_THREADS, 1)
           }
         }
       }
+      }
       boff += N;
       if (et == 0) STAMP(9 + 2 * l);
       if (!last) {
@@ -251,10 +265,12 @@ __global__ void __launch_bounds__(C_THREADS, 1)
         sm100::mbar_arrive(act_ready);
       } else if (args.mode_last == GEMM_OUT_CTR) {
         // the two halves' partial dots meet in smem: CTR = sigmoid(d_half0 + d_half1 + b)
-        if (half == 1) s_dot[r] = dot;
-        asm volatile("bar.sync 1, 256;" ::: "memory");
+        if (C_HALVES > 1) {
+          if (half == 1) s_dot[r] = dot;
+          asm volatile("bar.sync 1, %0;" ::"n"(C_EPI_THREADS) : "memory");
+        }
         if (half == 0 && row_ok) {
-          const float logit = (dot + s_dot[r]) + args.b_last;
+          const float logit = (C_HALVES > 1 ? dot + s_dot[r] : dot) + args.b_last;
           args.ctr[row] = 1.f / (1.f + __expf(-logit));
           if (args.logit) args.logit[row] = logit;
         }
