@@ -293,8 +293,7 @@ bool chain_configure(ChainArgs& a) {
   // Shared-memory budget: a chain CTA co-resides with SLS CTAs of other co-located streams;
   // every KB of shared memory it takes is carved out of those SMs' L1, which the SLS gathers
   // need for their in-flight rows (measured: 208 KB chains cost 7 % RMC1 throughput vs
-  // <= 160 KB).  Prefer the fastest ring within REC_CHAIN_SMEM KB (default 132), else the
-  // smallest ring that fits at all.
+  // <= 160 KB).  Pick the fastest ring within REC_CHAIN_SMEM KB (default 132).
   int budget = 132;
   if (const char* e = getenv("REC_CHAIN_SMEM")) budget = atoi(e);
   int smax = 4;
@@ -306,6 +305,11 @@ bool chain_configure(ChainArgs& a) {
       if (chain_smem_bytes(a) <= static_cast<size_t>(budget) * 1024) return true;
     }
   }
+  // Over budget: per-layer GEMMs instead (measured on RMC3: a 192-KB bottom chain with the
+  // 2560-wide layer runs 8 CTAs for 80 us at B = 1024 and costs 13 % co-located throughput
+  // against the per-layer kernels).  REC_CHAIN_STRICT=0 keeps any chain that fits 227 KB.
+  const char* strict = getenv("REC_CHAIN_STRICT");
+  if (!strict || atoi(strict)) return false;
   for (int nch : {256, 128}) {
     for (int s = smax; s >= 2; --s) {
       a.stages = s;
