@@ -77,6 +77,10 @@ struct SlsSynthArgs {
   float* X;
   int x_stride;
   int* dB;
+  // optional fused dense-feature generation (a2 for the bottom MLP): bf16 [cap][Fpad] rows,
+  // written by the table-0 bag groups at the end of the kernel (nullptr: not fused)
+  __nv_bfloat16* dense_bf;
+  int F, Fpad;
   // TMA row-gather variant (REC_SLS=tma): map over the arena as [rows_total][D] fp32 rows
   // (device copy, 64-B aligned), arena row of (t, r) = tab_off[t] / D + r * row_stride / D.
   const CUtensorMap* tmap_rows;

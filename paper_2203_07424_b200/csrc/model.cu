@@ -259,6 +259,9 @@ void fill_genargs(rec_model_s* m, Workspace& w, GenArgs& ga, SlsSynthArgs& sa,
   sa.X = w.X;
   sa.x_stride = (m->T + 1) * m->D;
   sa.dB = w.dB;
+  sa.dense_bf = m->fuse_dense ? w.dense_bf : nullptr;
+  sa.F = m->F;
+  sa.Fpad = m->Fpad;
   sa.tma = m->sls_tma;
   sa.pdl = m->sls_pdl && !sa.tma;
   sa.tmap_rows = m->d_tmap_rows;
@@ -285,6 +288,32 @@ static rec_status synth_chain(rec_model_s* m, Workspace& w, SynthSlot& sl, bool 
   cudaStream_t s = w.stream, sb = w.stream_b;
   cudaEvent_t* gev = capture && with_events ? sl.ev : nullptr;
   mark(gev, 0, s);
+  if (!materialize && m->lo == m->hi && m->fuse_dense) {
+    // dense features generated inside the SLS kernel: one stream, SLS -> bottom -> top
+    mark(gev, 1, s);
+    cudaEvent_t e0 = gev ? nullptr : prof_begin(m, s);
+    launch_sls_synth(*sl.sb, sl.sa, s);
+    prof_end(m, s, 0, e0);
+    if (capture) {
+      size_t n = 0;
+      const cudaGraphNode_t* d = last_node(s, &n);
+      if (n != 1) {
+        set_error("graph capture: SLS node not found");
+        return REC_E_CUDA;
+      }
+      *sl.cap_gen = d[0];
+    }
+    m->launches += 1;
+    mark(gev, 2, s);
+    mark(gev, 6, s);
+    enqueue_bottom(m, w, s, w.cap, w.dB, gev);
+    mark(gev, 7, s);
+    mark(gev, 3, s);
+    enqueue_interact_top(m, w, s, w.cap, w.dB, w.ctr, w.logit, gev);
+    cudaError_t err = cudaGetLastError();
+    if (err != cudaSuccess) return cuda_fail(err, "synthetic chain launch");
+    return REC_OK;
+  }
   if (!materialize && m->lo == m->hi) {
     REC_CUDA(cudaEventRecord(w.ev_fork, s));
     REC_CUDA(cudaStreamWaitEvent(sb, w.ev_fork, 0));
@@ -470,7 +499,7 @@ rec_status synth_submit(rec_model_s* m, Workspace& w, const int32_t* segs, int n
     kp.blockDim = block;
     kp.kernelParams = args_a;
     REC_CUDA(cudaGraphExecKernelNodeSetParams(V.exec, V.gen_node, &kp));
-    if (fused) {
+    if (fused && V.dense_node) {
       cudaKernelNodeParams kd{};
       void* args_d[2] = {sl.sb, &sl.ga};
       kd.func = gen_dense_seg_kernel(sl.ga, &grid, &block);
@@ -961,6 +990,7 @@ rec_status rec_model_create(const rec_model_desc* d, rec_model_t* out) {
       g_dense_prio = atoi(pr) > 0 ? hi : 0;
       g_sls_prio = atoi(pr) < 0 ? hi : 0;
     }
+    if (const char* fd = getenv("REC_FUSE_DENSE")) m->fuse_dense = atoi(fd) != 0;
     const char* p = getenv("REC_PDL");
     m->sls_pdl = !(p && strcmp(p, "0") == 0);
     CHECK_CUDA_CREATE(cudaDeviceGetAttribute(&m->nsm, cudaDevAttrMultiProcessorCount, m->device));

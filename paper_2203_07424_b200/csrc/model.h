@@ -137,6 +137,7 @@ struct rec_model_s {
   CUtensorMap* d_tmap_rows = nullptr;
   int sls_tma = 0, nsm = 0;
   int sls_pdl = 1;    // REC_PDL=0 disables programmatic dependent launch of the SLS
+  int fuse_dense = 0;  // dense features generated by the SLS kernel (REC_FUSE_DENSE)
   int diag_skip = 0;  // REC_STEP_DIAG (diagnostic): stages dropped from the synthetic step
   // MLP
   std::vector<rec::Layer> bottom, top;  // top excludes the width-1 output layer
