@@ -502,7 +502,7 @@ def main():
     ap.add_argument("--sls-batches", type=int, default=1000, help="batches in the back-to-back SLS pass")
     ap.add_argument("--queries", type=int, default=20000)
     ap.add_argument("--e2e-steps", type=int, default=300)
-    ap.add_argument("--sla-queries", type=int, default=20000)
+    ap.add_argument("--sla-queries", type=int, default=100000)
     ap.add_argument("--cpu-items", type=int, default=256)
     ap.add_argument("--mlp-batch", type=int, default=65536, help="large-batch MLP TC probe (0 = off)")
     ap.add_argument("--ref-items", type=int, default=64)
