@@ -49,6 +49,31 @@ namespace rec {
 
 int g_sls_prio = 0;
 
+// Same load with an explicit L2 eviction-priority policy (createpolicy): the hot-row prefix
+// is read evict_last, everything else evict_first, so hot rows stay L2-resident under the
+// streaming gather (the access-policy window does not govern these non-coherent loads).
+__device__ __forceinline__ float4 ldg_row_pol(const float4* base, uint32_t row, uint32_t stride_bytes,
+                                              uint64_t pol) {
+  float4 v;
+  asm volatile(
+      "{\n\t.reg .u64 a;\n\t"
+      "mad.wide.u32 a, %4, %5, %6;\n\t"
+      "ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [a], %7;\n\t}"
+      : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+      : "r"(row), "r"(stride_bytes), "l"(base), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
 // Streaming 128-bit load of row `row` (address = base + row * stride_bytes, formed inside the
 // asm so no 64-bit address stays live per in-flight load; rows are never reused from L1).
 __device__ __forceinline__ float4 ldg_row(const float4* base, uint32_t row, uint32_t stride_bytes) {
@@ -170,7 +195,7 @@ __global__ void __launch_bounds__(THREADS, REC_SLS_MINB) k_sls(const float* __re
 // accumulate structure, but lane `sub` computes the index of slot base + sub with Philox
 // (G2) instead of loading it, so the kernel has no predecessor in the chain and
 // no dependent index load in front of its first row loads.
-template <int LANES, int THREADS, int RIF>
+template <int LANES, int THREADS, int RIF, bool HOT = false>
 __global__ void __launch_bounds__(THREADS, REC_SLS_MINB) k_sls_synth(const __grid_constant__ SegBatch sb,
                                                                         const SlsSynthArgs a) {
   using S = SlsShape<LANES, RIF>;
@@ -198,6 +223,11 @@ __global__ void __launch_bounds__(THREADS, REC_SLS_MINB) k_sls_synth(const __gri
                                        : (((1u << LANES) - 1u) << ((threadIdx.x & 31) & ~(LANES - 1)));
   const int L = a.L;
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  uint64_t pol_hot = 0, pol_cold = 0;
+  if (HOT) {
+    pol_hot = l2_policy_evict_last();
+    pol_cold = l2_policy_evict_first();
+  }
   int cur[S::IPL];
 #pragma unroll
   for (int q = 0; q < S::IPL; ++q) {
@@ -215,7 +245,10 @@ __global__ void __launch_bounds__(THREADS, REC_SLS_MINB) k_sls_synth(const __gri
       for (int k = 0; k < S::U; ++k) {
         const int r = kk + k;
         const int rr = __shfl_sync(gmask, cur[r / LANES], r % LANES, LANES);
-        if (r < n) v[k] = ldg_row(tab, static_cast<uint32_t>(rr), stride_bytes);
+        if (r < n)
+          v[k] = HOT ? ldg_row_pol(tab, static_cast<uint32_t>(rr), stride_bytes,
+                                   rr < a.hot_rows ? pol_hot : pol_cold)
+                     : ldg_row(tab, static_cast<uint32_t>(rr), stride_bytes);
       }
       if (kk + S::U >= S::ROWS) {  // next round's indices, computed while the rows are in flight
 #pragma unroll
@@ -401,6 +434,11 @@ void* sls_synth_kernel(const SlsSynthArgs& a, dim3* grid, dim3* block, size_t* s
   *grid = dim3((nb + THREADS / L - 1) / (THREADS / L));
   *block = dim3(THREADS);
   if (smem) *smem = 0;
+  if (a.hot_rows > 0) {
+    if (L == 8) return reinterpret_cast<void*>(k_sls_synth<8, THREADS, REC_SLS_RIF, true>);
+    if (L == 16) return reinterpret_cast<void*>(k_sls_synth<16, THREADS, REC_SLS_RIF, true>);
+    return reinterpret_cast<void*>(k_sls_synth<32, THREADS, REC_SLS_RIF, true>);
+  }
   if (L == 8) return reinterpret_cast<void*>(k_sls_synth<8, THREADS, REC_SLS_RIF>);
   if (L == 16) return reinterpret_cast<void*>(k_sls_synth<16, THREADS, REC_SLS_RIF>);
   return reinterpret_cast<void*>(k_sls_synth<32, THREADS, REC_SLS_RIF>);

@@ -77,6 +77,10 @@ struct SlsSynthArgs {
   float* X;
   int x_stride;
   int* dB;
+  // hot-row residency: rows r < hot_rows of every table are loaded with an L2 evict_last
+  // policy, all others evict_first (0 = plain loads); the interleaved arena makes these rows
+  // one contiguous prefix of hot_rows * T * D * 4 bytes
+  int hot_rows;
   // optional fused dense-feature generation (a2 for the bottom MLP): bf16 [cap][Fpad] rows,
   // written by the table-0 bag groups at the end of the kernel (nullptr: not fused)
   __nv_bfloat16* dense_bf;

@@ -259,6 +259,14 @@ void fill_genargs(rec_model_s* m, Workspace& w, GenArgs& ga, SlsSynthArgs& sa,
   sa.X = w.X;
   sa.x_stride = (m->T + 1) * m->D;
   sa.dB = w.dB;
+  sa.hot_rows = 0;
+  if (m->l2_persist_bytes > 0 && m->interleaved && !(m->shard == REC_SHARD_ROW && m->world > 1))
+    sa.hot_rows = static_cast<int>(std::min<int64_t>(
+        m->l2_persist_bytes / (static_cast<int64_t>(m->T_loc) * m->D * 4), m->rows[m->t0]));
+  {  // per-load hints are opt-in: measured slower than the window alone
+    const char* e = getenv("REC_HOT_POLICY");
+    if (!e || !atoi(e)) sa.hot_rows = 0;
+  }
   sa.dense_bf = m->fuse_dense ? w.dense_bf : nullptr;
   sa.F = m->F;
   sa.Fpad = m->Fpad;
@@ -1223,13 +1231,15 @@ rec_status rec_model_create(const rec_model_desc* d, rec_model_t* out) {
     }
     size_t win = std::min<size_t>(static_cast<size_t>(m->l2_persist_bytes), m->table_bytes);
     win = std::min<size_t>(win, static_cast<size_t>(prop.accessPolicyMaxWindowSize));
-    CHECK_CUDA_CREATE(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize,
-                                         std::min<size_t>(win, prop.persistingL2CacheMaxSize)));
+    const size_t carve = std::min<size_t>(win, prop.persistingL2CacheMaxSize);
+    CHECK_CUDA_CREATE(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, carve));
     for (auto& w : m->ws) {
       cudaStreamAttrValue v{};
       v.accessPolicyWindow.base_ptr = m->tables;
       v.accessPolicyWindow.num_bytes = win;
-      v.accessPolicyWindow.hitRatio = 1.0f;
+      // a window larger than the persisting carve-out would thrash it: persist a random
+      // carve/win fraction of the window's lines (the rest stream)
+      v.accessPolicyWindow.hitRatio = static_cast<float>(std::min(1.0, double(carve) / double(win)));
       v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
       v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
       CHECK_CUDA_CREATE(cudaStreamSetAttribute(w.stream, cudaStreamAttributeAccessPolicyWindow, &v));
