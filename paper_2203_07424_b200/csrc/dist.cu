@@ -19,7 +19,10 @@
 // value mode (G4), within the SLS tolerance otherwise.
 #include <nccl.h>
 
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <vector>
 
 #include "model.h"
 
@@ -44,7 +47,100 @@ rec_status dist_init(rec_model_s* m, const void* nccl_id) {
   ncclComm_t comm = nullptr;
   REC_NCCL(ncclCommInitRank(&comm, m->world, id, m->rank));
   m->nccl_comm = comm;
-  return sharded_alloc(m);
+  rec_status st = sharded_alloc(m);
+  if (st != REC_OK) return st;
+  return p2p_init(m);
+}
+
+// Fused table-wise exchange: map every peer's X buffer and arrival flags into
+// this process (CUDA IPC; handles exchanged with one ncclAllGather) so the SLS kernel stores
+// pooled vectors straight into the owning rank's X over NVLink.  Off with REC_P2P=0, for the
+// row-wise mode, or when some pair of GPUs has no peer access (NCCL path then).
+rec_status p2p_init(rec_model_s* m) {
+  const char* e = getenv("REC_P2P");
+  if (m->shard == REC_SHARD_REPLICA || (e && atoi(e) == 0)) return REC_OK;
+  const int G = m->world;
+  // peer access: every rank must reach every other rank's memory
+  int ok = 1;
+  {
+    int ndev = 0;
+    REC_CUDA(cudaGetDeviceCount(&ndev));
+    std::vector<int> devs(G, -1);
+    // each rank contributes its device ordinal (same box: ordinals are comparable)
+    int* d = nullptr;
+    REC_CUDA(cudaMalloc(reinterpret_cast<void**>(&d), sizeof(int) * (G + 1)));
+    REC_CUDA(cudaMemcpy(d + G, &m->device, sizeof(int), cudaMemcpyHostToDevice));
+    ncclComm_t comm = static_cast<ncclComm_t>(m->nccl_comm);
+    REC_NCCL(ncclAllGather(d + G, d, 1, ncclInt32, comm, m->ws[0].stream));
+    REC_CUDA(cudaStreamSynchronize(m->ws[0].stream));
+    REC_CUDA(cudaMemcpy(devs.data(), d, sizeof(int) * G, cudaMemcpyDeviceToHost));
+    cudaFree(d);
+    for (int q = 0; q < G; ++q) {
+      if (q == m->rank) continue;
+      int can = 0;
+      if (devs[q] < 0 || devs[q] >= ndev || devs[q] == m->device ||
+          cudaDeviceCanAccessPeer(&can, m->device, devs[q]) != cudaSuccess || !can)
+        ok = 0;
+    }
+    // all ranks must agree: MIN over ranks
+    int* f = nullptr;
+    REC_CUDA(cudaMalloc(reinterpret_cast<void**>(&f), sizeof(int)));
+    REC_CUDA(cudaMemcpy(f, &ok, sizeof(int), cudaMemcpyHostToDevice));
+    REC_NCCL(ncclAllReduce(f, f, 1, ncclInt32, ncclMin, comm, m->ws[0].stream));
+    REC_CUDA(cudaStreamSynchronize(m->ws[0].stream));
+    REC_CUDA(cudaMemcpy(&ok, f, sizeof(int), cudaMemcpyDeviceToHost));
+    cudaFree(f);
+  }
+  if (!ok) return REC_OK;
+  REC_CUDA(cudaMalloc(reinterpret_cast<void**>(&m->p2p_flags), sizeof(unsigned) * G));
+  REC_CUDA(cudaMemset(m->p2p_flags, 0, sizeof(unsigned) * G));
+  REC_CUDA(cudaMalloc(reinterpret_cast<void**>(&m->p2p_counter), sizeof(unsigned)));
+  float* target = m->ws[0].X;
+  if (m->shard == REC_SHARD_ROW) {  // partial sums of every source rank: [G][Bq][T][D]
+    const int64_t Bq = (m->max_batch + G - 1) / G;
+    REC_CUDA(cudaMalloc(reinterpret_cast<void**>(&m->p2p_stage),
+                        sizeof(float) * G * Bq * m->T * static_cast<int64_t>(m->D)));
+    target = m->p2p_stage;
+  }
+  cudaIpcMemHandle_t mine[2];
+  REC_CUDA(cudaIpcGetMemHandle(&mine[0], target));
+  REC_CUDA(cudaIpcGetMemHandle(&mine[1], m->p2p_flags));
+  const size_t hb = sizeof(mine);
+  uint8_t* dh = nullptr;
+  REC_CUDA(cudaMalloc(reinterpret_cast<void**>(&dh), hb * (G + 1)));
+  REC_CUDA(cudaMemcpy(dh + hb * G, mine, hb, cudaMemcpyHostToDevice));
+  REC_NCCL(ncclAllGather(dh + hb * G, dh, hb, ncclUint8, static_cast<ncclComm_t>(m->nccl_comm),
+                         m->ws[0].stream));
+  REC_CUDA(cudaStreamSynchronize(m->ws[0].stream));
+  std::vector<cudaIpcMemHandle_t> all(2 * G);
+  REC_CUDA(cudaMemcpy(all.data(), dh, hb * G, cudaMemcpyDeviceToHost));
+  cudaFree(dh);
+  std::vector<float*> px(G);
+  std::vector<unsigned*> pf(G);
+  for (int q = 0; q < G; ++q) {
+    if (q == m->rank) {
+      px[q] = target;
+      pf[q] = m->p2p_flags;
+      continue;
+    }
+    void* a = nullptr;
+    void* b = nullptr;
+    REC_CUDA(cudaIpcOpenMemHandle(&a, all[2 * q], cudaIpcMemLazyEnablePeerAccess));
+    m->p2p_opened.push_back(a);
+    REC_CUDA(cudaIpcOpenMemHandle(&b, all[2 * q + 1], cudaIpcMemLazyEnablePeerAccess));
+    m->p2p_opened.push_back(b);
+    px[q] = static_cast<float*>(a);
+    pf[q] = static_cast<unsigned*>(b);
+  }
+  REC_CUDA(cudaMalloc(reinterpret_cast<void**>(&m->d_peer_X), sizeof(float*) * G));
+  REC_CUDA(cudaMalloc(reinterpret_cast<void**>(&m->d_peer_flags), sizeof(unsigned*) * G));
+  REC_CUDA(cudaMemcpy(m->d_peer_X, px.data(), sizeof(float*) * G, cudaMemcpyHostToDevice));
+  REC_CUDA(cudaMemcpy(m->d_peer_flags, pf.data(), sizeof(unsigned*) * G, cudaMemcpyHostToDevice));
+  m->p2p = true;
+  if (getenv("REC_VERBOSE"))
+    fprintf(stderr, "[rec] rank %d: fused %s exchange over peer memory (%d ranks)\n", m->rank,
+            m->shard == REC_SHARD_TABLE ? "all-to-all" : "reduce-scatter", G);
+  return REC_OK;
 }
 
 rec_status sharded_alloc(rec_model_s* m) {
@@ -62,6 +158,19 @@ rec_status sharded_alloc(rec_model_s* m) {
 
 void dist_destroy(rec_model_s* m) {
   if (!m) return;
+  for (void* p : m->p2p_opened) cudaIpcCloseMemHandle(p);
+  m->p2p_opened.clear();
+  cudaFree(m->d_peer_X);
+  cudaFree(m->d_peer_flags);
+  cudaFree(m->p2p_flags);
+  cudaFree(m->p2p_counter);
+  cudaFree(m->p2p_stage);
+  m->p2p_stage = nullptr;
+  m->d_peer_X = nullptr;
+  m->d_peer_flags = nullptr;
+  m->p2p_flags = nullptr;
+  m->p2p_counter = nullptr;
+  m->p2p = false;
   if (m->nccl_comm) {
     ncclCommDestroy(static_cast<ncclComm_t>(m->nccl_comm));
     m->nccl_comm = nullptr;
@@ -82,7 +191,35 @@ rec_status sharded_forward(rec_model_s* m, Workspace& w, const float* d_dense, c
   ncclComm_t comm = static_cast<ncclComm_t>(m->nccl_comm);
   const size_t xs = sizeof(float) * (T + 1) * D;
   // a3 on this GPU's shard, written in all-to-all / reduce-scatter order
-  if (m->shard == REC_SHARD_TABLE) {
+  if (m->p2p) {
+    // fused: pooled vectors land in the owners' X slots 1 + t0 .. over NVLink, then wait for
+    // every rank's arrival flag of this epoch (the previous epoch's X readers all finished:
+    // the CTR all-gather of the previous query completed on every rank before it returned)
+    P2PArgs pa{};
+    pa.peer_X = m->d_peer_X;
+    pa.peer_flags = m->d_peer_flags;
+    pa.counter = m->p2p_counter;
+    pa.my_flags = m->p2p_flags;
+    pa.Bq = Bq;
+    pa.G = G;
+    pa.rank = r;
+    pa.epoch = ++m->p2p_epoch;
+    REC_CUDA(cudaMemsetAsync(m->p2p_counter, 0, sizeof(unsigned), s));
+    if (m->shard == REC_SHARD_TABLE) {
+      pa.row_off = 0;
+      launch_sls_p2p(m->tables, m->d_tab_off, m->row_stride, m->d_rows, d_idx, d_off + m->t0 * B, B,
+                     TL, D, (T + 1) * D, 1 + m->t0, w.flag, pa, s);
+      launch_p2p_wait(pa, s);
+      m->launches += 2;
+    } else {  // row-wise: partial sums into the owner's staging slot of this rank, then reduce
+      pa.row_off = r * Bq;
+      launch_sls_p2p(m->tables, m->d_tab_off, m->row_stride, m->d_rows, d_idx, d_off, B, T, D,
+                     T * D, 0, w.flag, pa, s, static_cast<int>(m->row_lo), static_cast<int>(m->row_hi));
+      launch_p2p_wait(pa, s);
+      launch_p2p_reduce(m->p2p_stage, w.X, Bl, Bq, T, D, G, s);
+      m->launches += 3;
+    }
+  } else if (m->shard == REC_SHARD_TABLE) {
     launch_sls(m->tables, m->d_tab_off, m->row_stride, m->d_rows, d_idx, d_off + m->t0 * B, B,
                nullptr, TL, D, m->sh_send, TL * D, 0, w.flag, s);
     REC_NCCL(ncclAlltoAll(m->sh_send, m->sh_recv, static_cast<size_t>(Bq) * TL * D, ncclFloat, comm, s));

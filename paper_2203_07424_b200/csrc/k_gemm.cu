@@ -25,6 +25,8 @@
 
 namespace rec {
 
+int g_gemm_stages = 0;  // cap on the per-layer GEMM ring depth (0 = kernel maximum)
+
 constexpr int BM = 128;
 constexpr int BK = 64;
 constexpr int A_STAGE_BYTES = BM * BK * 2;  // 16 KB
@@ -198,7 +200,9 @@ static void launch_bn(const CUtensorMap* ta, const CUtensorMap* tw, const GemmAr
   constexpr int STAGE = MT * A_STAGE_BYTES + BN * BK * 2;
   constexpr int SMAX = (MT == 1 ? 4 : 3);
   const int nkb = (a.K + BK - 1) / BK;
-  const int stages = nkb < SMAX ? (nkb < 1 ? 1 : nkb) : SMAX;
+  int smax = SMAX;
+  if (g_gemm_stages > 0 && g_gemm_stages < smax) smax = g_gemm_stages;
+  const int stages = nkb < smax ? (nkb < 1 ? 1 : nkb) : smax;
   const size_t smem = static_cast<size_t>(stages) * STAGE + 1024 + 256;
   dim3 grid((a.N + BN - 1) / BN, (a.M + BM * MT - 1) / (BM * MT));
   k_gemm_tc<BN, MT><<<grid, 128, smem, s>>>(*ta, *tw, a, stages);

@@ -13,6 +13,8 @@
 
 namespace rec {
 
+int g_interact_wpc = 8;  // warps (items) per CTA, REC_INTERACT_WPC
+
 // Pair p of the strict lower triangle in row-major order: (i, j), 1 <= i <= T, 0 <= j < i,
 // p = i(i-1)/2 + j.
 __device__ __forceinline__ int2 pair_of(int p) {
@@ -75,7 +77,7 @@ void launch_interact(const float* X, int B, const int* dB, int T, int D, __nv_bf
   if (B <= 0) return;
   const size_t per_warp = (static_cast<size_t>(T + 1) * (D + 4) + ld_top / 2) * sizeof(float);
   int wpc = static_cast<int>((96 * 1024) / per_warp);
-  if (wpc > 8) wpc = 8;
+  if (wpc > g_interact_wpc) wpc = g_interact_wpc;
   if (wpc < 1) wpc = 1;
   const size_t smem = wpc * per_warp;
   if (smem > 48 * 1024)

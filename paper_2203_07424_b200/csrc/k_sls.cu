@@ -11,6 +11,8 @@
 // the bag's indices LANES at a time (one per lane), broadcasts them with shuffles, and keeps
 // LANES independent 128-bit row loads in flight per lane (ld.global.nc.L1::no_allocate —
 // rows are streamed, never reused from L1) before accumulating them in order.
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.h"
 #include "sm100.cuh"
@@ -97,7 +99,16 @@ struct SlsShape {
   static constexpr int U = RIF;  // RIF x 16 B in flight per lane (8: ~90 regs, 5 CTAs of 128/SM)
 };
 
-template <int LANES, int THREADS>
+__device__ __forceinline__ void st_release_sys(unsigned* p, unsigned v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+template <int LANES, int THREADS, bool P2P = false>
 __global__ void __launch_bounds__(THREADS, REC_SLS_MINB) k_sls(const float* __restrict__ tables,
                                                     const int64_t* __restrict__ tab_off,
                                                     int64_t row_stride,
@@ -107,13 +118,13 @@ __global__ void __launch_bounds__(THREADS, REC_SLS_MINB) k_sls(const float* __re
                                                     const int* __restrict__ dB, int T,
                                                     int D, float* __restrict__ X, int x_stride,
                                                     int x_slot0, int* __restrict__ flag, int row_lo,
-                                                    int row_hi) {
+                                                    int row_hi, const P2PArgs p2p) {
   using S = SlsShape<LANES>;
   constexpr int GROUPS = THREADS / LANES;
   __shared__ int s_off[GROUPS + 1];
   if (dB) B = *dB;  // device-side batch size (graph replay); grid sized for the capacity
   const int nbags = T * B;
-  if (static_cast<int>(blockIdx.x) * GROUPS >= nbags) return;
+  if (!P2P && static_cast<int>(blockIdx.x) * GROUPS >= nbags) return;  // (P2P grids are exact)
   const int g0 = blockIdx.x * GROUPS;
   for (int i = threadIdx.x; i <= GROUPS; i += THREADS) {
     const int g = min(g0 + i, nbags);
@@ -184,11 +195,49 @@ __global__ void __launch_bounds__(THREADS, REC_SLS_MINB) k_sls(const float* __re
     for (int j = 0; j < S::IPL; ++j) cur[j] = nxt[j];
   }
   if (oob) atomicOr(flag, 1);
+  if (!P2P) {
+    if (active) {
+      float4* dst = reinterpret_cast<float4*>(X + (static_cast<int64_t>(b) * x_stride +
+                                                   static_cast<int64_t>(x_slot0 + t) * D + col));
+      *dst = acc;
+    }
+    return;
+  }
+  // fused all-to-all: item b lives on rank b / Bq as local row b % Bq
   if (active) {
-    float4* dst = reinterpret_cast<float4*>(X + (static_cast<int64_t>(b) * x_stride +
-                                                 static_cast<int64_t>(x_slot0 + t) * D + col));
+    const int p = b / p2p.Bq, bi = p2p.row_off + b - p * p2p.Bq;
+    float4* dst = reinterpret_cast<float4*>(p2p.peer_X[p] + (static_cast<int64_t>(bi) * x_stride +
+                                                             static_cast<int64_t>(x_slot0 + t) * D + col));
     *dst = acc;
   }
+  __syncthreads();  // the CTA's peer stores happen-before thread 0's system-scope fence
+  if (threadIdx.x == 0) {  // (threads of empty groups have exited: they do not take part)
+    __threadfence_system();
+    const unsigned prev = atomicAdd(p2p.counter, 1u);
+    if (prev == gridDim.x - 1) {  // last CTA: every CTA's stores are fenced
+      __threadfence_system();
+      for (int q = 0; q < p2p.G; ++q) st_release_sys(p2p.peer_flags[q] + p2p.rank, p2p.epoch);
+    }
+  }
+}
+
+// One thread per rank: wait until rank q's arrival flag reached this epoch (bounded: a lost
+// peer traps instead of hanging the GPU).
+__global__ void k_p2p_wait(const P2PArgs p2p) {
+  const int q = threadIdx.x;
+  if (q >= p2p.G) return;
+  unsigned long long t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  while (ld_acquire_sys(p2p.my_flags + q) < p2p.epoch) {
+    __nanosleep(200);
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > 20ull * 1000 * 1000 * 1000) __trap();  // 20 s: a peer died
+  }
+}
+
+void launch_p2p_wait(const P2PArgs& p2p, cudaStream_t s) {
+  k_p2p_wait<<<1, 32 * ((p2p.G + 31) / 32), 0, s>>>(p2p);
 }
 
 // Synthetic-index variant (device-synth serving mode, fixed pooling): identical gather /
@@ -474,7 +523,58 @@ static void launch_l(const float* tables, const int64_t* tab_off, int64_t row_st
   const int nbags = T * B;
   k_sls<L, THREADS><<<(nbags + THREADS / L - 1) / (THREADS / L), THREADS, 0, s>>>(
       tables, tab_off, row_stride, rows, indices, offsets, B, dB, T, D, X, x_stride_items, x_slot0,
-      flag, row_lo, row_hi);
+      flag, row_lo, row_hi, P2PArgs{});
+}
+
+// Row-wise reduction of the staged partial sums, fixed source order q = 0..G-1 (with int8 x 2^e
+// tables every partial sum is exact, so the result equals any other summation order).
+__global__ void k_p2p_reduce(const float4* __restrict__ stage, float4* __restrict__ X, int Bl,
+                             int Bq, int T, int d4, int G) {
+  const int64_t n = static_cast<int64_t>(Bl) * T * d4;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t it = e / d4;  // (i, t)
+    const int c = static_cast<int>(e - it * d4);
+    const int i = static_cast<int>(it / T), t = static_cast<int>(it - static_cast<int64_t>(i) * T);
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int q = 0; q < G; ++q) {
+      const float4 v = stage[((static_cast<int64_t>(q) * Bq + i) * T + t) * d4 + c];
+      acc.x += v.x;
+      acc.y += v.y;
+      acc.z += v.z;
+      acc.w += v.w;
+    }
+    X[(static_cast<int64_t>(i) * (T + 1) + 1 + t) * d4 + c] = acc;
+  }
+}
+
+void launch_p2p_reduce(const float* stage, float* X, int Bl, int Bq, int T, int D, int G,
+                       cudaStream_t s) {
+  const int64_t n = static_cast<int64_t>(Bl) * T * (D / 4);
+  if (n == 0) return;
+  const int blocks = static_cast<int>(std::min<int64_t>((n + 255) / 256, 148 * 8));
+  k_p2p_reduce<<<blocks, 256, 0, s>>>(reinterpret_cast<const float4*>(stage),
+                                      reinterpret_cast<float4*>(X), Bl, Bq, T, D / 4, G);
+}
+
+void launch_sls_p2p(const float* tables, const int64_t* tab_off, int64_t row_stride,
+                    const int64_t* rows, const int* indices, const int* offsets, int B, int T, int D,
+                    int x_stride_items, int x_slot0, int* flag, const P2PArgs& p2p, cudaStream_t s,
+                    int row_lo, int row_hi) {
+  constexpr int THREADS = 128;
+  const int nbags = T * B;
+  if (nbags == 0) return;
+  const int L = D / 4 <= 8 ? 8 : D / 4 <= 16 ? 16 : 32;
+  const int grid = (nbags + THREADS / L - 1) / (THREADS / L);
+  if (L == 8)
+    k_sls<8, THREADS, true><<<grid, THREADS, 0, s>>>(tables, tab_off, row_stride, rows, indices, offsets, B,
+        nullptr, T, D, nullptr, x_stride_items, x_slot0, flag, row_lo, row_hi, p2p);
+  else if (L == 16)
+    k_sls<16, THREADS, true><<<grid, THREADS, 0, s>>>(tables, tab_off, row_stride, rows, indices, offsets, B,
+        nullptr, T, D, nullptr, x_stride_items, x_slot0, flag, row_lo, row_hi, p2p);
+  else
+    k_sls<32, THREADS, true><<<grid, THREADS, 0, s>>>(tables, tab_off, row_stride, rows, indices, offsets, B,
+        nullptr, T, D, nullptr, x_stride_items, x_slot0, flag, row_lo, row_hi, p2p);
 }
 
 void set_max_smem_carveout(int c) {

@@ -57,6 +57,30 @@ void set_max_smem_carveout(int percent);  // SLS kernels' preferred shared-memor
 // Row r of table t lives at tables + tab_off[t] + r * row_stride (floats).
 // B: batch (or capacity when dB != nullptr: then the kernels read the batch from *dB,
 // which lets one captured CUDA graph serve every batch size).
+// Table-wise sharding with the all-to-all fused into the SLS (dist.cu): the
+// pooled vector of bag (t, b) is stored straight into the X buffer of the rank that owns item
+// b (peer memory over NVLink, CUDA IPC mappings), then the grid's last CTA raises this rank's
+// arrival flag on every peer (system-scope release).
+struct P2PArgs {
+  float* const* peer_X;         // [G] device array: every rank's X (table-wise) or partial-sum
+                                // staging [G][Bq][T][D] (row-wise); own rank: local buffer
+  int row_off;                  // destination row offset: 0 (table-wise) or rank * Bq (row-wise)
+  unsigned* const* peer_flags;  // [G] device array: every rank's arrival-flag array [G]
+  unsigned* counter;            // CTA completion counter of this launch (zeroed before it)
+  unsigned* my_flags;           // this rank's arrival flags [G] (written by the peers)
+  int Bq, G, rank;              // items per rank block, world size, this rank
+  unsigned epoch;               // query sequence number (flags reach it when the data landed)
+};
+void launch_sls_p2p(const float* tables, const int64_t* tab_off, int64_t row_stride,
+                    const int64_t* rows, const int* indices, const int* offsets, int B, int T, int D,
+                    int x_stride_items, int x_slot0, int* flag, const P2PArgs& p2p, cudaStream_t s,
+                    int row_lo = 0, int row_hi = 0x7fffffff);
+// Row-wise: X[i][1 + t] = sum over source ranks q (in order) of stage[q][i][t] for i < Bl.
+void launch_p2p_reduce(const float* stage, float* X, int Bl, int Bq, int T, int D, int G,
+                       cudaStream_t s);
+// Block the stream until every rank's SLS of this epoch has landed in this rank's X.
+void launch_p2p_wait(const P2PArgs& p2p, cudaStream_t s);
+
 // row_lo/row_hi: row-wise sharding keeps rows [row_lo, row_hi) of every table on this GPU
 // (arena row r - row_lo); other rows add nothing.  Replicated / table-wise: 0, INT32_MAX.
 void launch_sls(const float* tables, const int64_t* tab_off, int64_t row_stride,
@@ -160,6 +184,8 @@ void launch_mlp_chain(const ChainMaps& maps, const ChainArgs& a, cudaStream_t s)
 // launch attribute (0 = stream default).  Experiment knob (REC_PRIO).
 extern int g_dense_prio;
 extern int g_sls_prio;  // same for the synthetic-index SLS
+extern int g_gemm_stages;
+extern int g_interact_wpc;  // interaction warps per CTA (REC_INTERACT_WPC)  // per-layer GEMM ring depth cap (REC_GEMM_STAGES; 0 = maximum)
 
 // --------------------------------------------------------------- interaction (a5)
 void launch_interact(const float* X, int B, const int* dB, int T, int D, __nv_bfloat16* A_top,

@@ -999,6 +999,8 @@ rec_status rec_model_create(const rec_model_desc* d, rec_model_t* out) {
       g_sls_prio = atoi(pr) < 0 ? hi : 0;
     }
     if (const char* fd = getenv("REC_FUSE_DENSE")) m->fuse_dense = atoi(fd) != 0;
+    if (const char* gs = getenv("REC_GEMM_STAGES")) g_gemm_stages = atoi(gs);
+    if (const char* iw = getenv("REC_INTERACT_WPC")) g_interact_wpc = std::max(1, std::min(8, atoi(iw)));
     const char* p = getenv("REC_PDL");
     m->sls_pdl = !(p && strcmp(p, "0") == 0);
     CHECK_CUDA_CREATE(cudaDeviceGetAttribute(&m->nsm, cudaDevAttrMultiProcessorCount, m->device));

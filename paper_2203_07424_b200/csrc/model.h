@@ -170,6 +170,15 @@ struct rec_model_s {
   float* sh_send = nullptr;            // [B_pad][T_loc][D] (table) or [B_pad][T][D] (row)
   float* sh_recv = nullptr;            // [world][Bq][T_loc][D] (table) or [Bq][T][D] (row)
   float* sh_ctr = nullptr;             // [world * Bq]
+  // table-wise sharding with the all-to-all fused into the SLS (peer stores over NVLink)
+  bool p2p = false;
+  float** d_peer_X = nullptr;          // [world] device array of every rank's ws[0].X
+  unsigned** d_peer_flags = nullptr;   // [world] device array of every rank's arrival flags
+  unsigned* p2p_flags = nullptr;       // this rank's arrival flags [world]
+  unsigned* p2p_counter = nullptr;     // CTA counter of the fused SLS launch
+  float* p2p_stage = nullptr;          // row-wise: partial sums of every source rank [G][Bq][T][D]
+  unsigned p2p_epoch = 0;
+  std::vector<void*> p2p_opened;       // IPC mappings to close
 };
 
 namespace rec {
@@ -210,6 +219,7 @@ rec_status sharded_forward(rec_model_s* m, Workspace& w, const float* d_dense, c
 rec_status sharded_alloc(rec_model_s* m);
 cudaEvent_t prof_begin(rec_model_s* m, cudaStream_t s);
 rec_status dist_init(rec_model_s* m, const void* nccl_id);   // dist.cu
+rec_status p2p_init(rec_model_s* m);                          // dist.cu (fused table-wise exchange)
 void dist_destroy(rec_model_s* m);
 void prof_end(rec_model_s* m, cudaStream_t s, int kernel, cudaEvent_t a);
 }  // namespace rec
