@@ -101,8 +101,12 @@ rec_status rec_query_debug(rec_model_t m, const float* dense, const int32_t* ind
                            float* pooled, float* logits);
 
 /* Enqueue rec_query on stream slot `slot` (0 <= slot < streams) without waiting.
- * DEVICE pointers only; `nnz` = offsets[T*B] (not read back).  Completion and the
- * device error flag are collected by rec_sync(m, slot). */
+ * Device or host pointers: host inputs are copied into the slot's device buffers on its
+ * stream and host ctr is filled by a device-to-host copy there (pinned host memory keeps
+ * the call asynchronous; the caller must not modify host inputs or read ctr before
+ * rec_sync(m, slot)).  `nnz` = offsets[T*B] (not read back; host indices: <= T * max_batch
+ * * pooling_hi).  Offsets are validated on the device; completion and the device error
+ * flag are collected by rec_sync(m, slot). */
 rec_status rec_query_async(rec_model_t m, int32_t slot, const float* dense,
                            const int32_t* indices, const int32_t* offsets, int64_t nnz,
                            int32_t batch, float* ctr);

@@ -1308,9 +1308,37 @@ rec_status rec_query_async(rec_model_t m, int32_t slot, const float* dense, cons
     if (st != REC_OK) return st;
   }
   Workspace& w = m->ws[slot];
-  launch_dense_to_bf16(dense, batch, m->F, m->Fpad, w.dense_bf, w.stream);
-  m->launches += 1;
-  return forward_enqueue(m, w, indices, offsets, batch, nullptr, ctr, w.logit, nullptr);
+  cudaStream_t s = w.stream;
+  // host buffers (pinned: fully asynchronous) are copied straight into this slot's device
+  // buffers on its stream; the CTRs come back the same way (e2e serving path)
+  const int nb = m->T * batch;
+  const int* d_off = offsets;
+  const int* d_idx = indices;
+  const float* d_dense = dense;
+  if (!is_device_ptr(offsets)) {
+    REC_CUDA(cudaMemcpyAsync(w.offsets, offsets, sizeof(int) * (nb + 1), cudaMemcpyHostToDevice, s));
+    d_off = w.offsets;
+  }
+  if (!is_device_ptr(indices)) {
+    if (nnz > w.idx_cap) {
+      set_error("nnz = %lld exceeds the index capacity %lld", (long long)nnz, (long long)w.idx_cap);
+      return REC_E_INVALID_ARG;
+    }
+    REC_CUDA(cudaMemcpyAsync(w.indices, indices, sizeof(int) * nnz, cudaMemcpyHostToDevice, s));
+    d_idx = w.indices;
+  }
+  if (!is_device_ptr(dense)) {
+    REC_CUDA(cudaMemcpyAsync(w.dense_f32, dense, sizeof(float) * batch * m->F, cudaMemcpyHostToDevice, s));
+    d_dense = w.dense_f32;
+  }
+  const bool ctr_dev = is_device_ptr(ctr);
+  launch_check_offsets(d_off, nb, w.flag, s);
+  launch_dense_to_bf16(d_dense, batch, m->F, m->Fpad, w.dense_bf, s);
+  m->launches += 2;
+  rec_status st = forward_enqueue(m, w, d_idx, d_off, batch, nullptr, ctr_dev ? ctr : w.ctr, w.logit, nullptr);
+  if (st != REC_OK) return st;
+  if (!ctr_dev) REC_CUDA(cudaMemcpyAsync(ctr, w.ctr, sizeof(float) * batch, cudaMemcpyDeviceToHost, s));
+  return REC_OK;
 }
 
 rec_status rec_synth_query_async(rec_model_t m, int32_t slot, const int32_t* segs, int32_t nseg,
