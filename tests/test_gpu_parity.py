@@ -126,6 +126,16 @@ def test_device_pointers_match_host():
     m2.rec_query_async(1, dv, iv, ov, int(off[-1]), B, cv2)
     m2.rec_sync(1)
     assert np.array_equal(cv2.cpu().numpy(), c_host)
+    # async path with HOST inputs/outputs (pinned and pageable): same bits
+    pin = [torch.from_numpy(x).pin_memory() for x in (dense, ind, off)]
+    cp = torch.zeros(B).pin_memory()
+    m2.rec_query_async(0, pin[0], pin[1], pin[2], int(off[-1]), B, cp)
+    c_np = np.zeros(B, np.float32)
+    m2.rec_query_async(1, dense, ind, off, int(off[-1]), B, c_np)
+    m2.rec_sync(0)
+    m2.rec_sync(1)
+    assert np.array_equal(cp.numpy(), c_host)
+    assert np.array_equal(c_np, c_host)
 
 
 def test_synth_query_matches_host_inputs():
