@@ -102,9 +102,14 @@ rec_status p2p_init(rec_model_s* m) {
                         sizeof(float) * G * Bq * m->T * static_cast<int64_t>(m->D)));
     target = m->p2p_stage;
   }
-  cudaIpcMemHandle_t mine[2];
+  REC_CUDA(cudaMalloc(reinterpret_cast<void**>(&m->p2p_ctr_flags), sizeof(unsigned) * G));
+  REC_CUDA(cudaMemset(m->p2p_ctr_flags, 0, sizeof(unsigned) * G));
+  constexpr int NH = 4;  // exported buffers: X / staging, arrival flags, CTR gather, CTR flags
+  cudaIpcMemHandle_t mine[NH];
   REC_CUDA(cudaIpcGetMemHandle(&mine[0], target));
   REC_CUDA(cudaIpcGetMemHandle(&mine[1], m->p2p_flags));
+  REC_CUDA(cudaIpcGetMemHandle(&mine[2], m->sh_ctr));
+  REC_CUDA(cudaIpcGetMemHandle(&mine[3], m->p2p_ctr_flags));
   const size_t hb = sizeof(mine);
   uint8_t* dh = nullptr;
   REC_CUDA(cudaMalloc(reinterpret_cast<void**>(&dh), hb * (G + 1)));
@@ -112,30 +117,37 @@ rec_status p2p_init(rec_model_s* m) {
   REC_NCCL(ncclAllGather(dh + hb * G, dh, hb, ncclUint8, static_cast<ncclComm_t>(m->nccl_comm),
                          m->ws[0].stream));
   REC_CUDA(cudaStreamSynchronize(m->ws[0].stream));
-  std::vector<cudaIpcMemHandle_t> all(2 * G);
+  std::vector<cudaIpcMemHandle_t> all(NH * G);
   REC_CUDA(cudaMemcpy(all.data(), dh, hb * G, cudaMemcpyDeviceToHost));
   cudaFree(dh);
-  std::vector<float*> px(G);
-  std::vector<unsigned*> pf(G);
+  std::vector<float*> px(G), pc(G);
+  std::vector<unsigned*> pf(G), pcf(G);
   for (int q = 0; q < G; ++q) {
     if (q == m->rank) {
       px[q] = target;
       pf[q] = m->p2p_flags;
+      pc[q] = m->sh_ctr;
+      pcf[q] = m->p2p_ctr_flags;
       continue;
     }
-    void* a = nullptr;
-    void* b = nullptr;
-    REC_CUDA(cudaIpcOpenMemHandle(&a, all[2 * q], cudaIpcMemLazyEnablePeerAccess));
-    m->p2p_opened.push_back(a);
-    REC_CUDA(cudaIpcOpenMemHandle(&b, all[2 * q + 1], cudaIpcMemLazyEnablePeerAccess));
-    m->p2p_opened.push_back(b);
-    px[q] = static_cast<float*>(a);
-    pf[q] = static_cast<unsigned*>(b);
+    void* a[NH] = {};
+    for (int k = 0; k < NH; ++k) {
+      REC_CUDA(cudaIpcOpenMemHandle(&a[k], all[NH * q + k], cudaIpcMemLazyEnablePeerAccess));
+      m->p2p_opened.push_back(a[k]);
+    }
+    px[q] = static_cast<float*>(a[0]);
+    pf[q] = static_cast<unsigned*>(a[1]);
+    pc[q] = static_cast<float*>(a[2]);
+    pcf[q] = static_cast<unsigned*>(a[3]);
   }
   REC_CUDA(cudaMalloc(reinterpret_cast<void**>(&m->d_peer_X), sizeof(float*) * G));
   REC_CUDA(cudaMalloc(reinterpret_cast<void**>(&m->d_peer_flags), sizeof(unsigned*) * G));
+  REC_CUDA(cudaMalloc(reinterpret_cast<void**>(&m->d_peer_ctr), sizeof(float*) * G));
+  REC_CUDA(cudaMalloc(reinterpret_cast<void**>(&m->d_peer_ctr_flags), sizeof(unsigned*) * G));
   REC_CUDA(cudaMemcpy(m->d_peer_X, px.data(), sizeof(float*) * G, cudaMemcpyHostToDevice));
   REC_CUDA(cudaMemcpy(m->d_peer_flags, pf.data(), sizeof(unsigned*) * G, cudaMemcpyHostToDevice));
+  REC_CUDA(cudaMemcpy(m->d_peer_ctr, pc.data(), sizeof(float*) * G, cudaMemcpyHostToDevice));
+  REC_CUDA(cudaMemcpy(m->d_peer_ctr_flags, pcf.data(), sizeof(unsigned*) * G, cudaMemcpyHostToDevice));
   m->p2p = true;
   if (getenv("REC_VERBOSE"))
     fprintf(stderr, "[rec] rank %d: fused %s exchange over peer memory (%d ranks)\n", m->rank,
@@ -165,7 +177,13 @@ void dist_destroy(rec_model_s* m) {
   cudaFree(m->p2p_flags);
   cudaFree(m->p2p_counter);
   cudaFree(m->p2p_stage);
+  cudaFree(m->d_peer_ctr);
+  cudaFree(m->d_peer_ctr_flags);
+  cudaFree(m->p2p_ctr_flags);
   m->p2p_stage = nullptr;
+  m->d_peer_ctr = nullptr;
+  m->d_peer_ctr_flags = nullptr;
+  m->p2p_ctr_flags = nullptr;
   m->d_peer_X = nullptr;
   m->d_peer_flags = nullptr;
   m->p2p_flags = nullptr;
@@ -194,7 +212,8 @@ rec_status sharded_forward(rec_model_s* m, Workspace& w, const float* d_dense, c
   if (m->p2p) {
     // fused: pooled vectors land in the owners' X slots 1 + t0 .. over NVLink, then wait for
     // every rank's arrival flag of this epoch (the previous epoch's X readers all finished:
-    // the CTR all-gather of the previous query completed on every rank before it returned)
+    // every rank raised its CTR flag of the previous epoch after its interaction, and this
+    // rank saw all of them before the previous query returned)
     P2PArgs pa{};
     pa.peer_X = m->d_peer_X;
     pa.peer_flags = m->d_peer_flags;
@@ -247,7 +266,20 @@ rec_status sharded_forward(rec_model_s* m, Workspace& w, const float* d_dense, c
     enqueue_interact_top(m, w, s, Bl, nullptr, w.ctr, w.logit, nullptr);
   }
   // C3: every rank gets every CTR (positions >= B of the padded gather are ignored)
-  REC_NCCL(ncclAllGather(w.ctr, m->sh_ctr, Bq, ncclFloat, comm, s));
+  if (m->p2p) {  // peer stores + flags (this also orders the next query's X writes, see above)
+    P2PArgs pc{};
+    pc.peer_X = m->d_peer_ctr;
+    pc.peer_flags = m->d_peer_ctr_flags;
+    pc.my_flags = m->p2p_ctr_flags;
+    pc.G = G;
+    pc.rank = r;
+    pc.epoch = m->p2p_epoch;
+    launch_p2p_ctr_scatter(w.ctr, Bl, item0, pc, s);
+    launch_p2p_wait(pc, s);
+    m->launches += 2;
+  } else {
+    REC_NCCL(ncclAllGather(w.ctr, m->sh_ctr, Bq, ncclFloat, comm, s));
+  }
   REC_CUDA(cudaMemcpyAsync(w.flag_host, w.flag, sizeof(int), cudaMemcpyDeviceToHost, s));
   REC_CUDA(cudaStreamSynchronize(s));
   const int f = *w.flag_host;

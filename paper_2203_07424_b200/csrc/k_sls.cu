@@ -236,6 +236,20 @@ __global__ void k_p2p_wait(const P2PArgs p2p) {
   }
 }
 
+__global__ void k_p2p_ctr_scatter(const float* __restrict__ ctr, int Bl, int item0, const P2PArgs p2p) {
+  for (int q = 0; q < p2p.G; ++q)
+    for (int i = threadIdx.x; i < Bl; i += blockDim.x) p2p.peer_X[q][item0 + i] = ctr[i];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    for (int q = 0; q < p2p.G; ++q) st_release_sys(p2p.peer_flags[q] + p2p.rank, p2p.epoch);
+  }
+}
+
+void launch_p2p_ctr_scatter(const float* ctr, int Bl, int item0, const P2PArgs& p2p, cudaStream_t s) {
+  k_p2p_ctr_scatter<<<1, 512, 0, s>>>(ctr, Bl, item0, p2p);
+}
+
 void launch_p2p_wait(const P2PArgs& p2p, cudaStream_t s) {
   k_p2p_wait<<<1, 32 * ((p2p.G + 31) / 32), 0, s>>>(p2p);
 }

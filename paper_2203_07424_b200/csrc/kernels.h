@@ -80,6 +80,10 @@ void launch_p2p_reduce(const float* stage, float* X, int Bl, int Bq, int T, int 
                        cudaStream_t s);
 // Block the stream until every rank's SLS of this epoch has landed in this rank's X.
 void launch_p2p_wait(const P2PArgs& p2p, cudaStream_t s);
+// All-gather of the CTRs over peer memory: this rank's ctr[0..Bl) goes to every rank's
+// gather buffer at [item0, item0 + Bl), then this rank's flag is raised on every peer
+// (p2p.peer_X = the ranks' gather buffers, p2p.peer_flags = their CTR-flag arrays).
+void launch_p2p_ctr_scatter(const float* ctr, int Bl, int item0, const P2PArgs& p2p, cudaStream_t s);
 
 // row_lo/row_hi: row-wise sharding keeps rows [row_lo, row_hi) of every table on this GPU
 // (arena row r - row_lo); other rows add nothing.  Replicated / table-wise: 0, INT32_MAX.

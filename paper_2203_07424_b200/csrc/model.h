@@ -175,6 +175,9 @@ struct rec_model_s {
   float** d_peer_X = nullptr;          // [world] device array of every rank's ws[0].X
   unsigned** d_peer_flags = nullptr;   // [world] device array of every rank's arrival flags
   unsigned* p2p_flags = nullptr;       // this rank's arrival flags [world]
+  float** d_peer_ctr = nullptr;        // [world] device array of every rank's sh_ctr
+  unsigned** d_peer_ctr_flags = nullptr;
+  unsigned* p2p_ctr_flags = nullptr;   // this rank's CTR-gather flags [world]
   unsigned* p2p_counter = nullptr;     // CTA counter of the fused SLS launch
   float* p2p_stage = nullptr;          // row-wise: partial sums of every source rank [G][Bq][T][D]
   unsigned p2p_epoch = 0;
