@@ -16,6 +16,10 @@ DLRM's pairwise dot interaction without self-pairs.
               v = [x, Z(1,0), Z(2,0), Z(2,1), ..., Z(T,T-1)]         (R1)
   F4 top      ReLU hidden layers, last (width 1) linear -> logit,
               ctr = 1 / (1 + exp(-logit))                            (Table I Predict-FC; R2)
+
+MT-WnD (Table I row 4; readings R26-R29): one-hot lookups (F1 with bags of one
+index), no Bottom-FC, u = [p_0, ..., p_{T-1}] (concatenation, T*D), and per task k
+  logit_k = tower_k(u) + <v_k, u>,  ctr_k = sigmoid(logit_k)      (deep tower + wide part)
 """
 from __future__ import annotations
 
@@ -89,10 +93,25 @@ def forward(cfg, seed: int, dense: np.ndarray, indices: np.ndarray, offsets: np.
     shift = gen.emb_shift(cfg.pooling_lo, cfg.pooling_hi)
     rows_fn = lambda t, r: gen.table_values(seed, t, r, D, shift, cfg.value_mode)
     pooled = sls(rows_fn, T, B, D, np.asarray(indices), np.asarray(offsets))
+    if getattr(cfg, "arch", 0) == 1:
+        return forward_mtwnd(pooled, top, return_all)
     x = mlp(np.asarray(dense, dtype=np.float64), bottom, relu_last=True)
     v = interaction(x, pooled)
     logit = mlp(v, top, relu_last=False)[:, 0]
     ctr = sigmoid(logit)
     if return_all:
         return dict(pooled=pooled, x=x, v=v, logit=logit, ctr=ctr)
+    return ctr
+
+
+def forward_mtwnd(pooled: np.ndarray, towers_wide, return_all: bool = False):
+    """MT-WnD: CTR [B][N] (float64) from pooled [B][T][D] and (towers, wide) (R26-R28)."""
+    towers, wide = towers_wide
+    B = pooled.shape[0]
+    u = pooled.reshape(B, -1)
+    logit = np.stack([mlp(u, tw, relu_last=False)[:, 0] + u @ v for tw, v in zip(towers, wide)],
+                     axis=1)
+    ctr = sigmoid(logit)
+    if return_all:
+        return dict(pooled=pooled, x=np.zeros((B, 0)), v=u, logit=logit, ctr=ctr)
     return ctr

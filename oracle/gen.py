@@ -77,18 +77,34 @@ def layer_params(seed: int, layer: int, fan_in: int, fan_out: int, extra_shift: 
     return W, b
 
 
+TASK_LAYER_STRIDE = 16   # MT-WnD: tower k's layer l has id TOP_LAYER_BASE + 16 k + l (R29)
+WIDE_LAYER = 15          # ... and its wide vector id TOP_LAYER_BASE + 16 k + 15
+
+
 def model_params(cfg, seed: int):
-    """All MLP parameters of a config: (bottom [(W,b)...], top [(W,b)...])."""
+    """All MLP parameters of a config.
+
+    DLRM: (bottom [(W,b)...], top [(W,b)...]).
+    MT-WnD (R26-R29): (bottom = [], (towers [[(W,b)...] per task], wide [v_k [T*D]])) — tower k
+    uses layer ids TOP_LAYER_BASE + 16 k + l, its wide vector the id TOP_LAYER_BASE + 16 k + 15
+    (the W row of a fan_out = 1 layer; no bias); task 0's tower equals a DLRM top stack over
+    the same input width."""
     bottom = []
     for l in range(len(cfg.bottom) - 1):
         bottom.append(layer_params(seed, l, cfg.bottom[l], cfg.bottom[l + 1]))
-    T, D = cfg.num_tables, cfg.dim
-    widths = [D + T * (T + 1) // 2] + list(cfg.top)
-    top = []
-    for l in range(len(cfg.top)):
-        top.append(layer_params(seed, TOP_LAYER_BASE + l, widths[l], widths[l + 1],
-                                cfg.top_shift if l == 0 else 0))
-    return bottom, top
+    widths = [cfg.top_in] + list(cfg.top)
+    towers = []
+    for k in range(cfg.tasks):
+        tw = []
+        for l in range(len(cfg.top)):
+            tw.append(layer_params(seed, TOP_LAYER_BASE + TASK_LAYER_STRIDE * k + l, widths[l],
+                                   widths[l + 1], cfg.top_shift if l == 0 else 0))
+        towers.append(tw)
+    if getattr(cfg, "arch", 0) == 0:
+        return bottom, towers[0]
+    wide = [layer_params(seed, TOP_LAYER_BASE + TASK_LAYER_STRIDE * k + WIDE_LAYER, cfg.top_in, 1,
+                         cfg.top_shift)[0][0] for k in range(cfg.tasks)]
+    return bottom, (towers, wide)
 
 
 # ------------------------------------------------------------------ query inputs (G2, G3)

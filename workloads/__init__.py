@@ -23,6 +23,9 @@ REC_VALUES_FP32 = 1
 INDEX_UNIFORM = 0
 INDEX_SKEW2 = 2
 
+ARCH_DLRM = 0    # SLS -> bottom MLP -> dot interaction -> top MLP (Table I rows 1-3)
+ARCH_MTWND = 1   # one-hot lookups -> concat -> N task towers + wide part (Table I row 4; R26-R29)
+
 
 @dataclass(frozen=True)
 class ModelConfig:
@@ -49,10 +52,19 @@ class ModelConfig:
     sla_ms: float
     value_mode: int = REC_VALUES_INT8_EXACT
     index_dist: int = INDEX_UNIFORM
+    arch: int = ARCH_DLRM
+    tasks: int = 1            # MT-WnD: number of task towers N (reading R27)
 
     @property
     def dense_dim(self) -> int:
-        return self.bottom[0]
+        return self.bottom[0] if self.bottom else 0
+
+    @property
+    def top_in(self) -> int:
+        """Width of the first top / tower layer's input: the interaction vector (DLRM) or
+        the concatenated embeddings (MT-WnD, reading R26)."""
+        T, D = self.num_tables, self.dim
+        return T * D if self.arch == ARCH_MTWND else D + T * (T + 1) // 2
 
     @property
     def pooling_fixed(self) -> bool:
@@ -78,8 +90,14 @@ RMC2 = ModelConfig("DLRM-RMC2", 40, 1_000_000, 64, 120, 120, (256, 128, 64), (51
 # SLA 50 ms
 RMC3 = ModelConfig("DLRM-RMC3", 10, 1_000_000, 32, 20, 20, (2560, 512, 32), (512, 128, 1), 1, 1024, 50.0)
 
-CONFIGS = {c.name: c for c in (TINY, RMC1, RMC2, RMC3)}
-SHORT = {"tiny": TINY, "rmc1": RMC1, "rmc2": RMC2, "rmc3": RMC3}
+# SURVEY §8(f) 4 / Table I row MT-WnD: 26 tables, one-hot lookups (pooling
+# 1, no Gather-Reduce), no Bottom-FC, Predict-FC N x (1024-512-256); SLA 100 ms.
+# dim 32 and N = 2 tasks are readings R26/R27; top_shift keeps the logits non-vacuous (R21).
+MTWND = ModelConfig("MT-WnD", 26, 1_000_000, 32, 1, 1, (), (1024, 512, 256, 1), 0, 1024, 100.0,
+                    arch=ARCH_MTWND, tasks=2)
+
+CONFIGS = {c.name: c for c in (TINY, RMC1, RMC2, RMC3, MTWND)}
+SHORT = {"tiny": TINY, "rmc1": RMC1, "rmc2": RMC2, "rmc3": RMC3, "mtwnd": MTWND}
 
 
 def small_variant(cfg: ModelConfig, rows: int = 4096) -> ModelConfig:
@@ -146,7 +164,8 @@ def random_segments(batch: int, seed: int, max_qid: int = 1 << 20,
 
 
 __all__ = [
-    "ModelConfig", "TINY", "RMC1", "RMC2", "RMC3", "CONFIGS", "SHORT", "small_variant",
+    "ModelConfig", "TINY", "RMC1", "RMC2", "RMC3", "MTWND", "CONFIGS", "SHORT", "small_variant",
+    "ARCH_DLRM", "ARCH_MTWND",
     "TRACE_DTYPE", "query_sizes", "poisson_trace", "burst_trace", "random_segments",
     "REC_VALUES_INT8_EXACT", "REC_VALUES_FP32", "INDEX_UNIFORM", "INDEX_SKEW2",
 ]
