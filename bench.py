@@ -52,13 +52,15 @@ def sls_bytes_per_item(cfg, synth: bool = False) -> int:
 
 
 def mlp_flops_per_item(cfg) -> int:
+    """2 * sum(fan_in * fan_out) over the bottom MLP and every top stack / task tower (+ the
+    MT-WnD wide dot products)."""
     f = 0
     for a, b in zip(cfg.bottom[:-1], cfg.bottom[1:]):
         f += 2 * a * b
-    widths = [cfg.dim + cfg.num_tables * (cfg.num_tables + 1) // 2] + list(cfg.top)
-    for a, b in zip(widths[:-1], widths[1:]):
-        f += 2 * a * b
-    return f
+    widths = [cfg.top_in] + list(cfg.top)
+    tower = sum(2 * a * b for a, b in zip(widths[:-1], widths[1:]))
+    wide = 2 * cfg.top_in if cfg.arch == W.ARCH_MTWND else 0
+    return f + cfg.tasks * (tower + wide)
 
 
 def peaks():
@@ -343,7 +345,7 @@ def run_ours(args):
             ind, off, dense = model.rec_gen_batch(batches[b])
             host.append((torch.from_numpy(dense).pin_memory(), torch.from_numpy(ind).pin_memory(),
                          torch.from_numpy(off).pin_memory(), int(off[-1]), items_b[b], done_b[b]))
-        outs = [torch.empty(d, dtype=torch.float32).pin_memory() for _ in range(m_streams)]
+        outs = [torch.empty(d * cfg.tasks, dtype=torch.float32).pin_memory() for _ in range(m_streams)]
         for i in range(2 * m_streams):
             h = host[i % len(host)]
             model.rec_query_async(i % m_streams, h[0], h[1], h[2], h[3], h[4], outs[i % m_streams])
@@ -357,7 +359,7 @@ def run_ours(args):
             model.rec_query_async(i % m_streams, h[0], h[1], h[2], h[3], h[4], outs[i % m_streams])
             q_e2e += h[5]
             h2d += h[0].numel() * 4 + h[1].numel() * 4 + h[2].numel() * 4
-            d2h += 4 * h[4]
+            d2h += 4 * h[4] * cfg.tasks
         sync_all()
         wall = time.perf_counter() - t0
         tw = torch.tensor([wall, q_e2e], dtype=torch.float64, device="cuda")
@@ -408,15 +410,15 @@ def run_ours(args):
         mb = args.mlp_batch
         mm = RecModel(cfg.with_(rows=1000), seed=1, max_batch=mb, streams=1, device=local)
         fb = sum(2 * x * y for x, y in zip(cfg.bottom[:-1], cfg.bottom[1:]))
-        wt = [cfg.dim + cfg.num_tables * (cfg.num_tables + 1) // 2] + list(cfg.top)
-        ft = sum(2 * x * y for x, y in zip(wt[:-1], wt[1:]))
+        wt = [cfg.top_in] + list(cfg.top)
+        ft = cfg.tasks * sum(2 * x * y for x, y in zip(wt[:-1], wt[1:]))
         tb = mm.rec_bench_mlp(0, mb, 20)
         ti = mm.rec_bench_mlp(2, mb, 20)
         tt = mm.rec_bench_mlp(1, mb, 20)
         mm.close()
         mlp_large = {"batch": mb,
-                     "bottom": {"us": 1e3 * tb, "tflops": fb * mb / (tb * 1e-3) / 1e12,
-                                "frac": fb * mb / (tb * 1e-3) / 1e12 / bf16_peak},
+                     "bottom": ({"us": 1e3 * tb, "tflops": fb * mb / (tb * 1e-3) / 1e12,
+                                 "frac": fb * mb / (tb * 1e-3) / 1e12 / bf16_peak} if fb else None),
                      "top": {"us": 1e3 * (tt - ti), "tflops": ft * mb / ((tt - ti) * 1e-3) / 1e12,
                              "frac": ft * mb / ((tt - ti) * 1e-3) / 1e12 / bf16_peak},
                      "measured": "rec_bench_mlp: 20 back-to-back launches of each stage on one stream "

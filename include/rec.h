@@ -76,7 +76,16 @@ typedef struct {
   const void* nccl_id;            /* 128-byte ncclUniqueId shared by all ranks (world > 1)  */
   int64_t l2_persist_bytes;       /* > 0: L2 persisting window over the hot row prefix of
                                      every table (A10/D2 residue), 0 = off       */
+  int32_t arch;                   /* REC_ARCH_DLRM (0) | REC_ARCH_MTWND (1), SURVEY 8(f)4:
+                                     MT-WnD (Table I; R26-R29) has no bottom MLP
+                                     (n_bottom = 0, no dense input), concatenates the T
+                                     looked-up vectors (top input T*D) and runs n_tasks
+                                     towers top_widths, each plus a wide linear part       */
+  int32_t n_tasks;                /* MT-WnD task towers N in [1, 8]; DLRM: 0 or 1          */
 } rec_model_desc;
+
+#define REC_ARCH_DLRM 0
+#define REC_ARCH_MTWND 1
 
 /* Build the model: validate, allocate the fp32 table arena and the bf16 weights,
  * generate all parameters on the device from `seed` (G4/G5), encode TMA tensor maps,
@@ -86,7 +95,8 @@ rec_status rec_model_create(const rec_model_desc* desc, rec_model_t* out);
 void rec_model_destroy(rec_model_t m);                       /* NULL-safe; frees everything */
 
 /* One batched query forward: SLS -> bottom MLP -> dot interaction ->
- * top MLP -> sigmoid.  dense [B][F] fp32 row-major (F = bottom_widths[0]);
+ * top MLP -> sigmoid (MT-WnD: lookups -> concat -> towers + wide, ctr [B][n_tasks] item-major,
+ * dense unused and may be NULL).  dense [B][F] fp32 row-major (F = bottom_widths[0]);
  * indices [nnz] int32 and offsets [T*B+1] int32 in table-major CSR (bag g = t*B + b
  * spans indices[offsets[g] .. offsets[g+1])); ctr [B] fp32 out.  Host or device
  * pointers.  Synchronous.  Errors: INVALID_ARG (batch <= 0 or > max_batch),

@@ -44,7 +44,8 @@ class rec_model_desc(C.Structure):
                 ("top_shift", C.c_int32), ("seed", C.c_uint64), ("value_mode", C.c_int32),
                 ("index_dist", C.c_int32), ("max_batch", C.c_int32), ("streams", C.c_int32),
                 ("device", C.c_int32), ("shard", C.c_int32), ("rank", C.c_int32),
-                ("world", C.c_int32), ("nccl_id", C.c_void_p), ("l2_persist_bytes", C.c_int64)]
+                ("world", C.c_int32), ("nccl_id", C.c_void_p), ("l2_persist_bytes", C.c_int64),
+                ("arch", C.c_int32), ("n_tasks", C.c_int32)]
 
 
 class rec_serve_policy(C.Structure):
@@ -178,6 +179,8 @@ class RecModel:
         d.shard, d.rank, d.world = shard, rank, world
         d.nccl_id = C.cast(self._nccl, C.c_void_p) if self._nccl is not None else None
         d.l2_persist_bytes = l2_persist_bytes
+        d.arch = getattr(cfg, "arch", 0)
+        d.n_tasks = getattr(cfg, "tasks", 1)
         self.desc = d
         self.max_batch = d.max_batch
         self.streams = streams

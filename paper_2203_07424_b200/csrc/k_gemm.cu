@@ -184,9 +184,11 @@ __global__ void __launch_bounds__(128, 1)
     }
   }
   if (args.mode == GEMM_OUT_CTR && row_ok) {
-    const float logit = dot + args.b_last;
-    args.ctr[row] = 1.f / (1.f + __expf(-logit));
-    if (args.logit) args.logit[row] = logit;
+    float logit = dot + args.b_last;
+    if (args.logit_add) logit += args.logit_add[static_cast<int64_t>(row) * args.add_stride];
+    const int64_t o = static_cast<int64_t>(row) * (args.ctr_stride > 0 ? args.ctr_stride : 1);
+    args.ctr[o] = 1.f / (1.f + __expf(-logit));
+    if (args.logit) args.logit[o] = logit;
   }
   }
   sm100::tc_fence_before();

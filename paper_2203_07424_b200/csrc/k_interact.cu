@@ -102,4 +102,47 @@ void launch_interact(const float* X, int B, const int* dB, int T, int D, __nv_bf
   cudaLaunchKernelEx(&cfg, k_interact, X, B, dB, T, D, A_top, ld_top, wpc);
 }
 
+// MT-WnD join (R26, R28): one warp per item; the concatenated pooled vectors become the bf16
+// A row of the first tower layer, and each task's wide term is an fp32 dot product whose
+// lane-strided partial sums meet in a fixed xor-shuffle tree (deterministic; with int8 x 2^e
+// tables and weights every product and partial sum is exact, so the order is immaterial).
+__global__ void k_concat(const float* __restrict__ X, int B, const int* __restrict__ dB, int T, int D,
+                         __nv_bfloat16* __restrict__ A, int ld, const float* __restrict__ v,
+                         int n_tasks, float* __restrict__ wide) {
+  if (dB) B = *dB;
+  const int warps = blockDim.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int K = T * D;
+  for (int b = blockIdx.x * warps + (threadIdx.x >> 5); b < B; b += gridDim.x * warps) {
+    const float* u = X + static_cast<int64_t>(b) * (T + 1) * D + D;  // slots 1..T
+    __nv_bfloat16* a = A + static_cast<int64_t>(b) * ld;
+    float part[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) part[k] = 0.f;
+    for (int c = lane; c < ld; c += 32) {
+      const float x = c < K ? u[c] : 0.f;
+      a[c] = __float2bfloat16_rn(x);
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (k < n_tasks && c < K) part[k] = fmaf(x, __ldg(&v[static_cast<int64_t>(k) * K + c]), part[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      if (k >= n_tasks) break;
+      float p = part[k];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) p += __shfl_xor_sync(0xffffffffu, p, o);
+      if (lane == 0) wide[static_cast<int64_t>(b) * n_tasks + k] = p;
+    }
+  }
+}
+
+void launch_concat(const float* X, int B, const int* dB, int T, int D, __nv_bfloat16* A_top, int ld,
+                   const float* v, int n_tasks, float* wide, cudaStream_t s) {
+  if (B <= 0) return;
+  int blocks = (B + 7) / 8;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  k_concat<<<blocks, 256, 0, s>>>(X, B, dB, T, D, A_top, ld, v, n_tasks, wide);
+}
+
 }  // namespace rec

@@ -284,6 +284,7 @@ __global__ void k_dense_to_bf16(const float* __restrict__ d, int B, int F, int F
 void launch_dense_to_bf16(const float* dense, int B, int F, int Fpad, __nv_bfloat16* out,
                           cudaStream_t s) {
   const int64_t n = (int64_t)B * Fpad;
+  if (n == 0) return;  // no dense input (MT-WnD)
   int blocks = static_cast<int>((n + 255) / 256);
   if (blocks > 148 * 16) blocks = 148 * 16;
   k_dense_to_bf16<<<blocks, 256, 0, s>>>(dense, B, F, Fpad, out);

@@ -140,8 +140,11 @@ struct GemmArgs {
   float* out_f32;           // mode 1: X base; row r col c -> out_f32[r*ldo + c]
   const float* w_last;      // mode 2: [N] final width-1 layer
   float b_last;
-  float* ctr;               // mode 2: [M]
-  float* logit;             // mode 2: [M] optional
+  float* ctr;               // mode 2: [M] (element r * ctr_stride)
+  float* logit;             // mode 2: [M] optional (same stride)
+  int ctr_stride;           // mode 2: 0 or 1 = dense; MT-WnD: n_tasks (item-major [M][N])
+  const float* logit_add;   // mode 2: optional per-row addend (MT-WnD wide part) ...
+  int add_stride;           // ... at logit_add[r * add_stride]
 };
 int gemm_bn(int N);                  // tile width used for a layer of width N (W tmap box)
 void gemm_prepare();                 // per-device one-time kernel attributes
@@ -192,6 +195,10 @@ extern int g_gemm_stages;
 extern int g_interact_wpc;  // interaction warps per CTA (REC_INTERACT_WPC)  // per-layer GEMM ring depth cap (REC_GEMM_STAGES; 0 = maximum)
 
 // --------------------------------------------------------------- interaction (a5)
+// MT-WnD (R26, R28): A_top[b] = bf16(X[b][1..T] concatenated) ++ 0-pad (ld = Ktop_pad) and
+// wide[b][k] = sum_c u[c] v_k[c] (fp32) for the n_tasks wide vectors v [n_tasks][T*D].
+void launch_concat(const float* X, int B, const int* dB, int T, int D, __nv_bfloat16* A_top, int ld,
+                   const float* v, int n_tasks, float* wide, cudaStream_t s);
 void launch_interact(const float* X, int B, const int* dB, int T, int D, __nv_bfloat16* A_top,
                      int ld_top, cudaStream_t s);
 

@@ -104,6 +104,7 @@ void enqueue_bottom(rec_model_s* m, Workspace& w, cudaStream_t st, int B, const 
                     cudaEvent_t* gev) {
   const int T = m->T, D = m->D;
   const int nb = static_cast<int>(m->bottom.size());
+  if (nb == 0) return;    // MT-WnD: no Bottom-FC
   if (m->chain_bottom) {  // whole bottom MLP in one kernel (k_mlp.cu)
     ChainArgs a = m->chain_bottom_args;
     a.M = B;
@@ -144,6 +145,46 @@ void enqueue_bottom(rec_model_s* m, Workspace& w, cudaStream_t st, int B, const 
 void enqueue_interact_top(rec_model_s* m, Workspace& w, cudaStream_t st, int B, const int* dB,
                           float* ctr_out, float* logit_out, cudaEvent_t* gev) {
   const int T = m->T, D = m->D;
+  if (m->arch == REC_ARCH_MTWND) {  // concat + wide part, then one tower per task
+    cudaEvent_t e1 = gev ? nullptr : prof_begin(m, st);
+    launch_concat(w.X, B, dB, T, D, w.A_top, m->Ktop_pad, m->wide_v, m->tasks, w.wide, st);
+    prof_end(m, st, 2, e1);
+    mark(gev, 4, st);
+    const int nt = static_cast<int>(m->top.size());
+    for (int k = 0; k < m->tasks; ++k) {
+      const std::vector<Layer>& Ls = k == 0 ? m->top : m->towers[k - 1];
+      for (int j = 0; j < nt; ++j) {
+        const Layer& L = Ls[j];
+        GemmArgs a{};
+        a.M = B;
+        a.dM = dB;
+        a.N = L.N;
+        a.K = L.K;
+        a.bias = L.bias;
+        a.relu = 1;
+        if (j == nt - 1) {
+          a.mode = GEMM_OUT_CTR;
+          a.w_last = k == 0 ? m->w_last : m->w_last_t[k - 1];
+          a.b_last = k == 0 ? m->b_last : m->b_last_t[k - 1];
+          a.ctr = ctr_out + k;
+          a.logit = logit_out ? logit_out + k : nullptr;
+          a.ctr_stride = m->tasks;
+          a.logit_add = w.wide + k;
+          a.add_stride = m->tasks;
+        } else {
+          a.mode = GEMM_OUT_BF16;
+          a.out_bf16 = static_cast<__nv_bfloat16*>(w.out_top[j]);
+          a.ldo = L.Npad;
+        }
+        cudaEvent_t e = gev ? nullptr : prof_begin(m, st);
+        launch_gemm_tc(&w.tmap_a_top[j], &L.tmap_w, a, st);
+        prof_end(m, st, 1, e);
+      }
+    }
+    mark(gev, 5, st);
+    m->launches += 1 + m->tasks * nt;
+    return;
+  }
   // a5: interaction -> A_top
   cudaEvent_t e1 = gev ? nullptr : prof_begin(m, st);
   launch_interact(w.X, B, dB, T, D, w.A_top, m->Ktop_pad, st);
@@ -296,7 +337,7 @@ static rec_status synth_chain(rec_model_s* m, Workspace& w, SynthSlot& sl, bool 
   cudaStream_t s = w.stream, sb = w.stream_b;
   cudaEvent_t* gev = capture && with_events ? sl.ev : nullptr;
   mark(gev, 0, s);
-  if (!materialize && m->lo == m->hi && m->fuse_dense) {
+  if (!materialize && m->lo == m->hi && (m->fuse_dense || m->F == 0)) {
     // dense features generated inside the SLS kernel: one stream, SLS -> bottom -> top
     mark(gev, 1, s);
     cudaEvent_t e0 = gev ? nullptr : prof_begin(m, s);
@@ -561,7 +602,7 @@ static rec_status sync_ws(Workspace& w) {
 static rec_status query_impl(rec_model_s* m, const float* dense, const int32_t* indices,
                              const int32_t* offsets, int32_t B, float* ctr, float* pooled,
                              float* logits) {
-  if (!m || !dense || !indices || !offsets || !ctr) {
+  if (!m || !indices || !offsets || !ctr || (!dense && m->F > 0)) {
     set_error("null argument (model, dense, indices, offsets and ctr are required)");
     return REC_E_INVALID_ARG;
   }
@@ -622,7 +663,7 @@ static rec_status query_impl(rec_model_s* m, const float* dense, const int32_t* 
     }
   }
   const float* d_dense = dense;
-  if (!den_dev) {
+  if (!den_dev && m->F > 0) {
     memcpy(pin + pos, dense, sizeof(float) * B * m->F);
     REC_CUDA(cudaMemcpyAsync(w.dense_f32, pin + pos, sizeof(float) * B * m->F,
                              cudaMemcpyHostToDevice, s));
@@ -639,8 +680,9 @@ static rec_status query_impl(rec_model_s* m, const float* dense, const int32_t* 
   REC_CUDA(cudaStreamSynchronize(s));
   st = read_flag(w);
   if (st != REC_OK) return st;
-  REC_CUDA(cudaMemcpyAsync(ctr, w.ctr, sizeof(float) * B, cudaMemcpyDefault, s));
-  if (logits) REC_CUDA(cudaMemcpyAsync(logits, w.logit, sizeof(float) * B, cudaMemcpyDefault, s));
+  REC_CUDA(cudaMemcpyAsync(ctr, w.ctr, sizeof(float) * B * m->tasks, cudaMemcpyDefault, s));
+  if (logits)
+    REC_CUDA(cudaMemcpyAsync(logits, w.logit, sizeof(float) * B * m->tasks, cudaMemcpyDefault, s));
   if (pooled) {
     const int D = m->D;
     REC_CUDA(cudaMemcpy2DAsync(pooled, sizeof(float) * T * D, w.X + D, sizeof(float) * (T + 1) * D,
@@ -743,6 +785,13 @@ static void free_model(rec_model_s* m) {
     cudaFree(L.bias);
   }
   cudaFree(m->w_last);
+  for (auto& tw : m->towers)
+    for (auto& L : tw) {
+      cudaFree(L.W);
+      cudaFree(L.bias);
+    }
+  for (float* p : m->w_last_t) cudaFree(p);
+  cudaFree(m->wide_v);
   cudaFree(m->bias_bottom_all);
   cudaFree(m->bias_top_all);
   cudaFree(m->tables);
@@ -810,7 +859,24 @@ rec_status rec_model_create(const rec_model_desc* d, rec_model_t* out) {
     set_error("dim = %d must be a positive multiple of 4 and <= 128", d->dim);
     return d->dim <= 0 ? REC_E_INVALID_ARG : REC_E_UNSUPPORTED;
   }
-  if (!d->bottom_widths || d->n_bottom < 2) {
+  const bool mtwnd = d->arch == REC_ARCH_MTWND;
+  if (d->arch != REC_ARCH_DLRM && !mtwnd) {
+    set_error("arch = %d unknown", d->arch);
+    return REC_E_INVALID_ARG;
+  }
+  if (mtwnd ? (d->n_tasks < 1 || d->n_tasks > 8) : (d->n_tasks > 1 || d->n_tasks < 0)) {
+    set_error("n_tasks = %d: MT-WnD needs 1..8 task towers, DLRM 0 or 1", d->n_tasks);
+    return REC_E_INVALID_ARG;
+  }
+  if (mtwnd && d->n_bottom != 0) {
+    set_error("MT-WnD has no bottom MLP: n_bottom must be 0 (Table I, P:191)");
+    return REC_E_INVALID_ARG;
+  }
+  if (mtwnd && d->shard != REC_SHARD_REPLICA) {
+    set_error("MT-WnD serves as replicas (no sharded mode)");
+    return REC_E_UNSUPPORTED;
+  }
+  if (!mtwnd && (!d->bottom_widths || d->n_bottom < 2)) {
     set_error("bottom_widths must list >= 2 widths (input first, R3)");
     return REC_E_INVALID_ARG;
   }
@@ -828,7 +894,7 @@ rec_status rec_model_create(const rec_model_desc* d, rec_model_t* out) {
       set_error("top_widths[%d] = %d out of [1, 16384]", i, d->top_widths[i]);
       return REC_E_INVALID_ARG;
     }
-  if (d->bottom_widths[d->n_bottom - 1] != d->dim) {
+  if (!mtwnd && d->bottom_widths[d->n_bottom - 1] != d->dim) {
     set_error("dim = %d must equal bottom_widths[n_bottom-1] = %d (dot interaction, R4)", d->dim,
               d->bottom_widths[d->n_bottom - 1]);
     return REC_E_INVALID_ARG;
@@ -904,9 +970,11 @@ rec_status rec_model_create(const rec_model_desc* d, rec_model_t* out) {
   m->T = d->num_tables;
   m->D = d->dim;
   m->rows.assign(d->rows, d->rows + d->num_tables);
-  m->bottom_w.assign(d->bottom_widths, d->bottom_widths + d->n_bottom);
+  if (d->n_bottom > 0) m->bottom_w.assign(d->bottom_widths, d->bottom_widths + d->n_bottom);
   m->top_w.assign(d->top_widths, d->top_widths + d->n_top);
-  m->F = m->bottom_w[0];
+  m->arch = d->arch;
+  m->tasks = mtwnd ? d->n_tasks : 1;
+  m->F = mtwnd ? 0 : m->bottom_w[0];
   m->Fpad = pad8(m->F);
   m->lo = d->pooling_lo;
   m->hi = d->pooling_hi;
@@ -1043,7 +1111,7 @@ rec_status rec_model_create(const rec_model_desc* d, rec_model_t* out) {
     }
     return REC_OK;
   };
-  const int nbl = d->n_bottom - 1;
+  const int nbl = std::max(0, d->n_bottom - 1);
   m->bottom.resize(nbl);
   for (int l = 0; l < nbl; ++l) {
     rec_status st = make_layer(m->bottom_w[l], m->bottom_w[l + 1], l, 0, m->bottom[l]);
@@ -1052,7 +1120,7 @@ rec_status rec_model_create(const rec_model_desc* d, rec_model_t* out) {
       return st;
     }
   }
-  m->Ktop = D + T * (T + 1) / 2;
+  m->Ktop = m->arch == REC_ARCH_MTWND ? T * D : D + T * (T + 1) / 2;
   m->Ktop_pad = pad8(m->Ktop);
   std::vector<int> tw;
   tw.push_back(m->Ktop);
@@ -1072,6 +1140,39 @@ rec_status rec_model_create(const rec_model_desc* d, rec_model_t* out) {
     const int ef = -7 + wexp(Kf) - (ntl == 0 ? m->top_shift : 0);
     launch_init_final(m->w_last, m->w_last + Kf, Kf, TOP_LAYER_BASE + ntl, ef, m->k0, m->k1, 0);
     CHECK_CUDA_CREATE(cudaMemcpy(&m->b_last, m->w_last + Kf, sizeof(float), cudaMemcpyDeviceToHost));
+  }
+  if (m->arch == REC_ARCH_MTWND) {
+    // towers of tasks 1..N-1 (layer ids TOP_LAYER_BASE + 16 k + l, oracle/gen.py) and the wide
+    // vectors of every task (id TOP_LAYER_BASE + 16 k + 15: the weight row of a fan-out-1 layer)
+    constexpr int kTaskStride = 16, kWide = 15;
+    m->towers.resize(m->tasks - 1);
+    m->w_last_t.assign(m->tasks - 1, nullptr);
+    m->b_last_t.assign(m->tasks - 1, 0.f);
+    const int Kf = tw[ntl];
+    for (int k = 1; k < m->tasks; ++k) {
+      auto& L = m->towers[k - 1];
+      L.resize(ntl);
+      for (int j = 0; j < ntl; ++j) {
+        rec_status st = make_layer(tw[j], tw[j + 1], TOP_LAYER_BASE + kTaskStride * k + j,
+                                   j == 0 ? m->top_shift : 0, L[j]);
+        if (st != REC_OK) {
+          free_model(m);
+          return st;
+        }
+      }
+      ALLOC(m->w_last_t[k - 1], sizeof(float) * (Kf + 1));
+      const int ef = -7 + wexp(Kf) - (ntl == 0 ? m->top_shift : 0);
+      launch_init_final(m->w_last_t[k - 1], m->w_last_t[k - 1] + Kf, Kf,
+                        TOP_LAYER_BASE + kTaskStride * k + ntl, ef, m->k0, m->k1, 0);
+      CHECK_CUDA_CREATE(cudaMemcpy(&m->b_last_t[k - 1], m->w_last_t[k - 1] + Kf, sizeof(float),
+                                   cudaMemcpyDeviceToHost));
+    }
+    ALLOC(m->wide_v, sizeof(float) * (int64_t(m->tasks) * m->Ktop + 1));
+    const int ew = -7 + wexp(m->Ktop) - m->top_shift;
+    for (int k = 0; k < m->tasks; ++k)  // row k of [N][Ktop]; the "bias" lands on row k+1's
+      launch_init_final(m->wide_v + int64_t(k) * m->Ktop, m->wide_v + int64_t(k + 1) * m->Ktop,
+                        m->Ktop, TOP_LAYER_BASE + kTaskStride * k + kWide, ew, m->k0, m->k1, 0);
+    CHECK_CUDA_CREATE(cudaDeviceSynchronize());  // (row k's bias slot is rewritten by row k+1)
   }
   m->hmax = 8;
   for (int l = 1; l < d->n_bottom - 1; ++l) m->hmax = std::max(m->hmax, pad8(m->bottom_w[l]));
@@ -1120,7 +1221,8 @@ rec_status rec_model_create(const rec_model_desc* d, rec_model_t* out) {
     };
     CHECK_CUDA_CREATE(cudaDeviceSynchronize());  // biases initialised
     m->chain_bottom = build(m->bottom, m->chain_bottom_args, &m->bias_bottom_all, GEMM_OUT_X_F32);
-    m->chain_top = build(m->top, m->chain_top_args, &m->bias_top_all, GEMM_OUT_CTR);
+    if (m->arch == REC_ARCH_DLRM)  // MT-WnD towers run as per-layer GEMMs (1024-wide)
+      m->chain_top = build(m->top, m->chain_top_args, &m->bias_top_all, GEMM_OUT_CTR);
   }
 
   // ---------------------------------------------------------------- workspaces
@@ -1145,14 +1247,15 @@ rec_status rec_model_create(const rec_model_desc* d, rec_model_t* out) {
     ALLOC(w.segs, sizeof(int4) * cap);
     ALLOC(w.rowq, sizeof(int) * cap);
     ALLOC(w.rowi, sizeof(int) * cap);
-    ALLOC(w.dense_f32, sizeof(float) * int64_t(cap) * m->F);
-    ALLOC(w.dense_bf, sizeof(__nv_bfloat16) * int64_t(cap) * m->Fpad);
+    ALLOC(w.dense_f32, sizeof(float) * int64_t(cap) * std::max(m->F, 1));
+    ALLOC(w.dense_bf, sizeof(__nv_bfloat16) * int64_t(cap) * std::max(m->Fpad, 8));
     ALLOC(w.X, sizeof(float) * int64_t(cap) * (T + 1) * D);
     ALLOC(w.A_top, sizeof(__nv_bfloat16) * int64_t(cap) * m->Ktop_pad);
     ALLOC(w.h[0], sizeof(__nv_bfloat16) * int64_t(cap) * m->hmax);
     ALLOC(w.h[1], sizeof(__nv_bfloat16) * int64_t(cap) * m->hmax);
-    ALLOC(w.ctr, sizeof(float) * cap);
-    ALLOC(w.logit, sizeof(float) * cap);
+    ALLOC(w.ctr, sizeof(float) * cap * m->tasks);
+    ALLOC(w.logit, sizeof(float) * cap * m->tasks);
+    if (m->arch == REC_ARCH_MTWND) ALLOC(w.wide, sizeof(float) * cap * m->tasks);
     ALLOC(w.flag, sizeof(int));
     CHECK_CUDA_CREATE(cudaMemset(w.flag, 0, sizeof(int)));
     CHECK_CUDA_CREATE(cudaMemset(w.dense_bf, 0, sizeof(__nv_bfloat16) * int64_t(cap) * m->Fpad));
@@ -1203,7 +1306,8 @@ rec_status rec_model_create(const rec_model_desc* d, rec_model_t* out) {
         *ws_[l] = nch == 128 ? L.tmap_w128 : L.tmap_w;
       }
     };
-    fill_maps(w.chain_bottom, w.tmap_a_bottom[0], m->bottom, m->chain_bottom_args.nchunk);
+    if (!m->bottom.empty())
+      fill_maps(w.chain_bottom, w.tmap_a_bottom[0], m->bottom, m->chain_bottom_args.nchunk);
     fill_maps(w.chain_top, w.tmap_a_top[0], m->top, m->chain_top_args.nchunk);
   }
   // synthetic-batch staging ring + one captured CUDA graph per slot (a2-a6 chain)
@@ -1282,7 +1386,7 @@ rec_status rec_query_debug(rec_model_t m, const float* dense, const int32_t* ind
 
 rec_status rec_query_async(rec_model_t m, int32_t slot, const float* dense, const int32_t* indices,
                            const int32_t* offsets, int64_t nnz, int32_t batch, float* ctr) {
-  if (!m || !dense || !indices || !offsets || !ctr) {
+  if (!m || !indices || !offsets || !ctr || (!dense && m->F > 0)) {
     set_error("null argument");
     return REC_E_INVALID_ARG;
   }
@@ -1327,7 +1431,7 @@ rec_status rec_query_async(rec_model_t m, int32_t slot, const float* dense, cons
     REC_CUDA(cudaMemcpyAsync(w.indices, indices, sizeof(int) * nnz, cudaMemcpyHostToDevice, s));
     d_idx = w.indices;
   }
-  if (!is_device_ptr(dense)) {
+  if (m->F > 0 && !is_device_ptr(dense)) {
     REC_CUDA(cudaMemcpyAsync(w.dense_f32, dense, sizeof(float) * batch * m->F, cudaMemcpyHostToDevice, s));
     d_dense = w.dense_f32;
   }
@@ -1337,7 +1441,8 @@ rec_status rec_query_async(rec_model_t m, int32_t slot, const float* dense, cons
   m->launches += 2;
   rec_status st = forward_enqueue(m, w, d_idx, d_off, batch, nullptr, ctr_dev ? ctr : w.ctr, w.logit, nullptr);
   if (st != REC_OK) return st;
-  if (!ctr_dev) REC_CUDA(cudaMemcpyAsync(ctr, w.ctr, sizeof(float) * batch, cudaMemcpyDeviceToHost, s));
+  if (!ctr_dev)
+    REC_CUDA(cudaMemcpyAsync(ctr, w.ctr, sizeof(float) * batch * m->tasks, cudaMemcpyDeviceToHost, s));
   return REC_OK;
 }
 
@@ -1361,7 +1466,7 @@ rec_status rec_synth_query_async(rec_model_t m, int32_t slot, const int32_t* seg
   rec_status st = synth_submit(m, w, segs, nseg, &B, nullptr);
   if (st != REC_OK) return st;
   if (ctr && ctr != w.ctr)
-    REC_CUDA(cudaMemcpyAsync(ctr, w.ctr, sizeof(float) * B, cudaMemcpyDeviceToDevice, w.stream));
+    REC_CUDA(cudaMemcpyAsync(ctr, w.ctr, sizeof(float) * B * m->tasks, cudaMemcpyDeviceToDevice, w.stream));
   return REC_OK;
 }
 
@@ -1426,7 +1531,8 @@ rec_status rec_gen_batch(rec_model_t m, const int32_t* segs, int32_t nseg, int32
   nnz = *w.flag_host;
   *w.flag_host = 0;
   REC_CUDA(cudaMemcpyAsync(indices, w.indices, sizeof(int) * nnz, cudaMemcpyDefault, s));
-  REC_CUDA(cudaMemcpyAsync(dense, w.dense_f32, sizeof(float) * B * m->F, cudaMemcpyDefault, s));
+  if (m->F > 0)
+    REC_CUDA(cudaMemcpyAsync(dense, w.dense_f32, sizeof(float) * B * m->F, cudaMemcpyDefault, s));
   REC_CUDA(cudaStreamSynchronize(s));
   return REC_OK;
 }
@@ -1447,6 +1553,8 @@ rec_status rec_bench_mlp(rec_model_t m, int32_t which, int32_t batch, int32_t it
   auto once = [&]() {
     if (which == 0) enqueue_bottom(m, w, s, batch, nullptr, nullptr);
     else if (which == 1) enqueue_interact_top(m, w, s, batch, nullptr, w.ctr, w.logit, nullptr);
+    else if (m->arch == REC_ARCH_MTWND)
+      launch_concat(w.X, batch, nullptr, m->T, m->D, w.A_top, m->Ktop_pad, m->wide_v, m->tasks, w.wide, s);
     else launch_interact(w.X, batch, nullptr, m->T, m->D, w.A_top, m->Ktop_pad, s);
   };
   for (int i = 0; i < 3; ++i) once();

@@ -73,8 +73,9 @@ struct Workspace {
   float* X = nullptr;                // [cap][T+1][D]
   __nv_bfloat16* A_top = nullptr;    // [cap][Ktop_pad]
   __nv_bfloat16* h[2] = {nullptr, nullptr};  // hidden ping-pong [cap][hmax]
-  float* ctr = nullptr;              // [cap]
-  float* logit = nullptr;            // [cap]
+  float* ctr = nullptr;              // [cap][n_tasks]
+  float* logit = nullptr;            // [cap][n_tasks]
+  float* wide = nullptr;             // MT-WnD: [cap][n_tasks] wide-part logits
   int* flag = nullptr;               // device error flags (bit0 OOB, bit1 offsets)
   int* flag_host = nullptr;          // pinned mirror
   uint8_t* pin = nullptr;            // pinned staging
@@ -143,6 +144,13 @@ struct rec_model_s {
   std::vector<rec::Layer> bottom, top;  // top excludes the width-1 output layer
   float* w_last = nullptr;
   float b_last = 0.f;
+  // MT-WnD (arch 1): towers of tasks 1..N-1 (task 0 = `top`), their output layers, and the
+  // wide vectors of all tasks [N][Ktop]
+  int arch = 0, tasks = 1;
+  std::vector<std::vector<rec::Layer>> towers;
+  std::vector<float*> w_last_t;
+  std::vector<float> b_last_t;
+  float* wide_v = nullptr;
   // fused FC stacks (one kernel per MLP per 128-row tile) when they fit
   bool chain_bottom = false, chain_top = false;
   rec::ChainArgs chain_bottom_args{}, chain_top_args{};

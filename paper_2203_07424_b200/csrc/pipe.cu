@@ -203,8 +203,8 @@ rec_status pipe_submit(rec_model_s* m, const int32_t* segs, const int64_t* batch
                           std::chrono::steady_clock::now().time_since_epoch()).count();
     if (ctr_out) {
       for (int i = 0; i < N; ++i) {
-        REC_CUDA(cudaMemcpyAsync(ctr_out + item0, m->ws[L.ws[i]].ctr, sizeof(float) * Bs[i],
-                                 cudaMemcpyDeviceToDevice, head.stream));
+        REC_CUDA(cudaMemcpyAsync(ctr_out + item0 * m->tasks, m->ws[L.ws[i]].ctr,
+                                 sizeof(float) * Bs[i] * m->tasks, cudaMemcpyDeviceToDevice, head.stream));
         item0 += Bs[i];
       }
     }
@@ -223,8 +223,8 @@ rec_status pipe_submit(rec_model_s* m, const int32_t* segs, const int64_t* batch
     rec_status st = synth_submit(m, w, segs + 3 * s0, static_cast<int>(s1 - s0), &B, nullptr);
     if (st != REC_OK) return st;
     if (ctr_out) {
-      REC_CUDA(cudaMemcpyAsync(ctr_out + item0, w.ctr, sizeof(float) * B, cudaMemcpyDeviceToDevice,
-                               w.stream));
+      REC_CUDA(cudaMemcpyAsync(ctr_out + item0 * m->tasks, w.ctr, sizeof(float) * B * m->tasks,
+                               cudaMemcpyDeviceToDevice, w.stream));
       item0 += B;
     }
   }
@@ -243,8 +243,8 @@ rec_status rec_set_pipeline(rec_model_t m, int32_t lanes) {
     set_error("lanes = %d: must be 0 or divide streams = %d into groups of 2..64", lanes, m->nstreams);
     return REC_E_INVALID_ARG;
   }
-  if (lanes > 0 && (m->lo != m->hi || (m->world > 1 && m->shard != REC_SHARD_REPLICA))) {
-    set_error("pipeline lanes need fixed pooling and an unsharded model");
+  if (lanes > 0 && (m->lo != m->hi || m->F == 0 || (m->world > 1 && m->shard != REC_SHARD_REPLICA))) {
+    set_error("pipeline lanes need fixed pooling, a bottom MLP and an unsharded model");
     return REC_E_UNSUPPORTED;
   }
   REC_CUDA(cudaSetDevice(m->device));

@@ -192,7 +192,8 @@ static rec_status host_input_enqueue(rec_model_s* m, Workspace& w, const HostInp
   REC_CUDA(cudaMemcpyAsync(w.offsets, off, sizeof(int32_t) * (static_cast<size_t>(T) * B + 1),
                            cudaMemcpyHostToDevice, s));
   REC_CUDA(cudaMemcpyAsync(w.indices, idx, sizeof(int32_t) * nnz, cudaMemcpyHostToDevice, s));
-  REC_CUDA(cudaMemcpyAsync(w.dense_f32, dn, sizeof(float) * B * F, cudaMemcpyHostToDevice, s));
+  if (F > 0)
+    REC_CUDA(cudaMemcpyAsync(w.dense_f32, dn, sizeof(float) * B * F, cudaMemcpyHostToDevice, s));
   REC_CUDA(cudaEventRecord(w.pin_free, s));
   launch_dense_to_bf16(w.dense_f32, B, F, m->Fpad, w.dense_bf, s);
   m->launches += 1;
@@ -310,7 +311,8 @@ rec_status rec_serve(rec_model_t m, const rec_trace_row* trace, int64_t n, doubl
   std::vector<Lane> lanes(M);
   for (int s = 0; s < M; ++s) {
     REC_CUDA(cudaEventCreateWithFlags(&lanes[s].done, cudaEventDisableTiming));
-    if (ctr_out) REC_CUDA(cudaMallocHost(reinterpret_cast<void**>(&lanes[s].ctr_host), sizeof(float) * d));
+    if (ctr_out)
+      REC_CUDA(cudaMallocHost(reinterpret_cast<void**>(&lanes[s].ctr_host), sizeof(float) * d * m->tasks));
     if (!virt) {  // host-mapped completion word (falls back to event polling if unavailable)
       void* hp = nullptr;
       void* dp = nullptr;
@@ -365,7 +367,8 @@ rec_status rec_serve(rec_model_t m, const rec_trace_row* trace, int64_t n, doubl
       int row = 0;
       for (int64_t c = bt.first_chunk; c < bt.first_chunk + bt.nchunks; ++c) {
         const Chunk& ch = fifo[c];
-        memcpy(ctr_out + item_base[ch.pos] + ch.start, src + row, sizeof(float) * ch.len);
+        memcpy(ctr_out + (item_base[ch.pos] + ch.start) * m->tasks, src + int64_t(row) * m->tasks,
+               sizeof(float) * ch.len * m->tasks);
         row += ch.len;
       }
     }
@@ -393,7 +396,8 @@ rec_status rec_serve(rec_model_t m, const rec_trace_row* trace, int64_t n, doubl
       if (st != REC_OK) return st;
     }
     if (ctr_out)
-      REC_CUDA(cudaMemcpyAsync(lanes[s].ctr_host, w.ctr, sizeof(float) * B, cudaMemcpyDeviceToHost, w.stream));
+      REC_CUDA(cudaMemcpyAsync(lanes[s].ctr_host, w.ctr, sizeof(float) * B * m->tasks,
+                               cudaMemcpyDeviceToHost, w.stream));
     REC_CUDA(cudaEventRecord(lanes[s].done, w.stream));
     lanes[s].busy = true;
     lanes[s].batch = bi;
@@ -552,7 +556,8 @@ rec_status rec_serve(rec_model_t m, const rec_trace_row* trace, int64_t n, doubl
             if (rs == REC_OK) rs = forward_enqueue(m, w, w.indices, w.offsets, B, nullptr, w.ctr, w.logit, nullptr);
           }
           if (rs == REC_OK && ctr_out)
-            if (cudaMemcpyAsync(L.ctr_host, w.ctr, sizeof(float) * B, cudaMemcpyDeviceToHost, w.stream) != cudaSuccess)
+            if (cudaMemcpyAsync(L.ctr_host, w.ctr, sizeof(float) * B * m->tasks, cudaMemcpyDeviceToHost,
+                                w.stream) != cudaSuccess)
               rs = REC_E_CUDA;
           if (rs == REC_OK) {
             ++O.seq;

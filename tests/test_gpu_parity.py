@@ -250,3 +250,35 @@ def test_large_batch_weight_sharing_gemm_invariance():
     i2, o2, d2 = gen.gen_batch(cfg, 1, sub)
     exp = fw.forward(cfg, 1, d2, i2, o2)
     assert np.abs(big[pick] - exp).max() <= CTR_TOL
+
+
+def test_mtwnd_parity_and_invariance():
+    """MT-WnD (R26-R29): one-hot lookups bit-exact, per-task CTRs within 2e-2
+    of the oracle, identical bits whatever the batch, device-synth == host inputs."""
+    import torch
+    cfg = W.small_variant(W.MTWND, 20000)
+    N = cfg.tasks
+    m = _model(cfg, max_batch=300)
+    for B in (1, 300):
+        segs = W.random_segments(B, seed=50 + B)
+        ind, off, dense = gen.gen_batch(cfg, 1, segs)
+        assert dense.shape == (B, 0)
+        gi, go, gd = m.rec_gen_batch(segs)
+        assert np.array_equal(gi, ind) and np.array_equal(go, off)
+        ctr = np.zeros((B, N), np.float32)
+        pooled = np.zeros((B, cfg.num_tables, cfg.dim), np.float32)
+        logit = np.zeros((B, N), np.float32)
+        m.rec_query_debug(dense, ind, off, B, ctr, pooled=pooled, logits=logit)
+        exp = fw.forward(cfg, 1, dense, ind, off, return_all=True)
+        assert np.array_equal(pooled.astype(np.float64), exp["pooled"])
+        assert np.abs(ctr - exp["ctr"]).max() <= CTR_TOL
+        assert np.abs(logit - exp["logit"]).max() < 0.15
+        if B == 300:
+            assert np.all(exp["logit"].std(axis=0) > 0.5)
+            # batch invariance on a sub-batch, device-synthesised path
+            q, it = gen.expand_segments(segs)
+            sub = np.array([[q[k], it[k], 1] for k in range(40, 77)], np.int32)
+            cs = torch.zeros(37 * N, device="cuda")
+            m.rec_synth_query_async(0, sub, cs)
+            m.rec_sync(0)
+            assert np.array_equal(cs.cpu().numpy().reshape(37, N), ctr[40:77])

@@ -50,9 +50,10 @@ def test_struct_layouts_match_header():
 #include <stddef.h>
 #include "rec.h"
 int main(void){
- printf("%zu %zu %zu %zu %zu\n", sizeof(rec_model_desc), offsetof(rec_model_desc, seed),
+ printf("%zu %zu %zu %zu %zu %zu %zu\n", sizeof(rec_model_desc), offsetof(rec_model_desc, seed),
         offsetof(rec_model_desc, nccl_id), offsetof(rec_model_desc, l2_persist_bytes),
-        offsetof(rec_model_desc, top_shift));
+        offsetof(rec_model_desc, top_shift), offsetof(rec_model_desc, arch),
+        offsetof(rec_model_desc, n_tasks));
  printf("%zu %zu %zu\n", sizeof(rec_serve_policy), sizeof(rec_serve_report), sizeof(rec_trace_row));
  printf("%zu %zu\n", offsetof(rec_serve_report, completed), offsetof(rec_serve_report, stable));
  return 0; }
@@ -67,7 +68,8 @@ int main(void){
     a = [int(x) for x in lines[0].split()]
     assert a == [C.sizeof(b.rec_model_desc), b.rec_model_desc.seed.offset,
                  b.rec_model_desc.nccl_id.offset, b.rec_model_desc.l2_persist_bytes.offset,
-                 b.rec_model_desc.top_shift.offset]
+                 b.rec_model_desc.top_shift.offset, b.rec_model_desc.arch.offset,
+                 b.rec_model_desc.n_tasks.offset]
     p = [int(x) for x in lines[1].split()]
     assert p == [C.sizeof(b.rec_serve_policy), C.sizeof(b.rec_serve_report), W.TRACE_DTYPE.itemsize]
     r = [int(x) for x in lines[2].split()]
