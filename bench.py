@@ -403,6 +403,23 @@ def run_ours(args):
                        "device-synth inputs, replica dispatch q mod G; Alg. 1 gradient search over "
                        "(streams, max_batch)"}
 
+    # dense stages at the serving batch d: back-to-back launches on one stream (CUDA events)
+    fb_i = sum(2 * x * y for x, y in zip(cfg.bottom[:-1], cfg.bottom[1:]))
+    wt_i = [cfg.top_in] + list(cfg.top)
+    ft_i = cfg.tasks * sum(2 * x * y for x, y in zip(wt_i[:-1], wt_i[1:]))
+    tb_d = model.rec_bench_mlp(0, d, 50) if fb_i else 0.0
+    ti_d = model.rec_bench_mlp(2, d, 50)
+    tt_d = model.rec_bench_mlp(1, d, 50)
+    mlp_serving = {"batch": d,
+                   "bottom": ({"us": 1e3 * tb_d, "tflops": fb_i * d / (tb_d * 1e-3) / 1e12}
+                              if fb_i else None),
+                   "top": {"us": 1e3 * (tt_d - ti_d),
+                           "tflops": ft_i * d / ((tt_d - ti_d) * 1e-3) / 1e12},
+                   "join_us": 1e3 * ti_d,
+                   "measured": "rec_bench_mlp at the serving batch d: 50 back-to-back launches of "
+                               "each stage on one stream (CUDA events)"}
+    mlp_step_tflops = mlp_flops_per_item(cfg) * tot_items / (ms_max * 1e-3) / 1e12 / world
+
     # MLP tensor-pipe utilisation at a large batch (north_star "MLP TC util"): the same MLP
     # stacks in a second handle with max_batch = --mlp-batch (tiny tables: SLS not involved)
     mlp_large = None
@@ -479,7 +496,10 @@ def run_ours(args):
                     "frac": (gemm_tf / bf16_peak) if gemm_tf else None, "flops_per_item": mlp_flops_per_item(cfg),
                     "launches": gemm_n, "ms": gemm_ms,
                     "measured": "per-launch CUDA events in the single-stream pass (batches <= d: "
-                                "latency-bound)", "large_batch": mlp_large},
+                                "latency-bound)", "serving_batch": mlp_serving,
+                    "in_step_aggregate": {"tflops_per_gpu": mlp_step_tflops,
+                                          "frac": mlp_step_tflops / bf16_peak},
+                    "large_batch": mlp_large},
             "breakdown_us_per_batch_single_stream": {
                 "gen": 1e3 * gen_ms / rsteps, "sls": 1e3 * sls_ms / rsteps,
                 "gemm": 1e3 * gemm_ms / rsteps, "interact": 1e3 * int_ms / rsteps},
@@ -491,6 +511,18 @@ def run_ours(args):
             "sla": sla,
             "cpu_baseline": cpu,
         }
+        if cfg.arch == W.ARCH_MTWND:
+            # one-hot lookups move ~1 KB per item; the task towers (7.4 MFLOP per item) dominate:
+            # report the tensor roofline of the tower GEMMs first, the SLS one beside it
+            top = mlp_serving["top"]
+            line["roofline_sls"] = line["roofline"]
+            line["roofline"] = {
+                "bound": "tensor", "kernel": "k_gemm_tc (task towers)", "achieved": top["tflops"],
+                "peak": bf16_peak, "unit": "TFLOP/s", "frac": top["tflops"] / bf16_peak,
+                "traffic": None, "peak_kind": peak_kind,
+                "flops_per_item": ft_i, "avg_launch_us": top["us"],
+                "measured": mlp_serving["measured"] + "; towers = (concat + towers) - concat",
+                "in_step_aggregate": line["mlp"]["in_step_aggregate"]}
         print(json.dumps(line), flush=True)
     model.close()
     if world > 1:
