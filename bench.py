@@ -529,6 +529,119 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def run_sharded(args):
+    """Model-parallel serving (BASELINE configs[2]: RMC2 "table-wise sharded across 8 x B200 with
+    all-to-all"): every step is ONE global batch of <= d items whose embedding tables are split
+    over the G ranks (table-wise: T/G tables per rank; row-wise: R/G rows of every table), the
+    exchange fused into the SLS as peer stores over NVLink (dist.cu).  value = queries of the
+    global batches / time (counted once, not per rank; scaling "strong")."""
+    import torch
+    import torch.distributed as dist
+    from paper_2203_07424_b200 import (RecModel, rec_split_fuse, nccl_unique_id, REC_SHARD_TABLE,
+                                       REC_SHARD_ROW)
+    world = int(os.environ["WORLD_SIZE"])
+    rank = int(os.environ["RANK"])
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = W.SHORT[args.config]
+    d = args.batch
+    t = torch.zeros(128, dtype=torch.uint8, device="cuda")
+    if rank == 0:
+        t.copy_(torch.frombuffer(bytearray(nccl_unique_id()), dtype=torch.uint8))
+    dist.broadcast(t, 0)
+    shard = REC_SHARD_TABLE if args.shard == "table" else REC_SHARD_ROW
+    model = RecModel(cfg, seed=1, max_batch=d, streams=1, device=local, shard=shard, rank=rank,
+                     world=world, nccl_id=bytes(t.cpu().numpy()))
+    trace = W.burst_trace(args.queries, seed=11)   # the same global query stream on every rank
+    segs, bstart = rec_split_fuse(trace, d)
+    nb = len(bstart) - 1
+    sizes = trace["size"].astype(np.int64)
+    last_chunk_start = ((sizes - 1) // d) * d
+    nin = min(nb, 32)
+    inputs = []
+    for b in range(nin):
+        sg = np.ascontiguousarray(segs[bstart[b]:bstart[b + 1]])
+        ind, off, dense = model.rec_gen_batch(sg)
+        inputs.append((torch.from_numpy(dense).cuda(), torch.from_numpy(ind).cuda(),
+                       torch.from_numpy(off).cuda(), int(sg[:, 2].sum()),
+                       int(np.sum(sg[:, 1] == last_chunk_start[sg[:, 0]]))))
+    ctr = torch.zeros(d * cfg.tasks, device="cuda")
+
+    def step(i):
+        h = inputs[i % nin]
+        model.rec_query(h[0], h[1], h[2], h[3], ctr)
+        return h
+
+    clk = ClockSampler(local).__enter__()
+    for i in range(args.warmup):
+        step(i)
+    dist.barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t_region0 = time.perf_counter()
+    ev0.record()
+    items = queries = 0
+    for i in range(args.warmup, args.warmup + args.steps):
+        h = step(i)
+        items += h[3]
+        queries += h[4]
+    ev1.record()
+    torch.cuda.synchronize()
+    t_region1 = time.perf_counter()
+    dist.barrier()
+    ms = torch.tensor([ev0.elapsed_time(ev1)], dtype=torch.float64, device="cuda")
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    ms_max = float(ms[0])
+    clk.__exit__(None, None, None)
+    # e2e: the same queries with pinned HOST inputs (H2D every step) and the CTRs read back
+    host = [(x[0].cpu().pin_memory(), x[1].cpu().pin_memory(), x[2].cpu().pin_memory(), x[3], x[4])
+            for x in inputs]
+    out = torch.zeros(d * cfg.tasks).pin_memory()
+    e2e_steps = min(args.e2e_steps, 500)
+    dist.barrier()
+    t0 = time.perf_counter()
+    q_e2e = h2d = 0
+    for i in range(e2e_steps):
+        h = host[i % nin]
+        model.rec_query(h[0], h[1], h[2], h[3], out)
+        q_e2e += h[4]
+        h2d += (h[0].numel() + h[1].numel() + h[2].numel()) * 4
+    wall = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
+    dist.all_reduce(wall, op=dist.ReduceOp.MAX)
+    hbm_peak, bf16_peak, peak_kind = peaks()
+    sls_bytes = sls_bytes_per_item(cfg, synth=False) * items
+    agg = sls_bytes / (ms_max * 1e-3) / 1e9 / world
+    if rank == 0:
+        line = {
+            "metric": BASELINE_METRIC, "value": queries / (ms_max * 1e-3), "unit": "QPS",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32 (SLS) + bf16 (MLP, fp32 accumulate)", "data": "synthetic",
+            "config": {"workload": cfg.name, "max_batch_d": d, "tables": cfg.num_tables,
+                       "rows": cfg.rows, "dim": cfg.dim, "pooling": cfg.pooling_lo,
+                       "parallelism": f"{args.shard}-wise sharding x{world} (exchange fused into "
+                                      f"the SLS, peer stores over NVLink)",
+                       "items_per_s": items / (ms_max * 1e-3),
+                       "l2": "inputs larger than L2 (tables >> 126 MB, uniform random rows)",
+                       "value_is": "synchronous global batches (rec_query), one at a time"},
+            "roofline": {"bound": "hbm", "kernel": "k_sls (sharded)", "achieved": agg, "peak": hbm_peak,
+                         "unit": "GB/s", "frac": agg / hbm_peak, "traffic": None, "peak_kind": peak_kind,
+                         "measured": "per-GPU share of the SLS algorithmic bytes / the step time "
+                                     "(lower bound: the step also runs the exchange and dense part)"},
+            "gpu_launches": None,
+            "clocks": clk.summary(t_region0, t_region1),
+            "e2e": {"value": q_e2e / float(wall[0]), "unit": "QPS",
+                    "h2d_bytes_per_step": int(h2d / max(e2e_steps, 1)),
+                    "d2h_bytes_per_step": int(4 * d * cfg.tasks), "steps": e2e_steps,
+                    "api": "rec_query with pinned host inputs (synchronous), max wall over ranks"},
+            "cpu_baseline": None,
+        }
+        print(json.dumps(line), flush=True)
+    model.close()
+    dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -539,6 +652,8 @@ def main():
     ap.add_argument("--batch", type=int, default=1024)
     ap.add_argument("--streams", type=int, default=16)
     ap.add_argument("--submit", default="batch", choices=["batch", "python"])
+    ap.add_argument("--shard", default="replica", choices=["replica", "table", "row"],
+                    help="N > 1: model-parallel embedding sharding instead of replicas")
     ap.add_argument("--pipe", type=int, default=0,
                     help="S-D pipeline lanes (rec_set_pipeline) for the timed region; 0 = slot graphs")
     ap.add_argument("--roofline-steps", type=int, default=1000)
@@ -554,6 +669,8 @@ def main():
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
         run_reference(args)
+    elif args.shard != "replica" and int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        run_sharded(args)
     else:
         run_ours(args)
 
