@@ -385,7 +385,7 @@ def run_ours(args):
 
         def evaluate(m, dd):
             lam, pr = sla_search(model, cfg, world, rank, dist, m, dd, lam_hint[0],
-                                 args.sla_queries, cfg.sla_ms)
+                                 args.sla_queries, cfg.sla_ms, tau_ms=args.fusion_timeout_ms)
             probes_all[f"m{m}_d{dd}"] = pr
             if lam > 0:
                 lam_hint[0] = lam
@@ -661,6 +661,8 @@ def main():
     ap.add_argument("--queries", type=int, default=20000)
     ap.add_argument("--e2e-steps", type=int, default=3000)
     ap.add_argument("--sla-queries", type=int, default=100000)
+    ap.add_argument("--fusion-timeout-ms", type=float, default=0.0,
+                    help="serving policy tau: a partial batch waits up to tau for more queries (R15)")
     ap.add_argument("--cpu-items", type=int, default=256)
     ap.add_argument("--mlp-batch", type=int, default=65536, help="large-batch MLP TC probe (0 = off)")
     ap.add_argument("--ref-items", type=int, default=64)

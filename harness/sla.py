@@ -25,7 +25,7 @@ def p95_nearest_rank(lat_ms: np.ndarray) -> float:
     return float(s[max((95 * s.size + 99) // 100, 1) - 1]) if s.size else float("nan")
 
 
-def sla_search(model, cfg, world, rank, dist, streams, d, lam0, n, sla_ms, max_iter=10):
+def sla_search(model, cfg, world, rank, dist, streams, d, lam0, n, sla_ms, max_iter=10, tau_ms=0.0):
     """lambda*: largest offered Poisson rate (all GPUs) with p95 <= SLA and every GPU keeping up
     (S5; geometric bracketing then bisection).  Real clock, device-synth inputs."""
     import torch
@@ -36,7 +36,7 @@ def sla_search(model, cfg, world, rank, dist, streams, d, lam0, n, sla_ms, max_i
         count[0] += 1
         tr = W.poisson_trace(lam, n, seed=12)
         mine = rank_share(tr, world, rank)
-        rep = model.rec_serve(mine, sla_ms, streams, d, warmup_frac=0.1)
+        rep = model.rec_serve(mine, sla_ms, streams, d, fusion_timeout_ms=tau_ms, warmup_frac=0.1)
         arr = mine["arrival_s"]
         w_end = tr["arrival_s"][0] + 0.1 * (tr["arrival_s"][-1] - tr["arrival_s"][0])
         lat = gather_latencies(rep["latency_ms"][arr >= w_end], world, rank, dist)

@@ -23,6 +23,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <deque>
 #include <queue>
 #include <vector>
 
@@ -489,8 +490,16 @@ rec_status rec_serve(rec_model_t m, const rec_trace_row* trace, int64_t n, doubl
     struct Own {
       uint32_t seq = 0;
       int64_t my_batch = -1;
+      std::deque<std::pair<int64_t, uint32_t>> pend;  // (batch, sequence word) in flight
     };
     std::vector<Own> own(M);
+    // batches in flight per stream: 1 = the paper's co-located instance (one batch at a time);
+    // 2 lets the next fused batch wait in the stream queue so the GPU never idles between a
+    // completion and the host's next submit (REC_SERVE_DEPTH; needs the mapped completion word
+    // and no CTR read-back, whose staging buffer is per stream)
+    int depth = 1;
+    if (const char* e = getenv("REC_SERVE_DEPTH")) depth = std::max(1, std::min(4, atoi(e)));
+    if (ctr_out || !lanes[0].flag_host) depth = 1;
     auto worker = [&](int tid) {
       cudaSetDevice(m->device);
       std::vector<int32_t> segs_local;
@@ -501,16 +510,27 @@ rec_status rec_serve(rec_model_t m, const rec_trace_row* trace, int64_t n, doubl
           Workspace& w = m->ws[s];
           Lane& L = lanes[s];
           Own& O = own[s];
-          if (L.busy) {
-            const bool done = L.flag_host ? (*reinterpret_cast<volatile uint32_t*>(L.flag_host) == O.seq)
-                                          : (cudaEventQuery(L.done) == cudaSuccess);
-            if (!done) continue;
-            const double t_c = now_s() - t0;
-            std::lock_guard<std::mutex> g(mu);
-            finish_batch(O.my_batch, t_c);
-            done_q.store(completed, std::memory_order_relaxed);
-            L.busy = false;
-            progressed = true;
+          if (!O.pend.empty()) {
+            if (L.flag_host) {
+              const uint32_t done_seq = *reinterpret_cast<volatile uint32_t*>(L.flag_host);
+              while (!O.pend.empty() && static_cast<int32_t>(done_seq - O.pend.front().second) >= 0) {
+                const double t_c = now_s() - t0;
+                std::lock_guard<std::mutex> g(mu);
+                finish_batch(O.pend.front().first, t_c);
+                done_q.store(completed, std::memory_order_relaxed);
+                O.pend.pop_front();
+                progressed = true;
+              }
+            } else if (cudaEventQuery(L.done) == cudaSuccess) {
+              const double t_c = now_s() - t0;
+              std::lock_guard<std::mutex> g(mu);
+              finish_batch(O.pend.front().first, t_c);
+              done_q.store(completed, std::memory_order_relaxed);
+              O.pend.pop_front();
+              progressed = true;
+            }
+            L.busy = !O.pend.empty();
+            if (static_cast<int>(O.pend.size()) >= depth) continue;
           }
           int64_t k = 0, items = 0, c0 = 0;
           if (avail.load(std::memory_order_acquire) <= head_a.load(std::memory_order_acquire)) continue;
@@ -572,6 +592,7 @@ rec_status rec_serve(rec_model_t m, const rec_trace_row* trace, int64_t n, doubl
             failed.store(true);
             return;
           }
+          O.pend.emplace_back(O.my_batch, O.seq);
           L.busy = true;
           progressed = true;
         }
