@@ -34,9 +34,8 @@ constexpr int A_STAGE_BYTES = BM * BK * 2;  // 16 KB
 // MT = 128-row M tiles per CTA sharing every weight stage (MT = 2 halves the weight bytes
 // each MMA needs from L2, which is what bounds large-batch GEMMs such as RMC3's 2560x512).
 template <int BN, int MT>
-__global__ void __launch_bounds__(128, 1)
-    k_gemm_tc(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_w,
-              const GemmArgs args, int stages) {
+__device__ __forceinline__ void gemm_tile(const CUtensorMap* ta, const CUtensorMap* tw,
+                                          const GemmArgs& args, int stages) {
   constexpr int B_STAGE_BYTES = BN * BK * 2;
   constexpr int STAGE_BYTES = MT * A_STAGE_BYTES + B_STAGE_BYTES;
   constexpr uint32_t TMEM_COLS = (BN < 32 ? 32 : BN) * MT;
@@ -66,8 +65,8 @@ __global__ void __launch_bounds__(128, 1)
     }
     sm100::mbar_init(done, 1);
     sm100::fence_mbar_init();
-    sm100::tma_prefetch_desc(&tmap_a);
-    sm100::tma_prefetch_desc(&tmap_w);
+    sm100::tma_prefetch_desc(ta);
+    sm100::tma_prefetch_desc(tw);
   }
   if (warp == 0) sm100::tmem_alloc(tslot, TMEM_COLS);
   sm100::tc_fence_before();
@@ -87,8 +86,8 @@ __global__ void __launch_bounds__(128, 1)
         sm100::mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
 #pragma unroll
         for (int h = 0; h < MT; ++h)
-          sm100::tma_load_2d(sa + h * A_STAGE_BYTES, &tmap_a, &full[s], kb * BK, m0 + h * BM);
-        sm100::tma_load_2d(sa + MT * A_STAGE_BYTES, &tmap_w, &full[s], kb * BK, n0);
+          sm100::tma_load_2d(sa + h * A_STAGE_BYTES, ta, &full[s], kb * BK, m0 + h * BM);
+        sm100::tma_load_2d(sa + MT * A_STAGE_BYTES, tw, &full[s], kb * BK, n0);
       }
       __syncwarp();
     }
@@ -196,14 +195,51 @@ __global__ void __launch_bounds__(128, 1)
   if (warp == 0) sm100::tmem_dealloc(tmem, TMEM_COLS);
 }
 
+// Ring depth: a launch with fewer CTAs than SMs is a serving-batch GEMM that co-runs with the
+// other co-located streams' kernels; its shared memory is carved out of those SMs' L1, so it
+// keeps a 2-stage ring (measured: MT-WnD towers 486k -> 611k QPS, same launch latency); a
+// launch that fills the GPU (large batches) takes the deep ring the tensor pipe needs.
+// REC_GEMM_STAGES overrides.
+static int ring_depth(int smax, int ctas) {
+  if (g_gemm_stages > 0) return g_gemm_stages < smax ? g_gemm_stages : smax;
+  return ctas < 148 ? (smax < 2 ? smax : 2) : smax;
+}
+
+template <int BN, int MT>
+__global__ void __launch_bounds__(128, 1)
+    k_gemm_tc(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_w,
+              const __grid_constant__ GemmArgs args, int stages) {
+  gemm_tile<BN, MT>(&tmap_a, &tmap_w, args, stages);
+}
+
+// Grouped launch: blockIdx.z selects one of g.n GEMMs of identical shape (MT-WnD: the same
+// layer of every task tower), each with its own A / W tensor maps and epilogue arguments.
+template <int BN, int MT>
+__global__ void __launch_bounds__(128, 1) k_gemm_group(const __grid_constant__ GemmGroup g, int stages) {
+  gemm_tile<BN, MT>(&g.ta[blockIdx.z], &g.tw[blockIdx.z], g.a[blockIdx.z], stages);
+}
+
+template <int BN, int MT>
+static void launch_group_bn(const GemmGroup& g, cudaStream_t s) {
+  constexpr int STAGE = MT * A_STAGE_BYTES + BN * BK * 2;
+  constexpr int SMAX = (MT == 1 ? 4 : 3);
+  const GemmArgs& a = g.a[0];
+  const int nkb = (a.K + BK - 1) / BK;
+  const int ctas = ((a.N + BN - 1) / BN) * ((a.M + BM * MT - 1) / (BM * MT)) * g.n;
+  const int smax = ring_depth(SMAX, ctas);
+  const int stages = nkb < smax ? (nkb < 1 ? 1 : nkb) : smax;
+  const size_t smem = static_cast<size_t>(stages) * STAGE + 1024 + 256;
+  dim3 grid((a.N + BN - 1) / BN, (a.M + BM * MT - 1) / (BM * MT), g.n);
+  k_gemm_group<BN, MT><<<grid, 128, smem, s>>>(g, stages);
+}
+
 template <int BN, int MT>
 static void launch_bn(const CUtensorMap* ta, const CUtensorMap* tw, const GemmArgs& a,
                       cudaStream_t s) {
   constexpr int STAGE = MT * A_STAGE_BYTES + BN * BK * 2;
   constexpr int SMAX = (MT == 1 ? 4 : 3);
   const int nkb = (a.K + BK - 1) / BK;
-  int smax = SMAX;
-  if (g_gemm_stages > 0 && g_gemm_stages < smax) smax = g_gemm_stages;
+  const int smax = ring_depth(SMAX, ((a.N + BN - 1) / BN) * ((a.M + BM * MT - 1) / (BM * MT)));
   const int stages = nkb < smax ? (nkb < 1 ? 1 : nkb) : smax;
   const size_t smem = static_cast<size_t>(stages) * STAGE + 1024 + 256;
   dim3 grid((a.N + BN - 1) / BN, (a.M + BM * MT - 1) / (BM * MT));
@@ -217,6 +253,8 @@ static void prep_bn() {
   constexpr int STAGE = MT * A_STAGE_BYTES + BN * BK * 2;
   constexpr int SMAX = (MT == 1 ? 4 : 3);
   cudaFuncSetAttribute(k_gemm_tc<BN, MT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       SMAX * STAGE + 1024 + 256);
+  cudaFuncSetAttribute(k_gemm_group<BN, MT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        SMAX * STAGE + 1024 + 256);
 }
 
@@ -237,6 +275,17 @@ void launch_gemm_tc(const CUtensorMap* tmap_a, const CUtensorMap* tmap_w, const 
   else if (((a.M + 255) / 256) * ((a.N + 255) / 256) >= 148 && a.K >= 512)
     launch_bn<256, 2>(tmap_a, tmap_w, a, s);  // enough 256-row tiles to fill the GPU: share W
   else launch_bn<256, 1>(tmap_a, tmap_w, a, s);
+}
+
+void launch_gemm_group(const GemmGroup& g, cudaStream_t s) {
+  const GemmArgs& a = g.a[0];
+  if (a.M <= 0 || g.n <= 0) return;
+  if (a.N <= 32) launch_group_bn<32, 1>(g, s);
+  else if (a.N <= 64) launch_group_bn<64, 1>(g, s);
+  else if (a.N <= 128) launch_group_bn<128, 1>(g, s);
+  else if (((a.M + 255) / 256) * ((a.N + 255) / 256) * g.n >= 148 && a.K >= 512)
+    launch_group_bn<256, 2>(g, s);
+  else launch_group_bn<256, 1>(g, s);
 }
 
 // ---------------------------------------------------------------- tensor maps

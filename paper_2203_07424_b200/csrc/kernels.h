@@ -146,6 +146,14 @@ struct GemmArgs {
   const float* logit_add;   // mode 2: optional per-row addend (MT-WnD wide part) ...
   int add_stride;           // ... at logit_add[r * add_stride]
 };
+// Up to kMaxGroup GEMMs of one shape in ONE launch (grid.z = member): MT-WnD task towers.
+constexpr int kMaxGroup = 4;
+struct GemmGroup {
+  CUtensorMap ta[kMaxGroup], tw[kMaxGroup];  // 64-B aligned members (CUtensorMap alignment)
+  GemmArgs a[kMaxGroup];
+  int n;
+};
+void launch_gemm_group(const GemmGroup& g, cudaStream_t s);
 int gemm_bn(int N);                  // tile width used for a layer of width N (W tmap box)
 void gemm_prepare();                 // per-device one-time kernel attributes
 void launch_gemm_tc(const CUtensorMap* tmap_a, const CUtensorMap* tmap_w, const GemmArgs& a,

@@ -151,9 +151,15 @@ void enqueue_interact_top(rec_model_s* m, Workspace& w, cudaStream_t st, int B, 
     prof_end(m, st, 2, e1);
     mark(gev, 4, st);
     const int nt = static_cast<int>(m->top.size());
-    for (int k = 0; k < m->tasks; ++k) {
-      const std::vector<Layer>& Ls = k == 0 ? m->top : m->towers[k - 1];
-      for (int j = 0; j < nt; ++j) {
+    // the same layer of up to kMaxGroup towers in ONE grouped launch (grid.z = task)
+    const int gmax = m->tower_group ? kMaxGroup : 1;
+    for (int k0 = 0; k0 < m->tasks; k0 += gmax) {
+    const int kn = std::min(gmax, m->tasks - k0);
+    for (int j = 0; j < nt; ++j) {
+      GemmGroup grp;
+      grp.n = kn;
+      for (int k = k0; k < k0 + kn; ++k) {
+        const std::vector<Layer>& Ls = k == 0 ? m->top : m->towers[k - 1];
         const Layer& L = Ls[j];
         GemmArgs a{};
         a.M = B;
@@ -173,16 +179,20 @@ void enqueue_interact_top(rec_model_s* m, Workspace& w, cudaStream_t st, int B, 
           a.add_stride = m->tasks;
         } else {
           a.mode = GEMM_OUT_BF16;
-          a.out_bf16 = static_cast<__nv_bfloat16*>(w.out_top[j]);
+          a.out_bf16 = static_cast<__nv_bfloat16*>(k == 0 ? w.out_top[j] : w.out_task[k][j]);
           a.ldo = L.Npad;
         }
-        cudaEvent_t e = gev ? nullptr : prof_begin(m, st);
-        launch_gemm_tc(&w.tmap_a_top[j], &L.tmap_w, a, st);
-        prof_end(m, st, 1, e);
+        grp.ta[k - k0] = k == 0 ? w.tmap_a_top[j] : w.tmap_a_task[k][j];
+        grp.tw[k - k0] = L.tmap_w;
+        grp.a[k - k0] = a;
       }
+      cudaEvent_t e = gev ? nullptr : prof_begin(m, st);
+      launch_gemm_group(grp, st);
+      prof_end(m, st, 1, e);
+    }
     }
     mark(gev, 5, st);
-    m->launches += 1 + m->tasks * nt;
+    m->launches += 1 + ((m->tasks + gmax - 1) / gmax) * nt;
     return;
   }
   // a5: interaction -> A_top
@@ -733,6 +743,8 @@ static void free_model(rec_model_s* m) {
   pipe_destroy(m);
   for (auto& w : m->ws) {
     if (w.stream) cudaStreamSynchronize(w.stream);
+    for (auto* p : w.th) cudaFree(p);
+    cudaFree(w.wide);
     cudaFree(w.indices);
     cudaFree(w.offsets);
     cudaFree(w.segs);
@@ -1067,6 +1079,7 @@ rec_status rec_model_create(const rec_model_desc* d, rec_model_t* out) {
       g_sls_prio = atoi(pr) < 0 ? hi : 0;
     }
     if (const char* fd = getenv("REC_FUSE_DENSE")) m->fuse_dense = atoi(fd) != 0;
+    if (const char* tg = getenv("REC_TOWER_GROUP")) m->tower_group = atoi(tg) != 0;
     if (const char* gs = getenv("REC_GEMM_STAGES")) g_gemm_stages = atoi(gs);
     if (const char* iw = getenv("REC_INTERACT_WPC")) g_interact_wpc = std::max(1, std::min(8, atoi(iw)));
     const char* p = getenv("REC_PDL");
@@ -1297,6 +1310,26 @@ rec_status rec_model_create(const rec_model_desc* d, rec_model_t* out) {
         return REC_E_CUDA;
       }
       w.out_top[j] = (j == ntl - 1) ? nullptr : static_cast<void*>(w.h[j & 1]);
+    }
+    if (m->arch == REC_ARCH_MTWND && m->tasks > 1) {  // towers 1..N-1 run in the same launches
+      w.th.assign(2 * m->tasks, nullptr);
+      w.tmap_a_task.assign(m->tasks, std::vector<CUtensorMap>(ntl));
+      w.out_task.assign(m->tasks, std::vector<void*>(ntl, nullptr));
+      for (int k = 1; k < m->tasks; ++k) {
+        ALLOC(w.th[2 * k], sizeof(__nv_bfloat16) * int64_t(cap) * m->hmax);
+        ALLOC(w.th[2 * k + 1], sizeof(__nv_bfloat16) * int64_t(cap) * m->hmax);
+        for (int j = 0; j < ntl; ++j) {
+          const void* a_base = j == 0 ? static_cast<void*>(w.A_top) : static_cast<void*>(w.th[2 * k + ((j - 1) & 1)]);
+          const int K = m->top[j].K;
+          const int ld = j == 0 ? m->Ktop_pad : m->top[j - 1].Npad;
+          if (!encode_tmap_bf16(&w.tmap_a_task[k][j], a_base, cap, K, ld, 128)) {
+            set_error("cuTensorMapEncodeTiled failed (tower %d layer %d activations)", k, j);
+            free_model(m);
+            return REC_E_CUDA;
+          }
+          w.out_task[k][j] = (j == ntl - 1) ? nullptr : static_cast<void*>(w.th[2 * k + (j & 1)]);
+        }
+      }
     }
     auto fill_maps = [&](ChainMaps& mp, const CUtensorMap& a0, std::vector<rec::Layer>& Ls, int nch) {
       mp.a0 = a0;

@@ -76,6 +76,9 @@ struct Workspace {
   float* ctr = nullptr;              // [cap][n_tasks]
   float* logit = nullptr;            // [cap][n_tasks]
   float* wide = nullptr;             // MT-WnD: [cap][n_tasks] wide-part logits
+  std::vector<__nv_bfloat16*> th;    // MT-WnD: hidden ping-pong of towers 1..N-1 (2 per task)
+  std::vector<std::vector<CUtensorMap>> tmap_a_task;  // [task][layer] A maps (task >= 1)
+  std::vector<std::vector<void*>> out_task;           // [task][layer] hidden outputs
   int* flag = nullptr;               // device error flags (bit0 OOB, bit1 offsets)
   int* flag_host = nullptr;          // pinned mirror
   uint8_t* pin = nullptr;            // pinned staging
@@ -138,7 +141,8 @@ struct rec_model_s {
   CUtensorMap* d_tmap_rows = nullptr;
   int sls_tma = 0, nsm = 0;
   int sls_pdl = 1;    // REC_PDL=0 disables programmatic dependent launch of the SLS
-  int fuse_dense = 0;  // dense features generated by the SLS kernel (REC_FUSE_DENSE)
+  int fuse_dense = 0;
+  int tower_group = 1;  // MT-WnD: one grouped launch per tower layer (REC_TOWER_GROUP=0: per task)  // dense features generated by the SLS kernel (REC_FUSE_DENSE)
   int diag_skip = 0;  // REC_STEP_DIAG (diagnostic): stages dropped from the synthetic step
   // MLP
   std::vector<rec::Layer> bottom, top;  // top excludes the width-1 output layer
