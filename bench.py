@@ -385,7 +385,7 @@ def run_ours(args):
 
         def evaluate(m, dd):
             lam, pr = sla_search(model, cfg, world, rank, dist, m, dd, lam_hint[0],
-                                 args.sla_queries, cfg.sla_ms, tau_ms=args.fusion_timeout_ms)
+                                 args.sla_queries * world, cfg.sla_ms, tau_ms=args.fusion_timeout_ms)
             probes_all[f"m{m}_d{dd}"] = pr
             if lam > 0:
                 lam_hint[0] = lam
@@ -397,7 +397,7 @@ def run_ours(args):
         sla = {"sla_ms": cfg.sla_ms, "percentile": "p95 (nearest rank)",
                "lambda_star_qps": res["qps"], "policy": {"streams": res["m"], "max_batch": res["d"]},
                "alg1_path": res["path"], "alg1_evaluated": res["evaluated"],
-               "queries_per_probe": args.sla_queries,
+               "queries_per_probe": args.sla_queries * world,
                "probes_at_best": probes_all.get(f"m{res['m']}_d{res['d']}"),
                "mode": "rec_serve real clock, Poisson arrivals, lognormal sizes (R13), split/fuse, "
                        "device-synth inputs, replica dispatch q mod G; Alg. 1 gradient search over "
@@ -660,7 +660,7 @@ def main():
     ap.add_argument("--sls-batches", type=int, default=1000, help="batches in the back-to-back SLS pass")
     ap.add_argument("--queries", type=int, default=20000)
     ap.add_argument("--e2e-steps", type=int, default=3000)
-    ap.add_argument("--sla-queries", type=int, default=100000)
+    ap.add_argument("--sla-queries", type=int, default=100000, help="Poisson queries per probe per GPU")
     ap.add_argument("--fusion-timeout-ms", type=float, default=0.0,
                     help="serving policy tau: a partial batch waits up to tau for more queries (R15)")
     ap.add_argument("--cpu-items", type=int, default=256)
