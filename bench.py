@@ -159,21 +159,38 @@ from harness.schedsearch import gradient_search  # noqa: E402
 
 # ---------------------------------------------------------------------- reference arm
 def run_reference(args):
+    """The tier's reference arm: the CPU oracle (fp64 forward) as it stands, on the host cores,
+    one process per core (fork pool created once).  Each step is a bounded sample of the
+    workload (`cores` jobs of a few items), sized from the warm-up so the K timed steps take
+    about --ref-budget-s seconds."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    import multiprocessing as mp
     cfg = W.SHORT[args.config]
     cores = host_cores()
-    per_step = args.ref_items
     mean_q = float(W.query_sizes(200000, seed=11).mean())
-    for _ in range(args.warmup):
-        oracle_items_per_s(args.config, max(1, per_step // cores), cores, cores)
-    t0 = time.perf_counter()
-    items = 0
-    for _ in range(args.steps):
-        _, _, n = oracle_items_per_s(args.config, max(1, per_step // cores), cores, cores)
-        items += n
-    wall = time.perf_counter() - t0
+    ipj = max(1, args.ref_items // cores)
+    step_no = [0]
+
+    def one_step(pool, n_items):
+        step_no[0] += 1
+        work = [(args.config, W.random_segments(n_items, seed=1000 * step_no[0] + j), 1)
+                for j in range(cores)]
+        return sum(r[1] for r in pool.map(_oracle_job, work))
+
+    with mp.get_context("fork").Pool(cores) as pool:
+        t0 = time.perf_counter()
+        for _ in range(max(args.warmup, 1)):
+            one_step(pool, ipj)
+        t_step = (time.perf_counter() - t0) / max(args.warmup, 1)
+        if args.steps * t_step > args.ref_budget_s:   # shrink the per-step sample to fit
+            ipj = max(1, int(ipj * args.ref_budget_s / (args.steps * t_step)))
+        t0 = time.perf_counter()
+        items = 0
+        for _ in range(args.steps):
+            items += one_step(pool, ipj)
+        wall = time.perf_counter() - t0
     ips = items / wall
     qps = ips / mean_q
     line = {"impl": "reference", "metric": BASELINE_METRIC, "value": qps, "unit": "QPS",
@@ -183,9 +200,9 @@ def run_reference(args):
             "config": {"workload": cfg.name, "items_per_step": items // max(args.steps, 1),
                        "mean_query_items": mean_q, "items_per_s": ips},
             "cpu_baseline": {"value": qps, "unit": "QPS", "cores": cores, "kind": "oracle",
-                             "sample": f"{items // max(args.steps, 1)} items/step of {cfg.name}, "
-                                       f"oracle fp64 forward (SLS+MLP+interaction+sigmoid) in a "
-                                       f"{cores}-process pool"},
+                             "sample": f"{items // max(args.steps, 1)} items/step of {cfg.name} "
+                                       f"({cores} jobs x {ipj} items), oracle fp64 forward "
+                                       f"(SLS+MLP+interaction+sigmoid) in a {cores}-process pool"},
             "e2e": {"value": qps, "unit": "QPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -666,6 +683,8 @@ def main():
     ap.add_argument("--cpu-items", type=int, default=256)
     ap.add_argument("--mlp-batch", type=int, default=65536, help="large-batch MLP TC probe (0 = off)")
     ap.add_argument("--ref-items", type=int, default=64)
+    ap.add_argument("--ref-budget-s", type=float, default=150.0,
+                    help="reference arm: target wall time of the K timed steps")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
