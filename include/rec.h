@@ -241,8 +241,8 @@ rec_status rec_split_fuse(const rec_trace_row* trace, int64_t n, int32_t max_bat
  * latency_ms [n] (optional, per trace row) and batch_log (optional, flattened rows
  * (batch, stream, qid, start, len), capacity log_cap rows; the number of rows written
  * is returned in report->batches' companion, see rec_serve_log_rows).
- * ctr_out [sum sizes] (optional, host): CTR of every item, query-major in trace
- * order.  Errors: INVALID_ARG (bad policy, before any work), CUDA. */
+ * ctr_out [sum sizes][n_tasks] (optional, host): CTR(s) of every item, query-major in
+ * trace order.  Errors: INVALID_ARG (bad policy, before any work), CUDA. */
 rec_status rec_serve(rec_model_t m, const rec_trace_row* trace, int64_t n, double sla_ms,
                      const rec_serve_policy* pol, rec_serve_report* out,
                      double* latency_ms, int32_t* batch_log, int64_t log_cap,

@@ -285,13 +285,15 @@ class RecModel:
         lat = np.zeros(n, dtype=np.float64) if want_latency else None
         log = np.zeros((max(log_cap, 0), 5), dtype=np.int32) if log_cap > 0 else None
         rows = C.c_int64(0)
-        ctr = np.zeros(int(trace["size"].astype(np.int64).sum()), dtype=np.float32) if want_ctr else None
+        tasks = getattr(self.cfg, "tasks", 1)
+        ctr = (np.zeros(int(trace["size"].astype(np.int64).sum()) * tasks, dtype=np.float32)
+               if want_ctr else None)
         _check(lib().rec_serve(self.h, _ptr(trace), n, sla_ms, C.byref(pol), C.byref(rep), _ptr(lat),
                                _ptr(log), log_cap, C.byref(rows), _ptr(ctr)))
         out = rep.as_dict()
         out["latency_ms"] = lat
         out["batch_log"] = log[:rows.value] if log is not None else None
-        out["ctr"] = ctr
+        out["ctr"] = ctr.reshape(-1, tasks) if ctr is not None and tasks > 1 else ctr
         return out
 
 

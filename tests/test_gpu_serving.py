@@ -199,3 +199,27 @@ def test_concurrent_streams_match_sequential():
     for b in range(nb):
         assert np.array_equal(res[b].numpy(), seq[b]), b
     m.close()
+
+
+def test_mtwnd_serving_ctrs():
+    """rec_serve on the MT-WnD model (virtual clock): every served item's N task CTRs equal a
+    direct rec_query of the same items (batch invariance) and the oracle within 2e-2."""
+    from paper_2203_07424_b200 import RecModel
+    cfg = W.small_variant(W.MTWND, 20000)
+    m = RecModel(cfg, seed=1, max_batch=128, streams=2)
+    tr = W.poisson_trace(2000.0, 40, seed=17)
+    rep = m.rec_serve(tr, 100.0, 2, 128, clock=1, alpha_ns=30000.0, beta_ns=250.0, want_ctr=True)
+    ctr = rep["ctr"]
+    assert rep["completed"] == len(tr) and ctr.shape == (int(tr["size"].sum()), cfg.tasks)
+    base = np.concatenate([[0], np.cumsum(tr["size"].astype(np.int64))])
+    for q in (0, 7, 21):
+        n = int(tr["size"][q])
+        take = min(n, 128)
+        segs = np.array([[int(tr["qid"][q]), 0, take]], np.int32)
+        ind, off, dense = gen.gen_batch(cfg, 1, segs)
+        direct = np.zeros((take, cfg.tasks), np.float32)
+        m.rec_query(dense, ind, off, take, direct)
+        assert np.array_equal(ctr[base[q]:base[q] + take], direct)
+        exp = fw.forward(cfg, 1, dense, ind, off)
+        assert np.abs(direct - exp).max() <= 2e-2
+    m.close()
