@@ -195,6 +195,204 @@ __device__ __forceinline__ void gemm_tile(const CUtensorMap* ta, const CUtensorM
   if (warp == 0) sm100::tmem_dealloc(tmem, TMEM_COLS);
 }
 
+// CTA-pair variant (tcgen05 cta_group::2): a cluster of two CTAs computes a
+// 256 x BN tile; each CTA stages its own 128 A rows and HALF of the BN weight rows, the
+// leader's single thread issues M = 256 MMAs that read both CTAs' shared memory and write
+// both CTAs' TMEM (128 lanes x BN columns each), and both CTAs run the epilogue on their rows.
+// Per 256 x BN x 64 step the pair loads 2 x (16 + BN/2 * 128 B): half the weight bytes per
+// FLOP of a single-CTA 128 x BN tile, with BN TMEM columns per CTA.
+template <int BN>
+__device__ __forceinline__ void gemm_tile_2sm(const CUtensorMap* ta, const CUtensorMap* tw,
+                                              const GemmArgs& args, int stages) {
+  constexpr int MT = 1;
+  constexpr int B_STAGE_BYTES = (BN / 2) * BK * 2;  // this CTA's half of the weight rows
+  constexpr int STAGE_BYTES = MT * A_STAGE_BYTES + B_STAGE_BYTES;
+  constexpr uint32_t TMEM_COLS = BN;
+  const uint32_t rank = sm100::cluster_ctarank();
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + stages * STAGE_BYTES);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + stages;
+  uint64_t* done = bars + 2 * stages;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 2 * stages + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // grid.x runs over N blocks (fastest): the CTAs sharing an A tile are co-scheduled, so the
+  // second N block reads A from L2 instead of DRAM
+  const int m0 = blockIdx.y * BM * MT, n0 = blockIdx.x * BN;
+  const int nkb = (args.K + BK - 1) / BK;
+  const int M = args.dM ? *args.dM : args.M;  // device-side batch (graph replay)
+  if (static_cast<int>(blockIdx.y & ~1u) * BM >= M) return;  // whole PAIR beyond the batch
+  __shared__ float s_bias[BN];                // epilogue operands, staged by warps 2-3
+  __shared__ float s_wl[BN];
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < stages; ++s) {
+      sm100::mbar_init(&full[s], 1);
+      sm100::mbar_init(&empty[s], 1);
+    }
+    sm100::mbar_init(done, 1);
+    sm100::fence_mbar_init();
+    sm100::tma_prefetch_desc(ta);
+    sm100::tma_prefetch_desc(tw);
+  }
+  if (warp == 0) sm100::tmem_alloc_2sm(tslot, TMEM_COLS);
+  sm100::tc_fence_before();
+  sm100::cluster_sync();  // both CTAs' barriers initialised before any TMA signals the leader's
+  sm100::tc_fence_after();
+  const uint32_t tmem = *tslot;
+
+  // Whole warps run the role loops (lane 0 issues), so no lane of a role warp spins on a
+  // barrier while its issuing lane still has work (divergent spinning stalls the issuer).
+  if (warp == 0) {
+    // ---------------- TMA producer (both CTAs; completion counted on the leader's barrier)
+    for (int kb = 0; kb < nkb; ++kb) {
+      const int s = kb % stages, it = kb / stages;
+      if (it > 0) sm100::mbar_wait(&empty[s], (it - 1) & 1);
+      if (lane == 0) {
+        uint8_t* sa = smem + s * STAGE_BYTES;
+        if (rank == 0) sm100::mbar_arrive_expect_tx(&full[s], 2 * STAGE_BYTES);
+        sm100::tma_load_2d_2sm(sa, ta, &full[s], kb * BK, m0);
+        sm100::tma_load_2d_2sm(sa + A_STAGE_BYTES, tw, &full[s], kb * BK,
+                               n0 + static_cast<int>(rank) * (BN / 2));
+      }
+      __syncwarp();
+    }
+  } else if (warp == 1) {
+    // ---------------- single-thread MMA issuer of the pair (leader CTA only)
+    if (rank == 0) {
+      constexpr uint32_t idesc = sm100::idesc_bf16_f32(2 * BM, BN);
+      for (int kb = 0; kb < nkb; ++kb) {
+        const int s = kb % stages, it = kb / stages;
+        sm100::mbar_wait(&full[s], it & 1);
+        sm100::tc_fence_after();
+        if (lane == 0) {
+          const uint32_t sa = sm100::smem_u32(smem + s * STAGE_BYTES);
+          const uint64_t da = sm100::umma_desc_sw128(sa);
+          const uint64_t db = sm100::umma_desc_sw128(sa + A_STAGE_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k)
+            sm100::mma_bf16_ss_2sm(tmem, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
+          sm100::mma_commit_2sm_mc(&empty[s], 0x3);
+          if (kb == nkb - 1) sm100::mma_commit_2sm_mc(done, 0x3);
+        }
+        __syncwarp();
+      }
+    }
+  } else {
+    // ---------------- warps 2-3: stage bias (and the width-1 layer) while the MMA runs
+    for (int c = threadIdx.x - 64; c < BN; c += 64) {
+      const int n = n0 + c;
+      s_bias[c] = n < args.N ? __ldg(&args.bias[n]) : 0.f;
+      if (args.mode == GEMM_OUT_CTR) s_wl[c] = n < args.N ? __ldg(&args.w_last[n]) : 0.f;
+    }
+  }
+
+  // ---------------- epilogue: thread = row (TMEM lane warp*32 + lane)
+  sm100::mbar_wait(done, 0);
+  __syncthreads();  // s_bias / s_wl visible to every epilogue thread
+  sm100::tc_fence_after();
+#pragma unroll 1
+  for (int h = 0; h < MT; ++h) {
+  const int row = m0 + h * BM + warp * 32 + lane;
+  const bool row_ok = row < M;
+  const uint32_t trow = tmem + (static_cast<uint32_t>(warp * 32) << 16) + h * BN;
+  float dot = 0.f;
+#pragma unroll 1
+  for (int c0 = 0; c0 < BN; c0 += 16) {
+    const int cbase = n0 + c0;
+    if (cbase >= args.N) break;  // warp-uniform
+    uint32_t r[16];
+    sm100::tmem_ld_32x32b_x16(trow + c0, r);
+    sm100::tmem_ld_wait();
+    float v[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      float x = __uint_as_float(r[j]) + s_bias[c0 + j];
+      if (args.relu) x = fmaxf(x, 0.f);
+      v[j] = x;
+    }
+    if (!row_ok) continue;
+    if (args.mode == GEMM_OUT_BF16) {
+      __nv_bfloat16* dst = args.out_bf16 + static_cast<int64_t>(row) * args.ldo + cbase;
+      if (cbase + 16 <= args.N) {
+        uint32_t p[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * j], v[2 * j + 1]);
+          p[j] = *reinterpret_cast<uint32_t*>(&h);
+        }
+        uint4* d4 = reinterpret_cast<uint4*>(dst);
+        d4[0] = make_uint4(p[0], p[1], p[2], p[3]);
+        d4[1] = make_uint4(p[4], p[5], p[6], p[7]);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          if (cbase + j < args.N) dst[j] = __float2bfloat16_rn(v[j]);
+      }
+    } else if (args.mode == GEMM_OUT_X_F32) {
+      float* dst = args.out_f32 + static_cast<int64_t>(row) * args.ldo + cbase;
+      if (cbase + 16 <= args.N) {
+        float4* d4 = reinterpret_cast<float4*>(dst);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) d4[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          if (cbase + j < args.N) dst[j] = v[j];
+      }
+    } else {  // GEMM_OUT_CTR: width-1 output layer folded into the epilogue
+#pragma unroll
+      for (int j = 0; j < 16; ++j) dot = fmaf(v[j], s_wl[c0 + j], dot);
+    }
+  }
+  if (args.mode == GEMM_OUT_CTR && row_ok) {
+    float logit = dot + args.b_last;
+    if (args.logit_add) logit += args.logit_add[static_cast<int64_t>(row) * args.add_stride];
+    const int64_t o = static_cast<int64_t>(row) * (args.ctr_stride > 0 ? args.ctr_stride : 1);
+    args.ctr[o] = 1.f / (1.f + __expf(-logit));
+    if (args.logit) args.logit[o] = logit;
+  }
+  }
+  sm100::tc_fence_before();
+  sm100::cluster_sync();
+  if (warp == 0) sm100::tmem_dealloc_2sm(tmem, TMEM_COLS);
+}
+
+
+template <int BN>
+__global__ void __launch_bounds__(128, 1)
+    k_gemm_2sm(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_w,
+               const __grid_constant__ GemmArgs args, int stages) {
+  gemm_tile_2sm<BN>(&tmap_a, &tmap_w, args, stages);
+}
+
+// tmap_w must have a BN/2-row box (Layer::tmap_w128 for BN = 256).
+template <int BN>
+static void launch_2sm(const CUtensorMap* ta, const CUtensorMap* tw, const GemmArgs& a, cudaStream_t s) {
+  constexpr int STAGE = A_STAGE_BYTES + (BN / 2) * BK * 2;
+  const int nkb = (a.K + BK - 1) / BK;
+  const int stages = nkb < 4 ? (nkb < 1 ? 1 : nkb) : 4;
+  const size_t smem = static_cast<size_t>(stages) * STAGE + 1024 + 256;
+  int mblocks = (a.M + BM - 1) / BM;
+  mblocks += mblocks & 1;  // whole pairs
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((a.N + BN - 1) / BN, mblocks);
+  cfg.blockDim = dim3(128);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 1;
+  at[0].val.clusterDim.y = 2;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k_gemm_2sm<BN>, *ta, *tw, a, stages);
+}
+
 // Ring depth: a launch with fewer CTAs than SMs is a serving-batch GEMM that co-runs with the
 // other co-located streams' kernels; its shared memory is carved out of those SMs' L1, so it
 // keeps a 2-stage ring (measured: MT-WnD towers 486k -> 611k QPS, same launch latency); a
@@ -259,6 +457,8 @@ static void prep_bn() {
 }
 
 void gemm_prepare() {
+  cudaFuncSetAttribute(k_gemm_2sm<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       4 * (A_STAGE_BYTES + 128 * BK * 2) + 1024 + 256);
   prep_bn<32, 1>();
   prep_bn<64, 1>();
   prep_bn<128, 1>();
@@ -266,14 +466,18 @@ void gemm_prepare() {
   prep_bn<256, 2>();
 }
 
+int g_gemm_2sm = 0;  // REC_GEMM_2SM: CTA-pair GEMM for full-GPU launches (experimental)
+
 void launch_gemm_tc(const CUtensorMap* tmap_a, const CUtensorMap* tmap_w, const GemmArgs& a,
-                    cudaStream_t s) {
+                    cudaStream_t s, const CUtensorMap* tmap_w_half) {
   if (a.M <= 0) return;
   if (a.N <= 32) launch_bn<32, 1>(tmap_a, tmap_w, a, s);
   else if (a.N <= 64) launch_bn<64, 1>(tmap_a, tmap_w, a, s);
   else if (a.N <= 128) launch_bn<128, 1>(tmap_a, tmap_w, a, s);
-  else if (((a.M + 255) / 256) * ((a.N + 255) / 256) >= 148 && a.K >= 512)
-    launch_bn<256, 2>(tmap_a, tmap_w, a, s);  // enough 256-row tiles to fill the GPU: share W
+  else if (((a.M + 255) / 256) * ((a.N + 255) / 256) >= 148 && a.K >= 512) {
+    if (g_gemm_2sm && tmap_w_half) launch_2sm<256>(tmap_a, tmap_w_half, a, s);  // CTA pairs
+    else launch_bn<256, 2>(tmap_a, tmap_w, a, s);  // enough 256-row tiles to fill the GPU: share W
+  }
   else launch_bn<256, 1>(tmap_a, tmap_w, a, s);
 }
 

@@ -156,8 +156,10 @@ struct GemmGroup {
 void launch_gemm_group(const GemmGroup& g, cudaStream_t s);
 int gemm_bn(int N);                  // tile width used for a layer of width N (W tmap box)
 void gemm_prepare();                 // per-device one-time kernel attributes
+// tmap_w_half (optional): the same weights with a 128-row box, enabling the CTA-pair kernel.
 void launch_gemm_tc(const CUtensorMap* tmap_a, const CUtensorMap* tmap_w, const GemmArgs& a,
-                    cudaStream_t s);
+                    cudaStream_t s, const CUtensorMap* tmap_w_half = nullptr);
+extern int g_gemm_2sm;
 // Encode a 2D bf16 K-major tensor map [rows][K] (row pitch ldk elements) with a
 // 64 x box_rows box and 128-byte swizzle.  Returns false on failure.
 bool encode_tmap_rows_f32(CUtensorMap* map, const void* base, uint64_t rows, uint32_t width);

@@ -136,7 +136,7 @@ void enqueue_bottom(rec_model_s* m, Workspace& w, cudaStream_t st, int B, const 
       a.ldo = L.Npad;
     }
     cudaEvent_t e = gev ? nullptr : prof_begin(m, st);
-    launch_gemm_tc(&w.tmap_a_bottom[l], &L.tmap_w, a, st);
+    launch_gemm_tc(&w.tmap_a_bottom[l], &L.tmap_w, a, st, &L.tmap_w128);
     prof_end(m, st, 1, e);
   }
   m->launches += nb;
@@ -236,7 +236,7 @@ void enqueue_interact_top(rec_model_s* m, Workspace& w, cudaStream_t st, int B, 
       a.ldo = L.Npad;
     }
     cudaEvent_t e = gev ? nullptr : prof_begin(m, st);
-    launch_gemm_tc(&w.tmap_a_top[j], &L.tmap_w, a, st);
+    launch_gemm_tc(&w.tmap_a_top[j], &L.tmap_w, a, st, &L.tmap_w128);
     prof_end(m, st, 1, e);
   }
   mark(gev, 5, st);
@@ -1081,6 +1081,7 @@ rec_status rec_model_create(const rec_model_desc* d, rec_model_t* out) {
     if (const char* fd = getenv("REC_FUSE_DENSE")) m->fuse_dense = atoi(fd) != 0;
     if (const char* tg = getenv("REC_TOWER_GROUP")) m->tower_group = atoi(tg) != 0;
     if (const char* gs = getenv("REC_GEMM_STAGES")) g_gemm_stages = atoi(gs);
+    if (const char* g2 = getenv("REC_GEMM_2SM")) g_gemm_2sm = atoi(g2);
     if (const char* iw = getenv("REC_INTERACT_WPC")) g_interact_wpc = std::max(1, std::min(8, atoi(iw)));
     const char* p = getenv("REC_PDL");
     m->sls_pdl = !(p && strcmp(p, "0") == 0);
