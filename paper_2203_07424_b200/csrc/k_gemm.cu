@@ -221,10 +221,12 @@ __device__ __forceinline__ void gemm_tile_2sm(const CUtensorMap* ta, const CUten
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // grid.x runs over N blocks (fastest): the CTAs sharing an A tile are co-scheduled, so the
   // second N block reads A from L2 instead of DRAM
-  const int m0 = blockIdx.y * BM * MT, n0 = blockIdx.x * BN;
+  // grid (2, N blocks, M pairs), cluster (2, 1, 1): the pair's CTAs are x = 0 / 1; the N
+  // blocks of one M pair are launched next to each other (A tiles re-read from L2)
+  const int m0 = (blockIdx.z * 2 + blockIdx.x) * BM, n0 = blockIdx.y * BN;
   const int nkb = (args.K + BK - 1) / BK;
   const int M = args.dM ? *args.dM : args.M;  // device-side batch (graph replay)
-  if (static_cast<int>(blockIdx.y & ~1u) * BM >= M) return;  // whole PAIR beyond the batch
+  if (static_cast<int>(blockIdx.z * 2) * BM >= M) return;  // whole PAIR beyond the batch
   __shared__ float s_bias[BN];                // epilogue operands, staged by warps 2-3
   __shared__ float s_wl[BN];
 
@@ -363,7 +365,7 @@ __device__ __forceinline__ void gemm_tile_2sm(const CUtensorMap* ta, const CUten
 
 
 template <int BN>
-__global__ void __launch_bounds__(128, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1)
     k_gemm_2sm(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_w,
                const __grid_constant__ GemmArgs args, int stages) {
   gemm_tile_2sm<BN>(&tmap_a, &tmap_w, args, stages);
@@ -374,23 +376,12 @@ template <int BN>
 static void launch_2sm(const CUtensorMap* ta, const CUtensorMap* tw, const GemmArgs& a, cudaStream_t s) {
   constexpr int STAGE = A_STAGE_BYTES + (BN / 2) * BK * 2;
   const int nkb = (a.K + BK - 1) / BK;
-  const int stages = nkb < 4 ? (nkb < 1 ? 1 : nkb) : 4;
+  const int smax = g_gemm_2sm > 1 ? g_gemm_2sm : 4;  // REC_GEMM_2SM=n > 1: n-stage ring
+  const int stages = nkb < smax ? (nkb < 1 ? 1 : nkb) : smax;
   const size_t smem = static_cast<size_t>(stages) * STAGE + 1024 + 256;
   int mblocks = (a.M + BM - 1) / BM;
   mblocks += mblocks & 1;  // whole pairs
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3((a.N + BN - 1) / BN, mblocks);
-  cfg.blockDim = dim3(128);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = 1;
-  at[0].val.clusterDim.y = 2;
-  at[0].val.clusterDim.z = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, k_gemm_2sm<BN>, *ta, *tw, a, stages);
+  k_gemm_2sm<BN><<<dim3(2, (a.N + BN - 1) / BN, mblocks / 2), 128, smem, s>>>(*ta, *tw, a, stages);
 }
 
 // Ring depth: a launch with fewer CTAs than SMs is a serving-batch GEMM that co-runs with the
@@ -458,7 +449,7 @@ static void prep_bn() {
 
 void gemm_prepare() {
   cudaFuncSetAttribute(k_gemm_2sm<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       4 * (A_STAGE_BYTES + 128 * BK * 2) + 1024 + 256);
+                       6 * (A_STAGE_BYTES + 128 * BK * 2) + 1024 + 256);
   prep_bn<32, 1>();
   prep_bn<64, 1>();
   prep_bn<128, 1>();
