@@ -282,3 +282,27 @@ def test_mtwnd_parity_and_invariance():
             m.rec_synth_query_async(0, sub, cs)
             m.rec_sync(0)
             assert np.array_equal(cs.cpu().numpy().reshape(37, N), ctr[40:77])
+
+
+def test_bench_sls_measurement_call():
+    """rec_bench_sls (the roofline measurement) launches the production SLS kernel over a
+    batch sequence with and without PDL, returns positive times, rejects bad arguments and
+    leaves the model serving identical bits afterwards."""
+    import torch
+    from paper_2203_07424_b200 import RecError
+    cfg = W.small_variant(W.RMC1, 20000)
+    m = _model(cfg, max_batch=256)
+    segs = W.random_segments(200, seed=61)
+    before = torch.zeros(200, device="cuda")
+    m.rec_synth_query_async(0, segs, before)
+    m.rec_sync(0)
+    bsegs = np.array([[5000 + k, 0, 256] for k in range(8)], np.int32)
+    bst = np.arange(9, dtype=np.int64)
+    assert m.rec_bench_sls(bsegs, bst, pdl=True) > 0
+    assert m.rec_bench_sls(bsegs, bst, pdl=False) > 0
+    with pytest.raises(RecError):
+        m.rec_bench_sls(np.array([[1, 0, 300]], np.int32), np.array([0, 1], np.int64))  # > max_batch
+    after = torch.zeros(200, device="cuda")
+    m.rec_synth_query_async(0, segs, after)
+    m.rec_sync(0)
+    assert np.array_equal(after.cpu().numpy(), before.cpu().numpy())
