@@ -595,6 +595,7 @@ def run_sharded(args):
         step(i)
     dist.barrier()
     torch.cuda.synchronize()
+    base_launch = model.rec_profile_read(4)[1]
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t_region0 = time.perf_counter()
     ev0.record()
@@ -606,6 +607,7 @@ def run_sharded(args):
     ev1.record()
     torch.cuda.synchronize()
     t_region1 = time.perf_counter()
+    launches = model.rec_profile_read(4)[1] - base_launch
     dist.barrier()
     ms = torch.tensor([ev0.elapsed_time(ev1)], dtype=torch.float64, device="cuda")
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
@@ -646,7 +648,7 @@ def run_sharded(args):
                          "unit": "GB/s", "frac": agg / hbm_peak, "traffic": None, "peak_kind": peak_kind,
                          "measured": "per-GPU share of the SLS algorithmic bytes / the step time "
                                      "(lower bound: the step also runs the exchange and dense part)"},
-            "gpu_launches": None,
+            "gpu_launches": int(launches),
             "clocks": clk.summary(t_region0, t_region1),
             "e2e": {"value": q_e2e / float(wall[0]), "unit": "QPS",
                     "h2d_bytes_per_step": int(h2d / max(e2e_steps, 1)),
