@@ -14,6 +14,7 @@
 namespace rec {
 
 int g_interact_wpc = 8;  // warps (items) per CTA, REC_INTERACT_WPC
+int g_interact_pf = 0;   // few-CTA prefetching interaction (REC_INTERACT_PF=1; measured slightly slower)
 
 // Pair p of the strict lower triangle in row-major order: (i, j), 1 <= i <= T, 0 <= j < i,
 // p = i(i-1)/2 + j.
@@ -72,8 +73,90 @@ __global__ void k_interact(const float* __restrict__ X, int B, const int* __rest
   }
 }
 
+// Same computation, few CTAs: each warp walks ~kItemsPerWarp items and prefetches the next
+// item's X rows into registers while it computes the current one, so the kernel holds ~8x
+// fewer CTA-microseconds of SM residency (what co-running SLS CTAs pay for)
+// at about the same duration.  PF = float4 per lane per item ((T+1)*D/4 <= 32*PF).
+constexpr int kItemsPerWarp = 4;
+template <int PF>
+__global__ void k_interact_pf(const float* __restrict__ X, int B, const int* __restrict__ dB, int T,
+                              int D, __nv_bfloat16* __restrict__ A, int ld, int warps_per_cta) {
+  extern __shared__ float4 sm4[];
+  if (dB) B = *dB;
+  const int rows = T + 1, pitch = D + 4, npairs = T * (T + 1) / 2, d4 = D / 4;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int per_warp_f = rows * pitch + ld / 2;
+  float* xs = reinterpret_cast<float*>(sm4) + warp * per_warp_f;
+  __nv_bfloat16* outs = reinterpret_cast<__nv_bfloat16*>(xs + rows * pitch);
+  const int nvec = rows * d4;
+  const int stride = gridDim.x * warps_per_cta;
+  int b = blockIdx.x * warps_per_cta + warp;
+  float4 pf[PF];
+  if (b < B) {
+    const float4* xb = reinterpret_cast<const float4*>(X + static_cast<int64_t>(b) * rows * D);
+#pragma unroll
+    for (int q = 0; q < PF; ++q) {
+      const int e = lane + 32 * q;
+      if (e < nvec) pf[q] = __ldg(xb + e);
+    }
+  }
+  for (; b < B; b += stride) {
+#pragma unroll
+    for (int q = 0; q < PF; ++q) {  // prefetched rows of item b -> shared memory
+      const int e = lane + 32 * q;
+      if (e < nvec) {
+        const int r = e / d4, c = e - r * d4;
+        *reinterpret_cast<float4*>(xs + r * pitch + 4 * c) = pf[q];
+      }
+    }
+    const int bn = b + stride;
+    if (bn < B) {  // next item's rows in flight during this item's math
+      const float4* xb = reinterpret_cast<const float4*>(X + static_cast<int64_t>(bn) * rows * D);
+#pragma unroll
+      for (int q = 0; q < PF; ++q) {
+        const int e = lane + 32 * q;
+        if (e < nvec) pf[q] = __ldg(xb + e);
+      }
+    }
+    __syncwarp();
+    for (int k = lane; k < D; k += 32) outs[k] = __float2bfloat16_rn(xs[k]);
+    for (int p = lane; p < npairs; p += 32) {
+      const int2 ij = pair_of(p);
+      const float4* xi = reinterpret_cast<const float4*>(xs + ij.x * pitch);
+      const float4* xj = reinterpret_cast<const float4*>(xs + ij.y * pitch);
+      float acc = 0.f;
+      for (int k = 0; k < d4; ++k) {
+        const float4 a = xi[k], c = xj[k];
+        acc = fmaf(a.x, c.x, acc);
+        acc = fmaf(a.y, c.y, acc);
+        acc = fmaf(a.z, c.z, acc);
+        acc = fmaf(a.w, c.w, acc);
+      }
+      outs[D + p] = __float2bfloat16_rn(acc);
+    }
+    for (int k = D + npairs + lane; k < ld; k += 32) outs[k] = __float2bfloat16_rn(0.f);
+    __syncwarp();
+    int4* ab = reinterpret_cast<int4*>(A + static_cast<int64_t>(b) * ld);
+    const int4* os = reinterpret_cast<const int4*>(outs);
+    for (int v = lane; v < ld / 8; v += 32) ab[v] = os[v];
+    __syncwarp();
+  }
+}
+
 void launch_interact(const float* X, int B, const int* dB, int T, int D, __nv_bfloat16* A_top,
                      int ld_top, cudaStream_t s) {
+  if (B > 0 && g_interact_pf && (T + 1) * (D / 4) <= 32 * 4) {
+    const size_t per_warp = (static_cast<size_t>(T + 1) * (D + 4) + ld_top / 2) * sizeof(float);
+    const int wpc = 8;
+    int blocks = (B + wpc * kItemsPerWarp - 1) / (wpc * kItemsPerWarp);
+    if (blocks > 148) blocks = 148;
+    const size_t smem = wpc * per_warp;
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(k_interact_pf<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(smem));
+    k_interact_pf<4><<<blocks, 32 * wpc, smem, s>>>(X, B, dB, T, D, A_top, ld_top, wpc);
+    return;
+  }
   if (B <= 0) return;
   const size_t per_warp = (static_cast<size_t>(T + 1) * (D + 4) + ld_top / 2) * sizeof(float);
   int wpc = static_cast<int>((96 * 1024) / per_warp);

@@ -197,7 +197,7 @@ void enqueue_interact_top(rec_model_s* m, Workspace& w, cudaStream_t st, int B, 
   }
   // a5: interaction -> A_top
   cudaEvent_t e1 = gev ? nullptr : prof_begin(m, st);
-  launch_interact(w.X, B, dB, T, D, w.A_top, m->Ktop_pad, st);
+  if (!(m->diag_skip & 4)) launch_interact(w.X, B, dB, T, D, w.A_top, m->Ktop_pad, st);
   prof_end(m, st, 2, e1);
   mark(gev, 4, st);
   // a6: top MLP; the last hidden layer's epilogue applies the width-1 layer + sigmoid
@@ -1070,7 +1070,8 @@ rec_status rec_model_create(const rec_model_desc* d, rec_model_t* out) {
     const char* e = getenv("REC_SLS");
     const bool want = e && strcmp(e, "tma") == 0;  // measured slower: opt-in
     // diagnostic only (REC_STEP_DIAG, never set by tests or bench): bit 0 drops the bottom
-    // MLP, bit 1 the interaction + top MLP from the synthetic step graphs (CTRs invalid)
+    // MLP, bit 1 the interaction + top MLP, bit 2 the interaction alone from the synthetic
+    // step graphs (CTRs invalid)
     if (const char* d = getenv("REC_STEP_DIAG")) m->diag_skip = atoi(d);
     if (const char* pr = getenv("REC_PRIO")) {
       int lo = 0, hi = 0;
@@ -1083,6 +1084,7 @@ rec_status rec_model_create(const rec_model_desc* d, rec_model_t* out) {
     if (const char* gs = getenv("REC_GEMM_STAGES")) g_gemm_stages = atoi(gs);
     if (const char* g2 = getenv("REC_GEMM_2SM")) g_gemm_2sm = atoi(g2);
     if (const char* iw = getenv("REC_INTERACT_WPC")) g_interact_wpc = std::max(1, std::min(8, atoi(iw)));
+    if (const char* ip = getenv("REC_INTERACT_PF")) g_interact_pf = atoi(ip);
     const char* p = getenv("REC_PDL");
     m->sls_pdl = !(p && strcmp(p, "0") == 0);
     CHECK_CUDA_CREATE(cudaDeviceGetAttribute(&m->nsm, cudaDevAttrMultiProcessorCount, m->device));
