@@ -32,6 +32,9 @@ __device__ __forceinline__ int2 pair_of(int p) {
 __global__ void k_interact(const float* __restrict__ X, int B, const int* __restrict__ dB, int T,
                            int D, __nv_bfloat16* __restrict__ A, int ld, int warps_per_cta) {
   extern __shared__ float4 sm4[];
+  // the top MLP kernel that follows may be scheduled now: it sets up (barriers, TMEM, bias)
+  // and waits for this grid before reading A (programmatic dependent launch)
+  cudaTriggerProgrammaticLaunchCompletion();
   if (dB) B = *dB;
   if (static_cast<int>(blockIdx.x) * warps_per_cta >= B) return;
   const int rows = T + 1, pitch = D + 4, npairs = T * (T + 1) / 2, d4 = D / 4;

@@ -123,6 +123,7 @@ __global__ void __launch_bounds__(C_THREADS, REC_CHAIN_MINB)
         for (int kb = 0; kb < nkb; ++kb, ++it) {
           const int s = it % S, use = it / S;
           if (use > 0) sm100::mbar_wait(&empty[s], (use - 1) & 1);
+          if (args.pdl && it == 0) cudaGridDependencySynchronize();  // A written by predecessor
           if (lane == 0) {
             uint8_t* st = ring + s * C_STAGE;
             sm100::mbar_arrive_expect_tx(&full[s], bytes);
@@ -327,7 +328,7 @@ void chain_prepare() {
 void launch_mlp_chain(const ChainMaps& maps, const ChainArgs& a, cudaStream_t s) {
   if (a.M <= 0) return;
   const size_t smem = chain_smem_bytes(a);
-  if (g_dense_prio == 0) {
+  if (g_dense_prio == 0 && !a.pdl) {
     k_mlp_chain<<<(a.M + CBM - 1) / CBM, C_THREADS, smem, s>>>(maps, a);
     return;
   }
@@ -336,11 +337,18 @@ void launch_mlp_chain(const ChainMaps& maps, const ChainArgs& a, cudaStream_t s)
   cfg.blockDim = dim3(C_THREADS);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributePriority;
-  at[0].val.priority = g_dense_prio;
+  cudaLaunchAttribute at[2];
+  int na = 0;
+  if (g_dense_prio != 0) {
+    at[na].id = cudaLaunchAttributePriority;
+    at[na++].val.priority = g_dense_prio;
+  }
+  if (a.pdl) {
+    at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[na++].val.programmaticStreamSerializationAllowed = 1;
+  }
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = na;
   cudaLaunchKernelEx(&cfg, k_mlp_chain, maps, a);
 }
 

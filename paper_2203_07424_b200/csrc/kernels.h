@@ -172,6 +172,8 @@ struct ChainMaps {
   CUtensorMap w0, w1, w2, w3;  // weights of layer l [N_l][K_l] (box 64 x wbox[l])
 };
 struct ChainArgs {
+  int pdl;                // launched with programmatic dependent launch: the TMA producer waits
+                          // for the predecessor grid before reading layer-0 activations
   int M;
   const int* dM;          // optional device-side M (grid sized for M = capacity)
   int nlayers;            // <= 4 GEMM layers, ReLU after every one

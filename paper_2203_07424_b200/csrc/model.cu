@@ -204,6 +204,7 @@ void enqueue_interact_top(rec_model_s* m, Workspace& w, cudaStream_t st, int B, 
   const int nt = static_cast<int>(m->top.size());
   if (m->chain_top) {  // whole top MLP in one kernel (k_mlp.cu)
     ChainArgs a = m->chain_top_args;
+    a.pdl = m->chain_pdl;
     a.M = B;
     a.dM = dB;
     a.ctr = ctr_out;
@@ -1081,6 +1082,7 @@ rec_status rec_model_create(const rec_model_desc* d, rec_model_t* out) {
     }
     if (const char* fd = getenv("REC_FUSE_DENSE")) m->fuse_dense = atoi(fd) != 0;
     if (const char* tg = getenv("REC_TOWER_GROUP")) m->tower_group = atoi(tg) != 0;
+    if (const char* cp = getenv("REC_CHAIN_PDL")) m->chain_pdl = atoi(cp) != 0;
     if (const char* gs = getenv("REC_GEMM_STAGES")) g_gemm_stages = atoi(gs);
     if (const char* g2 = getenv("REC_GEMM_2SM")) g_gemm_2sm = atoi(g2);
     if (const char* iw = getenv("REC_INTERACT_WPC")) g_interact_wpc = std::max(1, std::min(8, atoi(iw)));
