@@ -457,7 +457,8 @@ void gemm_prepare() {
   prep_bn<256, 2>();
 }
 
-int g_gemm_2sm = 0;  // REC_GEMM_2SM: CTA-pair GEMM for full-GPU launches (experimental)
+int g_gemm_2sm = 0;     // REC_GEMM_2SM: CTA-pair GEMM for full-GPU launches (experimental)
+int g_gemm_narrow = 1;  // REC_GEMM_NARROW=0: keep 256-wide N tiles for sub-wave launches
 
 void launch_gemm_tc(const CUtensorMap* tmap_a, const CUtensorMap* tmap_w, const GemmArgs& a,
                     cudaStream_t s, const CUtensorMap* tmap_w_half) {
@@ -468,8 +469,14 @@ void launch_gemm_tc(const CUtensorMap* tmap_a, const CUtensorMap* tmap_w, const 
   else if (((a.M + 255) / 256) * ((a.N + 255) / 256) >= 148 && a.K >= 512) {
     if (g_gemm_2sm && tmap_w_half) launch_2sm<256>(tmap_a, tmap_w_half, a, s);  // CTA pairs
     else launch_bn<256, 2>(tmap_a, tmap_w, a, s);  // enough 256-row tiles to fill the GPU: share W
+  } else if (g_gemm_narrow && tmap_w_half && ((a.M + 127) / 128) * ((a.N + 255) / 256) < 64) {
+    // serving batch, few 128x256 tiles: 128-wide N tiles double the CTAs working on the layer
+    // (lower latency; every output element keeps the same K-ordered accumulation, so the
+    // result bits do not depend on the tiling)
+    launch_bn<128, 1>(tmap_a, tmap_w_half, a, s);
+  } else {
+    launch_bn<256, 1>(tmap_a, tmap_w, a, s);
   }
-  else launch_bn<256, 1>(tmap_a, tmap_w, a, s);
 }
 
 void launch_gemm_group(const GemmGroup& g, cudaStream_t s) {

@@ -160,6 +160,7 @@ void gemm_prepare();                 // per-device one-time kernel attributes
 void launch_gemm_tc(const CUtensorMap* tmap_a, const CUtensorMap* tmap_w, const GemmArgs& a,
                     cudaStream_t s, const CUtensorMap* tmap_w_half = nullptr);
 extern int g_gemm_2sm;
+extern int g_gemm_narrow;
 // Encode a 2D bf16 K-major tensor map [rows][K] (row pitch ldk elements) with a
 // 64 x box_rows box and 128-byte swizzle.  Returns false on failure.
 bool encode_tmap_rows_f32(CUtensorMap* map, const void* base, uint64_t rows, uint32_t width);
