@@ -405,7 +405,9 @@ __global__ void __launch_bounds__(128, 1)
 // layer of every task tower), each with its own A / W tensor maps and epilogue arguments.
 template <int BN, int MT>
 __global__ void __launch_bounds__(128, 1) k_gemm_group(const __grid_constant__ GemmGroup g, int stages) {
-  gemm_tile<BN, MT>(&g.ta[blockIdx.z], &g.tw[blockIdx.z], g.a[blockIdx.z], stages);
+  // 128-wide tiles read the 128-row-box weight maps (a 256-wide tile needs the full box)
+  gemm_tile<BN, MT>(&g.ta[blockIdx.z], BN == 128 && g.a[0].N > 128 ? &g.tw_half[blockIdx.z] : &g.tw[blockIdx.z],
+                    g.a[blockIdx.z], stages);
 }
 
 template <int BN, int MT>
@@ -458,7 +460,7 @@ void gemm_prepare() {
 }
 
 int g_gemm_2sm = 0;     // REC_GEMM_2SM: CTA-pair GEMM for full-GPU launches (experimental)
-int g_gemm_narrow = 1;  // REC_GEMM_NARROW=0: keep 256-wide N tiles for sub-wave launches
+int g_gemm_narrow = 0;  // REC_GEMM_NARROW=n: 128-wide N tiles below n 128x256 tiles (measured: RMC2/3 +0.5-1 %, MT-WnD -7 %)
 
 void launch_gemm_tc(const CUtensorMap* tmap_a, const CUtensorMap* tmap_w, const GemmArgs& a,
                     cudaStream_t s, const CUtensorMap* tmap_w_half) {
@@ -469,7 +471,7 @@ void launch_gemm_tc(const CUtensorMap* tmap_a, const CUtensorMap* tmap_w, const 
   else if (((a.M + 255) / 256) * ((a.N + 255) / 256) >= 148 && a.K >= 512) {
     if (g_gemm_2sm && tmap_w_half) launch_2sm<256>(tmap_a, tmap_w_half, a, s);  // CTA pairs
     else launch_bn<256, 2>(tmap_a, tmap_w, a, s);  // enough 256-row tiles to fill the GPU: share W
-  } else if (g_gemm_narrow && tmap_w_half && ((a.M + 127) / 128) * ((a.N + 255) / 256) < 64) {
+  } else if (g_gemm_narrow && tmap_w_half && ((a.M + 127) / 128) * ((a.N + 255) / 256) < g_gemm_narrow) {
     // serving batch, few 128x256 tiles: 128-wide N tiles double the CTAs working on the layer
     // (lower latency; every output element keeps the same K-ordered accumulation, so the
     // result bits do not depend on the tiling)
@@ -487,6 +489,8 @@ void launch_gemm_group(const GemmGroup& g, cudaStream_t s) {
   else if (a.N <= 128) launch_group_bn<128, 1>(g, s);
   else if (((a.M + 255) / 256) * ((a.N + 255) / 256) * g.n >= 148 && a.K >= 512)
     launch_group_bn<256, 2>(g, s);
+  else if (g_gemm_narrow && ((a.M + 127) / 128) * ((a.N + 255) / 256) * g.n < g_gemm_narrow)
+    launch_group_bn<128, 1>(g, s);
   else launch_group_bn<256, 1>(g, s);
 }
 

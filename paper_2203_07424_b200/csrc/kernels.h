@@ -150,6 +150,7 @@ struct GemmArgs {
 constexpr int kMaxGroup = 4;
 struct GemmGroup {
   CUtensorMap ta[kMaxGroup], tw[kMaxGroup];  // 64-B aligned members (CUtensorMap alignment)
+  CUtensorMap tw_half[kMaxGroup];            // same weights, 128-row box (narrow N tiles)
   GemmArgs a[kMaxGroup];
   int n;
 };

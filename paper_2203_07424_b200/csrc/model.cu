@@ -184,6 +184,7 @@ void enqueue_interact_top(rec_model_s* m, Workspace& w, cudaStream_t st, int B, 
         }
         grp.ta[k - k0] = k == 0 ? w.tmap_a_top[j] : w.tmap_a_task[k][j];
         grp.tw[k - k0] = L.tmap_w;
+        grp.tw_half[k - k0] = L.tmap_w128;
         grp.a[k - k0] = a;
       }
       cudaEvent_t e = gev ? nullptr : prof_begin(m, st);
