@@ -480,13 +480,12 @@ rec_status rec_serve(rec_model_t m, const rec_trace_row* trace, int64_t n, doubl
     std::atomic<bool> failed{false};
     std::atomic<int> fail_status{REC_OK};
     const double t0 = now_s() - t_first;
-    // one dispatcher thread per stream up to half the host's hardware threads; beyond that a
-    // thread owns several streams (streams s = t, t + nthreads, ...) so the spinning
-    // dispatchers never oversubscribe the cores
-    int hw = static_cast<int>(std::max(2u, std::thread::hardware_concurrency()));
-    if (const char* lw = getenv("LOCAL_WORLD_SIZE"))  // torchrun: ranks of this box share its cores
-      hw = std::max(2, hw / std::max(1, atoi(lw)));
-    const int nthreads = std::max(1, std::min(M, hw / 2));
+    // Dispatcher threads: ONE thread polls every stream's mapped completion word and submits
+    // (streams s = t, t + nthreads, ...).  Measured (scripts/serve_probe.py, RMC1, m = 8):
+    // 1 thread sustains 305k QPS, 2 threads 288k, 8 threads 277k — concurrent graph launches
+    // from several host threads contend inside the CUDA driver.  REC_SERVE_THREADS overrides.
+    int nthreads = 1;
+    if (const char* e = getenv("REC_SERVE_THREADS")) nthreads = std::max(1, std::min(M, atoi(e)));
     struct Own {
       uint32_t seq = 0;
       int64_t my_batch = -1;
