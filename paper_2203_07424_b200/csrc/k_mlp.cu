@@ -66,6 +66,79 @@ constexpr int C_Q = REC_CHAIN_Q;
 #endif
 constexpr int C_THREADS = 64 + C_EPI_THREADS;
 
+// ---------------------------------------------------------------- fused dot interaction
+// Top chain only (ChainArgs::ir = T + 1): the layer-0 A operand of tile row r is the
+// interaction row of item m0 + r (reading R1, k_interact.cu), computed here by the epilogue
+// warps straight into the swizzled activation buffer instead of by a separate kernel and a
+// TMA load.  Same arithmetic in the same order as k_interact (fp32 FMA chain over k = 0..D-1
+// per pair, round-to-nearest bf16), so the fused and unfused paths are bit-identical.
+__device__ __forceinline__ void act_st_bf16(uint8_t* act, int r, int col, float v) {
+  uint8_t* blk = act + (col >> 6) * C_A_BYTES + r * 128;
+  const int u = (col & 63) >> 3;
+  *reinterpret_cast<__nv_bfloat16*>(blk + ((u ^ (r & 7)) << 4) + (col & 7) * 2) = __float2bfloat16_rn(v);
+}
+__device__ __forceinline__ void act_st_unit(uint8_t* act, int r, int q, float4 a, float4 b) {
+  uint8_t* blk = act + (q >> 3) * C_A_BYTES + r * 128;
+  const __nv_bfloat162 h0 = __floats2bfloat162_rn(a.x, a.y), h1 = __floats2bfloat162_rn(a.z, a.w);
+  const __nv_bfloat162 h2 = __floats2bfloat162_rn(b.x, b.y), h3 = __floats2bfloat162_rn(b.z, b.w);
+  *reinterpret_cast<uint4*>(blk + (((q & 7) ^ (r & 7)) << 4)) =
+      make_uint4(*reinterpret_cast<const uint32_t*>(&h0), *reinterpret_cast<const uint32_t*>(&h1),
+                 *reinterpret_cast<const uint32_t*>(&h2), *reinterpret_cast<const uint32_t*>(&h3));
+}
+// Pairs (i, j) with I0 <= i < I1, 0 <= j < i (p = i(i-1)/2 + j) of one item; the half with
+// I0 == 1 also writes bf16(x_b) to columns 0..D-1.  xrow == nullptr: a row past M (zeros).
+// Chunks of 4 k are prefetched one ahead (the row's vectors come from L2).
+// Measured (RMC1, 16 co-located streams): -0.4 % against the separate kernel, and -1.2 % with
+// a two-ahead prefetch (124 -> 140 registers): the chain CTA's longer residency and larger
+// register file cost the co-running SLS CTAs more than the saved launch, so it is opt-in
+// (REC_FUSE_INTERACT=1).
+template <int D, int I0, int I1>
+__device__ __forceinline__ void interact_part(const float* __restrict__ xrow, int r, uint8_t* act) {
+  constexpr int C = D / 4;
+  constexpr int P0 = I0 * (I0 - 1) / 2, NPP = I1 * (I1 - 1) / 2 - P0;
+  float acc[NPP];
+#pragma unroll
+  for (int p = 0; p < NPP; ++p) acc[p] = 0.f;
+  const float4* xb = reinterpret_cast<const float4*>(xrow);
+  const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+  float4 cur[I1], nxt[I1];
+#pragma unroll
+  for (int i = 0; i < I1; ++i) cur[i] = xb ? __ldg(xb + i * C) : z4;
+  float4 x0prev = z4;
+#pragma unroll 1
+  for (int c = 0; c < C; ++c) {
+    if (c + 1 < C) {
+#pragma unroll
+      for (int i = 0; i < I1; ++i) nxt[i] = xb ? __ldg(xb + i * C + c + 1) : z4;
+    }
+#pragma unroll
+    for (int i = I0; i < I1; ++i)
+#pragma unroll
+      for (int j = 0; j < i; ++j) {
+        float& a = acc[i * (i - 1) / 2 + j - P0];
+        a = fmaf(cur[i].x, cur[j].x, a);
+        a = fmaf(cur[i].y, cur[j].y, a);
+        a = fmaf(cur[i].z, cur[j].z, a);
+        a = fmaf(cur[i].w, cur[j].w, a);
+      }
+    if (I0 == 1) {
+      if (c & 1) act_st_unit(act, r, c >> 1, x0prev, cur[0]);
+      x0prev = cur[0];
+    }
+#pragma unroll
+    for (int i = 0; i < I1; ++i) cur[i] = nxt[i];
+  }
+#pragma unroll
+  for (int p = 0; p < NPP; ++p) act_st_bf16(act, r, D + P0 + p, acc[p]);
+}
+// split point: the pairs of rows i < S and i >= S are about half each
+__host__ __device__ constexpr int interact_split(int R) {
+  int S = 2;
+  while (S * (S - 1) < R * (R - 1) / 2) ++S;
+  return S;
+}
+
+template <int IR, int ID>
 __global__ void __launch_bounds__(C_THREADS, REC_CHAIN_MINB)
     k_mlp_chain(const __grid_constant__ ChainMaps maps, const ChainArgs args) {
   extern __shared__ uint8_t smem_raw[];
@@ -119,15 +192,16 @@ __global__ void __launch_bounds__(C_THREADS, REC_CHAIN_MINB)
       const int nkb = (K + CBK - 1) / CBK;
       for (int n0 = 0; n0 < N; n0 += NCH) {
         const int box_rows = args.wbox[l];
-        const uint32_t bytes = (l == 0 ? C_A_BYTES : 0) + box_rows * CBK * 2;
+        const bool a_tma = l == 0 && IR == 0;  // fused interaction: layer-0 A is built in smem
+        const uint32_t bytes = (a_tma ? C_A_BYTES : 0) + box_rows * CBK * 2;
         for (int kb = 0; kb < nkb; ++kb, ++it) {
           const int s = it % S, use = it / S;
           if (use > 0) sm100::mbar_wait(&empty[s], (use - 1) & 1);
-          if (args.pdl && it == 0) cudaGridDependencySynchronize();  // A written by predecessor
+          if (IR == 0 && args.pdl && it == 0) cudaGridDependencySynchronize();  // A written by predecessor
           if (lane == 0) {
             uint8_t* st = ring + s * C_STAGE;
             sm100::mbar_arrive_expect_tx(&full[s], bytes);
-            if (l == 0) sm100::tma_load_2d(st, &maps.a0, &full[s], kb * CBK, m0);
+            if (a_tma) sm100::tma_load_2d(st, &maps.a0, &full[s], kb * CBK, m0);
             sm100::tma_load_2d(st + C_A_BYTES, wmap(maps, l), &full[s], kb * CBK, n0);
             if (it == 0) STAMP(2);
           }
@@ -141,8 +215,8 @@ __global__ void __launch_bounds__(C_THREADS, REC_CHAIN_MINB)
     for (int l = 0; l < nl; ++l) {
       const int K = args.K[l], N = args.N[l];
       const int nkb = (K + CBK - 1) / CBK;
-      if (l > 0) {  // the previous layer's activations are in smem; its TMEM has been drained
-        sm100::mbar_wait(act_ready, (l - 1) & 1);
+      if (l > 0 || IR) {  // the previous layer's activations (or the interaction) are in smem
+        sm100::mbar_wait(act_ready, (IR ? l : l - 1) & 1);
         sm100::tc_fence_after();
       }
       for (int n0 = 0; n0 < N; n0 += NCH) {
@@ -155,7 +229,7 @@ __global__ void __launch_bounds__(C_THREADS, REC_CHAIN_MINB)
           if (lane == 0) {
             if (it == 0) STAMP(3);
             const uint32_t st = sm100::smem_u32(ring + s * C_STAGE);
-            const uint64_t da = sm100::umma_desc_sw128(l == 0 ? st : sm100::smem_u32(act + kb * C_A_BYTES));
+            const uint64_t da = sm100::umma_desc_sw128(l == 0 && IR == 0 ? st : sm100::smem_u32(act + kb * C_A_BYTES));
             const uint64_t db = sm100::umma_desc_sw128(st + C_A_BYTES);
 #pragma unroll
             for (int k = 0; k < CBK / 16; ++k)
@@ -183,6 +257,19 @@ __global__ void __launch_bounds__(C_THREADS, REC_CHAIN_MINB)
     const int row = m0 + r;
     const bool row_ok = row < M;
     const uint32_t trow = tmem + (static_cast<uint32_t>(qw * 32) << 16);
+    if constexpr (IR > 0) {
+      if (args.pdl) cudaGridDependencySynchronize();  // X written by the predecessor grids
+      const float* xrow = row_ok ? args.ix + static_cast<int64_t>(row) * IR * ID : nullptr;
+      constexpr int SP = interact_split(IR);
+      if (C_HALVES == 1 || half == 0) interact_part<ID, 1, SP>(xrow, r, act);
+      if (C_HALVES == 1 || half == 1) {
+        interact_part<ID, SP, IR>(xrow, r, act);
+        for (int c = ID + IR * (IR - 1) / 2; c < args.K[0]; ++c) act_st_bf16(act, r, c, 0.f);
+      }
+      fence_async_smem();
+      sm100::tc_fence_before();
+      sm100::mbar_arrive(act_ready);
+    }
     int boff = 0;
     for (int l = 0; l < nl; ++l) {
       const int N = args.N[l];
@@ -321,15 +408,28 @@ bool chain_configure(ChainArgs& a) {
   return false;
 }
 
+using ChainKernel = void (*)(const ChainMaps, const ChainArgs);
+static ChainKernel chain_kernel(int ir) {
+  switch (ir) {
+    case 9: return k_mlp_chain<9, 32>;
+    case 11: return k_mlp_chain<11, 32>;
+    default: return k_mlp_chain<0, 0>;
+  }
+}
+
+bool chain_interact_supported(int T, int D) { return D == 32 && (T + 1 == 9 || T + 1 == 11); }
+
 void chain_prepare() {
-  cudaFuncSetAttribute(k_mlp_chain, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  for (int ir : {0, 9, 11})
+    cudaFuncSetAttribute(chain_kernel(ir), cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
 }
 
 void launch_mlp_chain(const ChainMaps& maps, const ChainArgs& a, cudaStream_t s) {
   if (a.M <= 0) return;
   const size_t smem = chain_smem_bytes(a);
+  const ChainKernel k = chain_kernel(a.ix ? a.ir : 0);
   if (g_dense_prio == 0 && !a.pdl) {
-    k_mlp_chain<<<(a.M + CBM - 1) / CBM, C_THREADS, smem, s>>>(maps, a);
+    k<<<(a.M + CBM - 1) / CBM, C_THREADS, smem, s>>>(maps, a);
     return;
   }
   cudaLaunchConfig_t cfg{};
@@ -349,7 +449,7 @@ void launch_mlp_chain(const ChainMaps& maps, const ChainArgs& a, cudaStream_t s)
   }
   cfg.attrs = at;
   cfg.numAttrs = na;
-  cudaLaunchKernelEx(&cfg, k_mlp_chain, maps, a);
+  cudaLaunchKernelEx(&cfg, k, maps, a);
 }
 
 }  // namespace rec

@@ -196,7 +196,10 @@ struct ChainArgs {
   int nchunk;             // N-chunk rows per MMA / weight box (128 or 256), set by chain_configure
   unsigned long long* dbg;  // diagnostic: %globaltimer stamps of CTA 0 (nullptr = off)
   int dbg_mode;             // diagnostic: bit0 skip TMEM loads, bit1 skip hidden smem stores
+  const float* ix;          // top chain with the dot interaction fused (nullptr = A by TMA):
+  int ir;                   //   X [M][ir][32] fp32, ir = T + 1 (chain_interact_supported)
 };
+bool chain_interact_supported(int T, int D);
 size_t chain_smem_bytes(const ChainArgs& a);
 bool chain_configure(ChainArgs& a);   // false: does not fit in shared memory
 void chain_prepare();                 // per-device kernel attribute

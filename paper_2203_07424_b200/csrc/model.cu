@@ -198,7 +198,8 @@ void enqueue_interact_top(rec_model_s* m, Workspace& w, cudaStream_t st, int B, 
   }
   // a5: interaction -> A_top
   cudaEvent_t e1 = gev ? nullptr : prof_begin(m, st);
-  if (!(m->diag_skip & 4)) launch_interact(w.X, B, dB, T, D, w.A_top, m->Ktop_pad, st);
+  const bool fused = m->chain_top && m->fuse_interact;
+  if (!(m->diag_skip & 4) && !fused) launch_interact(w.X, B, dB, T, D, w.A_top, m->Ktop_pad, st);
   prof_end(m, st, 2, e1);
   mark(gev, 4, st);
   // a6: top MLP; the last hidden layer's epilogue applies the width-1 layer + sigmoid
@@ -210,11 +211,15 @@ void enqueue_interact_top(rec_model_s* m, Workspace& w, cudaStream_t st, int B, 
     a.dM = dB;
     a.ctr = ctr_out;
     a.logit = logit_out;
+    if (fused) {
+      a.ix = w.X;
+      a.ir = T + 1;
+    }
     cudaEvent_t e = gev ? nullptr : prof_begin(m, st);
     launch_mlp_chain(w.chain_top, a, st);
     prof_end(m, st, 1, e);
     mark(gev, 5, st);
-    m->launches += 2;
+    m->launches += fused ? 1 : 2;
     return;
   }
   for (int j = 0; j < nt; ++j) {
@@ -1084,6 +1089,7 @@ rec_status rec_model_create(const rec_model_desc* d, rec_model_t* out) {
     if (const char* fd = getenv("REC_FUSE_DENSE")) m->fuse_dense = atoi(fd) != 0;
     if (const char* tg = getenv("REC_TOWER_GROUP")) m->tower_group = atoi(tg) != 0;
     if (const char* cp = getenv("REC_CHAIN_PDL")) m->chain_pdl = atoi(cp) != 0;
+    if (const char* fi = getenv("REC_FUSE_INTERACT")) m->fuse_interact = atoi(fi) != 0;
     if (const char* gs = getenv("REC_GEMM_STAGES")) g_gemm_stages = atoi(gs);
     if (const char* g2 = getenv("REC_GEMM_2SM")) g_gemm_2sm = atoi(g2);
     if (const char* gn = getenv("REC_GEMM_NARROW")) g_gemm_narrow = atoi(gn);
@@ -1243,6 +1249,10 @@ rec_status rec_model_create(const rec_model_desc* d, rec_model_t* out) {
     m->chain_bottom = build(m->bottom, m->chain_bottom_args, &m->bias_bottom_all, GEMM_OUT_X_F32);
     if (m->arch == REC_ARCH_DLRM)  // MT-WnD towers run as per-layer GEMMs (1024-wide)
       m->chain_top = build(m->top, m->chain_top_args, &m->bias_top_all, GEMM_OUT_CTR);
+    // the fused interaction builds layer 0's A (Ktop_pad columns) in the activation buffer
+    if (!(m->chain_top && m->arch == REC_ARCH_DLRM && chain_interact_supported(m->T, m->D) &&
+          m->chain_top_args.act_kblocks * 64 >= m->chain_top_args.K[0]))
+      m->fuse_interact = 0;
   }
 
   // ---------------------------------------------------------------- workspaces

@@ -143,6 +143,7 @@ struct rec_model_s {
   int sls_pdl = 1;    // REC_PDL=0 disables programmatic dependent launch of the SLS
   int fuse_dense = 0;
   int chain_pdl = 1;    // top fused MLP launched with PDL after the interaction (REC_CHAIN_PDL)
+  int fuse_interact = 0; // dot interaction inside the top chain (REC_FUSE_INTERACT=1; measured -0.4 %)
   int tower_group = 1;  // MT-WnD: one grouped launch per tower layer (REC_TOWER_GROUP=0: per task)  // dense features generated by the SLS kernel (REC_FUSE_DENSE)
   int diag_skip = 0;  // REC_STEP_DIAG (diagnostic): stages dropped from the synthetic step
   // MLP

@@ -306,3 +306,33 @@ def test_bench_sls_measurement_call():
     m.rec_synth_query_async(0, segs, after)
     m.rec_sync(0)
     assert np.array_equal(after.cpu().numpy(), before.cpu().numpy())
+
+
+@pytest.mark.parametrize("name,cfg,B", [("tiny", W.TINY, 300),
+                                        ("rmc1", W.small_variant(W.RMC1, 20000), 300),
+                                        ("rmc3", W.small_variant(W.RMC3, 20000), 1),
+                                        ("rmc1_fp32", W.small_variant(W.RMC1, 20000).with_(
+                                            value_mode=W.REC_VALUES_FP32), 257)])
+def test_fused_interaction_bit_identical(name, cfg, B, monkeypatch):
+    """The dot interaction computed inside the top chain (REC_FUSE_INTERACT=1) gives the same CTR and
+    logit bits as the separate k_interact kernel + TMA-loaded A (REC_FUSE_INTERACT=0), and
+    both stay within the oracle bar."""
+    segs = W.random_segments(B, seed=31)
+    ind, off, dense = gen.gen_batch(cfg, 1, segs)
+    out = {}
+    for fuse in ("1", "0"):
+        monkeypatch.setenv("REC_FUSE_INTERACT", fuse)
+        m = _model(cfg, max_batch=max(B, 64))
+        ctr = np.zeros(B, np.float32)
+        logit = np.zeros(B, np.float32)
+        m.rec_query_debug(dense, ind, off, B, ctr, logits=logit)
+        ctr_g = np.zeros(B, np.float32)
+        m.rec_query(dense, ind, off, B, ctr_g)  # the captured-graph path
+        out[fuse] = (ctr, logit, ctr_g)
+        del m
+    assert np.array_equal(out["1"][0], out["0"][0])
+    assert np.array_equal(out["1"][1], out["0"][1])
+    assert np.array_equal(out["1"][2], out["0"][2])
+    assert np.array_equal(out["1"][2], out["1"][0])
+    exp = fw.forward(cfg, 1, dense, ind, off, return_all=True)
+    assert np.abs(out["1"][0].astype(np.float64) - exp["ctr"]).max() <= CTR_TOL
