@@ -153,6 +153,9 @@ def host_cores() -> int:
         return os.cpu_count() or 1
 
 
+# largest max-batch d the serving search may pick (BASELINE configs[1]: RMC1 batch 256-1024)
+SEARCH_D_MAX = {"DLRM-RMC1": 1024, "DLRM-tiny": 64}
+
 from harness.sla import rank_share, gather_latencies, p95_nearest_rank, sla_search  # noqa: E402
 from harness.schedsearch import gradient_search  # noqa: E402
 
@@ -401,7 +404,7 @@ def run_ours(args):
         lam_hint = [0.5 * value]
 
         def evaluate(m, dd):
-            lam, pr = sla_search(model, cfg, world, rank, dist, m, dd, lam_hint[0],
+            lam, pr = sla_search(serve_model, cfg, world, rank, dist, m, dd, lam_hint[0],
                                  args.sla_queries * world, cfg.sla_ms, tau_ms=args.fusion_timeout_ms)
             probes_all[f"m{m}_d{dd}"] = pr
             if lam > 0:
@@ -409,7 +412,13 @@ def run_ours(args):
             return lam
 
         ms = [x for x in (1, 2, 4, 8, 16) if x <= m_streams]
-        ds = [x for x in (256, 512, 1024) if x <= d]
+        # the policy's maximum fusion batch d ("maximum batch sizes fusing queries",
+        # bounded only by the SLA); RMC1's BASELINE config fixes 256-1024 (reading R30)
+        d_max = args.max_batch_search or SEARCH_D_MAX.get(cfg.name, 4096)
+        ds = [x for x in (256, 512, 1024, 2048, 4096) if x <= max(d, d_max)]
+        serve_model = model
+        if max(ds) > d:  # a second handle with the larger workspaces (tables are regenerated)
+            serve_model = RecModel(cfg, seed=1, max_batch=max(ds), streams=m_streams, device=local)
         res = gradient_search(evaluate, ms, ds, noise=0.02)
         sla = {"sla_ms": cfg.sla_ms, "percentile": "p95 (nearest rank)",
                "lambda_star_qps": res["qps"], "policy": {"streams": res["m"], "max_batch": res["d"]},
@@ -680,6 +689,9 @@ def main():
     ap.add_argument("--queries", type=int, default=20000)
     ap.add_argument("--e2e-steps", type=int, default=3000)
     ap.add_argument("--sla-queries", type=int, default=100000, help="Poisson queries per probe per GPU")
+    ap.add_argument("--max-batch-search", type=int, default=0,
+                    help="largest fusion batch d in the Alg. 1 search (0 = per-config default: "
+                         "1024 for RMC1 and tiny, 4096 otherwise)")
     ap.add_argument("--fusion-timeout-ms", type=float, default=0.0,
                     help="serving policy tau: a partial batch waits up to tau for more queries (R15)")
     ap.add_argument("--cpu-items", type=int, default=256)

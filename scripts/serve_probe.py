@@ -27,10 +27,14 @@ def main():
     out = {}
     for st in ms:
         tr = W.poisson_trace(a.rate, a.queries, seed=12)
+        m.rec_profile(False)  # resets the host-time counters of the submit path
         rep = m.rec_serve(tr, cfg.sla_ms, st, a.d, fusion_timeout_ms=a.tau, warmup_frac=0.1)
         out[st] = {k: (round(v, 3) if isinstance(v, float) else v) for k, v in rep.items()
                    if k in ("offered_qps", "achieved_qps", "p50_ms", "p95_ms", "batches", "mean_batch",
                             "stable", "breakdown_ms")}
+        nb = max(1, rep.get("batches", 1))
+        # host microseconds per batch: node-param update, graph launch, slot wait, whole submit
+        out[st]["host_us_per_batch"] = [round(m.rec_profile_read(k)[0] * 1e3 / nb, 2) for k in (5, 6, 7, 8)]
     print(json.dumps({"config": cfg.name, "rate": a.rate, "tau": a.tau, "by_streams": out}))
 
 
