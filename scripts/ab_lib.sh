@@ -1,6 +1,6 @@
 # A/B of library variants (REC_LIB_PATH) on one box: RMC1 step throughput + SLS rooflines
-B="--sla-queries 0 --no-cpu-baseline --e2e-steps 0 --roofline-steps 100 --sls-batches 200"
-P="import json,sys; d=json.loads(sys.stdin.read()); r=d['roofline']; print(round(d['value']), round(r['frac'],3), round(r['serialized']['frac'],3), round(r['isolated']['frac'],3), round(r['in_step_aggregate']['frac'],3))"
+B="--sla-queries 0 --no-cpu-baseline --e2e-steps 0 --roofline-steps 100 --sls-batches 200 --mlp-batch 0 --config ${CFG:-rmc1}"
+P="import json,sys; d=json.loads(sys.stdin.read()); r=d['roofline']; g=lambda k: round(r.get(k,{}).get('frac',-1),3); print(round(d['value']), round(r['frac'],3), g('serialized'), g('isolated'), g('in_step_aggregate'))"
 for i in 1 2; do
 for L in default "$@"; do
   echo -n "$L "
