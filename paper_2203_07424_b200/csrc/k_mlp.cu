@@ -186,6 +186,22 @@ __global__ void __launch_bounds__(C_THREADS, REC_CHAIN_MINB)
 
   if (warp == 0) {
     // ------------------------------------------------ TMA producer: (layer, n-chunk, k-block)
+    // With PDL, the weight tiles of the first ring fill do not depend on the predecessor
+    // grid: issue them before waiting for it, then only the A tiles wait (pre stages).
+    int pre = 0;
+    if (IR == 0 && args.pdl) {
+      const int nkb0 = (args.K[0] + CBK - 1) / CBK;
+      pre = min(S, nkb0 * ((args.N[0] + NCH - 1) / NCH));
+      if (lane == 0) {
+        for (int i = 0; i < pre; ++i) {
+          uint8_t* st = ring + i * C_STAGE;
+          sm100::mbar_arrive_expect_tx(&full[i], C_A_BYTES + args.wbox[0] * CBK * 2);
+          sm100::tma_load_2d(st + C_A_BYTES, wmap(maps, 0), &full[i], (i % nkb0) * CBK, (i / nkb0) * NCH);
+        }
+      }
+      __syncwarp();
+      cudaGridDependencySynchronize();  // A written by the predecessor grid
+    }
     int it = 0;
     for (int l = 0; l < nl; ++l) {
       const int K = args.K[l], N = args.N[l];
@@ -197,12 +213,11 @@ __global__ void __launch_bounds__(C_THREADS, REC_CHAIN_MINB)
         for (int kb = 0; kb < nkb; ++kb, ++it) {
           const int s = it % S, use = it / S;
           if (use > 0) sm100::mbar_wait(&empty[s], (use - 1) & 1);
-          if (IR == 0 && args.pdl && it == 0) cudaGridDependencySynchronize();  // A written by predecessor
           if (lane == 0) {
             uint8_t* st = ring + s * C_STAGE;
-            sm100::mbar_arrive_expect_tx(&full[s], bytes);
+            if (it >= pre) sm100::mbar_arrive_expect_tx(&full[s], bytes);
             if (a_tma) sm100::tma_load_2d(st, &maps.a0, &full[s], kb * CBK, m0);
-            sm100::tma_load_2d(st + C_A_BYTES, wmap(maps, l), &full[s], kb * CBK, n0);
+            if (it >= pre) sm100::tma_load_2d(st + C_A_BYTES, wmap(maps, l), &full[s], kb * CBK, n0);
             if (it == 0) STAMP(2);
           }
           __syncwarp();
