@@ -15,8 +15,93 @@
 #include <cstring>
 #include <mutex>
 
+#include <cuda.h>
+
 #include "common.cuh"
 #include "model.h"
+
+// ------------------------------------------------------------------ SM partitions
+// REC_GREEN_SMS=n (experiment): the dense stages (dense features, bottom, interaction, top)
+// run on streams of a green context holding n SMs, the SLS on the remaining SMs, so no SM
+// hosts both (DESIGN.md §6 co-location).  Driver entry points are resolved at run time.
+template <typename F>
+static F drv_fn(const char* name) {
+  void* p = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) != cudaSuccess ||
+      q != cudaDriverEntryPointSuccess)
+    return nullptr;
+  return reinterpret_cast<F>(p);
+}
+static bool green_setup(int device, int n_dense, void** out) {  // out[4]: 2 CUgreenCtx + 2 CUcontext
+  auto getdev = drv_fn<decltype(&cuDeviceGet)>("cuDeviceGet");
+  auto getres = drv_fn<decltype(&cuDeviceGetDevResource)>("cuDeviceGetDevResource");
+  auto split = drv_fn<decltype(&cuDevSmResourceSplitByCount)>("cuDevSmResourceSplitByCount");
+  auto gen = drv_fn<decltype(&cuDevResourceGenerateDesc)>("cuDevResourceGenerateDesc");
+  auto create = drv_fn<decltype(&cuGreenCtxCreate)>("cuGreenCtxCreate");
+  if (!getdev || !getres || !split || !gen || !create) return false;
+  CUdevice dev;
+  if (getdev(&dev, device) != CUDA_SUCCESS) return false;
+  CUdevResource all{}, part[1]{}, rest{};
+  unsigned nb = 1;
+  if (getres(dev, &all, CU_DEV_RESOURCE_TYPE_SM) != CUDA_SUCCESS) return false;
+  if (split(part, &nb, &all, &rest, 0, static_cast<unsigned>(n_dense)) != CUDA_SUCCESS || nb != 1) return false;
+  CUdevResourceDesc dd, ds;
+  if (gen(&dd, part, 1) != CUDA_SUCCESS || gen(&ds, &rest, 1) != CUDA_SUCCESS) return false;
+  CUgreenCtx g0, g1;
+  if (create(&g0, dd, dev, CU_GREEN_CTX_DEFAULT_STREAM) != CUDA_SUCCESS) return false;
+  if (create(&g1, ds, dev, CU_GREEN_CTX_DEFAULT_STREAM) != CUDA_SUCCESS) return false;
+  out[0] = g0;
+  out[1] = g1;
+  auto toctx = drv_fn<decltype(&cuCtxFromGreenCtx)>("cuCtxFromGreenCtx");
+  CUcontext c0, c1;
+  if (!toctx || toctx(&c0, g0) != CUDA_SUCCESS || toctx(&c1, g1) != CUDA_SUCCESS) return false;
+  out[2] = c0;
+  out[3] = c1;
+  if (getenv("REC_VERBOSE"))
+    fprintf(stderr, "[rec] SM partition: dense %u SMs, SLS %u SMs\n", part[0].sm.smCount, rest.sm.smCount);
+  return true;
+}
+// Kernel-node update of a graph node captured on a green-context stream: the runtime update
+// would name the primary context, so the driver call carries the kernel handle and the
+// partition's context.
+static cudaError_t green_node_update(cudaGraphExec_t exec, cudaGraphNode_t node, void* ctx,
+                                     const cudaKernelNodeParams& kp) {
+  static auto upd = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPointByVersion("cuGraphExecKernelNodeSetParams", &p, 12000, cudaEnableDefault, &q) !=
+            cudaSuccess || q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<CUresult (*)(CUgraphExec, CUgraphNode, const CUDA_KERNEL_NODE_PARAMS_v2*)>(p);
+  }();
+  if (!upd) return cudaErrorNotSupported;
+  CUDA_KERNEL_NODE_PARAMS_v2 p{};
+  cudaKernel_t k;
+  cudaError_t e = cudaGetKernel(&k, kp.func);
+  if (e != cudaSuccess) return e;
+  p.func = nullptr;
+  p.kern = reinterpret_cast<CUkernel>(k);
+  p.ctx = static_cast<CUcontext>(ctx);
+  p.gridDimX = kp.gridDim.x;
+  p.gridDimY = kp.gridDim.y;
+  p.gridDimZ = kp.gridDim.z;
+  p.blockDimX = kp.blockDim.x;
+  p.blockDimY = kp.blockDim.y;
+  p.blockDimZ = kp.blockDim.z;
+  p.sharedMemBytes = kp.sharedMemBytes;
+  p.kernelParams = kp.kernelParams;
+  return upd(reinterpret_cast<CUgraphExec>(exec), reinterpret_cast<CUgraphNode>(node), &p) == CUDA_SUCCESS
+             ? cudaSuccess
+             : cudaErrorInvalidValue;
+}
+static bool green_stream(void* g, cudaStream_t* s) {
+  auto mk = drv_fn<decltype(&cuGreenCtxStreamCreate)>("cuGreenCtxStreamCreate");
+  CUstream cs;
+  if (!mk || mk(&cs, static_cast<CUgreenCtx>(g), CU_STREAM_NON_BLOCKING, 0) != CUDA_SUCCESS) return false;
+  *s = reinterpret_cast<cudaStream_t>(cs);
+  return true;
+}
 
 namespace rec {
 
@@ -414,6 +499,18 @@ static rec_status synth_chain(rec_model_s* m, Workspace& w, SynthSlot& sl, bool 
     }
     m->launches += 2;
     mark(gev, 2, s);
+    if (m->green_sms > 0 && !(m->diag_skip & 2)) {
+      // SM partitions: the join and the dense tail run on the dense partition's stream
+      REC_CUDA(cudaEventRecord(w.ev_g1, s));
+      REC_CUDA(cudaStreamWaitEvent(sb, w.ev_g1, 0));
+      mark(gev, 3, sb);
+      enqueue_interact_top(m, w, sb, w.cap, w.dB, w.ctr, w.logit, gev);
+      REC_CUDA(cudaEventRecord(w.ev_g2, sb));
+      REC_CUDA(cudaStreamWaitEvent(s, w.ev_g2, 0));
+      cudaError_t err = cudaGetLastError();
+      if (err != cudaSuccess) return cuda_fail(err, "synthetic chain launch");
+      return REC_OK;
+    }
     REC_CUDA(cudaStreamWaitEvent(s, w.ev_join, 0));
     mark(gev, 3, s);
     if (!(m->diag_skip & 2)) {
@@ -564,7 +661,8 @@ rec_status synth_submit(rec_model_s* m, Workspace& w, const int32_t* segs, int n
     kp.gridDim = grid;
     kp.blockDim = block;
     kp.kernelParams = args_a;
-    REC_CUDA(cudaGraphExecKernelNodeSetParams(V.exec, V.gen_node, &kp));
+    if (m->green_sms > 0) REC_CUDA(green_node_update(V.exec, V.gen_node, m->green_cu[1], kp));
+    else REC_CUDA(cudaGraphExecKernelNodeSetParams(V.exec, V.gen_node, &kp));
     if (fused && V.dense_node) {
       cudaKernelNodeParams kd{};
       void* args_d[2] = {sl.sb, &sl.ga};
@@ -572,7 +670,8 @@ rec_status synth_submit(rec_model_s* m, Workspace& w, const int32_t* segs, int n
       kd.gridDim = grid;
       kd.blockDim = block;
       kd.kernelParams = args_d;
-      REC_CUDA(cudaGraphExecKernelNodeSetParams(V.exec, V.dense_node, &kd));
+      if (m->green_sms > 0) REC_CUDA(green_node_update(V.exec, V.dense_node, m->green_cu[0], kd));
+      else REC_CUDA(cudaGraphExecKernelNodeSetParams(V.exec, V.dense_node, &kd));
     }
     const double t2 = host_now_ns();
     REC_CUDA(cudaGraphLaunch(V.exec, w.stream));
@@ -785,6 +884,8 @@ static void free_model(rec_model_s* m) {
     if (w.ev_join) cudaEventDestroy(w.ev_join);
     if (w.ev_sls) cudaEventDestroy(w.ev_sls);
     if (w.ev_done) cudaEventDestroy(w.ev_done);
+    if (w.ev_g1) cudaEventDestroy(w.ev_g1);
+    if (w.ev_g2) cudaEventDestroy(w.ev_g2);
     if (w.stream_c) {
       cudaStreamSynchronize(w.stream_c);
       cudaStreamDestroy(w.stream_c);
@@ -823,6 +924,11 @@ static void free_model(rec_model_s* m) {
   }
   for (auto e : m->prof_pool) cudaEventDestroy(e);
   dist_destroy(m);
+  if (m->green[0] || m->green[1]) {  // after the workspaces' streams are gone
+    auto destroy = drv_fn<decltype(&cuGreenCtxDestroy)>("cuGreenCtxDestroy");
+    for (void* g : m->green)
+      if (g && destroy) destroy(static_cast<CUgreenCtx>(g));
+  }
   delete m;
 }
 
@@ -1090,6 +1196,17 @@ rec_status rec_model_create(const rec_model_desc* d, rec_model_t* out) {
     if (const char* tg = getenv("REC_TOWER_GROUP")) m->tower_group = atoi(tg) != 0;
     if (const char* cp = getenv("REC_CHAIN_PDL")) m->chain_pdl = atoi(cp) != 0;
     if (const char* fi = getenv("REC_FUSE_INTERACT")) m->fuse_interact = atoi(fi) != 0;
+    if (const char* gs = getenv("REC_GREEN_SMS")) {
+      const int n = atoi(gs);
+      void* g[4] = {nullptr, nullptr, nullptr, nullptr};
+      if (n > 0 && green_setup(m->device, n, g)) {
+        m->green_sms = n;
+        for (int k = 0; k < 2; ++k) {
+          m->green[k] = g[k];
+          m->green_cu[k] = g[2 + k];
+        }
+      }
+    }
     if (const char* gs = getenv("REC_GEMM_STAGES")) g_gemm_stages = atoi(gs);
     if (const char* g2 = getenv("REC_GEMM_2SM")) g_gemm_2sm = atoi(g2);
     if (const char* gn = getenv("REC_GEMM_NARROW")) g_gemm_narrow = atoi(gn);
@@ -1262,8 +1379,18 @@ rec_status rec_model_create(const rec_model_desc* d, rec_model_t* out) {
     rec::Workspace& w = m->ws[s];
     w.cap = cap;
     w.idx_cap = idx_cap;
-    CHECK_CUDA_CREATE(cudaStreamCreateWithFlags(&w.stream, cudaStreamNonBlocking));
-    CHECK_CUDA_CREATE(cudaStreamCreateWithFlags(&w.stream_b, cudaStreamNonBlocking));
+    if (m->green_sms > 0) {
+      if (!green_stream(m->green[1], &w.stream) || !green_stream(m->green[0], &w.stream_b)) {
+        set_error("green-context stream creation failed");
+        free_model(m);
+        return REC_E_CUDA;
+      }
+      CHECK_CUDA_CREATE(cudaEventCreateWithFlags(&w.ev_g1, cudaEventDisableTiming));
+      CHECK_CUDA_CREATE(cudaEventCreateWithFlags(&w.ev_g2, cudaEventDisableTiming));
+    } else {
+      CHECK_CUDA_CREATE(cudaStreamCreateWithFlags(&w.stream, cudaStreamNonBlocking));
+      CHECK_CUDA_CREATE(cudaStreamCreateWithFlags(&w.stream_b, cudaStreamNonBlocking));
+    }
     CHECK_CUDA_CREATE(cudaEventCreateWithFlags(&w.ev_fork, cudaEventDisableTiming));
     CHECK_CUDA_CREATE(cudaEventCreateWithFlags(&w.ev_join, cudaEventDisableTiming));
     CHECK_CUDA_CREATE(cudaStreamCreateWithFlags(&w.stream_c, cudaStreamNonBlocking));

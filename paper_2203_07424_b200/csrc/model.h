@@ -59,6 +59,7 @@ struct Workspace {
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaStream_t stream_c = nullptr;   // pipeline lanes: interaction + top of this workspace's batch
   cudaEvent_t ev_sls = nullptr, ev_done = nullptr;  // pipeline capture edges
+  cudaEvent_t ev_g1 = nullptr, ev_g2 = nullptr;     // SM-partition (green context) edges
   int* dB = nullptr;                 // device batch size of the in-flight synthetic batch
   int4* gsegs = nullptr;             // device segments for batches with > kParamSegs segments
   int cap = 0;                       // max items
@@ -143,6 +144,9 @@ struct rec_model_s {
   int sls_pdl = 1;    // REC_PDL=0 disables programmatic dependent launch of the SLS
   int fuse_dense = 0;
   int chain_pdl = 1;    // top fused MLP launched with PDL after the interaction (REC_CHAIN_PDL)
+  int green_sms = 0;    // SMs reserved for the dense stages (REC_GREEN_SMS; 0 = shared SMs)
+  void* green[2] = {nullptr, nullptr};  // CUgreenCtx: [0] dense partition, [1] SLS partition
+  void* green_cu[2] = {nullptr, nullptr};  // their CUcontext handles (graph node updates)
   int fuse_interact = 0; // dot interaction inside the top chain (REC_FUSE_INTERACT=1; measured -0.4 %)
   int tower_group = 1;  // MT-WnD: one grouped launch per tower layer (REC_TOWER_GROUP=0: per task)  // dense features generated by the SLS kernel (REC_FUSE_DENSE)
   int diag_skip = 0;  // REC_STEP_DIAG (diagnostic): stages dropped from the synthetic step

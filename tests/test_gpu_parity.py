@@ -336,3 +336,26 @@ def test_fused_interaction_bit_identical(name, cfg, B, monkeypatch):
     assert np.array_equal(out["1"][2], out["1"][0])
     exp = fw.forward(cfg, 1, dense, ind, off, return_all=True)
     assert np.abs(out["1"][0].astype(np.float64) - exp["ctr"]).max() <= CTR_TOL
+
+
+def test_sm_partition_same_bits(monkeypatch):
+    """REC_GREEN_SMS=24: dense stages on a 24-SM green context, the SLS on the other SMs
+    (captured graphs updated through the driver with the partition's context) — the CTR bits
+    equal the shared-SM default on the graph path."""
+    cfg = W.small_variant(W.RMC1, 20000)
+    segs = W.random_segments(700, seed=41)
+    import torch
+    out = {}
+    for g in ("0", "24"):
+        monkeypatch.setenv("REC_GREEN_SMS", g)
+        m = _model(cfg, max_batch=1024)
+        ctr = torch.zeros(700, dtype=torch.float32, device="cuda")
+        for _ in range(3):  # several launches of the same slot graph (node updates)
+            m.rec_synth_query_async(0, segs, ctr)
+            m.rec_sync(0)
+        out[g] = ctr.cpu().numpy()
+        del m
+    assert np.array_equal(out["0"], out["24"])
+    ind, off, dense = gen.gen_batch(cfg, 1, segs)
+    exp = fw.forward(cfg, 1, dense, ind, off)
+    assert np.abs(out["24"].astype(np.float64) - exp).max() <= CTR_TOL
