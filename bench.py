@@ -225,7 +225,8 @@ def run_ours(args):
     cfg = W.SHORT[args.config]
     d = args.batch
     m_streams = args.streams
-    model = RecModel(cfg, seed=1, max_batch=d, streams=m_streams, device=local)
+    l2p = int(args.l2_persist_mb) << 20
+    model = RecModel(cfg, seed=1, max_batch=d, streams=m_streams, device=local, l2_persist_bytes=l2p)
     dev = torch.device("cuda", local)
     streams = [torch.cuda.ExternalStream(model.rec_stream_handle(k), device=dev) for k in range(m_streams)]
     stream = streams[0]
@@ -418,7 +419,8 @@ def run_ours(args):
         ds = [x for x in (256, 512, 1024, 2048, 4096) if x <= max(d, d_max)]
         serve_model = model
         if max(ds) > d:  # a second handle with the larger workspaces (tables are regenerated)
-            serve_model = RecModel(cfg, seed=1, max_batch=max(ds), streams=m_streams, device=local)
+            serve_model = RecModel(cfg, seed=1, max_batch=max(ds), streams=m_streams, device=local,
+                                   l2_persist_bytes=l2p)
         res = gradient_search(evaluate, ms, ds, noise=0.02)
         sla = {"sla_ms": cfg.sla_ms, "percentile": "p95 (nearest rank)",
                "lambda_star_qps": res["qps"], "policy": {"streams": res["m"], "max_batch": res["d"]},
@@ -482,7 +484,7 @@ def run_ours(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f32 (SLS) + bf16 (MLP, fp32 accumulate)", "data": "synthetic",
-            "config": {"workload": cfg.name, "max_batch_d": d, "tables": cfg.num_tables,
+            "config": {"workload": cfg.name, "max_batch_d": d, "l2_persist_mb": args.l2_persist_mb, "tables": cfg.num_tables,
                        "rows": cfg.rows, "dim": cfg.dim, "pooling": cfg.pooling_lo,
                        "items_per_s": tot_items / (ms_max * 1e-3), "queries_per_step": tot_q / args.steps / world,
                        "mean_query_items": float(sizes.mean()), "parallelism": f"replicas x{world}",
@@ -689,6 +691,8 @@ def main():
     ap.add_argument("--queries", type=int, default=20000)
     ap.add_argument("--e2e-steps", type=int, default=3000)
     ap.add_argument("--sla-queries", type=int, default=100000, help="Poisson queries per probe per GPU")
+    ap.add_argument("--l2-persist-mb", type=int, default=0,
+                    help="L2 persisting window over the hot row prefix of the tables (MB, 0 = off)")
     ap.add_argument("--max-batch-search", type=int, default=0,
                     help="largest fusion batch d in the Alg. 1 search (0 = per-config default: "
                          "1024 for RMC1 and tiny, 4096 otherwise)")
