@@ -460,6 +460,7 @@ void gemm_prepare() {
 }
 
 int g_gemm_2sm = 0;     // REC_GEMM_2SM: CTA-pair GEMM for full-GPU launches (experimental)
+int g_gemm_mt1 = 0;     // REC_GEMM_MT1=1: 128x256 tiles (one M tile per CTA) for full-GPU launches too (A/B)
 int g_gemm_narrow = 0;  // REC_GEMM_NARROW=n: 128-wide N tiles below n 128x256 tiles (measured: RMC2/3 +0.5-1 %, MT-WnD -7 %)
 
 void launch_gemm_tc(const CUtensorMap* tmap_a, const CUtensorMap* tmap_w, const GemmArgs& a,
@@ -470,6 +471,7 @@ void launch_gemm_tc(const CUtensorMap* tmap_a, const CUtensorMap* tmap_w, const 
   else if (a.N <= 128) launch_bn<128, 1>(tmap_a, tmap_w, a, s);
   else if (((a.M + 255) / 256) * ((a.N + 255) / 256) >= 148 && a.K >= 512) {
     if (g_gemm_2sm && tmap_w_half) launch_2sm<256>(tmap_a, tmap_w_half, a, s);  // CTA pairs
+    else if (g_gemm_mt1) launch_bn<256, 1>(tmap_a, tmap_w, a, s);
     else launch_bn<256, 2>(tmap_a, tmap_w, a, s);  // enough 256-row tiles to fill the GPU: share W
   } else if (g_gemm_narrow && tmap_w_half && ((a.M + 127) / 128) * ((a.N + 255) / 256) < g_gemm_narrow) {
     // serving batch, few 128x256 tiles: 128-wide N tiles double the CTAs working on the layer

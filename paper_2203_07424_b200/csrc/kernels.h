@@ -209,6 +209,7 @@ void launch_mlp_chain(const ChainMaps& maps, const ChainArgs& a, cudaStream_t s)
 extern int g_dense_prio;
 extern int g_sls_prio;  // same for the synthetic-index SLS
 extern int g_gemm_stages;
+extern int g_gemm_mt1;
 extern int g_interact_wpc;  // interaction warps per CTA (REC_INTERACT_WPC)
 extern int g_interact_pf;   // few-CTA prefetching interaction kernel (REC_INTERACT_PF)  // per-layer GEMM ring depth cap (REC_GEMM_STAGES; 0 = maximum)
 

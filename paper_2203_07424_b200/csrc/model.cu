@@ -1210,6 +1210,7 @@ rec_status rec_model_create(const rec_model_desc* d, rec_model_t* out) {
     if (const char* gs = getenv("REC_GEMM_STAGES")) g_gemm_stages = atoi(gs);
     if (const char* g2 = getenv("REC_GEMM_2SM")) g_gemm_2sm = atoi(g2);
     if (const char* gn = getenv("REC_GEMM_NARROW")) g_gemm_narrow = atoi(gn);
+    if (const char* g1 = getenv("REC_GEMM_MT1")) g_gemm_mt1 = atoi(g1);
     if (const char* iw = getenv("REC_INTERACT_WPC")) g_interact_wpc = std::max(1, std::min(8, atoi(iw)));
     if (const char* ip = getenv("REC_INTERACT_PF")) g_interact_pf = atoi(ip);
     const char* p = getenv("REC_PDL");
