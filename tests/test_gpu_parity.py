@@ -206,20 +206,21 @@ def test_device_offsets_validation():
     assert ei.value.status == -3
 
 
-@pytest.mark.parametrize("name", ["rmc1", "rmc3"])
+@pytest.mark.parametrize("name", ["rmc1", "rmc2", "rmc3", "mtwnd"])
 def test_full_size_sampled(name):
     """BASELINE sizes (1M rows/table, B = 1024, the bench launch configuration): sampled items."""
     import torch
     cfg = W.SHORT[name]
     B = 1024
+    N = max(cfg.tasks, 1)
     m = _model(cfg, max_batch=B)
     segs = W.random_segments(B, seed=31)
-    cv = torch.zeros(B, device="cuda")
+    cv = torch.zeros(B * N, device="cuda")
     m.rec_synth_query_async(0, segs, cv)
     m.rec_sync(0)
-    ctr = cv.cpu().numpy()
+    ctr = cv.cpu().numpy().reshape(B, N) if N > 1 else cv.cpu().numpy()
     q, it = gen.expand_segments(segs)
-    pick = np.random.default_rng(0).choice(B, size=48, replace=False)
+    pick = np.random.default_rng(0).choice(B, size=24 if name == "rmc2" else 48, replace=False)
     sub = np.array([[q[k], it[k], 1] for k in pick], np.int32)
     i2, o2, d2 = gen.gen_batch(cfg, 1, sub)
     exp = fw.forward(cfg, 1, d2, i2, o2)
