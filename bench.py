@@ -345,8 +345,10 @@ def run_ours(args):
     hbm_peak, bf16_peak, peak_kind = peaks()
     traffic = None  # ncu dram__bytes_read.sum + dram__bytes_write.sum per SLS launch (committed capture)
     tp = os.path.join(ROOT, "profiles", "sls_traffic.json")
-    if os.path.exists(tp) and cfg.name in json.load(open(tp)).get("workload", ""):
-        per_item = json.load(open(tp)).get("dram_bytes_per_item")
+    tj = json.load(open(tp)) if os.path.exists(tp) else {}
+    tj = tj.get("by_workload", {}).get(cfg.name, tj if cfg.name in tj.get("workload", "") else {})
+    if tj:
+        per_item = tj.get("dram_bytes_per_item")
         if per_item:  # scaled to the mean batch of the measured launches
             traffic = per_item * (b2b_bytes / sls_bytes_per_item(cfg, synth=True)) / max(b2b_n, 1)
     sls_bytes = sls_bytes_per_item(cfg, synth=True) * ritems
