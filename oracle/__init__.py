@@ -17,7 +17,9 @@ Modules
   serving  split, fuse, virtual-clock replay, p95, lambda* search (S1-S5)
 
 Parity pins: every function is pinned by tests/test_oracle_*.py against closed
-forms, brute force, invariants or external KATs.  Functions with no such pin say
+forms, brute force, invariants or external KATs; the DLRM composition forward() by an
+explicit-loop brute force on a T = 3, D = 4 model (test_forward_dlrm_bruteforce_tiny),
+MT-WnD's by test_mtwnd_bruteforce_tiny.  Functions with no such pin say
 "parity unpinned" in their docstring (none at present; absolute QPS / GB/s are
 measurements, not oracle outputs).
 """

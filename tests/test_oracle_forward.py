@@ -6,6 +6,7 @@ linearity of pooling, interaction symmetry / ordering / metamorphic table swap,
 textbook special cases of the MLP, and the non-vacuity guard of the CTR check.
 """
 import itertools
+import math
 
 import numpy as np
 import pytest
@@ -189,3 +190,90 @@ def test_ctr_non_vacuity_guard(name):
     W0[0, j] += 1.0
     c2 = fw.forward(cfg, 1, dense, ind, off, params=(bottom, top[:-1] + [(W0, b0)]))
     assert np.max(np.abs(c2 - c)) > 2e-2
+
+
+def _dlrm_brute(cfg, seed, dense, ind, off, B):
+    """The DLRM query forward written out as explicit loops (DESIGN.md
+    R1, R2, R8, R24): every sum, product, ReLU and the interaction's pair order by hand.
+    Parameters come from the seeded parameter scheme (G4/G5, pinned in test_oracle_gen.py);
+    the embedding scale s = round(log2(0.577 sqrt(mean L))) is restated here (G4)."""
+    T, D = cfg.num_tables, cfg.dim
+    bottom, top = gen.model_params(cfg, seed)
+    s = int(round(math.log2(0.577 * math.sqrt(0.5 * (cfg.pooling_lo + cfg.pooling_hi)))))
+    out = []
+    for b in range(B):
+        # F1 SLS: p_t = sum of the bag's rows, in index order (P:140, P:933; R8 sum)
+        p = []
+        for t in range(T):
+            acc = [0.0] * D
+            for j in range(int(off[t * B + b]), int(off[t * B + b + 1])):
+                row = gen.table_values(seed, t, np.array([ind[j]]), D, s, cfg.value_mode)[0]
+                for k in range(D):
+                    acc[k] += float(row[k])
+            p.append(acc)
+        # F2 bottom: ReLU after EVERY layer, including the last (R2)
+        h = [float(v) for v in dense[b]]
+        for Wm, bv in bottom:
+            h = [max(0.0, float(bv[o]) + sum(float(Wm[o, i]) * h[i] for i in range(len(h))))
+                 for o in range(Wm.shape[0])]
+        x = h
+        # F3 interaction: X = [x; p_0; ...; p_{T-1}]; pairs (i, j), i = 1..T, j < i (R1)
+        X = [x] + p
+        v = list(x)
+        for i in range(1, T + 1):
+            for j in range(i):
+                v.append(sum(X[i][k] * X[j][k] for k in range(D)))
+        # F4 top: ReLU on hidden layers, the width-1 last layer linear, then sigmoid (R2)
+        h = v
+        for li, (Wm, bv) in enumerate(top):
+            z = [float(bv[o]) + sum(float(Wm[o, i]) * h[i] for i in range(len(h)))
+                 for o in range(Wm.shape[0])]
+            h = z if li == len(top) - 1 else [max(0.0, q) for q in z]
+        out.append(1.0 / (1.0 + math.exp(-h[0])))
+    return np.array(out)
+
+
+@pytest.mark.parametrize("lo,hi,vm", [(3, 3, 0), (0, 4, 0), (2, 5, 1)])
+def test_forward_dlrm_bruteforce_tiny(lo, hi, vm):
+    """oracle.forward.forward (the composition of F1-F4) equals the loop definition on a
+    T = 3, D = 4 DLRM: catches a bottom without the last ReLU, [pooled; x] order, a transposed
+    pair index, a wrong embedding scale, or the sigmoid on the wrong value."""
+    cfg = W.ModelConfig("dlrm-brute", 3, 40, 4, lo, hi, (5, 6, 4), (7, 3, 1), 0, 8, 1.0,
+                        value_mode=vm)
+    B = 9
+    segs = W.random_segments(B, seed=17, max_seg=4)
+    ind, off, dense = gen.gen_batch(cfg, 1, segs)
+    if lo == 0:
+        assert np.any(np.diff(off) == 0)              # the case has empty bags
+    got = fw.forward(cfg, 1, dense, ind, off)
+    exp = _dlrm_brute(cfg, 1, dense, ind, off, B)
+    assert np.allclose(got, exp, rtol=0, atol=1e-12)
+    assert exp.std() > 1e-3                            # not a constant (non-vacuous)
+
+
+def test_forward_dlrm_bruteforce_detects_plausible_slips():
+    """Negative control of the pin above: each plausible slip in the composition moves the
+    CTRs far beyond 1e-12 on the same inputs."""
+    cfg = W.ModelConfig("dlrm-brute", 3, 40, 4, 3, 3, (5, 6, 4), (7, 3, 1), 0, 8, 1.0)
+    B = 9
+    ind, off, dense = gen.gen_batch(cfg, 1, W.random_segments(B, seed=17, max_seg=4))
+    exp = _dlrm_brute(cfg, 1, dense, ind, off, B)
+    bottom, top = gen.model_params(cfg, 1)
+    shift = gen.emb_shift(3, 3)
+    rows_fn = lambda t, r, s=shift: gen.table_values(1, t, r, 4, s, 0)
+    pooled = fw.sls(rows_fn, 3, B, 4, ind, off)
+    x = fw.mlp(dense.astype(np.float64), bottom, relu_last=True)
+    slips = {
+        "no last bottom ReLU": (fw.mlp(dense.astype(np.float64), bottom, relu_last=False), pooled),
+        "wrong emb shift": (x, fw.sls(lambda t, r: gen.table_values(1, t, r, 4, shift + 1, 0),
+                                      3, B, 4, ind, off)),
+    }
+    for name, (xx, pp) in slips.items():
+        c = fw.sigmoid(fw.mlp(fw.interaction(xx, pp), top, relu_last=False)[:, 0])
+        assert np.max(np.abs(c - exp)) > 1e-6, name
+    # [pooled; x] order instead of [x; pooled]
+    Xs = np.concatenate([pooled, x[:, None]], axis=1)
+    ii, jj = np.tril_indices(4, k=-1)
+    Z = np.einsum("bid,bjd->bij", Xs, Xs)
+    c = fw.sigmoid(fw.mlp(np.concatenate([x, Z[:, ii, jj]], 1), top, relu_last=False)[:, 0])
+    assert np.max(np.abs(c - exp)) > 1e-6
