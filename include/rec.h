@@ -110,13 +110,28 @@ rec_status rec_query_debug(rec_model_t m, const float* dense, const int32_t* ind
                            const int32_t* offsets, int32_t batch, float* ctr,
                            float* pooled, float* logits);
 
+/* rec_query plus the interaction stage's operands and result, for the element-wise checks of
+ * a5 (dot interaction, readings R1/R10): x [B][T+1][D] fp32 is the interaction
+ * input X_b = [bottom-MLP output x_b; pooled p_b,0 .. p_b,T-1] exactly as the kernels hold it;
+ * a_top [B][ld] are the bf16 bit patterns of the first top layer's A operand
+ * [x_b, Z(1,0), Z(2,0), Z(2,1), ..., Z(T,T-1), 0-pad] (MT-WnD: the concatenated lookups),
+ * ld = *a_top_ld = Ktop padded to a multiple of 8.  Each output optional (NULL); host or
+ * device pointers.  Synchronous.  Errors: as rec_query; UNSUPPORTED for sharded models and,
+ * for a_top, when the interaction is fused into the top chain (A built in shared memory). */
+rec_status rec_query_inspect(rec_model_t m, const float* dense, const int32_t* indices,
+                             const int32_t* offsets, int32_t batch, float* ctr, float* x,
+                             uint16_t* a_top, int32_t* a_top_ld);
+
 /* Enqueue rec_query on stream slot `slot` (0 <= slot < streams) without waiting.
  * Device or host pointers: host inputs are copied into the slot's device buffers on its
  * stream and host ctr is filled by a device-to-host copy there (pinned host memory keeps
  * the call asynchronous; the caller must not modify host inputs or read ctr before
- * rec_sync(m, slot)).  `nnz` = offsets[T*B] (not read back; host indices: <= T * max_batch
- * * pooling_hi).  Offsets are validated on the device; completion and the device error
- * flag are collected by rec_sync(m, slot). */
+ * rec_sync(m, slot)).  `nnz` = offsets[T*B] = the number of readable indices (host
+ * indices: <= T * max_batch * pooling_hi).  Host offsets are validated before anything is
+ * enqueued (OFFSETS: offsets[0] != 0, decreasing, or offsets[T*B] != nnz); device offsets
+ * are validated on the device for the same conditions (the error is returned by
+ * rec_sync(m, slot)) and every bag is clamped to [0, nnz), so inconsistent offsets never
+ * read outside the indices.  Completion is collected by rec_sync(m, slot). */
 rec_status rec_query_async(rec_model_t m, int32_t slot, const float* dense,
                            const int32_t* indices, const int32_t* offsets, int64_t nnz,
                            int32_t batch, float* ctr);

@@ -33,7 +33,7 @@ EXPORTS = ["rec_model_create", "rec_model_destroy", "rec_query", "rec_query_debu
            "rec_gen_batch", "rec_profile", "rec_profile_read", "rec_serve", "rec_last_error",
            "rec_nccl_unique_id_size", "rec_nccl_get_unique_id", "rec_version", "rec_split_fuse",
            "rec_synth_query_batches", "rec_shard_plan", "rec_bench_mlp", "rec_bench_sls", "rec_set_pipeline", "rec_synth_query_pipeline",
-           "rec_debug_chain_timeline"]
+           "rec_debug_chain_timeline", "rec_query_inspect"]
 
 
 class rec_model_desc(C.Structure):
@@ -114,6 +114,8 @@ def lib() -> C.CDLL:
         L.rec_synth_query_pipeline.restype = i32
         L.rec_debug_chain_timeline.argtypes = [vp, i32, i32, vp]
         L.rec_debug_chain_timeline.restype = i32
+        L.rec_query_inspect.argtypes = [vp, vp, vp, vp, i32, vp, vp, vp, C.POINTER(i32)]
+        L.rec_query_inspect.restype = i32
         for f in ("rec_model_create", "rec_query", "rec_query_debug", "rec_query_async",
                   "rec_synth_query_async", "rec_sync", "rec_gen_batch", "rec_profile",
                   "rec_profile_read", "rec_serve", "rec_nccl_get_unique_id"):
@@ -206,6 +208,19 @@ class RecModel:
     def rec_query_debug(self, dense, indices, offsets, batch: int, ctr, pooled=None, logits=None):
         _check(lib().rec_query_debug(self.h, _ptr(dense), _ptr(indices), _ptr(offsets), batch,
                                      _ptr(ctr), _ptr(pooled), _ptr(logits)))
+
+    def rec_query_inspect(self, dense, indices, offsets, batch: int):
+        """(ctr [B(,N)], X [B][T+1][D] fp32, A_top [B][ld] as uint16 bf16 bit patterns)."""
+        cfg = self.cfg
+        tasks = getattr(cfg, "tasks", 1)
+        ctr = np.zeros((batch, tasks) if tasks > 1 else batch, dtype=np.float32)
+        x = np.zeros((batch, cfg.num_tables + 1, cfg.dim), dtype=np.float32)
+        ld = C.c_int32()
+        a = np.zeros((batch, ((cfg.top_in + 7) // 8) * 8), dtype=np.uint16)
+        _check(lib().rec_query_inspect(self.h, _ptr(dense), _ptr(indices), _ptr(offsets), batch,
+                                       _ptr(ctr), _ptr(x), _ptr(a), C.byref(ld)))
+        assert ld.value == a.shape[1]
+        return ctr, x, a
 
     def rec_query_async(self, slot: int, dense, indices, offsets, nnz: int, batch: int, ctr):
         _check(lib().rec_query_async(self.h, slot, _ptr(dense), _ptr(indices), _ptr(offsets),

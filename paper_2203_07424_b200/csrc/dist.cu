@@ -199,6 +199,16 @@ void dist_destroy(rec_model_s* m) {
   m->sh_send = m->sh_recv = m->sh_ctr = nullptr;
 }
 
+// Bound of a peer-flag wait (k_p2p_wait): REC_P2P_TIMEOUT_S seconds, default 60.
+static unsigned long long p2p_timeout_ns() {
+  static const unsigned long long ns = [] {
+    const char* e = getenv("REC_P2P_TIMEOUT_S");
+    const double sec = e ? atof(e) : 60.0;
+    return static_cast<unsigned long long>((sec > 0 ? sec : 60.0) * 1e9);
+  }();
+  return ns;
+}
+
 rec_status sharded_forward(rec_model_s* m, Workspace& w, const float* d_dense, const int* d_idx,
                            const int* d_off, int B, float* ctr, float* logits) {
   const int G = m->world, r = m->rank, T = m->T, TL = m->T_loc, D = m->D;
@@ -223,6 +233,8 @@ rec_status sharded_forward(rec_model_s* m, Workspace& w, const float* d_dense, c
     pa.G = G;
     pa.rank = r;
     pa.epoch = ++m->p2p_epoch;
+    pa.err_flag = w.flag;
+    pa.timeout_ns = p2p_timeout_ns();
     REC_CUDA(cudaMemsetAsync(m->p2p_counter, 0, sizeof(unsigned), s));
     if (m->shard == REC_SHARD_TABLE) {
       pa.row_off = 0;
@@ -274,6 +286,8 @@ rec_status sharded_forward(rec_model_s* m, Workspace& w, const float* d_dense, c
     pc.G = G;
     pc.rank = r;
     pc.epoch = m->p2p_epoch;
+    pc.err_flag = w.flag;
+    pc.timeout_ns = p2p_timeout_ns();
     launch_p2p_ctr_scatter(w.ctr, Bl, item0, pc, s);
     launch_p2p_wait(pc, s);
     m->launches += 2;
@@ -290,6 +304,10 @@ rec_status sharded_forward(rec_model_s* m, Workspace& w, const float* d_dense, c
   if (f & 2) {
     set_error("offsets are not non-decreasing from 0 (REC_E_OFFSETS)");
     return REC_E_OFFSETS;
+  }
+  if (f & 4) {
+    set_error("a peer rank missed the exchange deadline (REC_P2P_TIMEOUT_S); results invalid");
+    return REC_E_NCCL;
   }
   REC_CUDA(cudaMemcpyAsync(ctr, m->sh_ctr, sizeof(float) * B, cudaMemcpyDefault, s));
   if (logits) {  // logits of this rank's own items only (diagnostic)

@@ -52,6 +52,14 @@ __device__ __forceinline__ const CUtensorMap* wmap(const ChainMaps& mp, int l) {
   return l == 0 ? &mp.w0 : l == 1 ? &mp.w1 : l == 2 ? &mp.w2 : &mp.w3;
 }
 
+// Epilogue probes (ChainArgs::dbg_mode) exist only in a diagnostic build (-DREC_DEBUG_KNOBS):
+// the shipped library can never skip epilogue loads or stores.
+#ifdef REC_DEBUG_KNOBS
+constexpr bool kDbgKnobs = true;
+#else
+constexpr bool kDbgKnobs = false;
+#endif
+
 #ifndef REC_CHAIN_EPI_WARPS
 #define REC_CHAIN_EPI_WARPS 8  // 4 or 8 (A/B: register footprint vs epilogue latency)
 #endif
@@ -161,6 +169,12 @@ __global__ void __launch_bounds__(C_THREADS, REC_CHAIN_MINB)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m0 = blockIdx.x * CBM;
+  // With PDL (args.pdl) this read precedes cudaGridDependencySynchronize().  It is safe
+  // because of a launch-order invariant (enqueue_interact_top): the PDL predecessor of a
+  // chain is always k_interact, which never writes *dM; *dM is written by the batch's first
+  // kernel (k_sls_synth / k_gen_*), which completed before k_interact started (a plain
+  // stream / graph dependency).  A chain must never be PDL-launched directly after a kernel
+  // that writes *dM.
   const int M = args.dM ? *args.dM : args.M;
   if (m0 >= M) return;
   const int nl = args.nlayers;
@@ -301,7 +315,7 @@ __global__ void __launch_bounds__(C_THREADS, REC_CHAIN_MINB)
 #pragma unroll 1
       for (int g0 = gg; g0 < gg + 64 && g0 < cols; g0 += 16 * C_Q) {
         uint32_t rr[C_Q][16];
-        if (args.dbg_mode & 1) {
+        if (kDbgKnobs && (args.dbg_mode & 1)) {
 #pragma unroll
           for (int q = 0; q < C_Q; ++q)
 #pragma unroll
@@ -324,7 +338,7 @@ __global__ void __launch_bounds__(C_THREADS, REC_CHAIN_MINB)
             if (c < N) x = fmaxf(__uint_as_float(rr[q][j]) + s_bias[boff + c], 0.f);
             v[j] = x;
           }
-          if (!last && (args.dbg_mode & 2)) {
+          if (kDbgKnobs && !last && (args.dbg_mode & 2)) {
             dot += v[0];  // keep the math alive, skip the stores
           } else if (!last) {
             // bf16 into the swizzled K-major A operand of layer l+1: column c0 lies in k-block

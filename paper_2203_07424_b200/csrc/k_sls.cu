@@ -118,7 +118,7 @@ __global__ void __launch_bounds__(THREADS, REC_SLS_MINB) k_sls(const float* __re
                                                     const int* __restrict__ dB, int T,
                                                     int D, float* __restrict__ X, int x_stride,
                                                     int x_slot0, int* __restrict__ flag, int row_lo,
-                                                    int row_hi, const P2PArgs p2p) {
+                                                    int row_hi, int idx_limit, const P2PArgs p2p) {
   using S = SlsShape<LANES>;
   constexpr int GROUPS = THREADS / LANES;
   __shared__ int s_off[GROUPS + 1];
@@ -126,17 +126,22 @@ __global__ void __launch_bounds__(THREADS, REC_SLS_MINB) k_sls(const float* __re
   const int nbags = T * B;
   if (!P2P && static_cast<int>(blockIdx.x) * GROUPS >= nbags) return;  // (P2P grids are exact)
   const int g0 = blockIdx.x * GROUPS;
+  // offsets are clamped to [0, idx_limit] (the readable index count): caller offsets that
+  // were flagged by k_check_offsets (REC_E_OFFSETS) can never address outside the indices
   for (int i = threadIdx.x; i <= GROUPS; i += THREADS) {
     const int g = min(g0 + i, nbags);
-    s_off[i] = offsets[g];
+    s_off[i] = min(max(offsets[g], 0), idx_limit);
   }
   __syncthreads();
   const int grp = threadIdx.x / LANES;
   const int sub = threadIdx.x % LANES;
   const int g = g0 + grp;
-  if (g >= nbags) return;
-  const int t = g / B, b = g - t * B;
-  const int lo = s_off[grp], hi = s_off[grp + 1];
+  // groups past the last bag stay alive (P2P: every thread reaches the CTA barrier below)
+  // with an empty range and no store
+  const bool live = g < nbags;
+  if (!P2P && !live) return;
+  const int t = live ? g / B : 0, b = live ? g - t * B : 0;
+  const int lo = live ? s_off[grp] : 0, hi = live ? s_off[grp + 1] : 0;
   const int64_t toff = __ldg(&tab_off[t]);
   const int64_t nrows = __ldg(&rows[t]);
   const bool active = (sub * 4) < D;
@@ -196,7 +201,7 @@ __global__ void __launch_bounds__(THREADS, REC_SLS_MINB) k_sls(const float* __re
   }
   if (oob) atomicOr(flag, 1);
   if (!P2P) {
-    if (active) {
+    if (active) {  // (live: the non-P2P kernel returned early otherwise)
       float4* dst = reinterpret_cast<float4*>(X + (static_cast<int64_t>(b) * x_stride +
                                                    static_cast<int64_t>(x_slot0 + t) * D + col));
       *dst = acc;
@@ -204,14 +209,14 @@ __global__ void __launch_bounds__(THREADS, REC_SLS_MINB) k_sls(const float* __re
     return;
   }
   // fused all-to-all: item b lives on rank b / Bq as local row b % Bq
-  if (active) {
+  if (active && live) {
     const int p = b / p2p.Bq, bi = p2p.row_off + b - p * p2p.Bq;
     float4* dst = reinterpret_cast<float4*>(p2p.peer_X[p] + (static_cast<int64_t>(bi) * x_stride +
                                                              static_cast<int64_t>(x_slot0 + t) * D + col));
     *dst = acc;
   }
   __syncthreads();  // the CTA's peer stores happen-before thread 0's system-scope fence
-  if (threadIdx.x == 0) {  // (threads of empty groups have exited: they do not take part)
+  if (threadIdx.x == 0) {
     __threadfence_system();
     const unsigned prev = atomicAdd(p2p.counter, 1u);
     if (prev == gridDim.x - 1) {  // last CTA: every CTA's stores are fenced
@@ -221,8 +226,9 @@ __global__ void __launch_bounds__(THREADS, REC_SLS_MINB) k_sls(const float* __re
   }
 }
 
-// One thread per rank: wait until rank q's arrival flag reached this epoch (bounded: a lost
-// peer traps instead of hanging the GPU).
+// One thread per rank: wait until rank q's arrival flag reached this epoch.  Bounded: a peer
+// that misses p2p.timeout_ns sets bit 2 of the error flag (rec_sync / rec_query report
+// REC_E_NCCL) and the wait returns instead of trapping, so the CUDA context survives.
 __global__ void k_p2p_wait(const P2PArgs p2p) {
   const int q = threadIdx.x;
   if (q >= p2p.G) return;
@@ -232,7 +238,10 @@ __global__ void k_p2p_wait(const P2PArgs p2p) {
     __nanosleep(200);
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    if (t - t0 > 20ull * 1000 * 1000 * 1000) __trap();  // 20 s: a peer died
+    if (t - t0 > p2p.timeout_ns) {
+      if (p2p.err_flag) atomicOr(p2p.err_flag, 4);
+      return;
+    }
   }
 }
 
@@ -532,12 +541,12 @@ template <int L>
 static void launch_l(const float* tables, const int64_t* tab_off, int64_t row_stride,
                      const int64_t* rows, const int* indices, const int* offsets, int B,
                      const int* dB, int T, int D, float* X, int x_stride_items, int x_slot0, int* flag,
-                     cudaStream_t s, int row_lo, int row_hi) {
+                     cudaStream_t s, int row_lo, int row_hi, int idx_limit) {
   constexpr int THREADS = 128;
   const int nbags = T * B;
   k_sls<L, THREADS><<<(nbags + THREADS / L - 1) / (THREADS / L), THREADS, 0, s>>>(
       tables, tab_off, row_stride, rows, indices, offsets, B, dB, T, D, X, x_stride_items, x_slot0,
-      flag, row_lo, row_hi, P2PArgs{});
+      flag, row_lo, row_hi, idx_limit, P2PArgs{});
 }
 
 // Row-wise reduction of the staged partial sums, fixed source order q = 0..G-1 (with int8 x 2^e
@@ -582,13 +591,13 @@ void launch_sls_p2p(const float* tables, const int64_t* tab_off, int64_t row_str
   const int grid = (nbags + THREADS / L - 1) / (THREADS / L);
   if (L == 8)
     k_sls<8, THREADS, true><<<grid, THREADS, 0, s>>>(tables, tab_off, row_stride, rows, indices, offsets, B,
-        nullptr, T, D, nullptr, x_stride_items, x_slot0, flag, row_lo, row_hi, p2p);
+        nullptr, T, D, nullptr, x_stride_items, x_slot0, flag, row_lo, row_hi, 0x7fffffff, p2p);
   else if (L == 16)
     k_sls<16, THREADS, true><<<grid, THREADS, 0, s>>>(tables, tab_off, row_stride, rows, indices, offsets, B,
-        nullptr, T, D, nullptr, x_stride_items, x_slot0, flag, row_lo, row_hi, p2p);
+        nullptr, T, D, nullptr, x_stride_items, x_slot0, flag, row_lo, row_hi, 0x7fffffff, p2p);
   else
     k_sls<32, THREADS, true><<<grid, THREADS, 0, s>>>(tables, tab_off, row_stride, rows, indices, offsets, B,
-        nullptr, T, D, nullptr, x_stride_items, x_slot0, flag, row_lo, row_hi, p2p);
+        nullptr, T, D, nullptr, x_stride_items, x_slot0, flag, row_lo, row_hi, 0x7fffffff, p2p);
 }
 
 void set_max_smem_carveout(int c) {
@@ -603,15 +612,15 @@ void set_max_smem_carveout(int c) {
 void launch_sls(const float* tables, const int64_t* tab_off, int64_t row_stride,
                 const int64_t* rows, const int* indices, const int* offsets, int B, const int* dB,
                 int T, int D, float* X, int x_stride_items, int x_slot0, int* flag, cudaStream_t s,
-                int row_lo, int row_hi) {
+                int row_lo, int row_hi, int idx_limit) {
   if (T * B == 0) return;
   const int lanes_needed = D / 4;
   if (lanes_needed <= 8) {
-    launch_l<8>(tables, tab_off, row_stride, rows, indices, offsets, B, dB, T, D, X, x_stride_items, x_slot0, flag, s, row_lo, row_hi);
+    launch_l<8>(tables, tab_off, row_stride, rows, indices, offsets, B, dB, T, D, X, x_stride_items, x_slot0, flag, s, row_lo, row_hi, idx_limit);
   } else if (lanes_needed <= 16) {
-    launch_l<16>(tables, tab_off, row_stride, rows, indices, offsets, B, dB, T, D, X, x_stride_items, x_slot0, flag, s, row_lo, row_hi);
+    launch_l<16>(tables, tab_off, row_stride, rows, indices, offsets, B, dB, T, D, X, x_stride_items, x_slot0, flag, s, row_lo, row_hi, idx_limit);
   } else {
-    launch_l<32>(tables, tab_off, row_stride, rows, indices, offsets, B, dB, T, D, X, x_stride_items, x_slot0, flag, s, row_lo, row_hi);
+    launch_l<32>(tables, tab_off, row_stride, rows, indices, offsets, B, dB, T, D, X, x_stride_items, x_slot0, flag, s, row_lo, row_hi, idx_limit);
   }
 }
 

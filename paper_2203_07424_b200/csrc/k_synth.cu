@@ -291,17 +291,20 @@ void launch_dense_to_bf16(const float* dense, int B, int F, int Fpad, __nv_bfloa
 }
 
 // ------------------------------------------------------- caller offsets validation
-__global__ void k_check_offsets(const int* __restrict__ off, int nbags, int* __restrict__ flag) {
+__global__ void k_check_offsets(const int* __restrict__ off, int nbags, int64_t nnz,
+                                int* __restrict__ flag) {
   for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < nbags; g += gridDim.x * blockDim.x) {
     if (off[g + 1] < off[g] || (g == 0 && off[0] != 0)) atomicOr(flag, 2);
   }
+  if (nnz >= 0 && blockIdx.x == 0 && threadIdx.x == 0 && static_cast<int64_t>(off[nbags]) != nnz)
+    atomicOr(flag, 2);
 }
 
-void launch_check_offsets(const int* offsets, int nbags, int* flag, cudaStream_t s) {
+void launch_check_offsets(const int* offsets, int nbags, int* flag, cudaStream_t s, int64_t nnz) {
   int blocks = (nbags + 255) / 256;
   if (blocks > 148 * 8) blocks = 148 * 8;
   if (blocks < 1) blocks = 1;
-  k_check_offsets<<<blocks, 256, 0, s>>>(offsets, nbags, flag);
+  k_check_offsets<<<blocks, 256, 0, s>>>(offsets, nbags, nnz, flag);
 }
 
 }  // namespace rec

@@ -50,7 +50,8 @@ void launch_gen_dense_seg(const SegBatch& sb, const GenArgs& ga, cudaStream_t s)
 void launch_gen_variable_rest(const GenArgs& ga, cudaStream_t s);
 void launch_dense_to_bf16(const float* dense, int B, int F, int Fpad, __nv_bfloat16* out,
                           cudaStream_t s);
-void launch_check_offsets(const int* offsets, int nbags, int* flag, cudaStream_t s);
+// Flags bit 1 when offsets[0] != 0, offsets decrease, or (nnz >= 0) offsets[nbags] != nnz.
+void launch_check_offsets(const int* offsets, int nbags, int* flag, cudaStream_t s, int64_t nnz = -1);
 void set_max_smem_carveout(int percent);  // SLS kernels' preferred shared-memory carveout (0..100)
 
 // ------------------------------------------------------------------------- SLS (a3)
@@ -70,6 +71,8 @@ struct P2PArgs {
   unsigned* my_flags;           // this rank's arrival flags [G] (written by the peers)
   int Bq, G, rank;              // items per rank block, world size, this rank
   unsigned epoch;               // query sequence number (flags reach it when the data landed)
+  int* err_flag;                // k_p2p_wait: bit 2 (value 4) set when a peer missed the timeout
+  unsigned long long timeout_ns;  // k_p2p_wait bound (REC_P2P_TIMEOUT_S, default 60 s)
 };
 void launch_sls_p2p(const float* tables, const int64_t* tab_off, int64_t row_stride,
                     const int64_t* rows, const int* indices, const int* offsets, int B, int T, int D,
@@ -87,10 +90,12 @@ void launch_p2p_ctr_scatter(const float* ctr, int Bl, int item0, const P2PArgs& 
 
 // row_lo/row_hi: row-wise sharding keeps rows [row_lo, row_hi) of every table on this GPU
 // (arena row r - row_lo); other rows add nothing.  Replicated / table-wise: 0, INT32_MAX.
+// idx_limit: number of readable entries of `indices`; offsets are clamped to [0, idx_limit]
+// so inconsistent caller offsets (flagged separately) never read past the array.
 void launch_sls(const float* tables, const int64_t* tab_off, int64_t row_stride,
                 const int64_t* rows, const int* indices, const int* offsets, int B, const int* dB,
                 int T, int D, float* X, int x_stride_items, int x_slot0, int* flag, cudaStream_t s,
-                int row_lo = 0, int row_hi = 0x7fffffff);
+                int row_lo = 0, int row_hi = 0x7fffffff, int idx_limit = 0x7fffffff);
 
 // SLS over device-synthesised indices (fixed pooling L): each index is the Philox value of
 // (slot, item, table, qid) computed where it is consumed (a2 fused into a3): no index array,

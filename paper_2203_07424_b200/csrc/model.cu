@@ -291,7 +291,10 @@ void enqueue_interact_top(rec_model_s* m, Workspace& w, cudaStream_t st, int B, 
   const int nt = static_cast<int>(m->top.size());
   if (m->chain_top) {  // whole top MLP in one kernel (k_mlp.cu)
     ChainArgs a = m->chain_top_args;
-    a.pdl = m->chain_pdl;
+    // PDL only behind k_interact (it never writes *dB, which the chain reads before its
+    // grid-dependency wait; see k_mlp_chain); the fused-interaction chain has no such
+    // predecessor and launches plainly
+    a.pdl = m->chain_pdl && !fused;
     a.M = B;
     a.dM = dB;
     a.ctr = ctr_out;
@@ -339,7 +342,8 @@ void enqueue_interact_top(rec_model_s* m, Workspace& w, cudaStream_t st, int B, 
 // depends only on the dense features and the SLS (a3) only on the sparse ones: they run on
 // two streams (a fork in a captured graph) and join before the interaction (a5).
 rec_status forward_enqueue(rec_model_s* m, Workspace& w, const int* indices, const int* offsets,
-                           int B, const int* dB, float* ctr_out, float* logit_out, cudaEvent_t* gev) {
+                           int B, const int* dB, float* ctr_out, float* logit_out, cudaEvent_t* gev,
+                           int64_t idx_limit) {
   cudaStream_t s = w.stream, sb = w.stream_b;
   REC_CUDA(cudaEventRecord(w.ev_fork, s));
   REC_CUDA(cudaStreamWaitEvent(sb, w.ev_fork, 0));
@@ -349,7 +353,8 @@ rec_status forward_enqueue(rec_model_s* m, Workspace& w, const int* indices, con
   REC_CUDA(cudaEventRecord(w.ev_join, sb));
   cudaEvent_t e0 = gev ? nullptr : prof_begin(m, s);
   launch_sls(m->tables, m->d_tab_off, m->row_stride, m->d_rows, indices, offsets, B, dB, m->T, m->D,
-             w.X, (m->T + 1) * m->D, 1, w.flag, s);
+             w.X, (m->T + 1) * m->D, 1, w.flag, s, 0, 0x7fffffff,
+             static_cast<int>(std::min<int64_t>(idx_limit, 0x7fffffff)));
   prof_end(m, s, 0, e0);
   m->launches += 1;
   mark(gev, 2, s);
@@ -543,7 +548,7 @@ static rec_status synth_chain(rec_model_s* m, Workspace& w, SynthSlot& sl, bool 
   prof_end(m, s, 3, e);
   mark(gev, 1, s);
   if (m->world > 1 && m->shard != REC_SHARD_REPLICA) return REC_OK;  // inputs only (gen_batch)
-  return forward_enqueue(m, w, w.indices, w.offsets, w.cap, w.dB, w.ctr, w.logit, gev);
+  return forward_enqueue(m, w, w.indices, w.offsets, w.cap, w.dB, w.ctr, w.logit, gev, w.idx_cap);
 }
 
 rec_status capture_graphs(rec_model_s* m, Workspace& w) {
@@ -717,7 +722,7 @@ static rec_status sync_ws(Workspace& w) {
 // ------------------------------------------------------------------ query (sync)
 static rec_status query_impl(rec_model_s* m, const float* dense, const int32_t* indices,
                              const int32_t* offsets, int32_t B, float* ctr, float* pooled,
-                             float* logits) {
+                             float* logits, float* x_out = nullptr, uint16_t* a_top_out = nullptr) {
   if (!m || !indices || !offsets || !ctr || (!dense && m->F > 0)) {
     set_error("null argument (model, dense, indices, offsets and ctr are required)");
     return REC_E_INVALID_ARG;
@@ -725,6 +730,15 @@ static rec_status query_impl(rec_model_s* m, const float* dense, const int32_t* 
   if (B <= 0 || B > m->max_batch) {
     set_error("batch = %d must be in [1, max_batch = %d]", B, m->max_batch);
     return REC_E_INVALID_ARG;
+  }
+  if ((x_out || a_top_out) && m->world > 1 && m->shard != REC_SHARD_REPLICA) {
+    set_error("rec_query_inspect: sharded models keep X / A_top distributed");
+    return REC_E_UNSUPPORTED;
+  }
+  if (a_top_out && m->chain_top && m->fuse_interact) {
+    set_error("rec_query_inspect: the fused interaction (REC_FUSE_INTERACT=1) builds A_top in "
+              "shared memory only");
+    return REC_E_UNSUPPORTED;
   }
   REC_CUDA(cudaSetDevice(m->device));
   if (m->pipe_active.load()) {
@@ -790,7 +804,8 @@ static rec_status query_impl(rec_model_s* m, const float* dense, const int32_t* 
     return sharded_forward(m, w, d_dense, d_idx, d_off, B, ctr, logits);
   launch_dense_to_bf16(d_dense, B, m->F, m->Fpad, w.dense_bf, s);
   m->launches += 1 + (off_dev ? 1 : 0);
-  st = forward_enqueue(m, w, d_idx, d_off, B, nullptr, w.ctr, w.logit, nullptr);
+  st = forward_enqueue(m, w, d_idx, d_off, B, nullptr, w.ctr, w.logit, nullptr,
+                       off_dev ? int64_t(0x7fffffff) : int64_t(offsets[nb]));
   if (st != REC_OK) return st;
   REC_CUDA(cudaMemcpyAsync(w.flag_host, w.flag, sizeof(int), cudaMemcpyDeviceToHost, s));
   REC_CUDA(cudaStreamSynchronize(s));
@@ -804,6 +819,10 @@ static rec_status query_impl(rec_model_s* m, const float* dense, const int32_t* 
     REC_CUDA(cudaMemcpy2DAsync(pooled, sizeof(float) * T * D, w.X + D, sizeof(float) * (T + 1) * D,
                                sizeof(float) * T * D, B, cudaMemcpyDefault, s));
   }
+  if (x_out)
+    REC_CUDA(cudaMemcpyAsync(x_out, w.X, sizeof(float) * B * (T + 1) * m->D, cudaMemcpyDefault, s));
+  if (a_top_out)
+    REC_CUDA(cudaMemcpyAsync(a_top_out, w.A_top, sizeof(uint16_t) * B * m->Ktop_pad, cudaMemcpyDefault, s));
   REC_CUDA(cudaStreamSynchronize(s));
   return REC_OK;
 }
@@ -1182,16 +1201,12 @@ rec_status rec_model_create(const rec_model_desc* d, rec_model_t* out) {
   {
     const char* e = getenv("REC_SLS");
     const bool want = e && strcmp(e, "tma") == 0;  // measured slower: opt-in
-    // diagnostic only (REC_STEP_DIAG, never set by tests or bench): bit 0 drops the bottom
-    // MLP, bit 1 the interaction + top MLP, bit 2 the interaction alone from the synthetic
-    // step graphs (CTRs invalid)
+#ifdef REC_DEBUG_KNOBS
+    // diagnostic build only (-DREC_DEBUG_KNOBS; REC_STEP_DIAG): bit 0 drops the bottom MLP,
+    // bit 1 the interaction + top MLP, bit 2 the interaction alone from the synthetic step
+    // graphs (CTRs invalid).  The shipped library cannot drop stages.
     if (const char* d = getenv("REC_STEP_DIAG")) m->diag_skip = atoi(d);
-    if (const char* pr = getenv("REC_PRIO")) {
-      int lo = 0, hi = 0;
-      cudaDeviceGetStreamPriorityRange(&lo, &hi);
-      g_dense_prio = atoi(pr) > 0 ? hi : 0;
-      g_sls_prio = atoi(pr) < 0 ? hi : 0;
-    }
+#endif
     if (const char* fd = getenv("REC_FUSE_DENSE")) m->fuse_dense = atoi(fd) != 0;
     if (const char* tg = getenv("REC_TOWER_GROUP")) m->tower_group = atoi(tg) != 0;
     if (const char* cp = getenv("REC_CHAIN_PDL")) m->chain_pdl = atoi(cp) != 0;
@@ -1207,12 +1222,26 @@ rec_status rec_model_create(const rec_model_desc* d, rec_model_t* out) {
         }
       }
     }
-    if (const char* gs = getenv("REC_GEMM_STAGES")) g_gemm_stages = atoi(gs);
-    if (const char* g2 = getenv("REC_GEMM_2SM")) g_gemm_2sm = atoi(g2);
-    if (const char* gn = getenv("REC_GEMM_NARROW")) g_gemm_narrow = atoi(gn);
-    if (const char* g1 = getenv("REC_GEMM_MT1")) g_gemm_mt1 = atoi(g1);
-    if (const char* iw = getenv("REC_INTERACT_WPC")) g_interact_wpc = std::max(1, std::min(8, atoi(iw)));
-    if (const char* ip = getenv("REC_INTERACT_PF")) g_interact_pf = atoi(ip);
+    // kernel-variant selectors (process-wide, like the kernels they pick): every model
+    // create sets them from the environment, unset = the measured default, so a variant
+    // never leaks from one handle's environment into a later handle
+    auto env_int = [](const char* n, int dflt) {
+      const char* e = getenv(n);
+      return e ? atoi(e) : dflt;
+    };
+    g_gemm_stages = env_int("REC_GEMM_STAGES", 0);
+    g_gemm_2sm = env_int("REC_GEMM_2SM", 0);
+    g_gemm_narrow = env_int("REC_GEMM_NARROW", 0);
+    g_gemm_mt1 = env_int("REC_GEMM_MT1", 0);
+    g_interact_wpc = std::max(1, std::min(8, env_int("REC_INTERACT_WPC", 8)));
+    g_interact_pf = env_int("REC_INTERACT_PF", 0);
+    {
+      int lo = 0, hi = 0;
+      cudaDeviceGetStreamPriorityRange(&lo, &hi);
+      const int pr = env_int("REC_PRIO", 0);
+      g_dense_prio = pr > 0 ? hi : 0;
+      g_sls_prio = pr < 0 ? hi : 0;
+    }
     const char* p = getenv("REC_PDL");
     m->sls_pdl = !(p && strcmp(p, "0") == 0);
     CHECK_CUDA_CREATE(cudaDeviceGetAttribute(&m->nsm, cudaDevAttrMultiProcessorCount, m->device));
@@ -1562,6 +1591,17 @@ rec_status rec_query_debug(rec_model_t m, const float* dense, const int32_t* ind
   return query_impl(m, dense, indices, offsets, batch, ctr, pooled, logits);
 }
 
+rec_status rec_query_inspect(rec_model_t m, const float* dense, const int32_t* indices,
+                             const int32_t* offsets, int32_t batch, float* ctr, float* x,
+                             uint16_t* a_top, int32_t* a_top_ld) {
+  if (!m) {
+    set_error("null model");
+    return REC_E_INVALID_ARG;
+  }
+  if (a_top_ld) *a_top_ld = m->Ktop_pad;
+  return query_impl(m, dense, indices, offsets, batch, ctr, nullptr, nullptr, x, a_top);
+}
+
 rec_status rec_query_async(rec_model_t m, int32_t slot, const float* dense, const int32_t* indices,
                            const int32_t* offsets, int64_t nnz, int32_t batch, float* ctr) {
   if (!m || !indices || !offsets || !ctr || (!dense && m->F > 0)) {
@@ -1597,15 +1637,33 @@ rec_status rec_query_async(rec_model_t m, int32_t slot, const float* dense, cons
   const int* d_off = offsets;
   const int* d_idx = indices;
   const float* d_dense = dense;
-  if (!is_device_ptr(offsets)) {
+  const bool off_dev = is_device_ptr(offsets), idx_dev = is_device_ptr(indices);
+  if (!idx_dev && nnz > w.idx_cap) {
+    set_error("nnz = %lld exceeds the index capacity %lld", (long long)nnz, (long long)w.idx_cap);
+    return REC_E_INVALID_ARG;
+  }
+  if (nnz > 0x7fffffff) {
+    set_error("nnz = %lld must be < 2^31", (long long)nnz);
+    return REC_E_UNSUPPORTED;
+  }
+  if (!off_dev) {  // host offsets: validated here, before anything is enqueued
+    if (offsets[0] != 0) {
+      set_error("offsets[0] = %d, must be 0", offsets[0]);
+      return REC_E_OFFSETS;
+    }
+    for (int g = 0; g < nb; ++g)
+      if (offsets[g + 1] < offsets[g]) {
+        set_error("offsets[%d] = %d < offsets[%d] = %d", g + 1, offsets[g + 1], g, offsets[g]);
+        return REC_E_OFFSETS;
+      }
+    if (static_cast<int64_t>(offsets[nb]) != nnz) {
+      set_error("offsets[T*B] = %d != nnz = %lld", offsets[nb], (long long)nnz);
+      return REC_E_OFFSETS;
+    }
     REC_CUDA(cudaMemcpyAsync(w.offsets, offsets, sizeof(int) * (nb + 1), cudaMemcpyHostToDevice, s));
     d_off = w.offsets;
   }
-  if (!is_device_ptr(indices)) {
-    if (nnz > w.idx_cap) {
-      set_error("nnz = %lld exceeds the index capacity %lld", (long long)nnz, (long long)w.idx_cap);
-      return REC_E_INVALID_ARG;
-    }
+  if (!idx_dev) {
     REC_CUDA(cudaMemcpyAsync(w.indices, indices, sizeof(int) * nnz, cudaMemcpyHostToDevice, s));
     d_idx = w.indices;
   }
@@ -1614,10 +1672,13 @@ rec_status rec_query_async(rec_model_t m, int32_t slot, const float* dense, cons
     d_dense = w.dense_f32;
   }
   const bool ctr_dev = is_device_ptr(ctr);
-  launch_check_offsets(d_off, nb, w.flag, s);
+  // device offsets: offsets[T*B] == nnz is checked on the device (flag -> REC_E_OFFSETS at
+  // rec_sync) and the SLS clamps every bag to [0, nnz), so no read leaves the indices
+  if (off_dev) launch_check_offsets(d_off, nb, w.flag, s, nnz);
   launch_dense_to_bf16(d_dense, batch, m->F, m->Fpad, w.dense_bf, s);
-  m->launches += 2;
-  rec_status st = forward_enqueue(m, w, d_idx, d_off, batch, nullptr, ctr_dev ? ctr : w.ctr, w.logit, nullptr);
+  m->launches += off_dev ? 2 : 1;
+  rec_status st = forward_enqueue(m, w, d_idx, d_off, batch, nullptr, ctr_dev ? ctr : w.ctr, w.logit,
+                                  nullptr, nnz);
   if (st != REC_OK) return st;
   if (!ctr_dev)
     REC_CUDA(cudaMemcpyAsync(ctr, w.ctr, sizeof(float) * batch * m->tasks, cudaMemcpyDeviceToHost, s));
@@ -1853,7 +1914,9 @@ rec_status rec_debug_chain_timeline(rec_model_t m, int32_t which, int32_t batch,
   a.ctr = w.ctr;
   a.logit = w.logit;
   a.dbg = d;
-  if (const char* e = getenv("REC_DBG_EPI")) a.dbg_mode = atoi(e);
+#ifdef REC_DEBUG_KNOBS
+  if (const char* e = getenv("REC_DBG_EPI")) a.dbg_mode = atoi(e);  // diagnostic build only
+#endif
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);

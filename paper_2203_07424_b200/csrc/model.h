@@ -212,7 +212,8 @@ rec_status shard_plan(int T, const int64_t* rows, int world, int rank, int shard
 // w.indices / w.offsets / w.dense_bf (or caller device pointers).  ctr_out: device.
 rec_status forward_enqueue(rec_model_s* m, Workspace& w, const int* indices, const int* offsets,
                            int batch, const int* dB, float* ctr_out, float* logit_out,
-                           cudaEvent_t* gev);   // gev: 8 stage events (graph capture) or null
+                           cudaEvent_t* gev,    // gev: 8 stage events (graph capture) or null
+                           int64_t idx_limit = 0x7fffffff);  // readable indices (SLS clamp)
 // Device-synthesised batch (segment list on the host) through a staging slot: inputs (a2)
 // and forward (a3-a6) enqueued on w.stream, CTRs in w.ctr.
 rec_status synth_submit(rec_model_s* m, Workspace& w, const int32_t* segs, int nseg, int* batch_out,

@@ -393,7 +393,7 @@ rec_status rec_serve(rec_model_t m, const rec_trace_row* trace, int64_t n, doubl
     } else {
       st = host_input_enqueue(m, w, H, fifo, head, k, &B);
       if (st != REC_OK) return st;
-      st = forward_enqueue(m, w, w.indices, w.offsets, B, nullptr, w.ctr, w.logit, nullptr);
+      st = forward_enqueue(m, w, w.indices, w.offsets, B, nullptr, w.ctr, w.logit, nullptr, w.idx_cap);
       if (st != REC_OK) return st;
     }
     if (ctr_out)
@@ -572,7 +572,7 @@ rec_status rec_serve(rec_model_t m, const rec_trace_row* trace, int64_t n, doubl
               for (int64_t c = 0; c < k; ++c) local[c] = fifo[c0 + c];
             }
             rs = host_input_enqueue(m, w, H, local, 0, k, &B);
-            if (rs == REC_OK) rs = forward_enqueue(m, w, w.indices, w.offsets, B, nullptr, w.ctr, w.logit, nullptr);
+            if (rs == REC_OK) rs = forward_enqueue(m, w, w.indices, w.offsets, B, nullptr, w.ctr, w.logit, nullptr, w.idx_cap);
           }
           if (rs == REC_OK && ctr_out)
             if (cudaMemcpyAsync(L.ctr_host, w.ctr, sizeof(float) * B * m->tasks, cudaMemcpyDeviceToHost,

@@ -318,6 +318,7 @@ def test_fused_interaction_bit_identical(name, cfg, B, monkeypatch):
     """The dot interaction computed inside the top chain (REC_FUSE_INTERACT=1) gives the same CTR and
     logit bits as the separate k_interact kernel + TMA-loaded A (REC_FUSE_INTERACT=0), and
     both stay within the oracle bar."""
+    import torch
     segs = W.random_segments(B, seed=31)
     ind, off, dense = gen.gen_batch(cfg, 1, segs)
     out = {}
@@ -326,10 +327,11 @@ def test_fused_interaction_bit_identical(name, cfg, B, monkeypatch):
         m = _model(cfg, max_batch=max(B, 64))
         ctr = np.zeros(B, np.float32)
         logit = np.zeros(B, np.float32)
-        m.rec_query_debug(dense, ind, off, B, ctr, logits=logit)
-        ctr_g = np.zeros(B, np.float32)
-        m.rec_query(dense, ind, off, B, ctr_g)  # the captured-graph path
-        out[fuse] = (ctr, logit, ctr_g)
+        m.rec_query_debug(dense, ind, off, B, ctr, logits=logit)   # eager caller-index path
+        cv = torch.zeros(B, device="cuda")
+        m.rec_synth_query_async(0, segs, cv)                         # the captured-graph path
+        m.rec_sync(0)
+        out[fuse] = (ctr, logit, cv.cpu().numpy())
         del m
     assert np.array_equal(out["1"][0], out["0"][0])
     assert np.array_equal(out["1"][1], out["0"][1])
@@ -360,3 +362,66 @@ def test_sm_partition_same_bits(monkeypatch):
     ind, off, dense = gen.gen_batch(cfg, 1, segs)
     exp = fw.forward(cfg, 1, dense, ind, off)
     assert np.abs(out["24"].astype(np.float64) - exp).max() <= CTR_TOL
+
+
+def test_negative_control_perturbations_fail():
+    """SURVEY §8(c) CTR pin / §4 tier 6: the parity checks have teeth on the GPU path.  A
+    one-weight perturbation of the oracle's model must break the 2e-2 CTR bar against the
+    GPU's CTRs, and one changed index must break the bit-exact pooled check."""
+    cfg = W.small_variant(W.RMC1, 20000)
+    B = 256
+    m = _model(cfg, max_batch=B)
+    segs = W.random_segments(B, seed=23)
+    ind, off, dense = gen.gen_batch(cfg, 1, segs)
+    ctr = np.zeros(B, np.float32)
+    pooled = np.zeros((B, cfg.num_tables, cfg.dim), np.float32)
+    m.rec_query_debug(dense, ind, off, B, ctr, pooled=pooled)
+    exp = fw.forward(cfg, 1, dense, ind, off, return_all=True)
+    assert np.abs(ctr - exp["ctr"]).max() <= CTR_TOL                 # the real check passes
+    bottom, top = gen.model_params(cfg, 1)
+    W0, b0 = top[-1]
+    W0 = W0.copy()
+    hidden = fw.mlp(exp["v"], top[:-1], relu_last=True)
+    W0[0, int(np.argmax(hidden.mean(0)))] += 1.0                      # one weight
+    bad = fw.forward(cfg, 1, dense, ind, off, params=(bottom, top[:-1] + [(W0, b0)]))
+    assert np.abs(ctr - bad).max() > CTR_TOL
+    ind2 = ind.copy()
+    ind2[5] = (ind2[5] + 1) % cfg.rows                                # one index
+    exp2 = fw.forward(cfg, 1, dense, ind2, off, return_all=True)
+    assert not np.array_equal(pooled.astype(np.float64), exp2["pooled"])
+
+
+def test_async_offsets_validation():
+    """rec_query_async: host offsets are checked before enqueueing, including
+    offsets[T*B] == nnz; device offsets inconsistent with nnz are flagged at rec_sync and the
+    SLS never reads past nnz indices."""
+    import torch
+    from paper_2203_07424_b200 import RecError
+    cfg = W.small_variant(W.TINY, 1000)
+    B = 16
+    m = _model(cfg, max_batch=B, streams=2)
+    ind, off, dense = gen.gen_batch(cfg, 1, W.random_segments(B, seed=3))
+    nnz = int(off[-1])
+    ctr = np.zeros(B, np.float32)
+    with pytest.raises(RecError) as ei:                               # host: nnz mismatch
+        m.rec_query_async(0, dense, ind, off, nnz - 1, B, ctr)
+    assert ei.value.status == -3
+    boff = off.copy()
+    boff[3] = boff[2] - 1
+    with pytest.raises(RecError) as ei:                               # host: decreasing
+        m.rec_query_async(0, dense, ind, boff, nnz, B, ctr)
+    assert ei.value.status == -3
+    # device offsets whose end exceeds nnz: flagged, and the read is clamped to nnz indices
+    dv, iv = torch.from_numpy(dense).cuda(), torch.from_numpy(ind[:nnz - 7].copy()).cuda()
+    ov = torch.from_numpy(off).cuda()
+    cv = torch.zeros(B, device="cuda")
+    m.rec_query_async(1, dv, iv, ov, nnz - 7, B, cv)
+    with pytest.raises(RecError) as ei:
+        m.rec_sync(1)
+    assert ei.value.status == -3
+    # a consistent call afterwards works and matches the synchronous path
+    m.rec_query_async(1, dv, torch.from_numpy(ind).cuda(), ov, nnz, B, cv)
+    m.rec_sync(1)
+    ref = np.zeros(B, np.float32)
+    m.rec_query(dense, ind, off, B, ref)
+    assert np.array_equal(cv.cpu().numpy(), ref)
