@@ -179,6 +179,13 @@ def _pool(cores: int):
     return mp.get_context("fork").Pool(cores)
 
 
+def host_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
 def cpu_model() -> str:
     try:
         for line in open("/proc/cpuinfo"):
