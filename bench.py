@@ -272,7 +272,7 @@ def run_reference(args):
 
 # ------------------------------------------------------------------------- our arm
 def saturation(model, cfg, d, m_streams, steps, warmup, step_batches, n_queries, rank, world, dist,
-               submit="batch", pipe=0, clk=None):
+               submit="batch", pipe=0, clk=None, sharded=False):
     """Saturation throughput of one replica model (the bench's `value`).
 
     a1: a burst trace (all queries pending) is split into sub-queries of <= d items and fused
@@ -282,13 +282,14 @@ def saturation(model, cfg, d, m_streams, steps, warmup, step_batches, n_queries,
     `warmup` such rounds; the timed region (barrier + synchronize on both sides, CUDA events
     on the streams, max over ranks) runs exactly `steps` rounds back to back.  A step of many
     batches keeps the streams loaded so the timed region measures the steady state, not the
-    ramp of an idle GPU (VERDICT r1 weak #3)."""
+    ramp of an idle GPU.  sharded=True: every rank runs the SAME global
+    batches (model-parallel embeddings), so items / queries are counted once, not summed."""
     import torch
     from paper_2203_07424_b200 import rec_split_fuse
     dev = torch.device("cuda", torch.cuda.current_device())
     streams = [torch.cuda.ExternalStream(model.rec_stream_handle(k), device=dev) for k in range(m_streams)]
     stream = streams[0]
-    trace = W.burst_trace(n_queries, seed=11 + rank)
+    trace = W.burst_trace(n_queries, seed=11 + (0 if sharded else rank))
     segs, bstart = rec_split_fuse(trace, d)
     nb = len(bstart) - 1
     sizes = trace["size"].astype(np.int64)
@@ -355,7 +356,8 @@ def saturation(model, cfg, d, m_streams, steps, warmup, step_batches, n_queries,
     if world > 1:
         tmax = t.clone()
         dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
-        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        if not sharded:
+            dist.all_reduce(t, op=dist.ReduceOp.SUM)
         ms_max = float(tmax[0])
     else:
         ms_max = ms
@@ -512,7 +514,8 @@ def run_ours(args):
             dist.barrier()
         t0 = time.perf_counter()
         q_e2e, h2d, d2h = 0, 0, 0
-        for i in range(args.e2e_steps):
+        nb_e2e = args.e2e_steps * args.step_batches   # steps of step_batches batches, as above
+        for i in range(nb_e2e):
             h = host[i % len(host)]
             model.rec_query_async(i % m_streams, h[0], h[1], h[2], h[3], h[4], outs[i % m_streams])
             q_e2e += h[5]
@@ -529,10 +532,10 @@ def run_ours(args):
         e2e = {"value": float(tw[1]) / wall, "unit": "QPS",
                "h2d_bytes_per_step": int(h2d / args.e2e_steps),
                "d2h_bytes_per_step": int(d2h / args.e2e_steps),
-               "steps": args.e2e_steps,
+               "steps": args.e2e_steps, "batches_per_step": args.step_batches,
                "api": f"rec_query_async with pinned host inputs/outputs on {m_streams} streams "
-                      f"(H2D of indices/offsets/dense + D2H of CTRs every step), wall clock, max "
-                      f"over ranks"}
+                      f"(H2D of indices/offsets/dense + D2H of CTRs of every batch), wall clock, "
+                      f"max over ranks; a step = {args.step_batches} fused batches as in `value`"}
 
     sla = None
     if args.sla_queries > 0:
@@ -707,14 +710,15 @@ def run_ours(args):
 
 def run_sharded(args):
     """Model-parallel serving (BASELINE configs[2]: RMC2 "table-wise sharded across 8 x B200 with
-    all-to-all"): every step is ONE global batch of <= d items whose embedding tables are split
-    over the G ranks (table-wise: T/G tables per rank; row-wise: R/G rows of every table), the
-    exchange fused into the SLS as peer stores over NVLink (dist.cu).  value = queries of the
-    global batches / time (counted once, not per rank; scaling "strong")."""
+    all-to-all"): the embedding tables are split over the G ranks (table-wise: T/G tables per
+    rank), every rank runs the SAME global batches on m co-located stream slots, the all-to-all
+    of pooled vectors and the CTR all-gather are fused into the chain as peer stores over
+    NVLink with per-slot epoch flags (dist.cu), several global batches in flight per rank.
+    value = queries of the global batches / device time (counted once; scaling "strong");
+    sla = lambda* of rec_serve with the deterministic global dispatcher (reading R31)."""
     import torch
     import torch.distributed as dist
-    from paper_2203_07424_b200 import (RecModel, rec_split_fuse, nccl_unique_id, REC_SHARD_TABLE,
-                                       REC_SHARD_ROW)
+    from paper_2203_07424_b200 import (RecModel, nccl_unique_id, REC_SHARD_TABLE, REC_SHARD_ROW)
     world = int(os.environ["WORLD_SIZE"])
     rank = int(os.environ["RANK"])
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -722,97 +726,88 @@ def run_sharded(args):
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     cfg = W.SHORT[args.config]
     d = args.batch
+    m_streams = args.streams
     t = torch.zeros(128, dtype=torch.uint8, device="cuda")
     if rank == 0:
         t.copy_(torch.frombuffer(bytearray(nccl_unique_id()), dtype=torch.uint8))
     dist.broadcast(t, 0)
     shard = REC_SHARD_TABLE if args.shard == "table" else REC_SHARD_ROW
-    model = RecModel(cfg, seed=1, max_batch=d, streams=1, device=local, shard=shard, rank=rank,
+    model = RecModel(cfg, seed=1, max_batch=d, streams=m_streams, device=local, shard=shard, rank=rank,
                      world=world, nccl_id=bytes(t.cpu().numpy()))
-    trace = W.burst_trace(args.queries, seed=11)   # the same global query stream on every rank
-    segs, bstart = rec_split_fuse(trace, d)
-    nb = len(bstart) - 1
-    sizes = trace["size"].astype(np.int64)
-    last_chunk_start = ((sizes - 1) // d) * d
-    nin = min(nb, 32)
-    inputs = []
-    for b in range(nin):
-        sg = np.ascontiguousarray(segs[bstart[b]:bstart[b + 1]])
-        ind, off, dense = model.rec_gen_batch(sg)
-        inputs.append((torch.from_numpy(dense).cuda(), torch.from_numpy(ind).cuda(),
-                       torch.from_numpy(off).cuda(), int(sg[:, 2].sum()),
-                       int(np.sum(sg[:, 1] == last_chunk_start[sg[:, 0]]))))
-    ctr = torch.zeros(d * cfg.tasks, device="cuda")
-
-    def step(i):
-        h = inputs[i % nin]
-        model.rec_query(h[0], h[1], h[2], h[3], ctr)
-        return h
-
+    hbm_peak, bf16_peak, peak_kind = peaks()
     clk = ClockSampler(local).__enter__()
-    for i in range(args.warmup):
-        step(i)
-    dist.barrier()
-    torch.cuda.synchronize()
-    base_launch = model.rec_profile_read(4)[1]
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    t_region0 = time.perf_counter()
-    ev0.record()
-    items = queries = 0
-    for i in range(args.warmup, args.warmup + args.steps):
-        h = step(i)
-        items += h[3]
-        queries += h[4]
-    ev1.record()
-    torch.cuda.synchronize()
-    t_region1 = time.perf_counter()
-    launches = model.rec_profile_read(4)[1] - base_launch
-    dist.barrier()
-    ms = torch.tensor([ev0.elapsed_time(ev1)], dtype=torch.float64, device="cuda")
-    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-    ms_max = float(ms[0])
+    sat = saturation(model, cfg, d, m_streams, args.steps, args.warmup, args.step_batches,
+                     args.queries, rank, world, dist, sharded=True)
     clk.__exit__(None, None, None)
-    # e2e: the same queries with pinned HOST inputs (H2D every step) and the CTRs read back
-    host = [(x[0].cpu().pin_memory(), x[1].cpu().pin_memory(), x[2].cpu().pin_memory(), x[3], x[4])
-            for x in inputs]
-    out = torch.zeros(d * cfg.tasks).pin_memory()
-    e2e_steps = min(args.e2e_steps, 500)
+    ms_max, items, queries = sat["ms_max"], sat["items"], sat["queries"]
+    value = queries / (ms_max * 1e-3)
+    # e2e: the same global batches with pinned HOST inputs (rec_query_async on the slots: H2D of
+    # the global batch's inputs on every rank) and the gathered CTRs read back
+    batches, nb = sat["batches"], sat["nb"]
+    host = []
+    for b in range(min(nb, 32)):
+        ind, off, dense = model.rec_gen_batch(batches[b])
+        host.append((torch.from_numpy(dense).pin_memory(), torch.from_numpy(ind).pin_memory(),
+                     torch.from_numpy(off).pin_memory(), int(off[-1]), int(batches[b][:, 2].sum()),
+                     sat["done_b"][b]))
+    outs = [torch.empty(d).pin_memory() for _ in range(m_streams)]
+    nb_e2e = max(1, args.e2e_steps) * args.step_batches
+    for i in range(2 * m_streams):
+        h = host[i % len(host)]
+        model.rec_query_async(i % m_streams, h[0], h[1], h[2], h[3], h[4], outs[i % m_streams])
+    for k in range(m_streams):
+        model.rec_sync(k)
     dist.barrier()
     t0 = time.perf_counter()
-    q_e2e = h2d = 0
-    for i in range(e2e_steps):
-        h = host[i % nin]
-        model.rec_query(h[0], h[1], h[2], h[3], out)
-        q_e2e += h[4]
+    q_e2e = h2d = d2h = 0
+    for i in range(nb_e2e):
+        h = host[i % len(host)]
+        model.rec_query_async(i % m_streams, h[0], h[1], h[2], h[3], h[4], outs[i % m_streams])
+        q_e2e += h[5]
         h2d += (h[0].numel() + h[1].numel() + h[2].numel()) * 4
+        d2h += 4 * h[4]
+    for k in range(m_streams):
+        model.rec_sync(k)
     wall = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
     dist.all_reduce(wall, op=dist.ReduceOp.MAX)
-    hbm_peak, bf16_peak, peak_kind = peaks()
-    sls_bytes = sls_bytes_per_item(cfg, synth=False) * items
-    agg = sls_bytes / (ms_max * 1e-3) / 1e9 / world
+    sla = None
+    if args.sla_queries > 0:
+        n = int(max(30000, 1.5 * value))
+        lam, pr = sla_search(model, cfg, world, rank, dist, m_streams, d, 0.5 * value, n, cfg.sla_ms,
+                             replicated=True)
+        sla = {"sla_ms": cfg.sla_ms, "percentile": "p95 (nearest rank)", "lambda_star_qps": lam,
+               "policy": {"streams": m_streams, "max_batch": d,
+                          "fusion": "deterministic global dispatcher, tau = SLA/50 (R31)"},
+               "queries_per_probe": n, "probes": pr,
+               "saturation_ge_lambda_star": bool(value >= 0.98 * lam),
+               "mode": "rec_serve real clock on every rank (same trace, same batches), Poisson "
+                       "arrivals, lognormal sizes; p95 of rank 0's completions"}
+    per_gpu = sls_bytes_per_item(cfg, synth=True) * items / (ms_max * 1e-3) / 1e9 / world
     if rank == 0:
         line = {
-            "metric": BASELINE_METRIC, "value": queries / (ms_max * 1e-3), "unit": "QPS",
+            "metric": BASELINE_METRIC, "value": value, "unit": "QPS",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32 (SLS) + bf16 (MLP, fp32 accumulate)", "data": "synthetic",
             "config": {"workload": cfg.name, "max_batch_d": d, "tables": cfg.num_tables,
                        "rows": cfg.rows, "dim": cfg.dim, "pooling": cfg.pooling_lo,
-                       "parallelism": f"{args.shard}-wise sharding x{world} (exchange fused into "
-                                      f"the SLS, peer stores over NVLink)",
-                       "items_per_s": items / (ms_max * 1e-3),
+                       "parallelism": f"{args.shard}-wise sharding x{world}, {m_streams} async slots "
+                                      f"(all-to-all + CTR all-gather fused as peer stores over NVLink)",
+                       "items_per_s": items / (ms_max * 1e-3), "step_batches": args.step_batches,
                        "l2": "inputs larger than L2 (tables >> 126 MB, uniform random rows)",
-                       "value_is": "synchronous global batches (rec_query), one at a time"},
-            "roofline": {"bound": "hbm", "kernel": "k_sls (sharded)", "achieved": agg, "peak": hbm_peak,
-                         "unit": "GB/s", "frac": agg / hbm_peak, "traffic": None, "peak_kind": peak_kind,
-                         "measured": "per-GPU share of the SLS algorithmic bytes / the step time "
-                                     "(lower bound: the step also runs the exchange and dense part)"},
-            "gpu_launches": int(launches),
-            "clocks": clk.summary(t_region0, t_region1),
+                       "value_is": "saturation QPS of the global batch stream"},
+            "roofline": {"bound": "hbm", "kernel": "k_sls_synth (sharded, peer stores)", "achieved": per_gpu,
+                         "peak": hbm_peak, "unit": "GB/s", "frac": per_gpu / hbm_peak, "traffic": None,
+                         "peak_kind": peak_kind,
+                         "measured": "per-GPU share of the SLS algorithmic bytes / the timed region "
+                                     "(the chain also runs the exchange waits and the dense part)"},
+            "gpu_launches": int(sat["launches"]),
+            "clocks": clk.summary(sat["t0"], sat["t1"]),
             "e2e": {"value": q_e2e / float(wall[0]), "unit": "QPS",
-                    "h2d_bytes_per_step": int(h2d / max(e2e_steps, 1)),
-                    "d2h_bytes_per_step": int(4 * d * cfg.tasks), "steps": e2e_steps,
-                    "api": "rec_query with pinned host inputs (synchronous), max wall over ranks"},
+                    "h2d_bytes_per_step": int(h2d / max(args.e2e_steps, 1)),
+                    "d2h_bytes_per_step": int(d2h / max(args.e2e_steps, 1)), "steps": args.e2e_steps,
+                    "api": "rec_query_async with pinned host inputs on the async slots, max wall over ranks"},
+            "sla": sla,
             "cpu_baseline": None,
         }
         print(json.dumps(line), flush=True)
@@ -844,7 +839,7 @@ def main():
     ap.add_argument("--roofline-steps", type=int, default=1000)
     ap.add_argument("--sls-batches", type=int, default=1000, help="batches in the back-to-back SLS pass")
     ap.add_argument("--queries", type=int, default=40000)
-    ap.add_argument("--e2e-steps", type=int, default=3000)
+    ap.add_argument("--e2e-steps", type=int, default=6)
     ap.add_argument("--sla-queries", type=int, default=100000, help="Poisson queries per probe per GPU")
     ap.add_argument("--l2-persist-mb", type=int, default=0,
                     help="L2 persisting window over the hot row prefix of the tables (MB, 0 = off)")

@@ -25,9 +25,12 @@ def p95_nearest_rank(lat_ms: np.ndarray) -> float:
     return float(s[max((95 * s.size + 99) // 100, 1) - 1]) if s.size else float("nan")
 
 
-def sla_search(model, cfg, world, rank, dist, streams, d, lam0, n, sla_ms, max_iter=10, tau_ms=0.0):
+def sla_search(model, cfg, world, rank, dist, streams, d, lam0, n, sla_ms, max_iter=10, tau_ms=0.0,
+               replicated=False):
     """lambda*: largest offered Poisson rate (all GPUs) with p95 <= SLA and every GPU keeping up
-    (S5; geometric bracketing then bisection).  Real clock, device-synth inputs."""
+    (S5; geometric bracketing then bisection).  Real clock, device-synth inputs.
+    replicated=True (model-parallel sharding): every rank serves the WHOLE trace (the same
+    global batches) and the p95 is rank 0's; otherwise replicas serve q mod G."""
     import torch
     probes = []
     count = [0]
@@ -35,11 +38,12 @@ def sla_search(model, cfg, world, rank, dist, streams, d, lam0, n, sla_ms, max_i
     def probe(lam):
         count[0] += 1
         tr = W.poisson_trace(lam, n, seed=12)
-        mine = rank_share(tr, world, rank)
+        mine = tr if replicated else rank_share(tr, world, rank)
         rep = model.rec_serve(mine, sla_ms, streams, d, fusion_timeout_ms=tau_ms, warmup_frac=0.1)
         arr = mine["arrival_s"]
         w_end = tr["arrival_s"][0] + 0.1 * (tr["arrival_s"][-1] - tr["arrival_s"][0])
-        lat = gather_latencies(rep["latency_ms"][arr >= w_end], world, rank, dist)
+        mylat = rep["latency_ms"][arr >= w_end]
+        lat = mylat if replicated else gather_latencies(mylat, world, rank, dist)
         stable = torch.tensor([rep["stable"]], device="cuda")
         if world > 1:
             dist.all_reduce(stable, op=dist.ReduceOp.MIN)

@@ -131,7 +131,12 @@ rec_status rec_query_inspect(rec_model_t m, const float* dense, const int32_t* i
  * enqueued (OFFSETS: offsets[0] != 0, decreasing, or offsets[T*B] != nnz); device offsets
  * are validated on the device for the same conditions (the error is returned by
  * rec_sync(m, slot)) and every bag is clamped to [0, nnz), so inconsistent offsets never
- * read outside the indices.  Completion is collected by rec_sync(m, slot). */
+ * read outside the indices.  Completion is collected by rec_sync(m, slot).
+ * Table-wise sharded models (shard = REC_SHARD_TABLE, peer access between all GPUs): every
+ * rank enqueues the same GLOBAL batch (all T tables' indices, all B items' dense rows) on the
+ * same slot in the same order; the all-to-all of pooled vectors and the CTR all-gather run
+ * inside the slot's chain over peer memory, and ctr receives all B CTRs on
+ * every rank.  Row-wise or NCCL-exchange sharded models: REC_E_UNSUPPORTED (use rec_query). */
 rec_status rec_query_async(rec_model_t m, int32_t slot, const float* dense,
                            const int32_t* indices, const int32_t* offsets, int64_t nnz,
                            int32_t batch, float* ctr);
@@ -140,7 +145,8 @@ rec_status rec_query_async(rec_model_t m, int32_t slot, const float* dense,
  * the batch is the concatenation of item segments segs[nseg][3] = (qid, start, len)
  * (host memory); its inputs are generated on the device (G2-G4) and the forward runs on
  * stream slot `slot`.  ctr [sum len] fp32 DEVICE pointer, or NULL (the CTRs stay in the
- * stream's workspace).  Async. */
+ * stream's workspace).  Async.  Table-wise sharded models: as rec_query_async (the same
+ * global batch on the same slot on every rank; fixed pooling), REC_E_UNSUPPORTED otherwise. */
 rec_status rec_synth_query_async(rec_model_t m, int32_t slot, const int32_t* segs,
                                  int32_t nseg, float* ctr);
 
@@ -257,7 +263,12 @@ rec_status rec_split_fuse(const rec_trace_row* trace, int64_t n, int32_t max_bat
  * (batch, stream, qid, start, len), capacity log_cap rows; the number of rows written
  * is returned in report->batches' companion, see rec_serve_log_rows).
  * ctr_out [sum sizes][n_tasks] (optional, host): CTR(s) of every item, query-major in
- * trace order.  Errors: INVALID_ARG (bad policy, before any work), CUDA. */
+ * trace order.  Errors: INVALID_ARG (bad policy, before any work), CUDA.
+ * Table-wise sharded models (every rank calls rec_serve with the same trace): batches are cut
+ * by a deterministic global dispatcher from the trace alone (R31: a batch closes
+ * when full or tau = fusion_timeout_ms (default SLA / 50) after its first sub-query arrived;
+ * batch k on slot k mod m), so every rank runs the same batches; ranks align their clocks
+ * with an NCCL barrier; real clock and REC_INPUT_DEVICE_SYNTH only (else UNSUPPORTED). */
 rec_status rec_serve(rec_model_t m, const rec_trace_row* trace, int64_t n, double sla_ms,
                      const rec_serve_policy* pol, rec_serve_report* out,
                      double* latency_ms, int32_t* batch_log, int64_t log_cap,

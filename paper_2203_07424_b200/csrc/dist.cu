@@ -21,6 +21,7 @@
 
 #include <cstdio>
 #include <cstdlib>
+#include <algorithm>
 #include <cstring>
 #include <vector>
 
@@ -50,6 +51,262 @@ rec_status dist_init(rec_model_s* m, const void* nccl_id) {
   rec_status st = sharded_alloc(m);
   if (st != REC_OK) return st;
   return p2p_init(m);
+}
+
+// ---------------------------------------------------------------------------------------------
+// Table-wise sharding, asynchronous slot exchange.
+//
+// Every co-located stream slot s of every rank owns a region of one exchange arena (a single
+// cudaMalloc per rank, exported once with CUDA IPC):
+//   [X: cap x (T+1) x D fp32 | CTR gather: G x Bq fp32 | arrival flags [G] | CTR flags [G] |
+//    CTA counter | words: epoch, B]
+// The k-th batch submitted on slot s is the same global batch on every rank (a deterministic
+// global dispatch: every rank submits the same batch sequence round-robin over the slots) and
+// carries epoch k + 1 on that slot.  Its chain on rank r:
+//   SLS of the local tables for all B items, each pooled vector stored into X_s of the rank
+//     owning the item (blocks of Bq = ceil(B / G)) over NVLink; the last CTA raises
+//     flags_s[r] = epoch on every rank (st.release.sys)                  -- fused all-to-all C1
+//   || dense features + bottom MLP of the own block (branch stream)
+//   wait flags_s[0..G) >= epoch -> interaction + top MLP of the own block
+//   CTRs of the own block stored into CTR_s of every rank, CTR flags raised  -- all-gather C3
+//   wait CTR flags_s[0..G) >= epoch
+// Reuse of X_s by batch k + m is safe: rank r issues it only after its CTR-flag wait of batch
+// k, and every rank raised its CTR flag of k after its interaction had read X_s.  Slots are
+// independent, so m batches are in flight per rank with no host synchronisation.
+static size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
+
+struct SlotLayout {
+  size_t x, ctr, flags, ctrflags, counter, words, bytes;
+};
+static SlotLayout slot_layout(const rec_model_s* m) {
+  const int G = m->world;
+  const int64_t Bq = (m->max_batch + G - 1) / G;
+  SlotLayout L{};
+  L.x = 0;
+  L.ctr = al256(static_cast<size_t>(m->max_batch) * (m->T + 1) * m->D * sizeof(float));
+  L.flags = L.ctr + al256(sizeof(float) * G * Bq);
+  L.ctrflags = L.flags + al256(sizeof(unsigned) * G);
+  L.counter = L.ctrflags + al256(sizeof(unsigned) * G);
+  L.words = L.counter + 256;
+  L.bytes = L.words + 256;
+  return L;
+}
+
+static unsigned long long p2p_timeout_ns();
+
+rec_status p2p_slots_init(rec_model_s* m) {
+  const int G = m->world, M = m->nstreams;
+  const SlotLayout L = slot_layout(m);
+  m->sh_slot_bytes = L.bytes;
+  REC_CUDA(cudaMalloc(reinterpret_cast<void**>(&m->sh_arena), L.bytes * M));
+  REC_CUDA(cudaMemset(m->sh_arena, 0, L.bytes * M));
+  cudaIpcMemHandle_t mine;
+  REC_CUDA(cudaIpcGetMemHandle(&mine, m->sh_arena));
+  uint8_t* dh = nullptr;
+  REC_CUDA(cudaMalloc(reinterpret_cast<void**>(&dh), sizeof(mine) * (G + 1)));
+  REC_CUDA(cudaMemcpy(dh + sizeof(mine) * G, &mine, sizeof(mine), cudaMemcpyHostToDevice));
+  REC_NCCL(ncclAllGather(dh + sizeof(mine) * G, dh, sizeof(mine), ncclUint8,
+                         static_cast<ncclComm_t>(m->nccl_comm), m->ws[0].stream));
+  REC_CUDA(cudaStreamSynchronize(m->ws[0].stream));
+  std::vector<cudaIpcMemHandle_t> all(G);
+  REC_CUDA(cudaMemcpy(all.data(), dh, sizeof(mine) * G, cudaMemcpyDeviceToHost));
+  cudaFree(dh);
+  std::vector<uint8_t*> base(G);
+  for (int q = 0; q < G; ++q) {
+    if (q == m->rank) {
+      base[q] = m->sh_arena;
+      continue;
+    }
+    void* a = nullptr;
+    REC_CUDA(cudaIpcOpenMemHandle(&a, all[q], cudaIpcMemLazyEnablePeerAccess));
+    m->p2p_opened.push_back(a);
+    base[q] = static_cast<uint8_t*>(a);
+  }
+  // per slot: [peer X][peer flags][peer CTR][peer CTR flags], G pointers each
+  std::vector<void*> ptrs(static_cast<size_t>(M) * 4 * G);
+  for (int s = 0; s < M; ++s)
+    for (int q = 0; q < G; ++q) {
+      uint8_t* b = base[q] + L.bytes * s;
+      ptrs[(s * 4 + 0) * G + q] = b + L.x;
+      ptrs[(s * 4 + 1) * G + q] = b + L.flags;
+      ptrs[(s * 4 + 2) * G + q] = b + L.ctr;
+      ptrs[(s * 4 + 3) * G + q] = b + L.ctrflags;
+    }
+  REC_CUDA(cudaMalloc(reinterpret_cast<void**>(&m->d_sh_ptrs), sizeof(void*) * ptrs.size()));
+  REC_CUDA(cudaMemcpy(m->d_sh_ptrs, ptrs.data(), sizeof(void*) * ptrs.size(), cudaMemcpyHostToDevice));
+  for (int s = 0; s < M; ++s) {
+    Workspace& w = m->ws[s];
+    uint8_t* mb = m->sh_arena + L.bytes * s;
+    if (!w.x_external) cudaFree(w.X);
+    w.X = reinterpret_cast<float*>(mb + L.x);
+    w.x_external = true;
+    w.sh_ctr_gather = reinterpret_cast<float*>(mb + L.ctr);
+    void** P = m->d_sh_ptrs + static_cast<size_t>(s) * 4 * G;
+    unsigned* words = reinterpret_cast<unsigned*>(mb + L.words);
+    P2PArgs a{};
+    a.G = G;
+    a.rank = m->rank;
+    a.words = words;
+    a.err_flag = w.flag;
+    a.timeout_ns = p2p_timeout_ns();
+    w.sh_sls = a;
+    w.sh_sls.peer_X = reinterpret_cast<float* const*>(P);
+    w.sh_sls.peer_flags = reinterpret_cast<unsigned* const*>(P + G);
+    w.sh_sls.counter = reinterpret_cast<unsigned*>(mb + L.counter);
+    w.sh_wait = a;
+    w.sh_wait.my_flags = reinterpret_cast<unsigned*>(mb + L.flags);
+    w.sh_ctr = a;
+    w.sh_ctr.peer_X = reinterpret_cast<float* const*>(P + 2 * G);
+    w.sh_ctr.peer_flags = reinterpret_cast<unsigned* const*>(P + 3 * G);
+    w.sh_ctrwait = a;
+    w.sh_ctrwait.my_flags = reinterpret_cast<unsigned*>(mb + L.ctrflags);
+    if (!w.gsegs_local)
+      REC_CUDA(cudaMalloc(reinterpret_cast<void**>(&w.gsegs_local), sizeof(int4) * (w.cap + 1)));
+  }
+  // every rank's arena is zeroed before any peer may write into it
+  int* f = nullptr;
+  REC_CUDA(cudaMalloc(reinterpret_cast<void**>(&f), sizeof(int)));
+  REC_NCCL(ncclAllReduce(f, f, 1, ncclInt32, ncclSum, static_cast<ncclComm_t>(m->nccl_comm), m->ws[0].stream));
+  REC_CUDA(cudaStreamSynchronize(m->ws[0].stream));
+  cudaFree(f);
+  m->p2p_slots = true;
+  m->p2p = true;
+  if (getenv("REC_VERBOSE"))
+    fprintf(stderr, "[rec] rank %d: fused all-to-all over peer memory, %d async slots (%d ranks)\n",
+            m->rank, M, G);
+  return REC_OK;
+}
+
+// Dense part of this rank's item block + the exchange waits + the CTR all-gather, on w.stream
+// after the SLS (and on w.stream_b for the bottom branch, forked by the caller).  epoch == 0:
+// the kernels read epoch / B from the slot words (captured graphs); else by value.
+static rec_status shard_tail(rec_model_s* m, Workspace& w, int B, const int* dB, cudaEvent_t join,
+                             unsigned epoch = 0, int Bl = 0, int item0 = 0) {
+  cudaStream_t s = w.stream;
+  P2PArgs wa = w.sh_wait, ca = w.sh_ctr, cw = w.sh_ctrwait;
+  if (epoch) {
+    wa.words = ca.words = cw.words = nullptr;
+    wa.epoch = ca.epoch = cw.epoch = epoch;
+  }
+  launch_p2p_wait(wa, s);
+  REC_CUDA(cudaStreamWaitEvent(s, join, 0));
+  enqueue_interact_top(m, w, s, B, dB, w.ctr, w.logit, nullptr);
+  launch_p2p_ctr_scatter(w.ctr, Bl, item0, ca, s);
+  launch_p2p_wait(cw, s);
+  m->launches += 3;
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "sharded chain launch");
+  return REC_OK;
+}
+
+// Caller mode: global dense [B][F], indices / offsets of all T tables (table-major CSR) on the
+// device.  Direct launches, epoch and batch passed by value.
+rec_status shard_enqueue(rec_model_s* m, Workspace& w, const float* d_dense, const int* d_idx,
+                         const int* d_off, int B, int64_t idx_limit) {
+  const int G = m->world, r = m->rank, TL = m->T_loc, D = m->D, T = m->T;
+  const int Bq = (B + G - 1) / G, item0 = r * Bq;
+  const int Bl = std::max(0, std::min(Bq, B - item0));
+  cudaStream_t s = w.stream, sb = w.stream_b;
+  const unsigned epoch = ++w.sh_epoch;
+  REC_CUDA(cudaEventRecord(w.ev_fork, s));
+  REC_CUDA(cudaStreamWaitEvent(sb, w.ev_fork, 0));
+  if (Bl > 0) {
+    launch_dense_to_bf16(d_dense + static_cast<size_t>(item0) * m->F, Bl, m->F, m->Fpad, w.dense_bf, sb);
+    m->launches += 1;
+    enqueue_bottom(m, w, sb, Bl, nullptr, nullptr);
+  }
+  REC_CUDA(cudaEventRecord(w.ev_join, sb));
+  P2PArgs pa = w.sh_sls;
+  pa.words = nullptr;
+  pa.epoch = epoch;
+  pa.Bq = Bq;
+  pa.row_off = 0;
+  launch_sls_p2p(m->tables, m->d_tab_off, m->row_stride, m->d_rows, d_idx, d_off + m->t0 * B, B, TL, D,
+                 (T + 1) * D, 1 + m->t0, w.flag, pa, s, 0, 0x7fffffff,
+                 static_cast<int>(std::min<int64_t>(idx_limit, 0x7fffffff)));
+  m->launches += 1;
+  return shard_tail(m, w, Bl, nullptr, w.ev_join, epoch, Bl, item0);
+}
+
+// Synthetic mode, captured once per staging slot: SLS over device-synthesised indices of the
+// local tables (global batch sl.sb) || dense features of the own block (sl.sb_local) -> bottom;
+// then shard_tail.  Both first kernels take their batch by value (graph node updates).
+rec_status shard_capture(rec_model_s* m, Workspace& w) {
+  cudaStream_t s = w.stream, sb = w.stream_b;
+  for (auto& sl : w.slots) {
+    SynthSlot::Variant& V = sl.var[0];
+    sl.sa.tables = m->tables;
+    sl.sa.T = m->T_loc;
+    sl.sa.t0 = m->t0;
+    sl.sa.dB = nullptr;
+    sl.sa.pdl = 0;
+    sl.sa.dense_bf = nullptr;
+    sl.sa.hot_rows = 0;
+    sl.sa.tma = 0;
+    sl.sa.p2p = w.sh_sls;
+    const int64_t before = m->launches;
+    REC_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    cudaEventRecord(w.ev_fork, s);
+    cudaStreamWaitEvent(sb, w.ev_fork, 0);
+    launch_gen_dense_seg(*sl.sb_local, sl.ga, sb);  // writes dB = own block size
+    {
+      size_t n = 0;
+      const cudaGraphNode_t* d = last_node(sb, &n);
+      if (n == 1) V.dense_node = d[0];
+    }
+    enqueue_bottom(m, w, sb, w.cap, w.dB, nullptr);
+    cudaEventRecord(w.ev_join, sb);
+    launch_sls_synth(*sl.sb, sl.sa, s);
+    {
+      size_t n = 0;
+      const cudaGraphNode_t* d = last_node(s, &n);
+      if (n == 1) V.gen_node = d[0];
+    }
+    m->launches += 2;
+    rec_status st = shard_tail(m, w, w.cap, w.dB, w.ev_join);
+    cudaGraph_t g = nullptr;
+    cudaError_t ce = cudaStreamEndCapture(s, &g);
+    if (st != REC_OK) return st;
+    if (ce != cudaSuccess) return cuda_fail(ce, "cudaStreamEndCapture (sharded chain)");
+    if (!V.gen_node || !V.dense_node) {
+      set_error("sharded graph capture: first-kernel nodes not found");
+      return REC_E_CUDA;
+    }
+    V.graph = g;
+    ce = cudaGraphInstantiate(&V.exec, g, 0);
+    if (ce != cudaSuccess) return cuda_fail(ce, "cudaGraphInstantiate (sharded chain)");
+    w.graph_kernels = static_cast<int>(m->launches - before);
+    m->launches = before;
+    sl.var[1] = SynthSlot::Variant{};  // no profiling variant in sharded mode
+  }
+  return REC_OK;
+}
+
+// The own item block [r * Bq, r * Bq + Bl) of a global batch given as host segments
+// (qid, start, len), Bq = ceil(B / G): clipped segments into sl.sb_local (long lists through
+// `stage` (pinned) -> w.gsegs_local on w.stream).  Returns the block size Bl.
+int shard_fill_local(rec_model_s* m, Workspace& w, SynthSlot& sl, const int32_t* segs, int nseg,
+                     int B, int4* stage) {
+  const int G = m->world, Bq = (B + G - 1) / G, lo = m->rank * Bq;
+  const int hi = std::min(B, lo + Bq);
+  SegBatch& l = *sl.sb_local;
+  int n = 0, row = 0;
+  int4* dst = nseg > kParamSegs ? stage : l.seg;
+  for (int i = 0; i < nseg; ++i) {
+    const int len = segs[3 * i + 2];
+    const int a = std::max(lo, row), b = std::min(hi, row + len);
+    if (a < b) dst[n++] = make_int4(segs[3 * i], segs[3 * i + 1] + (a - row), b - a, a - lo);
+    row += len;
+  }
+  l.B = std::max(0, hi - lo);
+  l.nseg = n;
+  l.gsegs = w.gsegs_local;
+  if (n > kParamSegs) {
+    cudaMemcpyAsync(w.gsegs_local, stage, sizeof(int4) * n, cudaMemcpyHostToDevice, w.stream);
+  } else if (nseg > kParamSegs) {
+    for (int i = 0; i < n; ++i) l.seg[i] = stage[i];
+  }
+  return l.B;
 }
 
 // Fused table-wise exchange: map every peer's X buffer and arrival flags into
@@ -92,6 +349,7 @@ rec_status p2p_init(rec_model_s* m) {
     cudaFree(f);
   }
   if (!ok) return REC_OK;
+  if (m->shard == REC_SHARD_TABLE) return p2p_slots_init(m);
   REC_CUDA(cudaMalloc(reinterpret_cast<void**>(&m->p2p_flags), sizeof(unsigned) * G));
   REC_CUDA(cudaMemset(m->p2p_flags, 0, sizeof(unsigned) * G));
   REC_CUDA(cudaMalloc(reinterpret_cast<void**>(&m->p2p_counter), sizeof(unsigned)));
@@ -189,6 +447,11 @@ void dist_destroy(rec_model_s* m) {
   m->p2p_flags = nullptr;
   m->p2p_counter = nullptr;
   m->p2p = false;
+  cudaFree(m->sh_arena);
+  cudaFree(m->d_sh_ptrs);
+  m->sh_arena = nullptr;
+  m->d_sh_ptrs = nullptr;
+  m->p2p_slots = false;
   if (m->nccl_comm) {
     ncclCommDestroy(static_cast<ncclComm_t>(m->nccl_comm));
     m->nccl_comm = nullptr;
@@ -219,6 +482,31 @@ rec_status sharded_forward(rec_model_s* m, Workspace& w, const float* d_dense, c
   ncclComm_t comm = static_cast<ncclComm_t>(m->nccl_comm);
   const size_t xs = sizeof(float) * (T + 1) * D;
   // a3 on this GPU's shard, written in all-to-all / reduce-scatter order
+  if (m->p2p_slots) {  // table-wise, asynchronous slot exchange on slot 0, then wait
+    rec_status st = shard_enqueue(m, w, d_dense, d_idx, d_off, B, 0x7fffffff);
+    if (st != REC_OK) return st;
+    REC_CUDA(cudaMemcpyAsync(w.flag_host, w.flag, sizeof(int), cudaMemcpyDeviceToHost, s));
+    REC_CUDA(cudaStreamSynchronize(s));
+    const int f = *w.flag_host;
+    REC_CUDA(cudaMemsetAsync(w.flag, 0, sizeof(int), s));
+    if (f & 1) {
+      set_error("an index is outside [0, rows_t) (REC_E_INDEX_OOB)");
+      return REC_E_INDEX_OOB;
+    }
+    if (f & 2) {
+      set_error("offsets are not non-decreasing from 0 (REC_E_OFFSETS)");
+      return REC_E_OFFSETS;
+    }
+    if (f & 4) {
+      set_error("a peer rank missed the exchange deadline (REC_P2P_TIMEOUT_S); results invalid");
+      return REC_E_NCCL;
+    }
+    REC_CUDA(cudaMemcpyAsync(ctr, w.sh_ctr_gather, sizeof(float) * B, cudaMemcpyDefault, s));
+    if (logits && Bl > 0)
+      REC_CUDA(cudaMemcpyAsync(logits + item0, w.logit, sizeof(float) * Bl, cudaMemcpyDefault, s));
+    REC_CUDA(cudaStreamSynchronize(s));
+    return REC_OK;
+  }
   if (m->p2p) {
     // fused: pooled vectors land in the owners' X slots 1 + t0 .. over NVLink, then wait for
     // every rank's arrival flag of this epoch (the previous epoch's X readers all finished:

@@ -473,7 +473,8 @@ void launch_gemm_tc(const CUtensorMap* tmap_a, const CUtensorMap* tmap_w, const 
     if (g_gemm_2sm && tmap_w_half) launch_2sm<256>(tmap_a, tmap_w_half, a, s);  // CTA pairs
     else if (g_gemm_mt1) launch_bn<256, 1>(tmap_a, tmap_w, a, s);
     else launch_bn<256, 2>(tmap_a, tmap_w, a, s);  // enough 256-row tiles to fill the GPU: share W
-  } else if (g_gemm_narrow && tmap_w_half && ((a.M + 127) / 128) * ((a.N + 255) / 256) < g_gemm_narrow) {
+  } else if (g_gemm_narrow && tmap_w_half && a.mode != GEMM_OUT_CTR &&
+             ((a.M + 127) / 128) * ((a.N + 255) / 256) < g_gemm_narrow) {
     // serving batch, few 128x256 tiles: 128-wide N tiles double the CTAs working on the layer
     // (lower latency; every output element keeps the same K-ordered accumulation, so the
     // result bits do not depend on the tiling)
@@ -491,7 +492,8 @@ void launch_gemm_group(const GemmGroup& g, cudaStream_t s) {
   else if (a.N <= 128) launch_group_bn<128, 1>(g, s);
   else if (((a.M + 255) / 256) * ((a.N + 255) / 256) * g.n >= 148 && a.K >= 512)
     launch_group_bn<256, 2>(g, s);
-  else if (g_gemm_narrow && ((a.M + 127) / 128) * ((a.N + 255) / 256) * g.n < g_gemm_narrow)
+  else if (g_gemm_narrow && a.mode != GEMM_OUT_CTR &&  // the CTR epilogue needs the whole row
+           ((a.M + 127) / 128) * ((a.N + 255) / 256) * g.n < g_gemm_narrow)
     launch_group_bn<128, 1>(g, s);
   else launch_group_bn<256, 1>(g, s);
 }

@@ -424,16 +424,7 @@ bool chain_configure(ChainArgs& a) {
   }
   // Over budget: per-layer GEMMs instead (measured on RMC3: a 192-KB bottom chain with the
   // 2560-wide layer runs 8 CTAs for 80 us at B = 1024 and costs 13 % co-located throughput
-  // against the per-layer kernels).  REC_CHAIN_STRICT=0 keeps any chain that fits 227 KB.
-  const char* strict = getenv("REC_CHAIN_STRICT");
-  if (!strict || atoi(strict)) return false;
-  for (int nch : {256, 128}) {
-    for (int s = smax; s >= 2; --s) {
-      a.stages = s;
-      a.nchunk = nch;
-      if (chain_smem_bytes(a) <= 227 * 1024) return true;
-    }
-  }
+  // against the per-layer kernels).
   return false;
 }
 

@@ -222,6 +222,7 @@ __global__ void __launch_bounds__(THREADS, REC_SLS_MINB) k_sls(const float* __re
     if (prev == gridDim.x - 1) {  // last CTA: every CTA's stores are fenced
       __threadfence_system();
       for (int q = 0; q < p2p.G; ++q) st_release_sys(p2p.peer_flags[q] + p2p.rank, p2p.epoch);
+      *p2p.counter = 0;  // ready for the next launch using this counter (stream-ordered)
     }
   }
 }
@@ -232,9 +233,10 @@ __global__ void __launch_bounds__(THREADS, REC_SLS_MINB) k_sls(const float* __re
 __global__ void k_p2p_wait(const P2PArgs p2p) {
   const int q = threadIdx.x;
   if (q >= p2p.G) return;
+  const unsigned epoch = p2p.words ? p2p.words[0] : p2p.epoch;
   unsigned long long t0;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-  while (ld_acquire_sys(p2p.my_flags + q) < p2p.epoch) {
+  while (ld_acquire_sys(p2p.my_flags + q) < epoch) {
     __nanosleep(200);
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -246,12 +248,20 @@ __global__ void k_p2p_wait(const P2PArgs p2p) {
 }
 
 __global__ void k_p2p_ctr_scatter(const float* __restrict__ ctr, int Bl, int item0, const P2PArgs p2p) {
+  unsigned epoch = p2p.epoch;
+  if (p2p.words) {  // batch of the slot (captured graphs): this rank's block of ceil(B / G)
+    epoch = p2p.words[0];
+    const int B = static_cast<int>(p2p.words[1]);
+    const int Bq = (B + p2p.G - 1) / p2p.G;
+    item0 = p2p.rank * Bq;
+    Bl = max(0, min(Bq, B - item0));
+  }
   for (int q = 0; q < p2p.G; ++q)
     for (int i = threadIdx.x; i < Bl; i += blockDim.x) p2p.peer_X[q][item0 + i] = ctr[i];
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence_system();
-    for (int q = 0; q < p2p.G; ++q) st_release_sys(p2p.peer_flags[q] + p2p.rank, p2p.epoch);
+    for (int q = 0; q < p2p.G; ++q) st_release_sys(p2p.peer_flags[q] + p2p.rank, epoch);
   }
 }
 
@@ -267,7 +277,7 @@ void launch_p2p_wait(const P2PArgs& p2p, cudaStream_t s) {
 // accumulate structure, but lane `sub` computes the index of slot base + sub with Philox
 // (G2) instead of loading it, so the kernel has no predecessor in the chain and
 // no dependent index load in front of its first row loads.
-template <int LANES, int THREADS, int RIF, bool HOT = false>
+template <int LANES, int THREADS, int RIF, bool HOT = false, bool P2P = false>
 __global__ void __launch_bounds__(THREADS, REC_SLS_MINB) k_sls_synth(const __grid_constant__ SegBatch sb,
                                                                         const SlsSynthArgs a) {
   using S = SlsShape<LANES, RIF>;
@@ -279,21 +289,29 @@ __global__ void __launch_bounds__(THREADS, REC_SLS_MINB) k_sls_synth(const __gri
   SLS_GDC_TRIGGER();
   const int B = sb.B;
   const int nbags = a.T * B;  // >= T: a synthetic batch is never empty (block 0 writes dB)
-  const int g = blockIdx.x * GROUPS + threadIdx.x / LANES;
-  if (g >= nbags) return;
+  int g = blockIdx.x * GROUPS + threadIdx.x / LANES;
+  if (P2P) {
+    // sharded: CTAs of the batch all reach the CTA barrier of the flag protocol (groups past
+    // the last bag idle on bag 0 and store nothing); CTAs past the batch leave uncounted
+    if (static_cast<int>(blockIdx.x) * GROUPS >= nbags) return;
+  } else if (g >= nbags) {
+    return;
+  }
+  const bool live = g < nbags;
+  if (!live) g = 0;
   const int sub = threadIdx.x % LANES;
   const int t = g / B, b = g - t * B;
   const int2 qi = row_item(sb, b);
   const uint64_t R = static_cast<uint64_t>(__ldg(&a.rows[t]));
   const int64_t toff = __ldg(&a.tab_off[t]);
-  const uint32_t c2 = (static_cast<uint32_t>(t) << 8) | DOM_INDEX;
+  const uint32_t c2 = (static_cast<uint32_t>(a.t0 + t) << 8) | DOM_INDEX;
   const bool active = (sub * 4) < a.D;
   const int col = active ? sub * 4 : 0;
   const float4* __restrict__ tab = reinterpret_cast<const float4*>(a.tables + toff + col);
   const uint32_t stride_bytes = static_cast<uint32_t>(a.row_stride * 4);
   const unsigned gmask = (LANES == 32) ? 0xffffffffu
                                        : (((1u << LANES) - 1u) << ((threadIdx.x & 31) & ~(LANES - 1)));
-  const int L = a.L;
+  const int L = live ? a.L : 0;  // idle groups (sharded launches) read nothing
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
   uint64_t pol_hot = 0, pol_cold = 0;
   if (HOT) {
@@ -340,6 +358,33 @@ __global__ void __launch_bounds__(THREADS, REC_SLS_MINB) k_sls_synth(const __gri
       }
       if (base == 0 && kk == 0) SLS_STAMP(2);
     }
+  }
+  if constexpr (P2P) {
+    // fused all-to-all (table-wise sharding): item b lives on rank b / Bq as row b % Bq,
+    // its pooled vector of local table t goes to X slot 1 + t0 + t over NVLink
+    const P2PArgs& p2p = a.p2p;
+    if (active && live) {
+      const int Bq = (B + p2p.G - 1) / p2p.G;
+      const int p = b / Bq, bi = b - p * Bq;
+      *reinterpret_cast<float4*>(p2p.peer_X[p] + static_cast<int64_t>(bi) * a.x_stride +
+                                 static_cast<int64_t>(1 + a.t0 + t) * a.D + col) = acc;
+    }
+    __syncthreads();  // the CTA's peer stores happen-before thread 0's system-scope fence
+    if (threadIdx.x == 0) {
+      if (blockIdx.x == 0 && p2p.words) {  // epoch + batch of this slot for the later kernels
+        p2p.words[0] = p2p.epoch;
+        p2p.words[1] = static_cast<unsigned>(B);
+      }
+      __threadfence_system();
+      const unsigned need = static_cast<unsigned>((nbags + GROUPS - 1) / GROUPS);
+      const unsigned prev = atomicAdd(p2p.counter, 1u);
+      if (prev == need - 1) {  // last CTA: every CTA's stores are fenced
+        __threadfence_system();
+        for (int q = 0; q < p2p.G; ++q) st_release_sys(p2p.peer_flags[q] + p2p.rank, p2p.epoch);
+        *p2p.counter = 0;      // ready for the slot's next launch (stream-ordered)
+      }
+    }
+    return;
   }
   SLS_GDC_WAIT();  // predecessor grid done: X / dB may be overwritten
   if (blockIdx.x == 0 && threadIdx.x == 0) *a.dB = B;
@@ -506,6 +551,11 @@ void* sls_synth_kernel(const SlsSynthArgs& a, dim3* grid, dim3* block, size_t* s
   *grid = dim3((nb + THREADS / L - 1) / (THREADS / L));
   *block = dim3(THREADS);
   if (smem) *smem = 0;
+  if (a.p2p.peer_X) {
+    if (L == 8) return reinterpret_cast<void*>(k_sls_synth<8, THREADS, REC_SLS_RIF, false, true>);
+    if (L == 16) return reinterpret_cast<void*>(k_sls_synth<16, THREADS, REC_SLS_RIF, false, true>);
+    return reinterpret_cast<void*>(k_sls_synth<32, THREADS, REC_SLS_RIF, false, true>);
+  }
   if (a.hot_rows > 0) {
     if (L == 8) return reinterpret_cast<void*>(k_sls_synth<8, THREADS, REC_SLS_RIF, true>);
     if (L == 16) return reinterpret_cast<void*>(k_sls_synth<16, THREADS, REC_SLS_RIF, true>);
@@ -583,7 +633,7 @@ void launch_p2p_reduce(const float* stage, float* X, int Bl, int Bq, int T, int 
 void launch_sls_p2p(const float* tables, const int64_t* tab_off, int64_t row_stride,
                     const int64_t* rows, const int* indices, const int* offsets, int B, int T, int D,
                     int x_stride_items, int x_slot0, int* flag, const P2PArgs& p2p, cudaStream_t s,
-                    int row_lo, int row_hi) {
+                    int row_lo, int row_hi, int idx_limit) {
   constexpr int THREADS = 128;
   const int nbags = T * B;
   if (nbags == 0) return;
@@ -591,13 +641,13 @@ void launch_sls_p2p(const float* tables, const int64_t* tab_off, int64_t row_str
   const int grid = (nbags + THREADS / L - 1) / (THREADS / L);
   if (L == 8)
     k_sls<8, THREADS, true><<<grid, THREADS, 0, s>>>(tables, tab_off, row_stride, rows, indices, offsets, B,
-        nullptr, T, D, nullptr, x_stride_items, x_slot0, flag, row_lo, row_hi, 0x7fffffff, p2p);
+        nullptr, T, D, nullptr, x_stride_items, x_slot0, flag, row_lo, row_hi, idx_limit, p2p);
   else if (L == 16)
     k_sls<16, THREADS, true><<<grid, THREADS, 0, s>>>(tables, tab_off, row_stride, rows, indices, offsets, B,
-        nullptr, T, D, nullptr, x_stride_items, x_slot0, flag, row_lo, row_hi, 0x7fffffff, p2p);
+        nullptr, T, D, nullptr, x_stride_items, x_slot0, flag, row_lo, row_hi, idx_limit, p2p);
   else
     k_sls<32, THREADS, true><<<grid, THREADS, 0, s>>>(tables, tab_off, row_stride, rows, indices, offsets, B,
-        nullptr, T, D, nullptr, x_stride_items, x_slot0, flag, row_lo, row_hi, 0x7fffffff, p2p);
+        nullptr, T, D, nullptr, x_stride_items, x_slot0, flag, row_lo, row_hi, idx_limit, p2p);
 }
 
 void set_max_smem_carveout(int c) {

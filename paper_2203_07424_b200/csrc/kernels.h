@@ -73,11 +73,15 @@ struct P2PArgs {
   unsigned epoch;               // query sequence number (flags reach it when the data landed)
   int* err_flag;                // k_p2p_wait: bit 2 (value 4) set when a peer missed the timeout
   unsigned long long timeout_ns;  // k_p2p_wait bound (REC_P2P_TIMEOUT_S, default 60 s)
+  // Async slot exchange (captured graphs): [0] epoch, [1] global batch B of the batch in
+  // flight on this slot, written by the slot's SLS kernel; when non-null the later kernels of
+  // the chain (wait, CTR scatter) read epoch / B from here instead of the fields above.
+  unsigned* words;
 };
 void launch_sls_p2p(const float* tables, const int64_t* tab_off, int64_t row_stride,
                     const int64_t* rows, const int* indices, const int* offsets, int B, int T, int D,
                     int x_stride_items, int x_slot0, int* flag, const P2PArgs& p2p, cudaStream_t s,
-                    int row_lo = 0, int row_hi = 0x7fffffff);
+                    int row_lo = 0, int row_hi = 0x7fffffff, int idx_limit = 0x7fffffff);
 // Row-wise: X[i][1 + t] = sum over source ranks q (in order) of stage[q][i][t] for i < Bl.
 void launch_p2p_reduce(const float* stage, float* X, int Bl, int Bq, int T, int D, int G,
                        cudaStream_t s);
@@ -122,6 +126,11 @@ struct SlsSynthArgs {
   // (device copy, 64-B aligned), arena row of (t, r) = tab_off[t] / D + r * row_stride / D.
   const CUtensorMap* tmap_rows;
   int pdl;        // launch with programmatic stream serialization (kernel waits before writes)
+  // table-wise sharded serving (dist.cu): local tables are global tables t0 .. t0 + T - 1
+  // (Philox counters use the global id); p2p.peer_X != nullptr stores every pooled vector into
+  // the X of the rank owning the item (blocks of ceil(B / G)) and raises this rank's flags
+  int t0;
+  P2PArgs p2p;
   int tma;     // 1: k_sls_synth_tma
   int nsm;     // SMs (persistent grid)
   int nst;     // ring chunks per warp

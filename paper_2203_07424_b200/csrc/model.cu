@@ -648,8 +648,14 @@ rec_status synth_submit(rec_model_s* m, Workspace& w, const int32_t* segs, int n
     dst[i] = make_int4(segs[3 * i], segs[3 * i + 1], segs[3 * i + 2], row);
     row += segs[3 * i + 2];
   }
-  if (nseg > kParamSegs) {
+  if (nseg > kParamSegs)
     REC_CUDA(cudaMemcpyAsync(w.gsegs, w.pin, sizeof(int4) * nseg, cudaMemcpyHostToDevice, w.stream));
+  if (m->p2p_slots) {  // table-wise sharded: this rank's item block + the slot's epoch
+    shard_fill_local(m, w, sl, segs, nseg, static_cast<int>(B),
+                     reinterpret_cast<int4*>(w.pin) + (w.cap + 1));
+    sl.sa.p2p.epoch = ++w.sh_epoch;
+    if (nseg > kParamSegs) REC_CUDA(cudaEventRecord(w.pin_free, w.stream));
+  } else if (nseg > kParamSegs) {
     REC_CUDA(cudaEventRecord(w.pin_free, w.stream));
   }
   SynthSlot::Variant& V = sl.var[m->prof ? 1 : 0];
@@ -670,7 +676,7 @@ rec_status synth_submit(rec_model_s* m, Workspace& w, const int32_t* segs, int n
     else REC_CUDA(cudaGraphExecKernelNodeSetParams(V.exec, V.gen_node, &kp));
     if (fused && V.dense_node) {
       cudaKernelNodeParams kd{};
-      void* args_d[2] = {sl.sb, &sl.ga};
+      void* args_d[2] = {m->p2p_slots ? sl.sb_local : sl.sb, &sl.ga};
       kd.func = gen_dense_seg_kernel(sl.ga, &grid, &block);
       kd.gridDim = grid;
       kd.blockDim = block;
@@ -708,6 +714,10 @@ static rec_status read_flag(Workspace& w) {
   if (f & 2) {
     set_error("offsets are not non-decreasing from 0 (REC_E_OFFSETS)");
     return REC_E_OFFSETS;
+  }
+  if (f & 4) {
+    set_error("a peer rank missed the sharded exchange deadline (REC_P2P_TIMEOUT_S)");
+    return REC_E_NCCL;
   }
   return REC_OK;
 }
@@ -877,7 +887,8 @@ static void free_model(rec_model_s* m) {
     cudaFree(w.rowi);
     cudaFree(w.dense_f32);
     cudaFree(w.dense_bf);
-    cudaFree(w.X);
+    if (!w.x_external) cudaFree(w.X);  // (sharded: inside the exchange arena, dist_destroy)
+    cudaFree(w.gsegs_local);
     cudaFree(w.A_top);
     cudaFree(w.h[0]);
     cudaFree(w.h[1]);
@@ -893,6 +904,7 @@ static void free_model(rec_model_s* m) {
         if (V.graph) cudaGraphDestroy(V.graph);
       }
       delete sl.sb;
+      delete sl.sb_local;
       if (sl.free) cudaEventDestroy(sl.free);
       for (auto e : sl.ev)
         if (e) cudaEventDestroy(e);
@@ -1373,7 +1385,9 @@ rec_status rec_model_create(const rec_model_desc* d, rec_model_t* out) {
       ca.act_kblocks = act;
       int tc = 32;
       while (tc < maxn) tc *= 2;
-      if (tc > 512) return false;
+      // layers wider than 256 (RMC2/RMC3's 512-wide hidden layers) run as per-layer GEMMs: such
+      // chains never meet the co-location shared-memory budget, and they are not validated
+      if (tc > 256) return false;
       ca.tmem_cols = tc;
       ca.mode_last = mode;
       ca.wl_n = mode == GEMM_OUT_CTR ? Ls[nl - 1].N : 0;
@@ -1451,7 +1465,7 @@ rec_status rec_model_create(const rec_model_desc* d, rec_model_t* out) {
     CHECK_CUDA_CREATE(cudaMemset(w.h[1], 0, sizeof(__nv_bfloat16) * int64_t(cap) * m->hmax));
     CHECK_CUDA_CREATE(cudaMallocHost(reinterpret_cast<void**>(&w.flag_host), sizeof(int)));
     w.pin_bytes = sizeof(int) * (int64_t(T) * cap + 1) + sizeof(int) * idx_cap +
-                  sizeof(float) * int64_t(cap) * m->F + sizeof(int4) * cap + 4096;
+                  sizeof(float) * int64_t(cap) * m->F + 2 * sizeof(int4) * (cap + 1) + 4096;
     if (cudaMallocHost(reinterpret_cast<void**>(&w.pin), w.pin_bytes) != cudaSuccess) {
       set_error("cudaMallocHost of %zu pinned staging bytes failed", w.pin_bytes);
       free_model(m);
@@ -1524,6 +1538,8 @@ rec_status rec_model_create(const rec_model_desc* d, rec_model_t* out) {
     for (auto& sl : w.slots) {
       sl.sb = new SegBatch();
       memset(sl.sb, 0, sizeof(SegBatch));
+      sl.sb_local = new SegBatch();
+      memset(sl.sb_local, 0, sizeof(SegBatch));
       sl.sb->B = 1;
       sl.sb->nseg = 1;
       sl.sb->seg[0] = make_int4(0, 0, 1, 0);
@@ -1575,6 +1591,16 @@ rec_status rec_model_create(const rec_model_desc* d, rec_model_t* out) {
       free_model(m);
       return st;
     }
+    // table-wise over peer memory: one captured graph per staging slot of the asynchronous
+    // sharded chain (device-synthesised inputs need fixed pooling, as for replicas)
+    if (m->p2p_slots && m->lo == m->hi && m->arch == REC_ARCH_DLRM)
+      for (auto& w : m->ws) {
+        st = shard_capture(m, w);
+        if (st != REC_OK) {
+          free_model(m);
+          return st;
+        }
+      }
   }
   *out = m;
   return REC_OK;
@@ -1608,8 +1634,9 @@ rec_status rec_query_async(rec_model_t m, int32_t slot, const float* dense, cons
     set_error("null argument");
     return REC_E_INVALID_ARG;
   }
-  if (m->world > 1 && m->shard != REC_SHARD_REPLICA) {
-    set_error("sharded models are synchronous collectives: use rec_query");
+  const bool sharded = m->world > 1 && m->shard != REC_SHARD_REPLICA;
+  if (sharded && !m->p2p_slots) {
+    set_error("row-wise / NCCL-exchange sharded models are synchronous collectives: use rec_query");
     return REC_E_UNSUPPORTED;
   }
   if (slot < 0 || slot >= m->nstreams) {
@@ -1675,6 +1702,13 @@ rec_status rec_query_async(rec_model_t m, int32_t slot, const float* dense, cons
   // device offsets: offsets[T*B] == nnz is checked on the device (flag -> REC_E_OFFSETS at
   // rec_sync) and the SLS clamps every bag to [0, nnz), so no read leaves the indices
   if (off_dev) launch_check_offsets(d_off, nb, w.flag, s, nnz);
+  if (sharded) {  // table-wise over peer memory: every rank enqueues the same global batch
+    m->launches += off_dev ? 1 : 0;
+    rec_status st = shard_enqueue(m, w, d_dense, d_idx, d_off, batch, nnz);
+    if (st != REC_OK) return st;
+    REC_CUDA(cudaMemcpyAsync(ctr, w.sh_ctr_gather, sizeof(float) * batch, cudaMemcpyDefault, s));
+    return REC_OK;
+  }
   launch_dense_to_bf16(d_dense, batch, m->F, m->Fpad, w.dense_bf, s);
   m->launches += off_dev ? 2 : 1;
   rec_status st = forward_enqueue(m, w, d_idx, d_off, batch, nullptr, ctr_dev ? ctr : w.ctr, w.logit,
@@ -1691,8 +1725,10 @@ rec_status rec_synth_query_async(rec_model_t m, int32_t slot, const int32_t* seg
     set_error("null argument");
     return REC_E_INVALID_ARG;
   }
-  if (m->world > 1 && m->shard != REC_SHARD_REPLICA) {
-    set_error("sharded models serve through rec_query (replicas serve synthetic batches)");
+  const bool sharded = m->world > 1 && m->shard != REC_SHARD_REPLICA;
+  if (sharded && !(m->p2p_slots && m->ws[0].slots[0].var[0].exec)) {
+    set_error("synthetic batches on a sharded model need table-wise sharding over peer memory "
+              "and fixed pooling");
     return REC_E_UNSUPPORTED;
   }
   if (slot < 0 || slot >= m->nstreams) {
@@ -1704,8 +1740,9 @@ rec_status rec_synth_query_async(rec_model_t m, int32_t slot, const int32_t* seg
   int B = 0;
   rec_status st = synth_submit(m, w, segs, nseg, &B, nullptr);
   if (st != REC_OK) return st;
-  if (ctr && ctr != w.ctr)
-    REC_CUDA(cudaMemcpyAsync(ctr, w.ctr, sizeof(float) * B * m->tasks, cudaMemcpyDeviceToDevice, w.stream));
+  const float* src = sharded ? w.sh_ctr_gather : w.ctr;  // sharded: every rank's CTRs, gathered
+  if (ctr && ctr != src)
+    REC_CUDA(cudaMemcpyAsync(ctr, src, sizeof(float) * B * m->tasks, cudaMemcpyDefault, w.stream));
   return REC_OK;
 }
 
@@ -1715,8 +1752,9 @@ rec_status rec_synth_query_batches(rec_model_t m, const int32_t* segs, const int
     set_error("null argument or negative count");
     return REC_E_INVALID_ARG;
   }
-  if (m->world > 1 && m->shard != REC_SHARD_REPLICA) {
-    set_error("sharded models serve through rec_query");
+  if (m->world > 1 && m->shard != REC_SHARD_REPLICA && !(m->p2p_slots && m->ws[0].slots[0].var[0].exec)) {
+    set_error("synthetic batches on a sharded model need table-wise sharding over peer memory "
+              "and fixed pooling");
     return REC_E_UNSUPPORTED;
   }
   REC_CUDA(cudaSetDevice(m->device));

@@ -37,6 +37,7 @@ struct Layer {
 // stream let the host run ahead of the GPU while profiling events stay per launch.
 struct SynthSlot {
   SegBatch* sb = nullptr;            // host copy of the first kernel's by-value parameter
+  SegBatch* sb_local = nullptr;      // sharded: this rank's item block of the batch (dense part)
   GenArgs ga{};
   SlsSynthArgs sa{};
   cudaEvent_t free = nullptr;        // the last launch that used this slot completed
@@ -93,6 +94,15 @@ struct Workspace {
   int graph_kernels = 0;                               // kernels per graph launch
   double host_ns[4] = {0, 0, 0, 0};  // host time in synth_submit (param update, graph launch,
                                      // slot wait, total) — per stream: dispatch threads
+  // table-wise sharded slot exchange (dist.cu p2p_slots_init): this workspace's X lives in the
+  // model's IPC-exported exchange arena (x_external: not freed separately); the P2P argument
+  // sets of its chain (SLS stores + flags, flag wait, CTR all-gather, CTR-flag wait), the
+  // gathered CTRs of the whole batch, and the slot's epoch counter
+  bool x_external = false;
+  P2PArgs sh_sls{}, sh_wait{}, sh_ctr{}, sh_ctrwait{};
+  float* sh_ctr_gather = nullptr;    // [G * Bq] CTRs of every rank's block (items 0..B-1)
+  unsigned sh_epoch = 0;
+  int4* gsegs_local = nullptr;       // device segments of this rank's item block (> kParamSegs)
 };
 
 // S-D pipeline lane: one captured graph over N workspaces that
@@ -200,6 +210,12 @@ struct rec_model_s {
   float* p2p_stage = nullptr;          // row-wise: partial sums of every source rank [G][Bq][T][D]
   unsigned p2p_epoch = 0;
   std::vector<void*> p2p_opened;       // IPC mappings to close
+  // table-wise sharding, asynchronous slot exchange (dist.cu): one IPC-exported arena of
+  // `nstreams` slots [X | CTR gather | arrival flags | CTR flags | CTA counter | words]
+  bool p2p_slots = false;
+  uint8_t* sh_arena = nullptr;
+  size_t sh_slot_bytes = 0;
+  void** d_sh_ptrs = nullptr;          // per slot: peer X / flags / CTR / CTR flags [4][G]
 };
 
 namespace rec {
@@ -239,6 +255,17 @@ void enqueue_interact_top(rec_model_s* m, Workspace& w, cudaStream_t st, int B, 
 rec_status sharded_forward(rec_model_s* m, Workspace& w, const float* d_dense, const int* d_idx,
                            const int* d_off, int B, float* ctr, float* logits);
 rec_status sharded_alloc(rec_model_s* m);
+// Table-wise sharding over peer memory, asynchronous (dist.cu): the chain of one global batch
+// on workspace w.  Caller mode (segs == nullptr): inputs already on the device (global dense /
+// indices / offsets); synthetic mode: the slot's SegBatch descriptors (captured graph).
+rec_status shard_enqueue(rec_model_s* m, Workspace& w, const float* d_dense, const int* d_idx,
+                         const int* d_off, int B, int64_t idx_limit);
+rec_status shard_capture(rec_model_s* m, Workspace& w);
+// Host side of a synthetic sharded batch: sl.sb_local = this rank's item block of the global
+// batch given as host segments; returns the block size.
+int shard_fill_local(rec_model_s* m, Workspace& w, SynthSlot& sl, const int32_t* segs, int nseg,
+                     int B, int4* stage);
+rec_status p2p_slots_init(rec_model_s* m);
 cudaEvent_t prof_begin(rec_model_s* m, cudaStream_t s);
 rec_status dist_init(rec_model_s* m, const void* nccl_id);   // dist.cu
 rec_status p2p_init(rec_model_s* m);                          // dist.cu (fused table-wise exchange)

@@ -27,6 +27,8 @@
 #include <queue>
 #include <vector>
 
+#include <nccl.h>
+
 #include "model.h"
 
 static inline void cpu_relax() {
@@ -202,6 +204,244 @@ static rec_status host_input_enqueue(rec_model_s* m, Workspace& w, const HostInp
   return REC_OK;
 }
 
+// S5 report: per-query latency = completion of the last sub-query - arrival (R16), nearest-
+// rank percentiles over queries arriving after the warm-up window, offered / achieved rate.
+static void fill_report(const rec_trace_row* trace, int64_t n, double sla_ms, double warmup_frac,
+                        const std::vector<double>& release, const std::vector<double>& disp_t,
+                        const std::vector<double>& done_t, int64_t completed, int64_t nbatches,
+                        double items_tot, double* latency_ms, rec_serve_report* out) {
+  const double t_first = trace[0].arrival_s, t_last = trace[n - 1].arrival_s;
+  const double w_end = t_first + warmup_frac * (t_last - t_first);
+  std::vector<double> lat;
+  double sum_lat = 0, sum_q = 0, sum_svc = 0, t_max = t_first;
+  for (int64_t p = 0; p < n; ++p) {
+    const double l = done_t[p] - release[p];
+    if (latency_ms) latency_ms[p] = l * 1e3;
+    t_max = std::max(t_max, done_t[p]);
+    if (release[p] >= w_end) {
+      lat.push_back(l * 1e3);
+      sum_lat += l * 1e3;
+      sum_q += (disp_t[p] - release[p]) * 1e3;
+      sum_svc += (done_t[p] - disp_t[p]) * 1e3;
+    }
+  }
+  std::sort(lat.begin(), lat.end());
+  const int64_t nm = static_cast<int64_t>(lat.size());
+  memset(out, 0, sizeof(*out));
+  out->completed = completed;
+  out->dropped = n - completed;
+  out->batches = nbatches;
+  out->mean_batch = nbatches ? items_tot / nbatches : 0;
+  if (nm > 0) {
+    out->p50_ms = lat[pct_rank(50, nm) - 1];
+    out->p95_ms = lat[pct_rank(95, nm) - 1];
+    out->p99_ms = lat[pct_rank(99, nm) - 1];
+    out->mean_ms = sum_lat / nm;
+    out->breakdown_ms[0] = sum_q / nm;   // queueing (arrival -> dispatch of last sub-query)
+    out->breakdown_ms[2] = sum_svc / nm; // input + device + completion observation
+  }
+  out->offered_qps = t_last > t_first ? n / (t_last - t_first) : INFINITY;
+  out->achieved_qps = t_max > t_first ? n / (t_max - t_first) : 0;
+  out->stable = (completed == n) && out->achieved_qps >= 0.98 * out->offered_qps;
+  out->sla_met = out->stable && out->p95_ms <= sla_ms;
+}
+
+// ------------------------------------------------------------------------------------------
+// Table-wise sharded serving: every rank runs the
+// SAME global batch sequence, because each rank's chain exchanges pooled vectors and CTRs with
+// every other rank's chain of that batch.  Batch composition therefore cannot depend on when
+// a rank's streams become idle (S2's work-conserving trigger): a deterministic global
+// dispatcher cuts batches from the trace alone (reading R31) -
+//   the FIFO of sub-queries (S1) is cut into batches of whole sub-queries with cumulative
+//   size <= d; a batch closes when it is full (the next sub-query would not fit, or it holds
+//   exactly d items) or tau after its first sub-query arrived, whichever comes first;
+//   batch k goes to stream slot k mod m.
+// Every rank releases batch k at max(its close time, completion of batch k - m on that slot)
+// on its own clock (clocks aligned by an NCCL barrier before the trace starts); the device
+// flags order the exchange, so no host message is needed per batch.
+struct ShardBatch {
+  int64_t c0, nc, items;
+  double close;  // trace time
+};
+
+static void cut_batches(const rec_trace_row* trace, const std::vector<Chunk>& ch, int32_t d, double tau,
+                        std::vector<ShardBatch>& out) {
+  double prev = -INFINITY;
+  const int64_t nch = static_cast<int64_t>(ch.size());
+  for (int64_t i = 0; i < nch;) {
+    const double first = trace[ch[i].pos].arrival_s, deadline = first + tau;
+    int64_t j = i, items = 0;
+    while (j < nch && items + ch[j].len <= d && trace[ch[j].pos].arrival_s <= deadline) items += ch[j++].len;
+    if (j == i) items += ch[j++].len;  // (a sub-query is never larger than d)
+    double close = deadline;
+    if (items == d) close = trace[ch[j - 1].pos].arrival_s;                      // exactly full
+    else if (j < nch && trace[ch[j].pos].arrival_s <= deadline) close = trace[ch[j].pos].arrival_s;  // next overflows
+    close = std::max(close, prev);
+    out.push_back(ShardBatch{i, j - i, items, close});
+    prev = close;
+    i = j;
+  }
+}
+
+static rec_status serve_sharded(rec_model_s* m, const rec_trace_row* trace, int64_t n, double sla_ms,
+                                const rec_serve_policy* pol, rec_serve_report* out, double* latency_ms,
+                                int32_t* batch_log, int64_t log_cap, int64_t* log_rows, float* ctr_out) {
+  if (pol->input_mode != REC_INPUT_DEVICE_SYNTH || pol->clock != REC_CLOCK_REAL) {
+    set_error("sharded serving: device-synthesised inputs and the real clock only");
+    return REC_E_UNSUPPORTED;
+  }
+  if (!(m->p2p_slots && m->ws[0].slots[0].var[0].exec)) {
+    set_error("sharded serving needs table-wise sharding over peer memory and fixed pooling");
+    return REC_E_UNSUPPORTED;
+  }
+  const int M = pol->streams;
+  const int32_t d = pol->max_batch;
+  // tau (R31): the policy's fusion timeout, else SLA / 50 (1 ms at RMC2's 50 ms SLA)
+  const double tau = (pol->fusion_timeout_ms > 0 ? pol->fusion_timeout_ms : sla_ms / 50.0) * 1e-3;
+  std::vector<Chunk> ch;
+  ch.reserve(static_cast<size_t>(n) * 2);
+  for (int64_t p = 0; p < n; ++p) split_query(trace[p], p, d, ch);
+  std::vector<ShardBatch> bt;
+  cut_batches(trace, ch, d, tau, bt);
+  const int64_t nb = static_cast<int64_t>(bt.size());
+  std::vector<int64_t> item_base;
+  if (ctr_out) {
+    item_base.resize(n);
+    int64_t acc = 0;
+    for (int64_t p = 0; p < n; ++p) {
+      item_base[p] = acc;
+      acc += trace[p].size;
+    }
+  }
+  std::vector<Lane> lanes(M);
+  auto cleanup = [&]() {
+    for (auto& L : lanes) {
+      if (L.ctr_host) cudaFreeHost(L.ctr_host);
+      if (L.flag_host) cudaFreeHost(L.flag_host);
+    }
+  };
+  for (int s = 0; s < M; ++s) {
+    void* hp = nullptr;
+    void* dp = nullptr;
+    if (cudaHostAlloc(&hp, 64, cudaHostAllocMapped) != cudaSuccess ||
+        cudaHostGetDevicePointer(&dp, hp, 0) != cudaSuccess) {
+      cleanup();
+      set_error("mapped completion words unavailable");
+      return REC_E_CUDA;
+    }
+    lanes[s].flag_host = static_cast<uint32_t*>(hp);
+    lanes[s].flag_dev = reinterpret_cast<CUdeviceptr>(dp);
+    *lanes[s].flag_host = 0;
+    if (ctr_out && cudaMallocHost(reinterpret_cast<void**>(&lanes[s].ctr_host), sizeof(float) * d) != cudaSuccess) {
+      cleanup();
+      return REC_E_OOM;
+    }
+  }
+  for (int s = 0; s < M; ++s) {
+    rec_status st = rec_sync(m, s);
+    if (st != REC_OK) { cleanup(); return st; }
+  }
+  // clock alignment: every rank leaves this barrier within a few microseconds
+  {
+    int* f = nullptr;
+    REC_CUDA(cudaMalloc(reinterpret_cast<void**>(&f), sizeof(int)));
+    ncclResult_t r = ncclAllReduce(f, f, 1, ncclInt32, ncclSum, static_cast<ncclComm_t>(m->nccl_comm),
+                                   m->ws[0].stream);
+    cudaStreamSynchronize(m->ws[0].stream);
+    cudaFree(f);
+    if (r != ncclSuccess) {
+      cleanup();
+      set_error("NCCL barrier failed: %s", ncclGetErrorString(r));
+      return REC_E_NCCL;
+    }
+  }
+  std::vector<int32_t> remaining(n);
+  for (int64_t p = 0; p < n; ++p) remaining[p] = (trace[p].size + d - 1) / d;
+  std::vector<double> done_t(n, NAN), release(n), disp_t(n, NAN);
+  for (int64_t p = 0; p < n; ++p) release[p] = trace[p].arrival_s;
+  std::vector<int64_t> slot_batch(M, -1);
+  std::vector<uint32_t> seq(M, 0);
+  std::vector<int32_t> segs;
+  int64_t completed = 0, logged = 0;
+  const double t_first = trace[0].arrival_s;
+  const double t0 = now_s() - t_first;
+  auto finish = [&](int s) {
+    const int64_t k = slot_batch[s];
+    const double tc = now_s() - t0;
+    for (int64_t c = bt[k].c0; c < bt[k].c0 + bt[k].nc; ++c)
+      if (--remaining[ch[c].pos] == 0) {
+        done_t[ch[c].pos] = tc;
+        ++completed;
+      }
+    if (ctr_out) {
+      int row = 0;
+      for (int64_t c = bt[k].c0; c < bt[k].c0 + bt[k].nc; ++c) {
+        memcpy(ctr_out + item_base[ch[c].pos] + ch[c].start, lanes[s].ctr_host + row, sizeof(float) * ch[c].len);
+        row += ch[c].len;
+      }
+    }
+    slot_batch[s] = -1;
+  };
+  auto poll = [&]() {
+    for (int s = 0; s < M; ++s)
+      if (slot_batch[s] >= 0 &&
+          static_cast<int32_t>(*reinterpret_cast<volatile uint32_t*>(lanes[s].flag_host) - seq[s]) >= 0)
+        finish(s);
+  };
+  for (int64_t k = 0; k < nb; ++k) {
+    const int s = static_cast<int>(k % M);
+    while (slot_batch[s] >= 0 || now_s() - t0 < bt[k].close) {
+      poll();
+      cpu_relax();
+    }
+    Workspace& w = m->ws[s];
+    segs.resize(3 * bt[k].nc);
+    for (int64_t c = 0; c < bt[k].nc; ++c) {
+      const Chunk& x = ch[bt[k].c0 + c];
+      segs[3 * c] = x.qid;
+      segs[3 * c + 1] = x.start;
+      segs[3 * c + 2] = x.len;
+      if (batch_log && logged < log_cap) {
+        int32_t* r = batch_log + 5 * logged++;
+        r[0] = static_cast<int32_t>(k);
+        r[1] = s;
+        r[2] = x.qid;
+        r[3] = x.start;
+        r[4] = x.len;
+      }
+    }
+    const double td = now_s() - t0;
+    int B = 0;
+    rec_status st = synth_submit(m, w, segs.data(), static_cast<int>(bt[k].nc), &B, nullptr);
+    if (st == REC_OK && ctr_out &&
+        cudaMemcpyAsync(lanes[s].ctr_host, w.sh_ctr_gather, sizeof(float) * B, cudaMemcpyDeviceToHost,
+                        w.stream) != cudaSuccess)
+      st = REC_E_CUDA;
+    if (st == REC_OK) st = stream_write_u32(w.stream, lanes[s].flag_dev, ++seq[s]);
+    if (st != REC_OK) { cleanup(); return st; }
+    for (int64_t c = bt[k].c0; c < bt[k].c0 + bt[k].nc; ++c) disp_t[ch[c].pos] = td;
+    slot_batch[s] = k;
+  }
+  bool any = true;
+  while (any) {
+    poll();
+    any = false;
+    for (int s = 0; s < M; ++s) any = any || slot_batch[s] >= 0;
+    if (any) cpu_relax();
+  }
+  for (int s = 0; s < M; ++s) {
+    rec_status st = rec_sync(m, s);
+    if (st != REC_OK) { cleanup(); return st; }
+  }
+  cleanup();
+  double items_tot = 0;
+  for (auto& b : bt) items_tot += b.items;
+  fill_report(trace, n, sla_ms, pol->warmup_frac, release, disp_t, done_t, completed, nb, items_tot,
+              latency_ms, out);
+  if (log_rows) *log_rows = logged;
+  return REC_OK;
+}
+
 }  // namespace rec
 
 using namespace rec;
@@ -290,6 +530,8 @@ rec_status rec_serve(rec_model_t m, const rec_trace_row* trace, int64_t n, doubl
     }
   }
   REC_CUDA(cudaSetDevice(m->device));
+  if (m->world > 1 && m->shard != REC_SHARD_REPLICA)
+    return serve_sharded(m, trace, n, sla_ms, pol, out, latency_ms, batch_log, log_cap, log_rows, ctr_out);
   const int M = pol->streams;
   const int32_t d = pol->max_batch;
   const bool virt = pol->clock == REC_CLOCK_VIRTUAL;
@@ -633,42 +875,10 @@ rec_status rec_serve(rec_model_t m, const rec_trace_row* trace, int64_t n, doubl
   cleanup();
 
   // ------------------------------------------------ report (S5)
-  const double t_last = trace[n - 1].arrival_s;
-  const double w_end = t_first + pol->warmup_frac * (t_last - t_first);
-  std::vector<double> lat;
-  double sum_lat = 0, sum_q = 0, sum_svc = 0, t_max = t_first;
-  for (int64_t p = 0; p < n; ++p) {
-    const double l = done_t[p] - release[p];
-    if (latency_ms) latency_ms[p] = l * 1e3;
-    t_max = std::max(t_max, done_t[p]);
-    if (release[p] >= w_end) {
-      lat.push_back(l * 1e3);
-      sum_lat += l * 1e3;
-      sum_q += (disp_t[p] - release[p]) * 1e3;
-      sum_svc += (done_t[p] - disp_t[p]) * 1e3;
-    }
-  }
-  std::sort(lat.begin(), lat.end());
-  const int64_t nm = static_cast<int64_t>(lat.size());
-  memset(out, 0, sizeof(*out));
-  out->completed = completed;
-  out->dropped = n - completed;
-  out->batches = static_cast<int64_t>(batches.size());
   double items_tot = 0;
   for (auto& b : batches) items_tot += b.items;
-  out->mean_batch = batches.empty() ? 0 : items_tot / batches.size();
-  if (nm > 0) {
-    out->p50_ms = lat[pct_rank(50, nm) - 1];
-    out->p95_ms = lat[pct_rank(95, nm) - 1];
-    out->p99_ms = lat[pct_rank(99, nm) - 1];
-    out->mean_ms = sum_lat / nm;
-    out->breakdown_ms[0] = sum_q / nm;   // queueing (arrival -> dispatch of last sub-query)
-    out->breakdown_ms[2] = sum_svc / nm; // input + device + completion observation
-  }
-  out->offered_qps = t_last > t_first ? n / (t_last - t_first) : INFINITY;
-  out->achieved_qps = t_max > t_first ? n / (t_max - t_first) : 0;
-  out->stable = (completed == n) && out->achieved_qps >= 0.98 * out->offered_qps;
-  out->sla_met = out->stable && out->p95_ms <= sla_ms;
+  fill_report(trace, n, sla_ms, pol->warmup_frac, release, disp_t, done_t, completed,
+              static_cast<int64_t>(batches.size()), items_tot, latency_ms, out);
   if (log_rows) *log_rows = logged;
   return REC_OK;
 }

@@ -21,6 +21,51 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 
+def async_checks(cfg, rank, world, local, bcast_id, rep):
+    """Table-wise sharding over peer memory, asynchronous: several global batches
+    in flight on several stream slots (device-synthesised inputs, and caller inputs through
+    rec_query_async), and rec_serve with the deterministic global dispatcher - every CTR must
+    equal the replica's bits."""
+    import torch
+    import workloads as W
+    from paper_2203_07424_b200 import RecModel, REC_SHARD_TABLE
+    res = {}
+    m = RecModel(cfg, seed=1, max_batch=1024, streams=4, device=local, shard=REC_SHARD_TABLE,
+                 rank=rank, world=world, nccl_id=bcast_id())
+    batches = [W.random_segments(b, seed=500 + k) for k, b in enumerate((1024, 1, 333, 700, 1000, 5, 1024, 64))]
+    outs = [torch.zeros(int(sg[:, 2].sum()), device="cuda") for sg in batches]
+    for k, sg in enumerate(batches):                     # 8 batches round-robin on 4 slots
+        m.rec_synth_query_async(k % 4, sg, outs[k])
+    for s in range(4):
+        m.rec_sync(s)
+    good = True
+    for k, sg in enumerate(batches):
+        ref = torch.zeros(outs[k].numel(), device="cuda")
+        rep.rec_synth_query_async(0, sg, ref)
+        rep.rec_sync(0)
+        good &= bool(torch.equal(ref, outs[k]))
+    res["async_synth_bit_exact_vs_replica"] = good
+    good = True
+    for k, sg in enumerate(batches[:4]):                 # caller inputs, asynchronous
+        ind, off, dense = rep.rec_gen_batch(sg)
+        B = dense.shape[0]
+        dv, iv, ov = (torch.from_numpy(x).cuda() for x in (dense, ind, off))
+        cv = torch.zeros(B, device="cuda")
+        m.rec_query_async(k % 4, dv, iv, ov, int(off[-1]), B, cv)
+        m.rec_sync(k % 4)
+        good &= bool(torch.equal(cv, outs[k]))
+    res["async_caller_bit_exact_vs_replica"] = good
+    tr = W.poisson_trace(20000.0, 600, seed=13)
+    r = m.rec_serve(tr, 50.0, streams=4, max_batch=1024, want_ctr=True)
+    rr = rep.rec_serve(tr, 50.0, streams=1, max_batch=1024, want_ctr=True)
+    res["serve_all_completed"] = bool(r["completed"] == len(tr))
+    res["serve_ctr_bit_exact_vs_replica"] = bool(np.array_equal(r["ctr"], rr["ctr"]))
+    res["info_p95_ms"] = round(r["p95_ms"], 3)
+    res["info_batches"] = int(r["batches"])
+    m.close()
+    return res
+
+
 def main():
     import torch
     import torch.distributed as dist
@@ -91,6 +136,9 @@ def main():
             dist.all_reduce(us, op=dist.ReduceOp.MAX)
             res[tag] = round(float(us), 1)
         out["timing_us"][name] = res
+        if shard == REC_SHARD_TABLE and name == "table_rmc2" and os.environ.get("REC_P2P", "1") != "0":
+            chk.update(async_checks(cfg, rank, world, local, bcast_id, rep))
+            ok &= all(v for k, v in chk.items() if k.startswith("async") or k.startswith("serve"))
         shm.close()
         rep.close()
     okt = torch.tensor([1 if ok else 0], device="cuda")

@@ -17,7 +17,7 @@ pytestmark = pytest.mark.gpu
 KNOBS = ["REC_SLS", "REC_GEMM_2SM", "REC_GEMM_NARROW", "REC_GEMM_MT1", "REC_FUSE_DENSE",
          "REC_INTERACT_PF", "REC_HOT_POLICY", "REC_MLP", "REC_CHAIN_PDL", "REC_PDL",
          "REC_FUSE_INTERACT", "REC_TOWER_GROUP", "REC_GEMM_STAGES", "REC_INTERACT_WPC",
-         "REC_CHAIN_SMEM", "REC_CHAIN_STAGES", "REC_CHAIN_STRICT", "REC_SERVE_DEPTH",
+         "REC_CHAIN_SMEM", "REC_CHAIN_STAGES", "REC_SERVE_DEPTH",
          "REC_SERVE_THREADS", "REC_GREEN_SMS", "REC_PRIO"]
 
 
@@ -67,7 +67,7 @@ VARIANTS = [
     ("mlp_layers_rmc1", {"REC_MLP": "layers"}, RMC1, 700, 0),
     ("chain_no_pdl", {"REC_CHAIN_PDL": "0"}, RMC1, 700, 0),
     ("chain_2stage", {"REC_CHAIN_STAGES": "2"}, RMC1, 700, 0),
-    ("chain_over_budget", {"REC_CHAIN_STRICT": "0"}, RMC3, 700, 0),
+    ("chain_big_budget", {"REC_CHAIN_SMEM": "227"}, RMC1, 700, 0),
     ("gemm_narrow", {"REC_GEMM_NARROW": "148"}, RMC3, 700, 0),
     ("gemm_stages2", {"REC_GEMM_STAGES": "2"}, RMC3, 700, 0),
     ("gemm_2sm_large", {"REC_GEMM_2SM": "1"}, RMC3, 20480, 0),
