@@ -757,6 +757,15 @@ def run_sharded(args):
         model.rec_query_async(i % m_streams, h[0], h[1], h[2], h[3], h[4], outs[i % m_streams])
     for k in range(m_streams):
         model.rec_sync(k)
+    from paper_2203_07424_b200 import rec_shard_plan
+
+    def h2d_bytes(h):  # what rec_query_async copies on this rank: offsets, the local tables'
+        B = h[4]       # indices, the own block's dense rows (include/rec.h)
+        pl = rec_shard_plan([cfg.rows] * cfg.num_tables, world, rank, shard, B)
+        off = h[2].numpy()
+        nidx = int(off[(pl["t0"] + pl["t_local"]) * B]) - int(off[pl["t0"] * B])
+        return 4 * (off.size + nidx + pl["items"] * cfg.dense_dim)
+    hb = [h2d_bytes(h) for h in host]
     dist.barrier()
     t0 = time.perf_counter()
     q_e2e = h2d = d2h = 0
@@ -764,7 +773,7 @@ def run_sharded(args):
         h = host[i % len(host)]
         model.rec_query_async(i % m_streams, h[0], h[1], h[2], h[3], h[4], outs[i % m_streams])
         q_e2e += h[5]
-        h2d += (h[0].numel() + h[1].numel() + h[2].numel()) * 4
+        h2d += hb[i % len(host)]
         d2h += 4 * h[4]
     for k in range(m_streams):
         model.rec_sync(k)

@@ -39,7 +39,8 @@ typedef enum {
 } rec_status;
 
 enum { REC_VALUES_INT8_EXACT = 0, REC_VALUES_FP32 = 1 };           /* DESIGN.md G4        */
-enum { REC_INDEX_UNIFORM = 0, REC_INDEX_SKEW2 = 2 };                /* DESIGN.md G2, R17   */
+enum { REC_INDEX_UNIFORM = 0, REC_INDEX_SKEW2 = 2,                 /* DESIGN.md G2, R17   */
+       REC_INDEX_ZIPF = 3 };   /* Zipf(0.9) rows scattered by a bijection (G2z) */
 enum { REC_SHARD_REPLICA = 0, REC_SHARD_TABLE = 1, REC_SHARD_ROW = 2 };
 enum { REC_INPUT_DEVICE_SYNTH = 0, REC_INPUT_HOST = 1 };
 enum { REC_CLOCK_REAL = 0, REC_CLOCK_VIRTUAL = 1 };                 /* DESIGN.md S4        */
@@ -67,7 +68,7 @@ typedef struct {
   int32_t top_shift;              /* extra 2^-top_shift on the first top layer (R21)        */
   uint64_t seed;                  /* tables, weights and synthetic inputs = f(seed) (G1-G5) */
   int32_t value_mode;             /* REC_VALUES_INT8_EXACT | REC_VALUES_FP32                */
-  int32_t index_dist;             /* REC_INDEX_UNIFORM | REC_INDEX_SKEW2 (synthetic inputs) */
+  int32_t index_dist;             /* REC_INDEX_UNIFORM | REC_INDEX_SKEW2 | REC_INDEX_ZIPF    */
   int32_t max_batch;              /* workspace capacity in items per call/batch (>= 1)      */
   int32_t streams;                /* co-located streams m, workspaces, >= 1     */
   int32_t device;                 /* CUDA device ordinal used by this handle                */
@@ -217,6 +218,22 @@ rec_status rec_bench_sls(rec_model_t m, const int32_t* segs, const int64_t* batc
  * time of the launch in ns.  Zero = stage not reached. */
 rec_status rec_debug_chain_timeline(rec_model_t m, int32_t which, int32_t batch, int64_t* out16);
 rec_status rec_profile_read(rec_model_t m, int32_t kernel, double* total_ms, int64_t* launches);
+
+/* Locality-aware hot-row partition ("hot" embeddings placed in
+ * the fastest memory, the partition sized by "memory capacity / model co-location").
+ * indices / offsets [T*batch+1]: a profiling sample of queries (table-major CSR, original row
+ * ids, host or device).  The library counts accesses per (table, row), orders every table's
+ * rows by descending count (ties by row id), physically permutes the embedding arena so the
+ * hot rows of all tables form one contiguous prefix (interleaved arena), and from then on
+ * maps every index (caller or device-synthesised) to its arena row before the gather; CTRs
+ * are unchanged (the same rows are summed in the same order).  A persisting L2 access-policy
+ * window then covers the first window_bytes of the arena: window_bytes = 0 -> the device's
+ * persisting-L2 capacity / the number of models co-located on the device, < 0 -> no window.
+ * *hot_rows (optional) = rows per table inside the window.  Synchronises the device and
+ * re-captures the model's graphs.  Errors: INVALID_ARG, UNSUPPORTED (sharded models, unequal
+ * rows), OFFSETS, INDEX_OOB (profile index out of range), OOM, CUDA. */
+rec_status rec_hot_remap(rec_model_t m, const int32_t* indices, const int32_t* offsets, int32_t batch,
+                         int64_t window_bytes, int64_t* hot_rows);
 
 /* ---------------------------------------------------------------- serving (a1, a7) */
 typedef struct { double arrival_s; int32_t size; int32_t qid; } rec_trace_row;

@@ -143,9 +143,60 @@ def bag_indices(seed: int, cfg, t: int, q: np.ndarray, it: np.ndarray, lengths_t
     j = (np.arange(nnz, dtype=np.int64) - starts).astype(np.uint64)
     w0, w1, w2, w3 = philox(j, bi, np.uint64((t << 8) | 1), bq, k0, k1)
     r = _u64(w0, w1)
+    if cfg.index_dist == 3:                  # Zipf(0.9), scattered (G2z)
+        return zipf_rows(r, rows_t, t)
     if cfg.index_dist == 2:                  # skewed: product of two uniforms (G2)
         r = mulhi64(r, _u64(w2, w3))
     return mulhi64(r, np.uint64(rows_t)).astype(np.int64)
+
+
+# ------------------------------------------------------------------ Zipf(0.9) indices (G2z)
+# SPEC.md:279 draws embedding rows from a Zipf law with exponent 0.9 ("hot" rows, the locality
+# the hot-embedding partition exploits).  G2z is the continuous inverse-CDF
+# form of that law, written so that every step is an exactly rounded IEEE fp64 operation (no
+# pow, no fused multiply-add), hence bit-identical wherever it is evaluated:
+#   c     = the largest double in [1, 16] with pow10(c) <= R, by 60 bisection steps
+#   u     = (r >> 11) * 2^-53                      (53-bit uniform in [0, 1))
+#   x     = 1 + u * (c - 1)                        (x uniform in [1, c))
+#   y     = pow10(x) = ((x^2)^2)^2 * x^2           (y = x^10 has density prop. to y^-0.9)
+#   rank  = min(floor(y) - 1, R - 1)               (0 = hottest)
+#   row   = (rank * 2654435761 + 7919 t) mod R    (a bijection: 2654435761 is prime > R, so
+#                                                  hot rows are scattered over the table and
+#                                                  only a frequency profile finds them)
+ZIPF_MULT = 2654435761
+ZIPF_T_OFF = 7919
+
+
+def pow10(x):
+    """x^10 as four exactly rounded multiplications (x2 = x*x, x4, x8, x8*x2)."""
+    x2 = x * x
+    x4 = x2 * x2
+    x8 = x4 * x4
+    return x8 * x2
+
+
+def zipf_c(R: int) -> float:
+    lo, hi = 1.0, 16.0
+    for _ in range(60):
+        mid = (lo + hi) * 0.5
+        if pow10(mid) <= float(R):
+            lo = mid
+        else:
+            hi = mid
+    return lo
+
+
+def zipf_rank(r: np.ndarray, R: int) -> np.ndarray:
+    c = zipf_c(R)
+    u = (np.asarray(r, dtype=np.uint64) >> np.uint64(11)).astype(np.float64) * 2.0 ** -53
+    x = 1.0 + u * (c - 1.0)
+    y = pow10(x)
+    return np.minimum(np.floor(y).astype(np.int64) - 1, R - 1)
+
+
+def zipf_rows(r: np.ndarray, R: int, t: int) -> np.ndarray:
+    rank = zipf_rank(r, R).astype(np.uint64)
+    return ((rank * np.uint64(ZIPF_MULT) + np.uint64(ZIPF_T_OFF * t)) % np.uint64(R)).astype(np.int64)
 
 
 def dense_features(seed: int, F: int, q: np.ndarray, it: np.ndarray) -> np.ndarray:

@@ -22,7 +22,7 @@ REC_OK = 0
 STATUS = {0: "REC_OK", -1: "REC_E_INVALID_ARG", -2: "REC_E_INDEX_OOB", -3: "REC_E_OFFSETS",
           -4: "REC_E_OOM", -5: "REC_E_CUDA", -6: "REC_E_NCCL", -7: "REC_E_UNSUPPORTED"}
 REC_VALUES_INT8_EXACT, REC_VALUES_FP32 = 0, 1
-REC_INDEX_UNIFORM, REC_INDEX_SKEW2 = 0, 2
+REC_INDEX_UNIFORM, REC_INDEX_SKEW2, REC_INDEX_ZIPF = 0, 2, 3
 REC_SHARD_REPLICA, REC_SHARD_TABLE, REC_SHARD_ROW = 0, 1, 2
 REC_INPUT_DEVICE_SYNTH, REC_INPUT_HOST = 0, 1
 REC_CLOCK_REAL, REC_CLOCK_VIRTUAL = 0, 1
@@ -33,7 +33,7 @@ EXPORTS = ["rec_model_create", "rec_model_destroy", "rec_query", "rec_query_debu
            "rec_gen_batch", "rec_profile", "rec_profile_read", "rec_serve", "rec_last_error",
            "rec_nccl_unique_id_size", "rec_nccl_get_unique_id", "rec_version", "rec_split_fuse",
            "rec_synth_query_batches", "rec_shard_plan", "rec_bench_mlp", "rec_bench_sls", "rec_set_pipeline", "rec_synth_query_pipeline",
-           "rec_debug_chain_timeline", "rec_query_inspect"]
+           "rec_debug_chain_timeline", "rec_query_inspect", "rec_hot_remap"]
 
 
 class rec_model_desc(C.Structure):
@@ -116,6 +116,8 @@ def lib() -> C.CDLL:
         L.rec_debug_chain_timeline.restype = i32
         L.rec_query_inspect.argtypes = [vp, vp, vp, vp, i32, vp, vp, vp, C.POINTER(i32)]
         L.rec_query_inspect.restype = i32
+        L.rec_hot_remap.argtypes = [vp, vp, vp, i32, i64, C.POINTER(i64)]
+        L.rec_hot_remap.restype = i32
         for f in ("rec_model_create", "rec_query", "rec_query_debug", "rec_query_async",
                   "rec_synth_query_async", "rec_sync", "rec_gen_batch", "rec_profile",
                   "rec_profile_read", "rec_serve", "rec_nccl_get_unique_id"):
@@ -221,6 +223,12 @@ class RecModel:
                                        _ptr(ctr), _ptr(x), _ptr(a), C.byref(ld)))
         assert ld.value == a.shape[1]
         return ctr, x, a
+
+    def rec_hot_remap(self, indices, offsets, batch: int, window_bytes: int = 0) -> int:
+        """Hot-row partition from a profiling sample; returns rows per table in the L2 window."""
+        h = C.c_int64()
+        _check(lib().rec_hot_remap(self.h, _ptr(indices), _ptr(offsets), batch, window_bytes, C.byref(h)))
+        return h.value
 
     def rec_query_async(self, slot: int, dense, indices, offsets, nnz: int, batch: int, ctr):
         _check(lib().rec_query_async(self.h, slot, _ptr(dense), _ptr(indices), _ptr(offsets),

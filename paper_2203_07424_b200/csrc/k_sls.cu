@@ -305,6 +305,8 @@ __global__ void __launch_bounds__(THREADS, REC_SLS_MINB) k_sls_synth(const __gri
   const uint64_t R = static_cast<uint64_t>(__ldg(&a.rows[t]));
   const int64_t toff = __ldg(&a.tab_off[t]);
   const uint32_t c2 = (static_cast<uint32_t>(a.t0 + t) << 8) | DOM_INDEX;
+  const double zc = a.index_dist == 3 ? zipf_c(R) : 0.0;
+  const int* __restrict__ remap = a.remap ? a.remap + __ldg(&a.remap_off[t]) : nullptr;
   const bool active = (sub * 4) < a.D;
   const int col = active ? sub * 4 : 0;
   const float4* __restrict__ tab = reinterpret_cast<const float4*>(a.tables + toff + col);
@@ -322,7 +324,8 @@ __global__ void __launch_bounds__(THREADS, REC_SLS_MINB) k_sls_synth(const __gri
 #pragma unroll
   for (int q = 0; q < S::IPL; ++q) {
     const int j = q * LANES + sub;
-    cur[q] = j < L ? gen_index(j, qi.y, c2, qi.x, a.k0, a.k1, R, a.index_dist) : 0;
+    cur[q] = j < L ? gen_index(j, qi.y, c2, qi.x, a.k0, a.k1, R, a.index_dist, zc) : 0;
+    if (remap) cur[q] = __ldg(remap + cur[q]);  // hot-row partition: arena row of the index
   }
   SLS_STAMP(1);
   for (int base = 0; base < L; base += S::ROWS) {
@@ -344,7 +347,8 @@ __global__ void __launch_bounds__(THREADS, REC_SLS_MINB) k_sls_synth(const __gri
 #pragma unroll
         for (int q = 0; q < S::IPL; ++q) {
           const int j = base + S::ROWS + q * LANES + sub;
-          cur[q] = j < L ? gen_index(j, qi.y, c2, qi.x, a.k0, a.k1, R, a.index_dist) : 0;
+          cur[q] = j < L ? gen_index(j, qi.y, c2, qi.x, a.k0, a.k1, R, a.index_dist, zc) : 0;
+          if (remap) cur[q] = __ldg(remap + cur[q]);
         }
       }
 #pragma unroll
@@ -464,7 +468,8 @@ __global__ void __launch_bounds__(SLS_TMA_WARPS * 32, 1)
       const int2 qi = row_item(sb, b);
       const uint64_t R = static_cast<uint64_t>(__ldg(&a.rows[t]));
       const uint32_t c2 = (static_cast<uint32_t>(t) << 8) | DOM_INDEX;
-      const int idx = gen_index(c * SLS_TMA_CR + lane, qi.y, c2, qi.x, a.k0, a.k1, R, a.index_dist);
+      const int idx = gen_index(c * SLS_TMA_CR + lane, qi.y, c2, qi.x, a.k0, a.k1, R, a.index_dist,
+                                a.index_dist == 3 ? zipf_c(R) : 0.0);
       coord = static_cast<int>(__ldg(&a.tab_off[t]) / D) + idx * rs;
     }
     const int nops = (n + 3) >> 2;

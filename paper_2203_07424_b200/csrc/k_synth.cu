@@ -1,3 +1,4 @@
+#include <algorithm>
 // k_synth.cu — synthetic parameters and batch inputs as Philox functions of counters
 // (G2-G5).  Every value is bit-identical to oracle/gen.py.
 #include "common.cuh"
@@ -90,9 +91,10 @@ __global__ void __launch_bounds__(32 * kGenWPB) k_gen_fused(const __grid_constan
     if (lane == 0) ga.offsets[g] = g * L;
     const uint64_t R = static_cast<uint64_t>(__ldg(&ga.rows[t]));
     const uint32_t c2 = (static_cast<uint32_t>(t) << 8) | DOM_INDEX;
+    const double zc = ga.index_dist == 3 ? zipf_c(R) : 0.0;
     int* dst = ga.indices + static_cast<int64_t>(g) * L;
     for (int j = lane; j < L; j += 32)
-      dst[j] = gen_index(j, qi.y, c2, qi.x, ga.k0, ga.k1, R, ga.index_dist);
+      dst[j] = gen_index(j, qi.y, c2, qi.x, ga.k0, ga.k1, R, ga.index_dist, zc);
   } else {
     const int b = (blockIdx.x - ga.nbag_blocks) * kGenWPB + (threadIdx.x >> 5);
     if (b >= B) return;
@@ -233,8 +235,9 @@ __global__ void k_gen_indices(const int* __restrict__ rowq, const int* __restric
     const uint64_t R = static_cast<uint64_t>(rows[t]);
     const uint32_t c2 = (static_cast<uint32_t>(t) << 8) | DOM_INDEX;
     const int s0 = off[g], e = off[g + 1];
+    const double zc = index_dist == 3 ? zipf_c(R) : 0.0;
     for (int j = lane; j < e - s0; j += 32)
-      indices[s0 + j] = gen_index(j, it, c2, q, k0, k1, R, index_dist);
+      indices[s0 + j] = gen_index(j, it, c2, q, k0, k1, R, index_dist, zc);
   }
 }
 
@@ -288,6 +291,60 @@ void launch_dense_to_bf16(const float* dense, int B, int F, int Fpad, __nv_bfloa
   int blocks = static_cast<int>((n + 255) / 256);
   if (blocks > 148 * 16) blocks = 148 * 16;
   k_dense_to_bf16<<<blocks, 256, 0, s>>>(dense, B, F, Fpad, out);
+}
+
+// ------------------------------------------------------- hot-row partition (rec_hot_remap)
+__global__ void k_remap(const int* __restrict__ in, const int* __restrict__ off, int B,
+                        const int* __restrict__ dB, const int64_t* __restrict__ rows,
+                        const int* __restrict__ remap, const int64_t* __restrict__ remap_off,
+                        int* __restrict__ out, int64_t cap, int* __restrict__ flag) {
+  if (dB) B = *dB;
+  const int t = blockIdx.y;
+  const int lo = off[t * B], hi = off[(t + 1) * B];
+  const int64_t R = rows[t];
+  const int* map = remap + remap_off[t];
+  bool oob = false, over = false;
+  for (int i = lo + blockIdx.x * blockDim.x + threadIdx.x; i < hi; i += gridDim.x * blockDim.x) {
+    const int r = in[i];
+    const bool ok = r >= 0 && r < R;
+    oob |= !ok;
+    if (i < cap) out[i] = ok ? __ldg(map + r) : 0;
+    else over = true;
+  }
+  if (oob) atomicOr(flag, 1);
+  if (over) atomicOr(flag, 2);
+}
+
+void launch_remap(const int* in, const int* offsets, int B, const int* dB, int T, const int64_t* rows,
+                  const int* remap, const int64_t* remap_off, int* out, int64_t cap, int* flag,
+                  cudaStream_t s) {
+  if (T <= 0 || B <= 0) return;
+  k_remap<<<dim3(32, T), 256, 0, s>>>(in, offsets, B, dB, rows, remap, remap_off, out, cap, flag);
+}
+
+__global__ void k_permute_rows(const float4* __restrict__ src, float4* __restrict__ dst,
+                               const int64_t* __restrict__ tab_off, int64_t row_stride,
+                               const int64_t* __restrict__ rows, int D, const int* __restrict__ inv,
+                               const int64_t* __restrict__ remap_off) {
+  const int t = blockIdx.y;
+  const int64_t R = rows[t];
+  const int d4 = D / 4;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < R * d4;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t p = e / d4;
+    const int c = static_cast<int>(e - p * d4);
+    const int64_t o = inv[remap_off[t] + p];
+    dst[(tab_off[t] + p * row_stride) / 4 + c] = src[(tab_off[t] + o * row_stride) / 4 + c];
+  }
+}
+
+void launch_permute_rows(const float* src, float* dst, const int64_t* tab_off, int64_t row_stride,
+                         const int64_t* rows, int T, int D, const int* inv, const int64_t* remap_off,
+                         int64_t max_rows, cudaStream_t s) {
+  const int64_t n = max_rows * (D / 4);
+  const int bx = static_cast<int>(std::min<int64_t>((n + 255) / 256, 4096));
+  k_permute_rows<<<dim3(bx, T), 256, 0, s>>>(reinterpret_cast<const float4*>(src), reinterpret_cast<float4*>(dst),
+                                             tab_off, row_stride, rows, D, inv, remap_off);
 }
 
 // ------------------------------------------------------- caller offsets validation

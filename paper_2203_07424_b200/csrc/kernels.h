@@ -52,6 +52,17 @@ void launch_dense_to_bf16(const float* dense, int B, int F, int Fpad, __nv_bfloa
                           cudaStream_t s);
 // Flags bit 1 when offsets[0] != 0, offsets decrease, or (nnz >= 0) offsets[nbags] != nnz.
 void launch_check_offsets(const int* offsets, int nbags, int* flag, cudaStream_t s, int64_t nnz = -1);
+// Hot-row partition (rec_hot_remap): out[i] = remap[remap_off[t] + in[i]] for every index of
+// the table-major CSR batch (t from the offsets); indices outside [0, rows_t) set flag bit 0
+// and map to 0; positions >= cap are not written (flag bit 1).  B from *dB when dB != nullptr.
+void launch_remap(const int* in, const int* offsets, int B, const int* dB, int T, const int64_t* rows,
+                  const int* remap, const int64_t* remap_off, int* out, int64_t cap, int* flag,
+                  cudaStream_t s);
+// Arena row permutation: new arena row p of table t = old row inv[remap_off[t] + p] (interleaved
+// or table-major arena: row r of table t at tab_off[t] + r * row_stride).
+void launch_permute_rows(const float* src, float* dst, const int64_t* tab_off, int64_t row_stride,
+                         const int64_t* rows, int T, int D, const int* inv, const int64_t* remap_off,
+                         int64_t max_rows, cudaStream_t s);
 void set_max_smem_carveout(int percent);  // SLS kernels' preferred shared-memory carveout (0..100)
 
 // ------------------------------------------------------------------------- SLS (a3)
@@ -131,6 +142,10 @@ struct SlsSynthArgs {
   // the X of the rank owning the item (blocks of ceil(B / G)) and raises this rank's flags
   int t0;
   P2PArgs p2p;
+  // hot-row partition (rec_hot_remap): synthesised row r of table t is stored at arena row
+  // remap[remap_off[t] + r] (rows sorted by profiled frequency); nullptr = identity
+  const int* remap;
+  const int64_t* remap_off;
   int tma;     // 1: k_sls_synth_tma
   int nsm;     // SMs (persistent grid)
   int nst;     // ring chunks per warp

@@ -351,6 +351,13 @@ rec_status forward_enqueue(rec_model_s* m, Workspace& w, const int* indices, con
   enqueue_bottom(m, w, sb, B, dB, gev);
   mark(gev, 7, sb);
   REC_CUDA(cudaEventRecord(w.ev_join, sb));
+  if (m->d_remap) {  // hot-row partition: caller / materialised ids -> arena rows
+    launch_remap(indices, offsets, B, dB, m->T, m->d_rows, m->d_remap, m->d_remap_off, w.indices,
+                 w.idx_cap, w.flag, s);
+    m->launches += 1;
+    indices = w.indices;
+    idx_limit = std::min<int64_t>(idx_limit, w.idx_cap);
+  }
   cudaEvent_t e0 = gev ? nullptr : prof_begin(m, s);
   launch_sls(m->tables, m->d_tab_off, m->row_stride, m->d_rows, indices, offsets, B, dB, m->T, m->D,
              w.X, (m->T + 1) * m->D, 1, w.flag, s, 0, 0x7fffffff,
@@ -418,7 +425,9 @@ void fill_genargs(rec_model_s* m, Workspace& w, GenArgs& ga, SlsSynthArgs& sa,
   sa.dense_bf = m->fuse_dense ? w.dense_bf : nullptr;
   sa.F = m->F;
   sa.Fpad = m->Fpad;
-  sa.tma = m->sls_tma;
+  sa.remap = m->d_remap;
+  sa.remap_off = m->d_remap_off;
+  sa.tma = m->d_remap ? 0 : m->sls_tma;  // (the TMA variant does not read the remap)
   sa.pdl = m->sls_pdl && !sa.tma;
   sa.tmap_rows = m->d_tmap_rows;
   sa.nsm = m->nsm;
@@ -872,8 +881,19 @@ extern "C" {
 const char* rec_last_error(void) { return g_err.c_str(); }
 int32_t rec_version(void) { return 1; }
 
+// Models co-located on each device: the hot-row window of rec_hot_remap is the
+// persisting L2 capacity divided among them ("memory capacity / model co-location").
+static std::mutex g_reg_mu;
+static int g_models_on[64] = {};
+
 static void free_model(rec_model_s* m) {
   if (!m) return;
+  if (m->counted) {
+    std::lock_guard<std::mutex> g(g_reg_mu);
+    --g_models_on[m->device & 63];
+  }
+  cudaFree(m->d_remap);
+  cudaFree(m->d_remap_off);
   cudaSetDevice(m->device);
   pipe_destroy(m);
   for (auto& w : m->ws) {
@@ -1077,7 +1097,8 @@ rec_status rec_model_create(const rec_model_desc* d, rec_model_t* out) {
     set_error("value_mode = %d unknown", d->value_mode);
     return REC_E_INVALID_ARG;
   }
-  if (d->index_dist != REC_INDEX_UNIFORM && d->index_dist != REC_INDEX_SKEW2) {
+  if (d->index_dist != REC_INDEX_UNIFORM && d->index_dist != REC_INDEX_SKEW2 &&
+      d->index_dist != REC_INDEX_ZIPF) {
     set_error("index_dist = %d unknown", d->index_dist);
     return REC_E_INVALID_ARG;
   }
@@ -1602,6 +1623,11 @@ rec_status rec_model_create(const rec_model_desc* d, rec_model_t* out) {
         }
       }
   }
+  {
+    std::lock_guard<std::mutex> g(g_reg_mu);
+    ++g_models_on[m->device & 63];
+    m->counted = true;
+  }
   *out = m;
   return REC_OK;
 }
@@ -1615,6 +1641,152 @@ rec_status rec_query_debug(rec_model_t m, const float* dense, const int32_t* ind
                            const int32_t* offsets, int32_t batch, float* ctr, float* pooled,
                            float* logits) {
   return query_impl(m, dense, indices, offsets, batch, ctr, pooled, logits);
+}
+
+// ---------------------------------------------------------------- hot-row partition (f3)
+// L2 persisting window over the first `bytes` of the arena (the hot-row prefix: with the
+// interleaved layout row r of every table precedes row r + 1 of any table).
+static rec_status set_l2_window(rec_model_s* m, size_t bytes) {
+  cudaDeviceProp prop;
+  REC_CUDA(cudaGetDeviceProperties(&prop, m->device));
+  size_t win = std::min<size_t>(bytes, m->table_bytes);
+  win = std::min<size_t>(win, static_cast<size_t>(prop.accessPolicyMaxWindowSize));
+  const size_t carve = std::min<size_t>(win, prop.persistingL2CacheMaxSize);
+  if (win > 0) REC_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, carve));
+  for (auto& w : m->ws) {
+    cudaStreamAttrValue v{};
+    v.accessPolicyWindow.base_ptr = win > 0 ? m->tables : nullptr;
+    v.accessPolicyWindow.num_bytes = win;
+    v.accessPolicyWindow.hitRatio = win > 0 ? static_cast<float>(std::min(1.0, double(carve) / double(win))) : 0.f;
+    v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    REC_CUDA(cudaStreamSetAttribute(w.stream, cudaStreamAttributeAccessPolicyWindow, &v));
+  }
+  m->hot_window = static_cast<int64_t>(win);
+  return REC_OK;
+}
+
+// Re-derive every staging slot's kernel arguments and re-capture its graphs (graph kernel
+// nodes keep the stream attributes of their capture, e.g. the L2 window).
+static rec_status recapture(rec_model_s* m) {
+  for (auto& w : m->ws) {
+    REC_CUDA(cudaStreamSynchronize(w.stream));
+    for (auto& sl : w.slots) {
+      fill_genargs(m, w, sl.ga, sl.sa, nullptr);
+      for (auto& V : sl.var) {
+        if (V.exec) cudaGraphExecDestroy(V.exec);
+        if (V.graph) cudaGraphDestroy(V.graph);
+        V = SynthSlot::Variant{};
+      }
+    }
+    rec_status st = capture_graphs(m, w);
+    if (st != REC_OK) return st;
+  }
+  return REC_OK;
+}
+
+rec_status rec_hot_remap(rec_model_t m, const int32_t* indices, const int32_t* offsets, int32_t batch,
+                         int64_t window_bytes, int64_t* hot_rows) {
+  if (!m || !indices || !offsets || batch < 1) {
+    set_error("model, indices, offsets and batch >= 1 are required");
+    return REC_E_INVALID_ARG;
+  }
+  if (m->world > 1 && m->shard != REC_SHARD_REPLICA) {
+    set_error("rec_hot_remap: replicated models only");
+    return REC_E_UNSUPPORTED;
+  }
+  if (!m->interleaved) {
+    set_error("rec_hot_remap needs equal rows per table (interleaved arena: the hot rows of all "
+              "tables form one prefix)");
+    return REC_E_UNSUPPORTED;
+  }
+  if (!m->pipe.empty()) {
+    set_error("rec_hot_remap: remove the pipeline lanes first (rec_set_pipeline(m, 0))");
+    return REC_E_INVALID_ARG;
+  }
+  REC_CUDA(cudaSetDevice(m->device));
+  REC_CUDA(cudaDeviceSynchronize());
+  const int T = m->T, D = m->D;
+  // 1. access-frequency profile of the sample (host copy of the caller's arrays)
+  const int nb = T * batch;
+  std::vector<int32_t> off(nb + 1);
+  REC_CUDA(cudaMemcpy(off.data(), offsets, sizeof(int32_t) * (nb + 1), cudaMemcpyDefault));
+  for (int g = 0; g < nb; ++g)
+    if (off[0] != 0 || off[g + 1] < off[g]) {
+      set_error("offsets are not non-decreasing from 0");
+      return REC_E_OFFSETS;
+    }
+  std::vector<int32_t> idx(off[nb]);
+  REC_CUDA(cudaMemcpy(idx.data(), indices, sizeof(int32_t) * idx.size(), cudaMemcpyDefault));
+  std::vector<int64_t> roff(T + 1, 0);
+  for (int t = 0; t < T; ++t) roff[t + 1] = roff[t] + m->rows[t];
+  std::vector<uint32_t> cnt(roff[T], 0);
+  for (int t = 0; t < T; ++t)
+    for (int64_t j = off[t * batch]; j < off[(t + 1) * batch]; ++j) {
+      const int32_t r = idx[j];
+      if (r < 0 || r >= m->rows[t]) {
+        set_error("profile index %d of table %d outside [0, %lld)", r, t, (long long)m->rows[t]);
+        return REC_E_INDEX_OOB;
+      }
+      ++cnt[roff[t] + r];
+    }
+  // 2. per table: rows by descending count (ties by row id) -> arena position
+  std::vector<int32_t> inv(roff[T]), remap(roff[T]);
+  for (int t = 0; t < T; ++t) {
+    int32_t* iv = inv.data() + roff[t];
+    for (int64_t r = 0; r < m->rows[t]; ++r) iv[r] = static_cast<int32_t>(r);
+    const uint32_t* c = cnt.data() + roff[t];
+    std::stable_sort(iv, iv + m->rows[t], [c](int32_t a, int32_t b) { return c[a] > c[b]; });
+    for (int64_t p = 0; p < m->rows[t]; ++p) remap[roff[t] + iv[p]] = static_cast<int32_t>(p);
+  }
+  // 3. regenerate the tables in id order and permute them into the arena
+  int* d_inv = nullptr;
+  float* tmp = nullptr;
+  if (!m->d_remap) {
+    REC_CUDA(cudaMalloc(reinterpret_cast<void**>(&m->d_remap), sizeof(int32_t) * roff[T]));
+    REC_CUDA(cudaMalloc(reinterpret_cast<void**>(&m->d_remap_off), sizeof(int64_t) * T));
+  }
+  REC_CUDA(cudaMemcpy(m->d_remap, remap.data(), sizeof(int32_t) * roff[T], cudaMemcpyHostToDevice));
+  REC_CUDA(cudaMemcpy(m->d_remap_off, roff.data(), sizeof(int64_t) * T, cudaMemcpyHostToDevice));
+  if (cudaMalloc(reinterpret_cast<void**>(&d_inv), sizeof(int32_t) * roff[T]) != cudaSuccess ||
+      cudaMalloc(reinterpret_cast<void**>(&tmp), m->table_bytes) != cudaSuccess) {
+    cudaFree(d_inv);
+    set_error("rec_hot_remap: no device memory for the permutation");
+    return REC_E_OOM;
+  }
+  REC_CUDA(cudaMemcpy(d_inv, inv.data(), sizeof(int32_t) * roff[T], cudaMemcpyHostToDevice));
+  int64_t maxr = 0;
+  for (int t = 0; t < T; ++t) {
+    maxr = std::max(maxr, m->rows[t]);
+    launch_init_table(tmp + m->tab_off[t], m->rows[t], D, m->row_stride, m->t0 + t, m->k0, m->k1,
+                      m->emb_shift, m->value_mode, 0, 0);
+  }
+  launch_permute_rows(tmp, m->tables, m->d_tab_off, m->row_stride, m->d_rows, T, D, d_inv,
+                      m->d_remap_off, maxr, 0);
+  cudaError_t e = cudaDeviceSynchronize();
+  cudaFree(tmp);
+  cudaFree(d_inv);
+  if (e != cudaSuccess) return cuda_fail(e, "rec_hot_remap permute");
+  // 4. persisting L2 window over the hot prefix: capacity / co-located models
+  size_t win = 0;
+  if (window_bytes > 0) {
+    win = static_cast<size_t>(window_bytes);
+  } else if (window_bytes == 0) {
+    cudaDeviceProp prop;
+    REC_CUDA(cudaGetDeviceProperties(&prop, m->device));
+    int models = 1;
+    {
+      std::lock_guard<std::mutex> g(g_reg_mu);
+      models = std::max(1, g_models_on[m->device & 63]);
+    }
+    win = static_cast<size_t>(prop.persistingL2CacheMaxSize) / models;
+  }
+  rec_status st = set_l2_window(m, win);
+  if (st != REC_OK) return st;
+  st = recapture(m);
+  if (st != REC_OK) return st;
+  if (hot_rows) *hot_rows = m->hot_window / (static_cast<int64_t>(T) * D * 4);
+  return REC_OK;
 }
 
 rec_status rec_query_inspect(rec_model_t m, const float* dense, const int32_t* indices,
@@ -1691,11 +1863,25 @@ rec_status rec_query_async(rec_model_t m, int32_t slot, const float* dense, cons
     d_off = w.offsets;
   }
   if (!idx_dev) {
-    REC_CUDA(cudaMemcpyAsync(w.indices, indices, sizeof(int) * nnz, cudaMemcpyHostToDevice, s));
+    // table-wise sharded with host offsets: only this rank's tables' indices cross PCIe (the
+    // range [offsets[t0 B], offsets[(t0 + T_loc) B]) of the table-major CSR, same positions)
+    int64_t i0 = 0, i1 = nnz;
+    if (sharded && !off_dev) {
+      i0 = offsets[static_cast<int64_t>(m->t0) * batch];
+      i1 = offsets[static_cast<int64_t>(m->t0 + m->T_loc) * batch];
+    }
+    REC_CUDA(cudaMemcpyAsync(w.indices + i0, indices + i0, sizeof(int) * (i1 - i0), cudaMemcpyHostToDevice, s));
     d_idx = w.indices;
   }
   if (m->F > 0 && !is_device_ptr(dense)) {
-    REC_CUDA(cudaMemcpyAsync(w.dense_f32, dense, sizeof(float) * batch * m->F, cudaMemcpyHostToDevice, s));
+    int64_t r0 = 0, r1 = batch;  // sharded: only this rank's item block of the dense rows
+    if (sharded) {
+      const int Bq = (batch + m->world - 1) / m->world;
+      r0 = std::min<int64_t>(batch, static_cast<int64_t>(m->rank) * Bq);
+      r1 = std::min<int64_t>(batch, r0 + Bq);
+    }
+    REC_CUDA(cudaMemcpyAsync(w.dense_f32 + r0 * m->F, dense + r0 * m->F, sizeof(float) * (r1 - r0) * m->F,
+                             cudaMemcpyHostToDevice, s));
     d_dense = w.dense_f32;
   }
   const bool ctr_dev = is_device_ptr(ctr);

@@ -140,6 +140,12 @@ struct rec_model_s {
   uint32_t k0 = 0, k1 = 0;
   int emb_shift = 0;
   int64_t l2_persist_bytes = 0;
+  // hot-row partition (rec_hot_remap): old row -> arena row per
+  // table (concatenated, offsets remap_off), the L2 persisting window it set (bytes, 0 = none)
+  int* d_remap = nullptr;
+  int64_t* d_remap_off = nullptr;
+  int64_t hot_window = 0;
+  bool counted = false;                // counted in the per-device co-located model registry
   // embedding arena
   float* tables = nullptr;
   size_t table_bytes = 0;

@@ -359,14 +359,20 @@ static rec_status serve_sharded(rec_model_s* m, const rec_trace_row* trace, int6
   for (int64_t p = 0; p < n; ++p) remaining[p] = (trace[p].size + d - 1) / d;
   std::vector<double> done_t(n, NAN), release(n), disp_t(n, NAN);
   for (int64_t p = 0; p < n; ++p) release[p] = trace[p].arrival_s;
-  std::vector<int64_t> slot_batch(M, -1);
+  // depth 2: a slot's next batch waits in its stream behind the running one, so a slot never
+  // idles between a completion and the host's next submit (REC_SERVE_DEPTH overrides; the
+  // CTR read-back staging is per slot, so depth 1 when CTRs are returned)
+  int depth = 2;
+  if (const char* e = getenv("REC_SERVE_DEPTH")) depth = std::max(1, std::min(4, atoi(e)));
+  if (ctr_out) depth = 1;
+  std::vector<std::deque<std::pair<int64_t, uint32_t>>> pend(M);
   std::vector<uint32_t> seq(M, 0);
   std::vector<int32_t> segs;
   int64_t completed = 0, logged = 0;
   const double t_first = trace[0].arrival_s;
   const double t0 = now_s() - t_first;
   auto finish = [&](int s) {
-    const int64_t k = slot_batch[s];
+    const int64_t k = pend[s].front().first;
     const double tc = now_s() - t0;
     for (int64_t c = bt[k].c0; c < bt[k].c0 + bt[k].nc; ++c)
       if (--remaining[ch[c].pos] == 0) {
@@ -380,17 +386,18 @@ static rec_status serve_sharded(rec_model_s* m, const rec_trace_row* trace, int6
         row += ch[c].len;
       }
     }
-    slot_batch[s] = -1;
+    pend[s].pop_front();
   };
   auto poll = [&]() {
     for (int s = 0; s < M; ++s)
-      if (slot_batch[s] >= 0 &&
-          static_cast<int32_t>(*reinterpret_cast<volatile uint32_t*>(lanes[s].flag_host) - seq[s]) >= 0)
+      while (!pend[s].empty() &&
+             static_cast<int32_t>(*reinterpret_cast<volatile uint32_t*>(lanes[s].flag_host) -
+                                  pend[s].front().second) >= 0)
         finish(s);
   };
   for (int64_t k = 0; k < nb; ++k) {
     const int s = static_cast<int>(k % M);
-    while (slot_batch[s] >= 0 || now_s() - t0 < bt[k].close) {
+    while (static_cast<int>(pend[s].size()) >= depth || now_s() - t0 < bt[k].close) {
       poll();
       cpu_relax();
     }
@@ -420,13 +427,13 @@ static rec_status serve_sharded(rec_model_s* m, const rec_trace_row* trace, int6
     if (st == REC_OK) st = stream_write_u32(w.stream, lanes[s].flag_dev, ++seq[s]);
     if (st != REC_OK) { cleanup(); return st; }
     for (int64_t c = bt[k].c0; c < bt[k].c0 + bt[k].nc; ++c) disp_t[ch[c].pos] = td;
-    slot_batch[s] = k;
+    pend[s].emplace_back(k, seq[s]);
   }
   bool any = true;
   while (any) {
     poll();
     any = false;
-    for (int s = 0; s < M; ++s) any = any || slot_batch[s] >= 0;
+    for (int s = 0; s < M; ++s) any = any || !pend[s].empty();
     if (any) cpu_relax();
   }
   for (int s = 0; s < M; ++s) {

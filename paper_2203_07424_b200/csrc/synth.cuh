@@ -25,11 +25,41 @@ __device__ __forceinline__ int2 row_item(const SegBatch& sb, int b) {
   return make_int2(sg.x, sg.y + (b - sg.w));
 }
 
+// ------------------------------------------------------------ Zipf(0.9) rows (G2z)
+// Continuous inverse CDF of Zipf(0.9) from exactly rounded fp64 operations only (__dmul_rn /
+// __dadd_rn are never contracted into FMAs), so the rows are bit-identical to oracle/gen.py:
+// c = largest double with (c^10) <= R (60 bisection steps), x = 1 + u (c - 1), y = x^10,
+// rank = min(floor(y) - 1, R - 1), row = (rank * 2654435761 + 7919 t) mod R.
+__device__ __forceinline__ double pow10_rn(double x) {
+  const double x2 = __dmul_rn(x, x), x4 = __dmul_rn(x2, x2), x8 = __dmul_rn(x4, x4);
+  return __dmul_rn(x8, x2);
+}
+__device__ inline double zipf_c(uint64_t R) {
+  double lo = 1.0, hi = 16.0;
+  const double Rd = static_cast<double>(R);
+  for (int i = 0; i < 60; ++i) {
+    const double mid = __dmul_rn(__dadd_rn(lo, hi), 0.5);
+    if (pow10_rn(mid) <= Rd) lo = mid;
+    else hi = mid;
+  }
+  return lo;
+}
+__device__ __forceinline__ int zipf_row(uint64_t r, uint64_t R, double zc, uint32_t t) {
+  const double u = __dmul_rn(static_cast<double>(r >> 11), 0x1p-53);
+  const double x = __dadd_rn(1.0, __dmul_rn(u, __dadd_rn(zc, -1.0)));
+  uint64_t rank = static_cast<uint64_t>(floor(pow10_rn(x))) - 1;  // x >= 1: floor >= 1
+  if (rank > R - 1) rank = R - 1;
+  return static_cast<int>((rank * 2654435761ull + 7919ull * t) % R);
+}
+
 // ---------------------------------------------------------------------- indices (G2)
+// zc: zipf_c(R) of the table (index_dist 3 only; computed once per thread by the caller).
 __device__ __forceinline__ int gen_index(uint32_t j, uint32_t it, uint32_t c2, uint32_t q,
-                                         uint32_t k0, uint32_t k1, uint64_t R, int index_dist) {
+                                         uint32_t k0, uint32_t k1, uint64_t R, int index_dist,
+                                         double zc = 0.0) {
   const U4 w = philox(j, it, c2, q, k0, k1);
   uint64_t r = (static_cast<uint64_t>(w.y) << 32) | w.x;
+  if (index_dist == 3) return zipf_row(r, R, zc, c2 >> 8);
   if (index_dist == 2) r = __umul64hi(r, (static_cast<uint64_t>(w.w) << 32) | w.z);
   return static_cast<int>(__umul64hi(r, R));
 }

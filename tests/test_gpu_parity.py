@@ -45,6 +45,9 @@ CASES = [
     ("rmc3", W.small_variant(W.RMC3, 20000), 257),
     ("rmc1_var", W.small_variant(W.RMC1, 20000).with_(pooling_lo=20, pooling_hi=160), 129),
     ("rmc1_skew", W.small_variant(W.RMC1, 20000).with_(index_dist=W.INDEX_SKEW2), 64),
+    ("rmc1_zipf", W.small_variant(W.RMC1, 20000).with_(index_dist=W.INDEX_ZIPF), 129),
+    ("rmc1_zipf_var", W.small_variant(W.RMC1, 20000).with_(index_dist=W.INDEX_ZIPF, pooling_lo=20,
+                                                          pooling_hi=160), 65),
     ("rmc1_fp32", W.small_variant(W.RMC1, 20000).with_(value_mode=W.REC_VALUES_FP32), 150),
     ("one_hot", W.small_variant(W.TINY, 5000).with_(pooling_lo=1, pooling_hi=1), 77),
 ]

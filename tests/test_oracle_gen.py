@@ -121,3 +121,60 @@ def test_skewed_indices_are_skewed():
 
 def test_emb_shift_values():
     assert gen.emb_shift(80, 80) == 2 and gen.emb_shift(20, 20) == 1 and gen.emb_shift(120, 120) == 3
+
+
+# ----------------------------------------------------------------- Zipf(0.9) rows (G2z)
+def test_zipf_pow10_and_bisection_constant():
+    # pow10 is x^10 up to the rounding of four multiplications; c is the largest double with
+    # pow10(c) <= R (the next double up exceeds R), so every rank is < R
+    for R in (7, 1000, 20000, 1_000_000, (1 << 31) - 1):
+        c = gen.zipf_c(R)
+        assert gen.pow10(c) <= R < gen.pow10(np.nextafter(c, np.inf))
+        assert abs(c - R ** 0.1) <= 1e-12 * R ** 0.1
+    x = np.linspace(1.0, 8.0, 1001)
+    assert np.allclose(gen.pow10(x), x ** 10, rtol=1e-15, atol=0)
+
+
+def test_zipf_rank_cdf_closed_form():
+    # P(rank <= k - 1) = P(x^10 < k + 1) = ((k + 1)^0.1 - 1) / (c - 1): a Zipf law with
+    # exponent 0.9 (density of y = x^10 is proportional to y^-0.9); 2e5 draws, 5-sigma bounds
+    R = 1_000_000
+    rng = np.random.default_rng(4)
+    r = rng.integers(0, 1 << 63, size=200_000, dtype=np.uint64) * np.uint64(2) + rng.integers(0, 2, size=200_000, dtype=np.uint64)
+    rank = gen.zipf_rank(r, R)
+    assert rank.min() >= 0 and rank.max() <= R - 1
+    c = gen.zipf_c(R)
+    for k in (1, 10, 100, 10_000, 100_000, 999_999):
+        p = min(1.0, ((k + 1) ** 0.1 - 1.0) / (c - 1.0))
+        emp = np.mean(rank <= k - 1)
+        assert abs(emp - p) <= 5 * np.sqrt(p * (1 - p) / r.size) + 1e-12, (k, emp, p)
+    # the hottest 10 % of rows take ~72 % of the accesses (closed form 0.7247)
+    assert abs(np.mean(rank < R // 10) - ((R // 10) ** 0.1 - 1) / (c - 1)) < 0.01
+
+
+def test_zipf_rows_bijection_and_generator_counters():
+    R = 1000
+    ranks = np.arange(R, dtype=np.uint64)
+    for t in (0, 3):
+        rows = ((ranks * np.uint64(gen.ZIPF_MULT) + np.uint64(gen.ZIPF_T_OFF * t)) % np.uint64(R))
+        assert np.unique(rows).size == R                      # a permutation of the rows
+    # bag_indices with index_dist 3 follows G2's counters, then the G2z map (scalar rebuild)
+    cfg = W.TINY.with_(rows=5000, index_dist=W.INDEX_ZIPF)
+    segs = W.random_segments(20, seed=8)
+    q, it = gen.expand_segments(segs)
+    lens = gen.bag_lengths(11, cfg, q, it)
+    k0, k1 = ph.seed_key(11)
+    c = gen.zipf_c(5000)
+    for t in (0, 6):
+        idx = gen.bag_indices(11, cfg, t, q, it, lens[t], 5000)
+        pos = 0
+        for b in range(q.size):
+            for j in range(int(lens[t, b])):
+                w = ph.philox_scalar([j, int(it[b]), (t << 8) | 1, int(q[b])], [k0, k1])
+                r = (w[1] << 32) | w[0]
+                u = float(r >> 11) * 2.0 ** -53
+                rank = min(int(np.floor((1.0 + u * (c - 1.0)) ** 10)) - 1, 4999)  # pow: +-1 ulp
+                rk = int(gen.zipf_rank(np.array([r], np.uint64), 5000)[0])
+                assert abs(rk - rank) <= 1
+                assert idx[pos] == (rk * gen.ZIPF_MULT + gen.ZIPF_T_OFF * t) % 5000
+                pos += 1

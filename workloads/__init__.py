@@ -22,6 +22,7 @@ REC_VALUES_FP32 = 1
 
 INDEX_UNIFORM = 0
 INDEX_SKEW2 = 2
+INDEX_ZIPF = 3   # Zipf(0.9) rows scattered by a fixed bijection (G2z)
 
 ARCH_DLRM = 0    # SLS -> bottom MLP -> dot interaction -> top MLP (Table I rows 1-3)
 ARCH_MTWND = 1   # one-hot lookups -> concat -> N task towers + wide part (Table I row 4; R26-R29)
@@ -167,5 +168,5 @@ __all__ = [
     "ModelConfig", "TINY", "RMC1", "RMC2", "RMC3", "MTWND", "CONFIGS", "SHORT", "small_variant",
     "ARCH_DLRM", "ARCH_MTWND",
     "TRACE_DTYPE", "query_sizes", "poisson_trace", "burst_trace", "random_segments",
-    "REC_VALUES_INT8_EXACT", "REC_VALUES_FP32", "INDEX_UNIFORM", "INDEX_SKEW2",
+    "REC_VALUES_INT8_EXACT", "REC_VALUES_FP32", "INDEX_UNIFORM", "INDEX_SKEW2", "INDEX_ZIPF",
 ]
