@@ -367,6 +367,14 @@ def saturation(model, cfg, d, m_streams, steps, warmup, step_batches, n_queries,
             "timed_batches": nbt, "value": float(t[2]) / (ms_max * 1e-3)}
 
 
+def default_streams(args, name: str) -> int:
+    """Co-located streams m for the saturation step: --streams, or per workload
+    (profiles/r02/ab_*.txt: RMC3 16 -> 32 streams +16 %; RMC1 / RMC2 flat from 16)."""
+    if not getattr(args, "streams_auto", False) and args.streams > 0:
+        return args.streams
+    return 32 if name == "rmc3" else 16
+
+
 def per_model(name, args, rank, world, dist, local, hbm_peak):
     """The metric is per model (BASELINE.json: "SLA-bounded QPS (p95) per model at 1/2/4/8
     B200"): saturation QPS (the same step definition at fewer steps), the SLS roofline of
@@ -375,7 +383,7 @@ def per_model(name, args, rank, world, dist, local, hbm_peak):
     import torch
     from paper_2203_07424_b200 import RecModel
     cfg = W.SHORT[name]
-    d, m_streams = 1024, args.streams
+    d, m_streams = 1024, default_streams(args, name)
     model = RecModel(cfg, seed=1, max_batch=d, streams=m_streams, device=local)
     clk = ClockSampler(local).__enter__()
     sat = saturation(model, cfg, d, m_streams, args.pm_steps, 2, args.pm_step_batches,
@@ -422,7 +430,7 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     cfg = W.SHORT[args.config]
     d = args.batch
-    m_streams = args.streams
+    m_streams = default_streams(args, args.config)
     l2p = int(args.l2_persist_mb) << 20
     model = RecModel(cfg, seed=1, max_batch=d, streams=m_streams, device=local, l2_persist_bytes=l2p)
     dev = torch.device("cuda", local)
@@ -552,7 +560,7 @@ def run_ours(args):
                 lam_hint[0] = lam
             return lam
 
-        ms = [x for x in (1, 2, 4, 8, 16) if x <= m_streams]
+        ms = [x for x in (1, 2, 4, 8, 16, 32) if x <= m_streams]
         # the policy's maximum fusion batch d ("maximum batch sizes fusing queries",
         # bounded only by the SLA); RMC1's BASELINE config fixes 256-1024 (reading R30)
         d_max = args.max_batch_search or SEARCH_D_MAX.get(cfg.name, 4096)
@@ -726,7 +734,7 @@ def run_sharded(args):
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     cfg = W.SHORT[args.config]
     d = args.batch
-    m_streams = args.streams
+    m_streams = default_streams(args, args.config)
     t = torch.zeros(128, dtype=torch.uint8, device="cuda")
     if rank == 0:
         t.copy_(torch.frombuffer(bytearray(nccl_unique_id()), dtype=torch.uint8))
@@ -839,7 +847,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="rmc1", choices=list(W.SHORT))
     ap.add_argument("--batch", type=int, default=1024)
-    ap.add_argument("--streams", type=int, default=16)
+    ap.add_argument("--streams", type=int, default=0,
+                    help="co-located streams m (0 = per workload: 32 for RMC3, whose dense chain "
+                         "is latency-bound (16 -> 32: +16 %), else 16)")
     ap.add_argument("--submit", default="batch", choices=["batch", "python"])
     ap.add_argument("--shard", default="replica", choices=["replica", "table", "row"],
                     help="N > 1: model-parallel embedding sharding instead of replicas")
@@ -866,6 +876,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    args.streams_auto = args.streams == 0
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         # one process per GPU: re-launch this command under torch.distributed.run
         import socket

@@ -426,11 +426,13 @@ static void launch_group_bn(const GemmGroup& g, cudaStream_t s) {
 
 template <int BN, int MT>
 static void launch_bn(const CUtensorMap* ta, const CUtensorMap* tw, const GemmArgs& a,
-                      cudaStream_t s) {
+                      cudaStream_t s, bool deep = false) {
   constexpr int STAGE = MT * A_STAGE_BYTES + BN * BK * 2;
   constexpr int SMAX = (MT == 1 ? 4 : 3);
   const int nkb = (a.K + BK - 1) / BK;
-  const int smax = ring_depth(SMAX, ((a.N + BN - 1) / BN) * ((a.M + BM * MT - 1) / (BM * MT)));
+  const int smax = deep && g_gemm_stages == 0
+                       ? SMAX
+                       : ring_depth(SMAX, ((a.N + BN - 1) / BN) * ((a.M + BM * MT - 1) / (BM * MT)));
   const int stages = nkb < smax ? (nkb < 1 ? 1 : nkb) : smax;
   const size_t smem = static_cast<size_t>(stages) * STAGE + 1024 + 256;
   dim3 grid((a.N + BN - 1) / BN, (a.M + BM * MT - 1) / (BM * MT));
@@ -462,10 +464,27 @@ void gemm_prepare() {
 int g_gemm_2sm = 0;     // REC_GEMM_2SM: CTA-pair GEMM for full-GPU launches (experimental)
 int g_gemm_mt1 = 0;     // REC_GEMM_MT1=1: 128x256 tiles (one M tile per CTA) for full-GPU launches too (A/B)
 int g_gemm_narrow = 0;  // REC_GEMM_NARROW=n: 128-wide N tiles below n 128x256 tiles (measured: RMC2/3 +0.5-1 %, MT-WnD -7 %)
+int g_gemm_bn64 = 0;    // REC_GEMM_BN64=1: 64-wide serving tiles (below; measured: RMC3 -4 % at 16
+                        // co-located streams, -11 % at 32, RMC2 +2 %: off by default)
 
 void launch_gemm_tc(const CUtensorMap* tmap_a, const CUtensorMap* tmap_w, const GemmArgs& a,
-                    cudaStream_t s, const CUtensorMap* tmap_w_half) {
+                    cudaStream_t s, const CUtensorMap* tmap_w_half, const CUtensorMap* tmap_w64) {
   if (a.M <= 0) return;
+  // Serving-batch launch of a wide, deep layer (e.g. RMC3's 2560 -> 512 at B <= 1024): with
+  // 128 x 256 tiles it runs 16 CTAs whose 2-stage rings keep ~1.5 MB in flight, so the layer
+  // is bound by bytes in flight x L2 latency (~25 us).  64-wide N tiles give 4x the CTAs and,
+  // at the same shared memory per CTA (4 stages x 24 KB), twice the k-blocks in flight each.
+  // (Measured: the single-stream GEMM time of an RMC3 batch drops 70 -> 65 us, but the extra
+  // CTAs and deeper rings cost the co-running kernels more, see g_gemm_bn64.)
+  // Every output element still accumulates over K in the same order, so the bits do not
+  // depend on the tiling (batch invariance; tests/test_gpu_variants.py).  The width-1 CTR
+  // epilogue needs whole rows, so CTR layers keep their tiles.
+  const int m_tiles = (a.M + BM - 1) / BM;
+  if (g_gemm_bn64 && tmap_w64 && a.mode != GEMM_OUT_CTR && a.N >= 128 && a.K >= 512 &&
+      m_tiles * ((a.N + 255) / 256) < 74 && m_tiles * ((a.N + 63) / 64) <= 148) {
+    launch_bn<64, 1>(tmap_a, tmap_w64, a, s, true);
+    return;
+  }
   if (a.N <= 32) launch_bn<32, 1>(tmap_a, tmap_w, a, s);
   else if (a.N <= 64) launch_bn<64, 1>(tmap_a, tmap_w, a, s);
   else if (a.N <= 128) launch_bn<128, 1>(tmap_a, tmap_w, a, s);

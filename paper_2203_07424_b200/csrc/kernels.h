@@ -187,9 +187,12 @@ void launch_gemm_group(const GemmGroup& g, cudaStream_t s);
 int gemm_bn(int N);                  // tile width used for a layer of width N (W tmap box)
 void gemm_prepare();                 // per-device one-time kernel attributes
 // tmap_w_half (optional): the same weights with a 128-row box, enabling the CTA-pair kernel.
+// tmap_w64 (optional): 64-row box, enabling 64-wide N tiles for few-CTA serving launches.
 void launch_gemm_tc(const CUtensorMap* tmap_a, const CUtensorMap* tmap_w, const GemmArgs& a,
-                    cudaStream_t s, const CUtensorMap* tmap_w_half = nullptr);
+                    cudaStream_t s, const CUtensorMap* tmap_w_half = nullptr,
+                    const CUtensorMap* tmap_w64 = nullptr);
 extern int g_gemm_2sm;
+extern int g_gemm_bn64;
 extern int g_gemm_narrow;
 // Encode a 2D bf16 K-major tensor map [rows][K] (row pitch ldk elements) with a
 // 64 x box_rows box and 128-byte swizzle.  Returns false on failure.

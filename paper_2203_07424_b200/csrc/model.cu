@@ -221,7 +221,7 @@ void enqueue_bottom(rec_model_s* m, Workspace& w, cudaStream_t st, int B, const 
       a.ldo = L.Npad;
     }
     cudaEvent_t e = gev ? nullptr : prof_begin(m, st);
-    launch_gemm_tc(&w.tmap_a_bottom[l], &L.tmap_w, a, st, &L.tmap_w128);
+    launch_gemm_tc(&w.tmap_a_bottom[l], &L.tmap_w, a, st, &L.tmap_w128, &L.tmap_w64);
     prof_end(m, st, 1, e);
   }
   m->launches += nb;
@@ -331,7 +331,7 @@ void enqueue_interact_top(rec_model_s* m, Workspace& w, cudaStream_t st, int B, 
       a.ldo = L.Npad;
     }
     cudaEvent_t e = gev ? nullptr : prof_begin(m, st);
-    launch_gemm_tc(&w.tmap_a_top[j], &L.tmap_w, a, st, &L.tmap_w128);
+    launch_gemm_tc(&w.tmap_a_top[j], &L.tmap_w, a, st, &L.tmap_w128, &L.tmap_w64);
     prof_end(m, st, 1, e);
   }
   mark(gev, 5, st);
@@ -638,6 +638,7 @@ rec_status synth_submit(rec_model_s* m, Workspace& w, const int32_t* segs, int n
   }
   const double t0 = host_now_ns();
   SynthSlot& sl = w.slots[w.next_slot];
+  w.last_slot = w.next_slot;
   w.next_slot = (w.next_slot + 1) % static_cast<int>(w.slots.size());
   REC_CUDA(cudaEventSynchronize(sl.free));
   collect_slot(m, sl);
@@ -667,7 +668,7 @@ rec_status synth_submit(rec_model_s* m, Workspace& w, const int32_t* segs, int n
   } else if (nseg > kParamSegs) {
     REC_CUDA(cudaEventRecord(w.pin_free, w.stream));
   }
-  SynthSlot::Variant& V = sl.var[m->prof ? 1 : 0];
+  SynthSlot::Variant& V = sl.var[(m->prof || m->serve_events) && sl.var[1].exec ? 1 : 0];
   const bool direct = dense_f32_out != nullptr || !V.exec;
   if (!direct) {
     const bool fused = m->lo == m->hi;
@@ -1266,6 +1267,7 @@ rec_status rec_model_create(const rec_model_desc* d, rec_model_t* out) {
     g_gemm_2sm = env_int("REC_GEMM_2SM", 0);
     g_gemm_narrow = env_int("REC_GEMM_NARROW", 0);
     g_gemm_mt1 = env_int("REC_GEMM_MT1", 0);
+    g_gemm_bn64 = env_int("REC_GEMM_BN64", 0);
     g_interact_wpc = std::max(1, std::min(8, env_int("REC_INTERACT_WPC", 8)));
     g_interact_pf = env_int("REC_INTERACT_PF", 0);
     {
@@ -1307,6 +1309,10 @@ rec_status rec_model_create(const rec_model_desc* d, rec_model_t* out) {
       return REC_E_OOM;
     }
     launch_init_layer(L.W, L.bias, N, K, L.Kpad, layer_id, L.exp, m->k0, m->k1, 0);
+    if (!encode_tmap_bf16(&L.tmap_w64, L.W, N, K, L.Kpad, std::min(L.bn, 64))) {
+      set_error("cuTensorMapEncodeTiled failed for layer %d weights", layer_id);
+      return REC_E_CUDA;
+    }
     if (!encode_tmap_bf16(&L.tmap_w128, L.W, N, K, L.Kpad, std::min(L.bn, 128))) {
       set_error("cuTensorMapEncodeTiled failed for layer %d weights", layer_id);
       return REC_E_CUDA;

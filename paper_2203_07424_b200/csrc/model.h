@@ -30,6 +30,7 @@ struct Layer {
   float* bias = nullptr;                         // [N]
   CUtensorMap tmap_w;
   CUtensorMap tmap_w128;                         // box rows min(bn, 128) (fused MLP, 128-row chunks)
+  CUtensorMap tmap_w64;                          // box rows min(bn, 64) (64-wide serving tiles)
 };
 
 // A staging slot of device-synthesised batches: the batch descriptor (kernel parameters of
@@ -98,6 +99,7 @@ struct Workspace {
   // model's IPC-exported exchange arena (x_external: not freed separately); the P2P argument
   // sets of its chain (SLS stores + flags, flag wait, CTR all-gather, CTR-flag wait), the
   // gathered CTRs of the whole batch, and the slot's epoch counter
+  int last_slot = -1;                // staging slot of the last synth_submit (its stage events)
   bool x_external = false;
   P2PArgs sh_sls{}, sh_wait{}, sh_ctr{}, sh_ctrwait{};
   float* sh_ctr_gather = nullptr;    // [G * Bq] CTRs of every rank's block (items 0..B-1)
@@ -146,6 +148,7 @@ struct rec_model_s {
   int64_t* d_remap_off = nullptr;
   int64_t hot_window = 0;
   bool counted = false;                // counted in the per-device co-located model registry
+  bool serve_events = false;           // rec_serve: synthetic graphs with stage events (breakdown)
   // embedding arena
   float* tables = nullptr;
   size_t table_bytes = 0;

@@ -73,6 +73,8 @@ struct Batch {
   int stream = -1;
   int64_t first_chunk = 0, nchunks = 0, items = 0;
   double t_dispatch = 0, t_done = 0;
+  int slot = -1;            // staging slot whose graph (with stage events) ran the batch
+  double host_in_ms = 0;    // host-input mode: packing into pinned staging (host clock)
 };
 
 // Per-stream state of the serving loop.
@@ -83,7 +85,27 @@ struct Lane {
   float* ctr_host = nullptr;       // pinned [cap]
   uint32_t* flag_host = nullptr;   // pinned + mapped: batch sequence number written by the GPU
   CUdeviceptr flag_dev = 0;
+  cudaEvent_t hev[8] = {};         // host-input mode: stage events of the lane's batch
 };
+
+// Stage times of a finished batch (P:418 latency components), ms: [0] input (H2D / pack),
+// [1] sparse (SLS incl. fused index generation), [2] dense (chain device time not in the SLS:
+// the bottom branch beyond the SLS, interaction, top MLP).  ev: the stage events of forward_
+// enqueue / synth_chain (0 start, 1 inputs done, 2 SLS done, 5 top done).
+static void stage_times(const cudaEvent_t* ev, double host_in_ms, double out[3]) {
+  auto el = [&](int a, int b) {
+    float x = 0.f;
+    if (!ev[a] || !ev[b] || cudaEventElapsedTime(&x, ev[a], ev[b]) != cudaSuccess) {
+      cudaGetLastError();
+      return 0.0;
+    }
+    return static_cast<double>(x);
+  };
+  const double in = el(0, 1), sp = el(1, 2), all = el(0, 5);
+  out[0] = in + host_in_ms;
+  out[1] = sp;
+  out[2] = std::max(0.0, all - in - sp);
+}
 
 // cuStreamWriteValue32 through the runtime's driver entry point (no libcuda link).
 static rec_status stream_write_u32(cudaStream_t s, CUdeviceptr addr, uint32_t v) {
@@ -209,11 +231,12 @@ static rec_status host_input_enqueue(rec_model_s* m, Workspace& w, const HostInp
 static void fill_report(const rec_trace_row* trace, int64_t n, double sla_ms, double warmup_frac,
                         const std::vector<double>& release, const std::vector<double>& disp_t,
                         const std::vector<double>& done_t, int64_t completed, int64_t nbatches,
-                        double items_tot, double* latency_ms, rec_serve_report* out) {
+                        double items_tot, double* latency_ms, rec_serve_report* out,
+                        const std::vector<double>* comp = nullptr) {
   const double t_first = trace[0].arrival_s, t_last = trace[n - 1].arrival_s;
   const double w_end = t_first + warmup_frac * (t_last - t_first);
   std::vector<double> lat;
-  double sum_lat = 0, sum_q = 0, sum_svc = 0, t_max = t_first;
+  double sum_lat = 0, sum_q = 0, sum_svc = 0, t_max = t_first, sum_c[3] = {0, 0, 0};
   for (int64_t p = 0; p < n; ++p) {
     const double l = done_t[p] - release[p];
     if (latency_ms) latency_ms[p] = l * 1e3;
@@ -223,6 +246,8 @@ static void fill_report(const rec_trace_row* trace, int64_t n, double sla_ms, do
       sum_lat += l * 1e3;
       sum_q += (disp_t[p] - release[p]) * 1e3;
       sum_svc += (done_t[p] - disp_t[p]) * 1e3;
+      if (comp)
+        for (int k = 0; k < 3; ++k) sum_c[k] += comp[k][p];
     }
   }
   std::sort(lat.begin(), lat.end());
@@ -238,7 +263,13 @@ static void fill_report(const rec_trace_row* trace, int64_t n, double sla_ms, do
     out->p99_ms = lat[pct_rank(99, nm) - 1];
     out->mean_ms = sum_lat / nm;
     out->breakdown_ms[0] = sum_q / nm;   // queueing (arrival -> dispatch of last sub-query)
-    out->breakdown_ms[2] = sum_svc / nm; // input + device + completion observation
+    if (comp) {                          // stages of the batch that completed the query
+      out->breakdown_ms[1] = sum_c[0] / nm;  // input (H2D + host packing; 0 device-synth)
+      out->breakdown_ms[2] = sum_c[1] / nm;  // sparse (SLS)
+      out->breakdown_ms[3] = sum_c[2] / nm;  // dense (bottom beyond the SLS, interaction, top)
+    } else {
+      out->breakdown_ms[2] = sum_svc / nm;   // dispatch -> observed completion, undivided
+    }
   }
   out->offered_qps = t_last > t_first ? n / (t_last - t_first) : INFINITY;
   out->achieved_qps = t_max > t_first ? n / (t_max - t_first) : 0;
@@ -561,6 +592,8 @@ rec_status rec_serve(rec_model_t m, const rec_trace_row* trace, int64_t n, doubl
   std::vector<Lane> lanes(M);
   for (int s = 0; s < M; ++s) {
     REC_CUDA(cudaEventCreateWithFlags(&lanes[s].done, cudaEventDisableTiming));
+    if (pol->input_mode == REC_INPUT_HOST)
+      for (auto& e : lanes[s].hev) REC_CUDA(cudaEventCreate(&e));
     if (ctr_out)
       REC_CUDA(cudaMallocHost(reinterpret_cast<void**>(&lanes[s].ctr_host), sizeof(float) * d * m->tasks));
     if (!virt) {  // host-mapped completion word (falls back to event polling if unavailable)
@@ -578,13 +611,21 @@ rec_status rec_serve(rec_model_t m, const rec_trace_row* trace, int64_t n, doubl
       }
     }
   }
+  // latency breakdown: the synthetic graphs with stage events, host-mode lane events
+  const bool synth_events = m->ws[0].slots[0].var[1].exec != nullptr;
+  m->serve_events = synth_events;
   auto cleanup = [&]() {
+    m->serve_events = false;
     for (auto& L : lanes) {
       if (L.done) cudaEventDestroy(L.done);
       if (L.ctr_host) cudaFreeHost(L.ctr_host);
       if (L.flag_host) cudaFreeHost(L.flag_host);
+      for (auto e : L.hev)
+        if (e) cudaEventDestroy(e);
     }
   };
+  std::vector<double> comp[3];
+  for (auto& c : comp) c.assign(n, 0.0);
 
   std::vector<Chunk> fifo;
   fifo.reserve(static_cast<size_t>(n) * 2);
@@ -605,10 +646,14 @@ rec_status rec_serve(rec_model_t m, const rec_trace_row* trace, int64_t n, doubl
   auto finish_batch = [&](int64_t bi, double t_c) {
     Batch& bt = batches[bi];
     bt.t_done = t_c;
+    double st[3] = {0, 0, 0};
+    if (pol->input_mode == REC_INPUT_HOST) stage_times(lanes[bt.stream].hev, bt.host_in_ms, st);
+    else if (synth_events && bt.slot >= 0) stage_times(m->ws[bt.stream].slots[bt.slot].ev, 0.0, st);
     for (int64_t c = bt.first_chunk; c < bt.first_chunk + bt.nchunks; ++c) {
       const Chunk& ch = fifo[c];
       if (--remaining[ch.pos] == 0) {
         done_t[ch.pos] = t_c;
+        for (int k = 0; k < 3; ++k) comp[k][ch.pos] = st[k];
         ++completed;
       }
     }
@@ -639,10 +684,15 @@ rec_status rec_serve(rec_model_t m, const rec_trace_row* trace, int64_t n, doubl
       }
       st = synth_submit(m, w, segbuf.data(), static_cast<int>(k), &B, nullptr);  // a2-a6
       if (st != REC_OK) return st;
+      batches[bi].slot = w.last_slot;
     } else {
+      const double h0 = now_s();
+      REC_CUDA(cudaEventRecord(lanes[s].hev[0], w.stream));
       st = host_input_enqueue(m, w, H, fifo, head, k, &B);
       if (st != REC_OK) return st;
-      st = forward_enqueue(m, w, w.indices, w.offsets, B, nullptr, w.ctr, w.logit, nullptr, w.idx_cap);
+      batches[bi].host_in_ms = (now_s() - h0) * 1e3;
+      REC_CUDA(cudaEventRecord(lanes[s].hev[1], w.stream));
+      st = forward_enqueue(m, w, w.indices, w.offsets, B, nullptr, w.ctr, w.logit, lanes[s].hev, w.idx_cap);
       if (st != REC_OK) return st;
     }
     if (ctr_out)
@@ -747,7 +797,7 @@ rec_status rec_serve(rec_model_t m, const rec_trace_row* trace, int64_t n, doubl
     // and no CTR read-back, whose staging buffer is per stream)
     int depth = 1;
     if (const char* e = getenv("REC_SERVE_DEPTH")) depth = std::max(1, std::min(4, atoi(e)));
-    if (ctr_out || !lanes[0].flag_host) depth = 1;
+    if (ctr_out || !lanes[0].flag_host || pol->input_mode == REC_INPUT_HOST) depth = 1;  // per-lane staging
     auto worker = [&](int tid) {
       cudaSetDevice(m->device);
       std::vector<int32_t> segs_local;
@@ -814,14 +864,22 @@ rec_status rec_serve(rec_model_t m, const rec_trace_row* trace, int64_t n, doubl
           rec_status rs;
           if (pol->input_mode == REC_INPUT_DEVICE_SYNTH) {
             rs = synth_submit(m, w, segs_local.data(), static_cast<int>(k), &B, nullptr);
+            std::lock_guard<std::mutex> g(mu);
+            batches[O.my_batch].slot = w.last_slot;
           } else {
             std::vector<Chunk> local(k);
             {
               std::lock_guard<std::mutex> g(mu);
               for (int64_t c = 0; c < k; ++c) local[c] = fifo[c0 + c];
             }
+            const double h0 = now_s();
+            cudaEventRecord(L.hev[0], w.stream);
             rs = host_input_enqueue(m, w, H, local, 0, k, &B);
-            if (rs == REC_OK) rs = forward_enqueue(m, w, w.indices, w.offsets, B, nullptr, w.ctr, w.logit, nullptr, w.idx_cap);
+            const double hin = (now_s() - h0) * 1e3;
+            cudaEventRecord(L.hev[1], w.stream);
+            if (rs == REC_OK) rs = forward_enqueue(m, w, w.indices, w.offsets, B, nullptr, w.ctr, w.logit, L.hev, w.idx_cap);
+            std::lock_guard<std::mutex> g(mu);
+            batches[O.my_batch].host_in_ms = hin;
           }
           if (rs == REC_OK && ctr_out)
             if (cudaMemcpyAsync(L.ctr_host, w.ctr, sizeof(float) * B * m->tasks, cudaMemcpyDeviceToHost,
@@ -885,7 +943,7 @@ rec_status rec_serve(rec_model_t m, const rec_trace_row* trace, int64_t n, doubl
   double items_tot = 0;
   for (auto& b : batches) items_tot += b.items;
   fill_report(trace, n, sla_ms, pol->warmup_frac, release, disp_t, done_t, completed,
-              static_cast<int64_t>(batches.size()), items_tot, latency_ms, out);
+              static_cast<int64_t>(batches.size()), items_tot, latency_ms, out, comp);
   if (log_rows) *log_rows = logged;
   return REC_OK;
 }

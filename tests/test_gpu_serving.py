@@ -223,3 +223,20 @@ def test_mtwnd_serving_ctrs():
         exp = fw.forward(cfg, 1, dense, ind, off)
         assert np.abs(direct - exp).max() <= 2e-2
     m.close()
+
+
+@pytest.mark.parametrize("mode", ["synth", "host"])
+def test_latency_breakdown_components(model, mode):
+    """breakdown_ms = (queue, input, sparse, dense), P:418's latency components: every one is
+    non-negative, sparse and dense are positive device times, input is positive exactly in the
+    host-input (PCIe) mode, and queue + input + sparse + dense stays below the mean latency
+    (the rest is launch and completion-observation overhead)."""
+    from paper_2203_07424_b200 import REC_INPUT_HOST, REC_INPUT_DEVICE_SYNTH
+    tr = W.poisson_trace(3000.0, 300, seed=21)
+    im = REC_INPUT_HOST if mode == "host" else REC_INPUT_DEVICE_SYNTH
+    r = model.rec_serve(tr, 1e9, streams=2, max_batch=256, input_mode=im)
+    q, inp, sp, de = r["breakdown_ms"]
+    assert min(q, inp, sp, de) >= 0
+    assert sp > 0 and de > 0
+    assert (inp > 0) == (mode == "host")
+    assert q + inp + sp + de <= r["mean_ms"] * 1.001 + 1e-6
