@@ -473,6 +473,32 @@ def run_ours(args):
     b2b_ms = model.rec_bench_sls(bseg, tbstart[:b2b_n + 1], pdl=True)
     ser_ms = model.rec_bench_sls(bseg, tbstart[:b2b_n + 1], pdl=False)
     b2b_bytes = float(sls_bytes_per_item(cfg, synth=True) * int(bseg[:, 2].sum()))
+    # caller-index SLS (k_sls: device-resident indices + offsets, the rec_query / e2e path):
+    # back-to-back plain launches over distinct full batches of d items
+    caller = None
+    if args.caller_batches > 0:
+        nbc = args.caller_batches
+        gi, go = [], []
+        for k in range(nbc):
+            ind, off, _ = model.rec_gen_batch(np.array([[900000 + k, 0, d]], np.int32))
+            gi.append(ind)
+            go.append(off)
+        stride = max(x.size for x in gi)
+        idx_all = np.zeros((nbc, stride), np.int32)
+        for k, x in enumerate(gi):
+            idx_all[k, :x.size] = x
+        di = torch.from_numpy(idx_all).cuda()
+        do = torch.from_numpy(np.stack(go)).cuda()
+        c_ms = model.rec_bench_sls_caller(di, do, d, nbc, stride)
+        c_bytes = sls_bytes_per_item(cfg, synth=False) * d * nbc
+        c_gbs = c_bytes / (c_ms * 1e-3) / 1e9
+        caller = {"kernel": "k_sls (caller indices)", "achieved": c_gbs, "unit": "GB/s",
+                  "frac": c_gbs / peaks()[0], "bytes_per_item": sls_bytes_per_item(cfg, synth=False),
+                  "avg_launch_us": 1e3 * c_ms / nbc, "launches": nbc, "batch": d,
+                  "measured": "rec_bench_sls_caller: distinct device-resident batches, plain launches "
+                              "back to back, CUDA events on the launching stream"}
+        del di, do
+
     # host cost of the submit path (all streams, C++ loop, production graphs)
     hsteps = min(nbt, 1000)
     hb = tbstart[:hsteps + 1]
@@ -671,6 +697,7 @@ def run_ours(args):
                                       "measured": f"CUDA event nodes around the SLS node inside the "
                                                   f"step graph, {rsteps} single-stream steps (includes "
                                                   f"launch gap and ramp of a lone launch)"},
+                         "caller_index": caller,
                          "in_step_aggregate": {
                              "achieved": sls_bytes_per_item(cfg, synth=True) * tot_items / (ms_max * 1e-3) / 1e9,
                              "frac": sls_bytes_per_item(cfg, synth=True) * tot_items / (ms_max * 1e-3) / 1e9 / hbm_peak,
@@ -857,6 +884,8 @@ def main():
                     help="S-D pipeline lanes (rec_set_pipeline) for the timed region; 0 = slot graphs")
     ap.add_argument("--roofline-steps", type=int, default=1000)
     ap.add_argument("--sls-batches", type=int, default=1000, help="batches in the back-to-back SLS pass")
+    ap.add_argument("--caller-batches", type=int, default=48,
+                    help="distinct device-resident batches in the caller-index SLS pass (0 = off)")
     ap.add_argument("--queries", type=int, default=40000)
     ap.add_argument("--e2e-steps", type=int, default=6)
     ap.add_argument("--sla-queries", type=int, default=100000, help="Poisson queries per probe per GPU")

@@ -212,6 +212,15 @@ rec_status rec_bench_mlp(rec_model_t m, int32_t which, int32_t batch, int32_t it
  * bench.py uses it for the SLS roofline line. */
 rec_status rec_bench_sls(rec_model_t m, const int32_t* segs, const int64_t* batch_start,
                          int32_t nbatches, int32_t pdl, double* ms_total);
+/* Time back-to-back launches of the caller-index SLS kernel (k_sls: indices and offsets
+ * read from memory, rec_query / rec_query_async / e2e path) on stream slot 0: nbatches batches
+ * of `batch` items, batch k's offsets at offsets + k * (T * batch + 1) and its indices at
+ * indices + k * idx_stride (DEVICE pointers, table-major CSR per batch; idx_stride = readable
+ * indices per batch).  *ms_total = CUDA-event time of the nbatches launches.  Writes the
+ * workspace's X only.  Errors: INVALID_ARG (host pointers, sizes), UNSUPPORTED (sharded),
+ * INDEX_OOB / OFFSETS (device flags of the launches). */
+rec_status rec_bench_sls_caller(rec_model_t m, const int32_t* indices, const int32_t* offsets,
+                                int32_t batch, int32_t nbatches, int64_t idx_stride, double* ms_total);
 /* Diagnostic: %globaltimer stamps (ns) of CTA 0 of one fused-MLP launch (which: 0 bottom,
  * 1 top): [0] entry [1] TMEM+barriers ready [2] first TMA issued [3] first stage landed
  * [4+l] layer l MMAs committed [8+2l]/[9+2l] epilogue l start/end [15] exit; [14] = CUDA-event

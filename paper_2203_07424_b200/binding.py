@@ -33,7 +33,8 @@ EXPORTS = ["rec_model_create", "rec_model_destroy", "rec_query", "rec_query_debu
            "rec_gen_batch", "rec_profile", "rec_profile_read", "rec_serve", "rec_last_error",
            "rec_nccl_unique_id_size", "rec_nccl_get_unique_id", "rec_version", "rec_split_fuse",
            "rec_synth_query_batches", "rec_shard_plan", "rec_bench_mlp", "rec_bench_sls", "rec_set_pipeline", "rec_synth_query_pipeline",
-           "rec_debug_chain_timeline", "rec_query_inspect", "rec_hot_remap"]
+           "rec_debug_chain_timeline", "rec_query_inspect", "rec_hot_remap",
+           "rec_bench_sls_caller"]
 
 
 class rec_model_desc(C.Structure):
@@ -118,6 +119,8 @@ def lib() -> C.CDLL:
         L.rec_query_inspect.restype = i32
         L.rec_hot_remap.argtypes = [vp, vp, vp, i32, i64, C.POINTER(i64)]
         L.rec_hot_remap.restype = i32
+        L.rec_bench_sls_caller.argtypes = [vp, vp, vp, i32, i32, i64, C.POINTER(C.c_double)]
+        L.rec_bench_sls_caller.restype = i32
         for f in ("rec_model_create", "rec_query", "rec_query_debug", "rec_query_async",
                   "rec_synth_query_async", "rec_sync", "rec_gen_batch", "rec_profile",
                   "rec_profile_read", "rec_serve", "rec_nccl_get_unique_id"):
@@ -279,6 +282,13 @@ class RecModel:
         bs = np.ascontiguousarray(batch_start, dtype=np.int64)
         ms = C.c_double()
         _check(lib().rec_bench_sls(self.h, _ptr(segs), _ptr(bs), len(bs) - 1, int(pdl), C.byref(ms)))
+        return ms.value
+
+    def rec_bench_sls_caller(self, indices, offsets, batch: int, nbatches: int, idx_stride: int) -> float:
+        """Total CUDA-event ms of nbatches caller-index SLS launches (device arrays, rec.h)."""
+        ms = C.c_double()
+        _check(lib().rec_bench_sls_caller(self.h, _ptr(indices), _ptr(offsets), batch, nbatches,
+                                          idx_stride, C.byref(ms)))
         return ms.value
 
     def rec_debug_chain_timeline(self, which: int, batch: int):

@@ -289,11 +289,18 @@ __global__ void __launch_bounds__(THREADS, REC_SLS_MINB) k_sls_synth(const __gri
   SLS_GDC_TRIGGER();
   const int B = sb.B;
   const int nbags = a.T * B;  // >= T: a synthetic batch is never empty (block 0 writes dB)
-  int g = blockIdx.x * GROUPS + threadIdx.x / LANES;
+  // Bag -> (CTA, group): blocked (g = CTA * GROUPS + group) or, with a.interleave, dealt
+  // round-robin over a grid of exactly nsm x resident CTAs (g = group * gridDim + CTA), so
+  // every SM holds the same number of bags and the launch ends without a tail of SMs that
+  // got one CTA more (B = 1024: 640 blocked CTAs are 4.3 per SM).
+  int g = a.interleave ? (threadIdx.x / LANES) * static_cast<int>(gridDim.x) + static_cast<int>(blockIdx.x)
+                       : static_cast<int>(blockIdx.x) * GROUPS + threadIdx.x / LANES;
+  const int cta_has = a.interleave ? static_cast<int>(blockIdx.x) < nbags
+                                   : static_cast<int>(blockIdx.x) * GROUPS < nbags;
   if (P2P) {
     // sharded: CTAs of the batch all reach the CTA barrier of the flag protocol (groups past
     // the last bag idle on bag 0 and store nothing); CTAs past the batch leave uncounted
-    if (static_cast<int>(blockIdx.x) * GROUPS >= nbags) return;
+    if (!cta_has) return;
   } else if (g >= nbags) {
     return;
   }
@@ -380,7 +387,8 @@ __global__ void __launch_bounds__(THREADS, REC_SLS_MINB) k_sls_synth(const __gri
         p2p.words[1] = static_cast<unsigned>(B);
       }
       __threadfence_system();
-      const unsigned need = static_cast<unsigned>((nbags + GROUPS - 1) / GROUPS);
+      const unsigned need = a.interleave ? static_cast<unsigned>(min(nbags, static_cast<int>(gridDim.x)))
+                                         : static_cast<unsigned>((nbags + GROUPS - 1) / GROUPS);
       const unsigned prev = atomicAdd(p2p.counter, 1u);
       if (prev == need - 1) {  // last CTA: every CTA's stores are fenced
         __threadfence_system();
@@ -553,7 +561,9 @@ void* sls_synth_kernel(const SlsSynthArgs& a, dim3* grid, dim3* block, size_t* s
   constexpr int THREADS = 128;
   const int L = a.D / 4 <= 8 ? 8 : a.D / 4 <= 16 ? 16 : 32;
   const int nb = a.T * a.cap;
-  *grid = dim3((nb + THREADS / L - 1) / (THREADS / L));
+  const int blocked = (nb + THREADS / L - 1) / (THREADS / L);
+  // interleaved: one full wave of nsm x REC_SLS_MINB CTAs (fewer if the capacity is smaller)
+  *grid = dim3(a.interleave ? std::min(blocked, a.nsm * REC_SLS_MINB) : blocked);
   *block = dim3(THREADS);
   if (smem) *smem = 0;
   if (a.p2p.peer_X) {

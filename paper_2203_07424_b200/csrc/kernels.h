@@ -148,6 +148,7 @@ struct SlsSynthArgs {
   const int64_t* remap_off;
   int tma;     // 1: k_sls_synth_tma
   int nsm;     // SMs (persistent grid)
+  int interleave;  // bags dealt round-robin over one wave of nsm x resident CTAs (k_sls_synth)
   int nst;     // ring chunks per warp
 };
 // Returns the kernel for this configuration; grid / block / dynamic smem are written back.

@@ -431,6 +431,7 @@ void fill_genargs(rec_model_s* m, Workspace& w, GenArgs& ga, SlsSynthArgs& sa,
   sa.pdl = m->sls_pdl && !sa.tma;
   sa.tmap_rows = m->d_tmap_rows;
   sa.nsm = m->nsm;
+  sa.interleave = m->sls_interleave;
   if (sa.tma) sls_tma_configure(sa);
 }
 
@@ -1279,6 +1280,7 @@ rec_status rec_model_create(const rec_model_desc* d, rec_model_t* out) {
     }
     const char* p = getenv("REC_PDL");
     m->sls_pdl = !(p && strcmp(p, "0") == 0);
+    m->sls_interleave = env_int("REC_SLS_GRID", 1);
     CHECK_CUDA_CREATE(cudaDeviceGetAttribute(&m->nsm, cudaDevAttrMultiProcessorCount, m->device));
     if (want && m->value_mode == REC_VALUES_INT8_EXACT && sls_tma_supported(D) &&
         total_rows < (int64_t(1) << 31)) {
@@ -2119,6 +2121,52 @@ rec_status rec_bench_sls(rec_model_t m, const int32_t* segs, const int64_t* batc
   m->launches += 3 + nbatches;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "rec_bench_sls");
+  return REC_OK;
+}
+
+rec_status rec_bench_sls_caller(rec_model_t m, const int32_t* indices, const int32_t* offsets,
+                                int32_t batch, int32_t nbatches, int64_t idx_stride, double* ms_total) {
+  if (!m || !indices || !offsets || batch < 1 || batch > m->max_batch || nbatches < 1 ||
+      idx_stride < 0 || !ms_total) {
+    set_error("bad argument");
+    return REC_E_INVALID_ARG;
+  }
+  if (m->world > 1 && m->shard != REC_SHARD_REPLICA) {
+    set_error("rec_bench_sls_caller needs an unsharded model");
+    return REC_E_UNSUPPORTED;
+  }
+  if (!is_device_ptr(indices) || !is_device_ptr(offsets)) {
+    set_error("rec_bench_sls_caller: indices and offsets must be device memory");
+    return REC_E_INVALID_ARG;
+  }
+  REC_CUDA(cudaSetDevice(m->device));
+  REC_CUDA(cudaDeviceSynchronize());
+  Workspace& w = m->ws[0];
+  const int T = m->T, D = m->D;
+  const int64_t ostride = static_cast<int64_t>(T) * batch + 1;
+  auto one = [&](int k) {
+    launch_sls(m->tables, m->d_tab_off, m->row_stride, m->d_rows, indices + k * idx_stride,
+               offsets + k * ostride, batch, nullptr, T, D, w.X, (T + 1) * D, 1, w.flag, w.stream, 0,
+               0x7fffffff, static_cast<int>(std::min<int64_t>(idx_stride, 0x7fffffff)));
+  };
+  cudaEvent_t a, b;
+  REC_CUDA(cudaEventCreate(&a));
+  REC_CUDA(cudaEventCreate(&b));
+  for (int i = 0; i < 3; ++i) one(0);
+  REC_CUDA(cudaEventRecord(a, w.stream));
+  for (int k = 0; k < nbatches; ++k) one(k);
+  REC_CUDA(cudaEventRecord(b, w.stream));
+  REC_CUDA(cudaEventSynchronize(b));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, a, b);
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  *ms_total = ms;
+  m->launches += 3 + nbatches;
+  rec_status st = sync_ws(w);  // the device error flag (OOB / offsets) of the timed launches
+  if (st != REC_OK) return st;
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "rec_bench_sls_caller");
   return REC_OK;
 }
 

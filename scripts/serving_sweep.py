@@ -1,0 +1,123 @@
+"""Serving sweep (BASELINE.json configs[4]): SLA-bounded QPS lambda* per model at
+p95 <= SLA for SLA in {10, 20, 50, 100} ms, trace seeds {11, 12, 13}, in
+both input modes (device-synthesised inputs; REC_INPUT_HOST = the paper's PCIe data loading,
+P:446-448), on G replicas (one process per GPU under torch.distributed.run, query q served by
+rank q mod G, rank-0 p95 over all ranks' latencies).  Each point also records the latency
+breakdown (queue, input, sparse, dense) of the last passing probe.
+usage: [torchrun --nproc-per-node G ...] python scripts/serving_sweep.py --models rmc1,rmc2,rmc3
+Prints one JSON object on rank 0.
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    import torch
+    import torch.distributed as dist
+    import bench
+    import workloads as W
+    from harness.sla import rank_share, gather_latencies, p95_nearest_rank
+    from paper_2203_07424_b200 import RecModel, REC_INPUT_HOST, REC_INPUT_DEVICE_SYNTH
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--models", default="rmc1,rmc2,rmc3")
+    ap.add_argument("--slas", default="10,20,50,100")
+    ap.add_argument("--seeds", default="11,12,13")
+    ap.add_argument("--modes", default="synth,host")
+    ap.add_argument("--streams", type=int, default=8)
+    ap.add_argument("--batch", type=int, default=1024)
+    ap.add_argument("--probe-s", type=float, default=1.2, help="trace span per probe (s)")
+    ap.add_argument("--host-queries", type=int, default=20000, help="cap per probe in host mode")
+    a = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    out = {"world": world, "streams": a.streams, "max_batch": a.batch, "points": []}
+    t_start = time.time()
+    for name in a.models.split(","):
+        cfg = W.SHORT[name]
+        m = RecModel(cfg, seed=1, max_batch=a.batch, streams=a.streams, device=local)
+        sat = bench.saturation(m, cfg, a.batch, a.streams, 4, 2, 128, 20000, rank, world, dist)
+        out.setdefault("saturation_qps", {})[cfg.name] = sat["value"]
+        for mode in a.modes.split(","):
+            im = REC_INPUT_HOST if mode == "host" else REC_INPUT_DEVICE_SYNTH
+            for sla in [float(x) for x in a.slas.split(",")]:
+                for seed in [int(x) for x in a.seeds.split(",")]:
+                    probes = []
+                    best = {"lam": 0.0, "breakdown": None, "p95": None}
+
+                    def probe(lam):
+                        n = int(max(2000, lam * a.probe_s))
+                        if mode == "host":
+                            n = min(n, a.host_queries * world)
+                        tr = W.poisson_trace(lam, n, seed=seed)
+                        mine = rank_share(tr, world, rank)
+                        r = m.rec_serve(mine, sla, a.streams, a.batch, input_mode=im, warmup_frac=0.1)
+                        w_end = tr["arrival_s"][0] + 0.1 * (tr["arrival_s"][-1] - tr["arrival_s"][0])
+                        lat = gather_latencies(r["latency_ms"][mine["arrival_s"] >= w_end], world, rank, dist)
+                        st = torch.tensor([r["stable"]], device="cuda")
+                        bd = torch.tensor(r["breakdown_ms"], dtype=torch.float64, device="cuda")
+                        if world > 1:
+                            dist.all_reduce(st, op=dist.ReduceOp.MIN)
+                            dist.all_reduce(bd, op=dist.ReduceOp.SUM)
+                            bd /= world
+                        ok = torch.tensor([0], device="cuda")
+                        if rank == 0:
+                            p95 = p95_nearest_rank(lat)
+                            ok[0] = int(st.item() == 1 and p95 <= sla)
+                            probes.append({"offered_qps": round(lam), "p95_ms": round(p95, 3), "ok": int(ok.item()),
+                                           "queries": n})
+                            if ok.item() and lam > best["lam"]:
+                                best.update(lam=lam, breakdown=[round(x, 4) for x in bd.tolist()],
+                                            p95=round(p95, 3))
+                        if world > 1:
+                            dist.broadcast(ok, 0)
+                        return bool(ok.item())
+
+                    lo = hi = None
+                    lam = 0.5 * sat["value"] if mode == "synth" else 0.1 * sat["value"]
+                    for _ in range(10):  # bracket, then bisect to 2 %
+                        if probe(lam):
+                            lo = lam
+                            if hi is not None:
+                                break
+                            lam *= 2.0
+                        else:
+                            hi = lam
+                            if lo is not None:
+                                break
+                            lam *= 0.5
+                    it = 0
+                    while lo is not None and hi is not None and hi - lo > 0.02 * lo and it < 8:
+                        mid = 0.5 * (lo + hi)
+                        it += 1
+                        if probe(mid):
+                            lo = mid
+                        else:
+                            hi = mid
+                    if rank == 0:
+                        out["points"].append({"workload": cfg.name, "input": mode, "sla_ms": sla, "seed": seed,
+                                              "lambda_star_qps": lo or 0.0, "p95_ms_at_best": best["p95"],
+                                              "breakdown_ms_queue_input_sparse_dense": best["breakdown"],
+                                              "probes": probes})
+                        print(json.dumps(out["points"][-1]), file=sys.stderr, flush=True)
+        m.close()
+    out["wall_s"] = round(time.time() - t_start, 1)
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

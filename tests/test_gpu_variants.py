@@ -18,7 +18,7 @@ KNOBS = ["REC_SLS", "REC_GEMM_2SM", "REC_GEMM_NARROW", "REC_GEMM_MT1", "REC_FUSE
          "REC_INTERACT_PF", "REC_HOT_POLICY", "REC_MLP", "REC_CHAIN_PDL", "REC_PDL",
          "REC_FUSE_INTERACT", "REC_TOWER_GROUP", "REC_GEMM_STAGES", "REC_INTERACT_WPC",
          "REC_CHAIN_SMEM", "REC_CHAIN_STAGES", "REC_SERVE_DEPTH",
-         "REC_SERVE_THREADS", "REC_GREEN_SMS", "REC_PRIO", "REC_GEMM_BN64"]
+         "REC_SERVE_THREADS", "REC_GREEN_SMS", "REC_PRIO", "REC_GEMM_BN64", "REC_SLS_GRID"]
 
 
 @pytest.fixture(scope="module", autouse=True)
@@ -58,6 +58,8 @@ TINY = W.TINY
 VARIANTS = [
     ("sls_tma", {"REC_SLS": "tma"}, RMC1, 700, 0),
     ("sls_no_pdl", {"REC_PDL": "0"}, RMC1, 700, 0),
+    ("sls_blocked_grid", {"REC_SLS_GRID": "0"}, RMC1, 700, 0),
+    ("sls_blocked_grid_rmc2", {"REC_SLS_GRID": "0"}, W.small_variant(W.RMC2, 4096), 1024, 0),
     ("hot_policy_l2_window", {"REC_HOT_POLICY": "1"}, RMC1.with_(index_dist=W.INDEX_SKEW2), 700, 8 << 20),
     ("l2_window", {}, RMC1, 700, 8 << 20),
     ("fuse_dense", {"REC_FUSE_DENSE": "1"}, RMC1, 700, 0),
