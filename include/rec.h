@@ -259,7 +259,12 @@ typedef struct {
 
 typedef struct {
   double offered_qps, achieved_qps, mean_ms, p50_ms, p95_ms, p99_ms;
-  double breakdown_ms[4];     /* mean per query: queue, input, sparse+dense (device), tail */
+  double breakdown_ms[4];     /* mean per query: queue (arrival -> dispatch of its last
+                                 sub-query), input (H2D + host packing; 0 for device-synth),
+                                 sparse (SLS), dense (rest of the chain's device time) of the
+                                 batch completing the query - [1..3] only while profiling is on
+                                 (rec_profile(m, 1): stage-event graphs, slower); otherwise
+                                 [2] = dispatch -> observed completion and [1], [3] = 0        */
   int64_t completed, dropped, batches;
   double mean_batch;
   int32_t sla_met;            /* p95 <= SLA, all completed, achieved >= 0.98 offered (R23) */

@@ -182,7 +182,13 @@ static void prof_collect(rec_model_s* m) {
 //   gev: 0 chain start, 1 inputs done, 2 SLS done, 3 join, 4 interaction done, 5 top done,
 //        6/7 bottom-branch start/end (the branch stream)
 static inline void mark(cudaEvent_t* gev, int i, cudaStream_t st) {
-  if (gev) cudaEventRecordWithFlags(gev[i], st, cudaEventRecordExternal);
+  if (!gev) return;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(st, &cs);
+  // inside a capture: an external event node of the graph; outside (host-input serving with
+  // stage events): a plain record
+  if (cs == cudaStreamCaptureStatusActive) cudaEventRecordWithFlags(gev[i], st, cudaEventRecordExternal);
+  else cudaEventRecord(gev[i], st);
 }
 
 void enqueue_bottom(rec_model_s* m, Workspace& w, cudaStream_t st, int B, const int* dB,
@@ -669,7 +675,7 @@ rec_status synth_submit(rec_model_s* m, Workspace& w, const int32_t* segs, int n
   } else if (nseg > kParamSegs) {
     REC_CUDA(cudaEventRecord(w.pin_free, w.stream));
   }
-  SynthSlot::Variant& V = sl.var[(m->prof || m->serve_events) && sl.var[1].exec ? 1 : 0];
+  SynthSlot::Variant& V = sl.var[m->prof && sl.var[1].exec ? 1 : 0];
   const bool direct = dense_f32_out != nullptr || !V.exec;
   if (!direct) {
     const bool fused = m->lo == m->hi;

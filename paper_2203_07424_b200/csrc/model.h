@@ -148,7 +148,6 @@ struct rec_model_s {
   int64_t* d_remap_off = nullptr;
   int64_t hot_window = 0;
   bool counted = false;                // counted in the per-device co-located model registry
-  bool serve_events = false;           // rec_serve: synthetic graphs with stage events (breakdown)
   // embedding arena
   float* tables = nullptr;
   size_t table_bytes = 0;

@@ -92,7 +92,7 @@ struct Lane {
 // [1] sparse (SLS incl. fused index generation), [2] dense (chain device time not in the SLS:
 // the bottom branch beyond the SLS, interaction, top MLP).  ev: the stage events of forward_
 // enqueue / synth_chain (0 start, 1 inputs done, 2 SLS done, 5 top done).
-static void stage_times(const cudaEvent_t* ev, double host_in_ms, double out[3]) {
+static void stage_times(const cudaEvent_t* ev, bool host_mode, double host_in_ms, double out[3]) {
   auto el = [&](int a, int b) {
     float x = 0.f;
     if (!ev[a] || !ev[b] || cudaEventElapsedTime(&x, ev[a], ev[b]) != cudaSuccess) {
@@ -101,10 +101,17 @@ static void stage_times(const cudaEvent_t* ev, double host_in_ms, double out[3])
     }
     return static_cast<double>(x);
   };
-  const double in = el(0, 1), sp = el(1, 2), all = el(0, 5);
-  out[0] = in + host_in_ms;
-  out[1] = sp;
-  out[2] = std::max(0.0, all - in - sp);
+  if (host_mode) {  // 0 -> 1: the batch's H2D copies; then SLS; the rest is dense
+    const double in = el(0, 1), sp = el(1, 2), all = el(0, 5);
+    out[0] = in + host_in_ms;
+    out[1] = sp;
+    out[2] = std::max(0.0, all - in - sp);
+  } else {         // device-synthesised inputs are generated inside the SLS / dense kernels
+    const double sp = el(0, 2), all = el(0, 5);
+    out[0] = 0.0;
+    out[1] = sp;   // chain start -> SLS done (incl. waiting for SMs held by co-located batches)
+    out[2] = std::max(0.0, all - sp);
+  }
 }
 
 // cuStreamWriteValue32 through the runtime's driver entry point (no libcuda link).
@@ -611,11 +618,12 @@ rec_status rec_serve(rec_model_t m, const rec_trace_row* trace, int64_t n, doubl
       }
     }
   }
-  // latency breakdown: the synthetic graphs with stage events, host-mode lane events
-  const bool synth_events = m->ws[0].slots[0].var[1].exec != nullptr;
-  m->serve_events = synth_events;
+  // latency breakdown while profiling is on (rec_profile): the synthetic graphs with
+  // stage events / host-mode lane events.  Off by default: per-batch event nodes and their
+  // read-back cost serving throughput (measured: RMC1 lambda* 317k -> 206k QPS)
+  const bool breakdown = m->prof;
+  const bool synth_events = breakdown && m->ws[0].slots[0].var[1].exec != nullptr;
   auto cleanup = [&]() {
-    m->serve_events = false;
     for (auto& L : lanes) {
       if (L.done) cudaEventDestroy(L.done);
       if (L.ctr_host) cudaFreeHost(L.ctr_host);
@@ -647,8 +655,8 @@ rec_status rec_serve(rec_model_t m, const rec_trace_row* trace, int64_t n, doubl
     Batch& bt = batches[bi];
     bt.t_done = t_c;
     double st[3] = {0, 0, 0};
-    if (pol->input_mode == REC_INPUT_HOST) stage_times(lanes[bt.stream].hev, bt.host_in_ms, st);
-    else if (synth_events && bt.slot >= 0) stage_times(m->ws[bt.stream].slots[bt.slot].ev, 0.0, st);
+    if (breakdown && pol->input_mode == REC_INPUT_HOST) stage_times(lanes[bt.stream].hev, true, bt.host_in_ms, st);
+    else if (synth_events && bt.slot >= 0) stage_times(m->ws[bt.stream].slots[bt.slot].ev, false, 0.0, st);
     for (int64_t c = bt.first_chunk; c < bt.first_chunk + bt.nchunks; ++c) {
       const Chunk& ch = fifo[c];
       if (--remaining[ch.pos] == 0) {
@@ -687,12 +695,13 @@ rec_status rec_serve(rec_model_t m, const rec_trace_row* trace, int64_t n, doubl
       batches[bi].slot = w.last_slot;
     } else {
       const double h0 = now_s();
-      REC_CUDA(cudaEventRecord(lanes[s].hev[0], w.stream));
+      if (breakdown) REC_CUDA(cudaEventRecord(lanes[s].hev[0], w.stream));
       st = host_input_enqueue(m, w, H, fifo, head, k, &B);
       if (st != REC_OK) return st;
       batches[bi].host_in_ms = (now_s() - h0) * 1e3;
-      REC_CUDA(cudaEventRecord(lanes[s].hev[1], w.stream));
-      st = forward_enqueue(m, w, w.indices, w.offsets, B, nullptr, w.ctr, w.logit, lanes[s].hev, w.idx_cap);
+      if (breakdown) REC_CUDA(cudaEventRecord(lanes[s].hev[1], w.stream));
+      st = forward_enqueue(m, w, w.indices, w.offsets, B, nullptr, w.ctr, w.logit,
+                           breakdown ? lanes[s].hev : nullptr, w.idx_cap);
       if (st != REC_OK) return st;
     }
     if (ctr_out)
@@ -873,11 +882,13 @@ rec_status rec_serve(rec_model_t m, const rec_trace_row* trace, int64_t n, doubl
               for (int64_t c = 0; c < k; ++c) local[c] = fifo[c0 + c];
             }
             const double h0 = now_s();
-            cudaEventRecord(L.hev[0], w.stream);
+            if (breakdown) cudaEventRecord(L.hev[0], w.stream);
             rs = host_input_enqueue(m, w, H, local, 0, k, &B);
             const double hin = (now_s() - h0) * 1e3;
-            cudaEventRecord(L.hev[1], w.stream);
-            if (rs == REC_OK) rs = forward_enqueue(m, w, w.indices, w.offsets, B, nullptr, w.ctr, w.logit, L.hev, w.idx_cap);
+            if (breakdown) cudaEventRecord(L.hev[1], w.stream);
+            if (rs == REC_OK)
+              rs = forward_enqueue(m, w, w.indices, w.offsets, B, nullptr, w.ctr, w.logit,
+                                   breakdown ? L.hev : nullptr, w.idx_cap);
             std::lock_guard<std::mutex> g(mu);
             batches[O.my_batch].host_in_ms = hin;
           }
@@ -943,7 +954,8 @@ rec_status rec_serve(rec_model_t m, const rec_trace_row* trace, int64_t n, doubl
   double items_tot = 0;
   for (auto& b : batches) items_tot += b.items;
   fill_report(trace, n, sla_ms, pol->warmup_frac, release, disp_t, done_t, completed,
-              static_cast<int64_t>(batches.size()), items_tot, latency_ms, out, comp);
+              static_cast<int64_t>(batches.size()), items_tot, latency_ms, out,
+              breakdown ? comp : nullptr);
   if (log_rows) *log_rows = logged;
   return REC_OK;
 }

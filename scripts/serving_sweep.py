@@ -3,7 +3,7 @@ p95 <= SLA for SLA in {10, 20, 50, 100} ms, trace seeds {11,
 both input modes (device-synthesised inputs; REC_INPUT_HOST = the paper's PCIe data loading,
 P:446-448), on G replicas (one process per GPU under torch.distributed.run, query q served by
 rank q mod G, rank-0 p95 over all ranks' latencies).  Each point also records the latency
-breakdown (queue, input, sparse, dense) of the last passing probe.
+breakdown (queue, input, sparse, dense) of one probe at 0.9 lambda* with profiling on.
 usage: [torchrun --nproc-per-node G ...] python scripts/serving_sweep.py --models rmc1,rmc2,rmc3
 Prints one JSON object on rank 0.
 """
@@ -54,7 +54,7 @@ def main():
             for sla in [float(x) for x in a.slas.split(",")]:
                 for seed in [int(x) for x in a.seeds.split(",")]:
                     probes = []
-                    best = {"lam": 0.0, "breakdown": None, "p95": None}
+                    best = {"lam": 0.0, "p95": None}
 
                     def probe(lam):
                         n = int(max(2000, lam * a.probe_s))
@@ -66,11 +66,8 @@ def main():
                         w_end = tr["arrival_s"][0] + 0.1 * (tr["arrival_s"][-1] - tr["arrival_s"][0])
                         lat = gather_latencies(r["latency_ms"][mine["arrival_s"] >= w_end], world, rank, dist)
                         st = torch.tensor([r["stable"]], device="cuda")
-                        bd = torch.tensor(r["breakdown_ms"], dtype=torch.float64, device="cuda")
                         if world > 1:
                             dist.all_reduce(st, op=dist.ReduceOp.MIN)
-                            dist.all_reduce(bd, op=dist.ReduceOp.SUM)
-                            bd /= world
                         ok = torch.tensor([0], device="cuda")
                         if rank == 0:
                             p95 = p95_nearest_rank(lat)
@@ -78,8 +75,7 @@ def main():
                             probes.append({"offered_qps": round(lam), "p95_ms": round(p95, 3), "ok": int(ok.item()),
                                            "queries": n})
                             if ok.item() and lam > best["lam"]:
-                                best.update(lam=lam, breakdown=[round(x, 4) for x in bd.tolist()],
-                                            p95=round(p95, 3))
+                                best.update(lam=lam, p95=round(p95, 3))
                         if world > 1:
                             dist.broadcast(ok, 0)
                         return bool(ok.item())
@@ -105,11 +101,31 @@ def main():
                             lo = mid
                         else:
                             hi = mid
+                    # latency breakdown at 0.9 lambda*: one probe with profiling on
+                    # (stage-event graphs cost throughput, so lambda* is searched without them)
+                    bd_at = None
+                    if lo:
+                        m.rec_profile(True)
+                        n = int(max(2000, 0.9 * lo * a.probe_s))
+                        if mode == "host":
+                            n = min(n, a.host_queries * world)
+                        tr = W.poisson_trace(0.9 * lo, n, seed=seed)
+                        r = m.rec_serve(rank_share(tr, world, rank), sla, a.streams, a.batch, input_mode=im,
+                                        warmup_frac=0.1)
+                        m.rec_profile(False)
+                        bd = torch.tensor(list(r["breakdown_ms"]) + [r["mean_ms"], r["p95_ms"]],
+                                          dtype=torch.float64, device="cuda")
+                        if world > 1:
+                            dist.all_reduce(bd, op=dist.ReduceOp.SUM)
+                            bd /= world
+                        v = bd.tolist()
+                        bd_at = {"offered_qps": round(0.9 * lo),
+                                 "queue_input_sparse_dense_ms": [round(x, 4) for x in v[:4]],
+                                 "mean_ms": round(v[4], 3), "p95_ms_rank_mean": round(v[5], 3)}
                     if rank == 0:
                         out["points"].append({"workload": cfg.name, "input": mode, "sla_ms": sla, "seed": seed,
                                               "lambda_star_qps": lo or 0.0, "p95_ms_at_best": best["p95"],
-                                              "breakdown_ms_queue_input_sparse_dense": best["breakdown"],
-                                              "probes": probes})
+                                              "breakdown_at_0p9_lambda": bd_at, "probes": probes})
                         print(json.dumps(out["points"][-1]), file=sys.stderr, flush=True)
         m.close()
     out["wall_s"] = round(time.time() - t_start, 1)

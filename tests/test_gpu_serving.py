@@ -227,14 +227,17 @@ def test_mtwnd_serving_ctrs():
 
 @pytest.mark.parametrize("mode", ["synth", "host"])
 def test_latency_breakdown_components(model, mode):
-    """breakdown_ms = (queue, input, sparse, dense), P:418's latency components: every one is
+    """breakdown_ms = (queue, input, sparse, dense), P:418's latency components (recorded while
+    profiling is on, rec_profile): every one is
     non-negative, sparse and dense are positive device times, input is positive exactly in the
     host-input (PCIe) mode, and queue + input + sparse + dense stays below the mean latency
     (the rest is launch and completion-observation overhead)."""
     from paper_2203_07424_b200 import REC_INPUT_HOST, REC_INPUT_DEVICE_SYNTH
     tr = W.poisson_trace(3000.0, 300, seed=21)
     im = REC_INPUT_HOST if mode == "host" else REC_INPUT_DEVICE_SYNTH
+    model.rec_profile(True)                 # the breakdown is recorded while profiling
     r = model.rec_serve(tr, 1e9, streams=2, max_batch=256, input_mode=im)
+    model.rec_profile(False)
     q, inp, sp, de = r["breakdown_ms"]
     assert min(q, inp, sp, de) >= 0
     assert sp > 0 and de > 0
