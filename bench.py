@@ -432,7 +432,16 @@ def run_ours(args):
     d = args.batch
     m_streams = default_streams(args, args.config)
     l2p = int(args.l2_persist_mb) << 20
-    model = RecModel(cfg, seed=1, max_batch=d, streams=m_streams, device=local, l2_persist_bytes=l2p)
+    nid = None
+    if world > 1:  # replicas: a communicator only for rec_serve's all-rank percentiles (C4)
+        from paper_2203_07424_b200 import nccl_unique_id
+        t = torch.zeros(128, dtype=torch.uint8, device="cuda")
+        if rank == 0:
+            t.copy_(torch.frombuffer(bytearray(nccl_unique_id()), dtype=torch.uint8))
+        dist.broadcast(t, 0)
+        nid = bytes(t.cpu().numpy())
+    model = RecModel(cfg, seed=1, max_batch=d, streams=m_streams, device=local, l2_persist_bytes=l2p,
+                     rank=rank, world=world, nccl_id=nid)
     dev = torch.device("cuda", local)
     streams = [torch.cuda.ExternalStream(model.rec_stream_handle(k), device=dev) for k in range(m_streams)]
     stream = streams[0]
@@ -593,8 +602,16 @@ def run_ours(args):
         ds = [x for x in (256, 512, 1024, 2048, 4096) if x <= max(d, d_max)]
         serve_model = model
         if max(ds) > d:  # a second handle with the larger workspaces (tables are regenerated)
+            nid2 = None
+            if world > 1:
+                from paper_2203_07424_b200 import nccl_unique_id
+                t2 = torch.zeros(128, dtype=torch.uint8, device="cuda")
+                if rank == 0:
+                    t2.copy_(torch.frombuffer(bytearray(nccl_unique_id()), dtype=torch.uint8))
+                dist.broadcast(t2, 0)
+                nid2 = bytes(t2.cpu().numpy())
             serve_model = RecModel(cfg, seed=1, max_batch=max(ds), streams=m_streams, device=local,
-                                   l2_persist_bytes=l2p)
+                                   l2_persist_bytes=l2p, rank=rank, world=world, nccl_id=nid2)
         res = gradient_search(evaluate, ms, ds, noise=0.02)
         sla = {"sla_ms": cfg.sla_ms, "percentile": "p95 (nearest rank)",
                "lambda_star_qps": res["qps"], "policy": {"streams": res["m"], "max_batch": res["d"]},

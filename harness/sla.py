@@ -40,18 +40,21 @@ def sla_search(model, cfg, world, rank, dist, streams, d, lam0, n, sla_ms, max_i
         tr = W.poisson_trace(lam, n, seed=12)
         mine = tr if replicated else rank_share(tr, world, rank)
         rep = model.rec_serve(mine, sla_ms, streams, d, fusion_timeout_ms=tau_ms, warmup_frac=0.1)
-        arr = mine["arrival_s"]
-        w_end = tr["arrival_s"][0] + 0.1 * (tr["arrival_s"][-1] - tr["arrival_s"][0])
-        mylat = rep["latency_ms"][arr >= w_end]
-        lat = mylat if replicated else gather_latencies(mylat, world, rank, dist)
+        lib_global = world > 1 and rep.get("ranks", 1) == world   # the library gathered (C4)
+        if not lib_global:
+            arr = mine["arrival_s"]
+            w_end = tr["arrival_s"][0] + 0.1 * (tr["arrival_s"][-1] - tr["arrival_s"][0])
+            mylat = rep["latency_ms"][arr >= w_end]
+            lat = mylat if replicated else gather_latencies(mylat, world, rank, dist)
         stable = torch.tensor([rep["stable"]], device="cuda")
         if world > 1:
             dist.all_reduce(stable, op=dist.ReduceOp.MIN)
         ok = torch.tensor([0], device="cuda")
         if rank == 0:
-            p95 = p95_nearest_rank(lat)
+            p95 = rep["p95_ms"] if lib_global else p95_nearest_rank(lat)
             ok[0] = int(stable.item() == 1 and p95 <= sla_ms)
-            probes.append({"offered_qps": round(lam), "p95_ms": round(p95, 3), "ok": int(ok.item())})
+            probes.append({"offered_qps": round(lam), "p95_ms": round(p95, 3), "ok": int(ok.item()),
+                           "p95_from": "library (all ranks)" if lib_global else "python gather"})
         if world > 1:
             dist.broadcast(ok, 0)
         return bool(ok.item())

@@ -74,7 +74,9 @@ typedef struct {
   int32_t device;                 /* CUDA device ordinal used by this handle                */
   int32_t shard;                  /* REC_SHARD_REPLICA | REC_SHARD_TABLE | REC_SHARD_ROW    */
   int32_t rank, world;            /* this process's rank and the number of GPUs (1 => local) */
-  const void* nccl_id;            /* 128-byte ncclUniqueId shared by all ranks (world > 1)  */
+  const void* nccl_id;            /* 128-byte ncclUniqueId shared by all ranks (world > 1;
+                                     sharded: required; replicas: optional, enables rec_serve's
+                                     global percentiles)                                   */
   int64_t l2_persist_bytes;       /* > 0: L2 persisting window over the hot row prefix of
                                      every table (A10/D2 residue), 0 = off       */
   int32_t arch;                   /* REC_ARCH_DLRM (0) | REC_ARCH_MTWND (1), SURVEY 8(f)4:
@@ -269,6 +271,11 @@ typedef struct {
   double mean_batch;
   int32_t sla_met;            /* p95 <= SLA, all completed, achieved >= 0.98 offered (R23) */
   int32_t stable;
+  int32_t ranks;              /* ranks the percentiles cover: 1, or world for replica models
+                                 created with world > 1 and an nccl_id (every rank serves its
+                                 share of the trace, e.g. q mod G; latencies are all-gathered
+                                 (C4) so every rank reports the GLOBAL mean / p50 / p95 / p99,
+                                 stable = all ranks stable, offered / achieved = sums)        */
 } rec_serve_report;
 
 /* Query splitting + fusion (S1, S2) for queries that are all pending

@@ -60,7 +60,7 @@ class rec_serve_report(C.Structure):
                 ("p50_ms", C.c_double), ("p95_ms", C.c_double), ("p99_ms", C.c_double),
                 ("breakdown_ms", C.c_double * 4), ("completed", C.c_int64), ("dropped", C.c_int64),
                 ("batches", C.c_int64), ("mean_batch", C.c_double), ("sla_met", C.c_int32),
-                ("stable", C.c_int32)]
+                ("stable", C.c_int32), ("ranks", C.c_int32)]
 
     def as_dict(self) -> dict:
         d = {k: getattr(self, k) for k, _ in self._fields_ if k != "breakdown_ms"}

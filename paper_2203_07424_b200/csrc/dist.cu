@@ -48,6 +48,7 @@ rec_status dist_init(rec_model_s* m, const void* nccl_id) {
   ncclComm_t comm = nullptr;
   REC_NCCL(ncclCommInitRank(&comm, m->world, id, m->rank));
   m->nccl_comm = comm;
+  if (m->shard == REC_SHARD_REPLICA) return REC_OK;  // serving percentiles only
   rec_status st = sharded_alloc(m);
   if (st != REC_OK) return st;
   return p2p_init(m);
@@ -410,6 +411,37 @@ rec_status p2p_init(rec_model_s* m) {
   if (getenv("REC_VERBOSE"))
     fprintf(stderr, "[rec] rank %d: fused %s exchange over peer memory (%d ranks)\n", m->rank,
             m->shard == REC_SHARD_TABLE ? "all-to-all" : "reduce-scatter", G);
+  return REC_OK;
+}
+
+// C4: every rank's values (variable counts) to every rank, through the model's communicator.
+rec_status allgather_doubles(rec_model_s* m, const std::vector<double>& mine, std::vector<double>& all) {
+  const int G = m->world;
+  ncclComm_t comm = static_cast<ncclComm_t>(m->nccl_comm);
+  cudaStream_t s = m->ws[0].stream;
+  int64_t* dc = nullptr;
+  REC_CUDA(cudaMalloc(reinterpret_cast<void**>(&dc), sizeof(int64_t) * (G + 1)));
+  const int64_t n = static_cast<int64_t>(mine.size());
+  REC_CUDA(cudaMemcpy(dc + G, &n, sizeof(int64_t), cudaMemcpyHostToDevice));
+  REC_NCCL(ncclAllGather(dc + G, dc, 1, ncclInt64, comm, s));
+  std::vector<int64_t> cnt(G);
+  REC_CUDA(cudaStreamSynchronize(s));
+  REC_CUDA(cudaMemcpy(cnt.data(), dc, sizeof(int64_t) * G, cudaMemcpyDeviceToHost));
+  cudaFree(dc);
+  int64_t mx = 1;
+  for (int64_t c : cnt) mx = std::max(mx, c);
+  double* dv = nullptr;
+  REC_CUDA(cudaMalloc(reinterpret_cast<void**>(&dv), sizeof(double) * mx * (G + 1)));
+  std::vector<double> pad(mx, 0.0);
+  std::copy(mine.begin(), mine.end(), pad.begin());
+  REC_CUDA(cudaMemcpy(dv + mx * G, pad.data(), sizeof(double) * mx, cudaMemcpyHostToDevice));
+  REC_NCCL(ncclAllGather(dv + mx * G, dv, mx, ncclFloat64, comm, s));
+  std::vector<double> buf(mx * G);
+  REC_CUDA(cudaStreamSynchronize(s));
+  REC_CUDA(cudaMemcpy(buf.data(), dv, sizeof(double) * mx * G, cudaMemcpyDeviceToHost));
+  cudaFree(dv);
+  all.clear();
+  for (int q = 0; q < G; ++q) all.insert(all.end(), buf.begin() + q * mx, buf.begin() + q * mx + cnt[q]);
   return REC_OK;
 }
 

@@ -1620,6 +1620,14 @@ rec_status rec_model_create(const rec_model_desc* d, rec_model_t* out) {
     }
   }
 
+  if (m->world > 1 && m->shard == REC_SHARD_REPLICA && d->nccl_id) {
+    // replicas: a communicator only for rec_serve's all-rank percentiles (no data path use)
+    rec_status st = dist_init(m, d->nccl_id);
+    if (st != REC_OK) {
+      free_model(m);
+      return st;
+    }
+  }
   if (m->world > 1 && m->shard != REC_SHARD_REPLICA) {
     rec_status st = dist_init(m, d->nccl_id);
     if (st != REC_OK) {

@@ -264,6 +264,8 @@ void enqueue_interact_top(rec_model_s* m, Workspace& w, cudaStream_t st, int B, 
 rec_status sharded_forward(rec_model_s* m, Workspace& w, const float* d_dense, const int* d_idx,
                            const int* d_off, int B, float* ctr, float* logits);
 rec_status sharded_alloc(rec_model_s* m);
+// All ranks' values (variable counts) on every rank through the model's communicator (C4).
+rec_status allgather_doubles(rec_model_s* m, const std::vector<double>& mine, std::vector<double>& all);
 // Table-wise sharding over peer memory, asynchronous (dist.cu): the chain of one global batch
 // on workspace w.  Caller mode (segs == nullptr): inputs already on the device (global dense /
 // indices / offsets); synthetic mode: the slot's SegBatch descriptors (captured graph).

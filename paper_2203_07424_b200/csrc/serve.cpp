@@ -239,7 +239,7 @@ static void fill_report(const rec_trace_row* trace, int64_t n, double sla_ms, do
                         const std::vector<double>& release, const std::vector<double>& disp_t,
                         const std::vector<double>& done_t, int64_t completed, int64_t nbatches,
                         double items_tot, double* latency_ms, rec_serve_report* out,
-                        const std::vector<double>* comp = nullptr) {
+                        const std::vector<double>* comp = nullptr, rec_model_s* gm = nullptr) {
   const double t_first = trace[0].arrival_s, t_last = trace[n - 1].arrival_s;
   const double w_end = t_first + warmup_frac * (t_last - t_first);
   std::vector<double> lat;
@@ -257,11 +257,46 @@ static void fill_report(const rec_trace_row* trace, int64_t n, double sla_ms, do
         for (int k = 0; k < 3; ++k) sum_c[k] += comp[k][p];
     }
   }
+  double offered = t_last > t_first ? n / (t_last - t_first) : INFINITY;
+  double achieved = t_max > t_first ? n / (t_max - t_first) : 0;
+  bool stable = (completed == n) && achieved >= 0.98 * offered;
+  int ranks = 1;
+  int64_t n_all = n;
+  if (gm) {  // replicas with a communicator: percentiles over every rank's queries (C4)
+    std::vector<double> mine = {static_cast<double>(completed), static_cast<double>(n), stable ? 1.0 : 0.0,
+                                offered, achieved, sum_lat, sum_q, sum_svc, sum_c[0], sum_c[1], sum_c[2],
+                                static_cast<double>(nbatches), items_tot};
+    std::vector<double> sc, all_lat;
+    if (allgather_doubles(gm, mine, sc) == REC_OK && allgather_doubles(gm, lat, all_lat) == REC_OK) {
+      ranks = gm->world;
+      completed = 0;
+      n_all = 0;
+      offered = achieved = sum_lat = sum_q = sum_svc = items_tot = 0;
+      sum_c[0] = sum_c[1] = sum_c[2] = 0;
+      nbatches = 0;
+      for (int q = 0; q < ranks; ++q) {
+        const double* v = sc.data() + 13 * q;
+        completed += static_cast<int64_t>(v[0]);
+        n_all += static_cast<int64_t>(v[1]);
+        stable = stable && v[2] > 0.5;
+        offered += v[3];
+        achieved += v[4];
+        sum_lat += v[5];
+        sum_q += v[6];
+        sum_svc += v[7];
+        for (int k = 0; k < 3; ++k) sum_c[k] += v[8 + k];
+        nbatches += static_cast<int64_t>(v[11]);
+        items_tot += v[12];
+      }
+      lat.swap(all_lat);
+    }
+  }
   std::sort(lat.begin(), lat.end());
   const int64_t nm = static_cast<int64_t>(lat.size());
   memset(out, 0, sizeof(*out));
+  out->ranks = ranks;
   out->completed = completed;
-  out->dropped = n - completed;
+  out->dropped = n_all - completed;
   out->batches = nbatches;
   out->mean_batch = nbatches ? items_tot / nbatches : 0;
   if (nm > 0) {
@@ -278,9 +313,9 @@ static void fill_report(const rec_trace_row* trace, int64_t n, double sla_ms, do
       out->breakdown_ms[2] = sum_svc / nm;   // dispatch -> observed completion, undivided
     }
   }
-  out->offered_qps = t_last > t_first ? n / (t_last - t_first) : INFINITY;
-  out->achieved_qps = t_max > t_first ? n / (t_max - t_first) : 0;
-  out->stable = (completed == n) && out->achieved_qps >= 0.98 * out->offered_qps;
+  out->offered_qps = offered;
+  out->achieved_qps = achieved;
+  out->stable = stable;
   out->sla_met = out->stable && out->p95_ms <= sla_ms;
 }
 
@@ -953,9 +988,10 @@ rec_status rec_serve(rec_model_t m, const rec_trace_row* trace, int64_t n, doubl
   // ------------------------------------------------ report (S5)
   double items_tot = 0;
   for (auto& b : batches) items_tot += b.items;
+  rec_model_s* gm = m->world > 1 && m->shard == REC_SHARD_REPLICA && m->nccl_comm ? m : nullptr;
   fill_report(trace, n, sla_ms, pol->warmup_frac, release, disp_t, done_t, completed,
               static_cast<int64_t>(batches.size()), items_tot, latency_ms, out,
-              breakdown ? comp : nullptr);
+              breakdown ? comp : nullptr, gm);
   if (log_rows) *log_rows = logged;
   return REC_OK;
 }

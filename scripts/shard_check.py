@@ -141,6 +141,23 @@ def main():
             ok &= all(v for k, v in chk.items() if k.startswith("async") or k.startswith("serve"))
         shm.close()
         rep.close()
+    # replicas with a communicator: rec_serve's percentiles cover every rank's queries (C4)
+    cfg = W.small_variant(W.RMC1, 20000)
+    rm = RecModel(cfg, seed=1, max_batch=1024, streams=4, device=local, rank=rank, world=world,
+                  nccl_id=bcast_id())
+    tr = W.poisson_trace(40000.0, 4000, seed=17)
+    mine = tr[tr["qid"] % world == rank]
+    r = rm.rec_serve(mine, 20.0, 4, 1024, warmup_frac=0.1)
+    arr = mine["arrival_s"]
+    w_end = arr[0] + 0.1 * (arr[-1] - arr[0])
+    parts = [None] * world
+    dist.all_gather_object(parts, r["latency_ms"][arr >= w_end])
+    lat = np.sort(np.concatenate(parts))
+    p95 = float(lat[max((95 * lat.size + 99) // 100, 1) - 1])
+    same = bool(r["ranks"] == world and abs(r["p95_ms"] - p95) < 1e-9 and r["completed"] == len(tr))
+    out["checks"]["replica_serve_global_p95"] = {"ok": same, "p95_ms": r["p95_ms"], "ranks": r["ranks"]}
+    ok &= same
+    rm.close()
     okt = torch.tensor([1 if ok else 0], device="cuda")
     dist.all_reduce(okt, op=dist.ReduceOp.MIN)
     out["ok"] = bool(okt.item())
