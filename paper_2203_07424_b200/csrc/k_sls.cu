@@ -293,10 +293,13 @@ __global__ void __launch_bounds__(THREADS, REC_SLS_MINB) k_sls_synth(const __gri
   // round-robin over a grid of exactly nsm x resident CTAs (g = group * gridDim + CTA), so
   // every SM holds the same number of bags and the launch ends without a tail of SMs that
   // got one CTA more (B = 1024: 640 blocked CTAs are 4.3 per SM).
-  int g = a.interleave ? (threadIdx.x / LANES) * static_cast<int>(gridDim.x) + static_cast<int>(blockIdx.x)
-                       : static_cast<int>(blockIdx.x) * GROUPS + threadIdx.x / LANES;
-  const int cta_has = a.interleave ? static_cast<int>(blockIdx.x) < nbags
-                                   : static_cast<int>(blockIdx.x) * GROUPS < nbags;
+  // (the same predicate as the host's grid choice, sls_interleaved)
+  const bool inter = a.interleave && static_cast<int64_t>(a.nsm) * REC_SLS_MINB * GROUPS >=
+                                         static_cast<int64_t>(a.T) * a.cap;
+  int g = inter ? (threadIdx.x / LANES) * static_cast<int>(gridDim.x) + static_cast<int>(blockIdx.x)
+                : static_cast<int>(blockIdx.x) * GROUPS + threadIdx.x / LANES;
+  const int cta_has = inter ? static_cast<int>(blockIdx.x) < nbags
+                            : static_cast<int>(blockIdx.x) * GROUPS < nbags;
   if (P2P) {
     // sharded: CTAs of the batch all reach the CTA barrier of the flag protocol (groups past
     // the last bag idle on bag 0 and store nothing); CTAs past the batch leave uncounted
@@ -387,7 +390,7 @@ __global__ void __launch_bounds__(THREADS, REC_SLS_MINB) k_sls_synth(const __gri
         p2p.words[1] = static_cast<unsigned>(B);
       }
       __threadfence_system();
-      const unsigned need = a.interleave ? static_cast<unsigned>(min(nbags, static_cast<int>(gridDim.x)))
+      const unsigned need = inter ? static_cast<unsigned>(min(nbags, static_cast<int>(gridDim.x)))
                                          : static_cast<unsigned>((nbags + GROUPS - 1) / GROUPS);
       const unsigned prev = atomicAdd(p2p.counter, 1u);
       if (prev == need - 1) {  // last CTA: every CTA's stores are fenced
@@ -548,6 +551,14 @@ void sls_tma_configure(SlsSynthArgs& a) {
   cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
 }
 
+// The interleaved bag mapping applies when one wave of nsm x REC_SLS_MINB CTAs has a group for
+// every bag of the capacity (each group then handles at most one bag).
+static bool sls_interleaved(const SlsSynthArgs& a) {
+  const int L = a.D / 4 <= 8 ? 8 : a.D / 4 <= 16 ? 16 : 32;
+  return a.interleave && static_cast<int64_t>(a.nsm) * REC_SLS_MINB * (128 / L) >=
+                             static_cast<int64_t>(a.T) * a.cap;
+}
+
 void* sls_synth_kernel(const SlsSynthArgs& a, dim3* grid, dim3* block, size_t* smem) {
   if (a.tma) {
     const int chunk = SLS_TMA_CR * a.D * 4;
@@ -562,8 +573,10 @@ void* sls_synth_kernel(const SlsSynthArgs& a, dim3* grid, dim3* block, size_t* s
   const int L = a.D / 4 <= 8 ? 8 : a.D / 4 <= 16 ? 16 : 32;
   const int nb = a.T * a.cap;
   const int blocked = (nb + THREADS / L - 1) / (THREADS / L);
-  // interleaved: one full wave of nsm x REC_SLS_MINB CTAs (fewer if the capacity is smaller)
-  *grid = dim3(a.interleave ? std::min(blocked, a.nsm * REC_SLS_MINB) : blocked);
+  // interleaved: one full wave of nsm x REC_SLS_MINB CTAs, each group at most one bag - only
+  // when that wave covers every bag of the capacity (RMC1 / RMC3 at d = 1024: 10 240 bags,
+  // 11 840 groups); larger batches keep the blocked multi-wave grid (kernel_interleaved)
+  *grid = dim3(sls_interleaved(a) ? std::min(blocked, a.nsm * REC_SLS_MINB) : blocked);
   *block = dim3(THREADS);
   if (smem) *smem = 0;
   if (a.p2p.peer_X) {

@@ -1286,7 +1286,7 @@ rec_status rec_model_create(const rec_model_desc* d, rec_model_t* out) {
     }
     const char* p = getenv("REC_PDL");
     m->sls_pdl = !(p && strcmp(p, "0") == 0);
-    m->sls_interleave = env_int("REC_SLS_GRID", 1);
+    m->sls_interleave = env_int("REC_SLS_GRID", 0);
     CHECK_CUDA_CREATE(cudaDeviceGetAttribute(&m->nsm, cudaDevAttrMultiProcessorCount, m->device));
     if (want && m->value_mode == REC_VALUES_INT8_EXACT && sls_tma_supported(D) &&
         total_rows < (int64_t(1) << 31)) {

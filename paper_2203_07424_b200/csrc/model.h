@@ -160,7 +160,8 @@ struct rec_model_s {
   CUtensorMap* d_tmap_rows = nullptr;
   int sls_tma = 0, nsm = 0;
   int sls_pdl = 1;    // REC_PDL=0 disables programmatic dependent launch of the SLS
-  int sls_interleave = 1;  // REC_SLS_GRID=0: blocked bag -> CTA mapping (k_sls_synth)
+  int sls_interleave = 0;  // REC_SLS_GRID=1: bags round-robin over one wave (k_sls_synth;
+                           // measured: RMC1 304k vs 326k QPS, serialized 0.56 either way)
   int fuse_dense = 0;
   int chain_pdl = 1;    // top fused MLP launched with PDL after the interaction (REC_CHAIN_PDL)
   int green_sms = 0;    // SMs reserved for the dense stages (REC_GREEN_SMS; 0 = shared SMs)

@@ -101,9 +101,11 @@ static void stage_times(const cudaEvent_t* ev, bool host_mode, double host_in_ms
     }
     return static_cast<double>(x);
   };
-  if (host_mode) {  // 0 -> 1: the batch's H2D copies; then SLS; the rest is dense
+  if (host_mode) {  // 0 -> 1: host packing + the batch's H2D copies (ev 0 is recorded before
+                   // the packing); then SLS; the rest is dense
+    (void)host_in_ms;
     const double in = el(0, 1), sp = el(1, 2), all = el(0, 5);
-    out[0] = in + host_in_ms;
+    out[0] = in;
     out[1] = sp;
     out[2] = std::max(0.0, all - in - sp);
   } else {         // device-synthesised inputs are generated inside the SLS / dense kernels

@@ -39,12 +39,14 @@ def _run(cfg, B, segs, l2=0):
     from paper_2203_07424_b200 import RecModel
     m = RecModel(cfg, seed=1, max_batch=B, l2_persist_bytes=l2)
     ind, off, dense = gen.gen_batch(cfg, 1, segs)
-    eager = np.zeros(B * cfg.tasks, np.float32)
-    m.rec_query(dense, ind, off, B, eager)
+    # graph path FIRST on a fresh handle: no earlier launch has left this batch's pooled
+    # vectors in the workspace, so a kernel that skips bags cannot pass on stale X
     cv = torch.zeros(B * cfg.tasks, device="cuda")
     m.rec_synth_query_async(0, segs, cv)
     m.rec_sync(0)
     graph = cv.cpu().numpy()
+    eager = np.zeros(B * cfg.tasks, np.float32)
+    m.rec_query(dense, ind, off, B, eager)
     m.close()
     return eager, graph
 
@@ -58,8 +60,9 @@ TINY = W.TINY
 VARIANTS = [
     ("sls_tma", {"REC_SLS": "tma"}, RMC1, 700, 0),
     ("sls_no_pdl", {"REC_PDL": "0"}, RMC1, 700, 0),
-    ("sls_blocked_grid", {"REC_SLS_GRID": "0"}, RMC1, 700, 0),
-    ("sls_blocked_grid_rmc2", {"REC_SLS_GRID": "0"}, W.small_variant(W.RMC2, 4096), 1024, 0),
+    ("sls_interleaved_grid", {"REC_SLS_GRID": "1"}, RMC1, 1024, 0),
+    ("sls_interleaved_grid_rmc2", {"REC_SLS_GRID": "1"}, W.small_variant(W.RMC2, 4096), 1024, 0),
+    ("sls_interleaved_grid_rmc1_big", {"REC_SLS_GRID": "1"}, RMC1, 4096, 0),
     ("hot_policy_l2_window", {"REC_HOT_POLICY": "1"}, RMC1.with_(index_dist=W.INDEX_SKEW2), 700, 8 << 20),
     ("l2_window", {}, RMC1, 700, 8 << 20),
     ("fuse_dense", {"REC_FUSE_DENSE": "1"}, RMC1, 700, 0),
