@@ -35,6 +35,8 @@ def main():
     ap.add_argument("--batch", type=int, default=1024)
     ap.add_argument("--probe-s", type=float, default=1.2, help="trace span per probe (s)")
     ap.add_argument("--host-queries", type=int, default=20000, help="cap per probe in host mode")
+    ap.add_argument("--host-gb", type=float, default=6.0,
+                    help="host mode: cap of the materialised per-probe inputs (pinned host GB)")
     a = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -49,6 +51,9 @@ def main():
         m = RecModel(cfg, seed=1, max_batch=a.batch, streams=a.streams, device=local)
         sat = bench.saturation(m, cfg, a.batch, a.streams, 4, 2, 128, 20000, rank, world, dist)
         out.setdefault("saturation_qps", {})[cfg.name] = sat["value"]
+        # host mode materialises every query's inputs in host memory before the clock starts
+        item_bytes = 4 * (cfg.num_tables * (0.5 * (cfg.pooling_lo + cfg.pooling_hi) + 1) + cfg.dense_dim)
+        host_cap = int(min(a.host_queries, a.host_gb * 1e9 / (150.0 * item_bytes)))
         for mode in a.modes.split(","):
             im = REC_INPUT_HOST if mode == "host" else REC_INPUT_DEVICE_SYNTH
             for sla in [float(x) for x in a.slas.split(",")]:
@@ -59,7 +64,7 @@ def main():
                     def probe(lam):
                         n = int(max(2000, lam * a.probe_s))
                         if mode == "host":
-                            n = min(n, a.host_queries * world)
+                            n = min(n, host_cap * world)
                         tr = W.poisson_trace(lam, n, seed=seed)
                         mine = rank_share(tr, world, rank)
                         r = m.rec_serve(mine, sla, a.streams, a.batch, input_mode=im, warmup_frac=0.1)
@@ -109,7 +114,7 @@ def main():
                         m.rec_profile(True)
                         n = int(max(2000, 0.5 * lo * a.probe_s))
                         if mode == "host":
-                            n = min(n, a.host_queries * world)
+                            n = min(n, host_cap * world)
                         tr = W.poisson_trace(0.5 * lo, n, seed=seed)
                         r = m.rec_serve(rank_share(tr, world, rank), sla, a.streams, a.batch, input_mode=im,
                                         warmup_frac=0.1)
