@@ -9,7 +9,8 @@ counter (ctr0, ctr1, ctr2 = (table<<8)|domain, ctr3) under key = seed:
 
   domain 1  index   E-table row of (query q, item i, table t, slot j): ctr (j, i, t<<8|1, q)
   domain 2  length  pooling factor of (q, i, t) when pooling varies:  ctr (0, i, t<<8|2, q)
-  domain 3  dense   dense feature f of (q, i):                         ctr (f, i, 3, q)
+  domain 3  dense   dense features 16f'..16f'+15 of (q, i):             ctr (f', i, 3, q)
+                    (feature f = byte f mod 16 of the 16-byte output, round 2)
   domain 4  table   E_t[r][k]:                                         ctr (k, r, t<<8|4, 0)
   domain 5  weight  layer l, W[o][i]:                                  ctr (i, o, l<<8|5, 0)
   domain 6  bias    layer l, b[o]:                                     ctr (o, 0, l<<8|6, 0)
@@ -200,12 +201,20 @@ def zipf_rows(r: np.ndarray, R: int, t: int) -> np.ndarray:
 
 
 def dense_features(seed: int, F: int, q: np.ndarray, it: np.ndarray) -> np.ndarray:
-    """dense [B][F] in float64 (exact int8 * 2^-7 values) (G4)."""
+    """dense [B][F] in float64 (exact int8 * 2^-7 values) (G4, round 2): feature f
+    of (q, item) is byte f mod 16 of the 16-byte little-endian output (w0, w1, w2, w3) of
+    philox((f // 16, item, 3, q)), read as int8, times 2^-7."""
     k0, k1 = seed_key(seed)
-    f = np.arange(F, dtype=np.uint64).reshape(1, -1)
-    w0, _, _, _ = philox(f, it.astype(np.uint64).reshape(-1, 1), np.uint64(3),
-                         q.astype(np.uint64).reshape(-1, 1), k0, k1)
-    return _int8_low_byte(w0).astype(np.float64) * 2.0 ** -7
+    nblk = (F + 15) // 16
+    blk = np.arange(nblk, dtype=np.uint64).reshape(1, -1)
+    w = philox(blk, it.astype(np.uint64).reshape(-1, 1), np.uint64(3),
+               q.astype(np.uint64).reshape(-1, 1), k0, k1)            # 4 x [B][nblk]
+    B = np.asarray(it).size
+    out = np.empty((B, nblk * 16), dtype=np.float64)
+    for j in range(16):                                                # byte j of the block
+        word = w[j // 4]
+        out[:, j::16] = _int8_low_byte(word >> np.uint64(8 * (j % 4))).astype(np.float64)
+    return out[:, :F] * 2.0 ** -7
 
 
 def gen_batch(cfg, seed: int, segs, rows: Sequence[int] = None):

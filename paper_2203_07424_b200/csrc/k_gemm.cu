@@ -464,6 +464,7 @@ void gemm_prepare() {
 int g_gemm_2sm = 0;     // REC_GEMM_2SM: CTA-pair GEMM for full-GPU launches (experimental)
 int g_gemm_mt1 = 0;     // REC_GEMM_MT1=1: 128x256 tiles (one M tile per CTA) for full-GPU launches too (A/B)
 int g_gemm_narrow = 0;  // REC_GEMM_NARROW=n: 128-wide N tiles below n 128x256 tiles (measured: RMC2/3 +0.5-1 %, MT-WnD -7 %)
+int g_gemm_mt2 = 0;     // REC_GEMM_MT2=1: 256 x 256 weight-sharing tiles also for serving batches
 int g_gemm_bn64 = 0;    // REC_GEMM_BN64=1: 64-wide serving tiles (below; measured: RMC3 -4 % at 16
                         // co-located streams, -11 % at 32, RMC2 +2 %: off by default)
 
@@ -488,7 +489,7 @@ void launch_gemm_tc(const CUtensorMap* tmap_a, const CUtensorMap* tmap_w, const 
   if (a.N <= 32) launch_bn<32, 1>(tmap_a, tmap_w, a, s);
   else if (a.N <= 64) launch_bn<64, 1>(tmap_a, tmap_w, a, s);
   else if (a.N <= 128) launch_bn<128, 1>(tmap_a, tmap_w, a, s);
-  else if (((a.M + 255) / 256) * ((a.N + 255) / 256) >= 148 && a.K >= 512) {
+  else if ((((a.M + 255) / 256) * ((a.N + 255) / 256) >= 148 || g_gemm_mt2) && a.K >= 512) {
     if (g_gemm_2sm && tmap_w_half) launch_2sm<256>(tmap_a, tmap_w_half, a, s);  // CTA pairs
     else if (g_gemm_mt1) launch_bn<256, 1>(tmap_a, tmap_w, a, s);
     else launch_bn<256, 2>(tmap_a, tmap_w, a, s);  // enough 256-row tiles to fill the GPU: share W

@@ -406,12 +406,9 @@ __global__ void __launch_bounds__(THREADS, REC_SLS_MINB) k_sls_synth(const __gri
   if (active)
     *reinterpret_cast<float4*>(a.X + static_cast<int64_t>(b) * a.x_stride +
                                static_cast<int64_t>(1 + t) * a.D + col) = acc;
-  if (a.dense_bf && t == 0) {  // dense features of item b (same arithmetic as k_gen_dense_seg)
-    for (int f = sub; f < a.Fpad; f += LANES) {
-      const float v = f < a.F ? gen_dense(f, qi.y, qi.x, a.k0, a.k1) : 0.f;
-      a.dense_bf[static_cast<int64_t>(b) * a.Fpad + f] = __float2bfloat16_rn(v);
-    }
-  }
+  if (a.dense_bf && t == 0)  // dense features of item b (same arithmetic as k_gen_dense_seg)
+    gen_dense_row(qi.y, qi.x, a.k0, a.k1, a.F, a.Fpad, a.dense_bf + static_cast<int64_t>(b) * a.Fpad,
+                  nullptr, sub, LANES);
   SLS_STAMP(3);
 }
 

@@ -99,14 +99,8 @@ __global__ void __launch_bounds__(32 * kGenWPB) k_gen_fused(const __grid_constan
     const int b = (blockIdx.x - ga.nbag_blocks) * kGenWPB + (threadIdx.x >> 5);
     if (b >= B) return;
     const int2 qi = row_item(sb, b);
-    for (int f = lane; f < ga.Fpad; f += 32) {
-      float v = 0.f;
-      if (f < ga.F) {
-        v = gen_dense(f, qi.y, qi.x, ga.k0, ga.k1);
-        if (ga.dense_f32) ga.dense_f32[static_cast<int64_t>(b) * ga.F + f] = v;
-      }
-      ga.dense_bf[static_cast<int64_t>(b) * ga.Fpad + f] = __float2bfloat16_rn(v);
-    }
+    gen_dense_row(qi.y, qi.x, ga.k0, ga.k1, ga.F, ga.Fpad, ga.dense_bf + static_cast<int64_t>(b) * ga.Fpad,
+                  ga.dense_f32 ? ga.dense_f32 + static_cast<int64_t>(b) * ga.F : nullptr, lane, 32);
   }
 }
 
@@ -119,11 +113,8 @@ __global__ void __launch_bounds__(32 * kGenWPB) k_gen_dense_seg(const __grid_con
   if (b >= sb.B) return;
   const int lane = threadIdx.x & 31;
   const int2 qi = row_item(sb, b);
-  for (int f = lane; f < ga.Fpad; f += 32) {
-    float v = 0.f;
-    if (f < ga.F) v = gen_dense(f, qi.y, qi.x, ga.k0, ga.k1);
-    ga.dense_bf[static_cast<int64_t>(b) * ga.Fpad + f] = __float2bfloat16_rn(v);
-  }
+  gen_dense_row(qi.y, qi.x, ga.k0, ga.k1, ga.F, ga.Fpad, ga.dense_bf + static_cast<int64_t>(b) * ga.Fpad,
+                nullptr, lane, 32);
 }
 
 void* gen_dense_seg_kernel(const GenArgs& ga, dim3* grid, dim3* block) {
@@ -245,16 +236,21 @@ __global__ void k_gen_dense(const int* __restrict__ rowq, const int* __restrict_
                             const int* __restrict__ dB, int F, int Fpad, uint32_t k0, uint32_t k1,
                             __nv_bfloat16* __restrict__ dbf, float* __restrict__ df) {
   const int B = *dB;
-  const int64_t n = (int64_t)B * Fpad;
+  const int nblk = (Fpad + 15) / 16;
+  const int64_t n = (int64_t)B * nblk;  // one thread per (row, 16-feature block)
   for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < n;
        x += (int64_t)gridDim.x * blockDim.x) {
-    const int b = static_cast<int>(x / Fpad), f = static_cast<int>(x % Fpad);
-    float v = 0.f;
-    if (f < F) {
-      v = gen_dense(f, rowi[b], rowq[b], k0, k1);
-      if (df) df[(int64_t)b * F + f] = v;
+    const int b = static_cast<int>(x / nblk), blk = static_cast<int>(x % nblk);
+    float v[16];
+    gen_dense16(static_cast<uint32_t>(blk), rowi[b], rowq[b], k0, k1, v);
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int f = blk * 16 + j;
+      if (f >= Fpad) break;
+      const float x16 = f < F ? v[j] : 0.f;
+      if (df && f < F) df[(int64_t)b * F + f] = x16;
+      if (dbf) dbf[(int64_t)b * Fpad + f] = __float2bfloat16_rn(x16);
     }
-    if (dbf) dbf[x] = __float2bfloat16_rn(v);
   }
 }
 

@@ -829,7 +829,10 @@ rec_status rec_serve(rec_model_t m, const rec_trace_row* trace, int64_t n, doubl
     // (streams s = t, t + nthreads, ...).  Measured (scripts/serve_probe.py, RMC1, m = 8):
     // 1 thread sustains 305k QPS, 2 threads 288k, 8 threads 277k — concurrent graph launches
     // from several host threads contend inside the CUDA driver.  REC_SERVE_THREADS overrides.
-    int nthreads = 1;
+    // Host-input mode: each batch's inputs are packed into pinned staging on the
+    // host (megabytes per batch), so packing, not graph launching, bounds a single thread —
+    // one dispatcher thread per stream (at most 8) packs in parallel.
+    int nthreads = pol->input_mode == REC_INPUT_HOST ? std::min(M, 8) : 1;
     if (const char* e = getenv("REC_SERVE_THREADS")) nthreads = std::max(1, std::min(M, atoi(e)));
     struct Own {
       uint32_t seq = 0;

@@ -64,9 +64,41 @@ __device__ __forceinline__ int gen_index(uint32_t j, uint32_t it, uint32_t c2, u
   return static_cast<int>(__umul64hi(r, R));
 }
 
+// Dense features (G4, round 2): feature f of (q, item) is byte f mod 16 of the 16-byte
+// little-endian output (w0, w1, w2, w3) of philox((f / 16, item, 3, q)), as int8 * 2^-7 — one
+// Philox evaluation per 16 features (RMC3's 2560 features per item cost one Philox each in
+// round 1, as much ALU as the whole SLS).  gen_dense16 returns the 16 values of block blk.
+__device__ __forceinline__ void gen_dense16(uint32_t blk, uint32_t it, uint32_t q, uint32_t k0,
+                                            uint32_t k1, float v[16]) {
+  const U4 w = philox(blk, it, DOM_DENSE, q, k0, k1);
+  const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+  for (int j = 0; j < 16; ++j) v[j] = i8(ws[j >> 2] >> (8 * (j & 3))) * pow2f(-7);
+}
 __device__ __forceinline__ float gen_dense(uint32_t f, uint32_t it, uint32_t q, uint32_t k0,
                                            uint32_t k1) {
-  return i8(philox(f, it, DOM_DENSE, q, k0, k1).x) * pow2f(-7);
+  const U4 w = philox(f >> 4, it, DOM_DENSE, q, k0, k1);
+  const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+  const int j = static_cast<int>(f & 15);
+  return i8(ws[j >> 2] >> (8 * (j & 3))) * pow2f(-7);
+}
+// Row b of bf16 [.][Fpad] (and optionally fp32 [.][F]) for (q, item): lanes `lane`, `lane +
+// nl`, ... of a group of nl threads each own 16-feature blocks.
+__device__ __forceinline__ void gen_dense_row(uint32_t it, uint32_t q, uint32_t k0, uint32_t k1, int F,
+                                              int Fpad, __nv_bfloat16* __restrict__ bf,
+                                              float* __restrict__ f32, int lane, int nl) {
+  for (int blk = lane; blk * 16 < Fpad; blk += nl) {
+    float v[16];
+    gen_dense16(static_cast<uint32_t>(blk), it, q, k0, k1, v);
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int f = blk * 16 + j;
+      if (f >= Fpad) break;
+      const float x = f < F ? v[j] : 0.f;
+      bf[f] = __float2bfloat16_rn(x);
+      if (f32 && f < F) f32[f] = x;
+    }
+  }
 }
 
 }  // namespace rec

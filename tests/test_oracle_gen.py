@@ -178,3 +178,18 @@ def test_zipf_rows_bijection_and_generator_counters():
                 assert abs(rk - rank) <= 1
                 assert idx[pos] == (rk * gen.ZIPF_MULT + gen.ZIPF_T_OFF * t) % 5000
                 pos += 1
+
+
+def test_dense_features_byte_layout_scalar_rebuild():
+    """G4 dense features: feature f of (q, item) = int8 of byte f mod 16 of the little-endian
+    16-byte Philox output of counter (f // 16, item, 3, q), times 2^-7 (scalar rebuild from the
+    KAT-pinned scalar generator, bytes extracted by hand)."""
+    q, it, F = np.array([5, 900]), np.array([3, 77]), 45
+    d = gen.dense_features(9, F, q, it)
+    k0, k1 = ph.seed_key(9)
+    for b in range(2):
+        for f in range(F):
+            w = ph.philox_scalar([f // 16, int(it[b]), 3, int(q[b])], [k0, k1])
+            raw = b"".join(int(x).to_bytes(4, "little") for x in w)[f % 16]
+            val = raw - 256 if raw >= 128 else raw
+            assert d[b, f] == val * 2.0 ** -7
