@@ -241,15 +241,13 @@ __global__ void k_gen_dense(const int* __restrict__ rowq, const int* __restrict_
   for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < n;
        x += (int64_t)gridDim.x * blockDim.x) {
     const int b = static_cast<int>(x / nblk), blk = static_cast<int>(x % nblk);
-    float v[16];
-    gen_dense16(static_cast<uint32_t>(blk), rowi[b], rowq[b], k0, k1, v);
-#pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      const int f = blk * 16 + j;
-      if (f >= Fpad) break;
-      const float x16 = f < F ? v[j] : 0.f;
-      if (df && f < F) df[(int64_t)b * F + f] = x16;
-      if (dbf) dbf[(int64_t)b * Fpad + f] = __float2bfloat16_rn(x16);
+    if (dbf) {
+      gen_dense_row(static_cast<uint32_t>(rowi[b]), static_cast<uint32_t>(rowq[b]), k0, k1, F, Fpad,
+                    dbf + (int64_t)b * Fpad, df ? df + (int64_t)b * F : nullptr, blk, 1 << 30);
+    } else {
+      float v[16];
+      gen_dense16(static_cast<uint32_t>(blk), rowi[b], rowq[b], k0, k1, v);
+      for (int j = 0; j < 16 && blk * 16 + j < F; ++j) df[(int64_t)b * F + blk * 16 + j] = v[j];
     }
   }
 }

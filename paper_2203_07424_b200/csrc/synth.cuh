@@ -90,9 +90,31 @@ __device__ __forceinline__ void gen_dense_row(uint32_t it, uint32_t q, uint32_t 
   for (int blk = lane; blk * 16 < Fpad; blk += nl) {
     float v[16];
     gen_dense16(static_cast<uint32_t>(blk), it, q, k0, k1, v);
+    const int f0 = blk * 16;
+    if (f0 + 16 <= F && f0 + 16 <= Fpad) {
+      // whole block: two 16-byte stores (bf rows start 16-byte aligned: Fpad % 8 == 0), so a
+      // warp writes contiguous 512-byte runs instead of 2-byte scalars at a 32-byte stride
+      uint32_t p[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * j], v[2 * j + 1]);
+        p[j] = *reinterpret_cast<uint32_t*>(&h);
+      }
+      uint4* d = reinterpret_cast<uint4*>(bf + f0);
+      d[0] = make_uint4(p[0], p[1], p[2], p[3]);
+      d[1] = make_uint4(p[4], p[5], p[6], p[7]);
+      if (f32) {
+        float4* o = reinterpret_cast<float4*>(f32 + f0);  // (rec_gen_batch only; F % 4 alignment
+#pragma unroll                                          //  not guaranteed -> scalar below if not)
+        for (int j = 0; j < 4; ++j)
+          if ((reinterpret_cast<uintptr_t>(o) & 15) == 0) o[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+          else for (int k = 0; k < 4; ++k) f32[f0 + 4 * j + k] = v[4 * j + k];
+      }
+      continue;
+    }
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
-      const int f = blk * 16 + j;
+      const int f = f0 + j;
       if (f >= Fpad) break;
       const float x = f < F ? v[j] : 0.f;
       bf[f] = __float2bfloat16_rn(x);
