@@ -243,7 +243,7 @@ __global__ void k_gen_dense(const int* __restrict__ rowq, const int* __restrict_
     const int b = static_cast<int>(x / nblk), blk = static_cast<int>(x % nblk);
     if (dbf) {
       gen_dense_row(static_cast<uint32_t>(rowi[b]), static_cast<uint32_t>(rowq[b]), k0, k1, F, Fpad,
-                    dbf + (int64_t)b * Fpad, df ? df + (int64_t)b * F : nullptr, blk, 1 << 30);
+                    dbf + (int64_t)b * Fpad, df ? df + (int64_t)b * F : nullptr, blk, nblk);  // this block only
     } else {
       float v[16];
       gen_dense16(static_cast<uint32_t>(blk), rowi[b], rowq[b], k0, k1, v);

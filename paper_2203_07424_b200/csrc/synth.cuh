@@ -87,7 +87,8 @@ __device__ __forceinline__ float gen_dense(uint32_t f, uint32_t it, uint32_t q, 
 __device__ __forceinline__ void gen_dense_row(uint32_t it, uint32_t q, uint32_t k0, uint32_t k1, int F,
                                               int Fpad, __nv_bfloat16* __restrict__ bf,
                                               float* __restrict__ f32, int lane, int nl) {
-  for (int blk = lane; blk * 16 < Fpad; blk += nl) {
+  const int nblk = (Fpad + 15) / 16;
+  for (int blk = lane; blk < nblk; blk += nl) {  // (no blk * 16 in the bound: nl may be huge)
     float v[16];
     gen_dense16(static_cast<uint32_t>(blk), it, q, k0, k1, v);
     const int f0 = blk * 16;
