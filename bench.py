@@ -381,8 +381,9 @@ def default_streams(args, name: str) -> int:
 def per_model(name, args, rank, world, dist, local, hbm_peak):
     """The metric is per model (BASELINE.json: "SLA-bounded QPS (p95) per model at 1/2/4/8
     B200"): saturation QPS (the same step definition at fewer steps), the SLS roofline of
-    back-to-back launches, and lambda* at the model's paper SLA for the fixed
-    co-location policy m = 8 streams, d = 1024 (the Alg. 1 search runs for the headline model)."""
+    back-to-back launches, and lambda* at the model's paper SLA for the saturation
+    step's co-location (m = 16, RMC3 32) and d = 1024 (the Alg. 1 search runs for the headline
+    model)."""
     import torch
     from paper_2203_07424_b200 import RecModel
     cfg = W.SHORT[name]
@@ -411,8 +412,9 @@ def per_model(name, args, rank, world, dist, local, hbm_peak):
                                1e12 / world / peaks()[1])
     if args.pm_sla:
         n = int(max(30000, 1.5 * sat["value"]))
-        lam, pr = sla_search(model, cfg, world, rank, dist, 8, d, 0.5 * sat["value"], n, cfg.sla_ms)
-        out["sla"] = {"sla_ms": cfg.sla_ms, "lambda_star_qps": lam, "policy": {"streams": 8, "max_batch": d},
+        ms = min(m_streams, 16 if name != "rmc3" else 32)   # the saturation step's co-location
+        lam, pr = sla_search(model, cfg, world, rank, dist, ms, d, 0.5 * sat["value"], n, cfg.sla_ms)
+        out["sla"] = {"sla_ms": cfg.sla_ms, "lambda_star_qps": lam, "policy": {"streams": ms, "max_batch": d},
                       "queries_per_probe": n, "probes": pr,
                       "saturation_ge_lambda_star": bool(sat["value"] >= 0.98 * lam)}
     model.close()
