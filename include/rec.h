@@ -289,6 +289,17 @@ rec_status rec_split_fuse(const rec_trace_row* trace, int64_t n, int32_t max_bat
                           int32_t* segs_out, int64_t seg_cap, int64_t* batch_start,
                           int64_t bcap, int64_t* nbatches, int64_t* nsegs);
 
+/* The deterministic global dispatcher of sharded serving (R31; host-only): split
+ * every query into sub-queries of <= max_batch items (S1), then cut the FIFO into batches of
+ * whole sub-queries with cumulative size <= max_batch; a batch closes when it is full (the
+ * next sub-query does not fit, or it holds exactly max_batch items: close = that arrival) or
+ * tau_ms after its first sub-query arrived, whichever comes first; close times are made
+ * non-decreasing.  Output as rec_split_fuse plus close_s[b] (trace time, seconds).
+ * Errors: INVALID_ARG (tau_ms <= 0, bad trace, capacity). */
+rec_status rec_global_batches(const rec_trace_row* trace, int64_t n, int32_t max_batch, double tau_ms,
+                              int32_t* segs_out, int64_t seg_cap, int64_t* batch_start, double* close_s,
+                              int64_t bcap, int64_t* nbatches, int64_t* nsegs);
+
 /* Serve a query trace (rows sorted by arrival_s, qid unique) on this GPU under the
  * policy: split each query into chunks of d (S1), fuse FIFO chunks with
  * cumulative size <= d (S2) onto the lowest idle of m streams (S3), run the

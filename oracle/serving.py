@@ -19,6 +19,8 @@ SLA latency target" (latency-bounded throughput).
                        arrivals, then completions, then dispatch decisions
   S5 metric            p95 nearest rank over post-warm-up queries; lambda* by
                        geometric bracketing + bisection
+  R31 global batches   sharded serving: batches cut from the trace alone (full, or tau after
+                       the first sub-query arrived), so every rank runs the same batches
 """
 from __future__ import annotations
 
@@ -261,3 +263,46 @@ def brute_force_search(evaluate, ms, ds):
             if best is None or key > best[0]:
                 best = (key, m, d, v)
     return dict(m=best[1], d=best[2], qps=best[3])
+
+
+def global_batches(arrival_s, sizes, qids, d: int, tau_s: float):
+    """R31: the deterministic batch cut of sharded serving, step by step.
+
+    Sub-queries in FIFO (trace) order, each query split by S1.  Batch: starting at the oldest
+    pending sub-query (arrival a0), take sub-queries in order while the cumulative size stays
+    <= d and the sub-query arrived by a0 + tau (at least one).  The batch closes at
+      * the arrival of its last sub-query if it holds exactly d items,
+      * else the arrival of the next sub-query if that one arrived by a0 + tau (it did not fit),
+      * else a0 + tau;
+    and never before the previous batch's close.  Returns (segs [(qid, start, len)],
+    batch_start, close)."""
+    subs = []
+    for a, n, q in zip(arrival_s, sizes, qids):
+        for st, ln in split(int(n), d):
+            subs.append((float(a), int(q), st, ln))
+    segs, bstart, close = [], [0], []
+    prev = -np.inf
+    i = 0
+    while i < len(subs):
+        a0 = subs[i][0]
+        deadline = a0 + tau_s
+        j, items = i, 0
+        while j < len(subs) and items + subs[j][3] <= d and subs[j][0] <= deadline:
+            items += subs[j][3]
+            j += 1
+        if j == i:
+            items += subs[j][3]
+            j += 1
+        if items == d:
+            c = subs[j - 1][0]
+        elif j < len(subs) and subs[j][0] <= deadline:
+            c = subs[j][0]
+        else:
+            c = deadline
+        c = max(c, prev)
+        segs.extend((q, st, ln) for _, q, st, ln in subs[i:j])
+        bstart.append(j)
+        close.append(c)
+        prev = c
+        i = j
+    return np.array(segs, dtype=np.int32).reshape(-1, 3), np.array(bstart), np.array(close)

@@ -5,6 +5,7 @@ kernels + C++ serving runtime); this package only builds it (build.py) and binds
 (binding.py, ctypes marshalling).  It never imports the oracle.
 """
 from .binding import (RecModel, RecError, lib, nccl_unique_id, rec_split_fuse, rec_shard_plan, EXPORTS, STATUS,  # noqa: F401
+                      rec_global_batches,
                       REC_VALUES_INT8_EXACT, REC_VALUES_FP32, REC_INDEX_UNIFORM, REC_INDEX_SKEW2,
                       REC_SHARD_REPLICA, REC_SHARD_TABLE, REC_SHARD_ROW, REC_INPUT_DEVICE_SYNTH,
                       REC_INPUT_HOST, REC_CLOCK_REAL, REC_CLOCK_VIRTUAL, KERNEL_SLS, KERNEL_GEMM,

@@ -34,7 +34,7 @@ EXPORTS = ["rec_model_create", "rec_model_destroy", "rec_query", "rec_query_debu
            "rec_nccl_unique_id_size", "rec_nccl_get_unique_id", "rec_version", "rec_split_fuse",
            "rec_synth_query_batches", "rec_shard_plan", "rec_bench_mlp", "rec_bench_sls", "rec_set_pipeline", "rec_synth_query_pipeline",
            "rec_debug_chain_timeline", "rec_query_inspect", "rec_hot_remap",
-           "rec_bench_sls_caller"]
+           "rec_bench_sls_caller", "rec_global_batches"]
 
 
 class rec_model_desc(C.Structure):
@@ -121,6 +121,9 @@ def lib() -> C.CDLL:
         L.rec_hot_remap.restype = i32
         L.rec_bench_sls_caller.argtypes = [vp, vp, vp, i32, i32, i64, C.POINTER(C.c_double)]
         L.rec_bench_sls_caller.restype = i32
+        L.rec_global_batches.argtypes = [vp, i64, i32, C.c_double, vp, i64, vp, vp, i64,
+                                         C.POINTER(i64), C.POINTER(i64)]
+        L.rec_global_batches.restype = i32
         for f in ("rec_model_create", "rec_query", "rec_query_debug", "rec_query_async",
                   "rec_synth_query_async", "rec_sync", "rec_gen_batch", "rec_profile",
                   "rec_profile_read", "rec_serve", "rec_nccl_get_unique_id"):
@@ -341,6 +344,20 @@ def rec_split_fuse(trace: np.ndarray, max_batch: int):
     _check(lib().rec_split_fuse(_ptr(trace), n, max_batch, _ptr(segs), cap, _ptr(bstart), cap + 1,
                                 C.byref(nb), C.byref(ns)))
     return segs[:ns.value], bstart[:nb.value + 1]
+
+
+def rec_global_batches(trace: np.ndarray, max_batch: int, tau_ms: float):
+    """R31 deterministic global batch cut (host-only C++): (segs [n][3], batch_start, close_s)."""
+    trace = np.ascontiguousarray(trace)
+    n = len(trace)
+    cap = int(sum(-(-int(s) // max_batch) for s in trace["size"])) if n and max_batch > 0 else 0
+    segs = np.zeros((max(cap, 1), 3), dtype=np.int32)
+    bstart = np.zeros(cap + 2, dtype=np.int64)
+    close = np.zeros(cap + 1, dtype=np.float64)
+    nb, ns = C.c_int64(), C.c_int64()
+    _check(lib().rec_global_batches(_ptr(trace), n, max_batch, tau_ms, _ptr(segs), cap, _ptr(bstart),
+                                    _ptr(close), cap + 1, C.byref(nb), C.byref(ns)))
+    return segs[:ns.value], bstart[:nb.value + 1], close[:nb.value]
 
 
 def rec_shard_plan(rows, world: int, rank: int, shard: int, batch: int) -> dict:

@@ -575,6 +575,46 @@ rec_status rec_split_fuse(const rec_trace_row* trace, int64_t n, int32_t max_bat
   return REC_OK;
 }
 
+rec_status rec_global_batches(const rec_trace_row* trace, int64_t n, int32_t max_batch, double tau_ms,
+                              int32_t* segs_out, int64_t seg_cap, int64_t* batch_start, double* close_s,
+                              int64_t bcap, int64_t* nbatches, int64_t* nsegs) {
+  if (!trace || !segs_out || !batch_start || !close_s || !nbatches || !nsegs || n < 0) {
+    set_error("null argument");
+    return REC_E_INVALID_ARG;
+  }
+  if (max_batch < 1 || !(tau_ms > 0)) {
+    set_error("max_batch >= 1 and tau_ms > 0 are required");
+    return REC_E_INVALID_ARG;
+  }
+  std::vector<Chunk> ch;
+  for (int64_t p = 0; p < n; ++p) {
+    if (trace[p].size < 1 || (p > 0 && trace[p].arrival_s < trace[p - 1].arrival_s)) {
+      set_error("trace[%lld]: size >= 1 and non-decreasing arrival_s required", (long long)p);
+      return REC_E_INVALID_ARG;
+    }
+    split_query(trace[p], p, max_batch, ch);
+  }
+  std::vector<ShardBatch> bt;
+  cut_batches(trace, ch, max_batch, tau_ms * 1e-3, bt);
+  if (static_cast<int64_t>(ch.size()) > seg_cap || static_cast<int64_t>(bt.size()) > bcap) {
+    set_error("capacity too small (%zu sub-queries, %zu batches)", ch.size(), bt.size());
+    return REC_E_INVALID_ARG;
+  }
+  for (size_t i = 0; i < ch.size(); ++i) {
+    segs_out[3 * i] = ch[i].qid;
+    segs_out[3 * i + 1] = ch[i].start;
+    segs_out[3 * i + 2] = ch[i].len;
+  }
+  batch_start[0] = 0;
+  for (size_t k = 0; k < bt.size(); ++k) {
+    batch_start[k + 1] = bt[k].c0 + bt[k].nc;
+    close_s[k] = bt[k].close;
+  }
+  *nbatches = static_cast<int64_t>(bt.size());
+  *nsegs = static_cast<int64_t>(ch.size());
+  return REC_OK;
+}
+
 rec_status rec_serve(rec_model_t m, const rec_trace_row* trace, int64_t n, double sla_ms,
                      const rec_serve_policy* pol, rec_serve_report* out, double* latency_ms,
                      int32_t* batch_log, int64_t log_cap, int64_t* log_rows, float* ctr_out) {

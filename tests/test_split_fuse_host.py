@@ -44,3 +44,37 @@ def test_split_fuse_errors():
     tr["size"][2] = 0
     with pytest.raises(RecError):
         rec_split_fuse(tr, 16)
+
+
+def test_global_batches_match_oracle_and_invariants():
+    """R31 (sharded serving's deterministic dispatcher): the C++ cut equals the oracle's
+    step-by-step cut on random Poisson traces (batch lists bit-exact, close times exact), and
+    the invariants hold: coverage exactly once with S1 boundaries, FIFO, sum <= d, every batch
+    full or closed at first arrival + tau, non-decreasing close times."""
+    from paper_2203_07424_b200 import rec_global_batches
+    from oracle import serving as sv
+    for seed, rate, d, tau in ((1, 2000.0, 1024, 1.0), (2, 30000.0, 256, 0.5), (3, 500.0, 1024, 5.0),
+                               (4, 100000.0, 512, 0.2)):
+        tr = W.poisson_trace(rate, 400, seed=seed)
+        segs, bst, close = rec_global_batches(tr, d, tau)
+        osegs, obst, oclose = sv.global_batches(tr["arrival_s"], tr["size"], tr["qid"], d, tau * 1e-3)
+        assert np.array_equal(segs, osegs) and np.array_equal(bst, obst)
+        assert np.array_equal(close, oclose)
+        assert np.all(np.diff(close) >= 0)
+        arr = dict(zip(tr["qid"].tolist(), tr["arrival_s"].tolist()))
+        for b in range(len(bst) - 1):
+            sg = segs[bst[b]:bst[b + 1]]
+            items = int(sg[:, 2].sum())
+            assert items <= d or len(sg) == 1
+            first = arr[int(sg[0, 0])]
+            assert close[b] >= first - 1e-15
+            if items < d and b + 1 < len(bst) - 1:
+                nxt = segs[bst[b + 1]]
+                full = items + int(nxt[2]) > d and arr[int(nxt[0])] <= first + tau * 1e-3
+                assert full or abs(close[b] - max(first + tau * 1e-3, close[b - 1] if b else -1)) < 1e-12
+        # coverage: every query's items exactly once, in S1 chunks
+        got = {}
+        for q, st, ln in segs:
+            got.setdefault(int(q), []).append((int(st), int(ln)))
+        for q, n in zip(tr["qid"], tr["size"]):
+            assert got[int(q)] == sv.split(int(n), d)
