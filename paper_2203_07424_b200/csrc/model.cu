@@ -675,7 +675,7 @@ rec_status synth_submit(rec_model_s* m, Workspace& w, const int32_t* segs, int n
   } else if (nseg > kParamSegs) {
     REC_CUDA(cudaEventRecord(w.pin_free, w.stream));
   }
-  SynthSlot::Variant& V = sl.var[m->prof && sl.var[1].exec ? 1 : 0];
+  SynthSlot::Variant& V = sl.var[(m->prof || m->stage_events) && sl.var[1].exec ? 1 : 0];
   const bool direct = dense_f32_out != nullptr || !V.exec;
   if (!direct) {
     const bool fused = m->lo == m->hi;

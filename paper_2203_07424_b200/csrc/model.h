@@ -148,6 +148,8 @@ struct rec_model_s {
   int64_t* d_remap_off = nullptr;
   int64_t hot_window = 0;
   bool counted = false;                // counted in the per-device co-located model registry
+  bool stage_events = false;           // rec_serve breakdown: graphs with stage events, read by
+                                       // the server (not accumulated into the profile counters)
   // embedding arena
   float* tables = nullptr;
   size_t table_bytes = 0;

@@ -700,7 +700,17 @@ rec_status rec_serve(rec_model_t m, const rec_trace_row* trace, int64_t n, doubl
   // read-back cost serving throughput (measured: RMC1 lambda* 317k -> 206k QPS)
   const bool breakdown = m->prof;
   const bool synth_events = breakdown && m->ws[0].slots[0].var[1].exec != nullptr;
+  // during serving the stage events are read per batch here; the profile counters (which
+  // would read them again when a staging slot is reused) stay off
+  const bool prof_saved = m->prof;
+  if (breakdown) {
+    for (auto& w : m->ws) REC_CUDA(cudaStreamSynchronize(w.stream));
+    m->prof = false;
+    m->stage_events = synth_events;
+  }
   auto cleanup = [&]() {
+    m->prof = prof_saved;
+    m->stage_events = false;
     for (auto& L : lanes) {
       if (L.done) cudaEventDestroy(L.done);
       if (L.ctr_host) cudaFreeHost(L.ctr_host);

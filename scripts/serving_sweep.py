@@ -3,7 +3,7 @@ p95 <= SLA for SLA in {10, 20, 50, 100} ms, trace seeds {11,
 both input modes (device-synthesised inputs; REC_INPUT_HOST = the paper's PCIe data loading,
 P:446-448), on G replicas (one process per GPU under torch.distributed.run, query q served by
 rank q mod G, rank-0 p95 over all ranks' latencies).  Each point also records the latency
-breakdown (queue, input, sparse, dense) of one probe at 0.5 lambda* with profiling on.
+breakdown (queue, input, sparse, dense) of one probe at 0.3 lambda* with profiling on.
 usage: [torchrun --nproc-per-node G ...] python scripts/serving_sweep.py --models rmc1,rmc2,rmc3
 Prints one JSON object on rank 0.
 """
@@ -106,16 +106,16 @@ def main():
                             lo = mid
                         else:
                             hi = mid
-                    # latency breakdown at 0.5 lambda*: one probe with profiling on (the
+                    # latency breakdown at 0.3 lambda*: one probe with profiling on (the
                     # stage-event graphs cost ~1/3 of the throughput, so lambda* is searched
                     # without them and the breakdown is taken at a load they sustain)
                     bd_at = None
                     if lo:
                         m.rec_profile(True)
-                        n = int(max(2000, 0.5 * lo * a.probe_s))
+                        n = int(max(2000, 0.3 * lo * a.probe_s))
                         if mode == "host":
                             n = min(n, host_cap * world)
-                        tr = W.poisson_trace(0.5 * lo, n, seed=seed)
+                        tr = W.poisson_trace(0.3 * lo, n, seed=seed)
                         r = m.rec_serve(rank_share(tr, world, rank), sla, a.streams, a.batch, input_mode=im,
                                         warmup_frac=0.1)
                         m.rec_profile(False)
@@ -125,13 +125,13 @@ def main():
                             dist.all_reduce(bd, op=dist.ReduceOp.SUM)
                             bd /= world
                         v = bd.tolist()
-                        bd_at = {"offered_qps": round(0.5 * lo),
+                        bd_at = {"offered_qps": round(0.3 * lo),
                                  "queue_input_sparse_dense_ms": [round(x, 4) for x in v[:4]],
                                  "mean_ms": round(v[4], 3), "p95_ms_rank_mean": round(v[5], 3)}
                     if rank == 0:
                         out["points"].append({"workload": cfg.name, "input": mode, "sla_ms": sla, "seed": seed,
                                               "lambda_star_qps": lo or 0.0, "p95_ms_at_best": best["p95"],
-                                              "breakdown_at_0p5_lambda": bd_at, "probes": probes})
+                                              "breakdown_at_0p3_lambda": bd_at, "probes": probes})
                         print(json.dumps(out["points"][-1]), file=sys.stderr, flush=True)
         m.close()
     out["wall_s"] = round(time.time() - t_start, 1)
