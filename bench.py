@@ -886,7 +886,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--per-model", default="rmc2,rmc3",
+    ap.add_argument("--per-model", default="rmc2,rmc3,mtwnd",
                     help="other workloads reported in the line's per_model block ('' = none)")
     ap.add_argument("--pm-steps", type=int, default=6)
     ap.add_argument("--pm-step-batches", type=int, default=128)
