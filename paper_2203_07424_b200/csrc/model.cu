@@ -2065,7 +2065,7 @@ rec_status rec_bench_sls(rec_model_t m, const int32_t* segs, const int64_t* batc
     set_error("bad argument");
     return REC_E_INVALID_ARG;
   }
-  if (m->lo != m->hi || m->world > 1) {
+  if (m->lo != m->hi || (m->world > 1 && m->shard != REC_SHARD_REPLICA)) {
     set_error("rec_bench_sls needs fixed pooling and an unsharded model");
     return REC_E_UNSUPPORTED;
   }

@@ -37,3 +37,24 @@ def test_sharded_equals_replica(p2p):
     assert res["ok"], res
     fused = "over peer memory" in p.stderr
     assert fused == (p2p == "1"), p.stderr[-2000:]
+
+
+@pytest.mark.skipif(_ngpus() < 2, reason="needs >= 2 GPUs")
+def test_bench_line_on_two_gpus():
+    """The driver's scaling runs launch `bench.py --gpus N` under torch.distributed.run: replica
+    models then carry a communicator (all-rank serving percentiles) and every measurement pass
+    must accept them; the rank-0 line reports n_gpus = 2 with library-gathered p95s."""
+    import __graft_entry__
+    __graft_entry__.build()
+    cmd = [sys.executable, "bench.py", "--gpus", "2", "--steps", "2", "--warmup", "3", "--step-batches", "16",
+           "--per-model", "rmc3", "--pm-steps", "2", "--pm-step-batches", "16", "--pm-sla", "0",
+           "--sla-queries", "3000", "--max-batch-search", "256", "--mlp-batch", "0", "--e2e-steps", "1",
+           "--caller-batches", "2", "--roofline-steps", "8", "--sls-batches", "8", "--no-cpu-baseline"]
+    env = {k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK")}
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
+    line = [l for l in p.stdout.splitlines() if l.startswith("{")]
+    assert p.returncode == 0 and len(line) == 1, p.stdout[-2000:] + p.stderr[-3000:]
+    d = json.loads(line[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["scaling"] == "weak"
+    assert d["sla"]["lambda_star_qps"] > 0
+    assert all(pr.get("p95_from") == "library (all ranks)" for pr in d["sla"]["probes_at_best"] or [])
