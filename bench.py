@@ -721,10 +721,10 @@ def run_ours(args):
                                                   f"launch gap and ramp of a lone launch)"},
                          "caller_index": caller,
                          "in_step_aggregate": {
-                             "achieved": sls_bytes_per_item(cfg, synth=True) * tot_items / (ms_max * 1e-3) / 1e9,
-                             "frac": sls_bytes_per_item(cfg, synth=True) * tot_items / (ms_max * 1e-3) / 1e9 / hbm_peak,
-                             "measured": "SLS algorithmic bytes of all timed steps / timed region "
-                                         "(all kernels of the step running on co-located streams)"}},
+                             "achieved": sls_bytes_per_item(cfg, synth=True) * tot_items / (ms_max * 1e-3) / 1e9 / world,
+                             "frac": sls_bytes_per_item(cfg, synth=True) * tot_items / (ms_max * 1e-3) / 1e9 / world / hbm_peak,
+                             "measured": "per GPU: SLS algorithmic bytes of all timed steps / timed region "
+                                         "/ ranks (all kernels of the step running on co-located streams)"}},
             "mlp": {"bound": "tensor", "achieved_tflops": gemm_tf, "peak": bf16_peak,
                     "frac": (gemm_tf / bf16_peak) if gemm_tf else None, "flops_per_item": mlp_flops_per_item(cfg),
                     "launches": gemm_n, "ms": gemm_ms,
