@@ -97,9 +97,12 @@ typedef struct {
 rec_status rec_model_create(const rec_model_desc* desc, rec_model_t* out);
 void rec_model_destroy(rec_model_t m);                       /* NULL-safe; frees everything */
 
-/* One batched query forward: SLS -> bottom MLP -> dot interaction ->
- * top MLP -> sigmoid (MT-WnD: lookups -> concat -> towers + wide, ctr [B][n_tasks] item-major,
- * dense unused and may be NULL).  dense [B][F] fp32 row-major (F = bottom_widths[0]);
+/* One batched query forward: the SparseNet's SparseLengthsSum over the multi-hot embedding
+ * lookups ("memory-intensive sparse operations on embeddings"; "pooling" of the
+ * lookups per table; "Gather-Reduce") -> the DenseNet's Bottom-FC ->
+ * dot interaction (R1: P:127) -> Predict-FC -> sigmoid, with the layer widths of
+ * Table I (MT-WnD: lookups -> concat -> towers + wide, ctr [B][n_tasks]
+ * item-major, dense unused and may be NULL).  dense [B][F] fp32 row-major (F = bottom_widths[0]);
  * indices [nnz] int32 and offsets [T*B+1] int32 in table-major CSR (bag g = t*B + b
  * spans indices[offsets[g] .. offsets[g+1])); ctr [B] fp32 out.  Host or device
  * pointers.  Synchronous.  Errors: INVALID_ARG (batch <= 0 or > max_batch),
