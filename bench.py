@@ -370,6 +370,39 @@ def saturation(model, cfg, d, m_streams, steps, warmup, step_batches, n_queries,
             "timed_batches": nbt, "value": float(t[2]) / (ms_max * 1e-3)}
 
 
+def mlp_large_batch(cfg, mb: int, local: int):
+    """MLP utilisation at a large batch (north_star "MLP at >= 60 % of bf16 tensor-pipe peak"):
+    the model's bottom and top stacks in a handle with max_batch = mb (tiny tables: the SLS is
+    not involved), 20 back-to-back launches of each stage (CUDA events).  Each stack is judged
+    against the roofline that binds it: its algorithmic flops / its minimal HBM bytes (bf16
+    input row read, output written: the fp32 X slot of the bottom, the CTR of the top) against
+    the ridge point bf16 peak / HBM peak; RMC1's narrow stacks are memory-bound, RMC3's
+    2560-wide bottom is compute-bound."""
+    from paper_2203_07424_b200 import RecModel
+    hbm, bf16, _ = peaks()
+    mm = RecModel(cfg.with_(rows=1000), seed=1, max_batch=mb, streams=1, device=local)
+    fb = sum(2 * x * y for x, y in zip(cfg.bottom[:-1], cfg.bottom[1:]))
+    wt = [cfg.top_in] + list(cfg.top)
+    ft = cfg.tasks * sum(2 * x * y for x, y in zip(wt[:-1], wt[1:]))
+    tb = mm.rec_bench_mlp(0, mb, 20) if fb else 0.0
+    ti = mm.rec_bench_mlp(2, mb, 20)
+    tt = mm.rec_bench_mlp(1, mb, 20)
+    mm.close()
+
+    def judge(flops, nbytes, ms):
+        tf = flops * mb / (ms * 1e-3) / 1e12
+        gbs = nbytes * mb / (ms * 1e-3) / 1e9
+        bound = "tensor" if flops / nbytes > bf16 * 1e3 / hbm else "hbm"
+        frac = tf / bf16 if bound == "tensor" else gbs / hbm
+        return {"us": 1e3 * ms, "tflops": tf, "tensor_frac": tf / bf16, "gbs": gbs, "bound": bound,
+                "frac": frac, "flops_per_item": flops, "min_bytes_per_item": nbytes}
+    return {"batch": mb,
+            "bottom": judge(fb, 2 * cfg.bottom[0] + 4 * cfg.dim, tb) if fb else None,
+            "top": judge(ft, 2 * cfg.top_in + 4 * cfg.tasks, tt - ti),
+            "measured": "rec_bench_mlp: 20 back-to-back launches of each stage on one stream (CUDA "
+                        "events); top = (interaction + top) - interaction"}
+
+
 def default_streams(args, name: str) -> int:
     """Co-located streams m for the saturation step: --streams, or per workload
     (profiles/r02/ab_*.txt: RMC3 16 -> 32 streams +16 %; RMC1 / RMC2 flat from 16)."""
@@ -419,6 +452,8 @@ def per_model(name, args, rank, world, dist, local, hbm_peak):
                       "saturation_ge_lambda_star": bool(sat["value"] >= 0.98 * lam)}
     model.close()
     torch.cuda.synchronize()
+    if args.mlp_batch > 0 and rank == 0 and name == "rmc3":
+        out["mlp_large_batch"] = mlp_large_batch(cfg, args.mlp_batch, local)
     return out
 
 
@@ -646,24 +681,7 @@ def run_ours(args):
 
     # MLP tensor-pipe utilisation at a large batch (north_star "MLP TC util"): the same MLP
     # stacks in a second handle with max_batch = --mlp-batch (tiny tables: SLS not involved)
-    mlp_large = None
-    if args.mlp_batch > 0 and rank == 0:
-        mb = args.mlp_batch
-        mm = RecModel(cfg.with_(rows=1000), seed=1, max_batch=mb, streams=1, device=local)
-        fb = sum(2 * x * y for x, y in zip(cfg.bottom[:-1], cfg.bottom[1:]))
-        wt = [cfg.top_in] + list(cfg.top)
-        ft = cfg.tasks * sum(2 * x * y for x, y in zip(wt[:-1], wt[1:]))
-        tb = mm.rec_bench_mlp(0, mb, 20)
-        ti = mm.rec_bench_mlp(2, mb, 20)
-        tt = mm.rec_bench_mlp(1, mb, 20)
-        mm.close()
-        mlp_large = {"batch": mb,
-                     "bottom": ({"us": 1e3 * tb, "tflops": fb * mb / (tb * 1e-3) / 1e12,
-                                 "frac": fb * mb / (tb * 1e-3) / 1e12 / bf16_peak} if fb else None),
-                     "top": {"us": 1e3 * (tt - ti), "tflops": ft * mb / ((tt - ti) * 1e-3) / 1e12,
-                             "frac": ft * mb / ((tt - ti) * 1e-3) / 1e12 / bf16_peak},
-                     "measured": "rec_bench_mlp: 20 back-to-back launches of each stage on one stream "
-                                 "(CUDA events); top = (interaction + top) - interaction"}
+    mlp_large = mlp_large_batch(cfg, args.mlp_batch, local) if args.mlp_batch > 0 and rank == 0 else None
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
