@@ -150,6 +150,10 @@ rec_status p2p_slots_init(rec_model_s* m) {
     a.words = words;
     a.err_flag = w.flag;
     a.timeout_ns = p2p_timeout_ns();
+    {
+      const char* f = getenv("REC_P2P_FENCE");
+      a.sc_fence = f ? atoi(f) : 0;
+    }
     w.sh_sls = a;
     w.sh_sls.peer_X = reinterpret_cast<float* const*>(P);
     w.sh_sls.peer_flags = reinterpret_cast<unsigned* const*>(P + G);

@@ -102,6 +102,15 @@ struct SlsShape {
 __device__ __forceinline__ void st_release_sys(unsigned* p, unsigned v) {
   asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+// Release + acquire RMW at system scope: makes this CTA's earlier stores (ordered before it by
+// the CTA barrier) visible before the count, and the last CTA, which reads the final count,
+// observes every CTA's stores before it raises the flags (release cumulativity) — without the
+// full fence.sc.sys of __threadfence_system() in every CTA.
+__device__ __forceinline__ unsigned atom_add_acq_rel_sys(unsigned* p, unsigned v) {
+  unsigned old;
+  asm volatile("atom.acq_rel.sys.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
 __device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
   unsigned v;
   asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -215,11 +224,16 @@ __global__ void __launch_bounds__(THREADS, REC_SLS_MINB) k_sls(const float* __re
                                                              static_cast<int64_t>(x_slot0 + t) * D + col));
     *dst = acc;
   }
-  __syncthreads();  // the CTA's peer stores happen-before thread 0's system-scope fence
+  __syncthreads();  // the CTA's peer stores happen-before thread 0's system-scope release
   if (threadIdx.x == 0) {
-    __threadfence_system();
-    const unsigned prev = atomicAdd(p2p.counter, 1u);
-    if (prev == gridDim.x - 1) {  // last CTA: every CTA's stores are fenced
+    unsigned prev;
+    if (p2p.sc_fence) {
+      __threadfence_system();
+      prev = atomicAdd(p2p.counter, 1u);
+    } else {
+      prev = atom_add_acq_rel_sys(p2p.counter, 1u);
+    }
+    if (prev == gridDim.x - 1) {  // last CTA: every CTA's stores are visible
       __threadfence_system();
       for (int q = 0; q < p2p.G; ++q) st_release_sys(p2p.peer_flags[q] + p2p.rank, p2p.epoch);
       *p2p.counter = 0;  // ready for the next launch using this counter (stream-ordered)
@@ -389,11 +403,16 @@ __global__ void __launch_bounds__(THREADS, REC_SLS_MINB) k_sls_synth(const __gri
         p2p.words[0] = p2p.epoch;
         p2p.words[1] = static_cast<unsigned>(B);
       }
-      __threadfence_system();
       const unsigned need = inter ? static_cast<unsigned>(min(nbags, static_cast<int>(gridDim.x)))
                                          : static_cast<unsigned>((nbags + GROUPS - 1) / GROUPS);
-      const unsigned prev = atomicAdd(p2p.counter, 1u);
-      if (prev == need - 1) {  // last CTA: every CTA's stores are fenced
+      unsigned prev;
+      if (p2p.sc_fence) {          // (REC_P2P_FENCE=1: the round-1 protocol)
+        __threadfence_system();
+        prev = atomicAdd(p2p.counter, 1u);
+      } else {
+        prev = atom_add_acq_rel_sys(p2p.counter, 1u);
+      }
+      if (prev == need - 1) {  // last CTA: every CTA's stores are visible
         __threadfence_system();
         for (int q = 0; q < p2p.G; ++q) st_release_sys(p2p.peer_flags[q] + p2p.rank, p2p.epoch);
         *p2p.counter = 0;      // ready for the slot's next launch (stream-ordered)

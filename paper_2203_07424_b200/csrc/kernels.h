@@ -88,6 +88,7 @@ struct P2PArgs {
   // flight on this slot, written by the slot's SLS kernel; when non-null the later kernels of
   // the chain (wait, CTR scatter) read epoch / B from here instead of the fields above.
   unsigned* words;
+  int sc_fence;  // 1: fence.sc.sys + relaxed atomic per CTA; 0: one acq_rel.sys atomic per CTA
 };
 void launch_sls_p2p(const float* tables, const int64_t* tab_off, int64_t row_stride,
                     const int64_t* rows, const int* indices, const int* offsets, int B, int T, int D,
