@@ -559,6 +559,7 @@ rec_status sharded_forward(rec_model_s* m, Workspace& w, const float* d_dense, c
     pa.G = G;
     pa.rank = r;
     pa.epoch = ++m->p2p_epoch;
+    pa.sc_fence = 1;
     pa.err_flag = w.flag;
     pa.timeout_ns = p2p_timeout_ns();
     REC_CUDA(cudaMemsetAsync(m->p2p_counter, 0, sizeof(unsigned), s));
