@@ -173,6 +173,7 @@ rec_status p2p_slots_init(rec_model_s* m) {
   // every rank's arena is zeroed before any peer may write into it
   int* f = nullptr;
   REC_CUDA(cudaMalloc(reinterpret_cast<void**>(&f), sizeof(int)));
+  REC_CUDA(cudaMemsetAsync(f, 0, sizeof(int), m->ws[0].stream));
   REC_NCCL(ncclAllReduce(f, f, 1, ncclInt32, ncclSum, static_cast<ncclComm_t>(m->nccl_comm), m->ws[0].stream));
   REC_CUDA(cudaStreamSynchronize(m->ws[0].stream));
   cudaFree(f);

@@ -420,6 +420,7 @@ static rec_status serve_sharded(rec_model_s* m, const rec_trace_row* trace, int6
   {
     int* f = nullptr;
     REC_CUDA(cudaMalloc(reinterpret_cast<void**>(&f), sizeof(int)));
+    REC_CUDA(cudaMemsetAsync(f, 0, sizeof(int), m->ws[0].stream));
     ncclResult_t r = ncclAllReduce(f, f, 1, ncclInt32, ncclSum, static_cast<ncclComm_t>(m->nccl_comm),
                                    m->ws[0].stream);
     cudaStreamSynchronize(m->ws[0].stream);
@@ -702,15 +703,20 @@ rec_status rec_serve(rec_model_t m, const rec_trace_row* trace, int64_t n, doubl
   const bool synth_events = breakdown && m->ws[0].slots[0].var[1].exec != nullptr;
   // during serving the stage events are read per batch here; the profile counters (which
   // would read them again when a staging slot is reused) stay off
-  const bool prof_saved = m->prof;
+  struct ProfGuard {  // restores the profiling state on every return path
+    rec_model_s* m;
+    bool prof;
+    ~ProfGuard() {
+      m->prof = prof;
+      m->stage_events = false;
+    }
+  } prof_guard{m, m->prof};
   if (breakdown) {
     for (auto& w : m->ws) REC_CUDA(cudaStreamSynchronize(w.stream));
     m->prof = false;
     m->stage_events = synth_events;
   }
   auto cleanup = [&]() {
-    m->prof = prof_saved;
-    m->stage_events = false;
     for (auto& L : lanes) {
       if (L.done) cudaEventDestroy(L.done);
       if (L.ctr_host) cudaFreeHost(L.ctr_host);
