@@ -1,3 +1,4 @@
+#include <algorithm>
 // k_mlp.cu — a whole FC stack (bottom MLP, or top MLP + width-1 output) in ONE kernel per
 // 128-row tile (Table I Bottom-FC / Predict-FC).
 //
@@ -217,6 +218,9 @@ __global__ void __launch_bounds__(C_THREADS, REC_CHAIN_MINB)
       cudaGridDependencySynchronize();  // A written by the predecessor grid
     }
     int it = 0;
+    // persistent launches (grid < tiles, large batches): this CTA's tiles m0, m0 + grid * 128, ..
+    // — the ring keeps streaming across tiles, so the next tile's loads overlap this epilogue
+    for (int mt = m0; mt < M; mt += gridDim.x * CBM) {
     for (int l = 0; l < nl; ++l) {
       const int K = args.K[l], N = args.N[l];
       const int nkb = (K + CBK - 1) / CBK;
@@ -230,7 +234,7 @@ __global__ void __launch_bounds__(C_THREADS, REC_CHAIN_MINB)
           if (lane == 0) {
             uint8_t* st = ring + s * C_STAGE;
             if (it >= pre) sm100::mbar_arrive_expect_tx(&full[s], bytes);
-            if (a_tma) sm100::tma_load_2d(st, &maps.a0, &full[s], kb * CBK, m0);
+            if (a_tma) sm100::tma_load_2d(st, &maps.a0, &full[s], kb * CBK, mt);
             if (it >= pre) sm100::tma_load_2d(st + C_A_BYTES, wmap(maps, l), &full[s], kb * CBK, n0);
             if (it == 0) STAMP(2);
           }
@@ -238,14 +242,18 @@ __global__ void __launch_bounds__(C_THREADS, REC_CHAIN_MINB)
         }
       }
     }
+    }
   } else if (warp == 1) {
     // ------------------------------------------------ single-thread MMA issuer
-    int it = 0;
+    int it = 0, tile = 0;
+    for (int mt = m0; mt < M; mt += gridDim.x * CBM, ++tile) {
     for (int l = 0; l < nl; ++l) {
       const int K = args.K[l], N = args.N[l];
       const int nkb = (K + CBK - 1) / CBK;
-      if (l > 0 || IR) {  // the previous layer's activations (or the interaction) are in smem
-        sm100::mbar_wait(act_ready, (IR ? l : l - 1) & 1);
+      // act_ready completes nl times per tile (IR == 0): after each hidden layer's epilogue and
+      // once after the last layer's (its TMEM reads done), which the next tile's layer 0 needs
+      if (l > 0 || IR || tile > 0) {
+        sm100::mbar_wait(act_ready, (IR ? l : tile * nl + l - 1) & 1);
         sm100::tc_fence_after();
       }
       for (int n0 = 0; n0 < N; n0 += NCH) {
@@ -273,6 +281,7 @@ __global__ void __launch_bounds__(C_THREADS, REC_CHAIN_MINB)
         }
       }
     }
+    }
   } else {
     // ------------------------------------------------ epilogue warps 2..9
     const int et = threadIdx.x - 64;                 // 0..255
@@ -283,9 +292,11 @@ __global__ void __launch_bounds__(C_THREADS, REC_CHAIN_MINB)
     asm volatile("bar.sync 1, %0;" ::"n"(C_EPI_THREADS) : "memory");   // epilogue warps only
     const int qw = warp & 3;                         // TMEM lane quarter of this warp
     const int r = qw * 32 + lane;                    // tile row
-    const int row = m0 + r;
-    const bool row_ok = row < M;
     const uint32_t trow = tmem + (static_cast<uint32_t>(qw * 32) << 16);
+    int tile = 0;
+    for (int mt = m0; mt < M; mt += gridDim.x * CBM, ++tile) {
+    const int row = mt + r;
+    const bool row_ok = row < M;
     if constexpr (IR > 0) {
       if (args.pdl) cudaGridDependencySynchronize();  // X written by the predecessor grids
       const float* xrow = row_ok ? args.ix + static_cast<int64_t>(row) * IR * ID : nullptr;
@@ -303,7 +314,7 @@ __global__ void __launch_bounds__(C_THREADS, REC_CHAIN_MINB)
     for (int l = 0; l < nl; ++l) {
       const int N = args.N[l];
       const bool last = l == nl - 1;
-      sm100::mbar_wait(acc_full, l & 1);
+      sm100::mbar_wait(acc_full, (tile * nl + l) & 1);
       sm100::tc_fence_after();
       if (et == 0) STAMP(8 + 2 * l);
       float dot = 0.f;
@@ -393,6 +404,11 @@ __global__ void __launch_bounds__(C_THREADS, REC_CHAIN_MINB)
         }
       }
     }
+    if (IR == 0) {  // this tile's TMEM has been read: the next tile's layer 0 may overwrite it
+      sm100::tc_fence_before();
+      sm100::mbar_arrive(act_ready);
+    }
+    }
   }
   sm100::tc_fence_before();
   __syncthreads();
@@ -444,16 +460,40 @@ void chain_prepare() {
     cudaFuncSetAttribute(chain_kernel(ir), cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
 }
 
+extern int g_chain_persistent;
+
+// Grid of a chain launch: one CTA per 128-row tile, or — when the tiles exceed one wave of
+// resident CTAs (large batches) and the interaction is not fused — one wave of persistent CTAs
+// that each walk tiles blockIdx, blockIdx + grid, ... (the ring streams across tiles, so a
+// tile's operand loads overlap the previous tile's epilogue; every tile is computed exactly as
+// by a CTA of its own, so the bits do not depend on the grid).
+static int chain_grid(const ChainArgs& a, size_t smem) {
+  static int nsm = [] {
+    int dev = 0, n = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n;
+  }();
+  const int tiles = (a.M + CBM - 1) / CBM;
+  if (a.ix || g_chain_persistent == 0) return tiles;
+  const int per_sm = std::max(1, std::min(512 / std::max(a.tmem_cols, 32),
+                                          static_cast<int>((228 * 1024) / (smem + 1024))));
+  return std::min(tiles, nsm * per_sm);
+}
+
+int g_chain_persistent = 1;  // REC_CHAIN_PERSISTENT=0: one CTA per tile at every batch size
+
 void launch_mlp_chain(const ChainMaps& maps, const ChainArgs& a, cudaStream_t s) {
   if (a.M <= 0) return;
   const size_t smem = chain_smem_bytes(a);
   const ChainKernel k = chain_kernel(a.ix ? a.ir : 0);
+  const int grid = chain_grid(a, smem);
   if (g_dense_prio == 0 && !a.pdl) {
-    k<<<(a.M + CBM - 1) / CBM, C_THREADS, smem, s>>>(maps, a);
+    k<<<grid, C_THREADS, smem, s>>>(maps, a);
     return;
   }
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3((a.M + CBM - 1) / CBM);
+  cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(C_THREADS);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;

@@ -196,6 +196,7 @@ void launch_gemm_tc(const CUtensorMap* tmap_a, const CUtensorMap* tmap_w, const 
 extern int g_gemm_2sm;
 extern int g_gemm_bn64;
 extern int g_gemm_mt2;
+extern int g_chain_persistent;  // REC_CHAIN_PERSISTENT (k_mlp.cu)
 extern int g_gemm_narrow;
 // Encode a 2D bf16 K-major tensor map [rows][K] (row pitch ldk elements) with a
 // 64 x box_rows box and 128-byte swizzle.  Returns false on failure.

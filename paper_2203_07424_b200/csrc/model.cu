@@ -1276,6 +1276,7 @@ rec_status rec_model_create(const rec_model_desc* d, rec_model_t* out) {
     g_gemm_mt1 = env_int("REC_GEMM_MT1", 0);
     g_gemm_bn64 = env_int("REC_GEMM_BN64", 0);
     g_gemm_mt2 = env_int("REC_GEMM_MT2", 0);
+    g_chain_persistent = env_int("REC_CHAIN_PERSISTENT", 1);
     g_interact_wpc = std::max(1, std::min(8, env_int("REC_INTERACT_WPC", 8)));
     g_interact_pf = env_int("REC_INTERACT_PF", 0);
     {

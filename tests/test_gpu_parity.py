@@ -428,3 +428,36 @@ def test_async_offsets_validation():
     ref = np.zeros(B, np.float32)
     m.rec_query(dense, ind, off, B, ref)
     assert np.array_equal(cv.cpu().numpy(), ref)
+
+
+def test_persistent_chain_large_batch_invariance(monkeypatch):
+    """B = 40960 on RMC1 shapes: the fused bottom / top chains run as one wave of persistent
+    CTAs walking 320 tiles (the ring streams across tiles); every item's CTR equals the
+    small-batch (one CTA per tile) result bit for bit and the oracle within 2e-2, and equals the
+    non-persistent launch (REC_CHAIN_PERSISTENT=0)."""
+    import torch
+    monkeypatch.delenv("REC_CHAIN_PERSISTENT", raising=False)
+    cfg = W.small_variant(W.RMC1, 20000)
+    B = 40960
+    segs = W.random_segments(B, seed=43, max_seg=1000)
+    out = {}
+    for pers in ("1", "0"):
+        monkeypatch.setenv("REC_CHAIN_PERSISTENT", pers)
+        m = _model(cfg, max_batch=B)
+        cv = torch.zeros(B, device="cuda")
+        m.rec_synth_query_async(0, segs, cv)
+        m.rec_sync(0)
+        out[pers] = cv.cpu().numpy()
+        m.close()
+    assert np.array_equal(out["1"], out["0"])
+    monkeypatch.delenv("REC_CHAIN_PERSISTENT", raising=False)
+    q, it = gen.expand_segments(segs)
+    pick = np.random.default_rng(4).choice(B, size=40, replace=False)
+    sub = np.array([[q[k], it[k], 1] for k in pick], np.int32)
+    small = _model(cfg, max_batch=64)
+    cs = torch.zeros(40, device="cuda")
+    small.rec_synth_query_async(0, sub, cs)
+    small.rec_sync(0)
+    assert np.array_equal(cs.cpu().numpy(), out["1"][pick])
+    i2, o2, d2 = gen.gen_batch(cfg, 1, sub)
+    assert np.abs(out["1"][pick] - fw.forward(cfg, 1, d2, i2, o2)).max() <= CTR_TOL
