@@ -164,9 +164,15 @@ __global__ void __launch_bounds__(C_THREADS, REC_CHAIN_MINB)
   uint64_t* bars = reinterpret_cast<uint64_t*>(s_dot + CBM);
   uint64_t* full = bars;
   uint64_t* empty = bars + S;
-  uint64_t* acc_full = bars + 2 * S;   // MMA -> epilogue, one phase per layer
-  uint64_t* act_ready = bars + 2 * S + 1;  // epilogue -> MMA, one phase per hidden layer
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 2 * S + 2);
+  // acc_full[b] MMA -> epilogue, one phase per layer of a tile using TMEM buffer b;
+  // tmem_empty[b] epilogue -> MMA, one phase per tile using buffer b (its TMEM has been read);
+  // act_ready epilogue -> MMA, one phase per hidden layer (its activations are in smem).
+  // Persistent launches alternate two TMEM accumulators (args.dbuf), so tile j + 1's MMAs run
+  // while the epilogue still reads tile j; one-tile launches only use buffer 0.
+  uint64_t* acc_full = bars + 2 * S;        // [2]
+  uint64_t* tmem_empty = bars + 2 * S + 2;  // [2]
+  uint64_t* act_ready = bars + 2 * S + 4;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 2 * S + 5);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m0 = blockIdx.x * CBM;
@@ -186,13 +192,17 @@ __global__ void __launch_bounds__(C_THREADS, REC_CHAIN_MINB)
       sm100::mbar_init(&full[s], 1);
       sm100::mbar_init(&empty[s], 1);
     }
-    sm100::mbar_init(acc_full, 1);
+    for (int b = 0; b < 2; ++b) {
+      sm100::mbar_init(&acc_full[b], 1);
+      sm100::mbar_init(&tmem_empty[b], C_EPI_THREADS);
+    }
     sm100::mbar_init(act_ready, C_EPI_THREADS);
     sm100::fence_mbar_init();
     sm100::tma_prefetch_desc(&maps.a0);
     for (int l = 0; l < nl; ++l) sm100::tma_prefetch_desc(wmap(maps, l));
   }
-  if (warp == 0) sm100::tmem_alloc(tslot, args.tmem_cols);
+  const int tcols = args.tmem_cols * (args.dbuf ? 2 : 1);
+  if (warp == 0) sm100::tmem_alloc(tslot, tcols);
   sm100::tc_fence_before();
   __syncthreads();
   sm100::tc_fence_after();
@@ -250,12 +260,17 @@ __global__ void __launch_bounds__(C_THREADS, REC_CHAIN_MINB)
     for (int l = 0; l < nl; ++l) {
       const int K = args.K[l], N = args.N[l];
       const int nkb = (K + CBK - 1) / CBK;
-      // act_ready completes nl times per tile (IR == 0): after each hidden layer's epilogue and
-      // once after the last layer's (its TMEM reads done), which the next tile's layer 0 needs
-      if (l > 0 || IR || tile > 0) {
-        sm100::mbar_wait(act_ready, (IR ? l : tile * nl + l - 1) & 1);
+      const int buf = args.dbuf ? (tile & 1) : 0;
+      const int use = args.dbuf ? (tile >> 1) : tile;   // earlier tiles on this buffer
+      if (l == 0 && use > 0) {  // the epilogue has read this buffer's previous tile
+        sm100::mbar_wait(&tmem_empty[buf], (use - 1) & 1);
         sm100::tc_fence_after();
       }
+      if (l > 0 || IR) {  // the previous layer's activations (or the interaction) are in smem
+        sm100::mbar_wait(act_ready, (IR ? l : tile * (nl - 1) + l - 1) & 1);
+        sm100::tc_fence_after();
+      }
+      const uint32_t tbase = tmem + static_cast<uint32_t>(buf * args.tmem_cols);
       for (int n0 = 0; n0 < N; n0 += NCH) {
         const int nc = min(NCH, args.wbox[l]);
         const uint32_t idesc = sm100::idesc_bf16_f32(CBM, nc);
@@ -270,10 +285,10 @@ __global__ void __launch_bounds__(C_THREADS, REC_CHAIN_MINB)
             const uint64_t db = sm100::umma_desc_sw128(st + C_A_BYTES);
 #pragma unroll
             for (int k = 0; k < CBK / 16; ++k)
-              sm100::mma_bf16_ss(tmem + n0, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
+              sm100::mma_bf16_ss(tbase + n0, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
             sm100::mma_commit(&empty[s]);
             if (kb == nkb - 1 && n0 + NCH >= N) {
-              sm100::mma_commit(acc_full);
+              sm100::mma_commit(&acc_full[buf]);
               STAMP(4 + l);
             }
           }
@@ -292,11 +307,14 @@ __global__ void __launch_bounds__(C_THREADS, REC_CHAIN_MINB)
     asm volatile("bar.sync 1, %0;" ::"n"(C_EPI_THREADS) : "memory");   // epilogue warps only
     const int qw = warp & 3;                         // TMEM lane quarter of this warp
     const int r = qw * 32 + lane;                    // tile row
-    const uint32_t trow = tmem + (static_cast<uint32_t>(qw * 32) << 16);
     int tile = 0;
     for (int mt = m0; mt < M; mt += gridDim.x * CBM, ++tile) {
     const int row = mt + r;
     const bool row_ok = row < M;
+    const int buf = args.dbuf ? (tile & 1) : 0;
+    const int use = args.dbuf ? (tile >> 1) : tile;
+    const uint32_t trow = tmem + (static_cast<uint32_t>(qw * 32) << 16) +
+                          static_cast<uint32_t>(buf * args.tmem_cols);
     if constexpr (IR > 0) {
       if (args.pdl) cudaGridDependencySynchronize();  // X written by the predecessor grids
       const float* xrow = row_ok ? args.ix + static_cast<int64_t>(row) * IR * ID : nullptr;
@@ -314,7 +332,7 @@ __global__ void __launch_bounds__(C_THREADS, REC_CHAIN_MINB)
     for (int l = 0; l < nl; ++l) {
       const int N = args.N[l];
       const bool last = l == nl - 1;
-      sm100::mbar_wait(acc_full, (tile * nl + l) & 1);
+      sm100::mbar_wait(&acc_full[buf], (use * nl + l) & 1);
       sm100::tc_fence_after();
       if (et == 0) STAMP(8 + 2 * l);
       float dot = 0.f;
@@ -404,22 +422,22 @@ __global__ void __launch_bounds__(C_THREADS, REC_CHAIN_MINB)
         }
       }
     }
-    if (IR == 0) {  // this tile's TMEM has been read: the next tile's layer 0 may overwrite it
+    if (IR == 0) {  // this tile's TMEM has been read: a later tile may overwrite the buffer
       sm100::tc_fence_before();
-      sm100::mbar_arrive(act_ready);
+      sm100::mbar_arrive(&tmem_empty[buf]);
     }
     }
   }
   sm100::tc_fence_before();
   __syncthreads();
-  if (warp == 0) sm100::tmem_dealloc(tmem, args.tmem_cols);
+  if (warp == 0) sm100::tmem_dealloc(tmem, tcols);
   if (threadIdx.x == 0) STAMP(15);
 }
 
 size_t chain_smem_bytes(const ChainArgs& a) {
   return 1024 + static_cast<size_t>(a.stages) * (C_A_BYTES + a.nchunk * CBK * 2) +
          static_cast<size_t>(a.act_kblocks) * C_A_BYTES +
-         sizeof(float) * (a.bias_total + a.wl_n + 2 + CBM) + 8 * (2 * a.stages + 4);
+         sizeof(float) * (a.bias_total + a.wl_n + 2 + CBM) + 8 * (2 * a.stages + 8);
 }
 
 bool chain_configure(ChainArgs& a) {
@@ -476,18 +494,21 @@ static int chain_grid(const ChainArgs& a, size_t smem) {
   }();
   const int tiles = (a.M + CBM - 1) / CBM;
   if (a.ix || g_chain_persistent == 0) return tiles;
-  const int per_sm = std::max(1, std::min(512 / std::max(a.tmem_cols, 32),
-                                          static_cast<int>((228 * 1024) / (smem + 1024))));
+  const int tc = std::max(a.tmem_cols, 32) * (a.tmem_cols <= 256 ? 2 : 1);  // double-buffered
+  const int per_sm = std::max(1, std::min(512 / tc, static_cast<int>((228 * 1024) / (smem + 1024))));
   return std::min(tiles, nsm * per_sm);
 }
 
 int g_chain_persistent = 1;  // REC_CHAIN_PERSISTENT=0: one CTA per tile at every batch size
 
-void launch_mlp_chain(const ChainMaps& maps, const ChainArgs& a, cudaStream_t s) {
-  if (a.M <= 0) return;
-  const size_t smem = chain_smem_bytes(a);
-  const ChainKernel k = chain_kernel(a.ix ? a.ir : 0);
-  const int grid = chain_grid(a, smem);
+void launch_mlp_chain(const ChainMaps& maps, const ChainArgs& a0, cudaStream_t s) {
+  if (a0.M <= 0) return;
+  const size_t smem = chain_smem_bytes(a0);
+  const ChainKernel k = chain_kernel(a0.ix ? a0.ir : 0);
+  const int grid = chain_grid(a0, smem);
+  ChainArgs a = a0;
+  // two TMEM accumulators when CTAs walk several tiles (tiles > grid) and they fit
+  a.dbuf = grid < (a.M + CBM - 1) / CBM && a.tmem_cols <= 256 && !a.ix;
   if (g_dense_prio == 0 && !a.pdl) {
     k<<<grid, C_THREADS, smem, s>>>(maps, a);
     return;

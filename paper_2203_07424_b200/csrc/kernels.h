@@ -234,6 +234,7 @@ struct ChainArgs {
   int dbg_mode;             // diagnostic: bit0 skip TMEM loads, bit1 skip hidden smem stores
   const float* ix;          // top chain with the dot interaction fused (nullptr = A by TMA):
   int ir;                   //   X [M][ir][32] fp32, ir = T + 1 (chain_interact_supported)
+  int dbuf;                 // set by launch_mlp_chain: two TMEM accumulators (persistent CTAs)
 };
 bool chain_interact_supported(int T, int D);
 size_t chain_smem_bytes(const ChainArgs& a);
