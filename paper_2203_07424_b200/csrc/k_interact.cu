@@ -14,6 +14,9 @@
 namespace rec {
 
 int g_interact_wpc = 8;  // warps (items) per CTA, REC_INTERACT_WPC
+// rows of X_b (T + 1) from which the interaction uses 4 x 4 register blocks (REC_INTERACT_BLOCKED
+// sets it; 0 = never)
+int kBlockedRows = 24;
 int g_interact_pf = 0;   // few-CTA prefetching interaction (REC_INTERACT_PF=1; measured slightly slower)
 
 // Pair p of the strict lower triangle in row-major order: (i, j), 1 <= i <= T, 0 <= j < i,
@@ -30,7 +33,8 @@ __device__ __forceinline__ int2 pair_of(int p) {
 // each lane forms whole pairs as sequential fp32 FMA chains over k; the bf16 output row is
 // staged in shared memory and written with 16-B vector stores (ld is a multiple of 8).
 __global__ void k_interact(const float* __restrict__ X, int B, const int* __restrict__ dB, int T,
-                           int D, __nv_bfloat16* __restrict__ A, int ld, int warps_per_cta) {
+                           int D, __nv_bfloat16* __restrict__ A, int ld, int warps_per_cta,
+                           int blocked_rows) {
   extern __shared__ float4 sm4[];
   // the top MLP kernel that follows may be scheduled now: it sets up (barriers, TMEM, bias)
   // and waits for this grid before reading A (programmatic dependent launch)
@@ -53,19 +57,66 @@ __global__ void k_interact(const float* __restrict__ X, int B, const int* __rest
     }
     __syncwarp();
     for (int k = lane; k < D; k += 32) outs[k] = __float2bfloat16_rn(xs[k]);
-    for (int p = lane; p < npairs; p += 32) {
-      const int2 ij = pair_of(p);
-      const float4* xi = reinterpret_cast<const float4*>(xs + ij.x * pitch);
-      const float4* xj = reinterpret_cast<const float4*>(xs + ij.y * pitch);
-      float acc = 0.f;
-      for (int k = 0; k < d4; ++k) {
-        const float4 a = xi[k], c = xj[k];
-        acc = fmaf(a.x, c.x, acc);
-        acc = fmaf(a.y, c.y, acc);
-        acc = fmaf(a.z, c.z, acc);
-        acc = fmaf(a.w, c.w, acc);
+    if (rows >= blocked_rows) {
+      // many tables (RMC2: 41 rows, 820 pairs): each lane owns 4 x 4 blocks of the lower
+      // triangle, so one pair of 4-row float4 loads feeds 64 FMAs instead of 4 (the per-pair
+      // loop is shared-memory bound there).  Every Z(i, j) is still one fp32 FMA chain over
+      // k = 0..D-1 in the same order, so the bits equal the per-pair loop's.
+      const int nrb = (rows + 3) / 4, nblk = nrb * (nrb + 1) / 2;
+      const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int q = lane; q < nblk; q += 32) {
+        int I = static_cast<int>((sqrtf(8.f * static_cast<float>(q) + 1.f) - 1.f) * 0.5f);
+        while (I * (I + 1) / 2 > q) --I;
+        while ((I + 1) * (I + 2) / 2 <= q) ++I;
+        const int J = q - I * (I + 1) / 2;
+        float acc[4][4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int v = 0; v < 4; ++v) acc[u][v] = 0.f;
+        for (int k = 0; k < d4; ++k) {
+          float4 a[4], c[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int ri = 4 * I + u, rj = 4 * J + u;
+            a[u] = ri < rows ? reinterpret_cast<const float4*>(xs + ri * pitch)[k] : z4;
+            c[u] = rj < rows ? reinterpret_cast<const float4*>(xs + rj * pitch)[k] : z4;
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+              float t = acc[u][v];
+              t = fmaf(a[u].x, c[v].x, t);
+              t = fmaf(a[u].y, c[v].y, t);
+              t = fmaf(a[u].z, c[v].z, t);
+              t = fmaf(a[u].w, c[v].w, t);
+              acc[u][v] = t;
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            const int i = 4 * I + u, j = 4 * J + v;
+            if (i < rows && j < i) outs[D + i * (i - 1) / 2 + j] = __float2bfloat16_rn(acc[u][v]);
+          }
       }
-      outs[D + p] = __float2bfloat16_rn(acc);
+    } else {
+      for (int p = lane; p < npairs; p += 32) {
+        const int2 ij = pair_of(p);
+        const float4* xi = reinterpret_cast<const float4*>(xs + ij.x * pitch);
+        const float4* xj = reinterpret_cast<const float4*>(xs + ij.y * pitch);
+        float acc = 0.f;
+        for (int k = 0; k < d4; ++k) {
+          const float4 a = xi[k], c = xj[k];
+          acc = fmaf(a.x, c.x, acc);
+          acc = fmaf(a.y, c.y, acc);
+          acc = fmaf(a.z, c.z, acc);
+          acc = fmaf(a.w, c.w, acc);
+        }
+        outs[D + p] = __float2bfloat16_rn(acc);
+      }
     }
     for (int k = D + npairs + lane; k < ld; k += 32) outs[k] = __float2bfloat16_rn(0.f);
     __syncwarp();
@@ -83,7 +134,7 @@ __global__ void k_interact(const float* __restrict__ X, int B, const int* __rest
 constexpr int kItemsPerWarp = 4;
 template <int PF>
 __global__ void k_interact_pf(const float* __restrict__ X, int B, const int* __restrict__ dB, int T,
-                              int D, __nv_bfloat16* __restrict__ A, int ld, int warps_per_cta) {
+                              int D, __nv_bfloat16* __restrict__ A, int ld, int warps_per_cta, int blocked_rows) {
   extern __shared__ float4 sm4[];
   if (dB) B = *dB;
   const int rows = T + 1, pitch = D + 4, npairs = T * (T + 1) / 2, d4 = D / 4;
@@ -123,19 +174,66 @@ __global__ void k_interact_pf(const float* __restrict__ X, int B, const int* __r
     }
     __syncwarp();
     for (int k = lane; k < D; k += 32) outs[k] = __float2bfloat16_rn(xs[k]);
-    for (int p = lane; p < npairs; p += 32) {
-      const int2 ij = pair_of(p);
-      const float4* xi = reinterpret_cast<const float4*>(xs + ij.x * pitch);
-      const float4* xj = reinterpret_cast<const float4*>(xs + ij.y * pitch);
-      float acc = 0.f;
-      for (int k = 0; k < d4; ++k) {
-        const float4 a = xi[k], c = xj[k];
-        acc = fmaf(a.x, c.x, acc);
-        acc = fmaf(a.y, c.y, acc);
-        acc = fmaf(a.z, c.z, acc);
-        acc = fmaf(a.w, c.w, acc);
+    if (rows >= blocked_rows) {
+      // many tables (RMC2: 41 rows, 820 pairs): each lane owns 4 x 4 blocks of the lower
+      // triangle, so one pair of 4-row float4 loads feeds 64 FMAs instead of 4 (the per-pair
+      // loop is shared-memory bound there).  Every Z(i, j) is still one fp32 FMA chain over
+      // k = 0..D-1 in the same order, so the bits equal the per-pair loop's.
+      const int nrb = (rows + 3) / 4, nblk = nrb * (nrb + 1) / 2;
+      const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int q = lane; q < nblk; q += 32) {
+        int I = static_cast<int>((sqrtf(8.f * static_cast<float>(q) + 1.f) - 1.f) * 0.5f);
+        while (I * (I + 1) / 2 > q) --I;
+        while ((I + 1) * (I + 2) / 2 <= q) ++I;
+        const int J = q - I * (I + 1) / 2;
+        float acc[4][4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int v = 0; v < 4; ++v) acc[u][v] = 0.f;
+        for (int k = 0; k < d4; ++k) {
+          float4 a[4], c[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int ri = 4 * I + u, rj = 4 * J + u;
+            a[u] = ri < rows ? reinterpret_cast<const float4*>(xs + ri * pitch)[k] : z4;
+            c[u] = rj < rows ? reinterpret_cast<const float4*>(xs + rj * pitch)[k] : z4;
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+              float t = acc[u][v];
+              t = fmaf(a[u].x, c[v].x, t);
+              t = fmaf(a[u].y, c[v].y, t);
+              t = fmaf(a[u].z, c[v].z, t);
+              t = fmaf(a[u].w, c[v].w, t);
+              acc[u][v] = t;
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            const int i = 4 * I + u, j = 4 * J + v;
+            if (i < rows && j < i) outs[D + i * (i - 1) / 2 + j] = __float2bfloat16_rn(acc[u][v]);
+          }
       }
-      outs[D + p] = __float2bfloat16_rn(acc);
+    } else {
+      for (int p = lane; p < npairs; p += 32) {
+        const int2 ij = pair_of(p);
+        const float4* xi = reinterpret_cast<const float4*>(xs + ij.x * pitch);
+        const float4* xj = reinterpret_cast<const float4*>(xs + ij.y * pitch);
+        float acc = 0.f;
+        for (int k = 0; k < d4; ++k) {
+          const float4 a = xi[k], c = xj[k];
+          acc = fmaf(a.x, c.x, acc);
+          acc = fmaf(a.y, c.y, acc);
+          acc = fmaf(a.z, c.z, acc);
+          acc = fmaf(a.w, c.w, acc);
+        }
+        outs[D + p] = __float2bfloat16_rn(acc);
+      }
     }
     for (int k = D + npairs + lane; k < ld; k += 32) outs[k] = __float2bfloat16_rn(0.f);
     __syncwarp();
@@ -157,7 +255,7 @@ void launch_interact(const float* X, int B, const int* dB, int T, int D, __nv_bf
     if (smem > 48 * 1024)
       cudaFuncSetAttribute(k_interact_pf<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(smem));
-    k_interact_pf<4><<<blocks, 32 * wpc, smem, s>>>(X, B, dB, T, D, A_top, ld_top, wpc);
+    k_interact_pf<4><<<blocks, 32 * wpc, smem, s>>>(X, B, dB, T, D, A_top, ld_top, wpc, kBlockedRows);
     return;
   }
   if (B <= 0) return;
@@ -172,7 +270,7 @@ void launch_interact(const float* X, int B, const int* dB, int T, int D, __nv_bf
   int blocks = (B + wpc - 1) / wpc;
   if (blocks > 148 * 8) blocks = 148 * 8;
   if (g_dense_prio == 0) {
-    k_interact<<<blocks, 32 * wpc, smem, s>>>(X, B, dB, T, D, A_top, ld_top, wpc);
+    k_interact<<<blocks, 32 * wpc, smem, s>>>(X, B, dB, T, D, A_top, ld_top, wpc, kBlockedRows);
     return;
   }
   cudaLaunchConfig_t cfg{};
@@ -185,7 +283,7 @@ void launch_interact(const float* X, int B, const int* dB, int T, int D, __nv_bf
   at[0].val.priority = g_dense_prio;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, k_interact, X, B, dB, T, D, A_top, ld_top, wpc);
+  cudaLaunchKernelEx(&cfg, k_interact, X, B, dB, T, D, A_top, ld_top, wpc, kBlockedRows);
 }
 
 // MT-WnD join (R26, R28): one warp per item; the concatenated pooled vectors become the bf16

@@ -248,7 +248,8 @@ extern int g_sls_prio;  // same for the synthetic-index SLS
 extern int g_gemm_stages;
 extern int g_gemm_mt1;
 extern int g_interact_wpc;  // interaction warps per CTA (REC_INTERACT_WPC)
-extern int g_interact_pf;   // few-CTA prefetching interaction kernel (REC_INTERACT_PF)  // per-layer GEMM ring depth cap (REC_GEMM_STAGES; 0 = maximum)
+extern int g_interact_pf;   // few-CTA prefetching interaction kernel (REC_INTERACT_PF)
+extern int kBlockedRows;    // interaction register blocking from this many rows (REC_INTERACT_BLOCKED)  // per-layer GEMM ring depth cap (REC_GEMM_STAGES; 0 = maximum)
 
 // --------------------------------------------------------------- interaction (a5)
 // MT-WnD (R26, R28): A_top[b] = bf16(X[b][1..T] concatenated) ++ 0-pad (ld = Ktop_pad) and

@@ -1279,6 +1279,7 @@ rec_status rec_model_create(const rec_model_desc* d, rec_model_t* out) {
     g_chain_persistent = env_int("REC_CHAIN_PERSISTENT", 1);
     g_interact_wpc = std::max(1, std::min(8, env_int("REC_INTERACT_WPC", 8)));
     g_interact_pf = env_int("REC_INTERACT_PF", 0);
+    kBlockedRows = env_int("REC_INTERACT_BLOCKED", 24) > 0 ? env_int("REC_INTERACT_BLOCKED", 24) : 1 << 30;
     {
       int lo = 0, hi = 0;
       cudaDeviceGetStreamPriorityRange(&lo, &hi);

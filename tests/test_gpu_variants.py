@@ -18,7 +18,7 @@ KNOBS = ["REC_SLS", "REC_GEMM_2SM", "REC_GEMM_NARROW", "REC_GEMM_MT1", "REC_FUSE
          "REC_INTERACT_PF", "REC_HOT_POLICY", "REC_MLP", "REC_CHAIN_PDL", "REC_PDL",
          "REC_FUSE_INTERACT", "REC_TOWER_GROUP", "REC_GEMM_STAGES", "REC_INTERACT_WPC",
          "REC_CHAIN_SMEM", "REC_CHAIN_STAGES", "REC_SERVE_DEPTH",
-         "REC_SERVE_THREADS", "REC_GREEN_SMS", "REC_PRIO", "REC_GEMM_BN64", "REC_SLS_GRID", "REC_GEMM_MT2", "REC_CHAIN_PERSISTENT", "REC_P2P_FENCE"]
+         "REC_SERVE_THREADS", "REC_GREEN_SMS", "REC_PRIO", "REC_GEMM_BN64", "REC_SLS_GRID", "REC_GEMM_MT2", "REC_CHAIN_PERSISTENT", "REC_P2P_FENCE", "REC_INTERACT_BLOCKED"]
 
 
 @pytest.fixture(scope="module", autouse=True)
@@ -68,6 +68,8 @@ VARIANTS = [
     ("fuse_dense", {"REC_FUSE_DENSE": "1"}, RMC1, 700, 0),
     ("interact_pf", {"REC_INTERACT_PF": "1"}, RMC1, 700, 0),
     ("interact_wpc2", {"REC_INTERACT_WPC": "2"}, RMC1, 700, 0),
+    ("interact_per_pair_rmc2", {"REC_INTERACT_BLOCKED": "0"}, W.small_variant(W.RMC2, 4096), 700, 0),
+    ("interact_blocked_rmc1", {"REC_INTERACT_BLOCKED": "4"}, RMC1, 700, 0),
     ("mlp_layers_tiny", {"REC_MLP": "layers"}, TINY, 300, 0),
     ("mlp_layers_rmc1", {"REC_MLP": "layers"}, RMC1, 700, 0),
     ("chain_no_pdl", {"REC_CHAIN_PDL": "0"}, RMC1, 700, 0),
