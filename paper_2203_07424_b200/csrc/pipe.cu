@@ -270,6 +270,7 @@ rec_status rec_set_pipeline(rec_model_t m, int32_t lanes) {
       L.ga.emplace_back();
       L.sa.emplace_back();
       fill_genargs(m, m->ws[k], L.ga.back(), L.sa.back(), nullptr);
+      L.sa.back().dense_bf = nullptr;  // lanes generate dense features on the branch stream
     }
     rec_status st = pipe_capture(m, L);
     if (st != REC_OK) {
