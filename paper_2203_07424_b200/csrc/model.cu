@@ -428,7 +428,8 @@ void fill_genargs(rec_model_s* m, Workspace& w, GenArgs& ga, SlsSynthArgs& sa,
     const char* e = getenv("REC_HOT_POLICY");
     if (!e || !atoi(e)) sa.hot_rows = 0;
   }
-  sa.dense_bf = m->fuse_dense ? w.dense_bf : nullptr;
+  // dense features from the SLS kernel only where it implements them (not the TMA variant)
+  sa.dense_bf = m->fuse_dense && !m->sls_tma ? w.dense_bf : nullptr;
   sa.F = m->F;
   sa.Fpad = m->Fpad;
   sa.remap = m->d_remap;
@@ -460,7 +461,7 @@ static rec_status synth_chain(rec_model_s* m, Workspace& w, SynthSlot& sl, bool 
   cudaStream_t s = w.stream, sb = w.stream_b;
   cudaEvent_t* gev = capture && with_events ? sl.ev : nullptr;
   mark(gev, 0, s);
-  if (!materialize && m->lo == m->hi && (m->fuse_dense || m->F == 0)) {
+  if (!materialize && m->lo == m->hi && ((m->fuse_dense && !m->sls_tma) || m->F == 0)) {
     // dense features generated inside the SLS kernel: one stream, SLS -> bottom -> top
     mark(gev, 1, s);
     cudaEvent_t e0 = gev ? nullptr : prof_begin(m, s);
