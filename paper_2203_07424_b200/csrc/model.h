@@ -164,7 +164,7 @@ struct rec_model_s {
   int sls_pdl = 1;    // REC_PDL=0 disables programmatic dependent launch of the SLS
   int sls_interleave = 0;  // REC_SLS_GRID=1: bags round-robin over one wave (k_sls_synth;
                            // measured: RMC1 304k vs 326k QPS, serialized 0.56 either way)
-  int fuse_dense = 1;  // dense features generated inside the SLS kernel (REC_FUSE_DENSE=0: own kernel)
+  int fuse_dense = 0;  // REC_FUSE_DENSE=1: dense features generated inside the SLS kernel
   int chain_pdl = 1;    // top fused MLP launched with PDL after the interaction (REC_CHAIN_PDL)
   int green_sms = 0;    // SMs reserved for the dense stages (REC_GREEN_SMS; 0 = shared SMs)
   void* green[2] = {nullptr, nullptr};  // CUgreenCtx: [0] dense partition, [1] SLS partition

@@ -65,8 +65,9 @@ VARIANTS = [
     ("sls_interleaved_grid_rmc1_big", {"REC_SLS_GRID": "1"}, RMC1, 4096, 0),
     ("hot_policy_l2_window", {"REC_HOT_POLICY": "1"}, RMC1.with_(index_dist=W.INDEX_SKEW2), 700, 8 << 20),
     ("l2_window", {}, RMC1, 700, 8 << 20),
-    ("dense_own_kernel", {"REC_FUSE_DENSE": "0"}, RMC1, 700, 0),
-    ("dense_own_kernel_rmc3", {"REC_FUSE_DENSE": "0"}, RMC3, 700, 0),
+    ("fuse_dense", {"REC_FUSE_DENSE": "1"}, RMC1, 700, 0),
+    ("fuse_dense_rmc3", {"REC_FUSE_DENSE": "1"}, RMC3, 700, 0),
+    ("fuse_dense_tma", {"REC_FUSE_DENSE": "1", "REC_SLS": "tma"}, RMC1, 700, 0),
     ("interact_pf", {"REC_INTERACT_PF": "1"}, RMC1, 700, 0),
     ("interact_wpc2", {"REC_INTERACT_WPC": "2"}, RMC1, 700, 0),
     ("interact_per_pair_rmc2", {"REC_INTERACT_BLOCKED": "0"}, W.small_variant(W.RMC2, 4096), 700, 0),
