@@ -2,21 +2,24 @@
 
 One JSON line on rank 0.  Workload (N = 1): BASELINE.json configs[1], DLRM-RMC1 —
 10 tables x 1M rows x dim 32 (1.28 GB fp32, >> 126 MB L2), pooling 80, bottom
-256-128-32, top 256-64-1, fused batches of d = 1024 items.
+256-128-32, top 256-64-1, fused batches of d = 1024 items on 16 co-located streams.
 
-A STEP = one fused batch through the whole hot path: a1 (queries of a burst trace,
-split/fused into batches of <= d by the library's C++ splitter/fuser before timing; the
-step submits that batch's segment list), a2 (device-side generation of its indices,
-offsets and dense features from (seed, qid, item)), a3 SLS, a4 bottom MLP, a5 dot
-interaction, a6 top MLP + sigmoid.  `value` = queries completed per second (a query
-completes when its last sub-query's batch is done) = whole-job throughput summed over
-ranks (replicas, no data-path collective: scaling "weak").  It is the saturation
-(SLA-unbounded) QPS; the serving run that checks the p95 SLA is `sla` in the line.
+A STEP = one serving round of --step-batches (512) fused batches: a1 (queries of a burst
+trace, split/fused into batches of <= d by the library's C++ splitter/fuser before timing),
+then per batch a2 (device-side generation of its indices and dense features from (seed,
+qid, item)), a3 SLS, a4 bottom MLP, a5 dot interaction, a6 top MLP + sigmoid, the batches
+dealt round-robin to the co-located streams.  `value` = queries completed per
+second (a query completes when its last sub-query's batch is done) = whole-job throughput
+summed over ranks (replicas, no data-path collective: scaling "weak").  It is the saturation
+(SLA-unbounded) QPS; the serving run that checks the p95 SLA (Alg. 1 over streams x d) is
+`sla`, and `per_model` repeats saturation / SLS roofline / lambda* for RMC2, RMC3, MT-WnD.
 
-`e2e` is the same metric through rec_query with HOST buffers (indices, offsets, dense
-copied host->device and the CTRs device->host every step).  `roofline` is the SLS
-kernel: algorithmic bytes / its CUDA-event time on its own stream.
-`cpu_baseline` times the CPU oracle on the host cores on a bounded sample.
+`e2e` is the same metric through rec_query_async with HOST buffers (indices, offsets, dense
+copied host->device and the CTRs device->host for every batch).  `roofline` is the SLS kernel:
+algorithmic bytes / its CUDA-event time on its own stream (plus the in-step
+aggregate and the caller-index kernel).  `cpu_baseline` times the CPU oracle on the host cores
+on a bounded sample.  `--gpus N` re-executes under torch.distributed.run; `--shard table`
+measures table-wise sharded serving instead of replicas.
 
 --impl reference runs the CPU oracle (the tier's reference arm) as the timed program.
 """
