@@ -406,9 +406,13 @@ __global__ void __launch_bounds__(THREADS, REC_SLS_MINB) k_sls_synth(const __gri
       const unsigned need = inter ? static_cast<unsigned>(min(nbags, static_cast<int>(gridDim.x)))
                                          : static_cast<unsigned>((nbags + GROUPS - 1) / GROUPS);
       unsigned prev;
-      if (p2p.sc_fence) {          // (REC_P2P_FENCE=1: the round-1 protocol)
+      if (p2p.sc_fence == 1) {     // (REC_P2P_FENCE=1: the round-1 protocol)
         __threadfence_system();
         prev = atomicAdd(p2p.counter, 1u);
+#ifdef REC_DEBUG_KNOBS
+      } else if (p2p.sc_fence == 2) {  // diagnostic build only: no ordering (results invalid)
+        prev = atomicAdd(p2p.counter, 1u);
+#endif
       } else {
         prev = atom_add_acq_rel_sys(p2p.counter, 1u);
       }
