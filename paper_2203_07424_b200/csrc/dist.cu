@@ -60,7 +60,7 @@ rec_status dist_init(rec_model_s* m, const void* nccl_id) {
 // Every co-located stream slot s of every rank owns a region of one exchange arena (a single
 // cudaMalloc per rank, exported once with CUDA IPC):
 //   [X: cap x (T+1) x D fp32 | CTR gather: G x Bq fp32 | arrival flags [G] | CTR flags [G] |
-//    CTA counter | words: epoch, B]
+//    CTA counter | words: epoch, B | LL lines: Bq x T x D/4 x 2 x 16 B]
 // The k-th batch submitted on slot s is the same global batch on every rank (a deterministic
 // global dispatch: every rank submits the same batch sequence round-robin over the slots) and
 // carries epoch k + 1 on that slot.  Its chain on rank r:
@@ -77,7 +77,7 @@ rec_status dist_init(rec_model_s* m, const void* nccl_id) {
 static size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct SlotLayout {
-  size_t x, ctr, flags, ctrflags, counter, words, bytes;
+  size_t x, ctr, flags, ctrflags, counter, words, ll, bytes;
 };
 static SlotLayout slot_layout(const rec_model_s* m) {
   const int G = m->world;
@@ -89,7 +89,8 @@ static SlotLayout slot_layout(const rec_model_s* m) {
   L.ctrflags = L.flags + al256(sizeof(unsigned) * G);
   L.counter = L.ctrflags + al256(sizeof(unsigned) * G);
   L.words = L.counter + 256;
-  L.bytes = L.words + 256;
+  L.ll = L.words + 256;  // LL receive lines: [Bq][T][D / 4][2] x 16 B
+  L.bytes = L.ll + al256(static_cast<size_t>(Bq) * m->T * (m->D / 4) * 2 * sizeof(uint4));
   return L;
 }
 
@@ -123,15 +124,16 @@ rec_status p2p_slots_init(rec_model_s* m) {
     m->p2p_opened.push_back(a);
     base[q] = static_cast<uint8_t*>(a);
   }
-  // per slot: [peer X][peer flags][peer CTR][peer CTR flags], G pointers each
-  std::vector<void*> ptrs(static_cast<size_t>(M) * 4 * G);
+  // per slot: [peer X][peer flags][peer CTR][peer CTR flags][peer LL], G pointers each
+  std::vector<void*> ptrs(static_cast<size_t>(M) * 5 * G);
   for (int s = 0; s < M; ++s)
     for (int q = 0; q < G; ++q) {
       uint8_t* b = base[q] + L.bytes * s;
-      ptrs[(s * 4 + 0) * G + q] = b + L.x;
-      ptrs[(s * 4 + 1) * G + q] = b + L.flags;
-      ptrs[(s * 4 + 2) * G + q] = b + L.ctr;
-      ptrs[(s * 4 + 3) * G + q] = b + L.ctrflags;
+      ptrs[(s * 5 + 0) * G + q] = b + L.x;
+      ptrs[(s * 5 + 1) * G + q] = b + L.flags;
+      ptrs[(s * 5 + 2) * G + q] = b + L.ctr;
+      ptrs[(s * 5 + 3) * G + q] = b + L.ctrflags;
+      ptrs[(s * 5 + 4) * G + q] = b + L.ll;
     }
   REC_CUDA(cudaMalloc(reinterpret_cast<void**>(&m->d_sh_ptrs), sizeof(void*) * ptrs.size()));
   REC_CUDA(cudaMemcpy(m->d_sh_ptrs, ptrs.data(), sizeof(void*) * ptrs.size(), cudaMemcpyHostToDevice));
@@ -142,7 +144,8 @@ rec_status p2p_slots_init(rec_model_s* m) {
     w.X = reinterpret_cast<float*>(mb + L.x);
     w.x_external = true;
     w.sh_ctr_gather = reinterpret_cast<float*>(mb + L.ctr);
-    void** P = m->d_sh_ptrs + static_cast<size_t>(s) * 4 * G;
+    void** P = m->d_sh_ptrs + static_cast<size_t>(s) * 5 * G;
+    w.sh_ll = reinterpret_cast<uint4*>(mb + L.ll);
     unsigned* words = reinterpret_cast<unsigned*>(mb + L.words);
     P2PArgs a{};
     a.G = G;
@@ -160,6 +163,14 @@ rec_status p2p_slots_init(rec_model_s* m) {
     w.sh_sls.peer_X = reinterpret_cast<float* const*>(P);
     w.sh_sls.peer_flags = reinterpret_cast<unsigned* const*>(P + G);
     w.sh_sls.counter = reinterpret_cast<unsigned*>(mb + L.counter);
+    w.sh_sls.peer_ll = reinterpret_cast<uint4* const*>(P + 4 * G);
+    w.sh_sls.T_all = m->T;
+    {
+      // flag-in-data lines for remote items (captured synthetic chains); REC_P2P_LL=0: the
+      // pooled vectors go straight into the owner's X behind a per-CTA system-scope fence
+      const char* e = getenv("REC_P2P_LL");
+      w.sh_sls.ll = (e ? atoi(e) : 1) != 0 && m->D % 4 == 0;
+    }
     w.sh_wait = a;
     w.sh_wait.my_flags = reinterpret_cast<unsigned*>(mb + L.flags);
     w.sh_ctr = a;
@@ -197,6 +208,10 @@ static rec_status shard_tail(rec_model_s* m, Workspace& w, int B, const int* dB,
     wa.epoch = ca.epoch = cw.epoch = epoch;
   }
   launch_p2p_wait(wa, s);
+  if (!epoch && w.sh_sls.ll) {  // captured chains: remote tables' vectors from the LL lines
+    launch_p2p_ll_unpack(wa, w.sh_ll, w.X, m->T, m->D, m->t0, m->T_loc, m->nsm, s);
+    m->launches += 1;
+  }
   REC_CUDA(cudaStreamWaitEvent(s, join, 0));
   enqueue_interact_top(m, w, s, B, dB, w.ctr, w.logit, nullptr);
   launch_p2p_ctr_scatter(w.ctr, Bl, item0, ca, s);
@@ -225,6 +240,7 @@ rec_status shard_enqueue(rec_model_s* m, Workspace& w, const float* d_dense, con
   }
   REC_CUDA(cudaEventRecord(w.ev_join, sb));
   P2PArgs pa = w.sh_sls;
+  pa.ll = 0;  // (the caller-index kernel stores into X behind the fence protocol)
   pa.words = nullptr;
   pa.epoch = epoch;
   pa.Bq = Bq;

@@ -111,6 +111,21 @@ __device__ __forceinline__ unsigned atom_add_acq_rel_sys(unsigned* p, unsigned v
   asm volatile("atom.acq_rel.sys.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
   return old;
 }
+// LL lines: one 16-byte volatile store / load (each 8-byte {value, epoch} half is single-copy
+// atomic, also over NVLink).
+__device__ __forceinline__ void st_volatile_v4(uint4* p, uint4 v) {
+  asm volatile("st.volatile.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ uint4 ld_volatile_v4(const uint4* p) {
+  uint4 v;
+  asm volatile("ld.volatile.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p)
+               : "memory");
+  return v;
+}
 __device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
   unsigned v;
   asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -279,6 +294,49 @@ __global__ void k_p2p_ctr_scatter(const float* __restrict__ ctr, int Bl, int ite
   }
 }
 
+__global__ void __launch_bounds__(256) k_p2p_ll_unpack(const P2PArgs p2p, const uint4* __restrict__ ll,
+                                                        float* __restrict__ X, int T, int D, int t0, int TL) {
+  const unsigned epoch = p2p.words[0];
+  const int B = static_cast<int>(p2p.words[1]);
+  const int Bq = (B + p2p.G - 1) / p2p.G;
+  const int Bl = max(0, min(Bq, B - p2p.rank * Bq));
+  const int D4 = D / 4, TR = T - TL;
+  const int64_t n = static_cast<int64_t>(Bl) * TR * D4;
+  const int64_t x_stride = static_cast<int64_t>(T + 1) * D;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int c = static_cast<int>(i % D4);
+    const int64_t r = i / D4;
+    const int j = static_cast<int>(r % TR), bi = static_cast<int>(r / TR);
+    const int tg = j < t0 ? j : j + TL;
+    const uint4* src = ll + ((static_cast<int64_t>(bi) * T + tg) * D4 + c) * 2;
+    uint4 u0 = ld_volatile_v4(src), u1 = ld_volatile_v4(src + 1);
+    if (u0.y != epoch || u0.w != epoch || u1.y != epoch || u1.w != epoch) {
+      unsigned long long t_start;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+      for (;;) {
+        __nanosleep(100);
+        u0 = ld_volatile_v4(src);
+        u1 = ld_volatile_v4(src + 1);
+        if (u0.y == epoch && u0.w == epoch && u1.y == epoch && u1.w == epoch) break;
+        unsigned long long t_now;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_now));
+        if (t_now - t_start > p2p.timeout_ns) {
+          if (p2p.err_flag) atomicOr(p2p.err_flag, 4);
+          return;
+        }
+      }
+    }
+    *reinterpret_cast<float4*>(X + bi * x_stride + static_cast<int64_t>(1 + tg) * D + 4 * c) =
+        make_float4(__uint_as_float(u0.x), __uint_as_float(u0.z), __uint_as_float(u1.x), __uint_as_float(u1.z));
+  }
+}
+
+void launch_p2p_ll_unpack(const P2PArgs& p2p, const uint4* ll, float* X, int T, int D, int t0, int TL,
+                          int nsm, cudaStream_t s) {
+  k_p2p_ll_unpack<<<2 * nsm, 256, 0, s>>>(p2p, ll, X, T, D, t0, TL);
+}
+
 void launch_p2p_ctr_scatter(const float* ctr, int Bl, int item0, const P2PArgs& p2p, cudaStream_t s) {
   k_p2p_ctr_scatter<<<1, 512, 0, s>>>(ctr, Bl, item0, p2p);
 }
@@ -394,8 +452,14 @@ __global__ void __launch_bounds__(THREADS, REC_SLS_MINB) k_sls_synth(const __gri
     if (active && live) {
       const int Bq = (B + p2p.G - 1) / p2p.G;
       const int p = b / Bq, bi = b - p * Bq;
-      *reinterpret_cast<float4*>(p2p.peer_X[p] + static_cast<int64_t>(bi) * a.x_stride +
-                                 static_cast<int64_t>(1 + a.t0 + t) * a.D + col) = acc;
+      if (p2p.ll && p != p2p.rank) {  // flag-in-data lines into the owner's LL buffer
+        uint4* dst = p2p.peer_ll[p] + ((static_cast<int64_t>(bi) * p2p.T_all + a.t0 + t) * (a.D / 4) + sub) * 2;
+        st_volatile_v4(dst, make_uint4(__float_as_uint(acc.x), p2p.epoch, __float_as_uint(acc.y), p2p.epoch));
+        st_volatile_v4(dst + 1, make_uint4(__float_as_uint(acc.z), p2p.epoch, __float_as_uint(acc.w), p2p.epoch));
+      } else {
+        *reinterpret_cast<float4*>(p2p.peer_X[p] + static_cast<int64_t>(bi) * a.x_stride +
+                                   static_cast<int64_t>(1 + a.t0 + t) * a.D + col) = acc;
+      }
     }
     __syncthreads();  // the CTA's peer stores happen-before thread 0's system-scope fence
     if (threadIdx.x == 0) {
@@ -406,7 +470,9 @@ __global__ void __launch_bounds__(THREADS, REC_SLS_MINB) k_sls_synth(const __gri
       const unsigned need = inter ? static_cast<unsigned>(min(nbags, static_cast<int>(gridDim.x)))
                                          : static_cast<unsigned>((nbags + GROUPS - 1) / GROUPS);
       unsigned prev;
-      if (p2p.sc_fence == 1) {     // (REC_P2P_FENCE=1: the round-1 protocol)
+      if (p2p.ll) {                // data carries its own epoch: the count is only a hint
+        prev = atomicAdd(p2p.counter, 1u);
+      } else if (p2p.sc_fence == 1) {  // (REC_P2P_FENCE=1: the round-1 protocol)
         __threadfence_system();
         prev = atomicAdd(p2p.counter, 1u);
 #ifdef REC_DEBUG_KNOBS

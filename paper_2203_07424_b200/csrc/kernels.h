@@ -89,6 +89,15 @@ struct P2PArgs {
   // the chain (wait, CTR scatter) read epoch / B from here instead of the fields above.
   unsigned* words;
   int sc_fence;  // 1: fence.sc.sys + relaxed atomic per CTA; 0: one acq_rel.sys atomic per CTA
+  // Flag-in-data exchange (k_sls_synth, REC_P2P_LL, default on): pooled vectors of items owned
+  // by another rank go to that rank's LL buffer as 16-byte stores {v0, epoch, v1, epoch}
+  // (8-byte halves land atomically over NVLink), so no CTA waits on a system-scope fence; the
+  // owner's k_p2p_ll_unpack validates every half's epoch and writes X.  The flags raised by
+  // the last CTA are then only a hint that the data is (mostly) in flight or landed.
+  // Layout per rank: [ceil(cap / G)][T][D / 4][2] uint4, item row bi, global table tg.
+  uint4* const* peer_ll;  // [G] every rank's LL buffer of this slot
+  int ll;                 // 1: LL stores for remote items (own items go straight into X)
+  int T_all;              // global table count (LL row pitch)
 };
 void launch_sls_p2p(const float* tables, const int64_t* tab_off, int64_t row_stride,
                     const int64_t* rows, const int* indices, const int* offsets, int B, int T, int D,
@@ -99,6 +108,12 @@ void launch_p2p_reduce(const float* stage, float* X, int Bl, int Bq, int T, int 
                        cudaStream_t s);
 // Block the stream until every rank's SLS of this epoch has landed in this rank's X.
 void launch_p2p_wait(const P2PArgs& p2p, cudaStream_t s);
+// LL exchange: X[bi][1 + tg] of this rank's item block for every table tg outside the own
+// range [t0, t0 + TL), read from this rank's LL buffer `ll` once both epoch words of each
+// 16-byte line equal the slot epoch (p2p.words[0]; batch p2p.words[1]).  Bounded spin: a line
+// that misses p2p.timeout_ns sets bit 2 of p2p.err_flag.  Grid: nsm x 2 CTAs (grid-stride).
+void launch_p2p_ll_unpack(const P2PArgs& p2p, const uint4* ll, float* X, int T, int D, int t0, int TL,
+                          int nsm, cudaStream_t s);
 // All-gather of the CTRs over peer memory: this rank's ctr[0..Bl) goes to every rank's
 // gather buffer at [item0, item0 + Bl), then this rank's flag is raised on every peer
 // (p2p.peer_X = the ranks' gather buffers, p2p.peer_flags = their CTR-flag arrays).

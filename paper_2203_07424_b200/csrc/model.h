@@ -103,6 +103,7 @@ struct Workspace {
   bool x_external = false;
   P2PArgs sh_sls{}, sh_wait{}, sh_ctr{}, sh_ctrwait{};
   float* sh_ctr_gather = nullptr;    // [G * Bq] CTRs of every rank's block (items 0..B-1)
+  uint4* sh_ll = nullptr;  // this slot's LL receive buffer (flag-in-data exchange; inside sh_arena)
   unsigned sh_epoch = 0;
   int4* gsegs_local = nullptr;       // device segments of this rank's item block (> kParamSegs)
 };

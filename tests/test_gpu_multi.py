@@ -21,15 +21,19 @@ def _ngpus():
 
 
 @pytest.mark.skipif(_ngpus() < 2, reason="needs >= 2 GPUs")
-@pytest.mark.parametrize("p2p", ["1", "0"], ids=["fused_peer", "nccl"])
-def test_sharded_equals_replica(p2p):
+@pytest.mark.parametrize("p2p,ll", [("1", "1"), ("1", "0"), ("0", "1")],
+                         ids=["fused_peer_ll", "fused_peer_fenced", "nccl"])
+def test_sharded_equals_replica(p2p, ll):
+    """fused_peer_ll: the default flag-in-data lines (REC_P2P_LL=1) for the asynchronous
+    synthetic chains; fused_peer_fenced: pooled vectors stored straight into the owner's X
+    behind the per-CTA system-scope fence (REC_P2P_LL=0)."""
     import __graft_entry__
     __graft_entry__.build()
     n = min(_ngpus(), 4)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
-           "--master-addr", "127.0.0.1", "--master-port", "2953" + p2p,
+           "--master-addr", "127.0.0.1", "--master-port", "295" + p2p + ll,
            os.path.join(ROOT, "scripts", "shard_check.py"), "--iters", "5"]
-    env = dict(os.environ, REC_P2P=p2p, REC_VERBOSE="1")
+    env = dict(os.environ, REC_P2P=p2p, REC_P2P_LL=ll, REC_VERBOSE="1")
     p = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
     line = [l for l in p.stdout.splitlines() if l.startswith("{")]
     assert p.returncode == 0 and line, p.stdout[-3000:] + p.stderr[-3000:]

@@ -18,7 +18,7 @@ KNOBS = ["REC_SLS", "REC_GEMM_2SM", "REC_GEMM_NARROW", "REC_GEMM_MT1", "REC_FUSE
          "REC_INTERACT_PF", "REC_HOT_POLICY", "REC_MLP", "REC_CHAIN_PDL", "REC_PDL",
          "REC_FUSE_INTERACT", "REC_TOWER_GROUP", "REC_GEMM_STAGES", "REC_INTERACT_WPC",
          "REC_CHAIN_SMEM", "REC_CHAIN_STAGES", "REC_SERVE_DEPTH",
-         "REC_SERVE_THREADS", "REC_GREEN_SMS", "REC_PRIO", "REC_GEMM_BN64", "REC_SLS_GRID", "REC_GEMM_MT2", "REC_CHAIN_PERSISTENT", "REC_P2P_FENCE", "REC_INTERACT_BLOCKED"]
+         "REC_SERVE_THREADS", "REC_GREEN_SMS", "REC_PRIO", "REC_GEMM_BN64", "REC_SLS_GRID", "REC_GEMM_MT2", "REC_CHAIN_PERSISTENT", "REC_P2P_FENCE", "REC_INTERACT_BLOCKED", "REC_P2P_LL"]
 
 
 @pytest.fixture(scope="module", autouse=True)
