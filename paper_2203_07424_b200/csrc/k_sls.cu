@@ -31,9 +31,6 @@
 #ifndef REC_SLS_RIF
 #define REC_SLS_RIF 8  // independent 128-bit row loads in flight per lane
 #endif
-#ifndef REC_SLS_ROLL
-#define REC_SLS_ROLL 1  // k_sls_synth: rolling per-row refill (0: round-synchronous batches of U)
-#endif
 
 #ifdef REC_SLS_TIMELINE  // diagnostic build (scripts/sls_timeline.cu): per-warp %globaltimer
 __device__ unsigned long long g_sls_tl[4 * 65536];
@@ -405,64 +402,6 @@ __global__ void __launch_bounds__(THREADS, REC_SLS_MINB) k_sls_synth(const __gri
     pol_hot = l2_policy_evict_last();
     pol_cold = l2_policy_evict_first();
   }
-#if REC_SLS_ROLL
-  // Rolling prefetch: a ring of U row registers per lane, v[k] holding row k mod U.  Row r is
-  // accumulated (in index order) as soon as its own load returned and its register is refilled
-  // at once with row r + U, so every lane keeps U loads in flight for the whole bag instead of
-  // waiting for the slowest of U at the end of each round.  Indices: cur = this round, nxt =
-  // the next (rows r + U of the last U positions of a round), computed one round ahead.
-  int cur[S::IPL], nxt[S::IPL];
-#pragma unroll
-  for (int q = 0; q < S::IPL; ++q) {
-    const int j = q * LANES + sub, j2 = S::ROWS + j;
-    cur[q] = j < L ? gen_index(j, qi.y, c2, qi.x, a.k0, a.k1, R, a.index_dist, zc) : 0;
-    nxt[q] = j2 < L ? gen_index(j2, qi.y, c2, qi.x, a.k0, a.k1, R, a.index_dist, zc) : 0;
-    if (remap) {
-      cur[q] = __ldg(remap + cur[q]);
-      nxt[q] = __ldg(remap + nxt[q]);
-    }
-  }
-  SLS_STAMP(1);
-  float4 v[S::U];
-#pragma unroll
-  for (int k = 0; k < S::U; ++k) {  // prologue: rows 0 .. U - 1 (U <= ROWS: all in round 0)
-    const int rr = __shfl_sync(gmask, cur[k / LANES], k % LANES, LANES);
-    if (k < L)
-      v[k] = HOT ? ldg_row_pol(tab, static_cast<uint32_t>(rr), stride_bytes, rr < a.hot_rows ? pol_hot : pol_cold)
-                 : ldg_row(tab, static_cast<uint32_t>(rr), stride_bytes);
-  }
-  for (int base = 0; base < L; base += S::ROWS) {
-#pragma unroll
-    for (int kk = 0; kk < S::ROWS; kk += S::U) {
-#pragma unroll
-      for (int k = 0; k < S::U; ++k) {
-        const int r = kk + k;      // round position consumed now
-        const int f = r + S::U;    // round position refilled into v[k] (next round if >= ROWS)
-        const int fr = f < S::ROWS ? f : f - S::ROWS;
-        const int src = f < S::ROWS ? cur[fr / LANES] : nxt[fr / LANES];
-        const int rr = __shfl_sync(gmask, src, fr % LANES, LANES);
-        if (base + r < L) {
-          acc.x += v[k].x;
-          acc.y += v[k].y;
-          acc.z += v[k].z;
-          acc.w += v[k].w;
-        }
-        if (base + f < L)
-          v[k] = HOT ? ldg_row_pol(tab, static_cast<uint32_t>(rr), stride_bytes,
-                                   rr < a.hot_rows ? pol_hot : pol_cold)
-                     : ldg_row(tab, static_cast<uint32_t>(rr), stride_bytes);
-      }
-      if (base == 0 && kk == 0) SLS_STAMP(2);
-    }
-#pragma unroll
-    for (int q = 0; q < S::IPL; ++q) {  // indices two rounds ahead
-      cur[q] = nxt[q];
-      const int j = base + 2 * S::ROWS + q * LANES + sub;
-      nxt[q] = j < L ? gen_index(j, qi.y, c2, qi.x, a.k0, a.k1, R, a.index_dist, zc) : 0;
-      if (remap) nxt[q] = __ldg(remap + nxt[q]);
-    }
-  }
-#else
   int cur[S::IPL];
 #pragma unroll
   for (int q = 0; q < S::IPL; ++q) {
@@ -506,7 +445,6 @@ __global__ void __launch_bounds__(THREADS, REC_SLS_MINB) k_sls_synth(const __gri
       if (base == 0 && kk == 0) SLS_STAMP(2);
     }
   }
-#endif
   if constexpr (P2P) {
     // fused all-to-all (table-wise sharding): item b lives on rank b / Bq as row b % Bq,
     // its pooled vector of local table t goes to X slot 1 + t0 + t over NVLink
