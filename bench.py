@@ -408,9 +408,13 @@ def mlp_large_batch(cfg, mb: int, local: int):
 
 def default_streams(args, name: str) -> int:
     """Co-located streams m for the saturation step: --streams, or per workload
-    (profiles/r02/ab_*.txt: RMC3 16 -> 32 streams +16 %; RMC1 / RMC2 flat from 16)."""
+    (profiles/r02/ab_*.txt: RMC3 16 -> 32 streams +16 %; RMC1 flat from 16; RMC2 replicas
+    4 / 8 / 16: 30.0k / 29.9k / 29.0k QPS - its 1.23 MB-per-item gathers lose DRAM efficiency
+    with more concurrent batches - so 8; sharded RMC2 keeps 16 exchange slots)."""
     if not getattr(args, "streams_auto", False) and args.streams > 0:
         return args.streams
+    if name == "rmc2" and getattr(args, "shard", "replica") == "replica":
+        return 8
     return 32 if name == "rmc3" else 16
 
 
@@ -418,7 +422,7 @@ def per_model(name, args, rank, world, dist, local, hbm_peak):
     """The metric is per model (BASELINE.json: "SLA-bounded QPS (p95) per model at 1/2/4/8
     B200"): saturation QPS (the same step definition at fewer steps), the SLS roofline of
     back-to-back launches, and lambda* at the model's paper SLA for the saturation
-    step's co-location (m = 16, RMC3 32) and d = 1024 (the Alg. 1 search runs for the headline
+    step's co-location (m = 16; RMC2 8, RMC3 32) and d = 1024 (the Alg. 1 search runs for the headline
     model)."""
     import torch
     from paper_2203_07424_b200 import RecModel
@@ -910,7 +914,7 @@ def main():
     ap.add_argument("--per-model", default="rmc2,rmc3,mtwnd",
                     help="other workloads reported in the line's per_model block ('' = none)")
     ap.add_argument("--pm-steps", type=int, default=6)
-    ap.add_argument("--pm-step-batches", type=int, default=128)
+    ap.add_argument("--pm-step-batches", type=int, default=256)
     ap.add_argument("--pm-sla", type=int, default=1, help="lambda* for the per_model workloads")
     ap.add_argument("--step-batches", type=int, default=512,
                     help="fused batches per step (one serving round over the co-located streams)")
