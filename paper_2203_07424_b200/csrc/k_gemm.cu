@@ -373,10 +373,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1)
 
 // tmap_w must have a BN/2-row box (Layer::tmap_w128 for BN = 256).
 template <int BN>
-static void launch_2sm(const CUtensorMap* ta, const CUtensorMap* tw, const GemmArgs& a, cudaStream_t s) {
+static void launch_2sm(const CUtensorMap* ta, const CUtensorMap* tw, const GemmArgs& a, cudaStream_t s,
+                       int ring = 0) {
   constexpr int STAGE = A_STAGE_BYTES + (BN / 2) * BK * 2;
   const int nkb = (a.K + BK - 1) / BK;
-  const int smax = g_gemm_2sm > 1 ? g_gemm_2sm : 4;  // REC_GEMM_2SM=n > 1: n-stage ring
+  const int smax = ring > 0 ? ring : g_gemm_2sm > 1 ? g_gemm_2sm : 4;  // REC_GEMM_2SM=n > 1: n-stage ring
   const int stages = nkb < smax ? (nkb < 1 ? 1 : nkb) : smax;
   const size_t smem = static_cast<size_t>(stages) * STAGE + 1024 + 256;
   int mblocks = (a.M + BM - 1) / BM;
@@ -462,6 +463,7 @@ void gemm_prepare() {
 }
 
 int g_gemm_2sm = 0;     // REC_GEMM_2SM: CTA-pair GEMM for full-GPU launches (experimental)
+int g_gemm_2sm_serve = 2;  // REC_GEMM_2SM_SERVE=n: CTA-pair GEMM (n-stage ring) for serving launches (0: off)
 int g_gemm_mt1 = 0;     // REC_GEMM_MT1=1: 128x256 tiles (one M tile per CTA) for full-GPU launches too (A/B)
 int g_gemm_narrow = 0;  // REC_GEMM_NARROW=n: 128-wide N tiles below n 128x256 tiles (measured: RMC2/3 +0.5-1 %, MT-WnD -7 %)
 int g_gemm_mt2 = 0;     // REC_GEMM_MT2=1: 256 x 256 weight-sharing tiles also for serving batches
@@ -493,6 +495,10 @@ void launch_gemm_tc(const CUtensorMap* tmap_a, const CUtensorMap* tmap_w, const 
     if (g_gemm_2sm && tmap_w_half) launch_2sm<256>(tmap_a, tmap_w_half, a, s);  // CTA pairs
     else if (g_gemm_mt1) launch_bn<256, 1>(tmap_a, tmap_w, a, s);
     else launch_bn<256, 2>(tmap_a, tmap_w, a, s);  // enough 256-row tiles to fill the GPU: share W
+  } else if (g_gemm_2sm_serve && tmap_w_half && a.K >= 512) {
+    // serving batch on CTA pairs: each CTA of a pair loads its own 128 A rows and half of the
+    // 256-wide W tile, the pair's MMA reads both halves (1.5 x the flops per delivered byte)
+    launch_2sm<256>(tmap_a, tmap_w_half, a, s, g_gemm_2sm_serve);
   } else if (g_gemm_narrow && tmap_w_half && a.mode != GEMM_OUT_CTR &&
              ((a.M + 127) / 128) * ((a.N + 255) / 256) < g_gemm_narrow) {
     // serving batch, few 128x256 tiles: 128-wide N tiles double the CTAs working on the layer

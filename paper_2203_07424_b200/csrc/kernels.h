@@ -209,6 +209,7 @@ void launch_gemm_tc(const CUtensorMap* tmap_a, const CUtensorMap* tmap_w, const 
                     cudaStream_t s, const CUtensorMap* tmap_w_half = nullptr,
                     const CUtensorMap* tmap_w64 = nullptr);
 extern int g_gemm_2sm;
+extern int g_gemm_2sm_serve;  // REC_GEMM_2SM_SERVE=n: CTA-pair GEMM for serving launches (n-stage ring)
 extern int g_gemm_bn64;
 extern int g_gemm_mt2;
 extern int g_chain_persistent;  // REC_CHAIN_PERSISTENT (k_mlp.cu)

@@ -18,7 +18,7 @@ KNOBS = ["REC_SLS", "REC_GEMM_2SM", "REC_GEMM_NARROW", "REC_GEMM_MT1", "REC_FUSE
          "REC_INTERACT_PF", "REC_HOT_POLICY", "REC_MLP", "REC_CHAIN_PDL", "REC_PDL",
          "REC_FUSE_INTERACT", "REC_TOWER_GROUP", "REC_GEMM_STAGES", "REC_INTERACT_WPC",
          "REC_CHAIN_SMEM", "REC_CHAIN_STAGES", "REC_SERVE_DEPTH",
-         "REC_SERVE_THREADS", "REC_GREEN_SMS", "REC_PRIO", "REC_GEMM_BN64", "REC_SLS_GRID", "REC_GEMM_MT2", "REC_CHAIN_PERSISTENT", "REC_P2P_FENCE", "REC_INTERACT_BLOCKED", "REC_P2P_LL"]
+         "REC_SERVE_THREADS", "REC_GREEN_SMS", "REC_PRIO", "REC_GEMM_BN64", "REC_SLS_GRID", "REC_GEMM_MT2", "REC_CHAIN_PERSISTENT", "REC_P2P_FENCE", "REC_INTERACT_BLOCKED", "REC_P2P_LL", "REC_GEMM_2SM_SERVE"]
 
 
 @pytest.fixture(scope="module", autouse=True)
@@ -83,6 +83,9 @@ VARIANTS = [
     ("gemm_bn64_rmc2", {"REC_GEMM_BN64": "1"}, W.small_variant(W.RMC2, 4096), 700, 0),
     ("gemm_stages2", {"REC_GEMM_STAGES": "2"}, RMC3, 700, 0),
     ("gemm_2sm_large", {"REC_GEMM_2SM": "1"}, RMC3, 20480, 0),
+    ("gemm_2sm_serving_off_rmc3", {"REC_GEMM_2SM_SERVE": "0"}, RMC3, 1024, 0),
+    ("gemm_2sm_serving_rmc3_odd", {"REC_GEMM_2SM_SERVE": "4"}, RMC3, 700, 0),
+    ("gemm_2sm_serving_off_rmc2", {"REC_GEMM_2SM_SERVE": "0"}, W.small_variant(W.RMC2, 4096), 700, 0),
     ("gemm_mt1_large", {"REC_GEMM_MT1": "1"}, RMC3, 20480, 0),
     ("gemm_narrow_towers", {"REC_GEMM_NARROW": "148"}, MTWND, 700, 0),
     ("towers_per_task", {"REC_TOWER_GROUP": "0"}, MTWND, 700, 0),
