@@ -62,3 +62,21 @@ def test_bench_line_on_two_gpus():
     assert d["n_gpus"] == 2 and d["value"] > 0 and d["scaling"] == "weak"
     assert d["sla"]["lambda_star_qps"] > 0
     assert all(pr.get("p95_from") == "library (all ranks)" for pr in d["sla"]["probes_at_best"] or [])
+
+
+@pytest.mark.skipif(_ngpus() < 2, reason="needs >= 2 GPUs")
+def test_missing_peer_times_out_with_error():
+    """A sharded batch that a peer never joins: every cross-GPU wait of the chain (hint flags,
+    flag-in-data lines, CTR flags) is bounded by REC_P2P_TIMEOUT_S and rec_sync reports
+    REC_E_NCCL; the CUDA context keeps working (no trap)."""
+    import __graft_entry__
+    __graft_entry__.build()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", "29571",
+           os.path.join(ROOT, "scripts", "p2p_timeout_check.py")]
+    env = dict(os.environ, REC_P2P_TIMEOUT_S="2")
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=ROOT, env=env)
+    line = [l for l in p.stdout.splitlines() if l.startswith("{")]
+    assert p.returncode == 0 and line, p.stdout[-3000:] + p.stderr[-3000:]
+    res = json.loads(line[-1])
+    assert res["ok"] and res["lone_batch_status"] == -6, res
