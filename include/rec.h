@@ -142,7 +142,10 @@ rec_status rec_query_inspect(rec_model_t m, const float* dense, const int32_t* i
  * rank enqueues the same GLOBAL batch (all T tables' indices, all B items' dense rows) on the
  * same slot in the same order; the all-to-all of pooled vectors and the CTR all-gather run
  * inside the slot's chain over peer memory, and ctr receives all B CTRs on
- * every rank.  Row-wise or NCCL-exchange sharded models: REC_E_UNSUPPORTED (use rec_query). */
+ * every rank.  Every cross-GPU wait of the chain is bounded by REC_P2P_TIMEOUT_S (default
+ * 60 s): a peer that never joins the batch makes rec_sync(m, slot) return REC_E_NCCL (the CTRs
+ * of that batch are then undefined; the CUDA context stays usable, the model should be
+ * closed).  Row-wise or NCCL-exchange sharded models: REC_E_UNSUPPORTED (use rec_query). */
 rec_status rec_query_async(rec_model_t m, int32_t slot, const float* dense,
                            const int32_t* indices, const int32_t* offsets, int64_t nnz,
                            int32_t batch, float* ctr);
