@@ -463,7 +463,7 @@ void gemm_prepare() {
 }
 
 int g_gemm_2sm = 0;     // REC_GEMM_2SM: CTA-pair GEMM for full-GPU launches (experimental)
-int g_gemm_2sm_serve = 2;  // REC_GEMM_2SM_SERVE=n: CTA-pair GEMM (n-stage ring) for serving launches (0: off)
+int g_gemm_2sm_serve = 0;  // REC_GEMM_2SM_SERVE=n: CTA-pair GEMM (n-stage ring) for serving launches (opt-in, see DESIGN)
 int g_gemm_mt1 = 0;     // REC_GEMM_MT1=1: 128x256 tiles (one M tile per CTA) for full-GPU launches too (A/B)
 int g_gemm_narrow = 0;  // REC_GEMM_NARROW=n: 128-wide N tiles below n 128x256 tiles (measured: RMC2/3 +0.5-1 %, MT-WnD -7 %)
 int g_gemm_mt2 = 0;     // REC_GEMM_MT2=1: 256 x 256 weight-sharing tiles also for serving batches

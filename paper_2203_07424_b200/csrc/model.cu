@@ -1273,7 +1273,7 @@ rec_status rec_model_create(const rec_model_desc* d, rec_model_t* out) {
     };
     g_gemm_stages = env_int("REC_GEMM_STAGES", 0);
     g_gemm_2sm = env_int("REC_GEMM_2SM", 0);
-    g_gemm_2sm_serve = env_int("REC_GEMM_2SM_SERVE", 2);
+    g_gemm_2sm_serve = env_int("REC_GEMM_2SM_SERVE", 0);
     g_gemm_narrow = env_int("REC_GEMM_NARROW", 0);
     g_gemm_mt1 = env_int("REC_GEMM_MT1", 0);
     g_gemm_bn64 = env_int("REC_GEMM_BN64", 0);

@@ -83,9 +83,9 @@ VARIANTS = [
     ("gemm_bn64_rmc2", {"REC_GEMM_BN64": "1"}, W.small_variant(W.RMC2, 4096), 700, 0),
     ("gemm_stages2", {"REC_GEMM_STAGES": "2"}, RMC3, 700, 0),
     ("gemm_2sm_large", {"REC_GEMM_2SM": "1"}, RMC3, 20480, 0),
-    ("gemm_2sm_serving_off_rmc3", {"REC_GEMM_2SM_SERVE": "0"}, RMC3, 1024, 0),
+    ("gemm_2sm_serving_rmc3", {"REC_GEMM_2SM_SERVE": "2"}, RMC3, 1024, 0),
     ("gemm_2sm_serving_rmc3_odd", {"REC_GEMM_2SM_SERVE": "4"}, RMC3, 700, 0),
-    ("gemm_2sm_serving_off_rmc2", {"REC_GEMM_2SM_SERVE": "0"}, W.small_variant(W.RMC2, 4096), 700, 0),
+    ("gemm_2sm_serving_rmc2", {"REC_GEMM_2SM_SERVE": "2"}, W.small_variant(W.RMC2, 4096), 700, 0),
     ("gemm_mt1_large", {"REC_GEMM_MT1": "1"}, RMC3, 20480, 0),
     ("gemm_narrow_towers", {"REC_GEMM_NARROW": "148"}, MTWND, 700, 0),
     ("towers_per_task", {"REC_TOWER_GROUP": "0"}, MTWND, 700, 0),
