@@ -45,6 +45,11 @@ os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 import workloads as W  # noqa: E402
 
 BASELINE_METRIC = "SLA-bounded QPS (p95) per model at 1/2/4/8 B200; SLS HBM GB/s; MLP TC util"
+# saturation_ge_lambda_star: saturation >= LAMBDA_TOL x lambda*.  lambda* is resolved to 2 %
+# by the bisection and a finite Poisson trace passes as "stable" when it achieves >= 98 % of
+# the offered rate (csrc/serve.cpp), so a passing probe can sit up to ~4 % above the
+# steady-state capacity the saturation step measures.
+LAMBDA_TOL = 0.96
 
 
 def sls_bytes_per_item(cfg, synth: bool = False) -> int:
@@ -456,7 +461,7 @@ def per_model(name, args, rank, world, dist, local, hbm_peak):
         lam, pr = sla_search(model, cfg, world, rank, dist, ms, d, 0.5 * sat["value"], n, cfg.sla_ms)
         out["sla"] = {"sla_ms": cfg.sla_ms, "lambda_star_qps": lam, "policy": {"streams": ms, "max_batch": d},
                       "queries_per_probe": n, "probes": pr,
-                      "saturation_ge_lambda_star": bool(sat["value"] >= 0.98 * lam)}
+                      "saturation_ge_lambda_star": bool(sat["value"] >= LAMBDA_TOL * lam)}
     model.close()
     torch.cuda.synchronize()
     if args.mlp_batch > 0 and rank == 0 and name == "rmc3":
@@ -771,7 +776,7 @@ def run_ours(args):
             "per_model": models,
         }
         if sla:
-            sla["saturation_ge_lambda_star"] = bool(value >= 0.98 * sla["lambda_star_qps"])
+            sla["saturation_ge_lambda_star"] = bool(value >= LAMBDA_TOL * sla["lambda_star_qps"])
         if cfg.arch == W.ARCH_MTWND:
             # one-hot lookups move ~1 KB per item; the task towers (7.4 MFLOP per item) dominate:
             # report the tensor roofline of the tower GEMMs first, the SLS one beside it
@@ -870,7 +875,7 @@ def run_sharded(args):
                "policy": {"streams": m_streams, "max_batch": d,
                           "fusion": "deterministic global dispatcher, tau = SLA/50 (R31)"},
                "queries_per_probe": n, "probes": pr,
-               "saturation_ge_lambda_star": bool(value >= 0.98 * lam),
+               "saturation_ge_lambda_star": bool(value >= LAMBDA_TOL * lam),
                "mode": "rec_serve real clock on every rank (same trace, same batches), Poisson "
                        "arrivals, lognormal sizes; p95 of rank 0's completions"}
     per_gpu = sls_bytes_per_item(cfg, synth=True) * items / (ms_max * 1e-3) / 1e9 / world
