@@ -64,15 +64,19 @@ rec_status dist_init(rec_model_s* m, const void* nccl_id) {
 // The k-th batch submitted on slot s is the same global batch on every rank (a deterministic
 // global dispatch: every rank submits the same batch sequence round-robin over the slots) and
 // carries epoch k + 1 on that slot.  Its chain on rank r:
-//   SLS of the local tables for all B items, each pooled vector stored into X_s of the rank
-//     owning the item (blocks of Bq = ceil(B / G)) over NVLink; the last CTA raises
-//     flags_s[r] = epoch on every rank (st.release.sys)                  -- fused all-to-all C1
+//   SLS of the local tables for all B items; the pooled vector of a remote item (blocks of
+//     Bq = ceil(B / G)) goes over NVLink as two flag-in-data LL lines {v, epoch, v, epoch}
+//     into LL_s of its owner, an own item's straight into the local X_s; the last CTA raises
+//     flags_s[r] = epoch on every rank (st.release.sys, a hint)          -- fused all-to-all C1
+//     (caller-index chains, REC_P2P_LL=0: every vector into the owner's X_s behind a per-CTA
+//     system-scope fence, and the flag is the guarantee)
 //   || dense features + bottom MLP of the own block (branch stream)
-//   wait flags_s[0..G) >= epoch -> interaction + top MLP of the own block
+//   wait flags_s[0..G) >= epoch -> LL unpack (each line's epoch checked) into X_s ->
+//   interaction + top MLP of the own block
 //   CTRs of the own block stored into CTR_s of every rank, CTR flags raised  -- all-gather C3
 //   wait CTR flags_s[0..G) >= epoch
-// Reuse of X_s by batch k + m is safe: rank r issues it only after its CTR-flag wait of batch
-// k, and every rank raised its CTR flag of k after its interaction had read X_s.  Slots are
+// Reuse of X_s / LL_s by batch k + m is safe: rank r issues it only after its CTR-flag wait of
+// batch k, and every rank raised its CTR flag of k after its interaction had read X_s.  Slots are
 // independent, so m batches are in flight per rank with no host synchronisation.
 static size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
 
@@ -154,8 +158,9 @@ rec_status p2p_slots_init(rec_model_s* m) {
     a.err_flag = w.flag;
     a.timeout_ns = p2p_timeout_ns();
     {
-      // fence.sc.sys per CTA (default) or one acq_rel.sys atomic (REC_P2P_FENCE=0): measured
-      // equal (44.8k vs 44.7k QPS, RMC2 on 2 GPUs), so the plainly correct fence stays
+      // fenced protocol (caller-index chains, or REC_P2P_LL=0): fence.sc.sys per CTA (default)
+      // or one acq_rel.sys atomic (REC_P2P_FENCE=0): measured equal (44.8k vs 44.7k QPS, RMC2
+      // on 2 GPUs), so the plainly correct fence stays
       const char* f = getenv("REC_P2P_FENCE");
       a.sc_fence = f ? atoi(f) : 1;
     }
